@@ -1,0 +1,152 @@
+/*
+ * sbmds.h — C ABI of the B200-native sBMDS hot path (libsbmds.so).
+ *
+ * Sparse biharmonic MDS (Turek & Huth, arXiv 1705.10887): classical scaling on the
+ * factored squared-distance approximation  Ê = P W P^T  (Eq. 7),
+ * where P = S is the n x l sparse interpolation operator (Eq. 6,
+ * sparsified per PAPER.md:175-191) and W = D_ll the l x l landmark block
+ * (PAPER.md:149), already squared for MDS (reading R2).
+ *
+ *   operator   B~ = -1/2 J S D_ll S^T J,   J = I - (1/n) 1 1^T
+ *   eigs       top-m algebraic eigenpairs of B~ and Z = V_m Λ_m^{1/2},
+ *              "using only matrix-vector multiplications" — here a
+ *              block subspace iteration with Cholesky-QR and Rayleigh-Ritz
+ *              (BASELINE.json north_star) instead of the paper's Lanczos.
+ *
+ * Conventions for every entry point
+ *   - Pointer arguments may be HOST or DEVICE memory (detected per call with
+ *     cudaPointerGetAttributes). Host inputs are staged through library-owned device
+ *     buffers and the call synchronises `cuda_stream` before returning; with all
+ *     pointers on the device the call is asynchronous on `cuda_stream` (eigs reads a
+ *     small convergence flag back every rr_period iterations).
+ *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Dense blocks (X, Y, V, Z) are row-major n x b fp32: the b values of vertex i
+ *     are contiguous at offset i*b.
+ *   - Errors never abort: a non-OK status is returned and sbmds_last_error() gives a
+ *     thread-local message. Invalid arguments leave the handle unchanged.
+ *   - One handle serialises its own calls (shared workspace); distinct handles are
+ *     independent and may be used from different threads.
+ */
+#ifndef SBMDS_H
+#define SBMDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sbmds_ctx* sbmds_t; /* opaque handle */
+
+typedef enum {
+    SBMDS_OK = 0,
+    SBMDS_EINVAL = 1,     /* bad argument (sizes, ranges, NULL, overlap, asymmetric D) */
+    SBMDS_ENOMEM = 2,     /* device allocation failed */
+    SBMDS_ECUDA = 3,      /* CUDA runtime/driver error (message in sbmds_last_error) */
+    SBMDS_ENOCONV = 4,    /* eigs hit max_iters with tol > 0; outputs and info still filled */
+    SBMDS_EBREAKDOWN = 5  /* Cholesky-QR broke down even after the shifted retry */
+} sbmds_status;
+
+enum {
+    /* Keep a reference to the caller's DEVICE D_ll instead of copying it (the caller
+       keeps it alive and unchanged until sbmds_destroy). Ignored for host D, or when
+       l % 4 != 0 (TMA needs 16-byte row pitch; the library then copies). */
+    SBMDS_BORROW_D = 1u << 0,
+    /* Full input checks at create: row_ptr monotone with row_ptr[0] = 0 and
+       row_ptr[n] = nnz, 0 <= col_idx < l, all values finite, D symmetric
+       (|D_ij - D_ji| <= 1e-6 max|D|). Without it only sizes are checked. */
+    SBMDS_VALIDATE = 1u << 1
+};
+
+typedef struct {
+    int32_t iters;        /* subspace iterations run */
+    int32_t n_applies;    /* operator applies (= iters) */
+    int32_t n_negative;   /* negative eigenvalues among the top m (their Z column is 0) */
+    int32_t converged;    /* 1 if max_i<m r_i <= tol*|θ|max (always 0 when tol <= 0) */
+    double max_residual;  /* max_i<m ||B~v_i - θ_i v_i|| / max_j |θ_j| at the last RR */
+    double orth_error;    /* max |V^T V - I| of the returned V (fp64 Gram)           */
+    double gpu_ms;        /* device time of the whole call (CUDA events)             */
+} sbmds_info;
+
+/*
+ * sbmds_create — build a handle from S (CSR) and D_ll.
+ *   n, l, nnz   : S is n x l with nnz stored entries; 1 <= l <= n, 0 <= nnz < 2^31.
+ *   row_ptr     : int64[n+1], row_ptr[0] = 0, row_ptr[n] = nnz, nondecreasing.
+ *   col_idx     : int32[nnz], 0 <= col < l; any order within a row; duplicates summed.
+ *   val         : float[nnz]. No sign or row-sum assumption (the paper's thresholded
+ *                 P_sparse has neither).
+ *   D_ll        : float[l*l], row-major, symmetric ("d_M is symmetric";
+ *                 W_ij = d(b_i, b_j)), squared distances (R2).
+ *                 The kernels read D as D^T, which equals D for symmetric input.
+ *   flags       : SBMDS_BORROW_D | SBMDS_VALIDATE.
+ * The library copies S (and D unless borrowed) into device memory it owns, builds a
+ * row-sorted CSC copy of S on the device (for S^T X without atomics) and the vector
+ * w = S^T 1 / n used by the rank-one centring (J S = S - 1 w^T).
+ * Returns SBMDS_OK and *out, or an error with *out = NULL.
+ */
+sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const int64_t* row_ptr,
+                          const int32_t* col_idx, const float* val, const float* D_ll,
+                          uint32_t flags, void* cuda_stream, sbmds_t* out);
+
+/*
+ * sbmds_apply — Y = -1/2 J S D_ll S^T J X.
+ *   b    : block width, 1 <= b <= 64.
+ *   X, Y : n x b row-major fp32, host or device; must not overlap. X is not modified.
+ * Computed as s = 1^T X, Y1 = S^T X - w s^T, Y2 = D Y1, t = w^T Y2,
+ * Y = -1/2 (S Y2 - 1 t^T): no n-length centred copy is formed.
+ */
+sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float* Y, void* cuda_stream);
+
+/*
+ * sbmds_eigs — top-m algebraic eigenpairs of B~ and the embedding Z = V_m Λ_m^{1/2}
+ * ("truncating its decomposition to the biggest m eigenvalues").
+ *   m          : 1 <= m <= block.
+ *   block      : subspace width b, m <= b <= 64, b < n. Subspace iteration converges to
+ *                the largest |λ|, so b must also cover the negative eigenvalues with
+ *                |λ| > λ_m (reading R1).
+ *   max_iters  : >= 1 subspace iterations (one apply each).
+ *   tol        : > 0: stop when max_i<m ||B~v_i - θ_i v_i|| <= tol * max_j |θ_j|
+ *                (SPEC.md:52 form), checked every rr_period (default 5) iterations;
+ *                <= 0: run exactly max_iters iterations (status OK).
+ *   seed       : initial block X0 ~ N(0,1) from a counter-based Philox generator.
+ *   X0         : optional n x block warm start (host or device), or NULL.
+ *   eigvals    : HOST double[m], descending.
+ *   V, Z       : n x m fp32 (host or device), or NULL to skip. V orthonormal columns;
+ *                each column's largest-|v_i| entry is positive (ties: lowest i);
+ *                Z column j = sqrt(max(θ_j, 0)) V_j (negative θ_j -> zero column).
+ *   info       : HOST sbmds_info*, or NULL.
+ * Returns SBMDS_OK, SBMDS_ENOCONV (results filled), SBMDS_EBREAKDOWN, or an error.
+ */
+sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol,
+                        uint64_t seed, const float* X0, double* eigvals, float* V, float* Z,
+                        sbmds_info* info, void* cuda_stream);
+
+/* Frees everything the library allocated (not borrowed D). NULL-safe. */
+void sbmds_destroy(sbmds_t h);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char* sbmds_last_error(void);
+
+/*
+ * Tuning / introspection (tests and bench):
+ *   sbmds_set_option keys: "rr_period" (>=1), "use_graph" (0/1), "dstream"
+ *   (0 = auto, 1 = FFMA stream), "order_columns" (0/1: spatial CSC column order).
+ *   sbmds_get_stat keys: "n", "l", "nnz", "rowsum_dev_e9" (max |row sum - 1| * 1e9),
+ *   "d_borrowed", "csc_bytes", "workspace_bytes".
+ * Both return SBMDS_EINVAL for an unknown key.
+ */
+sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t value);
+sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* value);
+
+/* Number of kernels this library has launched in this process (graph replays count
+   each captured kernel). Monotone; for bench.py's gpu_launches. */
+int64_t sbmds_launch_count(void);
+
+/* ABI version: 1. */
+int32_t sbmds_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SBMDS_H */

@@ -1,0 +1,261 @@
+"""Pins for the fp64 oracle against what the paper and the mathematics fix (not against itself).
+
+Each test names the closed form / worked example it checks.
+A plausible slip in the oracle — a dropped -1/2, a missing centring, S vs S^T,
+a transposed D, ascending instead of descending order, a missing sqrt in Z —
+fails at least one of them (see test_mutations_are_caught).
+"""
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import sbmds_oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def sqdist(P):
+    P = np.asarray(P, dtype=np.float64)
+    return ((P[:, None, :] - P[None, :, :]) ** 2).sum(-1)
+
+
+def eye_csr(n):
+    return sp.identity(n, format="csr", dtype=np.float64)
+
+
+def load_golden(name):
+    """Golden fixtures: '# cite' lines, then 'key: v1 v2 ...' lines."""
+    out = {}
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            k, v = line.split(":", 1)
+            out[k.strip()] = np.array([float(x) for x in v.split()])
+    return out
+
+
+# --------------------------------------------------------------------------- SPEC worked examples
+def test_three_collinear_points():
+    """points 0,1,2, m=1 -> Z = (-1,0,1) up to sign, λ = 2."""
+    g = load_golden("mds_collinear3.txt")
+    E = sqdist(g["points"][:, None])
+    lam, V, Z = O.eigs_dense(eye_csr(3), E, 1)
+    assert np.allclose(lam, g["lambda"], atol=1e-12)
+    z = Z[:, 0] * np.sign(Z[2, 0])
+    assert np.allclose(z, g["Z"], atol=1e-12)
+
+
+def test_four_collinear_points_lambda5():
+    """-1/2 J E J of 4 collinear unit-spaced points: λ1 = 5 (= Σ centred x²)."""
+    g = load_golden("mds_collinear4.txt")
+    E = sqdist(g["points"][:, None])
+    lam, _, _ = O.eigs_dense(eye_csr(4), E, 2)
+    assert np.allclose(lam, g["lambda"], atol=1e-12)
+
+
+def test_unit_square():
+    """unit-square corners, m=2: λ = (1,1) and distances reproduced."""
+    g = load_golden("mds_unit_square.txt")
+    P = g["points"].reshape(4, 2)
+    E = sqdist(P)
+    lam, _, Z = O.eigs_dense(eye_csr(4), E, 2)
+    assert np.allclose(lam, g["lambda"], atol=1e-12)
+    assert np.allclose(sqdist(Z), E, atol=1e-10)
+
+
+def test_zero_distances():
+    """E = 0 -> Z = 0."""
+    lam, _, Z = O.eigs_dense(eye_csr(5), np.zeros((5, 5)), 2)
+    assert np.allclose(lam, 0) and np.allclose(Z, 0)
+
+
+def test_diag_spectrum_selection():
+    """operator diag(5,4,3,2,1), k=2 -> (5,4): top-m algebraic selection."""
+    lam, V, _ = O.mds_dense(np.diag([5.0, 4, 3, 2, 1]), 2)
+    assert np.allclose(lam, [5, 4])
+    lam, V, _ = O.mds_dense(np.diag([1.0, -9, 3, 2, 0.5]), 2)   # algebraic, not |λ|
+    assert np.allclose(lam, [3, 2])
+
+
+# --------------------------------------------------------------------------- closed forms
+def test_cf1_planar_points_recovered():
+    """CF1 (north_star): S = I, D = squared Euclidean distances of planar points Y.
+    B~ = (JY)(JY)^T: λ = eig((JY)^T JY), Z = JY up to a rigid motion."""
+    rng = np.random.default_rng(1)
+    Y = rng.standard_normal((60, 2)) * [3.0, 1.0]
+    lam, V, Z = O.eigs_dense(eye_csr(60), sqdist(Y), 2)
+    JY = Y - Y.mean(0)
+    ref = np.sort(np.linalg.eigvalsh(JY.T @ JY))[::-1]
+    assert np.allclose(lam, ref, rtol=1e-12)
+    # orthogonal Procrustes: min_Q ||Z Q - JY|| = 0
+    U, _, Wt = np.linalg.svd(Z.T @ JY)
+    assert np.linalg.norm(Z @ (U @ Wt) - JY) < 1e-9 * np.linalg.norm(JY)
+
+
+def random_pou(n, l, k, rng, landmark_rows=True):
+    """Random S with k nnz per row, rows summing to 1 (partition of unity)."""
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        if landmark_rows and i < l:
+            rows.append(i); cols.append(i); vals.append(1.0)
+            continue
+        c = rng.choice(l, size=k, replace=False)
+        w = rng.uniform(0.1, 1.0, size=k)
+        rows += [i] * k; cols += list(c); vals += list(w / w.sum())
+    return sp.csr_matrix((vals, (rows, cols)), shape=(n, l))
+
+
+def cf2_problem(n=300, l=40, k=5, seed=2):
+    rng = np.random.default_rng(seed)
+    S = random_pou(n, l, k, rng)
+    Yl = rng.standard_normal((l, 3)) * [3.0, 2.0, 1.0]
+    D = sqdist(Yl)
+    JSY = S @ Yl
+    JSY = JSY - JSY.mean(0)
+    return S, D, JSY
+
+
+def test_cf2_apply_is_rank3_gram():
+    """CF2: rows of S sum to 1 and D_ab = |y_a - y_b|^2 => B~ = (JSY)(JSY)^T exactly."""
+    S, D, JSY = cf2_problem()
+    X = np.random.default_rng(3).standard_normal((S.shape[0], 4))
+    Y = O.apply(S, D, X)
+    ref = JSY @ (JSY.T @ X)
+    assert np.linalg.norm(Y - ref) < 1e-11 * np.linalg.norm(ref)
+    B = O.dense_operator(S, D)
+    assert np.linalg.norm(B - JSY @ JSY.T) < 1e-11 * np.linalg.norm(B)
+
+
+def test_cf2_eigs_dense_matfree_bmds():
+    """CF2 eigenpairs = SVD of JSY (λ_i = σ_i², V = left singular vectors), for all three oracle paths."""
+    S, D, JSY = cf2_problem()
+    U, s, _ = np.linalg.svd(JSY, full_matrices=False)
+    for lam, V, Z in (O.eigs_dense(S, D, 3), O.eigs_matfree(S, D, 3)[:3], O.bmds(S, D, 3)):
+        assert np.allclose(lam, s ** 2, rtol=1e-9)
+        assert O.principal_angle(V, U) < 1e-7
+        assert np.allclose(Z @ Z.T, JSY @ JSY.T, atol=1e-8 * s[0] ** 2)
+
+
+def test_cf3_circle_negative_and_degenerate_spectrum():
+    """CF3: N points on a circle of radius ρ, S = I, D = squared arc length (circulant).
+    For k != 0 the Fourier modes are eigenvectors and J leaves them alone:
+    λ_k = -1/2 Σ_j D_0j cos(2πkj/N); the k=0 mode is annihilated (λ = 0)."""
+    N, rho = 24, 1.7
+    th = 2 * np.pi * np.arange(N) / N
+    diff = np.angle(np.exp(1j * (th[:, None] - th[None, :])))
+    D = (rho * diff) ** 2
+    B = O.dense_operator(eye_csr(N), D)
+    got = np.sort(np.linalg.eigvalsh(B))
+    j = np.arange(N)
+    lam = [-0.5 * np.sum(D[0] * np.cos(2 * np.pi * k * j / N)) for k in range(1, N)]
+    want = np.sort(np.concatenate([[0.0], lam]))
+    assert np.allclose(got, want, atol=1e-10 * np.abs(want).max())
+    assert (want < -1e-6).sum() > 0                   # genuinely indefinite
+    top, _, _ = O.eigs_dense(eye_csr(N), D, 2)         # cos/sin pair: exactly degenerate
+    assert abs(top[0] - top[1]) < 1e-10 * abs(top[0])
+
+
+def test_cf4_selector_s():
+    """CF4: every row of S is a unit vector and each landmark repeats c times (n = c l):
+    J_n S = S J_l, so the nonzero eigenvalues of B~ are c · eig(-1/2 J_l D J_l)."""
+    rng = np.random.default_rng(4)
+    l, c = 12, 5
+    n = l * c
+    cols = rng.permutation(np.repeat(np.arange(l), c))
+    S = sp.csr_matrix((np.ones(n), (np.arange(n), cols)), shape=(n, l))
+    A = rng.uniform(0, 10, size=(l, l))
+    D = A + A.T
+    np.fill_diagonal(D, 0)
+    Jl = np.eye(l) - 1.0 / l
+    small = np.linalg.eigvalsh(-0.5 * Jl @ D @ Jl)
+    big = np.linalg.eigvalsh(O.dense_operator(S, D))
+    want = np.sort(c * small)
+    got = np.sort(big)
+    # the n - l extra eigenvalues are exactly zero; compare after dropping n-l zeros
+    got_nz = np.delete(got, np.argsort(np.abs(got))[: n - l])
+    assert np.allclose(np.sort(got_nz), want, atol=1e-9 * np.abs(want).max())
+
+
+# --------------------------------------------------------------------------- brute force / invariants
+def test_brute_force_quadruple_sum():
+    """Tiny input: B~_ij = -1/2 Σ_pq J_ip (Σ_ab S_pa D_ab S_qb) J_qj written as loops."""
+    rng = np.random.default_rng(5)
+    n, l = 6, 3
+    S = rng.uniform(-0.5, 1.0, size=(n, l))            # general S: negative values, no row-sum constraint
+    A = rng.uniform(0, 4, size=(l, l))
+    D = A + A.T
+    E = [[sum(S[p, a] * D[a, b] * S[q, b] for a in range(l) for b in range(l))
+          for q in range(n)] for p in range(n)]
+    J = [[(1.0 if i == j else 0.0) - 1.0 / n for j in range(n)] for i in range(n)]
+    B = [[-0.5 * sum(J[i][p] * E[p][q] * J[q][j] for p in range(n) for q in range(n))
+          for j in range(n)] for i in range(n)]
+    B = np.array(B)
+    Ssp = sp.csr_matrix(S)
+    assert np.allclose(O.dense_operator(Ssp, D), B, atol=1e-12)
+    X = rng.standard_normal((n, 2))
+    assert np.allclose(O.apply(Ssp, D, X), B @ X, atol=1e-12)
+
+
+def test_invariants_on_config1():
+    """B~ symmetric, B~ 1 = 0, J 1 = 0, columns of B~X sum to 0; rows of S sum to 1, landmark rows e_j."""
+    from gen import configs
+    p = configs.config(1)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val)
+    B = O.dense_operator(S, p.D)
+    assert np.abs(B - B.T).max() < 1e-12 * np.abs(B).max()
+    assert np.abs(B @ np.ones(p.n)).max() < 1e-10 * np.abs(B).max()
+    assert np.abs(O.centering(7) @ np.ones(7)).max() < 1e-15
+    X = np.random.default_rng(0).standard_normal((p.n, 3))
+    Y = O.apply(S, p.D, X)
+    assert np.abs(Y.sum(0)).max() < 1e-10 * np.abs(Y).max() * p.n
+    assert np.allclose(np.asarray(S.sum(1)).ravel(), 1.0, atol=1e-14)
+    lm_rows = S[p.landmarks].toarray()
+    assert np.array_equal(lm_rows, np.eye(p.l))
+
+
+def test_dense_matfree_bmds_agree_on_config1():
+    """Config 1: full eigh, Lanczos on matvecs, and the QR route all give the same top-3 pairs."""
+    from gen import configs
+    p = configs.config(1)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val)
+    lam_d, V_d, _ = O.eigs_dense(S, p.D, p.m)
+    lam_m, V_m, _, _ = O.eigs_matfree(S, p.D, p.m)
+    lam_b, V_b, _ = O.bmds(S, p.D, p.m)
+    assert np.allclose(lam_m, lam_d, rtol=1e-10)
+    assert np.allclose(lam_b, lam_d, rtol=1e-10)
+    assert O.principal_angle(V_m, V_d) < 1e-7 and O.principal_angle(V_b, V_d) < 1e-7
+    # the dense spectrum has the structure SURVEY.md [Pr1] reports: clean cut at m=3
+    lam_all = np.sort(np.linalg.eigvalsh(O.dense_operator(S, p.D)))[::-1]
+    assert O.relgap(lam_all, 3) > 1e-2
+
+
+def test_embedding_and_angle_helpers():
+    V = np.eye(4)[:, :3]
+    Z = O.embedding(V, np.array([4.0, -1.0, 9.0]))
+    assert np.allclose(Z[:, 0], 2 * V[:, 0]) and np.allclose(Z[:, 1], 0) and np.allclose(Z[:, 2], 3 * V[:, 2])
+    t = 0.3
+    a = np.array([[1.0], [0.0], [0.0]])
+    b = np.array([[np.cos(t)], [np.sin(t)], [0.0]])
+    assert abs(O.principal_angle(a, b) - t) < 1e-12
+
+
+def test_mutations_are_caught():
+    """Each plausible oracle slip breaks CF2 (so the pins above would fail)."""
+    S, D, JSY = cf2_problem(n=80, l=12, k=3)
+    X = np.random.default_rng(9).standard_normal((80, 2))
+    ref = JSY @ (JSY.T @ X)
+    good = O.apply(S, D, X)
+    S64 = sp.csr_matrix(S)
+    muts = {
+        "no_half": -1.0 * (lambda T: T - T.mean(0))(S64 @ (D @ (S64.T @ (X - X.mean(0))))),
+        "no_left_J": -0.5 * (S64 @ (D @ (S64.T @ (X - X.mean(0))))),
+        "no_right_J": (lambda T: -0.5 * (T - T.mean(0)))(S64 @ (D @ (S64.T @ X))),
+        "sign": 0.5 * (lambda T: T - T.mean(0))(S64 @ (D @ (S64.T @ (X - X.mean(0))))),
+    }
+    assert np.linalg.norm(good - ref) < 1e-10 * np.linalg.norm(ref)
+    for name, Ym in muts.items():
+        assert np.linalg.norm(Ym - ref) > 1e-3 * np.linalg.norm(ref), name
