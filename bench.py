@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""bench.py — sBMDS hot path on B200 (BASELINE.json metric at config 4).
+
+Default workload: BASELINE.json configs[3] (torus 1200x1500, n = 1,800,000, l = 50,000,
+k = 32, fp32 D_ll 10 GB, m = 3, block 16, exactly 50 subspace iterations). A step is one
+full sbmds_eigs solve (50 applies of -1/2 J S D S^T J + Cholesky-QR + Rayleigh-Ritz +
+embedding) on inputs already resident in HBM; value = operator applies per second over
+all ranks. Inputs (10 GB D) are far larger than the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (N independent replicas, weak scaling)
+
+Rank 0 prints ONE JSON line. --impl reference times the fp64 CPU oracle (the only
+baseline that exists: the paper ships no code) on the same workload and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sBMDS operator applies/s & HBM GB/s vs peak; top-p MDS time at n=1.8M,l=50k"
+UNIT = "applies/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--iters", type=int, default=50, help="subspace iterations per eigs step")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ distributed
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_problem(cfg: int, ws: int, rank: int):
+    """Rank 0 generates (and caches) first; the other ranks then load the cache."""
+    from gen import configs
+    if rank == 0:
+        p = configs.config(cfg)
+        barrier(ws)
+    else:
+        barrier(ws)
+        p = configs.config(cfg)
+    return p
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled every 100 ms while active."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+               0x10: "sync_boost"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                fn = getattr(self.nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    self.nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                self.reasons |= int(fn(self.h))
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(v for k, v in self.REASONS.items() if self.reasons & k),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ our arm
+def algorithmic_bytes(p, b):
+    """Bytes one apply must move: full fp32 D once, S via
+    CSR and CSC (8 B per nnz each), row/col pointers, X read + Y written."""
+    return 4 * p.l * p.l + 16 * p.nnz + 4 * (p.n + 1) + 4 * (p.l + 1) + 8 * p.n * b
+
+
+def dstream_bytes(p, b):
+    """Dominant kernel (k_dstream_ffma): D read once + Y1 read + Y2 partials written."""
+    return 4 * p.l * p.l + 4 * p.l * b + 8 * p.l * b
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_1705_10887_b200 import from_problem, launch_count
+    torch.cuda.set_device(local)
+    p = load_problem(args.config, ws, rank)
+    m, b, iters = p.m, p.block, args.iters
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    h = from_problem(p, device="cuda")
+    st = torch.cuda.current_stream()
+    V = torch.empty((p.n, m), device="cuda")
+    Z = torch.empty((p.n, m), device="cuda")
+
+    def step():
+        return h.eigs(m, b, max_iters=iters, tol=0.0, seed=0, V=V, Z=Z)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    h.set_option("profile", 1 << 2)          # CUDA events around k_dstream_ffma only
+    h.set_option("profile_reset", 1)
+    n0 = launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0.record(st)
+        infos = [step()[3] for _ in range(args.steps)]
+        e1.record(st)
+        torch.cuda.synchronize()
+    n_launch = launch_count() - n0
+    ms = e0.elapsed_time(e1)
+    ds_ns, ds_n = h.stat("dstream_ns"), h.stat("dstream_launches")
+    h.set_option("profile", 0)
+    ms_max = max_over_ranks(ms, ws, device="cuda")
+    applies = sum(i["n_applies"] for i in infos)
+    value = ws * applies / (ms_max / 1e3)
+    ds_avg_s = ds_ns / max(ds_n, 1) / 1e9
+    ds_gbs = dstream_bytes(p, b) / ds_avg_s / 1e9
+    apply_gbs = algorithmic_bytes(p, b) * applies / (ms / 1e3) / 1e9
+    eigs_s = ms / 1e3 / args.steps
+
+    # parity spot check at full size: eigenvalues of the timed solves are deterministic
+    lam, _, _, info = step()
+
+    # ---- end to end through the C ABI from pinned HOST buffers (create + eigs + D2H)
+    e2e = None
+    if not args.no_e2e:
+        from paper_1705_10887_b200 import Sbmds
+        rp = torch.from_numpy(np.ascontiguousarray(p.row_ptr, dtype=np.int64)).pin_memory()
+        ci = torch.from_numpy(np.ascontiguousarray(p.col_idx)).pin_memory()
+        vv = torch.from_numpy(p.val32()).pin_memory()
+        Dh = torch.from_numpy(p.D).pin_memory()
+        Vh = torch.empty((p.n, m)).pin_memory()
+        Zh = torch.empty((p.n, m)).pin_memory()
+        del h
+        torch.cuda.empty_cache()
+        times = []
+        for s in range(args.e2e_steps + 1):
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(st)
+            with Sbmds(p.n, p.l, rp, ci, vv, Dh) as hh:
+                hh.eigs(m, b, max_iters=iters, tol=0.0, seed=0, V=Vh, Z=Zh)
+            z.record(st)
+            torch.cuda.synchronize()
+            if s > 0:                       # first one warms allocator / tensor maps
+                times.append(a.elapsed_time(z) / 1e3)
+        t_e2e = max_over_ranks(float(np.mean(times)), ws, device="cuda")
+        h2d = p.D.nbytes + 8 * (p.n + 1) + 12 * p.nnz
+        d2h = 8 * m + 2 * p.n * m * 4
+        e2e = {"value": ws * iters / t_e2e, "unit": UNIT, "seconds_per_solve": t_e2e,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "includes": "sbmds_create from pinned host CSR + D (H2D, CSC build) + sbmds_eigs "
+                           "(50 iters) + V, Z, eigenvalues to host + destroy"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(p)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded torus mesh stand-in for Dragon1800k; DESIGN.md §3)",
+        "config": {"workload": f"config {args.config}: {p.name}", "n": p.n, "l": p.l, "k": 32,
+                   "nnz": p.nnz, "block": b, "m": m, "iters_per_step": iters,
+                   "parallelism": f"replicas x{ws}", "l2": "inputs (10 GB D) >> 126 MB L2, no flush"},
+        "top_p_mds_seconds": eigs_s,
+        "apply_algorithmic_gbs": apply_gbs,
+        "eigenvalues": [float(x) for x in lam],
+        "max_residual": info["max_residual"], "orth_error": info["orth_error"],
+        "roofline": {"bound": "hbm", "achieved": ds_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": ds_gbs / hbm_peak, "traffic": load_traffic(),
+                     "kernel": "k_dstream_ffma", "launches": ds_n,
+                     "avg_launch_ms": ds_avg_s * 1e3, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": dstream_bytes(p, b)},
+        "gpu_launches": int(n_launch),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if cpu:
+        out["cpu_baseline"] = cpu
+    return out
+
+
+def load_traffic():
+    """DRAM bytes per k_dstream_ffma launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "dstream_traffic.json")
+    try:
+        return json.load(open(path))["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------ oracle arms
+def cpu_baseline(p, reps: int = 1):
+    """The fp64 oracle (oracle/sbmds_oracle.apply, as it stands) on this host's cores."""
+    from gen import configs
+    from oracle import sbmds_oracle as O
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    X = configs.x_block(p.n, p.block, seed=1)
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.apply(S, p.D, X)
+        t.append(time.perf_counter() - t0)
+    sec = float(np.median(t))
+    return {"value": 1.0 / sec, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"{reps} fp64 oracle apply (b={p.block}) of the full config-{4 if p.n == 1800000 else '?'} "
+                      f"operator, median wall {sec:.2f} s"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return None
+    from gen import configs
+    from oracle import sbmds_oracle as O
+    p = configs.config(args.config)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    X = configs.x_block(p.n, p.block, seed=1)
+    steps, warm = max(1, min(args.steps, 5)), min(args.warmup, 1)
+    for _ in range(warm):
+        O.apply(S, p.D, X)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.apply(S, p.D, X)
+    sec = (time.perf_counter() - t0) / steps
+    v = 1.0 / sec
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"fp64 oracle apply (b={p.block}) of config {args.config}, {steps} timed + {warm} warm-up "
+              f"(capped at 5 + 1 to bound the run)")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+            "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config {args.config}: {p.name}", "n": p.n, "l": p.l, "block": p.block},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        out = run_reference(args, ws, rank)
+    else:
+        out = run_ours(args, ws, rank, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

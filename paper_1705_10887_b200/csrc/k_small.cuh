@@ -1,0 +1,409 @@
+// Block subspace iteration kernels (BASELINE.json north_star:
+// "block subspace iteration with Cholesky-QR and Rayleigh-Ritz ... a tall-skinny Gram
+// X^T X kernel for Cholesky-QR; a single-block Jacobi kernel for the p x p Ritz problem,
+// so nothing falls back to the CPU").
+//
+//   k_gram        G = Y^T Y (and H = X^T Y), fp64 accumulation, deterministic        E2/E5
+//   k_chol        G = R^T R (shifted retry on breakdown), Rinv = R^-1, single CTA      E3
+//   k_rr          cyclic parallel Jacobi of H, Ritz values/vectors, residuals, conv.  E5
+//   k_rotate      out = in * M  (n x b times b x mo, fp64 arithmetic)                  E4/E6
+//   k_init_philox X0 ~ N(0,1), counter-based Philox4x32-10 + Box-Muller               E1
+//   k_col_argmax, k_finalize   sign canonicalisation and Z = V diag(sqrt(max θ, 0))  E6
+#pragma once
+#include "common.cuh"
+
+namespace sbmds {
+
+// ------------------------------------------------------------------ E2: tall-skinny Gram
+// Rows are cut into gridDim.x contiguous ranges; each block stages 32-row tiles of Y (and
+// X) in shared memory and accumulates its share of the b*b products in fp64 (the fp32
+// products are exact in fp64). Partials are summed in block order by the last block.
+template <bool WITH_H>
+__global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __restrict__ Y,
+                                              const float* __restrict__ X, double* __restrict__ part,
+                                              double* __restrict__ G, double* __restrict__ H,
+                                              unsigned int* __restrict__ counter) {
+    constexpr int TR = 32;
+    constexpr int PPT = (kMaxB * kMaxB) / 256;  // max pairs per thread (16)
+    __shared__ float Ys[TR * kMaxB];
+    __shared__ float Xs[WITH_H ? TR * kMaxB : 1];
+    const int tid = threadIdx.x;
+    const int bb = b * b;
+    double g[PPT], h[PPT];
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) g[u] = h[u] = 0.0;
+    const int64_t rows_per_blk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t beg = blockIdx.x * rows_per_blk, end = min(n, beg + rows_per_blk);
+    for (int64_t r0 = beg; r0 < end; r0 += TR) {
+        const int rows = (int)((end - r0) < TR ? (end - r0) : TR);
+        __syncthreads();
+        for (int e = tid; e < rows * b; e += 256) {
+            Ys[e] = Y[r0 * b + e];
+            if constexpr (WITH_H) Xs[e] = X[r0 * b + e];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int pq = tid + u * 256;
+            if (pq < bb) {
+                const int p = pq / b, q = pq % b;
+                double a = g[u], ah = h[u];
+                for (int r = 0; r < rows; ++r) {
+                    const double yq = (double)Ys[r * b + q];
+                    a = fma((double)Ys[r * b + p], yq, a);
+                    if constexpr (WITH_H) ah = fma((double)Xs[r * b + p], yq, ah);
+                }
+                g[u] = a;
+                h[u] = ah;
+            }
+        }
+    }
+    double* pg = part + (int64_t)blockIdx.x * (2 * kMaxB * kMaxB);
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+        const int pq = tid + u * 256;
+        if (pq < bb) {
+            pg[pq] = g[u];
+            if constexpr (WITH_H) pg[kMaxB * kMaxB + pq] = h[u];
+        }
+    }
+    if (last_block_done(counter)) {
+        for (int pq = tid; pq < bb; pq += 256) {
+            double a = 0.0, ah = 0.0;
+            for (unsigned int q = 0; q < gridDim.x; ++q) {
+                const double* pp = part + (int64_t)q * (2 * kMaxB * kMaxB);
+                a += pp[pq];
+                if constexpr (WITH_H) ah += pp[kMaxB * kMaxB + pq];
+            }
+            G[pq] = a;
+            if constexpr (WITH_H) H[pq] = ah;
+        }
+        if (tid == 0) *counter = 0;
+    }
+}
+
+// ------------------------------------------------------------------ E3: Cholesky + R^-1
+// status: 0 ok, 1 ok after the shifted retry, 2 breakdown. G, Rinv are b x b row-major.
+__global__ void __launch_bounds__(256) k_chol(int b, const double* __restrict__ G, double* __restrict__ Rinv,
+                                              int* __restrict__ status) {
+    __shared__ double A[kMaxB][kMaxB + 1];
+    __shared__ int fail;
+    __shared__ double shift;
+    const int tid = threadIdx.x;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        for (int e = tid; e < b * b; e += blockDim.x) {
+            const int i = e / b, j = e % b;
+            A[i][j] = 0.5 * (G[i * b + j] + G[j * b + i]);
+        }
+        if (tid == 0) {
+            fail = 0;
+            double tr = 0.0;
+            for (int i = 0; i < b; ++i) tr += fabs(G[i * b + i]);
+            shift = attempt == 0 ? 0.0 : 1e-13 * tr + 1e-300;
+        }
+        __syncthreads();
+        if (attempt == 1 && tid < b) A[tid][tid] += shift;
+        __syncthreads();
+        for (int k = 0; k < b; ++k) {
+            if (tid == 0) {
+                const double d = A[k][k];
+                if (!(d > 0.0) || !isfinite(d)) fail = 1;
+                else A[k][k] = sqrt(d);
+            }
+            __syncthreads();
+            if (fail) break;
+            if (tid > k && tid < b) A[k][tid] /= A[k][k];
+            __syncthreads();
+            const int m = b - k - 1;  // trailing (k+1..b-1)^2, upper part
+            for (int e = tid; e < m * m; e += blockDim.x) {
+                const int i = k + 1 + e / m, j = k + 1 + e % m;
+                if (j >= i) A[i][j] -= A[k][i] * A[k][j];
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (!fail) break;
+        __syncthreads();
+    }
+    if (fail) {
+        if (tid == 0) *status = 2;
+        return;
+    }
+    // R upper triangular in A (i <= j). Column c of R^-1 by back substitution.
+    if (tid < b) {
+        const int c = tid;
+        double x[kMaxB];
+        for (int i = 0; i < b; ++i) x[i] = 0.0;
+        x[c] = 1.0 / A[c][c];
+        for (int i = c - 1; i >= 0; --i) {
+            double sacc = 0.0;
+            for (int k = i + 1; k <= c; ++k) sacc += A[i][k] * x[k];
+            x[i] = -sacc / A[i][i];
+        }
+        for (int i = 0; i < b; ++i) Rinv[i * b + c] = x[i];
+    }
+    if (tid == 0) *status = (shift > 0.0) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ E5: Rayleigh-Ritz
+constexpr int kRrSmem = 2 * kMaxB * (kMaxB + 1) * sizeof(double);
+
+struct RrOut {
+    double theta[kMaxB];     // Ritz values, descending algebraic
+    double U[kMaxB * kMaxB]; // U[p*b + j]: component p of Ritz vector j (sorted)
+    double resid[kMaxB];     // ||B~ v_j - θ_j v_j|| for all j
+    double maxres;           // max_j<m resid_j / max_i |θ_i|
+    int converged;
+    int n_negative;          // among the top m
+    int sweeps;
+};
+
+// Parallel cyclic Jacobi (round-robin pair ordering) on sym(H); residuals from the Gram
+// G = Y^T Y with Y = B~ X: r_j^2 = u_j^T G u_j - θ_j^2 for orthonormal X.
+__global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const double* __restrict__ Hg,
+                                            const double* __restrict__ Gg, RrOut* __restrict__ out) {
+    extern __shared__ double rr_smem[];
+    double (*A)[kMaxB + 1] = reinterpret_cast<double (*)[kMaxB + 1]>(rr_smem);
+    double (*V)[kMaxB + 1] = reinterpret_cast<double (*)[kMaxB + 1]>(rr_smem + kMaxB * (kMaxB + 1));
+    __shared__ double cs[kMaxB / 2 + 1], sn[kMaxB / 2 + 1];
+    __shared__ int pp[kMaxB / 2 + 1], qq[kMaxB / 2 + 1];
+    __shared__ int perm[kMaxB + 1];
+    __shared__ double offn, nrm;
+    __shared__ int order[kMaxB];
+    const int tid = threadIdx.x;
+    const int be = b + (b & 1);
+    const int np = be / 2;
+    for (int e = tid; e < b * b; e += blockDim.x) {
+        const int i = e / b, j = e % b;
+        A[i][j] = 0.5 * (Hg[i * b + j] + Hg[j * b + i]);
+        V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    if (tid < be) perm[tid] = tid;
+    __syncthreads();
+    int sweep = 0;
+    for (; sweep < 40; ++sweep) {
+        if (tid == 0) {
+            double o = 0.0, f = 0.0;
+            for (int i = 0; i < b; ++i)
+                for (int j = 0; j < b; ++j) {
+                    const double v = A[i][j] * A[i][j];
+                    f += v;
+                    if (i != j) o += v;
+                }
+            offn = o;
+            nrm = f;
+        }
+        __syncthreads();
+        if (!(offn > 1e-30 * nrm) || nrm == 0.0) break;
+        for (int round = 0; round < be - 1; ++round) {
+            if (tid < np) {
+                int p = perm[tid], q = perm[be - 1 - tid];
+                if (p > q) { const int t = p; p = q; q = t; }
+                pp[tid] = p;
+                qq[tid] = q;
+                double c = 1.0, s = 0.0;
+                if (q < b) {
+                    const double apq = A[p][q];
+                    if (fabs(apq) > 1e-300) {
+                        const double th = (A[q][q] - A[p][p]) / (2.0 * apq);
+                        const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+                        c = 1.0 / sqrt(t * t + 1.0);
+                        s = t * c;
+                    }
+                }
+                cs[tid] = c;
+                sn[tid] = s;
+            }
+            __syncthreads();
+            // rows: A <- J^T A
+            for (int e = tid; e < np * b; e += blockDim.x) {
+                const int pr = e / b, k = e % b;
+                const int p = pp[pr], q = qq[pr];
+                if (q < b) {
+                    const double c = cs[pr], s = sn[pr];
+                    const double ap = A[p][k], aq = A[q][k];
+                    A[p][k] = c * ap - s * aq;
+                    A[q][k] = s * ap + c * aq;
+                }
+            }
+            __syncthreads();
+            // columns: A <- A J, V <- V J
+            for (int e = tid; e < np * b; e += blockDim.x) {
+                const int pr = e / b, k = e % b;
+                const int p = pp[pr], q = qq[pr];
+                if (q < b) {
+                    const double c = cs[pr], s = sn[pr];
+                    const double ap = A[k][p], aq = A[k][q];
+                    A[k][p] = c * ap - s * aq;
+                    A[k][q] = s * ap + c * aq;
+                    const double vp = V[k][p], vq = V[k][q];
+                    V[k][p] = c * vp - s * vq;
+                    V[k][q] = s * vp + c * vq;
+                }
+            }
+            __syncthreads();
+            // rotate the tournament: position 0 fixed, others shift by one
+            if (tid == 0) {
+                const int last = perm[be - 1];
+                for (int i = be - 1; i > 1; --i) perm[i] = perm[i - 1];
+                perm[1] = last;
+            }
+            __syncthreads();
+        }
+    }
+    if (tid == 0) {
+        for (int i = 0; i < b; ++i) order[i] = i;
+        for (int i = 0; i < b; ++i) {  // selection sort, descending θ, ties -> lower index
+            int best = i;
+            for (int j = i + 1; j < b; ++j)
+                if (A[order[j]][order[j]] > A[order[best]][order[best]]) best = j;
+            const int t = order[i]; order[i] = order[best]; order[best] = t;
+        }
+        out->sweeps = sweep;
+    }
+    __syncthreads();
+    for (int e = tid; e < b * b; e += blockDim.x) {
+        const int p = e / b, j = e % b;
+        out->U[p * b + j] = V[p][order[j]];
+    }
+    if (tid < b) out->theta[tid] = A[order[tid]][order[tid]];
+    // residuals: thread j computes u_j^T G u_j
+    if (tid < b) {
+        const int j = order[tid];
+        double s = 0.0;
+        for (int p = 0; p < b; ++p) {
+            double gp = 0.0;
+            for (int q = 0; q < b; ++q) gp += Gg[p * b + q] * V[q][j];
+            s += V[p][j] * gp;
+        }
+        const double th = A[j][j];
+        out->resid[tid] = sqrt(fmax(s - th * th, 0.0));
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double tmax = 0.0;
+        for (int i = 0; i < b; ++i) tmax = fmax(tmax, fabs(A[i][i]));
+        double mr = 0.0;
+        int neg = 0;
+        for (int j = 0; j < m; ++j) {
+            mr = fmax(mr, out->resid[j]);
+            if (out->theta[j] < 0.0) ++neg;
+        }
+        out->maxres = tmax > 0.0 ? mr / tmax : 0.0;
+        out->converged = (tol > 0.0 && out->maxres <= tol) ? 1 : 0;
+        out->n_negative = neg;
+    }
+}
+
+// ------------------------------------------------------------------ E4/E6: out = in * M
+// in: n x b (row stride b), M: b x mo fp64 row-major (leading dim ldm), out: n x mo.
+// addc (optional, mo): a constant added to every entry of column c (the exact null
+// eigenvector 1/sqrt(n) of B~, "J 1 = 0", when it belongs to the top m).
+__global__ void __launch_bounds__(256) k_rotate(int64_t n, int b, int mo, int ldm, const float* __restrict__ in,
+                                                const double* __restrict__ M, float* __restrict__ out,
+                                                const double* __restrict__ addc) {
+    __shared__ double Ms[kMaxB * kMaxB];
+    __shared__ double As[kMaxB];
+    for (int e = threadIdx.x; e < b * mo; e += blockDim.x) Ms[e] = M[(e / mo) * ldm + (e % mo)];
+    for (int e = threadIdx.x; e < mo; e += blockDim.x) As[e] = addc ? addc[e] : 0.0;
+    __syncthreads();
+    const int64_t total = n * mo;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / mo;
+        const int c = (int)(e % mo);
+        const float* row = in + i * b;
+        double acc = As[c];
+        for (int p = 0; p < b; ++p) acc = fma((double)__ldg(row + p), Ms[p * mo + c], acc);
+        out[e] = (float)acc;
+    }
+}
+
+// ------------------------------------------------------------------ E1: Philox N(0,1)
+__device__ __forceinline__ void philox4x32_10(uint32_t ctr[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * ctr[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * ctr[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ ctr[1] ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ ctr[3] ^ k1;
+        ctr[1] = (uint32_t)p1;
+        ctr[3] = (uint32_t)p0;
+        ctr[0] = n0;
+        ctr[2] = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+__global__ void k_init_philox(int64_t n, int b, uint64_t seed, float* __restrict__ X) {
+    const int64_t total = n * b;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t ctr[4] = {(uint32_t)e, (uint32_t)(e >> 32), 0x5eed5eedu, 0u};
+        philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
+        const double u1 = ((double)ctr[0] + 1.0) * (1.0 / 4294967296.0);  // (0, 1]
+        const double u2 = (double)ctr[1] * (1.0 / 4294967296.0);
+        X[e] = (float)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+    }
+}
+
+// ------------------------------------------------------------------ E6: signs and Z
+// Per column the entry of largest |v| (ties -> lowest row); sign[c] = its sign.
+__global__ void __launch_bounds__(256) k_col_argmax(int64_t n, int mo, const float* __restrict__ V,
+                                                    float* __restrict__ pval, long long* __restrict__ pidx,
+                                                    float* __restrict__ sign, unsigned int* __restrict__ counter) {
+    __shared__ float bv[256];
+    __shared__ long long bi[256];
+    const int tid = threadIdx.x;
+    const int rps = 256 / mo;
+    const int c = tid % mo, r0 = tid / mo;
+    const int64_t rows_per_blk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t beg = blockIdx.x * rows_per_blk, end = min(n, beg + rows_per_blk);
+    float best = -1.f;
+    long long bidx = -1;
+    if (r0 < rps)
+        for (int64_t i = beg + r0; i < end; i += rps) {
+            const float a = fabsf(V[i * mo + c]);
+            if (a > best) { best = a; bidx = i; }   // rows visited in increasing order
+        }
+    bv[tid] = best;
+    bi[tid] = bidx;
+    __syncthreads();
+    if (tid < mo) {
+        for (int q = 1; q < rps; ++q) {
+            const float a = bv[q * mo + tid];
+            const long long ii = bi[q * mo + tid];
+            if (ii >= 0 && (a > best || (a == best && (bidx < 0 || ii < bidx)))) { best = a; bidx = ii; }
+        }
+        pval[blockIdx.x * kMaxB + tid] = best;
+        pidx[blockIdx.x * kMaxB + tid] = bidx;
+    }
+    if (last_block_done(counter)) {
+        if (tid < mo) {
+            float bb = -1.f;
+            long long ii = -1;
+            for (unsigned int q = 0; q < gridDim.x; ++q) {
+                const float a = pval[q * kMaxB + tid];
+                const long long j = pidx[q * kMaxB + tid];
+                if (j >= 0 && (a > bb || (a == bb && (ii < 0 || j < ii)))) { bb = a; ii = j; }
+            }
+            sign[tid] = (ii >= 0 && V[ii * mo + tid] < 0.f) ? -1.f : 1.f;
+        }
+        if (tid == 0) *counter = 0;
+    }
+}
+
+__global__ void k_finalize(int64_t n, int mo, const float* __restrict__ sign, const double* __restrict__ theta,
+                           float* __restrict__ V, float* __restrict__ Z) {
+    const int64_t total = n * mo;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % mo);
+        const float v = V[e] * sign[c];
+        V[e] = v;
+        if (Z) Z[e] = (float)((double)v * sqrt(fmax(theta[c], 0.0)));
+    }
+}
+
+}  // namespace sbmds

@@ -1,0 +1,331 @@
+// Sparse stages of the sBMDS operator apply.
+//
+//   B~ X = -1/2 J S D S^T J X with J S = S - 1 w^T, w = S^T 1 / n, so
+//     s  = 1^T X                          k_colsum        (A1, "J ... rank-one")
+//     Y1 = S^T X - w s^T                   k_spmm_csc_*    (A2, right-multiply by P^T)
+//     Y2 = D Y1,  t = w^T Y2               k_dstream.cuh   (A3, A4)
+//     Y  = -1/2 (S Y2 - 1 t^T)             k_spmm_csr_*    (A5, left-multiply by P)
+// No n-length centred copy is formed; every reduction has a fixed order (no atomics on
+// values), so results are bitwise deterministic.
+#pragma once
+#include "common.cuh"
+
+namespace sbmds {
+
+// ------------------------------------------------------------------ create-time helpers
+__global__ void k_rowptr_to_i32(int64_t n, const int64_t* __restrict__ rp64, int32_t* __restrict__ rp32,
+                                int64_t nnz, int* __restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = rp64[i];
+        const bool ok = v >= 0 && v <= nnz && (i == 0 ? v == 0 : true) && (i == n ? v == nnz : true) &&
+                        (i == 0 || rp64[i - 1] <= v);
+        if (!ok) atomicOr(bad, 1);
+        rp32[i] = (int32_t)v;
+    }
+}
+
+// rowof[e] = row of stored entry e; checks 0 <= col < l and finite values.
+__global__ void k_expand_rows(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const float* __restrict__ val, int64_t l, int32_t* __restrict__ rowof,
+                              int* __restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        for (int32_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
+            rowof[e] = (int32_t)i;
+            const int32_t c = col[e];
+            if (c < 0 || c >= l || !isfinite(val[e])) atomicOr(bad, 2);
+        }
+    }
+}
+
+__global__ void k_iota(int32_t n, int32_t* __restrict__ out) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = i;
+}
+
+// After a stable sort of (col, entry) pairs: CSC row index / value gathers.
+__global__ void k_gather_csc(int32_t nnz, const int32_t* __restrict__ perm, const int32_t* __restrict__ rowof,
+                             const float* __restrict__ val, int32_t* __restrict__ row_idx,
+                             float* __restrict__ cval) {
+    for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x) {
+        const int32_t e = perm[p];
+        row_idx[p] = rowof[e];
+        cval[p] = val[e];
+    }
+}
+
+// col_ptr[c] = first position of column >= c in the sorted column keys (binary search).
+__global__ void k_col_ptr(int64_t l, int32_t nnz, const int32_t* __restrict__ keys,
+                          int32_t* __restrict__ col_ptr) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= l;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        int32_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const int32_t mid = lo + ((hi - lo) >> 1);
+            if (keys[mid] < c) lo = mid + 1; else hi = mid;
+        }
+        col_ptr[c] = lo;
+    }
+}
+
+// w_j = (1/n) Σ_i S_ij  (column sums, fixed order) and the spatial key of column j
+// (median row of its support) used to order the CSC SpMM for L2 locality.
+__global__ void k_colstats(int64_t l, int64_t n, const int32_t* __restrict__ col_ptr,
+                           const int32_t* __restrict__ row_idx, const float* __restrict__ cval,
+                           double* __restrict__ w, int32_t* __restrict__ key) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < l;
+         j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t b = col_ptr[j], e = col_ptr[j + 1];
+        double s = 0.0;
+        for (int32_t p = b + lane; p < e; p += 32) s += (double)cval[p];
+        s = warp_sum(s);
+        if (lane == 0) {
+            w[j] = s / (double)n;
+            key[j] = (e > b) ? row_idx[b + ((e - b) >> 1)] : 0;
+        }
+    }
+}
+
+// max |Σ_j S_ij - 1| over rows (diagnostic: PoU S has rows summing to 1).
+__global__ void k_rowsum_dev(int64_t n, const int32_t* __restrict__ rp, const float* __restrict__ val,
+                             unsigned long long* __restrict__ out_bits) {
+    const int lane = threadIdx.x & 31;
+    double dmax = 0.0;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double s = 0.0;
+        for (int32_t e = rp[i] + lane; e < rp[i + 1]; e += 32) s += (double)val[e];
+        s = warp_sum(s);
+        dmax = fmax(dmax, fabs(s - 1.0));
+    }
+    if (lane == 0) atomicMax(out_bits, (unsigned long long)__double_as_longlong(dmax));
+}
+
+// |D_ij - D_ji| max and a finiteness check (SBMDS_VALIDATE). Order-free max -> atomic ok.
+__global__ void k_check_sym(int64_t l, int64_t ld, const float* __restrict__ D,
+                            unsigned int* __restrict__ maxdiff_bits, unsigned int* __restrict__ maxabs_bits,
+                            int* __restrict__ bad) {
+    __shared__ float tile[32][33];
+    const int64_t bi = blockIdx.y * 32, bj = blockIdx.x * 32;
+    if (bj > bi) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    float md = 0.f, ma = 0.f;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = bj + r, j = bi + tx;
+        tile[r][tx] = (i < l && j < l) ? D[i * ld + j] : 0.f;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = bi + r, j = bj + tx;
+        if (i < l && j < l) {
+            const float a = D[i * ld + j], b = tile[tx][r];
+            if (!isfinite(a)) atomicOr(bad, 4);
+            md = fmaxf(md, fabsf(a - b));
+            ma = fmaxf(ma, fabsf(a));
+        }
+    }
+    atomicMax(maxdiff_bits, __float_as_uint(md));
+    atomicMax(maxabs_bits, __float_as_uint(ma));
+}
+
+// ------------------------------------------------------------------ A1: s = 1^T X  (fp64)
+// Block partials over row ranges, then the last block sums them in block order.
+__global__ void k_colsum(int64_t n, int b, const float* __restrict__ X, double* __restrict__ part,
+                         double* __restrict__ s, unsigned int* __restrict__ counter) {
+    __shared__ double red[256];
+    const int rps = blockDim.x / b;                 // rows per step (b <= 64 -> >= 4)
+    const int t = threadIdx.x;
+    const int c = t % b, r0 = t / b;
+    const int64_t rows_per_blk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t beg = blockIdx.x * rows_per_blk, end = min(n, beg + rows_per_blk);
+    double acc = 0.0;
+    if (r0 < rps)
+        for (int64_t i = beg + r0; i < end; i += rps) acc += (double)X[i * b + c];
+    red[t] = (r0 < rps) ? acc : 0.0;
+    __syncthreads();
+    if (t < b) {
+        double v = 0.0;
+        for (int q = 0; q < rps; ++q) v += red[q * b + t];
+        part[blockIdx.x * kMaxB + t] = v;
+    }
+    if (last_block_done(counter)) {
+        if (t < b) {
+            double v = 0.0;
+            for (unsigned int q = 0; q < gridDim.x; ++q) v += part[q * kMaxB + t];
+            s[t] = v;
+        }
+        if (t == 0) *counter = 0;
+    }
+}
+
+// ------------------------------------------------------------------ A2: Y1 = S^T X - w s^T
+// Transposed SpMM through the device CSC copy: one warp per column (processed in the
+// spatial `order`), LPR lanes per gathered X row (float4 each), G = 32/LPR rows in
+// flight; the G partial sums are combined with shuffles (fixed order). Y1 is l x bp
+// (bp = padded width; columns >= b are written as 0).
+template <int LPR>
+__global__ void __launch_bounds__(256) k_spmm_csc_vec4(
+    int64_t l, int b, int bp, const int32_t* __restrict__ col_ptr, const int32_t* __restrict__ row_idx,
+    const float* __restrict__ cval, const int32_t* __restrict__ order, const float* __restrict__ X,
+    const double* __restrict__ w, const double* __restrict__ s, float* __restrict__ Y1) {
+    constexpr int G = 32 / LPR;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / LPR, q = lane % LPR;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (wid >= l) return;
+    const int64_t j = order ? order[wid] : wid;
+    const int32_t beg = col_ptr[j], end = col_ptr[j + 1];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t base = beg; base < end; base += 32) {
+        const int32_t e = base + lane;
+        const int32_t r_l = e < end ? row_idx[e] : 0;
+        const float v_l = e < end ? cval[e] : 0.f;
+        const int cnt = min(32, end - base);
+#pragma unroll 4
+        for (int tq = g; tq < 32; tq += G) {
+            const int32_t r = __shfl_sync(0xffffffffu, r_l, tq);
+            const float v = __shfl_sync(0xffffffffu, v_l, tq);
+            if (tq < cnt) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(X + (int64_t)r * b) + q);
+                acc.x = fmaf(v, x.x, acc.x);
+                acc.y = fmaf(v, x.y, acc.y);
+                acc.z = fmaf(v, x.z, acc.z);
+                acc.w = fmaf(v, x.w, acc.w);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+    }
+    if (g == 0) {
+        const double wj = w[j];
+        const int c = 4 * q;
+        float4 out;
+        out.x = (float)((double)acc.x - wj * s[c + 0]);
+        out.y = (float)((double)acc.y - wj * s[c + 1]);
+        out.z = (float)((double)acc.z - wj * s[c + 2]);
+        out.w = (float)((double)acc.w - wj * s[c + 3]);
+        reinterpret_cast<float4*>(Y1 + j * bp)[q] = out;
+    }
+}
+
+// Generic width: LPR = nextpow2(b) (<= 32) lanes per row, NC columns per lane.
+template <int LPR, int NC>
+__global__ void __launch_bounds__(256) k_spmm_csc_gen(
+    int64_t l, int b, int bp, const int32_t* __restrict__ col_ptr, const int32_t* __restrict__ row_idx,
+    const float* __restrict__ cval, const int32_t* __restrict__ order, const float* __restrict__ X,
+    const double* __restrict__ w, const double* __restrict__ s, float* __restrict__ Y1) {
+    constexpr int G = 32 / LPR;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / LPR, q = lane % LPR;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (wid >= l) return;
+    const int64_t j = order ? order[wid] : wid;
+    const int32_t beg = col_ptr[j], end = col_ptr[j + 1];
+    float acc[NC];
+#pragma unroll
+    for (int u = 0; u < NC; ++u) acc[u] = 0.f;
+    for (int32_t base = beg; base < end; base += 32) {
+        const int32_t e = base + lane;
+        const int32_t r_l = e < end ? row_idx[e] : 0;
+        const float v_l = e < end ? cval[e] : 0.f;
+        const int cnt = min(32, end - base);
+#pragma unroll 4
+        for (int tq = g; tq < 32; tq += G) {
+            const int32_t r = __shfl_sync(0xffffffffu, r_l, tq);
+            const float v = __shfl_sync(0xffffffffu, v_l, tq);
+            if (tq < cnt) {
+#pragma unroll
+                for (int u = 0; u < NC; ++u) {
+                    const int c = q + u * LPR;
+                    if (c < b) acc[u] = fmaf(v, __ldg(X + (int64_t)r * b + c), acc[u]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int u = 0; u < NC; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+    if (g == 0) {
+        const double wj = w[j];
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+            const int c = q + u * LPR;
+            if (c < b) Y1[j * bp + c] = (float)((double)acc[u] - wj * s[c]);
+            else if (c < bp) Y1[j * bp + c] = 0.f;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ A5: Y = -1/2 (S Y2 - 1 t^T)
+// CSR SpMM: LPR lanes per row (float4 gathers of the L2-resident Y2 rows), G rows per warp.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_spmm_csr_vec4(
+    int64_t n, int b, int bp, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+    const float* __restrict__ val, const float* __restrict__ Y2, const double* __restrict__ t,
+    float* __restrict__ Y) {
+    constexpr int G = 32 / LPR;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / LPR, q = lane % LPR;
+    const int64_t i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G + g;
+    if (i >= n) return;
+    const int32_t beg = rp[i], end = rp[i + 1];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int32_t e = beg; e < end; ++e) {
+        const int32_t c = __ldg(col + e);
+        const float v = __ldg(val + e);
+        const float4 y = __ldg(reinterpret_cast<const float4*>(Y2 + (int64_t)c * bp) + q);
+        acc.x = fmaf(v, y.x, acc.x);
+        acc.y = fmaf(v, y.y, acc.y);
+        acc.z = fmaf(v, y.z, acc.z);
+        acc.w = fmaf(v, y.w, acc.w);
+    }
+    const int c0 = 4 * q;
+    float4 out;
+    out.x = (float)(-0.5 * ((double)acc.x - t[c0 + 0]));
+    out.y = (float)(-0.5 * ((double)acc.y - t[c0 + 1]));
+    out.z = (float)(-0.5 * ((double)acc.z - t[c0 + 2]));
+    out.w = (float)(-0.5 * ((double)acc.w - t[c0 + 3]));
+    reinterpret_cast<float4*>(Y + i * b)[q] = out;
+}
+
+template <int LPR, int NC>
+__global__ void __launch_bounds__(256) k_spmm_csr_gen(
+    int64_t n, int b, int bp, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+    const float* __restrict__ val, const float* __restrict__ Y2, const double* __restrict__ t,
+    float* __restrict__ Y) {
+    constexpr int G = 32 / LPR;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / LPR, q = lane % LPR;
+    const int64_t i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G + g;
+    if (i >= n) return;
+    const int32_t beg = rp[i], end = rp[i + 1];
+    float acc[NC];
+#pragma unroll
+    for (int u = 0; u < NC; ++u) acc[u] = 0.f;
+#pragma unroll 4
+    for (int32_t e = beg; e < end; ++e) {
+        const int32_t c = __ldg(col + e);
+        const float v = __ldg(val + e);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) {
+            const int cc = q + u * LPR;
+            if (cc < b) acc[u] = fmaf(v, __ldg(Y2 + (int64_t)c * bp + cc), acc[u]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < NC; ++u) {
+        const int cc = q + u * LPR;
+        if (cc < b) Y[i * b + cc] = (float)(-0.5 * ((double)acc[u] - t[cc]));
+    }
+}
+
+}  // namespace sbmds

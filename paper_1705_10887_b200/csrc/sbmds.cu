@@ -1,0 +1,852 @@
+// libsbmds — C-ABI implementation (include/sbmds.h). Host driver of the sBMDS hot path:
+// create (C1, C2), apply (A1-A5), eigs (E1-E6); see DESIGN.md §4 for the step list.
+#include <cub/cub.cuh>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sbmds.h"
+#include "common.cuh"
+#include "k_dstream.cuh"
+#include "k_small.cuh"
+#include "k_sparse.cuh"
+
+namespace sbmds {
+std::atomic<int64_t> g_launches{0};
+}
+
+using namespace sbmds;
+
+// ============================================================================ errors
+namespace {
+thread_local std::string t_err;
+
+sbmds_status fail(sbmds_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return st;
+}
+
+struct CudaError {
+    cudaError_t e;
+    const char* what;
+};
+
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t _e = (call);                                  \
+        if (_e != cudaSuccess) throw CudaError{_e, #call};        \
+    } while (0)
+
+template <typename K, typename... Args>
+void launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    kernel<<<grid, block, smem, st>>>(args...);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CK(cudaGetLastError());
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int next_pow2(int b) {
+    int p = 1;
+    while (p < b) p <<= 1;
+    return p;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void ensure(size_t nb) {
+        if (nb <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, nb);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            throw CudaError{e, "cudaMalloc"};
+        }
+        bytes = nb;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+// Per-kernel-family device timing with CUDA events recorded on the launching stream
+// (sbmds_set_option "profile" = bitmask of families; read back with sbmds_get_stat
+// "<family>_ns" / "<family>_launches"). Used by bench.py for the roofline line.
+enum { PK_COLSUM = 0, PK_CSC, PK_DSTREAM, PK_DREDUCE, PK_CSR, PK_GRAM, PK_CHOL, PK_ROTATE, PK_RR, PK_N };
+const char* const kProfNames[PK_N] = {"colsum", "csc", "dstream", "dreduce", "csr", "gram", "chol", "rotate", "rr"};
+
+struct Profiler {
+    uint32_t mask = 0;
+    std::vector<cudaEvent_t> pool;
+    struct Pend { int k; cudaEvent_t a, b; };
+    std::vector<Pend> pend;
+    double ns[PK_N] = {0};
+    int64_t cnt[PK_N] = {0};
+    cudaEvent_t get() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) throw CudaError{cudaErrorMemoryAllocation, "cudaEventCreate"};
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    void drain() {
+        for (auto& p : pend) {
+            float ms = 0.f;
+            cudaEventSynchronize(p.b);
+            cudaEventElapsedTime(&ms, p.a, p.b);
+            ns[p.k] += 1e6 * (double)ms;
+            cnt[p.k] += 1;
+            pool.push_back(p.a);
+            pool.push_back(p.b);
+        }
+        pend.clear();
+    }
+    ~Profiler() {
+        for (auto& p : pend) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+template <typename F>
+void profiled(Profiler& pr, int k, cudaStream_t st, F&& f) {
+    if (!(pr.mask & (1u << k))) {
+        f();
+        return;
+    }
+    cudaEvent_t a = pr.get(), b = pr.get();
+    CK(cudaEventRecord(a, st));
+    f();
+    CK(cudaEventRecord(b, st));
+    pr.pend.push_back({k, a, b});
+}
+
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs for the grid reductions
+constexpr int kCounters = 8;
+enum { CNT_COLSUM = 0, CNT_DRED = 1, CNT_GRAM = 2, CNT_ARGMAX = 3 };
+
+}  // namespace
+
+// ============================================================================ handle
+struct sbmds_ctx {
+    int64_t n = 0, l = 0, nnz = 0;
+    int dev = 0, num_sms = 148;
+    // S (CSR) and its device-built CSC copy
+    DevBuf rp, col, val, cptr, ridx, cval, order, w;
+    // D_ll
+    float* D = nullptr;
+    int64_t ldD = 0;
+    bool own_D = false;
+    DevBuf Dbuf;
+    CUtensorMap dmap[7];
+    bool dmap_ok[7] = {false, false, false, false, false, false, false};
+    // apply workspace
+    DevBuf Y1, Y2, P, colpart, s, t, tpart, counters;
+    int64_t y1_rows = 0;
+    // eigs workspace
+    DevBuf X, Y, gpart, G, H, Rinv, status, rr, vtmp, ztmp, sign, apval, apidx, xhost, yhost, vsel;
+    // options / stats
+    int rr_period = 5;
+    int use_graph = 0;
+    int order_columns = 1;
+    int dstream = 0;
+    double rowsum_dev = 0.0;
+    bool d_borrowed = false;
+    Profiler prof;
+};
+
+namespace {
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int bp_index(int bp) {
+    int i = 0;
+    while ((1 << i) < bp) ++i;
+    return i;  // 1->0, 2->1, ..., 64->6
+}
+
+template <int BP>
+void encode_dmap(sbmds_ctx* h) {
+    using C = DsCfg<BP>;
+    const int i = bp_index(BP);
+    if (h->dmap_ok[i]) return;
+    EncodeFn enc = get_encode();
+    if (!enc) throw CudaError{cudaErrorNotSupported, "cuTensorMapEncodeTiled entry point"};
+    cuuint64_t dims[2] = {(cuuint64_t)h->l, (cuuint64_t)h->l};
+    cuuint64_t strides[1] = {(cuuint64_t)(h->ldD * sizeof(float))};
+    cuuint32_t box[2] = {(cuuint32_t)C::BOXW, (cuuint32_t)C::BK};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&h->dmap[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)h->D, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue, "cuTensorMapEncodeTiled"};
+    h->dmap_ok[i] = true;
+}
+
+// ---------------------------------------------------------------------------- A3 + A4
+template <int BP>
+void run_dstream(sbmds_ctx* h, int b, cudaStream_t st) {
+    using C = DsCfg<BP>;
+    encode_dmap<BP>(h);
+    StreamK sk;
+    sk.RT = (h->l + C::TM - 1) / C::TM;
+    sk.KT = (h->l + C::BK - 1) / C::BK;
+    sk.T = sk.RT * sk.KT;
+    sk.grid = (int)std::min<int64_t>(h->num_sms, sk.T);
+    const int maxseg = (int)((sk.grid + sk.RT - 1) / sk.RT) + 2;
+    h->P.ensure((size_t)sk.RT * maxseg * C::TM * BP * sizeof(double));
+    static bool attr_set[7] = {false};
+    if (!attr_set[bp_index(BP)]) {
+        CK(cudaFuncSetAttribute(k_dstream_ffma<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM + 1024));
+        attr_set[bp_index(BP)] = true;
+    }
+    profiled(h->prof, PK_DSTREAM, st, [&] {
+        launch(k_dstream_ffma<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM + 1024, st,
+               h->dmap[bp_index(BP)], h->l, (const float*)h->Y1.as<float>(), sk, maxseg, h->P.as<double>());
+    });
+    const int rows_per_blk = 256 / BP;
+    const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
+    profiled(h->prof, PK_DREDUCE, st, [&] {
+        launch(k_dreduce, dim3(grid), dim3(256), 0, st, h->l, BP, b, C::TM, sk, maxseg,
+               (const double*)h->P.as<double>(), (const double*)h->w.as<double>(), h->Y2.as<float>(),
+               h->tpart.as<double>(), h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
+    });
+}
+
+void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st) {
+    switch (bp) {
+        case 1: run_dstream<1>(h, b, st); break;
+        case 2: run_dstream<2>(h, b, st); break;
+        case 4: run_dstream<4>(h, b, st); break;
+        case 8: run_dstream<8>(h, b, st); break;
+        case 16: run_dstream<16>(h, b, st); break;
+        case 32: run_dstream<32>(h, b, st); break;
+        default: run_dstream<64>(h, b, st); break;
+    }
+}
+
+// ---------------------------------------------------------------------------- A2 / A5 dispatch
+void spmm_csc(sbmds_ctx* h, int b, int bp, const float* X, cudaStream_t st) {
+    const int grid = (int)((h->l + 7) / 8);
+    const int32_t* ord = h->order_columns ? h->order.as<int32_t>() : nullptr;
+    const bool vec = (b == bp) && (b % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    auto args = std::make_tuple(h->l, b, bp, (const int32_t*)h->cptr.as<int32_t>(),
+                                (const int32_t*)h->ridx.as<int32_t>(), (const float*)h->cval.as<float>(), ord, X,
+                                (const double*)h->w.as<double>(), (const double*)h->s.as<double>(),
+                                h->Y1.as<float>());
+    auto go = [&](auto kern) {
+        std::apply([&](auto... a) { launch(kern, dim3(grid), dim3(256), 0, st, a...); }, args);
+    };
+    if (vec) {
+        switch (b / 4) {
+            case 1: go(k_spmm_csc_vec4<1>); break;
+            case 2: go(k_spmm_csc_vec4<2>); break;
+            case 4: go(k_spmm_csc_vec4<4>); break;
+            case 8: go(k_spmm_csc_vec4<8>); break;
+            default: go(k_spmm_csc_vec4<16>); break;
+        }
+    } else {
+        switch (bp) {
+            case 1: go(k_spmm_csc_gen<1, 1>); break;
+            case 2: go(k_spmm_csc_gen<2, 1>); break;
+            case 4: go(k_spmm_csc_gen<4, 1>); break;
+            case 8: go(k_spmm_csc_gen<8, 1>); break;
+            case 16: go(k_spmm_csc_gen<16, 1>); break;
+            case 32: go(k_spmm_csc_gen<32, 1>); break;
+            default: go(k_spmm_csc_gen<32, 2>); break;
+        }
+    }
+}
+
+void spmm_csr(sbmds_ctx* h, int b, int bp, float* Y, cudaStream_t st) {
+    const bool vec = (b == bp) && (b % 4 == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+    const int lpr = vec ? b / 4 : std::min(bp, 32);
+    const int G = 32 / lpr;
+    const int64_t warps = (h->n + G - 1) / G;
+    const int grid = (int)((warps + 7) / 8);
+    auto args = std::make_tuple(h->n, b, bp, (const int32_t*)h->rp.as<int32_t>(), (const int32_t*)h->col.as<int32_t>(),
+                                (const float*)h->val.as<float>(), (const float*)h->Y2.as<float>(),
+                                (const double*)h->t.as<double>(), Y);
+    auto go = [&](auto kern) {
+        std::apply([&](auto... a) { launch(kern, dim3(grid), dim3(256), 0, st, a...); }, args);
+    };
+    if (vec) {
+        switch (b / 4) {
+            case 1: go(k_spmm_csr_vec4<1>); break;
+            case 2: go(k_spmm_csr_vec4<2>); break;
+            case 4: go(k_spmm_csr_vec4<4>); break;
+            case 8: go(k_spmm_csr_vec4<8>); break;
+            default: go(k_spmm_csr_vec4<16>); break;
+        }
+    } else {
+        switch (bp) {
+            case 1: go(k_spmm_csr_gen<1, 1>); break;
+            case 2: go(k_spmm_csr_gen<2, 1>); break;
+            case 4: go(k_spmm_csr_gen<4, 1>); break;
+            case 8: go(k_spmm_csr_gen<8, 1>); break;
+            case 16: go(k_spmm_csr_gen<16, 1>); break;
+            case 32: go(k_spmm_csr_gen<32, 1>); break;
+            default: go(k_spmm_csr_gen<32, 2>); break;
+        }
+    }
+}
+
+void ensure_apply_ws(sbmds_ctx* h, int bp) {
+    const int64_t rows = (h->l + 31) / 32 * 32;
+    if (h->Y1.bytes < (size_t)rows * bp * sizeof(float)) {
+        h->Y1.ensure((size_t)rows * kMaxB * sizeof(float));
+        CK(cudaMemset(h->Y1.p, 0, h->Y1.bytes));  // pad rows/cols stay 0 (TMA tail reads them)
+    }
+    h->Y2.ensure((size_t)h->l * kMaxB * sizeof(float));
+}
+
+// The whole operator apply on device buffers (stream-ordered, no host sync).
+void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st) {
+    const int bp = next_pow2(b);
+    ensure_apply_ws(h, bp);
+    // A1: s = 1^T X
+    profiled(h->prof, PK_COLSUM, st, [&] {
+        launch(k_colsum, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(),
+               h->s.as<double>(), h->counters.as<unsigned int>() + CNT_COLSUM);
+    });
+    // A2: Y1 = S^T X - w s^T
+    profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
+    // A3, A4: Y2 = D Y1, t = w^T Y2
+    dstream(h, b, bp, st);
+    // A5: Y = -1/2 (S Y2 - 1 t^T)
+    profiled(h->prof, PK_CSR, st, [&] { spmm_csr(h, b, bp, Y, st); });
+}
+
+void destroy_ctx(sbmds_ctx* h) {
+    if (!h) return;
+    DevBuf* bufs[] = {&h->rp, &h->col, &h->val, &h->cptr, &h->ridx, &h->cval, &h->order, &h->w, &h->Dbuf,
+                      &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
+                      &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel};
+    for (DevBuf* b : bufs) b->release();
+    delete h;
+}
+
+}  // namespace
+
+// ============================================================================ create
+extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const int64_t* row_ptr,
+                                     const int32_t* col_idx, const float* val, const float* D_ll, uint32_t flags,
+                                     void* cuda_stream, sbmds_t* out) {
+    if (!out) return fail(SBMDS_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || l < 1 || l > n) return fail(SBMDS_EINVAL, "need 1 <= l <= n (n=%lld, l=%lld)", (long long)n, (long long)l);
+    if (nnz < 0 || nnz >= (int64_t(1) << 31)) return fail(SBMDS_EINVAL, "need 0 <= nnz < 2^31");
+    if (n >= (int64_t(1) << 31) || l > 46340 * 4) return fail(SBMDS_EINVAL, "n or l too large");
+    if (!row_ptr || !D_ll || (nnz > 0 && (!col_idx || !val))) return fail(SBMDS_EINVAL, "NULL input pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    sbmds_ctx* h = new sbmds_ctx();
+    h->n = n;
+    h->l = l;
+    h->nnz = nnz;
+    try {
+        CK(cudaGetDevice(&h->dev));
+        CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
+        const int64_t nz = std::max<int64_t>(nnz, 1);
+        h->rp.ensure((n + 1) * sizeof(int32_t));
+        h->col.ensure(nz * sizeof(int32_t));
+        h->val.ensure(nz * sizeof(float));
+        h->cptr.ensure((l + 1) * sizeof(int32_t));
+        h->ridx.ensure(nz * sizeof(int32_t));
+        h->cval.ensure(nz * sizeof(float));
+        h->order.ensure(l * sizeof(int32_t));
+        h->w.ensure(l * sizeof(double));
+        h->colpart.ensure(kRedBlocks * kMaxB * sizeof(double));
+        h->tpart.ensure(kRedBlocks * kMaxB * sizeof(double));
+        h->s.ensure(kMaxB * sizeof(double));
+        h->t.ensure(kMaxB * sizeof(double));
+        h->counters.ensure(kCounters * sizeof(unsigned int));
+        CK(cudaMemsetAsync(h->counters.p, 0, h->counters.bytes, st));
+
+        // ---- C1: upload (or borrow) S, check structure
+        DevBuf rp64, tmpA, tmpB, tmpC, flags_d;
+        rp64.ensure((n + 1) * sizeof(int64_t));
+        CK(cudaMemcpyAsync(rp64.p, row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
+        if (nnz > 0) {
+            CK(cudaMemcpyAsync(h->col.p, col_idx, nnz * sizeof(int32_t), cudaMemcpyDefault, st));
+            CK(cudaMemcpyAsync(h->val.p, val, nnz * sizeof(float), cudaMemcpyDefault, st));
+        }
+        flags_d.ensure(64);
+        CK(cudaMemsetAsync(flags_d.p, 0, 64, st));
+        int* bad = flags_d.as<int>();
+        launch(k_rowptr_to_i32, dim3(256), dim3(256), 0, st, n, (const int64_t*)rp64.as<int64_t>(),
+               h->rp.as<int32_t>(), nnz, bad);
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        rp64.release();
+        if (hbad) {
+            destroy_ctx(h);
+            return fail(SBMDS_EINVAL, "row_ptr must start at 0, be nondecreasing and end at nnz");
+        }
+
+        // ---- C2: CSC (stable radix sort of (col, entry) pairs keeps rows ascending)
+        if (nnz > 0) {
+            tmpA.ensure(nnz * sizeof(int32_t));  // rowof
+            launch(k_expand_rows, dim3(1024), dim3(256), 0, st, n, (const int32_t*)h->rp.as<int32_t>(),
+                   (const int32_t*)h->col.as<int32_t>(), (const float*)h->val.as<float>(), l, tmpA.as<int32_t>(), bad);
+            CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (hbad) {
+                destroy_ctx(h);
+                return fail(SBMDS_EINVAL, "col_idx out of [0, l) or non-finite val");
+            }
+            tmpB.ensure(2 * (size_t)nnz * sizeof(int32_t));  // iota | sorted perm
+            tmpC.ensure((size_t)nnz * sizeof(int32_t));      // sorted keys
+            int32_t* iota = tmpB.as<int32_t>();
+            int32_t* perm = iota + nnz;
+            launch(k_iota, dim3(1024), dim3(256), 0, st, (int32_t)nnz, iota);
+            int end_bit = 1;
+            while ((int64_t(1) << end_bit) <= l) ++end_bit;
+            size_t tmp_bytes = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, h->col.as<int32_t>(), tmpC.as<int32_t>(), iota, perm,
+                                               (int)nnz, 0, end_bit, st));
+            DevBuf cubtmp;
+            cubtmp.ensure(tmp_bytes + 16);
+            CK(cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, h->col.as<int32_t>(), tmpC.as<int32_t>(), iota, perm,
+                                               (int)nnz, 0, end_bit, st));
+            g_launches.fetch_add(1);
+            launch(k_gather_csc, dim3(1024), dim3(256), 0, st, (int32_t)nnz, (const int32_t*)perm,
+                   (const int32_t*)tmpA.as<int32_t>(), (const float*)h->val.as<float>(), h->ridx.as<int32_t>(),
+                   h->cval.as<float>());
+            launch(k_col_ptr, dim3((unsigned)((l + 256) / 256)), dim3(256), 0, st, l, (int32_t)nnz,
+                   (const int32_t*)tmpC.as<int32_t>(), h->cptr.as<int32_t>());
+            CK(cudaStreamSynchronize(st));
+            cubtmp.release();
+        } else {
+            CK(cudaMemsetAsync(h->cptr.p, 0, (l + 1) * sizeof(int32_t), st));
+        }
+        // w, column keys, spatial column order (sort columns by their median row)
+        {
+            DevBuf keys, keys2, ord0;
+            keys.ensure(l * sizeof(int32_t));
+            keys2.ensure(l * sizeof(int32_t));
+            ord0.ensure(l * sizeof(int32_t));
+            launch(k_colstats, dim3((unsigned)std::min<int64_t>(4096, (l + 7) / 8)), dim3(256), 0, st, l, n,
+                   (const int32_t*)h->cptr.as<int32_t>(), (const int32_t*)h->ridx.as<int32_t>(),
+                   (const float*)h->cval.as<float>(), h->w.as<double>(), keys.as<int32_t>());
+            launch(k_iota, dim3(64), dim3(256), 0, st, (int32_t)l, ord0.as<int32_t>());
+            int end_bit = 1;
+            while ((int64_t(1) << end_bit) <= n) ++end_bit;
+            size_t tmp_bytes = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.as<int32_t>(), keys2.as<int32_t>(),
+                                               ord0.as<int32_t>(), h->order.as<int32_t>(), (int)l, 0, end_bit, st));
+            DevBuf cubtmp;
+            cubtmp.ensure(tmp_bytes + 16);
+            CK(cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, keys.as<int32_t>(), keys2.as<int32_t>(),
+                                               ord0.as<int32_t>(), h->order.as<int32_t>(), (int)l, 0, end_bit, st));
+            g_launches.fetch_add(1);
+            // rowsum deviation (diagnostic)
+            DevBuf rs;
+            rs.ensure(sizeof(unsigned long long));
+            CK(cudaMemsetAsync(rs.p, 0, sizeof(unsigned long long), st));
+            launch(k_rowsum_dev, dim3(1024), dim3(256), 0, st, n, (const int32_t*)h->rp.as<int32_t>(),
+                   (const float*)h->val.as<float>(), rs.as<unsigned long long>());
+            unsigned long long bits = 0;
+            CK(cudaMemcpyAsync(&bits, rs.p, sizeof bits, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            double d;
+            memcpy(&d, &bits, sizeof d);
+            h->rowsum_dev = d;
+        }
+        tmpA.release();
+        tmpB.release();
+        tmpC.release();
+
+        // ---- D_ll: borrow (device, l % 4 == 0) or copy into a 16-byte-pitched buffer
+        const bool d_dev = is_device_ptr(D_ll);
+        h->ldD = (l + 3) / 4 * 4;
+        if ((flags & SBMDS_BORROW_D) && d_dev && h->ldD == l && (reinterpret_cast<uintptr_t>(D_ll) & 15) == 0) {
+            h->D = const_cast<float*>(D_ll);
+            h->d_borrowed = true;
+        } else {
+            h->Dbuf.ensure((size_t)l * h->ldD * sizeof(float));
+            CK(cudaMemcpy2DAsync(h->Dbuf.p, h->ldD * sizeof(float), D_ll, l * sizeof(float), l * sizeof(float), l,
+                                 cudaMemcpyDefault, st));
+            h->D = h->Dbuf.as<float>();
+            h->own_D = true;
+        }
+        if (flags & SBMDS_VALIDATE) {
+            DevBuf cb;
+            cb.ensure(64);
+            CK(cudaMemsetAsync(cb.p, 0, 64, st));
+            unsigned int* md = cb.as<unsigned int>();
+            const unsigned tiles = (unsigned)((l + 31) / 32);
+            launch(k_check_sym, dim3(tiles, tiles), dim3(256), 0, st, l, h->ldD, (const float*)h->D, md, md + 1,
+                   reinterpret_cast<int*>(md + 2));
+            unsigned int hv[3];
+            CK(cudaMemcpyAsync(hv, md, sizeof hv, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            float mdiff, mabs;
+            memcpy(&mdiff, &hv[0], 4);
+            memcpy(&mabs, &hv[1], 4);
+            if (hv[2]) {
+                destroy_ctx(h);
+                return fail(SBMDS_EINVAL, "D_ll has non-finite entries");
+            }
+            if (mdiff > 1e-6f * mabs) {
+                destroy_ctx(h);
+                return fail(SBMDS_EINVAL, "D_ll not symmetric: max|D-D^T| = %g, max|D| = %g", mdiff, mabs);
+            }
+        }
+        CK(cudaStreamSynchronize(st));
+    } catch (const CudaError& e) {
+        destroy_ctx(h);
+        if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
+        return fail(SBMDS_ECUDA, "%s: %s", e.what, cudaGetErrorString(e.e));
+    }
+    *out = h;
+    return SBMDS_OK;
+}
+
+extern "C" void sbmds_destroy(sbmds_t h) {
+    if (!h) return;
+    DevGuard g(h->dev);
+    cudaDeviceSynchronize();
+    destroy_ctx(h);
+}
+
+extern "C" const char* sbmds_last_error(void) { return t_err.c_str(); }
+extern "C" int64_t sbmds_launch_count(void) { return g_launches.load(); }
+extern "C" int32_t sbmds_abi_version(void) { return 1; }
+
+// ============================================================================ apply
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+    const char* x = (const char*)a;
+    const char* y = (const char*)b;
+    return x < y + nb && y < x + na;
+}
+
+extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float* Y, void* cuda_stream) {
+    if (!h) return fail(SBMDS_EINVAL, "NULL handle");
+    if (b < 1 || b > kMaxB) return fail(SBMDS_EINVAL, "need 1 <= b <= 64 (b=%d)", b);
+    if (!X || !Y) return fail(SBMDS_EINVAL, "NULL X or Y");
+    const size_t bytes = (size_t)h->n * b * sizeof(float);
+    if (overlap(X, bytes, Y, bytes)) return fail(SBMDS_EINVAL, "X and Y overlap");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    DevGuard g(h->dev);
+    try {
+        const bool xd = is_device_ptr(X), yd = is_device_ptr(Y);
+        const float* Xd = X;
+        float* Yd = Y;
+        if (!xd) {
+            h->xhost.ensure(bytes);
+            CK(cudaMemcpyAsync(h->xhost.p, X, bytes, cudaMemcpyHostToDevice, st));
+            Xd = h->xhost.as<float>();
+        }
+        if (!yd) {
+            h->yhost.ensure(bytes);
+            Yd = h->yhost.as<float>();
+        }
+        apply_device(h, b, Xd, Yd, st);
+        if (!yd) CK(cudaMemcpyAsync(Y, Yd, bytes, cudaMemcpyDeviceToHost, st));
+        if (!xd || !yd) CK(cudaStreamSynchronize(st));
+    } catch (const CudaError& e) {
+        if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
+        return fail(SBMDS_ECUDA, "%s: %s", e.what, cudaGetErrorString(e.e));
+    }
+    return SBMDS_OK;
+}
+
+// ============================================================================ eigs
+namespace {
+
+void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st) {
+    h->gpart.ensure((size_t)kRedBlocks * 2 * kMaxB * kMaxB * sizeof(double));
+    profiled(h->prof, PK_GRAM, st, [&] {
+    if (X)
+        launch(k_gram<true>, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, Y, X, h->gpart.as<double>(),
+               h->G.as<double>(), h->H.as<double>(), h->counters.as<unsigned int>() + CNT_GRAM);
+    else
+        launch(k_gram<false>, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, Y, (const float*)nullptr,
+               h->gpart.as<double>(), h->G.as<double>(), (double*)nullptr, h->counters.as<unsigned int>() + CNT_GRAM);
+    });
+}
+
+// X <- Y R^-1 with G = Y^T Y = R^T R. Returns false on breakdown (status read later).
+void cholqr(sbmds_ctx* h, int b, const float* Yin, float* Xout, cudaStream_t st) {
+    gram(h, b, Yin, nullptr, st);
+    profiled(h->prof, PK_CHOL, st, [&] {
+        launch(k_chol, dim3(1), dim3(256), 0, st, b, (const double*)h->G.as<double>(), h->Rinv.as<double>(),
+               h->status.as<int>());
+    });
+    const int grid = (int)std::min<int64_t>(4 * 148, (h->n * b + 255) / 256);
+    profiled(h->prof, PK_ROTATE, st, [&] {
+        launch(k_rotate, dim3(grid), dim3(256), 0, st, h->n, b, b, b, Yin, (const double*)h->Rinv.as<double>(), Xout,
+               (const double*)nullptr);
+    });
+}
+
+}  // namespace
+
+extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol, uint64_t seed,
+                                   const float* X0, double* eigvals, float* V, float* Z, sbmds_info* info,
+                                   void* cuda_stream) {
+    if (!h) return fail(SBMDS_EINVAL, "NULL handle");
+    if (block < 1 || block > kMaxB || block >= h->n) return fail(SBMDS_EINVAL, "need 1 <= block <= 64, block < n");
+    if (m < 1 || m > block) return fail(SBMDS_EINVAL, "need 1 <= m <= block");
+    if (max_iters < 1) return fail(SBMDS_EINVAL, "need max_iters >= 1");
+    if (!eigvals) return fail(SBMDS_EINVAL, "eigvals (host) is NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    DevGuard g(h->dev);
+    const int b = block;
+    const int64_t n = h->n;
+    sbmds_status ret = SBMDS_OK;
+    try {
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, st));
+        h->X.ensure((size_t)n * b * sizeof(float));
+        h->Y.ensure((size_t)n * b * sizeof(float));
+        h->G.ensure(kMaxB * kMaxB * sizeof(double));
+        h->H.ensure(kMaxB * kMaxB * sizeof(double));
+        h->Rinv.ensure(kMaxB * kMaxB * sizeof(double));
+        h->status.ensure(16);
+        h->rr.ensure(sizeof(RrOut));
+        float* X = h->X.as<float>();
+        float* Y = h->Y.as<float>();
+        // E1: initial block, orthonormalised by Cholesky-QR (into Y, then swap roles)
+        if (X0) {
+            CK(cudaMemcpyAsync(Y, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
+        } else {
+            launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, Y);
+        }
+        cholqr(h, b, Y, X, st);
+        int hstat = 0;
+        CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR of the initial block broke down");
+
+        RrOut rr_host;
+        int it = 0;
+        bool converged = false;
+        for (it = 1; it <= max_iters; ++it) {
+            apply_device(h, b, X, Y, st);  // Y = B~ X
+            const bool do_rr = (it % h->rr_period == 0) || it == max_iters;
+            if (do_rr) {
+                gram(h, b, Y, X, st);  // G = Y^T Y, H = X^T Y
+                static bool rr_attr = false;
+                if (!rr_attr) {
+                    CK(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, kRrSmem));
+                    rr_attr = true;
+                }
+                profiled(h->prof, PK_RR, st, [&] {
+                    launch(k_rr, dim3(1), dim3(256), (size_t)kRrSmem, st, b, m, tol, (const double*)h->H.as<double>(),
+                           (const double*)h->G.as<double>(), h->rr.as<RrOut>());
+                });
+                int conv = 0;
+                CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (conv || it == max_iters) {
+                    converged = conv != 0;
+                    break;
+                }
+            }
+            cholqr(h, b, Y, X, st);  // X = Y R^-1
+            if (do_rr || it % 16 == 0) {
+                CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR broke down at iteration %d", it);
+            }
+        }
+        if (it > max_iters) it = max_iters;
+        CK(cudaMemcpyAsync(&rr_host, h->rr.p, sizeof(RrOut), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        // E6: select the top-m algebraic pairs. B~ 1 = 0 exactly (J 1 = 0), but the iterate
+        // lives in 1^perp after the first apply, so the known pair (0, 1/sqrt(n)) is merged
+        // into the Ritz list: it enters the top m when fewer than m Ritz values are >= 0.
+        std::vector<double> Msel((size_t)b * m, 0.0), addc(m, 0.0), theta_out(m, 0.0);
+        {
+            int r = 0;
+            bool zero_used = false;
+            for (int j = 0; j < m; ++j) {
+                if (!zero_used && (r >= b || rr_host.theta[r] < 0.0)) {
+                    zero_used = true;
+                    addc[j] = 1.0 / std::sqrt((double)n);
+                    theta_out[j] = 0.0;
+                    continue;
+                }
+                for (int p = 0; p < b; ++p) Msel[(size_t)p * m + j] = rr_host.U[p * b + r];
+                theta_out[j] = rr_host.theta[r];
+                ++r;
+            }
+        }
+        h->vsel.ensure(((size_t)b * m + 2 * m) * sizeof(double));
+        double* Msel_d = h->vsel.as<double>();
+        CK(cudaMemcpyAsync(Msel_d, Msel.data(), Msel.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(Msel_d + (size_t)b * m, addc.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(Msel_d + (size_t)b * m + m, theta_out.data(), m * sizeof(double), cudaMemcpyHostToDevice,
+                           st));
+        const bool vdev = V && is_device_ptr(V), zdev = Z && is_device_ptr(Z);
+        const size_t vbytes = (size_t)n * m * sizeof(float);
+        float* Vd = vdev ? V : (h->vtmp.ensure(vbytes), h->vtmp.as<float>());
+        float* Zd = zdev ? Z : (Z ? (h->ztmp.ensure(vbytes), h->ztmp.as<float>()) : nullptr);
+        const int grid = (int)std::min<int64_t>(4 * 148, (n * m + 255) / 256);
+        const double* theta = Msel_d + (size_t)b * m + m;
+        launch(k_rotate, dim3(grid), dim3(256), 0, st, n, b, m, m, (const float*)X, (const double*)Msel_d, Vd,
+               (const double*)(Msel_d + (size_t)b * m));
+        h->sign.ensure(kMaxB * sizeof(float));
+        h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
+        h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
+        launch(k_col_argmax, dim3(kRedBlocks), dim3(256), 0, st, n, m, (const float*)Vd, h->apval.as<float>(),
+               h->apidx.as<long long>(), h->sign.as<float>(), h->counters.as<unsigned int>() + CNT_ARGMAX);
+        launch(k_finalize, dim3(grid), dim3(256), 0, st, n, m, (const float*)h->sign.as<float>(), theta, Vd, Zd);
+        // orthogonality of the returned V (fp64 Gram)
+        gram(h, m, Vd, nullptr, st);
+        std::vector<double> gv((size_t)m * m);
+        CK(cudaMemcpyAsync(gv.data(), h->G.p, gv.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (V && !vdev) CK(cudaMemcpyAsync(V, Vd, vbytes, cudaMemcpyDeviceToHost, st));
+        if (Z && !zdev) CK(cudaMemcpyAsync(Z, Zd, vbytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(e1, st));
+        CK(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        double orth = 0.0;
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j) orth = std::max(orth, std::fabs(gv[i * m + j] - (i == j ? 1.0 : 0.0)));
+        int n_neg = 0;
+        for (int j = 0; j < m; ++j) {
+            eigvals[j] = theta_out[j];
+            if (theta_out[j] < 0.0) ++n_neg;
+        }
+        if (info) {
+            info->iters = it;
+            info->n_applies = it;
+            info->n_negative = n_neg;
+            info->converged = converged ? 1 : 0;
+            info->max_residual = rr_host.maxres;
+            info->orth_error = orth;
+            info->gpu_ms = ms;
+        }
+        if (tol > 0.0 && !converged) ret = fail(SBMDS_ENOCONV, "no convergence in %d iterations (residual %g)",
+                                                max_iters, rr_host.maxres);
+    } catch (const CudaError& e) {
+        if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
+        return fail(SBMDS_ECUDA, "%s: %s", e.what, cudaGetErrorString(e.e));
+    }
+    return ret;
+}
+
+// ============================================================================ options / stats
+extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t value) {
+    if (!h || !key) return fail(SBMDS_EINVAL, "NULL handle or key");
+    if (!strcmp(key, "rr_period")) {
+        if (value < 1) return fail(SBMDS_EINVAL, "rr_period >= 1");
+        h->rr_period = (int)value;
+    } else if (!strcmp(key, "use_graph")) {
+        h->use_graph = value ? 1 : 0;
+    } else if (!strcmp(key, "order_columns")) {
+        h->order_columns = value ? 1 : 0;
+    } else if (!strcmp(key, "profile")) {
+        h->prof.mask = (uint32_t)value;
+    } else if (!strcmp(key, "profile_reset")) {
+        DevGuard g(h->dev);
+        h->prof.drain();
+        for (int k = 0; k < PK_N; ++k) { h->prof.ns[k] = 0; h->prof.cnt[k] = 0; }
+    } else if (!strcmp(key, "dstream")) {
+        if (value < 0 || value > 1) return fail(SBMDS_EINVAL, "dstream in {0, 1}");
+        h->dstream = (int)value;
+    } else {
+        return fail(SBMDS_EINVAL, "unknown option '%s'", key);
+    }
+    return SBMDS_OK;
+}
+
+extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* value) {
+    if (!h || !key || !value) return fail(SBMDS_EINVAL, "NULL argument");
+    if (!strcmp(key, "n")) *value = h->n;
+    else if (!strcmp(key, "l")) *value = h->l;
+    else if (!strcmp(key, "nnz")) *value = h->nnz;
+    else if (!strcmp(key, "rowsum_dev_e9")) *value = (int64_t)std::llround(h->rowsum_dev * 1e9);
+    else if (!strcmp(key, "d_borrowed")) *value = h->d_borrowed ? 1 : 0;
+    else if (!strcmp(key, "csc_bytes")) *value = (int64_t)(h->cptr.bytes + h->ridx.bytes + h->cval.bytes);
+    else if (!strcmp(key, "workspace_bytes"))
+        *value = (int64_t)(h->Y1.bytes + h->Y2.bytes + h->P.bytes + h->X.bytes + h->Y.bytes + h->gpart.bytes);
+    else {
+        for (int k = 0; k < PK_N; ++k) {
+            const std::string nm(kProfNames[k]);
+            if (key == nm + "_ns" || key == nm + "_launches") {
+                DevGuard g(h->dev);
+                h->prof.drain();
+                *value = (key == nm + "_ns") ? (int64_t)std::llround(h->prof.ns[k]) : h->prof.cnt[k];
+                return SBMDS_OK;
+            }
+        }
+        return fail(SBMDS_EINVAL, "unknown stat '%s'", key);
+    }
+    return SBMDS_OK;
+}

@@ -1,0 +1,144 @@
+"""Python binding of libsbmds (include/sbmds.h): argument marshalling only.
+
+Every step of the operator and of the eigensolver runs in the CUDA library; this
+module turns torch tensors / numpy arrays into pointers and a stream handle.
+torch CUDA tensors are passed as device pointers (asynchronous on the current
+stream); numpy arrays and CPU tensors are passed as host pointers (the library
+stages them and synchronises).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+from ._lib import SBMDS_BORROW_D, SBMDS_ENOCONV, SBMDS_VALIDATE, SbmdsError, SbmdsInfo, check, lib
+
+try:
+    import torch
+except Exception:  # pragma: no cover - torch is in the image
+    torch = None
+
+
+def _is_torch(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _ptr(x, dtype) -> int:
+    """Pointer to a contiguous buffer of `dtype` (torch tensor or numpy array)."""
+    if _is_torch(x):
+        want = {np.float32: torch.float32, np.int32: torch.int32, np.int64: torch.int64}[dtype]
+        if x.dtype != want or not x.is_contiguous():
+            raise TypeError(f"expected a contiguous {want} tensor, got {x.dtype}")
+        return x.data_ptr()
+    if not isinstance(x, np.ndarray) or x.dtype != dtype or not x.flags.c_contiguous:
+        raise TypeError(f"expected a C-contiguous numpy {np.dtype(dtype)} array")
+    return x.ctypes.data
+
+
+def _stream(stream) -> int:
+    if stream is not None:
+        return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+    if torch is not None and torch.cuda.is_available():
+        return int(torch.cuda.current_stream().cuda_stream)
+    return 0
+
+
+def launch_count() -> int:
+    """Kernels libsbmds has launched in this process (bench.py's gpu_launches)."""
+    return int(lib().sbmds_launch_count())
+
+
+class Sbmds:
+    """Handle over S (n x l CSR) and D_ll (l x l, symmetric squared landmark distances).
+
+    Mirrors sbmds_create / sbmds_apply / sbmds_eigs / sbmds_destroy.
+    """
+
+    def __init__(self, n: int, l: int, row_ptr, col_idx, val, D, *, validate: bool = False,
+                 borrow_d: bool = False, stream=None):
+        self.n, self.l = int(n), int(l)
+        nnz = int(row_ptr[-1])
+        flags = (SBMDS_VALIDATE if validate else 0) | (SBMDS_BORROW_D if borrow_d else 0)
+        self._keep = (row_ptr, col_idx, val, D) if borrow_d else ()
+        h = ctypes.c_void_p()
+        check(lib().sbmds_create(self.n, self.l, nnz, _ptr(row_ptr, np.int64),
+                                 _ptr(col_idx, np.int32), _ptr(val, np.float32), _ptr(D, np.float32),
+                                 flags, _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    # -- lifecycle ---------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sbmds_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- calls -------------------------------------------------------------------------
+    def apply(self, X, out=None, stream=None):
+        """Y = -1/2 J S D S^T J X for an n x b block (b <= 64)."""
+        if X.ndim != 2 or X.shape[0] != self.n:
+            raise ValueError(f"X must be n x b with n={self.n}")
+        b = int(X.shape[1])
+        if out is None:
+            out = torch.empty_like(X) if _is_torch(X) else np.empty_like(X)
+        check(lib().sbmds_apply(self._h, b, _ptr(X, np.float32), _ptr(out, np.float32),
+                                _stream(stream)))
+        return out
+
+    def eigs(self, m: int, block: int, max_iters: int = 500, tol: float = 1e-5, seed: int = 0,
+             X0=None, V=None, Z=None, device: str = "cuda", stream=None, raise_noconv=False):
+        """Top-m eigenpairs of B~ and Z = V_m Λ_m^{1/2}. Returns (eigvals, V, Z, info)."""
+        if V is None:
+            V = (torch.empty((self.n, m), dtype=torch.float32, device=device)
+                 if device != "numpy" else np.empty((self.n, m), dtype=np.float32))
+        if Z is None:
+            Z = (torch.empty((self.n, m), dtype=torch.float32, device=device)
+                 if device != "numpy" else np.empty((self.n, m), dtype=np.float32))
+        ev = np.zeros(m, dtype=np.float64)
+        info = SbmdsInfo()
+        x0 = _ptr(X0, np.float32) if X0 is not None else None
+        st = lib().sbmds_eigs(self._h, int(m), int(block), int(max_iters), float(tol), int(seed),
+                              x0, ev.ctypes.data, _ptr(V, np.float32), _ptr(Z, np.float32),
+                              ctypes.byref(info), _stream(stream))
+        if st == SBMDS_ENOCONV and not raise_noconv:
+            pass
+        else:
+            check(st)
+        d = {k: getattr(info, k) for k, _ in SbmdsInfo._fields_}
+        d["status"] = int(st)
+        return ev, V, Z, d
+
+    def set_option(self, key: str, value: int):
+        check(lib().sbmds_set_option(self._h, key.encode(), int(value)))
+
+    def stat(self, key: str) -> int:
+        v = ctypes.c_int64()
+        check(lib().sbmds_get_stat(self._h, key.encode(), ctypes.byref(v)))
+        return int(v.value)
+
+
+def from_problem(p, device: Optional[str] = "cuda", **kw) -> Sbmds:
+    """Convenience: build a handle from a gen.configs.Problem (host or device upload)."""
+    rp = np.ascontiguousarray(p.row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(p.col_idx, dtype=np.int32)
+    vv = np.ascontiguousarray(p.val, dtype=np.float32)
+    D = np.ascontiguousarray(p.D, dtype=np.float32)
+    if device and device != "numpy":
+        rp, ci, vv, D = (torch.from_numpy(a).to(device) for a in (rp, ci, vv, D))
+    return Sbmds(p.n, p.l, rp, ci, vv, D, **kw)
+
+
+__all__ = ["Sbmds", "SbmdsError", "from_problem", "launch_count"]

@@ -1,0 +1,171 @@
+"""GPU parity: sbmds_apply (CUDA, through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerance (BASELINE.json north_star): relative Frobenius error <= 1e-5 in fp32.
+Inputs are the seeded generators of gen/ (configs 1, 2, shrunken 3/5 shapes) plus
+edge cases: ragged l, empty columns, negative / non-normalised S, duplicates, b in 1..64.
+"""
+import numpy as np
+import pytest
+
+from gen import configs
+from oracle import sbmds_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def make_handle(p, **kw):
+    from paper_1705_10887_b200 import from_problem
+    return from_problem(p, **kw)
+
+
+def relerr(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def run_apply(h, X):
+    torch = _torch()
+    Xt = torch.from_numpy(X).cuda()
+    Y = h.apply(Xt)
+    torch.cuda.synchronize()
+    return Y.cpu().numpy()
+
+
+def oracle_apply(p, X):
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())  # the fp32 values the ABI receives
+    return O.apply(S, p.D, X.astype(np.float64))
+
+
+def synth_problem(n, l, k, seed, negative=False, rowsum_one=True, empty_cols=0, dup=False):
+    """Random CSR S (variable row lengths 1..k), symmetric D; not a paper workload — edge cases."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(1, k + 1, size=n)
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    row_ptr[1:] = np.cumsum(lens)
+    usable = l - empty_cols
+    cols = np.concatenate([np.sort(rng.choice(usable, size=c, replace=dup)) for c in lens]).astype(np.int32)
+    vals = rng.uniform(0.05, 1.0, size=row_ptr[-1])
+    if negative:
+        vals *= np.where(rng.random(row_ptr[-1]) < 0.3, -1.0, 1.0)
+    if rowsum_one:
+        sums = np.add.reduceat(vals, row_ptr[:-1])
+        vals = vals / np.repeat(sums, lens)
+    A = rng.uniform(0, 100, size=(l, l)).astype(np.float32)
+    D = np.ascontiguousarray((A + A.T) / 2)
+    p = configs.Problem("synth", n, l, row_ptr, cols, vals, D)
+    return p
+
+
+@pytest.mark.parametrize("b", [8, 1, 3, 16, 64])
+def test_apply_config1(b):
+    p = configs.config(1)
+    X = configs.x_block(p.n, b, seed=b)
+    with make_handle(p) as h:
+        Y = run_apply(h, X)
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
+
+
+@pytest.mark.parametrize("b", [16, 4, 1, 5])
+def test_apply_config2(b):
+    p = configs.config(2)
+    X = configs.x_block(p.n, b, seed=b)
+    with make_handle(p) as h:
+        Y = run_apply(h, X)
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
+
+
+@pytest.mark.parametrize("k,b", [(8, 1), (16, 4), (16, 16), (64, 64), (8, 32), (16, 2)])
+def test_apply_random_structure(k, b):
+    """Config-5 recipe at a size the oracle finishes in seconds (several tiles + ragged tail)."""
+    p = configs.random_problem(60_001, 2_003, k, seed=k + b, name="cfg5_small")
+    X = configs.x_block(p.n, b, seed=7)
+    with make_handle(p) as h:
+        Y = run_apply(h, X)
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
+
+
+@pytest.mark.parametrize("case", ["negative", "not_normalised", "empty_cols", "duplicates", "l_ragged"])
+def test_apply_edge_cases(case):
+    kw = dict(n=5000, l=333, k=12, seed=11)
+    if case == "negative":
+        p = synth_problem(**kw, negative=True)
+    elif case == "not_normalised":
+        p = synth_problem(**kw, rowsum_one=False)
+    elif case == "empty_cols":
+        p = synth_problem(**kw, empty_cols=40)
+    elif case == "duplicates":
+        p = synth_problem(**kw, dup=True)
+    else:
+        p = synth_problem(n=3001, l=1029, k=9, seed=3)
+    for b in (1, 4, 7, 16):
+        X = configs.x_block(p.n, b, seed=b)
+        with make_handle(p) as h:
+            Y = run_apply(h, X)
+        assert relerr(Y, oracle_apply(p, X)) <= TOL, (case, b)
+
+
+def test_apply_invariants_and_determinism():
+    """Columns of B~X sum to 0; X1^T(B~X2) = (B~X1)^T X2 (CSR vs CSC); B~1 = 0; bitwise repeatable."""
+    p = configs.config(2)
+    X1 = configs.x_block(p.n, 16, seed=1)
+    X2 = configs.x_block(p.n, 16, seed=2)
+    with make_handle(p) as h:
+        Y1 = run_apply(h, X1)
+        Y2 = run_apply(h, X2)
+        Y1b = run_apply(h, X1)
+        ones = np.ones((p.n, 4), dtype=np.float32)
+        Y0 = run_apply(h, ones)
+    scale = np.abs(Y1).max()
+    assert np.abs(Y1.astype(np.float64).sum(0)).max() <= 1e-5 * scale * np.sqrt(p.n)
+    a = X1.astype(np.float64).T @ Y2.astype(np.float64)
+    bm = Y1.astype(np.float64).T @ X2.astype(np.float64)
+    assert np.abs(a - bm).max() <= 1e-5 * np.abs(a).max()
+    assert np.abs(Y0).max() <= 1e-5 * scale
+    assert np.array_equal(Y1, Y1b)
+
+
+def test_apply_host_buffers_match_device():
+    """The C ABI accepts host pointers (numpy) and stages them itself."""
+    p = configs.config(1)
+    X = configs.x_block(p.n, 8, seed=3)
+    from paper_1705_10887_b200 import from_problem
+    with from_problem(p, device="numpy") as hh, make_handle(p) as hd:
+        Yh = hh.apply(X)
+        Yd = run_apply(hd, X)
+    assert np.array_equal(Yh, Yd)
+
+
+def test_apply_column_of_operator():
+    """B~ e_j equals column j of the dense oracle operator (SPEC.md:432 style)."""
+    p = configs.config(1)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    B = O.dense_operator(S, p.D)
+    E = np.zeros((p.n, 4), dtype=np.float32)
+    idx = [0, 17, 999, 1999]
+    E[idx, range(4)] = 1.0
+    with make_handle(p) as h:
+        Y = run_apply(h, E)
+    assert relerr(Y, B[:, idx]) <= TOL
+
+
+def test_errors_are_reported():
+    from paper_1705_10887_b200 import Sbmds, SbmdsError
+    p = configs.config(1)
+    with make_handle(p) as h:
+        torch = _torch()
+        X = torch.zeros((p.n, 65), device="cuda")
+        with pytest.raises(SbmdsError):
+            h.apply(X)
+    bad = p.col_idx.copy()
+    bad[5] = p.l
+    with pytest.raises(SbmdsError, match="EINVAL"):
+        Sbmds(p.n, p.l, p.row_ptr, bad, p.val32(), p.D)
+    Dn = p.D.copy()
+    Dn[0, 1] += 1.0
+    with pytest.raises(SbmdsError, match="symmetric"):
+        Sbmds(p.n, p.l, p.row_ptr, p.col_idx, p.val32(), Dn, validate=True)

@@ -1,0 +1,119 @@
+"""GPU parity: sbmds_eigs (block subspace iteration, CUDA) vs the fp64 oracle.
+
+Tolerances (BASELINE.json north_star): eigenvalues relative error <= 1e-4; embedding
+principal subspace angle <= 1e-3 rad. Subspaces are compared only across a spectral
+gap (reading R4); Z is compared through Z Z^T (rigid-motion invariant).
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from gen import configs
+from oracle import sbmds_oracle as O
+
+pytestmark = pytest.mark.gpu
+EIG_TOL, ANGLE_TOL = 1e-4, 1e-3
+
+
+def handle(p, **kw):
+    from paper_1705_10887_b200 import from_problem
+    return from_problem(p, **kw)
+
+
+def gpu_eigs(h, m, block, **kw):
+    lam, V, Z, info = h.eigs(m, block, **kw)
+    return lam, V.cpu().numpy().astype(np.float64), Z.cpu().numpy().astype(np.float64), info
+
+
+def check_against(lam, V, Z, lam_o, V_o, Z_o):
+    assert np.all(np.abs(lam - lam_o) <= EIG_TOL * np.abs(lam_o)), (lam, lam_o)
+    assert O.principal_angle(V, V_o) <= ANGLE_TOL
+    # orthonormal columns, canonical signs (largest |v_i| positive)
+    assert np.abs(V.T @ V - np.eye(V.shape[1])).max() < 1e-5
+    for j in range(V.shape[1]):
+        i = np.argmax(np.abs(V[:, j]))
+        assert V[i, j] > 0
+    assert np.allclose(Z, V * np.sqrt(np.maximum(lam, 0))[None, :], rtol=1e-5, atol=1e-7)
+
+
+def test_eigs_config1_vs_dense():
+    p = configs.config(1)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    lam_o, V_o, Z_o = O.eigs_dense(S, p.D, p.m)
+    with handle(p) as h:
+        lam, V, Z, info = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6)
+    assert info["status"] == 0 and info["converged"] == 1
+    check_against(lam, V, Z, lam_o, V_o, Z_o)
+    assert np.allclose(Z @ Z.T, Z_o @ Z_o.T, atol=1e-4 * lam_o[0])
+
+
+def test_eigs_config2_vs_lanczos():
+    p = configs.config(2)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, p.m)
+    with handle(p) as h:
+        lam, V, Z, info = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6)
+    check_against(lam, V, Z, lam_o, V_o, Z_o)
+
+
+def test_eigs_cf2_exact_rank3_at_config2_shape():
+    """CF2 at n = 100,000: S of config 2 (rows sum to 1), D = squared distances of landmark
+    points y ~ N(0, diag(9,4,1)) => eigenpairs are the SVD of J S Y (no eigensolver needed)."""
+    p = configs.config(2)
+    rng = np.random.default_rng(5)
+    Yl = rng.standard_normal((p.l, 3)) * [3.0, 2.0, 1.0]
+    D = ((Yl[:, None, :] - Yl[None, :, :]) ** 2).sum(-1).astype(np.float32)
+    q = configs.Problem("cf2", p.n, p.l, p.row_ptr, p.col_idx, p.val, D)
+    S = O.csr(q.n, q.l, q.row_ptr, q.col_idx, q.val32())
+    JSY = S @ Yl
+    JSY -= JSY.mean(0)
+    U, s, _ = np.linalg.svd(JSY, full_matrices=False)
+    with handle(q) as h:
+        lam, V, Z, info = gpu_eigs(h, 3, 8, max_iters=200, tol=1e-6)
+    assert np.all(np.abs(lam - s ** 2) <= EIG_TOL * s ** 2)
+    assert O.principal_angle(V, U) <= ANGLE_TOL
+
+
+def test_eigs_negative_top_m_zeroed():
+    """CF3 circle (S = I): the top-m algebraic set reaches negative eigenvalues; their Z
+    columns are zero and info counts them."""
+    N, rho = 40, 1.0
+    th = 2 * np.pi * np.arange(N) / N
+    diff = np.angle(np.exp(1j * (th[:, None] - th[None, :])))
+    D = ((rho * diff) ** 2).astype(np.float32)
+    rp = np.arange(N + 1, dtype=np.int64)
+    ci = np.arange(N, dtype=np.int32)
+    p = configs.Problem("circle", N, N, rp, ci, np.ones(N), D)
+    lam_all = np.sort(np.linalg.eigvalsh(O.dense_operator(sp.identity(N, format="csr"), D.astype(np.float64))))[::-1]
+    m = 24
+    assert lam_all[m - 1] < 0
+    with handle(p) as h:
+        lam, V, Z, info = gpu_eigs(h, m, 39, max_iters=3000, tol=1e-7)
+    assert np.allclose(lam, lam_all[:m], rtol=1e-4, atol=1e-6 * abs(lam_all[0]))
+    neg = lam < 0
+    assert info["n_negative"] == int(neg.sum())
+    assert np.all(Z[:, neg] == 0)
+
+
+def test_eigs_fixed_iterations_and_warm_start():
+    p = configs.config(1)
+    with handle(p) as h:
+        lam, V, Z, info = gpu_eigs(h, p.m, p.block, max_iters=7, tol=0.0)
+        assert info["status"] == 0 and info["iters"] == 7
+        import torch
+        X0 = torch.zeros((p.n, p.block), device="cuda")
+        X0[:, :3] = torch.from_numpy(V.astype(np.float32)).cuda()
+        X0[:, 3:] = torch.randn((p.n, p.block - 3), device="cuda", generator=torch.Generator("cuda").manual_seed(0))
+        lam2, V2, _, info2 = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6, X0=X0)
+        lam3, V3, _, _ = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6, X0=X0)
+    assert info2["converged"] == 1
+    assert np.array_equal(lam2, lam3) and np.array_equal(V2, V3)   # deterministic
+
+
+def test_eigs_host_outputs():
+    p = configs.config(1)
+    with handle(p) as h:
+        lam, V, Z, info = h.eigs(p.m, p.block, tol=1e-6, device="numpy")
+        lam_d, V_d, Z_d, _ = gpu_eigs(h, p.m, p.block, tol=1e-6)
+    assert np.array_equal(lam, lam_d)
+    assert np.array_equal(V, V_d.astype(np.float32))
