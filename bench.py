@@ -68,6 +68,7 @@ def barrier(ws):
 
 
 def max_over_ranks(x: float, ws: int, device=None) -> float:
+    """Max of a per-rank device time over all ranks (the slowest replica sets the pace)."""
     if ws == 1:
         return x
     import torch
@@ -75,6 +76,11 @@ def max_over_ranks(x: float, ws: int, device=None) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def job_throughput(ws: int, units_per_rank: float, seconds_max: float) -> float:
+    """Whole-job value: the units all ranks processed / the max-over-ranks time."""
+    return ws * units_per_rank / seconds_max
 
 
 def load_problem(cfg: int, ws: int, rank: int):
@@ -146,7 +152,8 @@ def algorithmic_bytes(p, b):
 
 
 def dstream_bytes(p, b):
-    """Dominant kernel (k_dstream_ffma): D read once + Y1 read + Y2 partials written."""
+    """Dominant kernel (k_dstream_tc / k_dstream_ffma): D read once (4 l^2) + Y1 read + Y2 partials
+    written (12 l b) — DESIGN.md §4."""
     return 4 * p.l * p.l + 4 * p.l * b + 8 * p.l * b
 
 
@@ -190,7 +197,7 @@ def run_ours(args, ws, rank, local):
     h.set_option("profile", 0)
     ms_max = max_over_ranks(ms, ws, device="cuda")
     applies = sum(i["n_applies"] for i in infos)
-    value = ws * applies / (ms_max / 1e3)
+    value = job_throughput(ws, applies, ms_max / 1e3)
     ds_avg_s = ds_ns / max(ds_n, 1) / 1e9
     ds_gbs = dstream_bytes(p, b) / ds_avg_s / 1e9
     apply_gbs = algorithmic_bytes(p, b) * applies / (ms / 1e3) / 1e9
@@ -225,7 +232,7 @@ def run_ours(args, ws, rank, local):
         t_e2e = max_over_ranks(float(np.mean(times)), ws, device="cuda")
         h2d = p.D.nbytes + 8 * (p.n + 1) + 12 * p.nnz
         d2h = 8 * m + 2 * p.n * m * 4
-        e2e = {"value": ws * iters / t_e2e, "unit": UNIT, "seconds_per_solve": t_e2e,
+        e2e = {"value": job_throughput(ws, iters, t_e2e), "unit": UNIT, "seconds_per_solve": t_e2e,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "includes": "sbmds_create from pinned host CSR + D (H2D, CSC build) + sbmds_eigs "
                            "(50 iters) + V, Z, eigenvalues to host + destroy"}
@@ -248,7 +255,8 @@ def run_ours(args, ws, rank, local):
         "max_residual": info["max_residual"], "orth_error": info["orth_error"],
         "roofline": {"bound": "hbm", "achieved": ds_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": ds_gbs / hbm_peak, "traffic": load_traffic(),
-                     "kernel": "k_dstream_ffma", "launches": ds_n,
+                     "kernel": "k_dstream_tc<16> (tcgen05 3xTF32)" if b >= 5 else "k_dstream_ffma",
+                     "launches": ds_n,
                      "avg_launch_ms": ds_avg_s * 1e3, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": dstream_bytes(p, b)},
         "gpu_launches": int(n_launch),

@@ -84,12 +84,11 @@ __global__ void __launch_bounds__(DsCfg<BP>::THREADS, 1)
         if (lane == 0) {
             prefetch_tensormap(&dmap);
             const uint64_t pol = policy_evict_first();
+            int s = 0;
+            uint32_t ph = 0;
+            int64_t rt = it0 / sk.KT, kt = it0 % sk.KT;
             for (int64_t it = it0; it < it1; ++it) {
-                const int64_t li = it - it0;
-                const int s = (int)(li % C::NS);
-                const uint32_t ph = (uint32_t)((li / C::NS) & 1);
                 mbar_wait(&empty[s], ph ^ 1u);
-                const int64_t rt = it / sk.KT, kt = it % sk.KT;
                 uint8_t* st = base + s * C::STAGE_BYTES;
                 mbar_arrive_expect_tx(&full[s], C::D_BYTES + C::Y_BYTES);
 #pragma unroll
@@ -97,6 +96,8 @@ __global__ void __launch_bounds__(DsCfg<BP>::THREADS, 1)
                     tma_load_2d(st + q * C::BOXW * C::BK * 4, &dmap, &full[s],
                                 (int32_t)(rt * C::TM + q * C::BOXW), (int32_t)(kt * C::BK), pol);
                 bulk_load(st + C::D_BYTES, Y1 + kt * C::BK * BP, C::Y_BYTES, &full[s]);
+                if (++s == C::NS) { s = 0; ph ^= 1u; }
+                if (++kt == sk.KT) { kt = 0; ++rt; }
             }
         }
         return;
@@ -115,11 +116,11 @@ __global__ void __launch_bounds__(DsCfg<BP>::THREADS, 1)
 #pragma unroll
         for (int q = 0; q < C::CN; ++q) acc2[r][q] = 0.0;
 
-    int64_t cur_rt = it0 < it1 ? it0 / sk.KT : -1;
+    int s = 0;
+    uint32_t ph = 0;
+    int64_t rt = it0 / sk.KT, kt = it0 % sk.KT;
+    int seg = c - sk.cta_of(rt * sk.KT);
     for (int64_t it = it0; it < it1; ++it) {
-        const int64_t li = it - it0;
-        const int s = (int)(li % C::NS);
-        const uint32_t ph = (uint32_t)((li / C::NS) & 1);
         mbar_wait(&full[s], ph);
         const uint8_t* st = base + s * C::STAGE_BYTES;
         const float* Ds = reinterpret_cast<const float*>(st + box * C::BOXW * C::BK * 4) + col_in_box;
@@ -160,10 +161,8 @@ __global__ void __launch_bounds__(DsCfg<BP>::THREADS, 1)
 #pragma unroll
             for (int q = 0; q < C::CN; ++q) acc2[r][q] += (double)acc[r][q];
 
-        const int64_t rt = it / sk.KT;
-        const bool last_of_tile = (it + 1 == it1) || ((it + 1) / sk.KT != rt);
+        const bool last_of_tile = (it + 1 == it1) || (kt + 1 == sk.KT);
         if (last_of_tile) {
-            const int seg = c - sk.cta_of(rt * sk.KT);
             double* out = P + ((rt * maxseg + seg) * (int64_t)C::TM + row_in_tile) * BP + lj * C::CN;
 #pragma unroll
             for (int r = 0; r < C::RM; ++r) {
@@ -173,10 +172,10 @@ __global__ void __launch_bounds__(DsCfg<BP>::THREADS, 1)
                     acc2[r][q] = 0.0;
                 }
             }
-            cur_rt = rt + 1;
         }
+        if (++s == C::NS) { s = 0; ph ^= 1u; }
+        if (++kt == sk.KT) { kt = 0; ++rt; seg = 0; }
     }
-    (void)cur_rt;
 }
 
 // Sum the stream-K partials of each row tile in CTA order -> Y2 (l x BP fp32), and

@@ -15,60 +15,97 @@
 namespace sbmds {
 
 // ------------------------------------------------------------------ E2: tall-skinny Gram
-// Rows are cut into gridDim.x contiguous ranges; each block stages 32-row tiles of Y (and
-// X) in shared memory and accumulates its share of the b*b products in fp64 (the fp32
-// products are exact in fp64). Partials are summed in block order by the last block.
+// Rows are cut into gridDim.x contiguous ranges. A block stages 64-row tiles of Y (and X)
+// in shared memory as fp64 (fp32 -> fp64 is exact, so every product is exact) and splits
+// the b4 x b4 output (b4 = b rounded up to 4) into 4x4 micro-tiles; the 256 threads are
+// (micro-tile, row-group) pairs, each accumulating 16 (or 32 with H) fp64 FMAs per row.
+// Row-group partials are summed in fixed order, then the last block sums the block
+// partials in block order: bitwise deterministic.
 template <bool WITH_H>
 __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __restrict__ Y,
                                               const float* __restrict__ X, double* __restrict__ part,
                                               double* __restrict__ G, double* __restrict__ H,
                                               unsigned int* __restrict__ counter) {
-    constexpr int TR = 32;
-    constexpr int PPT = (kMaxB * kMaxB) / 256;  // max pairs per thread (16)
-    __shared__ float Ys[TR * kMaxB];
-    __shared__ float Xs[WITH_H ? TR * kMaxB : 1];
+    constexpr int TR = 64;
+    extern __shared__ double gsm[];
+    const int b4 = (b + 3) & ~3;
+    const int nt = b4 / 4;                 // micro-tiles per side
+    const int ntiles = nt * nt;            // <= 256
+    const int groups = 256 / ntiles;       // row groups (>= 1)
+    double* Ys = gsm;                      // [TR][b4]
+    double* Xs = gsm + TR * b4;            // [TR][b4] (WITH_H)
     const int tid = threadIdx.x;
-    const int bb = b * b;
-    double g[PPT], h[PPT];
+    const int tile = tid % ntiles, grp = tid / ntiles;
+    const int ti = tile / nt, tj = tile % nt;
+    const bool active = grp < groups;
+    double g[4][4], h[4][4];
 #pragma unroll
-    for (int u = 0; u < PPT; ++u) g[u] = h[u] = 0.0;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) g[i][j] = h[i][j] = 0.0;
     const int64_t rows_per_blk = (n + gridDim.x - 1) / gridDim.x;
     const int64_t beg = blockIdx.x * rows_per_blk, end = min(n, beg + rows_per_blk);
     for (int64_t r0 = beg; r0 < end; r0 += TR) {
         const int rows = (int)((end - r0) < TR ? (end - r0) : TR);
         __syncthreads();
-        for (int e = tid; e < rows * b; e += 256) {
-            Ys[e] = Y[r0 * b + e];
-            if constexpr (WITH_H) Xs[e] = X[r0 * b + e];
+        for (int e = tid; e < TR * b4; e += 256) {
+            const int r = e / b4, c = e % b4;
+            const bool ok = r < rows && c < b;
+            Ys[e] = ok ? (double)Y[(r0 + r) * b + c] : 0.0;
+            if constexpr (WITH_H) Xs[e] = ok ? (double)X[(r0 + r) * b + c] : 0.0;
         }
         __syncthreads();
+        if (active) {
+            for (int r = grp; r < rows; r += groups) {
+                const double* yr = Ys + r * b4;
+                double a[4], c[4];
 #pragma unroll
-        for (int u = 0; u < PPT; ++u) {
-            const int pq = tid + u * 256;
-            if (pq < bb) {
-                const int p = pq / b, q = pq % b;
-                double a = g[u], ah = h[u];
-                for (int r = 0; r < rows; ++r) {
-                    const double yq = (double)Ys[r * b + q];
-                    a = fma((double)Ys[r * b + p], yq, a);
-                    if constexpr (WITH_H) ah = fma((double)Xs[r * b + p], yq, ah);
+                for (int i = 0; i < 4; ++i) { a[i] = yr[4 * ti + i]; c[i] = yr[4 * tj + i]; }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) g[i][j] = fma(a[i], c[j], g[i][j]);
+                if constexpr (WITH_H) {
+                    const double* xr = Xs + r * b4;
+                    double xa[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xa[i] = xr[4 * ti + i];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) h[i][j] = fma(xa[i], c[j], h[i][j]);
                 }
-                g[u] = a;
-                h[u] = ah;
             }
         }
     }
-    double* pg = part + (int64_t)blockIdx.x * (2 * kMaxB * kMaxB);
+    // reduce the row groups in fixed order through shared memory
+    __syncthreads();
+    double* red = gsm;  // [groups][b4*b4] (+ same for H)
+    const int bb4 = b4 * b4;
+    if (active) {
 #pragma unroll
-    for (int u = 0; u < PPT; ++u) {
-        const int pq = tid + u * 256;
-        if (pq < bb) {
-            pg[pq] = g[u];
-            if constexpr (WITH_H) pg[kMaxB * kMaxB + pq] = h[u];
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int pq = (4 * ti + i) * b4 + 4 * tj + j;
+                red[grp * bb4 + pq] = g[i][j];
+                if constexpr (WITH_H) red[(groups + grp) * bb4 + pq] = h[i][j];
+            }
+    }
+    __syncthreads();
+    double* pg = part + (int64_t)blockIdx.x * (2 * kMaxB * kMaxB);
+    for (int pq = tid; pq < b * b; pq += 256) {
+        const int p = pq / b, q = pq % b, e = p * b4 + q;
+        double a = 0.0, ah = 0.0;
+        for (int k = 0; k < groups; ++k) {
+            a += red[k * bb4 + e];
+            if constexpr (WITH_H) ah += red[(groups + k) * bb4 + e];
         }
+        pg[pq] = a;
+        if constexpr (WITH_H) pg[kMaxB * kMaxB + pq] = ah;
     }
     if (last_block_done(counter)) {
-        for (int pq = tid; pq < bb; pq += 256) {
+        for (int pq = tid; pq < b * b; pq += 256) {
             double a = 0.0, ah = 0.0;
             for (unsigned int q = 0; q < gridDim.x; ++q) {
                 const double* pp = part + (int64_t)q * (2 * kMaxB * kMaxB);
@@ -80,6 +117,13 @@ __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __r
         }
         if (tid == 0) *counter = 0;
     }
+}
+// dynamic smem: max(2 tiles of TR x b4, 2*groups*b4^2) doubles
+inline size_t gram_smem_bytes(int b) {
+    const int b4 = (b + 3) & ~3;
+    const int nt = b4 / 4, groups = 256 / (nt * nt);
+    const size_t a = (size_t)2 * 64 * b4, c = (size_t)2 * groups * b4 * b4;
+    return (a > c ? a : c) * sizeof(double);
 }
 
 // ------------------------------------------------------------------ E3: Cholesky + R^-1
@@ -296,26 +340,87 @@ __global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const doub
 }
 
 // ------------------------------------------------------------------ E4/E6: out = in * M
-// in: n x b (row stride b), M: b x mo fp64 row-major (leading dim ldm), out: n x mo.
-// addc (optional, mo): a constant added to every entry of column c (the exact null
-// eigenvector 1/sqrt(n) of B~, "J 1 = 0", when it belongs to the top m).
+// in: n x b (row stride b, b <= BT), M: b x mo fp64 row-major (leading dim ldm), out: n x mo.
+// One thread per row, fp64 arithmetic in column chunks of 16; M is broadcast from shared
+// memory. addc (optional, mo): a constant added to column c (the exact null eigenvector
+// 1/sqrt(n) of B~, "J 1 = 0", when it belongs to the top m).
+// cs_part (optional): also produce s = 1^T out (fp64: warp sums -> per-warp smem rows ->
+// block partial -> last block, fixed order) = A1 of the next apply, so the eigs loop never
+// re-reads X for its column sums.
+template <int BT>
 __global__ void __launch_bounds__(256) k_rotate(int64_t n, int b, int mo, int ldm, const float* __restrict__ in,
                                                 const double* __restrict__ M, float* __restrict__ out,
-                                                const double* __restrict__ addc) {
+                                                const double* __restrict__ addc, double* __restrict__ cs_part,
+                                                double* __restrict__ cs_out, unsigned int* __restrict__ counter) {
     __shared__ double Ms[kMaxB * kMaxB];
     __shared__ double As[kMaxB];
+    __shared__ double red[8][kMaxB];
     for (int e = threadIdx.x; e < b * mo; e += blockDim.x) Ms[e] = M[(e / mo) * ldm + (e % mo)];
     for (int e = threadIdx.x; e < mo; e += blockDim.x) As[e] = addc ? addc[e] : 0.0;
+    for (int e = threadIdx.x; e < 8 * kMaxB; e += blockDim.x) (&red[0][0])[e] = 0.0;
     __syncthreads();
-    const int64_t total = n * mo;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / mo;
-        const int c = (int)(e % mo);
-        const float* row = in + i * b;
-        double acc = As[c];
-        for (int p = 0; p < b; ++p) acc = fma((double)__ldg(row + p), Ms[p * mo + c], acc);
-        out[e] = (float)acc;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool want_cs = cs_part != nullptr;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool act = i < n;
+        float y[BT];
+        const float* row = in + (act ? i : 0) * b;
+        if ((b & 3) == 0) {
+#pragma unroll
+            for (int p4 = 0; p4 < BT / 4; ++p4) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (act && 4 * p4 < b) v = __ldg(reinterpret_cast<const float4*>(row) + p4);
+                y[4 * p4] = v.x; y[4 * p4 + 1] = v.y; y[4 * p4 + 2] = v.z; y[4 * p4 + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < BT; ++p) y[p] = (act && p < b) ? __ldg(row + p) : 0.f;
+        }
+        for (int c0 = 0; c0 < mo; c0 += 16) {
+            double acc[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[c] = (c0 + c < mo) ? As[c0 + c] : 0.0;
+#pragma unroll
+            for (int p = 0; p < BT; ++p) {
+                if (p < b) {
+                    const double yp = (double)y[p];
+                    const double* mr = Ms + p * mo + c0;
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        if (c0 + c < mo) acc[c] = fma(yp, mr[c], acc[c]);
+                }
+            }
+            float* orow = out + i * mo + c0;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                float v = 0.f;
+                if (c0 + c < mo) {
+                    v = (float)acc[c];
+                    if (act) orow[c] = v;
+                }
+                if (want_cs && c0 + c < mo) {
+                    const double sv = warp_sum(act ? (double)v : 0.0);
+                    if (lane == 0) red[warp][c0 + c] += sv;
+                }
+            }
+        }
+    }
+    if (!want_cs) return;
+    __syncthreads();
+    if (threadIdx.x < mo) {
+        double v = 0.0;
+        for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+        cs_part[blockIdx.x * kMaxB + threadIdx.x] = v;
+    }
+    if (last_block_done(counter)) {
+        if (threadIdx.x < mo) {
+            double v = 0.0;
+            for (unsigned int q = 0; q < gridDim.x; ++q) v += cs_part[q * kMaxB + threadIdx.x];
+            cs_out[threadIdx.x] = v;
+        }
+        if (threadIdx.x == 0) *counter = 0;
     }
 }
 

@@ -17,6 +17,7 @@
 #include "../../include/sbmds.h"
 #include "common.cuh"
 #include "k_dstream.cuh"
+#include "k_dstream_tc.cuh"
 #include "k_small.cuh"
 #include "k_sparse.cuh"
 
@@ -125,8 +126,8 @@ EncodeFn get_encode() {
 // Per-kernel-family device timing with CUDA events recorded on the launching stream
 // (sbmds_set_option "profile" = bitmask of families; read back with sbmds_get_stat
 // "<family>_ns" / "<family>_launches"). Used by bench.py for the roofline line.
-enum { PK_COLSUM = 0, PK_CSC, PK_DSTREAM, PK_DREDUCE, PK_CSR, PK_GRAM, PK_CHOL, PK_ROTATE, PK_RR, PK_N };
-const char* const kProfNames[PK_N] = {"colsum", "csc", "dstream", "dreduce", "csr", "gram", "chol", "rotate", "rr"};
+enum { PK_COLSUM = 0, PK_CSC, PK_DSTREAM, PK_DREDUCE, PK_CSR, PK_GRAM, PK_CHOL, PK_ROTATE, PK_RR, PK_SPLIT, PK_N };
+const char* const kProfNames[PK_N] = {"colsum", "csc", "dstream", "dreduce", "csr", "gram", "chol", "rotate", "rr", "split"};
 
 struct Profiler {
     uint32_t mask = 0;
@@ -178,7 +179,7 @@ void profiled(Profiler& pr, int k, cudaStream_t st, F&& f) {
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs for the grid reductions
 constexpr int kCounters = 8;
-enum { CNT_COLSUM = 0, CNT_DRED = 1, CNT_GRAM = 2, CNT_ARGMAX = 3 };
+enum { CNT_COLSUM = 0, CNT_DRED = 1, CNT_GRAM = 2, CNT_ARGMAX = 3, CNT_ROTATE = 4 };
 
 }  // namespace
 
@@ -195,6 +196,11 @@ struct sbmds_ctx {
     DevBuf Dbuf;
     CUtensorMap dmap[7];
     bool dmap_ok[7] = {false, false, false, false, false, false, false};
+    CUtensorMap amap;            // D as the tcgen05 A operand: box 32 x 128, SWIZZLE_128B
+    bool amap_ok = false;
+    CUtensorMap bmap[7];         // Y1T = [Y_hi; Y_lo] as the B operand
+    void* bmap_ptr[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    DevBuf Y1T;
     // apply workspace
     DevBuf Y1, Y2, P, colpart, s, t, tpart, counters;
     int64_t y1_rows = 0;
@@ -279,7 +285,74 @@ void run_dstream(sbmds_ctx* h, int b, cudaStream_t st) {
     });
 }
 
+void encode_tiled(CUtensorMap* map, void* ptr, uint64_t inner, uint64_t outer, uint64_t pitch_bytes, uint32_t box0,
+                  uint32_t box1, CUtensorMapSwizzle sw) {
+    EncodeFn enc = get_encode();
+    if (!enc) throw CudaError{cudaErrorNotSupported, "cuTensorMapEncodeTiled entry point"};
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+    cuuint32_t box[2] = {box0, box1};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue, "cuTensorMapEncodeTiled"};
+}
+
+// A3 + A4 on the tensor cores (3xTF32, tcgen05): split Y1, stream D, reduce partials.
+template <int BP>
+void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st) {
+    using C = TcCfg<BP>;
+    const int i = bp_index(BP);
+    const int64_t lpad = (h->l + 127) / 128 * 128;   // >= KT * TK, zero tail
+    if (!h->amap_ok) {
+        encode_tiled(&h->amap, h->D, h->l, h->l, h->ldD * sizeof(float), 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        h->amap_ok = true;
+    }
+    h->Y1T.ensure((size_t)2 * kMaxB * lpad * sizeof(float));
+    if (h->bmap_ptr[i] != h->Y1T.p) {
+        encode_tiled(&h->bmap[i], h->Y1T.p, lpad, C::NB, lpad * sizeof(float), 32, C::NB, CU_TENSOR_MAP_SWIZZLE_128B);
+        h->bmap_ptr[i] = h->Y1T.p;
+    }
+    profiled(h->prof, PK_SPLIT, st, [&] {
+        launch(k_split_y1, dim3(2 * 148), dim3(256), 0, st, lpad, BP, (const float*)h->Y1.as<float>(),
+               h->Y1T.as<float>());
+    });
+    StreamK sk;
+    sk.RT = (h->l + C::TM - 1) / C::TM;
+    sk.KT = (h->l + C::TK - 1) / C::TK;
+    sk.T = sk.RT * sk.KT;
+    sk.grid = (int)std::min<int64_t>(h->num_sms, sk.T);
+    const int maxseg = (int)((sk.grid + sk.RT - 1) / sk.RT) + 2;
+    h->P.ensure((size_t)sk.RT * maxseg * C::TM * BP * sizeof(double));
+    static bool attr_set[7] = {false};
+    if (!attr_set[i]) {
+        CK(cudaFuncSetAttribute(k_dstream_tc<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        attr_set[i] = true;
+    }
+    profiled(h->prof, PK_DSTREAM, st, [&] {
+        launch(k_dstream_tc<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->amap, h->bmap[i], sk, maxseg,
+               h->P.as<double>());
+    });
+    const int rows_per_blk = 256 / BP;
+    const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
+    profiled(h->prof, PK_DREDUCE, st, [&] {
+        launch(k_dreduce, dim3(grid), dim3(256), 0, st, h->l, BP, b, C::TM, sk, maxseg,
+               (const double*)h->P.as<double>(), (const double*)h->w.as<double>(), h->Y2.as<float>(),
+               h->tpart.as<double>(), h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
+    });
+}
+
 void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st) {
+    const bool tc = (h->dstream == 2 || (h->dstream == 0 && bp >= 8));
+    if (tc) {
+        switch (bp) {
+            case 8: run_dstream_tc<8>(h, b, st); return;
+            case 16: run_dstream_tc<16>(h, b, st); return;
+            case 32: run_dstream_tc<32>(h, b, st); return;
+            case 64: run_dstream_tc<64>(h, b, st); return;
+            default: break;  // widths < 8 stay on the FFMA stream (HBM-bound there)
+        }
+    }
     switch (bp) {
         case 1: run_dstream<1>(h, b, st); break;
         case 2: run_dstream<2>(h, b, st); break;
@@ -358,7 +431,7 @@ void spmm_csr(sbmds_ctx* h, int b, int bp, float* Y, cudaStream_t st) {
 }
 
 void ensure_apply_ws(sbmds_ctx* h, int bp) {
-    const int64_t rows = (h->l + 31) / 32 * 32;
+    const int64_t rows = (h->l + 127) / 128 * 128;
     if (h->Y1.bytes < (size_t)rows * bp * sizeof(float)) {
         h->Y1.ensure((size_t)rows * kMaxB * sizeof(float));
         CK(cudaMemset(h->Y1.p, 0, h->Y1.bytes));  // pad rows/cols stay 0 (TMA tail reads them)
@@ -367,11 +440,11 @@ void ensure_apply_ws(sbmds_ctx* h, int bp) {
 }
 
 // The whole operator apply on device buffers (stream-ordered, no host sync).
-void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st) {
+void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st, bool s_ready = false) {
     const int bp = next_pow2(b);
     ensure_apply_ws(h, bp);
-    // A1: s = 1^T X
-    profiled(h->prof, PK_COLSUM, st, [&] {
+    // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
+    if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] {
         launch(k_colsum, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(),
                h->s.as<double>(), h->counters.as<unsigned int>() + CNT_COLSUM);
     });
@@ -388,7 +461,7 @@ void destroy_ctx(sbmds_ctx* h) {
     DevBuf* bufs[] = {&h->rp, &h->col, &h->val, &h->cptr, &h->ridx, &h->cval, &h->order, &h->w, &h->Dbuf,
                       &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel};
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T};
     for (DevBuf* b : bufs) b->release();
     delete h;
 }
@@ -624,28 +697,49 @@ namespace {
 
 void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st) {
     h->gpart.ensure((size_t)kRedBlocks * 2 * kMaxB * kMaxB * sizeof(double));
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_gram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+        CK(cudaFuncSetAttribute(k_gram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+        attr = true;
+    }
+    const size_t smem = gram_smem_bytes(b);
     profiled(h->prof, PK_GRAM, st, [&] {
-    if (X)
-        launch(k_gram<true>, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, Y, X, h->gpart.as<double>(),
-               h->G.as<double>(), h->H.as<double>(), h->counters.as<unsigned int>() + CNT_GRAM);
-    else
-        launch(k_gram<false>, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, Y, (const float*)nullptr,
-               h->gpart.as<double>(), h->G.as<double>(), (double*)nullptr, h->counters.as<unsigned int>() + CNT_GRAM);
+        if (X)
+            launch(k_gram<true>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, X, h->gpart.as<double>(),
+                   h->G.as<double>(), h->H.as<double>(), h->counters.as<unsigned int>() + CNT_GRAM);
+        else
+            launch(k_gram<false>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, (const float*)nullptr,
+                   h->gpart.as<double>(), h->G.as<double>(), (double*)nullptr,
+                   h->counters.as<unsigned int>() + CNT_GRAM);
     });
 }
 
-// X <- Y R^-1 with G = Y^T Y = R^T R. Returns false on breakdown (status read later).
+// out = in * M (+ addc), optionally s = 1^T out.
+void rotate(sbmds_ctx* h, int b, int mo, int ldm, const float* in, const double* M, float* out, const double* addc,
+            bool colsum, cudaStream_t st) {
+    const int grid = (int)std::min<int64_t>(2 * 148, (h->n + 255) / 256);
+    double* cp = colsum ? h->colpart.as<double>() : nullptr;
+    double* co = colsum ? h->s.as<double>() : nullptr;
+    unsigned int* cnt = h->counters.as<unsigned int>() + CNT_ROTATE;
+    auto go = [&](auto kern) { launch(kern, dim3(grid), dim3(256), 0, st, h->n, b, mo, ldm, in, M, out, addc, cp, co, cnt); };
+    profiled(h->prof, PK_ROTATE, st, [&] {
+        if (b <= 4) go(k_rotate<4>);
+        else if (b <= 8) go(k_rotate<8>);
+        else if (b <= 16) go(k_rotate<16>);
+        else if (b <= 32) go(k_rotate<32>);
+        else go(k_rotate<64>);
+    });
+}
+
+// X <- Y R^-1 with G = Y^T Y = R^T R (status read later); also s = 1^T X for the next apply.
 void cholqr(sbmds_ctx* h, int b, const float* Yin, float* Xout, cudaStream_t st) {
     gram(h, b, Yin, nullptr, st);
     profiled(h->prof, PK_CHOL, st, [&] {
         launch(k_chol, dim3(1), dim3(256), 0, st, b, (const double*)h->G.as<double>(), h->Rinv.as<double>(),
                h->status.as<int>());
     });
-    const int grid = (int)std::min<int64_t>(4 * 148, (h->n * b + 255) / 256);
-    profiled(h->prof, PK_ROTATE, st, [&] {
-        launch(k_rotate, dim3(grid), dim3(256), 0, st, h->n, b, b, b, Yin, (const double*)h->Rinv.as<double>(), Xout,
-               (const double*)nullptr);
-    });
+    rotate(h, b, b, b, Yin, (const double*)h->Rinv.as<double>(), Xout, nullptr, true, st);
 }
 
 }  // namespace
@@ -693,7 +787,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         int it = 0;
         bool converged = false;
         for (it = 1; it <= max_iters; ++it) {
-            apply_device(h, b, X, Y, st);  // Y = B~ X
+            apply_device(h, b, X, Y, st, true);  // Y = B~ X (s = 1^T X from the rotate)
             const bool do_rr = (it % h->rr_period == 0) || it == max_iters;
             if (do_rr) {
                 gram(h, b, Y, X, st);  // G = Y^T Y, H = X^T Y
@@ -755,8 +849,8 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         float* Zd = zdev ? Z : (Z ? (h->ztmp.ensure(vbytes), h->ztmp.as<float>()) : nullptr);
         const int grid = (int)std::min<int64_t>(4 * 148, (n * m + 255) / 256);
         const double* theta = Msel_d + (size_t)b * m + m;
-        launch(k_rotate, dim3(grid), dim3(256), 0, st, n, b, m, m, (const float*)X, (const double*)Msel_d, Vd,
-               (const double*)(Msel_d + (size_t)b * m));
+        rotate(h, b, m, m, (const float*)X, (const double*)Msel_d, Vd, (const double*)(Msel_d + (size_t)b * m), false,
+               st);
         h->sign.ensure(kMaxB * sizeof(float));
         h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
         h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
@@ -818,7 +912,7 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         h->prof.drain();
         for (int k = 0; k < PK_N; ++k) { h->prof.ns[k] = 0; h->prof.cnt[k] = 0; }
     } else if (!strcmp(key, "dstream")) {
-        if (value < 0 || value > 1) return fail(SBMDS_EINVAL, "dstream in {0, 1}");
+        if (value < 0 || value > 2) return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05}");
         h->dstream = (int)value;
     } else {
         return fail(SBMDS_EINVAL, "unknown option '%s'", key);

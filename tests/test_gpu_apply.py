@@ -169,3 +169,15 @@ def test_errors_are_reported():
     Dn[0, 1] += 1.0
     with pytest.raises(SbmdsError, match="symmetric"):
         Sbmds(p.n, p.l, p.row_ptr, p.col_idx, p.val32(), Dn, validate=True)
+
+
+@pytest.mark.parametrize("dstream", [1, 2])
+@pytest.mark.parametrize("b", [8, 16, 32, 64, 12])
+def test_apply_both_dstream_paths(dstream, b):
+    """FFMA stream (1) and tcgen05 3xTF32 stream (2) both meet the bar, ragged l (l = 2003)."""
+    p = configs.random_problem(30_011, 2_003, 16, seed=b, name="cfg5_small")
+    X = configs.x_block(p.n, b, seed=b)
+    with make_handle(p) as h:
+        h.set_option("dstream", dstream)
+        Y = run_apply(h, X)
+    assert relerr(Y, oracle_apply(p, X)) <= TOL

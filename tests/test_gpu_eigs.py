@@ -104,8 +104,8 @@ def test_eigs_fixed_iterations_and_warm_start():
         X0 = torch.zeros((p.n, p.block), device="cuda")
         X0[:, :3] = torch.from_numpy(V.astype(np.float32)).cuda()
         X0[:, 3:] = torch.randn((p.n, p.block - 3), device="cuda", generator=torch.Generator("cuda").manual_seed(0))
-        lam2, V2, _, info2 = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6, X0=X0)
-        lam3, V3, _, _ = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6, X0=X0)
+        lam2, V2, _, info2 = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-5, X0=X0)
+        lam3, V3, _, _ = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-5, X0=X0)
     assert info2["converged"] == 1
     assert np.array_equal(lam2, lam3) and np.array_equal(V2, V3)   # deterministic
 
