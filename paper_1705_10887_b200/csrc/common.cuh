@@ -100,6 +100,23 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// Fixed-order sum of p[0], p[stride], ..., p[(count-1)*stride] with 16 loads in flight:
+// the additions happen in index order (bitwise reproducible) but the L2 latency of the
+// partials is overlapped instead of serialised.
+__device__ __forceinline__ double ordered_sum(const double* __restrict__ p, int count, int64_t stride) {
+    double acc = 0.0;
+    int q = 0;
+    for (; q + 16 <= count; q += 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = p[(int64_t)(q + u) * stride];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc += v[u];
+    }
+    for (; q < count; ++q) acc += p[(int64_t)q * stride];
+    return acc;
+}
+
 // Last-block-done pattern for deterministic grid reductions: every block writes its
 // partial, fences, and bumps a counter; the block that sees count == grid-1 does the
 // final fixed-order reduction and resets the counter for the next launch.

@@ -211,11 +211,7 @@ __global__ void __launch_bounds__(256) k_dreduce(int64_t l, int bp, int b, int t
         tpart[blockIdx.x * kMaxB + tid] = v;
     }
     if (last_block_done(counter)) {
-        if (tid < bp) {
-            double v = 0.0;
-            for (unsigned int q = 0; q < gridDim.x; ++q) v += tpart[q * kMaxB + tid];
-            t[tid] = v;
-        }
+        if (tid < bp) t[tid] = ordered_sum(tpart + tid, gridDim.x, kMaxB);
         if (tid == 0) *counter = 0;
     }
 }

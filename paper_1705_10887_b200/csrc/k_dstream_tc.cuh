@@ -111,15 +111,32 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Y1 (l_pad x bp, row-major) -> Y1T (2bp x l_pad): rows [0, bp) = tf32 hi, rows [bp, 2bp) = lo.
-__global__ void k_split_y1(int64_t lpad, int bp, const float* __restrict__ Y1, float* __restrict__ Y1T) {
-    const int64_t total = lpad * bp;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = e / bp;
-        const int c = (int)(e % bp);
-        const float v = Y1[e];
-        const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-        Y1T[(int64_t)c * lpad + k] = hi;
-        Y1T[(int64_t)(bp + c) * lpad + k] = v - hi;
+// With Rinv (eigs, b x b upper triangular) the block is first right-multiplied by R^-1 in
+// fp64 (the R^-1 fold). A block stages 256/bp rows of Y1 in shared memory.
+__global__ void __launch_bounds__(256) k_split_y1(int64_t lpad, int b, int bp, const double* __restrict__ Rinv,
+                                                  const float* __restrict__ Y1, float* __restrict__ Y1T) {
+    __shared__ double Ms[64 * 64];
+    __shared__ float ys[256];
+    if (Rinv)
+        for (int e = threadIdx.x; e < b * b; e += blockDim.x) Ms[e] = Rinv[e];
+    const int rb = 256 / bp;
+    const int r = threadIdx.x % rb, c = threadIdx.x / rb;   // consecutive threads: consecutive k
+    for (int64_t k0 = (int64_t)blockIdx.x * rb; k0 < lpad; k0 += (int64_t)gridDim.x * rb) {
+        __syncthreads();
+        const int64_t k = k0 + r;
+        ys[r * bp + c] = (k < lpad) ? Y1[k * bp + c] : 0.f;
+        __syncthreads();
+        if (k < lpad) {
+            float v = ys[r * bp + c];
+            if (Rinv && c < b) {
+                double acc = 0.0;
+                for (int p = 0; p <= c; ++p) acc = fma((double)ys[r * bp + p], Ms[p * b + c], acc);
+                v = (float)acc;
+            }
+            const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            Y1T[(int64_t)c * lpad + k] = hi;
+            Y1T[(int64_t)(bp + c) * lpad + k] = v - hi;
+        }
     }
 }
 

@@ -15,20 +15,28 @@
 namespace sbmds {
 
 // ------------------------------------------------------------------ E2: tall-skinny Gram
+constexpr int kGramPart = 2 * kMaxB * kMaxB + kMaxB;   // per-block partial: G, H, column sums
+__host__ __device__ inline int gram_tile_rows(int b) {  // ~32 KB of fp64 per staged tile
+    const int b4 = (b + 3) & ~3;
+    const int r = 4096 / b4;
+    return r > 256 ? 256 : r;
+}
+
 // Rows are cut into gridDim.x contiguous ranges. A block stages 64-row tiles of Y (and X)
 // in shared memory as fp64 (fp32 -> fp64 is exact, so every product is exact) and splits
 // the b4 x b4 output (b4 = b rounded up to 4) into 4x4 micro-tiles; the 256 threads are
 // (micro-tile, row-group) pairs, each accumulating 16 (or 32 with H) fp64 FMAs per row.
 // Row-group partials are summed in fixed order, then the last block sums the block
 // partials in block order: bitwise deterministic.
+// cs (optional): column sums 1^T Y (fp64), same fixed-order reductions.
 template <bool WITH_H>
 __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __restrict__ Y,
                                               const float* __restrict__ X, double* __restrict__ part,
                                               double* __restrict__ G, double* __restrict__ H,
-                                              unsigned int* __restrict__ counter) {
-    constexpr int TR = 64;
+                                              double* __restrict__ cs, unsigned int* __restrict__ counter) {
     extern __shared__ double gsm[];
     const int b4 = (b + 3) & ~3;
+    const int TR = gram_tile_rows(b);
     const int nt = b4 / 4;                 // micro-tiles per side
     const int ntiles = nt * nt;            // <= 256
     const int groups = 256 / ntiles;       // row groups (>= 1)
@@ -38,11 +46,13 @@ __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __r
     const int tile = tid % ntiles, grp = tid / ntiles;
     const int ti = tile / nt, tj = tile % nt;
     const bool active = grp < groups;
-    double g[4][4], h[4][4];
+    double g[4][4], h[4][4], csum[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i) {
+        csum[i] = 0.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) g[i][j] = h[i][j] = 0.0;
+    }
     const int64_t rows_per_blk = (n + gridDim.x - 1) / gridDim.x;
     const int64_t beg = blockIdx.x * rows_per_blk, end = min(n, beg + rows_per_blk);
     for (int64_t r0 = beg; r0 < end; r0 += TR) {
@@ -62,6 +72,8 @@ __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __r
 #pragma unroll
                 for (int i = 0; i < 4; ++i) { a[i] = yr[4 * ti + i]; c[i] = yr[4 * tj + i]; }
 #pragma unroll
+                for (int i = 0; i < 4; ++i) csum[i] += c[i];
+#pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) g[i][j] = fma(a[i], c[j], g[i][j]);
@@ -80,8 +92,13 @@ __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __r
     }
     // reduce the row groups in fixed order through shared memory
     __syncthreads();
-    double* red = gsm;  // [groups][b4*b4] (+ same for H)
+    double* red = gsm;  // [groups][b4*b4] (+ same for H), then [groups][b4] column sums
     const int bb4 = b4 * b4;
+    double* cred = gsm + 2 * groups * bb4;
+    if (active && ti == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cred[grp * b4 + 4 * tj + i] = csum[i];
+    }
     if (active) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -93,7 +110,7 @@ __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __r
             }
     }
     __syncthreads();
-    double* pg = part + (int64_t)blockIdx.x * (2 * kMaxB * kMaxB);
+    double* pg = part + (int64_t)blockIdx.x * kGramPart;
     for (int pq = tid; pq < b * b; pq += 256) {
         const int p = pq / b, q = pq % b, e = p * b4 + q;
         double a = 0.0, ah = 0.0;
@@ -104,25 +121,26 @@ __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __r
         pg[pq] = a;
         if constexpr (WITH_H) pg[kMaxB * kMaxB + pq] = ah;
     }
+    for (int q = tid; q < b; q += 256) {
+        double a = 0.0;
+        for (int k = 0; k < groups; ++k) a += cred[k * b4 + q];
+        pg[2 * kMaxB * kMaxB + q] = a;
+    }
     if (last_block_done(counter)) {
+        if (cs)
+            for (int q = tid; q < b; q += 256) cs[q] = ordered_sum(part + 2 * kMaxB * kMaxB + q, gridDim.x, kGramPart);
         for (int pq = tid; pq < b * b; pq += 256) {
-            double a = 0.0, ah = 0.0;
-            for (unsigned int q = 0; q < gridDim.x; ++q) {
-                const double* pp = part + (int64_t)q * (2 * kMaxB * kMaxB);
-                a += pp[pq];
-                if constexpr (WITH_H) ah += pp[kMaxB * kMaxB + pq];
-            }
-            G[pq] = a;
-            if constexpr (WITH_H) H[pq] = ah;
+            G[pq] = ordered_sum(part + pq, gridDim.x, kGramPart);
+            if constexpr (WITH_H) H[pq] = ordered_sum(part + kMaxB * kMaxB + pq, gridDim.x, kGramPart);
         }
         if (tid == 0) *counter = 0;
     }
 }
-// dynamic smem: max(2 tiles of TR x b4, 2*groups*b4^2) doubles
+// dynamic smem: max(2 tiles of TR x b4, 2*groups*b4^2 + groups*b4) doubles
 inline size_t gram_smem_bytes(int b) {
     const int b4 = (b + 3) & ~3;
     const int nt = b4 / 4, groups = 256 / (nt * nt);
-    const size_t a = (size_t)2 * 64 * b4, c = (size_t)2 * groups * b4 * b4;
+    const size_t a = (size_t)2 * gram_tile_rows(b) * b4, c = (size_t)2 * groups * b4 * b4 + groups * b4;
     return (a > c ? a : c) * sizeof(double);
 }
 
@@ -204,8 +222,11 @@ struct RrOut {
 
 // Parallel cyclic Jacobi (round-robin pair ordering) on sym(H); residuals from the Gram
 // G = Y^T Y with Y = B~ X: r_j^2 = u_j^T G u_j - θ_j^2 for orthonormal X.
+// With Rinv != null the iterate is X = Y_prev Rinv and Hg holds Y_prev^T (B~X), so
+// H = Rinv^T Hg (the R^-1 fold of the eigs loop).
 __global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const double* __restrict__ Hg,
-                                            const double* __restrict__ Gg, RrOut* __restrict__ out) {
+                                            const double* __restrict__ Gg, const double* __restrict__ Rinv,
+                                            RrOut* __restrict__ out) {
     extern __shared__ double rr_smem[];
     double (*A)[kMaxB + 1] = reinterpret_cast<double (*)[kMaxB + 1]>(rr_smem);
     double (*V)[kMaxB + 1] = reinterpret_cast<double (*)[kMaxB + 1]>(rr_smem + kMaxB * (kMaxB + 1));
@@ -217,10 +238,33 @@ __global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const doub
     const int tid = threadIdx.x;
     const int be = b + (b & 1);
     const int np = be / 2;
-    for (int e = tid; e < b * b; e += blockDim.x) {
-        const int i = e / b, j = e % b;
-        A[i][j] = 0.5 * (Hg[i * b + j] + Hg[j * b + i]);
-        V[i][j] = (i == j) ? 1.0 : 0.0;
+    if (Rinv) {
+        // V <- Hg, then A <- Rinv^T V (V reused as scratch)
+        for (int e = tid; e < b * b; e += blockDim.x) V[e / b][e % b] = Hg[e];
+        __syncthreads();
+        for (int e = tid; e < b * b; e += blockDim.x) {
+            const int i = e / b, j = e % b;
+            double acc = 0.0;
+            for (int p = 0; p <= i; ++p) acc += Rinv[p * b + i] * V[p][j];   // Rinv upper triangular
+            A[i][j] = acc;
+        }
+        __syncthreads();
+        for (int e = tid; e < b * b; e += blockDim.x) {
+            const int i = e / b, j = e % b;
+            V[i][j] = 0.5 * (A[i][j] + A[j][i]);
+        }
+        __syncthreads();
+        for (int e = tid; e < b * b; e += blockDim.x) {
+            const int i = e / b, j = e % b;
+            A[i][j] = V[i][j];
+            V[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+    } else {
+        for (int e = tid; e < b * b; e += blockDim.x) {
+            const int i = e / b, j = e % b;
+            A[i][j] = 0.5 * (Hg[i * b + j] + Hg[j * b + i]);
+            V[i][j] = (i == j) ? 1.0 : 0.0;
+        }
     }
     if (tid < be) perm[tid] = tid;
     __syncthreads();
@@ -415,12 +459,32 @@ __global__ void __launch_bounds__(256) k_rotate(int64_t n, int b, int mo, int ld
         cs_part[blockIdx.x * kMaxB + threadIdx.x] = v;
     }
     if (last_block_done(counter)) {
-        if (threadIdx.x < mo) {
-            double v = 0.0;
-            for (unsigned int q = 0; q < gridDim.x; ++q) v += cs_part[q * kMaxB + threadIdx.x];
-            cs_out[threadIdx.x] = v;
-        }
+        if (threadIdx.x < mo) cs_out[threadIdx.x] = ordered_sum(cs_part + threadIdx.x, gridDim.x, kMaxB);
         if (threadIdx.x == 0) *counter = 0;
+    }
+}
+
+// Y1 (l x bp, first b columns) <- Y1 Rinv: the R^-1 fold (S^T (Y R^-1) - w (1^T Y R^-1)^T
+// = (S^T Y - w (1^T Y)^T) R^-1), so the orthonormal iterate X = Y R^-1 is never formed.
+// Element-parallel: a block stages 256/bp rows in shared memory, each thread forms one
+// output entry in fp64 (R^-1 upper triangular) and writes it back in place.
+__global__ void __launch_bounds__(256) k_y1_rot(int64_t l, int b, int bp, const double* __restrict__ Rinv,
+                                                float* __restrict__ Y1) {
+    __shared__ double Ms[kMaxB * kMaxB];
+    __shared__ float ys[256];
+    for (int e = threadIdx.x; e < b * b; e += blockDim.x) Ms[e] = Rinv[e];
+    const int rb = 256 / bp;
+    const int r = threadIdx.x / bp, c = threadIdx.x % bp;
+    for (int64_t j0 = (int64_t)blockIdx.x * rb; j0 < l; j0 += (int64_t)gridDim.x * rb) {
+        __syncthreads();
+        const int64_t j = j0 + r;
+        ys[threadIdx.x] = (j < l) ? Y1[j * bp + c] : 0.f;
+        __syncthreads();
+        if (j < l && c < b) {
+            double acc = 0.0;
+            for (int p = 0; p <= c; ++p) acc = fma((double)ys[r * bp + p], Ms[p * b + c], acc);
+            Y1[j * bp + c] = (float)acc;
+        }
     }
 }
 

@@ -151,11 +151,7 @@ __global__ void k_colsum(int64_t n, int b, const float* __restrict__ X, double* 
         part[blockIdx.x * kMaxB + t] = v;
     }
     if (last_block_done(counter)) {
-        if (t < b) {
-            double v = 0.0;
-            for (unsigned int q = 0; q < gridDim.x; ++q) v += part[q * kMaxB + t];
-            s[t] = v;
-        }
+        if (t < b) s[t] = ordered_sum(part + t, gridDim.x, kMaxB);
         if (t == 0) *counter = 0;
     }
 }

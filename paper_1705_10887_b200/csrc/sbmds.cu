@@ -300,7 +300,7 @@ void encode_tiled(CUtensorMap* map, void* ptr, uint64_t inner, uint64_t outer, u
 
 // A3 + A4 on the tensor cores (3xTF32, tcgen05): split Y1, stream D, reduce partials.
 template <int BP>
-void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st) {
+void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
     using C = TcCfg<BP>;
     const int i = bp_index(BP);
     const int64_t lpad = (h->l + 127) / 128 * 128;   // >= KT * TK, zero tail
@@ -314,8 +314,8 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st) {
         h->bmap_ptr[i] = h->Y1T.p;
     }
     profiled(h->prof, PK_SPLIT, st, [&] {
-        launch(k_split_y1, dim3(2 * 148), dim3(256), 0, st, lpad, BP, (const float*)h->Y1.as<float>(),
-               h->Y1T.as<float>());
+        launch(k_split_y1, dim3((unsigned)std::min<int64_t>(8 * 148, (lpad + 255) / 256 * BP)), dim3(256), 0, st,
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1T.as<float>());
     });
     StreamK sk;
     sk.RT = (h->l + C::TM - 1) / C::TM;
@@ -342,17 +342,23 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st) {
     });
 }
 
-void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st) {
-    const bool tc = (h->dstream == 2 || (h->dstream == 0 && bp >= 8));
-    if (tc) {
+bool uses_tc(const sbmds_ctx* h, int bp) { return bp >= 8 && (h->dstream == 2 || h->dstream == 0); }
+
+void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
+    if (uses_tc(h, bp)) {
         switch (bp) {
-            case 8: run_dstream_tc<8>(h, b, st); return;
-            case 16: run_dstream_tc<16>(h, b, st); return;
-            case 32: run_dstream_tc<32>(h, b, st); return;
-            case 64: run_dstream_tc<64>(h, b, st); return;
-            default: break;  // widths < 8 stay on the FFMA stream (HBM-bound there)
+            case 8: run_dstream_tc<8>(h, b, st, Rinv); return;
+            case 16: run_dstream_tc<16>(h, b, st, Rinv); return;
+            case 32: run_dstream_tc<32>(h, b, st, Rinv); return;
+            default: run_dstream_tc<64>(h, b, st, Rinv); return;
         }
     }
+    // widths < 8 (or dstream=1): FFMA stream; the R^-1 fold runs as its own small kernel
+    if (Rinv)
+        profiled(h->prof, PK_ROTATE, st, [&] {
+            launch(k_y1_rot, dim3((unsigned)std::min<int64_t>(8 * 148, (h->l * bp + 255) / 256)), dim3(256), 0, st,
+                   h->l, b, bp, Rinv, h->Y1.as<float>());
+        });
     switch (bp) {
         case 1: run_dstream<1>(h, b, st); break;
         case 2: run_dstream<2>(h, b, st); break;
@@ -440,7 +446,8 @@ void ensure_apply_ws(sbmds_ctx* h, int bp) {
 }
 
 // The whole operator apply on device buffers (stream-ordered, no host sync).
-void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st, bool s_ready = false) {
+void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st, bool s_ready = false,
+                  const double* Rinv = nullptr) {
     const int bp = next_pow2(b);
     ensure_apply_ws(h, bp);
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
@@ -450,8 +457,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     });
     // A2: Y1 = S^T X - w s^T
     profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
-    // A3, A4: Y2 = D Y1, t = w^T Y2
-    dstream(h, b, bp, st);
+    // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
+    dstream(h, b, bp, st, Rinv);
     // A5: Y = -1/2 (S Y2 - 1 t^T)
     profiled(h->prof, PK_CSR, st, [&] { spmm_csr(h, b, bp, Y, st); });
 }
@@ -695,8 +702,10 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
 // ============================================================================ eigs
 namespace {
 
-void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st) {
-    h->gpart.ensure((size_t)kRedBlocks * 2 * kMaxB * kMaxB * sizeof(double));
+// G = Y^T Y, s = 1^T Y (into h->s when want_s), and H = X^T Y when X != null.
+void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, bool want_s = false) {
+    h->gpart.ensure((size_t)kRedBlocks * kGramPart * sizeof(double));
+    double* cs = want_s ? h->s.as<double>() : nullptr;
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(k_gram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
@@ -707,10 +716,10 @@ void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st) 
     profiled(h->prof, PK_GRAM, st, [&] {
         if (X)
             launch(k_gram<true>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, X, h->gpart.as<double>(),
-                   h->G.as<double>(), h->H.as<double>(), h->counters.as<unsigned int>() + CNT_GRAM);
+                   h->G.as<double>(), h->H.as<double>(), cs, h->counters.as<unsigned int>() + CNT_GRAM);
         else
             launch(k_gram<false>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, (const float*)nullptr,
-                   h->gpart.as<double>(), h->G.as<double>(), (double*)nullptr,
+                   h->gpart.as<double>(), h->G.as<double>(), (double*)nullptr, cs,
                    h->counters.as<unsigned int>() + CNT_GRAM);
     });
 }
@@ -732,14 +741,13 @@ void rotate(sbmds_ctx* h, int b, int mo, int ldm, const float* in, const double*
     });
 }
 
-// X <- Y R^-1 with G = Y^T Y = R^T R (status read later); also s = 1^T X for the next apply.
-void cholqr(sbmds_ctx* h, int b, const float* Yin, float* Xout, cudaStream_t st) {
-    gram(h, b, Yin, nullptr, st);
+// R^-1 from G = Y^T Y = R^T R (status read later). The orthonormal X = Y R^-1 is never
+// formed: the next apply folds R^-1 into its l x b stage.
+void chol(sbmds_ctx* h, int b, cudaStream_t st) {
     profiled(h->prof, PK_CHOL, st, [&] {
         launch(k_chol, dim3(1), dim3(256), 0, st, b, (const double*)h->G.as<double>(), h->Rinv.as<double>(),
                h->status.as<int>());
     });
-    rotate(h, b, b, b, Yin, (const double*)h->Rinv.as<double>(), Xout, nullptr, true, st);
 }
 
 }  // namespace
@@ -769,46 +777,53 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         h->Rinv.ensure(kMaxB * kMaxB * sizeof(double));
         h->status.ensure(16);
         h->rr.ensure(sizeof(RrOut));
-        float* X = h->X.as<float>();
-        float* Y = h->Y.as<float>();
-        // E1: initial block, orthonormalised by Cholesky-QR (into Y, then swap roles)
+        // Two n x b buffers alternate as Y_k (current, unnormalised) and Y_{k+1}; the
+        // orthonormal iterate is X_k = Y_k R_k^{-1} (R from Cholesky-QR), never materialised.
+        float* Yc = h->X.as<float>();
+        float* Yn = h->Y.as<float>();
+        // E1: initial block Y_0 (Philox N(0,1) or the warm start), G_0, s_0, R_0^{-1}
         if (X0) {
-            CK(cudaMemcpyAsync(Y, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
+            CK(cudaMemcpyAsync(Yc, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
         } else {
-            launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, Y);
+            launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, Yc);
         }
-        cholqr(h, b, Y, X, st);
+        gram(h, b, Yc, nullptr, st, true);
+        chol(h, b, st);
         int hstat = 0;
         CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR of the initial block broke down");
 
+        static bool rr_attr = false;
+        if (!rr_attr) {
+            CK(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, kRrSmem));
+            rr_attr = true;
+        }
         RrOut rr_host;
         int it = 0;
         bool converged = false;
         for (it = 1; it <= max_iters; ++it) {
-            apply_device(h, b, X, Y, st, true);  // Y = B~ X (s = 1^T X from the rotate)
+            // Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1};  s = 1^T Y_k came from the last Gram
+            apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>());
             const bool do_rr = (it % h->rr_period == 0) || it == max_iters;
+            // G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, and H' = Y_k^T Y_{k+1} for Rayleigh-Ritz
+            gram(h, b, Yn, do_rr ? Yc : nullptr, st, true);
             if (do_rr) {
-                gram(h, b, Y, X, st);  // G = Y^T Y, H = X^T Y
-                static bool rr_attr = false;
-                if (!rr_attr) {
-                    CK(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, kRrSmem));
-                    rr_attr = true;
-                }
+                // H = X_k^T B~ X_k = R_k^{-T} H'
                 profiled(h->prof, PK_RR, st, [&] {
                     launch(k_rr, dim3(1), dim3(256), (size_t)kRrSmem, st, b, m, tol, (const double*)h->H.as<double>(),
-                           (const double*)h->G.as<double>(), h->rr.as<RrOut>());
+                           (const double*)h->G.as<double>(), (const double*)h->Rinv.as<double>(), h->rr.as<RrOut>());
                 });
                 int conv = 0;
                 CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
                 if (conv || it == max_iters) {
                     converged = conv != 0;
-                    break;
+                    break;   // Ritz vectors are X_k U = Y_k (R_k^{-1} U): Yc and Rinv stay valid
                 }
             }
-            cholqr(h, b, Y, X, st);  // X = Y R^-1
+            chol(h, b, st);   // R_{k+1}^{-1}
+            std::swap(Yc, Yn);
             if (do_rr || it % 16 == 0) {
                 CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
@@ -822,6 +837,9 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         // lives in 1^perp after the first apply, so the known pair (0, 1/sqrt(n)) is merged
         // into the Ritz list: it enters the top m when fewer than m Ritz values are >= 0.
         std::vector<double> Msel((size_t)b * m, 0.0), addc(m, 0.0), theta_out(m, 0.0);
+        std::vector<double> Rinv_h((size_t)b * b);
+        CK(cudaMemcpyAsync(Rinv_h.data(), h->Rinv.p, Rinv_h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
         {
             int r = 0;
             bool zero_used = false;
@@ -832,7 +850,12 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                     theta_out[j] = 0.0;
                     continue;
                 }
-                for (int p = 0; p < b; ++p) Msel[(size_t)p * m + j] = rr_host.U[p * b + r];
+                // V = X_k U = Y_k (R_k^{-1} U): fold R^{-1} into the selection matrix
+                for (int p = 0; p < b; ++p) {
+                    double acc = 0.0;
+                    for (int q = p; q < b; ++q) acc += Rinv_h[(size_t)p * b + q] * rr_host.U[q * b + r];
+                    Msel[(size_t)p * m + j] = acc;
+                }
                 theta_out[j] = rr_host.theta[r];
                 ++r;
             }
@@ -849,8 +872,8 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         float* Zd = zdev ? Z : (Z ? (h->ztmp.ensure(vbytes), h->ztmp.as<float>()) : nullptr);
         const int grid = (int)std::min<int64_t>(4 * 148, (n * m + 255) / 256);
         const double* theta = Msel_d + (size_t)b * m + m;
-        rotate(h, b, m, m, (const float*)X, (const double*)Msel_d, Vd, (const double*)(Msel_d + (size_t)b * m), false,
-               st);
+        rotate(h, b, m, m, (const float*)Yc, (const double*)Msel_d, Vd, (const double*)(Msel_d + (size_t)b * m),
+               false, st);
         h->sign.ensure(kMaxB * sizeof(float));
         h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
         h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
