@@ -1,0 +1,215 @@
+// Row-blocked S with per-block landmark dictionaries (SURVEY.md §7 hard part 3).
+//
+// The interpolation operator is local ("the number of data points influenced
+// by each landmark will shrink"; the sparse P keeps the few large entries),
+// so RB = 256 consecutive vertices touch only u_B ~ 200 landmarks at config 4 (40x reuse).
+// Both SpMMs therefore stage the touched rows in shared memory instead of gathering them
+// through L1/L2 (the CSR/CSC kernels of k_sparse.cuh are L1- resp. L2-latency bound):
+//
+//   S Y2  (A5):  block B loads Y2[dict_B] (u_B x bp) into smem; each nnz carries a 16-bit
+//                local column; rows are formed from smem gathers.             k_blk_spmm
+//   S^T X (A2):  block B loads its 256 X rows into smem and forms, for each dictionary
+//                entry d of B, the partial P1[d] = sum over the block's nnz in column
+//                dict[d] (a block-local CSC: 8-bit local row, value), in fixed order;
+//                k_blk_reduce sums the partials of landmark j over blocks in ascending
+//                block order and applies the rank-one centring.               k_blk_spmmt
+// Every sum has a fixed order: results are bitwise reproducible.
+#pragma once
+#include "common.cuh"
+
+namespace sbmds {
+
+constexpr int kRB = 256;   // rows per block (local row fits in 8 bits)
+
+// ------------------------------------------------------------------ create-time build
+__global__ void k_blk_offsets(int64_t n, int64_t nblk, const int32_t* __restrict__ rp, int32_t* __restrict__ off) {
+    for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B <= nblk; B += (int64_t)gridDim.x * blockDim.x)
+        off[B] = rp[min(B * kRB, n)];
+}
+
+// flag[p] = 1 where a new (block, column) pair starts in the block-segmented col sort.
+__global__ void k_blk_flags(int32_t nnz, const int32_t* __restrict__ scol, const int32_t* __restrict__ perm,
+                            const int32_t* __restrict__ rowof, const int32_t* __restrict__ off,
+                            int32_t* __restrict__ flag) {
+    for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x) {
+        const int32_t B = rowof[perm[p]] / kRB;
+        flag[p] = (p == off[B] || scol[p] != scol[p - 1]) ? 1 : 0;
+    }
+}
+
+// incl = inclusive scan of flags: dictionary slot of sorted entry p is incl[p] - 1.
+__global__ void k_blk_dictoff(int64_t nblk, int32_t nnz, const int32_t* __restrict__ off,
+                              const int32_t* __restrict__ flag, const int32_t* __restrict__ incl, int32_t total_u,
+                              int32_t* __restrict__ dict_off) {
+    for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B <= nblk; B += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = off[B];
+        dict_off[B] = (p < nnz) ? incl[p] - flag[p] : total_u;
+    }
+}
+
+__global__ void k_blk_umax(int64_t nblk, const int32_t* __restrict__ dict_off, unsigned int* __restrict__ umax) {
+    unsigned int m = 0;
+    for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B < nblk; B += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, (unsigned int)(dict_off[B + 1] - dict_off[B]));
+    atomicMax(umax, m);
+}
+
+__global__ void k_blk_scatter(int32_t nnz, const int32_t* __restrict__ scol, const int32_t* __restrict__ perm,
+                              const int32_t* __restrict__ rowof, const float* __restrict__ val,
+                              const int32_t* __restrict__ flag, const int32_t* __restrict__ incl,
+                              const int32_t* __restrict__ dict_off, int32_t* __restrict__ dict,
+                              int32_t* __restrict__ lcp, uint16_t* __restrict__ lcol, uint8_t* __restrict__ lrow,
+                              float* __restrict__ lval) {
+    for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x) {
+        const int32_t e = perm[p];
+        const int32_t row = rowof[e];
+        const int32_t B = row / kRB;
+        const int32_t d = incl[p] - 1;
+        if (flag[p]) {
+            dict[d] = scol[p];
+            lcp[d] = p;
+        }
+        lcol[e] = (uint16_t)(d - dict_off[B]);
+        lrow[p] = (uint8_t)(row - B * kRB);
+        lval[p] = val[e];
+    }
+}
+
+// ------------------------------------------------------------------ A5: Y = -1/2 (S Y2 - 1 t^T)
+// One CTA per 256-row block: Y2[dict_B] -> smem, then LPR lanes per row (float4 each);
+// a row's nnz metadata is read LPR entries at a time (one coalesced load per lane) and
+// broadcast within the lane group by shuffles.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_blk_spmm(int64_t n, int b, int bp, const int32_t* __restrict__ rp,
+                                                  const uint16_t* __restrict__ lcol, const float* __restrict__ val,
+                                                  const int32_t* __restrict__ dict, const int32_t* __restrict__ dict_off,
+                                                  const float* __restrict__ Y2, const double* __restrict__ t,
+                                                  float* __restrict__ Y) {
+    constexpr int G = 32 / LPR;
+    extern __shared__ float4 ys4[];
+    const int64_t B = blockIdx.x;
+    const int32_t d0 = dict_off[B], u = dict_off[B + 1] - d0;
+    const int nv = bp / 4;
+    for (int e = threadIdx.x; e < u * nv; e += blockDim.x) {
+        const int i = e / nv, q = e % nv;
+        ys4[e] = __ldg(reinterpret_cast<const float4*>(Y2 + (int64_t)dict[d0 + i] * bp) + q);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPR, q = lane % LPR;
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (g * LPR));
+    const double t0 = t[4 * q], t1 = t[4 * q + 1], t2 = t[4 * q + 2], t3 = t[4 * q + 3];
+    for (int r = warp * G + g; r < kRB; r += 8 * G) {
+        const int64_t i = B * kRB + r;
+        if (i >= n) break;
+        const int32_t beg = rp[i], end = rp[i + 1];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int32_t e0 = beg; e0 < end; e0 += LPR) {
+            const int32_t e = e0 + q;
+            const int lc_l = (e < end) ? (int)lcol[e] : 0;
+            const float v_l = (e < end) ? val[e] : 0.f;
+#pragma unroll
+            for (int tq = 0; tq < LPR; ++tq) {
+                const int lc = __shfl_sync(gmask, lc_l, tq, LPR);
+                const float v = __shfl_sync(gmask, v_l, tq, LPR);
+                const float4 y = ys4[lc * nv + q];
+                acc.x = fmaf(v, y.x, acc.x);
+                acc.y = fmaf(v, y.y, acc.y);
+                acc.z = fmaf(v, y.z, acc.z);
+                acc.w = fmaf(v, y.w, acc.w);
+            }
+        }
+        float4 out;
+        out.x = (float)(-0.5 * ((double)acc.x - t0));
+        out.y = (float)(-0.5 * ((double)acc.y - t1));
+        out.z = (float)(-0.5 * ((double)acc.z - t2));
+        out.w = (float)(-0.5 * ((double)acc.w - t3));
+        reinterpret_cast<float4*>(Y + i * b)[q] = out;
+    }
+}
+
+// ------------------------------------------------------------------ A2 part 1: block partials
+// One CTA per 256-row block: its X rows -> smem. Each group of LPR lanes owns one dictionary
+// entry d of the block (32/LPR entries per warp in flight) and walks the entry's block-local
+// column list in row order: metadata is read LPR entries at a time (one load per lane) and
+// broadcast within the group; P1[d] = the fp32 partial (bp wide), fixed summation order.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_blk_spmmt(int64_t n, int b, int bp, const float* __restrict__ X,
+                                                   const int32_t* __restrict__ dict_off, const int32_t* __restrict__ lcp,
+                                                   const uint8_t* __restrict__ lrow, const float* __restrict__ lval,
+                                                   float* __restrict__ P1) {
+    constexpr int G = 32 / LPR;
+    extern __shared__ float4 xs4[];   // kRB x bp/4 (dynamic: up to 64 KB at bp = 64)
+    const int64_t B = blockIdx.x;
+    const int nv = bp / 4;
+    const int64_t r0 = B * kRB;
+    const int rows = (int)((n - r0) < kRB ? (n - r0) : kRB);
+    for (int e = threadIdx.x; e < rows * nv; e += blockDim.x)
+        xs4[e] = __ldg(reinterpret_cast<const float4*>(X + (r0 + e / nv) * b) + (e % nv));
+    __syncthreads();
+    const int32_t d0 = dict_off[B], u = dict_off[B + 1] - d0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPR, q = lane % LPR;
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (g * LPR));
+    for (int di = warp * G + g; di < u; di += 8 * G) {
+        const int32_t d = d0 + di;
+        const int32_t beg = lcp[d], end = lcp[d + 1];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int32_t p0 = beg; p0 < end; p0 += LPR) {
+            const int32_t p = p0 + q;
+            const int r_l = (p < end) ? (int)lrow[p] : 0;
+            const float v_l = (p < end) ? lval[p] : 0.f;
+#pragma unroll
+            for (int tq = 0; tq < LPR; ++tq) {
+                const int r = __shfl_sync(gmask, r_l, tq, LPR);
+                const float v = __shfl_sync(gmask, v_l, tq, LPR);
+                const float4 x = xs4[r * nv + q];
+                acc.x = fmaf(v, x.x, acc.x);
+                acc.y = fmaf(v, x.y, acc.y);
+                acc.z = fmaf(v, x.z, acc.z);
+                acc.w = fmaf(v, x.w, acc.w);
+            }
+        }
+        reinterpret_cast<float4*>(P1 + (int64_t)d * bp)[q] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ A2 part 2: Y1 = sum_B P1 - w s^T
+// One warp per landmark j: the dictionary slots holding j (ascending block order) are
+// summed in fp64, LPR lanes per slot row, a fixed shuffle tree across the G slot groups.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, const int32_t* __restrict__ jptr,
+                                                    const int32_t* __restrict__ jlist, const float* __restrict__ P1,
+                                                    const double* __restrict__ w, const double* __restrict__ s,
+                                                    float* __restrict__ Y1) {
+    constexpr int G = 32 / LPR;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / LPR, q = lane % LPR;
+    const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (j >= l) return;
+    const int32_t beg = jptr[j], end = jptr[j + 1];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int32_t k = beg + g; k < end; k += G) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)jlist[k] * bp) + q);
+        a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+    }
+    if (g == 0) {
+        const double wj = w[j];
+        const int c = 4 * q;
+        float4 out;
+        out.x = (float)(a0 - wj * s[c + 0]);
+        out.y = (float)(a1 - wj * s[c + 1]);
+        out.z = (float)(a2 - wj * s[c + 2]);
+        out.w = (float)(a3 - wj * s[c + 3]);
+        reinterpret_cast<float4*>(Y1 + j * bp)[q] = out;
+    }
+}
+
+}  // namespace sbmds

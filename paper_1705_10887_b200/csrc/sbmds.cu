@@ -20,6 +20,7 @@
 #include "k_dstream_tc.cuh"
 #include "k_small.cuh"
 #include "k_sparse.cuh"
+#include "k_blocked.cuh"
 
 namespace sbmds {
 std::atomic<int64_t> g_launches{0};
@@ -189,6 +190,14 @@ struct sbmds_ctx {
     int dev = 0, num_sms = 148;
     // S (CSR) and its device-built CSC copy
     DevBuf rp, col, val, cptr, ridx, cval, order, w;
+    // row-blocked S (k_blocked.cuh): per 256-row block a landmark dictionary, 16-bit local
+    // columns for S Y2, a block-local CSC (8-bit rows) for S^T X, and the landmark -> slot lists
+    DevBuf bdoff, bdict, blcp, blcol, blrow, blval, bjptr, bjlist, P1;
+    int64_t nblk = 0;
+    int32_t total_u = 0;
+    uint32_t umax = 0;
+    bool blocked = false;
+    int use_blocked = 1;   // bit 0: S Y2 through the blocked kernel, bit 1: S^T X too
     // D_ll
     float* D = nullptr;
     int64_t ldD = 0;
@@ -253,6 +262,14 @@ void encode_dmap(sbmds_ctx* h) {
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue, "cuTensorMapEncodeTiled"};
     h->dmap_ok[i] = true;
+}
+
+constexpr size_t kBlkSmem = 96 * 1024;   // shared-memory budget of one staged dictionary
+
+bool blocked_ok(const sbmds_ctx* h, int b, int bp, const void* X, const void* Y) {
+    return h->blocked && b == bp && b >= 4 && (b % 4) == 0 &&
+           (size_t)h->umax * bp * sizeof(float) <= kBlkSmem && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
+           ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
 }
 
 // ---------------------------------------------------------------------------- A3 + A4
@@ -455,18 +472,158 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         launch(k_colsum, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(),
                h->s.as<double>(), h->counters.as<unsigned int>() + CNT_COLSUM);
     });
-    // A2: Y1 = S^T X - w s^T
-    profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
+    const bool blk = blocked_ok(h, b, bp, X, Y);
+    if (blk) {
+        static bool attr = false;   // opt the blocked kernels into > 48 KB of dynamic smem once
+        if (!attr) {
+            for (auto k : {k_blk_spmmt<1>, k_blk_spmmt<2>, k_blk_spmmt<4>, k_blk_spmmt<8>, k_blk_spmmt<16>})
+                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kRB * kMaxB * 4));
+            for (auto k : {k_blk_spmm<1>, k_blk_spmm<2>, k_blk_spmm<4>, k_blk_spmm<8>, k_blk_spmm<16>})
+                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlkSmem));
+            attr = true;
+        }
+    }
+    // A2: Y1 = S^T X - w s^T   (CSC SpMM by default; row-blocked partials + landmark
+    // reduction when enabled: both are bound by the 64-B-per-nonzero gather traffic)
+    if (blk && (h->use_blocked & 2)) {
+        h->P1.ensure((size_t)std::max<int32_t>(1, h->total_u) * kMaxB * sizeof(float));
+        const size_t smem_t = (size_t)kRB * bp * sizeof(float);
+        auto go_t = [&](auto kern) {
+            launch(kern, dim3((unsigned)h->nblk), dim3(256), smem_t, st, h->n, b, bp, X,
+                   (const int32_t*)h->bdoff.as<int32_t>(), (const int32_t*)h->blcp.as<int32_t>(),
+                   (const uint8_t*)h->blrow.as<uint8_t>(), (const float*)h->blval.as<float>(), h->P1.as<float>());
+        };
+        auto go_r = [&](auto kern) {
+            launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
+                   (const int32_t*)h->bjptr.as<int32_t>(), (const int32_t*)h->bjlist.as<int32_t>(),
+                   (const float*)h->P1.as<float>(), (const double*)h->w.as<double>(), (const double*)h->s.as<double>(),
+                   h->Y1.as<float>());
+        };
+        profiled(h->prof, PK_CSC, st, [&] {
+            switch (b / 4) {
+                case 1: go_t(k_blk_spmmt<1>); go_r(k_blk_reduce<1>); break;
+                case 2: go_t(k_blk_spmmt<2>); go_r(k_blk_reduce<2>); break;
+                case 4: go_t(k_blk_spmmt<4>); go_r(k_blk_reduce<4>); break;
+                case 8: go_t(k_blk_spmmt<8>); go_r(k_blk_reduce<8>); break;
+                default: go_t(k_blk_spmmt<16>); go_r(k_blk_reduce<16>); break;
+            }
+        });
+    } else {
+        profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
+    }
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     dstream(h, b, bp, st, Rinv);
     // A5: Y = -1/2 (S Y2 - 1 t^T)
-    profiled(h->prof, PK_CSR, st, [&] { spmm_csr(h, b, bp, Y, st); });
+    if (blk && (h->use_blocked & 1)) {
+        const size_t smem = (size_t)h->umax * bp * sizeof(float);
+        auto go = [&](auto kern) {
+            launch(kern, dim3((unsigned)h->nblk), dim3(256), smem, st, h->n, b, bp, (const int32_t*)h->rp.as<int32_t>(),
+                   (const uint16_t*)h->blcol.as<uint16_t>(), (const float*)h->val.as<float>(),
+                   (const int32_t*)h->bdict.as<int32_t>(), (const int32_t*)h->bdoff.as<int32_t>(),
+                   (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), Y);
+        };
+        profiled(h->prof, PK_CSR, st, [&] {
+            switch (b / 4) {
+                case 1: go(k_blk_spmm<1>); break;
+                case 2: go(k_blk_spmm<2>); break;
+                case 4: go(k_blk_spmm<4>); break;
+                case 8: go(k_blk_spmm<8>); break;
+                default: go(k_blk_spmm<16>); break;
+            }
+        });
+    } else {
+        profiled(h->prof, PK_CSR, st, [&] { spmm_csr(h, b, bp, Y, st); });
+    }
+}
+
+// Row-blocked S (k_blocked.cuh): segmented stable sort of each 256-row block's entries by
+// column, unique -> per-block dictionary, 16-bit local columns (CSR order), the block-local
+// CSC (sorted order), and for each landmark its dictionary slots in block order.
+void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
+    const int64_t n = h->n, l = h->l, nnz = h->nnz;
+    h->nblk = (n + kRB - 1) / kRB;
+    const int64_t nb = h->nblk;
+    DevBuf off, scol, iota_perm, flag, incl, tmp, keys2;
+    off.ensure((nb + 1) * sizeof(int32_t));
+    scol.ensure(nnz * sizeof(int32_t));
+    iota_perm.ensure(2 * nnz * sizeof(int32_t));
+    flag.ensure(nnz * sizeof(int32_t));
+    incl.ensure(nnz * sizeof(int32_t));
+    int32_t* iota = iota_perm.as<int32_t>();
+    int32_t* perm = iota + nnz;
+    launch(k_blk_offsets, dim3((unsigned)std::min<int64_t>(1024, (nb + 256) / 256)), dim3(256), 0, st, n, nb,
+           (const int32_t*)h->rp.as<int32_t>(), off.as<int32_t>());
+    launch(k_iota, dim3(1024), dim3(256), 0, st, (int32_t)nnz, iota);
+    size_t tb = 0;
+    CK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, h->col.as<int32_t>(), scol.as<int32_t>(), iota, perm,
+                                                 (int)nnz, (int)nb, off.as<int32_t>(), off.as<int32_t>() + 1, st));
+    tmp.ensure(tb + 16);
+    CK(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb, h->col.as<int32_t>(), scol.as<int32_t>(), iota, perm,
+                                                 (int)nnz, (int)nb, off.as<int32_t>(), off.as<int32_t>() + 1, st));
+    g_launches.fetch_add(1);
+    launch(k_blk_flags, dim3(1024), dim3(256), 0, st, (int32_t)nnz, (const int32_t*)scol.as<int32_t>(),
+           (const int32_t*)perm, rowof, (const int32_t*)off.as<int32_t>(), flag.as<int32_t>());
+    tb = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)nnz, st));
+    DevBuf tmp2;
+    tmp2.ensure(tb + 16);
+    CK(cub::DeviceScan::InclusiveSum(tmp2.p, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)nnz, st));
+    g_launches.fetch_add(1);
+    int32_t total_u = 0;
+    CK(cudaMemcpyAsync(&total_u, incl.as<int32_t>() + nnz - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h->total_u = total_u;
+    h->bdoff.ensure((nb + 1) * sizeof(int32_t));
+    h->bdict.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
+    h->blcp.ensure((total_u + 1) * sizeof(int32_t));
+    h->blcol.ensure(nnz * sizeof(uint16_t));
+    h->blrow.ensure(nnz * sizeof(uint8_t));
+    h->blval.ensure(nnz * sizeof(float));
+    h->bjptr.ensure((l + 1) * sizeof(int32_t));
+    h->bjlist.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
+    launch(k_blk_dictoff, dim3((unsigned)std::min<int64_t>(1024, (nb + 256) / 256)), dim3(256), 0, st, nb,
+           (int32_t)nnz, (const int32_t*)off.as<int32_t>(), (const int32_t*)flag.as<int32_t>(),
+           (const int32_t*)incl.as<int32_t>(), total_u, h->bdoff.as<int32_t>());
+    launch(k_blk_scatter, dim3(1024), dim3(256), 0, st, (int32_t)nnz, (const int32_t*)scol.as<int32_t>(),
+           (const int32_t*)perm, rowof, (const float*)h->val.as<float>(), (const int32_t*)flag.as<int32_t>(),
+           (const int32_t*)incl.as<int32_t>(), (const int32_t*)h->bdoff.as<int32_t>(), h->bdict.as<int32_t>(),
+           h->blcp.as<int32_t>(), h->blcol.as<uint16_t>(), h->blrow.as<uint8_t>(), h->blval.as<float>());
+    const int32_t nnz32 = (int32_t)nnz;
+    CK(cudaMemcpyAsync(h->blcp.as<int32_t>() + total_u, &nnz32, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    // largest dictionary (decides which block widths fit in shared memory)
+    DevBuf um;
+    um.ensure(sizeof(unsigned int));
+    CK(cudaMemsetAsync(um.p, 0, sizeof(unsigned int), st));
+    launch(k_blk_umax, dim3(256), dim3(256), 0, st, nb, (const int32_t*)h->bdoff.as<int32_t>(), um.as<unsigned int>());
+    // landmark -> dictionary slots, ascending slot (= block) order: stable sort of (dict, slot)
+    keys2.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
+    DevBuf slot;
+    slot.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
+    launch(k_iota, dim3(256), dim3(256), 0, st, total_u, slot.as<int32_t>());
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) <= l) ++end_bit;
+    tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->bdict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
+                                       h->bjlist.as<int32_t>(), total_u, 0, end_bit, st));
+    DevBuf tmp3;
+    tmp3.ensure(tb + 16);
+    CK(cub::DeviceRadixSort::SortPairs(tmp3.p, tb, h->bdict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
+                                       h->bjlist.as<int32_t>(), total_u, 0, end_bit, st));
+    g_launches.fetch_add(1);
+    launch(k_col_ptr, dim3((unsigned)((l + 256) / 256)), dim3(256), 0, st, l, total_u,
+           (const int32_t*)keys2.as<int32_t>(), h->bjptr.as<int32_t>());
+    unsigned int umax = 0;
+    CK(cudaMemcpyAsync(&umax, um.p, sizeof umax, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h->umax = umax;
+    h->blocked = true;
 }
 
 void destroy_ctx(sbmds_ctx* h) {
     if (!h) return;
     DevBuf* bufs[] = {&h->rp, &h->col, &h->val, &h->cptr, &h->ridx, &h->cval, &h->order, &h->w, &h->Dbuf,
-                      &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
+                      &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
+                      &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T};
     for (DevBuf* b : bufs) b->release();
@@ -564,6 +721,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
                    (const int32_t*)tmpC.as<int32_t>(), h->cptr.as<int32_t>());
             CK(cudaStreamSynchronize(st));
             cubtmp.release();
+            build_blocked(h, tmpA.as<int32_t>(), st);
         } else {
             CK(cudaMemsetAsync(h->cptr.p, 0, (l + 1) * sizeof(int32_t), st));
         }
@@ -926,6 +1084,9 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         h->rr_period = (int)value;
     } else if (!strcmp(key, "use_graph")) {
         h->use_graph = value ? 1 : 0;
+    } else if (!strcmp(key, "blocked")) {
+        if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "blocked is a bit mask in [0, 3]");
+        h->use_blocked = (int)value;
     } else if (!strcmp(key, "order_columns")) {
         h->order_columns = value ? 1 : 0;
     } else if (!strcmp(key, "profile")) {
@@ -950,6 +1111,8 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "nnz")) *value = h->nnz;
     else if (!strcmp(key, "rowsum_dev_e9")) *value = (int64_t)std::llround(h->rowsum_dev * 1e9);
     else if (!strcmp(key, "d_borrowed")) *value = h->d_borrowed ? 1 : 0;
+    else if (!strcmp(key, "blocked_umax")) *value = h->blocked ? (int64_t)h->umax : -1;
+    else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
     else if (!strcmp(key, "csc_bytes")) *value = (int64_t)(h->cptr.bytes + h->ridx.bytes + h->cval.bytes);
     else if (!strcmp(key, "workspace_bytes"))
         *value = (int64_t)(h->Y1.bytes + h->Y2.bytes + h->P.bytes + h->X.bytes + h->Y.bytes + h->gpart.bytes);

@@ -181,3 +181,16 @@ def test_apply_both_dstream_paths(dstream, b):
         h.set_option("dstream", dstream)
         Y = run_apply(h, X)
     assert relerr(Y, oracle_apply(p, X)) <= TOL
+
+
+@pytest.mark.parametrize("blocked", [0, 1, 2, 3])
+@pytest.mark.parametrize("b", [4, 8, 16, 32, 64])
+def test_apply_blocked_and_plain_sparse_paths(blocked, b):
+    """Row-blocked (smem dictionary) SpMMs and the plain CSR/CSC SpMMs both meet the bar."""
+    p = configs.config(2)
+    X = configs.x_block(p.n, b, seed=b)
+    with make_handle(p) as h:
+        h.set_option("blocked", blocked)
+        assert 0 < h.stat("blocked_umax") < 200     # torus: ~100 landmarks per 256-row block
+        Y = run_apply(h, X)
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
