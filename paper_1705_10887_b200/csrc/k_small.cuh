@@ -136,6 +136,144 @@ __global__ void __launch_bounds__(256) k_gram(int64_t n, int b, const float* __r
         if (tid == 0) *counter = 0;
     }
 }
+// Gram on the FP64 tensor cores: mma.sync.m8n8k4.f64 (fp32 -> fp64 is exact, so every product
+// is exact and only the fp64 accumulation rounds). A warp walks a contiguous row range 4 rows at
+// a time; lane t holds Y[r0 + (t & 3)][8c + (t >> 2)] for each 8-column block c, which is at the
+// same time the A fragment of (Y^T)_c (8 x 4, row-major) and the B fragment of Y_c (4 x 8,
+// col-major). G (symmetric) needs the NCB(NCB+1)/2 blocks c <= c'; H = X^T Y needs all NCB^2.
+// Warp fragments -> shared memory (fixed warp order) -> block partial -> last block, like k_gram.
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int NCB, bool WITH_H>
+__global__ void __launch_bounds__(256) k_gram_tc(int64_t n, int b, const float* __restrict__ Y,
+                                                 const float* __restrict__ X, double* __restrict__ part,
+                                                 double* __restrict__ G, double* __restrict__ H,
+                                                 double* __restrict__ cs, unsigned int* __restrict__ counter) {
+    constexpr int NPG = NCB * (NCB + 1) / 2;
+    constexpr int NPH = WITH_H ? NCB * NCB : 0;
+    extern __shared__ double gtc_smem[];   // per-warp G (H reuses it after) + column sums
+    auto red = reinterpret_cast<double (*)[NCB * 8][NCB * 8 + 1]>(gtc_smem);
+    auto cred = reinterpret_cast<double (*)[NCB * 8]>(gtc_smem + 8 * (NCB * 8) * (NCB * 8 + 1));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kr = lane & 3, cc = lane >> 2;   // fragment row-in-k and column-in-block
+    double g[NPG][2], h[NPH > 0 ? NPH : 1][2], csum[NCB];
+#pragma unroll
+    for (int i = 0; i < NPG; ++i) g[i][0] = g[i][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < (NPH > 0 ? NPH : 1); ++i) h[i][0] = h[i][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) csum[c] = 0.0;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    const int64_t wid = (int64_t)blockIdx.x * 8 + warp;
+    const int64_t rows_per_warp = ((n + nw - 1) / nw + 15) & ~int64_t(15);
+    const int64_t beg = wid * rows_per_warp, end = min(n, beg + rows_per_warp);
+    constexpr int U = 4;   // 4-row groups whose loads are issued together (memory-level parallelism)
+    for (int64_t r0 = beg; r0 < end; r0 += 4 * U) {
+        float yf[U][NCB], xf[U][NCB];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = r0 + 4 * u + kr;
+            const bool ok = r < end;
+#pragma unroll
+            for (int c = 0; c < NCB; ++c) {
+                const int col = 8 * c + cc;
+                yf[u][c] = (ok && col < b) ? __ldg(Y + r * b + col) : 0.f;
+                if constexpr (WITH_H) xf[u][c] = (ok && col < b) ? __ldg(X + r * b + col) : 0.f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double y[NCB], x[NCB];
+#pragma unroll
+            for (int c = 0; c < NCB; ++c) {
+                y[c] = (double)yf[u][c];
+                csum[c] += y[c];
+                if constexpr (WITH_H) x[c] = (double)xf[u][c];
+            }
+            int pi = 0;
+#pragma unroll
+            for (int c = 0; c < NCB; ++c)
+#pragma unroll
+                for (int c2 = c; c2 < NCB; ++c2) dmma_8x8x4(g[pi++], y[c], y[c2]);
+            if constexpr (WITH_H) {
+#pragma unroll
+                for (int c = 0; c < NCB; ++c)
+#pragma unroll
+                    for (int c2 = 0; c2 < NCB; ++c2) dmma_8x8x4(h[c * NCB + c2], x[c], y[c2]);
+            }
+        }
+    }
+    // column sums: lanes with the same cc hold the same columns
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) {
+        double v = csum[c];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (kr == 0) cred[warp][8 * c + cc] = v;
+    }
+    // C fragment: lane t holds (row t >> 2, cols 2(t & 3), 2(t & 3) + 1) of each 8 x 8 block
+    const int fr = lane >> 2, fc = 2 * (lane & 3);
+    {
+        int pi = 0;
+#pragma unroll
+        for (int c = 0; c < NCB; ++c)
+#pragma unroll
+            for (int c2 = c; c2 < NCB; ++c2) {
+                red[warp][8 * c + fr][8 * c2 + fc] = g[pi][0];
+                red[warp][8 * c + fr][8 * c2 + fc + 1] = g[pi][1];
+                red[warp][8 * c2 + fc][8 * c + fr] = g[pi][0];          // mirror (symmetric)
+                red[warp][8 * c2 + fc + 1][8 * c + fr] = g[pi][1];
+                ++pi;
+            }
+    }
+    __syncthreads();
+    double* pg = part + (int64_t)blockIdx.x * kGramPart;
+    for (int pq = threadIdx.x; pq < b * b; pq += 256) {
+        const int p = pq / b, q = pq % b;
+        double a = 0.0;
+        for (int w = 0; w < 8; ++w) a += red[w][p][q];
+        pg[pq] = a;
+    }
+    for (int q = threadIdx.x; q < b; q += 256) {
+        double a = 0.0;
+        for (int w = 0; w < 8; ++w) a += cred[w][q];
+        pg[2 * kMaxB * kMaxB + q] = a;
+    }
+    if constexpr (WITH_H) {
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < NCB; ++c)
+#pragma unroll
+            for (int c2 = 0; c2 < NCB; ++c2) {
+                red[warp][8 * c + fr][8 * c2 + fc] = h[c * NCB + c2][0];
+                red[warp][8 * c + fr][8 * c2 + fc + 1] = h[c * NCB + c2][1];
+            }
+        __syncthreads();
+        for (int pq = threadIdx.x; pq < b * b; pq += 256) {
+            const int p = pq / b, q = pq % b;
+            double a = 0.0;
+            for (int w = 0; w < 8; ++w) a += red[w][p][q];
+            pg[kMaxB * kMaxB + pq] = a;
+        }
+    }
+    if (last_block_done(counter)) {
+        if (cs)
+            for (int q = threadIdx.x; q < b; q += 256) cs[q] = ordered_sum(part + 2 * kMaxB * kMaxB + q, gridDim.x, kGramPart);
+        for (int pq = threadIdx.x; pq < b * b; pq += 256) {
+            G[pq] = ordered_sum(part + pq, gridDim.x, kGramPart);
+            if constexpr (WITH_H) H[pq] = ordered_sum(part + kMaxB * kMaxB + pq, gridDim.x, kGramPart);
+        }
+        if (threadIdx.x == 0) *counter = 0;
+    }
+}
+
+template <int NCB>
+constexpr size_t gram_tc_smem() { return (size_t)8 * (NCB * 8) * (NCB * 8 + 1 + 1) * sizeof(double); }
+
 // dynamic smem: max(2 tiles of TR x b4, 2*groups*b4^2 + groups*b4) doubles
 inline size_t gram_smem_bytes(int b) {
     const int b4 = (b + 3) & ~3;

@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "k_dstream.cuh"
 #include "k_dstream_tc.cuh"
+#include "k_dstream_sym.cuh"
 #include "k_small.cuh"
 #include "k_sparse.cuh"
 #include "k_blocked.cuh"
@@ -198,6 +199,8 @@ struct sbmds_ctx {
     uint32_t umax = 0;
     bool blocked = false;
     int use_blocked = 1;   // bit 0: S Y2 through the blocked kernel, bit 1: S^T X too
+    int gram_tc = 1;       // Gram on the FP64 tensor cores (b <= 32)
+    int sym_dbg = 0;
     // D_ll
     float* D = nullptr;
     int64_t ldD = 0;
@@ -209,7 +212,9 @@ struct sbmds_ctx {
     bool amap_ok = false;
     CUtensorMap bmap[7];         // Y1T = [Y_hi; Y_lo] as the B operand
     void* bmap_ptr[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    DevBuf Y1T;
+    DevBuf Y1T, PT;
+    int last_dpath = 0;          // D-stream path of the last apply: 1 ffma, 2 tcgen05, 3 tcgen05 symmetric half
+    int64_t last_dbytes = 0;     // its bytes per launch (bench roofline)
     // apply workspace
     DevBuf Y1, Y2, P, colpart, s, t, tpart, counters;
     int64_t y1_rows = 0;
@@ -293,6 +298,8 @@ void run_dstream(sbmds_ctx* h, int b, cudaStream_t st) {
         launch(k_dstream_ffma<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM + 1024, st,
                h->dmap[bp_index(BP)], h->l, (const float*)h->Y1.as<float>(), sk, maxseg, h->P.as<double>());
     });
+    h->last_dpath = 1;
+    h->last_dbytes = 4 * h->l * h->l + 12 * h->l * (int64_t)b;
     const int rows_per_blk = 256 / BP;
     const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     profiled(h->prof, PK_DREDUCE, st, [&] {
@@ -350,6 +357,8 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
         launch(k_dstream_tc<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->amap, h->bmap[i], sk, maxseg,
                h->P.as<double>());
     });
+    h->last_dpath = 2;
+    h->last_dbytes = 4 * h->l * h->l + 12 * h->l * (int64_t)b;
     const int rows_per_blk = 256 / BP;
     const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     profiled(h->prof, PK_DREDUCE, st, [&] {
@@ -359,9 +368,63 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
     });
 }
 
-bool uses_tc(const sbmds_ctx* h, int bp) { return bp >= 8 && (h->dstream == 2 || h->dstream == 0); }
+// A3 + A4 streaming only the upper triangle of D (NEXT-1, k_dstream_sym.cuh).
+template <int BP>
+void run_dstream_sym(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
+    using C = SymCfg<BP>;
+    const int i = bp_index(BP);
+    const int64_t lpad = (h->l + 127) / 128 * 128;
+    if (!h->amap_ok) {
+        encode_tiled(&h->amap, h->D, h->l, h->l, h->ldD * sizeof(float), 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        h->amap_ok = true;
+    }
+    h->Y1T.ensure((size_t)2 * kMaxB * lpad * sizeof(float));
+    if (h->bmap_ptr[i] != h->Y1T.p) {
+        encode_tiled(&h->bmap[i], h->Y1T.p, lpad, C::NB, lpad * sizeof(float), 32, C::NB, CU_TENSOR_MAP_SWIZZLE_128B);
+        h->bmap_ptr[i] = h->Y1T.p;
+    }
+    profiled(h->prof, PK_SPLIT, st, [&] {
+        launch(k_split_y1, dim3((unsigned)std::min<int64_t>(8 * 148, (lpad + 255) / 256 * BP)), dim3(256), 0, st,
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1T.as<float>());
+    });
+    SymSched sk;
+    sk.RT = (int)((h->l + C::T - 1) / C::T);
+    sk.NT = (int64_t)sk.RT * (sk.RT + 1) / 2;
+    sk.grid = (int)std::min<int64_t>(h->num_sms, sk.NT);
+    int maxseg = 1;
+    for (int I = 0; I < sk.RT; ++I)
+        maxseg = std::max(maxseg, sk.cta_of(sk.strip0(I) + (sk.RT - I) - 1) - sk.cta_of(sk.strip0(I)) + 1);
+    h->P.ensure((size_t)sk.RT * maxseg * C::T * BP * sizeof(double));
+    h->PT.ensure((size_t)std::max<int64_t>(1, (int64_t)sk.RT * (sk.RT - 1) / 2) * C::T * BP * sizeof(float));
+    static bool attr_set[7] = {false};
+    if (!attr_set[i]) {
+        CK(cudaFuncSetAttribute(k_dstream_sym<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        attr_set[i] = true;
+    }
+    profiled(h->prof, PK_DSTREAM, st, [&] {
+        launch(k_dstream_sym<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->amap, h->bmap[i], sk, maxseg,
+               h->P.as<double>(), h->PT.as<float>());
+    });
+    const int rows_per_blk = 256 / BP;
+    const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
+    profiled(h->prof, PK_DREDUCE, st, [&] {
+        launch(k_dreduce_sym, dim3(grid), dim3(256), 0, st, h->l, BP, b, sk, maxseg, (const double*)h->P.as<double>(),
+               (const float*)h->PT.as<float>(), (const double*)h->w.as<double>(), h->Y2.as<float>(),
+               h->tpart.as<double>(), h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
+    });
+    h->last_dpath = 3;
+    h->last_dbytes = sk.NT * (int64_t)C::T * C::T * 4 + (sk.NT - sk.RT) * (int64_t)C::T * BP * 4;
+}
+
+bool uses_tc(const sbmds_ctx* h, int bp) { return bp >= 8 && (h->dstream == 2 || h->dstream == 0 || h->dstream == 3); }
+bool uses_sym(const sbmds_ctx* h, int bp) { return (bp == 8 || bp == 16) && h->dstream == 3; }
 
 void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
+    if (uses_sym(h, bp)) {
+        if (bp == 8) run_dstream_sym<8>(h, b, st, Rinv);
+        else run_dstream_sym<16>(h, b, st, Rinv);
+        return;
+    }
     if (uses_tc(h, bp)) {
         switch (bp) {
             case 8: run_dstream_tc<8>(h, b, st, Rinv); return;
@@ -625,7 +688,7 @@ void destroy_ctx(sbmds_ctx* h) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T};
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->PT};
     for (DevBuf* b : bufs) b->release();
     delete h;
 }
@@ -871,14 +934,38 @@ void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, 
         attr = true;
     }
     const size_t smem = gram_smem_bytes(b);
+    double* Hd = h->H.as<double>();
+    double* Gd = h->G.as<double>();
+    double* P = h->gpart.as<double>();
+    unsigned int* cnt = h->counters.as<unsigned int>() + CNT_GRAM;
+    static bool tc_attr = false;
+    if (!tc_attr) {
+        CK(cudaFuncSetAttribute(k_gram_tc<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tc_smem<4>()));
+        CK(cudaFuncSetAttribute(k_gram_tc<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tc_smem<4>()));
+        tc_attr = true;
+    }
+    const size_t smem_tc = b <= 8 ? gram_tc_smem<1>() : (b <= 16 ? gram_tc_smem<2>() : gram_tc_smem<4>());
+    auto tc = [&](auto kern) {
+        launch(kern, dim3(kRedBlocks), dim3(256), smem_tc, st, h->n, b, Y, X, P, Gd, Hd, cs, cnt);
+    };
     profiled(h->prof, PK_GRAM, st, [&] {
-        if (X)
-            launch(k_gram<true>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, X, h->gpart.as<double>(),
-                   h->G.as<double>(), h->H.as<double>(), cs, h->counters.as<unsigned int>() + CNT_GRAM);
-        else
-            launch(k_gram<false>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, (const float*)nullptr,
-                   h->gpart.as<double>(), h->G.as<double>(), (double*)nullptr, cs,
-                   h->counters.as<unsigned int>() + CNT_GRAM);
+        if (h->gram_tc && b <= 32) {   // FP64 tensor cores (DMMA m8n8k4)
+            const int ncb = (b + 7) / 8;
+            if (X) {
+                if (ncb == 1) tc(k_gram_tc<1, true>);
+                else if (ncb == 2) tc(k_gram_tc<2, true>);
+                else tc(k_gram_tc<4, true>);
+            } else {
+                if (ncb == 1) tc(k_gram_tc<1, false>);
+                else if (ncb == 2) tc(k_gram_tc<2, false>);
+                else tc(k_gram_tc<4, false>);
+            }
+        } else if (X) {
+            launch(k_gram<true>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, X, P, Gd, Hd, cs, cnt);
+        } else {
+            launch(k_gram<false>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, (const float*)nullptr, P, Gd,
+                   (double*)nullptr, cs, cnt);
+        }
     });
 }
 
@@ -1087,6 +1174,10 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "blocked")) {
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "blocked is a bit mask in [0, 3]");
         h->use_blocked = (int)value;
+    } else if (!strcmp(key, "sym_dbg")) {
+        h->sym_dbg = (int)value;
+    } else if (!strcmp(key, "gram_tc")) {
+        h->gram_tc = value ? 1 : 0;
     } else if (!strcmp(key, "order_columns")) {
         h->order_columns = value ? 1 : 0;
     } else if (!strcmp(key, "profile")) {
@@ -1096,7 +1187,7 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         h->prof.drain();
         for (int k = 0; k < PK_N; ++k) { h->prof.ns[k] = 0; h->prof.cnt[k] = 0; }
     } else if (!strcmp(key, "dstream")) {
-        if (value < 0 || value > 2) return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05}");
+        if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric}");
         h->dstream = (int)value;
     } else {
         return fail(SBMDS_EINVAL, "unknown option '%s'", key);
@@ -1112,6 +1203,8 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "rowsum_dev_e9")) *value = (int64_t)std::llround(h->rowsum_dev * 1e9);
     else if (!strcmp(key, "d_borrowed")) *value = h->d_borrowed ? 1 : 0;
     else if (!strcmp(key, "blocked_umax")) *value = h->blocked ? (int64_t)h->umax : -1;
+    else if (!strcmp(key, "dstream_path")) *value = h->last_dpath;
+    else if (!strcmp(key, "dstream_bytes")) *value = h->last_dbytes;
     else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
     else if (!strcmp(key, "csc_bytes")) *value = (int64_t)(h->cptr.bytes + h->ridx.bytes + h->cval.bytes);
     else if (!strcmp(key, "workspace_bytes"))

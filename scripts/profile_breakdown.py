@@ -17,7 +17,7 @@ import torch  # noqa: E402
 from gen import configs  # noqa: E402
 from paper_1705_10887_b200 import from_problem  # noqa: E402
 
-FAM = ["colsum", "csc", "dstream", "dreduce", "csr", "gram", "chol", "rotate", "rr"]
+FAM = ["colsum", "csc", "dstream", "dreduce", "csr", "gram", "chol", "rotate", "rr", "split"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
@@ -27,12 +27,14 @@ ap.add_argument("--applies", type=int, default=20)
 ap.add_argument("--eigs", action="store_true")
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--order", type=int, default=1)
+ap.add_argument("--dstream", type=int, default=0)
 a = ap.parse_args()
 
 p = configs.config(a.config, k5=a.k5)
 b = a.b or p.block or 16
 h = from_problem(p)
 h.set_option("order_columns", a.order)
+h.set_option("dstream", a.dstream)
 X = torch.randn((p.n, b), device="cuda", generator=torch.Generator("cuda").manual_seed(0))
 Y = torch.empty_like(X)
 for _ in range(2 if a.quick else 3):
@@ -53,7 +55,7 @@ e1.record()
 torch.cuda.synchronize()
 tot = e0.elapsed_time(e1) / a.applies
 out = {"config": a.config, "b": b, "n": p.n, "l": p.l, "nnz": p.nnz, "apply_ms": tot,
-       "per_apply_ms": {f: h.stat(f + "_ns") / 1e6 / max(1, a.applies) for f in FAM[:5]}}
+       "per_apply_ms": {f: h.stat(f + "_ns") / 1e6 / max(1, a.applies) for f in FAM[:5] + ["split"]}, "dstream_path": h.stat("dstream_path"), "dstream_bytes": h.stat("dstream_bytes")}
 byt = 4 * p.l * p.l + 16 * p.nnz + 4 * (p.n + 1) + 4 * (p.l + 1) + 8 * p.n * b
 out["apply_algorithmic_GBps"] = byt / (tot / 1e3) / 1e9
 if a.eigs and p.m:

@@ -194,3 +194,26 @@ def test_apply_blocked_and_plain_sparse_paths(blocked, b):
         assert 0 < h.stat("blocked_umax") < 200     # torus: ~100 landmarks per 256-row block
         Y = run_apply(h, X)
     assert relerr(Y, oracle_apply(p, X)) <= TOL
+
+
+@pytest.mark.parametrize("b", [16, 12, 8, 5])
+def test_apply_symmetric_half_stream(b):
+    """NEXT-1: streaming only the upper triangle of D (k_dstream_sym) meets the bar; l = 2003
+    gives 16 row tiles with a ragged last one, so every off-diagonal/transposed case occurs."""
+    p = configs.random_problem(30_011, 2_003, 16, seed=b + 100, name="cfg5_small")
+    X = configs.x_block(p.n, b, seed=b)
+    with make_handle(p) as h:
+        h.set_option("dstream", 3)
+        Y = run_apply(h, X)
+        assert h.stat("dstream_path") == 3
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
+
+
+def test_symmetric_half_eigs_config2():
+    """The symmetric-half stream inside the eigensolver (config 2) agrees with the full stream."""
+    p = configs.config(2)
+    with make_handle(p) as h:
+        lam_a, _, _, _ = h.eigs(p.m, p.block, max_iters=200, tol=1e-6)
+        h.set_option("dstream", 3)
+        lam_b, _, _, _ = h.eigs(p.m, p.block, max_iters=200, tol=1e-6)
+    assert np.allclose(lam_a, lam_b, rtol=1e-5)

@@ -117,3 +117,15 @@ def test_eigs_host_outputs():
         lam_d, V_d, Z_d, _ = gpu_eigs(h, p.m, p.block, tol=1e-6)
     assert np.array_equal(lam, lam_d)
     assert np.array_equal(V, V_d.astype(np.float32))
+
+
+@pytest.mark.parametrize("gram_tc", [0, 1])
+def test_eigs_gram_paths_agree(gram_tc):
+    """Gram on FP64 tensor cores (DMMA) and on FP64 CUDA cores both solve config 1 to the bar."""
+    p = configs.config(1)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    lam_o, V_o, Z_o = O.eigs_dense(S, p.D, p.m)
+    with handle(p) as h:
+        h.set_option("gram_tc", gram_tc)
+        lam, V, Z, info = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6)
+    check_against(lam, V, Z, lam_o, V_o, Z_o)
