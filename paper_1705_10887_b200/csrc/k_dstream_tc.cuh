@@ -30,7 +30,7 @@ namespace sbmds {
 template <int BP>
 struct TcCfg {
     static constexpr int TM = 128;                       // tile rows (MMA M)
-    static constexpr int NA = 2;                         // 128B swizzle atoms (32 fp32 of k) per stage
+    static constexpr int NA = BP >= 32 ? 2 : 3;          // 128B swizzle atoms (32 fp32 of k) per stage
     static constexpr int TK = 32 * NA;                   // k per stage: 256 contiguous bytes per D row
     static constexpr int NB = 2 * BP;                    // B rows: [Y_hi; Y_lo]
     static constexpr int N1 = NB;                        // D_hi * [Y_hi | Y_lo]
@@ -49,7 +49,7 @@ struct TcCfg {
     static constexpr int TMEM_COLS = 512;
     static constexpr int ACC0 = 0;                       // acc buffer b at column b*ACC_COLS
     static constexpr int LO0 = 2 * ACC_COLS;             // A_lo slots
-    static constexpr int KC = 16 / NA;                   // k-tiles per accumulator drain (512 k)
+    static constexpr int KC = NA == 3 ? 5 : 16 / NA;     // k-tiles per accumulator drain (~512 k)
     static constexpr int NGROUP = 2;                     // converter groups (alternate stages)
     static constexpr int THREADS = (4 + 4 * NGROUP) * 32;
     static constexpr int SMEM = NS * STAGE_BYTES + 1024 + 256;

@@ -323,11 +323,15 @@ void encode_tiled(CUtensorMap* map, void* ptr, uint64_t inner, uint64_t outer, u
 }
 
 // A3 + A4 on the tensor cores (3xTF32, tcgen05): split Y1, stream D, reduce partials.
+// Padded k length of Y1 / Y1T shared by the tensor paths (their cached B tensor maps
+// encode it): a multiple of 384 = 3 swizzle atoms (k_dstream_tc) and of 128 (k_dstream_sym).
+int64_t y1t_lpad(const sbmds_ctx* h) { return (h->l + 383) / 384 * 384; }
+
 template <int BP>
 void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
     using C = TcCfg<BP>;
     const int i = bp_index(BP);
-    const int64_t lpad = (h->l + 127) / 128 * 128;   // >= KT * TK, zero tail
+    const int64_t lpad = y1t_lpad(h);
     if (!h->amap_ok) {
         encode_tiled(&h->amap, h->D, h->l, h->l, h->ldD * sizeof(float), 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         h->amap_ok = true;
@@ -373,7 +377,7 @@ template <int BP>
 void run_dstream_sym(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
     using C = SymCfg<BP>;
     const int i = bp_index(BP);
-    const int64_t lpad = (h->l + 127) / 128 * 128;
+    const int64_t lpad = y1t_lpad(h);
     if (!h->amap_ok) {
         encode_tiled(&h->amap, h->D, h->l, h->l, h->ldD * sizeof(float), 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         h->amap_ok = true;
@@ -517,7 +521,7 @@ void spmm_csr(sbmds_ctx* h, int b, int bp, float* Y, cudaStream_t st) {
 }
 
 void ensure_apply_ws(sbmds_ctx* h, int bp) {
-    const int64_t rows = (h->l + 127) / 128 * 128;
+    const int64_t rows = (h->l + 383) / 384 * 384;   // >= every D-stream path's padded k range
     if (h->Y1.bytes < (size_t)rows * bp * sizeof(float)) {
         h->Y1.ensure((size_t)rows * kMaxB * sizeof(float));
         CK(cudaMemset(h->Y1.p, 0, h->Y1.bytes));  // pad rows/cols stay 0 (TMA tail reads them)
