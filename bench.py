@@ -157,6 +157,12 @@ def dstream_bytes(p, b):
     return 4 * p.l * p.l + 4 * p.l * b + 8 * p.l * b
 
 
+def log(msg):
+    if os.environ.get("SBMDS_BENCH_TRACE"):
+        sys.stderr.write(f"[bench {time.strftime('%H:%M:%S')}] {msg}\n")
+        sys.stderr.flush()
+
+
 def run_ours(args, ws, rank, local):
     import torch
     from paper_1705_10887_b200 import from_problem, launch_count
@@ -168,7 +174,9 @@ def run_ours(args, ws, rank, local):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
+    log("inputs ready")
     h = from_problem(p, device="cuda")
+    log("handle created")
     st = torch.cuda.current_stream()
     V = torch.empty((p.n, m), device="cuda")
     Z = torch.empty((p.n, m), device="cuda")
@@ -179,6 +187,7 @@ def run_ours(args, ws, rank, local):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    log("warmup done")
     barrier(ws)
     h.set_option("profile", 1 << 2)          # CUDA events around k_dstream_ffma only
     h.set_option("profile_reset", 1)
@@ -191,6 +200,7 @@ def run_ours(args, ws, rank, local):
         infos = [step()[3] for _ in range(args.steps)]
         e1.record(st)
         torch.cuda.synchronize()
+    log("timed region done")
     n_launch = launch_count() - n0
     ms = e0.elapsed_time(e1)
     ds_ns, ds_n = h.stat("dstream_ns"), h.stat("dstream_launches")
@@ -219,20 +229,28 @@ def run_ours(args, ws, rank, local):
         del h
         torch.cuda.empty_cache()
         times = []
+        log("e2e start")
         for s in range(args.e2e_steps + 1):
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             a.record(st)
+            t_a = time.perf_counter()
             with Sbmds(p.n, p.l, rp, ci, vv, Dh) as hh:
+                t_b = time.perf_counter()
                 hh.eigs(m, b, max_iters=iters, tol=0.0, seed=0, V=Vh, Z=Zh)
+                t_c = time.perf_counter()
             z.record(st)
             torch.cuda.synchronize()
+            log(f"e2e step {s}: create {t_b - t_a:.3f} s, eigs {t_c - t_b:.3f} s, "
+                f"destroy {time.perf_counter() - t_c:.3f} s (host clocks)")
             if s > 0:                       # first one warms allocator / tensor maps
                 times.append(a.elapsed_time(z) / 1e3)
+            log(f"e2e step {s}: {a.elapsed_time(z) / 1e3:.3f} s")
         t_e2e = max_over_ranks(float(np.mean(times)), ws, device="cuda")
         h2d = p.D.nbytes + 8 * (p.n + 1) + 12 * p.nnz
         d2h = 8 * m + 2 * p.n * m * 4
         e2e = {"value": job_throughput(ws, iters, t_e2e), "unit": UNIT, "seconds_per_solve": t_e2e,
+               "seconds_each_step": [round(x, 4) for x in times],
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "includes": "sbmds_create from pinned host CSR + D (H2D, CSC build) + sbmds_eigs "
                            "(50 iters) + V, Z, eigenvalues to host + destroy"}

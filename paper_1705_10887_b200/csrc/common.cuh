@@ -52,16 +52,62 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Watchdog for pipeline waits: a wait that has not completed after ~4 s records where it is
+// stuck (tag, CTA, thread, parity) in host-mapped memory and traps, so a pipeline bug turns
+// into an SBMDS_ECUDA error with a location instead of a hung process.
+struct HangEntry {
+    unsigned int tag, block, thread, parity, bar_lo, bar_hi;
+};
+struct HangRecord {
+    unsigned int flag, count, pad0, pad1;
+    HangEntry e[512];
+};
+__device__ HangRecord* g_hang = nullptr;   // single translation unit (sbmds.cu)
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
         "{\n\t"
         ".reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t"
-        "}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t"
+        "}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+
+__device__ __noinline__ void mbar_hang(uint64_t* bar, uint32_t parity, int tag) {
+    HangRecord* r = g_hang;
+    if (r) {
+        const unsigned k = atomicAdd(&r->count, 1u);
+        if (k < 512) {
+            const uint64_t st = *reinterpret_cast<volatile uint64_t*>(bar);
+            r->e[k] = HangEntry{(unsigned)tag, blockIdx.x, threadIdx.x, parity, (unsigned)st, (unsigned)(st >> 32)};
+        }
+        r->flag = 1u;
+        __threadfence_system();
+        // let the other stuck waits of this launch time out and record themselves too
+        uint64_t t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); } while (t - t0 < 1500000000ull);
+    }
+    __trap();
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
+    if (mbar_try(bar, parity)) return;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (uint32_t k = 1;; ++k) {
+        if (mbar_try(bar, parity)) return;
+        if ((k & 1023u) == 0u) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 4000000000ull) mbar_hang(bar, parity, tag);
+        }
+    }
 }
 
 // 2-D TMA tile load global -> shared, completion on mbarrier (complete_tx bytes).

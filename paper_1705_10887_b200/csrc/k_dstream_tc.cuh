@@ -14,13 +14,15 @@
 //                    2bp x 32 (SWIZZLE_128B), complete_tx on full[s]
 //   warp 1           TMEM allocator; lane 0 issues the MMAs (SS: A = D_hi from smem; TS:
 //                    A = D_lo from TMEM) and tcgen05.commit -> empty[s] / acc_full[buf]
-//   warps 4-11       two converter groups (group g takes local stages li % 2 == g, so two
-//                    stages are converted concurrently): thread = tile row = TMEM lane; read
-//                    the row's 32 fp32 from the swizzled tile, D_lo -> tcgen05.st into TMEM
-//                    slot s, arrive lo_ready[s]. Every KC k-tiles both groups drain the
-//                    accumulators (tcgen05.ld), group g its half of the columns, into fp64
-//                    registers; at a row-tile boundary they write the fp64 partial for
-//                    k_dreduce (deterministic, same layout as the FFMA path).
+//   warps 4-7        converters: thread = tile row = TMEM lane; read the row's fp32 values
+//                    from the swizzled tile, D_lo -> tcgen05.st into TMEM slot s, arrive
+//                    lo_ready[s] (every stage)
+//   warps 8-11       epilogue: every KC k-tiles wait acc_full, drain the accumulators
+//                    (tcgen05.ld) into fp64 registers, arrive acc_empty; at a row-tile
+//                    boundary write the fp64 partial for k_dreduce (deterministic, same
+//                    layout as the FFMA path)
+// Each mbarrier has one producer role and one consumer role (canonical warp specialisation);
+// an earlier variant in which two converter groups also drained with a lag could deadlock.
 #pragma once
 #include "common.cuh"
 #include "k_dstream.cuh"
@@ -50,8 +52,7 @@ struct TcCfg {
     static constexpr int ACC0 = 0;                       // acc buffer b at column b*ACC_COLS
     static constexpr int LO0 = 2 * ACC_COLS;             // A_lo slots
     static constexpr int KC = NA == 3 ? 5 : 16 / NA;     // k-tiles per accumulator drain (~512 k)
-    static constexpr int NGROUP = 2;                     // converter groups (alternate stages)
-    static constexpr int THREADS = (4 + 4 * NGROUP) * 32;
+    static constexpr int THREADS = 12 * 32;               // producer, MMA, 2 idle, converters, epilogue
     static constexpr int SMEM = NS * STAGE_BYTES + 1024 + 256;
     static_assert(NS >= 2, "stages");
     static_assert(LO0 + NS * 32 * NA <= TMEM_COLS, "tmem");
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(TcCfg<BP>::THREADS, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 128 * C::NGROUP);
+            mbar_init(&acc_empty[b], 128);
         }
         fence_barrier_init();
     }
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(TcCfg<BP>::THREADS, 1)
             int32_t rt = (int32_t)(it0 / sk.KT), kt = (int32_t)(it0 % sk.KT);
             const int32_t KT = (int32_t)sk.KT;
             for (int64_t it = it0; it < it1; ++it) {
-                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_wait(&empty[s], ph ^ 1u, 101 * 65536 + (int)((it - it0) & 0xFFFF));
                 uint8_t* st = base + s * C::STAGE_BYTES;
                 mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
 #pragma unroll
@@ -223,11 +224,11 @@ __global__ void __launch_bounds__(TcCfg<BP>::THREADS, 1)
             for (int64_t it = it0; it < it1; ++it) {
                 if (first) {
                     // wait until the epilogue has drained this accumulator buffer (2 chunks ago)
-                    mbar_wait(&acc_empty[buf], (uint32_t)(((nchunk >> 1) & 1) ^ 1));
+                    mbar_wait(&acc_empty[buf], (uint32_t)(((nchunk >> 1) & 1) ^ 1), 102 * 65536 + (int)((it - it0) & 0xFFFF));
                     tc_fence_after();
                 }
-                mbar_wait(&full[s], ph);
-                mbar_wait(&lo_ready[s], ph);
+                mbar_wait(&full[s], ph, 103 * 65536 + (int)((it - it0) & 0xFFFF));
+                mbar_wait(&lo_ready[s], ph, 104 * 65536 + (int)((it - it0) & 0xFFFF));
                 tc_fence_after();
                 const uint32_t sa = smem_u32(base + s * C::STAGE_BYTES);
                 const uint32_t sb = sa + C::A_BYTES;
@@ -256,105 +257,85 @@ __global__ void __launch_bounds__(TcCfg<BP>::THREADS, 1)
                 if (++kt == KT) kt = 0;
             }
         }
-    } else if (warp >= 4) {
-        // ------------------------------------------------ converters + epilogue (row = TMEM lane)
-        const int g = (warp - 4) / 4;           // converter group
-        const int q = (warp - 4) % 4;           // TMEM lane quarter (= warp % 4)
-        const int row = 32 * q + lane;          // row within the 128-row tile
+    } else if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ converters (row = TMEM lane)
+        const int q = warp - 4;
+        const int row = 32 * q + lane;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-        constexpr int HB = BP / C::NGROUP;      // accumulator columns drained by this group
-        const int cbase = g * HB;
-        double acc64[HB];
-#pragma unroll
-        for (int j = 0; j < HB; ++j) acc64[j] = 0.0;
-        int buf = 0, nchunk = 0;
-        int s = 0, gsel = 0;
+        int s = 0;
         uint32_t ph = 0;
+        for (int64_t it = it0; it < it1; ++it) {
+            mbar_wait(&full[s], ph, 106 * 65536 + (int)((it - it0) & 0xFFFF));
+#pragma unroll
+            for (int a = 0; a < C::NA; ++a) {
+                const uint8_t* ta = base + s * C::STAGE_BYTES + a * C::A_ATOM + row * 128;
+                uint32_t lo[32];
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const float4 v = *reinterpret_cast<const float4*>(ta + ((cc ^ (row & 7)) << 4));
+                    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float hi = __uint_as_float(__float_as_uint(x[u]) & 0xFFFFE000u);
+                        lo[4 * cc + u] = __float_as_uint(x[u] - hi);
+                    }
+                }
+                tmem_st32(tbase + lane_off + C::LO0 + (s * C::NA + a) * 32, lo);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&lo_ready[s]);
+            if (++s == C::NS) { s = 0; ph ^= 1u; }
+        }
+    } else if (warp >= 8) {
+        // ------------------------------------------------ epilogue (row = TMEM lane)
+        const int q = warp - 8;
+        const int row = 32 * q + lane;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        double acc64[BP];
+#pragma unroll
+        for (int j = 0; j < BP; ++j) acc64[j] = 0.0;
+        int buf = 0, nchunk = 0;
         int32_t rt = (int32_t)(it0 / sk.KT), kt = (int32_t)(it0 % sk.KT);
         int seg = c - sk.cta_of((int64_t)rt * sk.KT);
-        // A finished chunk is drained DRAIN_LAG stages later (the MMA meanwhile fills the
-        // other accumulator buffer), so conversion never waits on the tensor-core commit.
-        constexpr int DRAIN_LAG = 4;
-        bool pend = false, pend_flush = false;
-        int pend_buf = 0, pend_n = 0, pend_age = 0;
-        int64_t pend_out = 0;
-        auto drain = [&]() {
-            mbar_wait(&acc_full[pend_buf], (uint32_t)((pend_n >> 1) & 1));
-            tc_fence_after();
-            const uint32_t t1 = tbase + lane_off + C::ACC0 + pend_buf * C::ACC_COLS;
-            const uint32_t t2 = t1 + C::N1C;
+        for (int64_t it = it0; it < it1; ++it) {
+            if (chunk_end(it, kt)) {
+                mbar_wait(&acc_full[buf], (uint32_t)((nchunk >> 1) & 1), 105 * 65536 + nchunk);
+                tc_fence_after();
+                const uint32_t t1 = tbase + lane_off + C::ACC0 + buf * C::ACC_COLS;
+                const uint32_t t2 = t1 + C::N1C;
 #pragma unroll
-            for (int c0 = 0; c0 < HB; c0 += 4) {
-                float h0[8], h1[8], l0[8];
-                const int cb = cbase + c0;       // x8 loads stay 8-column aligned
-                const int al = cb & ~7, off = cb - al;
-                tmem_ld8(t1 + al, h0);
-                tmem_ld8(t1 + BP + al, h1);
-                tmem_ld8(t2 + al, l0);
-                tmem_wait_ld();
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    acc64[c0 + u] += ((double)h0[off + u] + (double)h1[off + u]) + (double)l0[off + u];
-                if constexpr (C::N2 > BP) {  // b = 8: the D_lo * Y_lo rows of the second product
-                    float l1[8];
-                    tmem_ld8(t2 + BP + al, l1);
+                for (int c0 = 0; c0 < BP; c0 += 8) {
+                    float h0[8], h1[8], l0[8];
+                    tmem_ld8(t1 + c0, h0);
+                    tmem_ld8(t1 + BP + c0, h1);
+                    tmem_ld8(t2 + c0, l0);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) acc64[c0 + u] += (double)l1[off + u];
-                }
-            }
-            tc_fence_before();
-            mbar_arrive(&acc_empty[pend_buf]);
-            if (pend_flush) {
-                double* out = P + pend_out;
+                    for (int u = 0; u < 8; ++u) acc64[c0 + u] += ((double)h0[u] + (double)h1[u]) + (double)l0[u];
+                    if constexpr (C::N2 > BP) {  // b = 8: the D_lo * Y_lo rows of the second product
+                        float l1[8];
+                        tmem_ld8(t2 + BP + c0, l1);
+                        tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < HB; ++j) {
-                    out[j] = acc64[j];
-                    acc64[j] = 0.0;
-                }
-            }
-            pend = false;
-        };
-        for (int64_t it = it0; it < it1; ++it) {
-            if (gsel == g) {
-                mbar_wait(&full[s], ph);
-#pragma unroll
-                for (int a = 0; a < C::NA; ++a) {
-                    const uint8_t* ta = base + s * C::STAGE_BYTES + a * C::A_ATOM + row * 128;
-                    uint32_t lo[32];
-#pragma unroll
-                    for (int cc = 0; cc < 8; ++cc) {
-                        const float4 v = *reinterpret_cast<const float4*>(ta + ((cc ^ (row & 7)) << 4));
-                        const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const float hi = __uint_as_float(__float_as_uint(x[u]) & 0xFFFFE000u);
-                            lo[4 * cc + u] = __float_as_uint(x[u] - hi);
-                        }
+                        for (int u = 0; u < 8; ++u) acc64[c0 + u] += (double)l1[u];
                     }
-                    tmem_st32(tbase + lane_off + C::LO0 + (s * C::NA + a) * 32, lo);
                 }
-                tmem_wait_st();
                 tc_fence_before();
-                mbar_arrive(&lo_ready[s]);
-            }
-            if (pend && ++pend_age >= DRAIN_LAG) drain();
-            if (chunk_end(it, kt)) {
-                if (pend) drain();
-                pend = true;
-                pend_buf = buf;
-                pend_n = nchunk;
-                pend_age = 0;
-                pend_flush = (it + 1 == it1) || (kt + 1 == KT);
-                pend_out = (((int64_t)rt * maxseg + seg) * (int64_t)C::TM + row) * BP + cbase;
+                mbar_arrive(&acc_empty[buf]);
                 buf ^= 1;
                 ++nchunk;
+                if (it + 1 == it1 || kt + 1 == KT) {   // row-tile boundary: write the partial
+                    double* out = P + (((int64_t)rt * maxseg + seg) * (int64_t)C::TM + row) * BP;
+#pragma unroll
+                    for (int j = 0; j < BP; ++j) {
+                        out[j] = acc64[j];
+                        acc64[j] = 0.0;
+                    }
+                }
             }
-            if (++s == C::NS) { s = 0; ph ^= 1u; }
-            if (++gsel == C::NGROUP) gsel = 0;
             if (++kt == KT) { kt = 0; ++rt; seg = 0; }   // a later row tile starts with this CTA
         }
-        if (pend) drain();
     }
     tc_fence_before();
     __syncthreads();

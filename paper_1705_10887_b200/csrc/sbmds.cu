@@ -61,6 +61,46 @@ void launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args.
     CK(cudaGetLastError());
 }
 
+HangRecord* g_hang_host = nullptr;
+
+// Host-mapped record the device watchdog writes before trapping (common.cuh mbar_wait).
+void install_hang_record() {
+    static bool done = false;
+    if (done) return;
+    HangRecord* hp = nullptr;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&hp), sizeof(HangRecord), cudaHostAllocMapped) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    memset(hp, 0, sizeof(HangRecord));
+    HangRecord* dp = nullptr;
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), hp, 0) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_hang, &dp, sizeof(dp)) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    g_hang_host = hp;
+    done = true;
+}
+
+std::string hang_note() {
+    if (!g_hang_host || !g_hang_host->flag) return "";
+    std::string out = " [pipeline watchdog:";
+    const unsigned n = std::min(512u, g_hang_host->count);
+    std::vector<uint64_t> seen;
+    for (unsigned k = 0; k < n; ++k) {
+        const HangEntry& e = g_hang_host->e[k];
+        const uint64_t key = ((uint64_t)e.tag << 32) | ((uint64_t)e.block << 8) | (e.thread / 32);
+        if (std::find(seen.begin(), seen.end(), key) != seen.end()) continue;   // one line per (tag, block, warp)
+        seen.push_back(key);
+        char buf[128];
+        snprintf(buf, sizeof buf, " tag %u.%u blk %u thr %u par %u;", e.tag >> 16, e.tag & 0xFFFF, e.block, e.thread,
+                 e.parity);
+        out += buf;
+    }
+    return out + "]";
+}
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -77,28 +117,56 @@ int next_pow2(int b) {
     return p;
 }
 
+// Device buffers. Long-lived handle buffers (`pooled`) come from the device's default
+// stream-ordered memory pool with an unbounded release threshold, so memory freed by
+// sbmds_destroy stays mapped and the next sbmds_create reuses it (re-mapping ~12 GB per
+// create/destroy cycle cost 0.1-0.3 s stalls). Frees of pooled buffers happen only when the
+// device is idle for them (destroy syncs first; a growing ensure() syncs before freeing).
+// Create-time temporaries use plain cudaMalloc/cudaFree.
+void configure_pool_once() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done = true;
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    bool pooled = false;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void ensure(size_t nb) {
         if (nb <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        cudaError_t e = cudaMalloc(&p, nb);
+        if (p && pooled) cudaDeviceSynchronize();   // the old buffer may still be in flight
+        release();
+        cudaError_t e;
+        if (pooled) {
+            e = cudaMallocAsync(&p, nb, 0);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+        } else {
+            e = cudaMalloc(&p, nb);
+        }
         if (e != cudaSuccess) {
             cudaGetLastError();
             p = nullptr;
-            throw CudaError{e, "cudaMalloc"};
+            throw CudaError{e, pooled ? "cudaMallocAsync" : "cudaMalloc"};
         }
         bytes = nb;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (pooled) cudaFreeAsync(p, 0);
+            else cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -686,14 +754,20 @@ void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
     h->blocked = true;
 }
 
-void destroy_ctx(sbmds_ctx* h) {
-    if (!h) return;
+template <typename F>
+void for_each_buf(sbmds_ctx* h, F&& f) {
     DevBuf* bufs[] = {&h->rp, &h->col, &h->val, &h->cptr, &h->ridx, &h->cval, &h->order, &h->w, &h->Dbuf,
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->PT};
-    for (DevBuf* b : bufs) b->release();
+    for (DevBuf* b : bufs) f(b);
+}
+
+void destroy_ctx(sbmds_ctx* h) {
+    if (!h) return;
+    for_each_buf(h, [](DevBuf* b) { b->release(); });
+    cudaStreamSynchronize(0);
     delete h;
 }
 
@@ -717,6 +791,9 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     try {
         CK(cudaGetDevice(&h->dev));
         CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
+        install_hang_record();
+        configure_pool_once();
+        for_each_buf(h, [](DevBuf* b) { b->pooled = true; });
         const int64_t nz = std::max<int64_t>(nnz, 1);
         h->rp.ensure((n + 1) * sizeof(int32_t));
         h->col.ensure(nz * sizeof(int32_t));
@@ -869,7 +946,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     } catch (const CudaError& e) {
         destroy_ctx(h);
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
-        return fail(SBMDS_ECUDA, "%s: %s", e.what, cudaGetErrorString(e.e));
+        return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
     }
     *out = h;
     return SBMDS_OK;
@@ -919,7 +996,7 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
         if (!xd || !yd) CK(cudaStreamSynchronize(st));
     } catch (const CudaError& e) {
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
-        return fail(SBMDS_ECUDA, "%s: %s", e.what, cudaGetErrorString(e.e));
+        return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
     }
     return SBMDS_OK;
 }
@@ -1162,7 +1239,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                                                 max_iters, rr_host.maxres);
     } catch (const CudaError& e) {
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
-        return fail(SBMDS_ECUDA, "%s: %s", e.what, cudaGetErrorString(e.e));
+        return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
     }
     return ret;
 }
