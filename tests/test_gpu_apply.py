@@ -217,3 +217,61 @@ def test_symmetric_half_eigs_config2():
         h.set_option("dstream", 3)
         lam_b, _, _, _ = h.eigs(p.m, p.block, max_iters=200, tol=1e-6)
     assert np.allclose(lam_a, lam_b, rtol=1e-5)
+
+
+def test_degenerate_inputs():
+    """l = 1 (D = [[0]]), nnz = 0 (S = 0) and empty rows: B~X = 0 where the algebra says so,
+    and the oracle agrees everywhere."""
+    from paper_1705_10887_b200 import Sbmds
+    torch = _torch()
+    n = 1000
+    X = configs.x_block(n, 8, seed=1)
+    # l = 1: every row of S is e_1 -> J S = 0 -> B~ = 0
+    rp = np.arange(n + 1, dtype=np.int64)
+    h = Sbmds(n, 1, rp, np.zeros(n, np.int32), np.ones(n, np.float32), np.zeros((1, 1), np.float32))
+    Y = h.apply(torch.from_numpy(X).cuda()).cpu().numpy()
+    h.close()
+    assert np.abs(Y).max() < 1e-6 * np.abs(X).max()
+    # nnz = 0
+    h = Sbmds(n, 7, np.zeros(n + 1, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32),
+              np.ones((7, 7), np.float32))
+    Y = h.apply(torch.from_numpy(X).cuda()).cpu().numpy()
+    h.close()
+    assert np.abs(Y).max() == 0.0
+    # empty rows interleaved with full ones
+    p = synth_problem(n=3000, l=300, k=6, seed=9)
+    lens = np.diff(p.row_ptr)
+    keep = np.arange(p.n) % 3 != 0                        # every third row empty
+    new_lens = np.where(keep, lens, 0)
+    rp2 = np.zeros(p.n + 1, np.int64)
+    rp2[1:] = np.cumsum(new_lens)
+    mask = np.repeat(keep, lens)
+    q = configs.Problem("emptyrows", p.n, p.l, rp2, p.col_idx[mask], p.val[mask], p.D)
+    for b in (4, 16):
+        Xq = configs.x_block(q.n, b, seed=b)
+        with make_handle(q) as hq:
+            Yq = run_apply(hq, Xq)
+        assert relerr(Yq, oracle_apply(q, Xq)) <= TOL
+
+
+def test_borrowed_device_d():
+    """SBMDS_BORROW_D keeps the caller's device D (l % 4 == 0) and gives identical results."""
+    p = configs.config(2)
+    X = configs.x_block(p.n, 16, seed=2)
+    with make_handle(p) as h1, make_handle(p, borrow_d=True) as h2:
+        assert h1.stat("d_borrowed") == 0 and h2.stat("d_borrowed") == 1
+        assert np.array_equal(run_apply(h1, X), run_apply(h2, X))
+
+
+def test_invalid_eigs_arguments():
+    from paper_1705_10887_b200 import SbmdsError
+    p = configs.config(1)
+    with make_handle(p) as h:
+        for m, block, iters in ((3, 65, 10), (9, 8, 10), (0, 8, 10), (3, 8, 0)):
+            with pytest.raises(SbmdsError, match="EINVAL"):
+                h.eigs(m, block, max_iters=iters)
+        Dbad = p.D.copy()
+        Dbad[3, 3] = np.nan
+    from paper_1705_10887_b200 import Sbmds
+    with pytest.raises(SbmdsError, match="non-finite"):
+        Sbmds(p.n, p.l, p.row_ptr, p.col_idx, p.val32(), Dbad, validate=True)

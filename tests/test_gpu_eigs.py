@@ -129,3 +129,23 @@ def test_eigs_gram_paths_agree(gram_tc):
         h.set_option("gram_tc", gram_tc)
         lam, V, Z, info = gpu_eigs(h, p.m, p.block, max_iters=500, tol=1e-6)
     check_against(lam, V, Z, lam_o, V_o, Z_o)
+
+
+def test_eigs_block64_and_m_equals_block():
+    """block = 64 (the widest tcgen05 path, two swizzle atoms per stage) and m = block."""
+    p = configs.config(2)
+    rng = np.random.default_rng(8)
+    Yl = rng.standard_normal((p.l, 3)) * [3.0, 2.0, 1.0]
+    D = ((Yl[:, None, :] - Yl[None, :, :]) ** 2).sum(-1).astype(np.float32)
+    q = configs.Problem("cf2", p.n, p.l, p.row_ptr, p.col_idx, p.val, D)
+    S = O.csr(q.n, q.l, q.row_ptr, q.col_idx, q.val32())
+    JSY = S @ Yl
+    JSY -= JSY.mean(0)
+    U, s, _ = np.linalg.svd(JSY, full_matrices=False)
+    with handle(q) as h:
+        lam, V, Z, info = gpu_eigs(h, 3, 64, max_iters=100, tol=1e-6)
+        lam8, V8, _, _ = gpu_eigs(h, 8, 8, max_iters=100, tol=0.0)
+    assert np.all(np.abs(lam - s ** 2) <= EIG_TOL * s ** 2)
+    assert O.principal_angle(V, U) <= ANGLE_TOL
+    assert np.allclose(lam8[:3], s ** 2, rtol=1e-4)        # m = block: the rank-3 part, then ~0
+    assert np.all(np.abs(lam8[3:]) < 1e-3 * s[0] ** 2)
