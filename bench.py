@@ -151,10 +151,8 @@ def algorithmic_bytes(p, b):
     return 4 * p.l * p.l + 16 * p.nnz + 4 * (p.n + 1) + 4 * (p.l + 1) + 8 * p.n * b
 
 
-def dstream_bytes(p, b):
-    """Dominant kernel (k_dstream_tc / k_dstream_ffma): D read once (4 l^2) + Y1 read + Y2 partials
-    written (12 l b) — DESIGN.md §4."""
-    return 4 * p.l * p.l + 4 * p.l * b + 8 * p.l * b
+DSTREAM_KERNELS = {1: "k_dstream_ffma", 2: "k_dstream_tc (tcgen05 3xTF32, full D)",
+                   3: "k_dstream_pair (tcgen05 2xFP16, symmetric half of D, CTA pairs)"}
 
 
 def log(msg):
@@ -189,7 +187,7 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     log("warmup done")
     barrier(ws)
-    h.set_option("profile", 1 << 2)          # CUDA events around k_dstream_ffma only
+    h.set_option("profile", 1 << 2)          # CUDA events around the D-stream kernel only
     h.set_option("profile_reset", 1)
     n0 = launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -204,12 +202,13 @@ def run_ours(args, ws, rank, local):
     n_launch = launch_count() - n0
     ms = e0.elapsed_time(e1)
     ds_ns, ds_n = h.stat("dstream_ns"), h.stat("dstream_launches")
+    ds_path, ds_bytes = h.stat("dstream_path"), h.stat("dstream_bytes")   # per launch, DESIGN.md §4
     h.set_option("profile", 0)
     ms_max = max_over_ranks(ms, ws, device="cuda")
     applies = sum(i["n_applies"] for i in infos)
     value = job_throughput(ws, applies, ms_max / 1e3)
     ds_avg_s = ds_ns / max(ds_n, 1) / 1e9
-    ds_gbs = dstream_bytes(p, b) / ds_avg_s / 1e9
+    ds_gbs = ds_bytes / ds_avg_s / 1e9
     apply_gbs = algorithmic_bytes(p, b) * applies / (ms / 1e3) / 1e9
     eigs_s = ms / 1e3 / args.steps
 
@@ -262,7 +261,8 @@ def run_ours(args, ws, rank, local):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if ds_path != 3 else "f32 (D Y1 as a 2xfp16 split, fp32 accumulate; DESIGN.md §4)",
         "data": "synthetic (seeded torus mesh stand-in for Dragon1800k; DESIGN.md §3)",
         "config": {"workload": f"config {args.config}: {p.name}", "n": p.n, "l": p.l, "k": 32,
                    "nnz": p.nnz, "block": b, "m": m, "iters_per_step": iters,
@@ -272,11 +272,11 @@ def run_ours(args, ws, rank, local):
         "eigenvalues": [float(x) for x in lam],
         "max_residual": info["max_residual"], "orth_error": info["orth_error"],
         "roofline": {"bound": "hbm", "achieved": ds_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": ds_gbs / hbm_peak, "traffic": load_traffic(),
-                     "kernel": "k_dstream_tc<16> (tcgen05 3xTF32)" if b >= 5 else "k_dstream_ffma",
-                     "launches": ds_n,
+                     "frac": ds_gbs / hbm_peak, "traffic": load_traffic(ds_path),
+                     "kernel": DSTREAM_KERNELS.get(ds_path, str(ds_path)), "launches": ds_n,
                      "avg_launch_ms": ds_avg_s * 1e3, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": dstream_bytes(p, b)},
+                     "algorithmic_bytes_per_launch": ds_bytes,
+                     "full_d_equivalent_gbs": 4 * p.l * p.l / ds_avg_s / 1e9},
         "gpu_launches": int(n_launch),
         "clocks": clk.summary(),
     }
@@ -287,11 +287,12 @@ def run_ours(args, ws, rank, local):
     return out
 
 
-def load_traffic():
-    """DRAM bytes per k_dstream_ffma launch from the committed ncu --set full summary."""
+def load_traffic(path_id):
+    """DRAM bytes per launch of the D-stream kernel from the committed ncu --set full summary."""
     path = os.path.join(ROOT, "profiles", "dstream_traffic.json")
     try:
-        return json.load(open(path))["dram_bytes_per_launch"]
+        d = json.load(open(path))
+        return d.get("by_path", {}).get(str(path_id), d.get("dram_bytes_per_launch") if path_id == 2 else None)
     except Exception:
         return None
 

@@ -1,0 +1,524 @@
+// A3 on the symmetric half of D: Y2 = D Y1 reading only the
+// 128 x 128 tiles D_IJ with I <= J, each applied as D_IJ Y1_J (to rows I) and, for I < J,
+// as D_IJ^T Y1_I (to rows J). D is symmetric (P:111 E, P:215 W = D_ll).
+//
+// Arithmetic: "2xFP16" on tcgen05 kind::f16 (f32 accumulate). D is stored pre-scaled by an
+// exact power of two 2^sD and pre-split (k_pack_upper, once per handle) into two fp16
+// planes a = h1 + h2, h1 = f16(a), h2 = f16(a - h1) -- 4 bytes per element, the same as
+// fp32 -- and each column c of Y1 is scaled by 2^e_c and split the same way into y1, y2
+// (k_y16_split). The product keeps h1 y1 + h1 y2 + h2 y1 (b = 8: also h2 y2). Each piece
+// carries 11 significant bits, so a and y are represented to 2^-22 relative and the dropped
+// h2 y2 is 2^-22 relative: the class of 3xTF32, but a kind::f16 MMA covers K = 16 where
+// kind::tf32 covers K = 8 at the same cost per instruction (scripts/mma_cost_probe.cu: ~93
+// cycles for M = 128, N <= 64 either way), and nothing is converted in the stream (the
+// fp32 -> fp16 conversions ran at ~16/clk/SM in an in-kernel converter variant and bound
+// it). k_dreduce_pair undoes the scales (exact).
+//
+// Two products per tile: D_IJ by rows (N: M = i, K = j) and by columns (T: M = j, K = i).
+// For 16-bit types one SWIZZLE_128B image -- row i holds 64 consecutive j in 128 bytes,
+// 16-byte granule g at g ^ (i & 7) -- is both a K-major A operand (N) and an MN-major A
+// operand (T), so both products run as SS MMAs straight from the staged chunk. A CLUSTER
+// OF TWO CTAs streams the same tile sequence: rank 0 ("N") stages each tile as two
+// 64-column chunks, rank 1 ("T") as two 64-row chunks. Both CTAs' requests for a tile reach
+// L2 within a few tiles of each other and DRAM serves the tile once (scripts/sym_probe.cu;
+// ncu: DRAM bytes = the packed triangle). The producers couple through DSMEM (at most
+// kPairLag tiles apart), which keeps the pair inside L2's reuse window.
+//
+// Packed tile (64 KB, row-major over the upper triangle, so a block row of the walk reads
+// runs of S consecutive tiles): plane h1 then plane h2, each two 64-column boxes of 128 rows
+// x 128 bytes in the swizzled image above. A chunk is two 16 KB (N) or four 8 KB (T) plain
+// bulk copies.
+//
+// Walk: blocks of S x S tiles, block rows bi, block columns bj >= bi, inside a block
+// row-major; tiles with J < I or beyond l are absent. Each pair owns a contiguous range of
+// the walk (balanced tile counts). A "segment" is the part of one block inside one range.
+//
+// Accumulation: per tile a fresh TMEM accumulator (double-buffered) takes the tile's
+// 8 k-steps; the epilogue adds its column groups and folds the tile into a per-segment
+// fp32 accumulator kept in TMEM (row r for N, column c for T; round-to-nearest FADD, at
+// most S terms); at segment end each touched one becomes an fp32 partial (128 x bp) in a
+// slot numbered by the host schedule, and k_dreduce_pair adds each row tile's slots in
+// slot order in fp64 (deterministic). Tensor-core chains are 16 MMAs long: the tensor-core
+// accumulator does not round to nearest, so long chains would bias the sum.
+//
+// Roles per CTA (192 threads): warp 0 producer, warp 1 TMEM alloc + MMA issue, warps 2-5
+// epilogue. Each mbarrier has one producer role and one consumer role.
+#pragma once
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "k_dstream_tc.cuh"
+
+namespace sbmds {
+
+constexpr int kPairLag = 2;   // max tiles a pair CTA's producer may run ahead of its partner
+
+template <int BP>
+struct PairCfg {
+    static constexpr int TT = 128;                   // tile edge (MMA M, and K per tile)
+    static constexpr int KC = 64;                    // k per pipeline chunk (2 chunks per tile)
+    static constexpr int NB = 2 * BP;                // B rows [y1; y2] (fp16)
+    static constexpr int N2 = BP < 16 ? 16 : BP;     // N of the h2 product (>= 16 for M = 128)
+    static constexpr int ACCB = (NB + 31) / 32 * 32; // TMEM columns of one tile accumulator
+    static constexpr int LL0 = 2 * ACCB;             // per-segment accumulators (S x BP columns)
+    static constexpr int S = (512 - LL0) / BP > 16 ? 16 : (512 - LL0) / BP;   // block edge in tiles
+    static constexpr int TMEM_COLS = LL0 + S * BP <= 256 ? 256 : 512;
+    static constexpr int A_BYTES = 2 * TT * KC * 2;  // 32 KB: the chunk of both fp16 planes
+    static constexpr int BOX_B = NB * 128;           // the chunk's 64-k slice of [y1; y2]
+    static constexpr int STAGE = A_BYTES + BOX_B;
+    static constexpr int NS = (208 * 1024) / STAGE > 8 ? 8 : (208 * 1024) / STAGE;
+    static constexpr int THREADS = 6 * 32;           // producer, MMA, 4 epilogue warps
+    static constexpr int SMEM = NS * STAGE + 1024 + 1024;
+    static_assert(STAGE % 1024 == 0, "stage alignment");
+    static_assert(S <= 16, "masks are 16-bit");
+};
+
+// one epilogue event per processed tile (and per segment end): which per-segment
+// accumulator the tile folds into, whether it is its first tile in the segment, and the
+// segment flush (mask of accumulators, first slot, last event of the CTA)
+struct PairEvent {
+    uint32_t has_tile, a, first, mask, slot, last, pad0, pad1;
+};
+
+__device__ __forceinline__ void pair_spin_hang(const uint32_t* p, uint32_t want, int tag) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (uint32_t k = 1;; ++k) {
+        if (ld_relaxed_u32(p) >= want) return;
+        if ((k & 1023u) == 0u) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 4000000000ull) mbar_hang(reinterpret_cast<uint64_t*>(const_cast<uint32_t*>(p)), want, tag);
+        }
+    }
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
+}
+
+__host__ __device__ constexpr uint32_t idesc_f16_f32acc(int M, int N, int a_mn = 0) {
+    // c_format F32 (bit 4), a/b_format F16 (0), A K- or MN-major (bit 15), B K-major,
+    // n_dim = N >> 3, m_dim = M >> 4
+    return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// SWIZZLE_128B shared-memory descriptor with explicit LBO / SBO (bytes)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void tc_mma_ss_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// storage position of upper tile (I, J), I <= J: row-major over the upper triangle
+__host__ __device__ __forceinline__ int64_t upper_tile_index(int I, int J, int NT) {
+    return (int64_t)I * NT - (int64_t)I * (I - 1) / 2 + (J - I);
+}
+
+template <int BP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BP>::THREADS, 1)
+    k_dstream_pair(const __half* __restrict__ Dt, const __grid_constant__ CUtensorMap bmap,
+                   const uint32_t* __restrict__ tiles, const int64_t* __restrict__ pbeg,
+                   const int* __restrict__ sbase, int NT, float* __restrict__ P,
+                   unsigned long long* __restrict__ dbg, int dbg_mode) {
+    using C = PairCfg<BP>;
+    constexpr int S = C::S;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + C::NS * C::STAGE);
+    uint64_t* empty = full + C::NS;
+    uint64_t* acc_full = empty + C::NS;       // [2] tile accumulator + event ready
+    uint64_t* acc_empty = acc_full + 2;       // [2] event consumed
+    PairEvent* evq = reinterpret_cast<PairEvent*>(acc_empty + 2);   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(evq + 2);
+    uint32_t* progress = tmem_slot + 2;       // written by the partner CTA (8-byte aligned)
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t role = cluster_ctarank();  // 0 = N (D_IJ Y1_J), 1 = T (D_IJ^T Y1_I)
+    const int pair = blockIdx.x >> 1;
+    const int64_t t0 = pbeg[pair], t1 = (dbg_mode & 32) && role == 1 ? pbeg[pair] : pbeg[pair + 1];
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&acc_full[s], 2);     // tcgen05.commit + the MMA thread's event arrive
+            mbar_init(&acc_empty[s], 128);
+        }
+        progress[0] = 0u;
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(C::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();   // barrier inits and progress = 0 visible to the partner before any DSMEM store
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+
+    // optional wait-time instrumentation (option pair_dbg): one thread per role sums clock64
+    // cycles per wait site into dbg[cta * 16 + site]
+    unsigned long long tw[4] = {0ull, 0ull, 0ull, 0ull};
+    auto twait = [&](uint64_t* bar, uint32_t par, int tag, int k) {
+        if (dbg) {
+            const long long c0 = clock64();
+            mbar_wait(bar, par, tag);
+            tw[k] += (unsigned long long)(clock64() - c0);
+        } else {
+            mbar_wait(bar, par, tag);
+        }
+    };
+    const long long tk0 = clock64();
+    auto tflush = [&](int site0) {
+        if (dbg && lane == 0) {
+            for (int k = 0; k < 3; ++k) dbg[blockIdx.x * 16 + site0 + k] = tw[k];
+            dbg[blockIdx.x * 16 + site0 + 3] = (unsigned long long)(clock64() - tk0);
+        }
+    };
+
+    auto tile_of = [&](int64_t t, int& I, int& J) {
+        const uint32_t v = __ldg(tiles + t);
+        I = (int)(v >> 16);
+        J = (int)(v & 0xFFFFu);
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------ producer (bulk copies + Y TMA)
+        if (lane == 0) {
+            prefetch_tensormap(&bmap);
+            const uint64_t polb = policy_evict_last();
+            const uint32_t partner_progress = mapa_shared(progress, role ^ 1u);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t t = t0; t < t1; ++t) {
+                const uint32_t k = (uint32_t)(t - t0);
+                if (k > (uint32_t)kPairLag && !(dbg_mode & 16)) {
+                    const long long c0 = dbg ? clock64() : 0;
+                    pair_spin_hang(progress, k - kPairLag, 107 * 65536 + (int)(k & 0xFFFF));
+                    if (dbg) tw[0] += (unsigned long long)(clock64() - c0);
+                }
+                int I, J;
+                tile_of(t, I, J);
+                if (!(role == 1 && I == J)) {
+                    const uint8_t* tile = reinterpret_cast<const uint8_t*>(Dt) + upper_tile_index(I, J, NT) * 65536;
+                    const int kb = (role ? I : J) * C::TT;   // k offset of this tile's Y1 slice
+#pragma unroll 1
+                    for (int q = 0; q < 2; ++q) {
+                        twait(&empty[s], ph ^ 1u, 101 * 65536 + (int)(k & 0xFFFF), 1);
+                        uint8_t* st = base + s * C::STAGE;
+                        mbar_arrive_expect_tx(&full[s], C::STAGE);
+                        if (role == 0) {   // columns 64q .. 64q+63 (box q) of both planes
+                            bulk_load(st, tile + q * 16384, 16384, &full[s]);
+                            bulk_load(st + 16384, tile + 32768 + q * 16384, 16384, &full[s]);
+                        } else {           // rows 64q .. 64q+63 of both boxes of both planes
+#pragma unroll
+                            for (int pb = 0; pb < 4; ++pb)
+                                bulk_load(st + pb * 8192, tile + pb * 16384 + q * 8192, 8192, &full[s]);
+                        }
+                        tma_load_2d(st + C::A_BYTES, &bmap, &full[s], kb + 64 * q, 0, polb);
+                        if (++s == C::NS) { s = 0; ph ^= 1u; }
+                    }
+                }
+                st_cluster_u32(partner_progress, k + 1);
+            }
+            tflush(0);
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (A = fp16 planes from smem)
+        // the whole warp runs the loop (warp-uniform operands); one elected lane issues
+        constexpr uint32_t id1n = idesc_f16_f32acc(C::TT, C::NB, 0), id2n = idesc_f16_f32acc(C::TT, C::N2, 0);
+        constexpr uint32_t id1t = idesc_f16_f32acc(C::TT, C::NB, 1), id2t = idesc_f16_f32acc(C::TT, C::N2, 1);
+        const uint32_t id1 = role ? id1t : id1n, id2 = role ? id2t : id2n;
+        int s = 0;
+        uint32_t ph = 0;
+        uint32_t kc = 0, ev = 0, mask = 0;
+        uint32_t slot = (uint32_t)sbase[2 * pair + role];
+        for (int64_t t = t0; t < t1; ++t) {
+            int I, J;
+            tile_of(t, I, J);
+            const int bi = I / S, bj = J / S;
+            bool end_seg = (t + 1 == t1);
+            if (!end_seg) {
+                int I2, J2;
+                tile_of(t + 1, I2, J2);
+                end_seg = (I2 / S != bi) || (J2 / S != bj);
+            }
+            const bool skip = (role == 1 && I == J);
+            if (skip && !end_seg) continue;
+            const int buf = ev & 1;
+            twait(&acc_empty[buf], ((ev >> 1) & 1u) ^ 1u, 102 * 65536 + (int)(ev & 0xFFFF), 0);
+            tc_fence_after();
+            const int a = role ? (J - bj * S) : (I - bi * S);
+            const uint32_t bit = 1u << a;
+            PairEvent e{0u, (uint32_t)a, (mask & bit) ? 0u : 1u, 0u, slot, (t + 1 == t1) ? 1u : 0u, 0u, 0u};
+            if (!skip) {
+                e.has_tile = 1u;
+                mask |= bit;
+                const uint32_t dacc = tbase + (uint32_t)(buf * C::ACCB);
+#pragma unroll 1
+                for (int q = 0; q < 2; ++q) {
+                    twait(&full[s], ph, 103 * 65536 + (int)(kc & 0xFFFF), 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(base + s * C::STAGE);
+                    const uint32_t sb = sa + C::A_BYTES;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {   // K = 16 per MMA
+                            if (dbg_mode & 2) break;
+                            uint64_t d1, d2;
+                            if (role == 0) {   // K-major: k = column, 32 bytes per step inside the 128-byte rows
+                                d1 = umma_desc_sw128(sa + 32 * j, 16, 1024);
+                                d2 = umma_desc_sw128(sa + 16384 + 32 * j, 16, 1024);
+                            } else {           // MN-major: k = row, 16 rows per step; LBO = next 64 columns
+                                d1 = umma_desc_sw128(sa + 2048 * j, 8192, 1024);
+                                d2 = umma_desc_sw128(sa + 16384 + 2048 * j, 8192, 1024);
+                            }
+                            const uint64_t db = umma_desc_sw128(sb + 32 * j, 16, 1024);
+                            tc_mma_ss_f16(dacc, d1, db, id1, (q == 0 && j == 0) ? 0u : 1u);
+                            tc_mma_ss_f16(dacc, d2, db, id2, 1u);
+                        }
+                        tc_commit(&empty[s]);
+                    }
+                    __syncwarp();
+                    ++kc;
+                    if (++s == C::NS) { s = 0; ph ^= 1u; }
+                }
+            }
+            if (end_seg) {
+                e.mask = mask;
+                slot += (uint32_t)__popc(mask);
+                mask = 0;
+            }
+            if (elect_one()) {
+                evq[buf] = e;
+                tc_commit(&acc_full[buf]);
+                mbar_arrive(&acc_full[buf]);
+            }
+            __syncwarp();
+            ++ev;
+        }
+        tflush(4);
+    } else {
+        // ------------------------------------------------ epilogue warps 2-5 (TMEM lane = output row)
+        const int qd = warp & 3;
+        const int ln = 32 * qd + lane;
+        const uint32_t lane_off = (uint32_t)(32 * qd) << 16;
+        for (uint32_t ev = 0; t0 < t1; ++ev) {
+            const int buf = ev & 1;
+            twait(&acc_full[buf], (ev >> 1) & 1u, 105 * 65536 + (int)(ev & 0xFFFF), 0);
+            tc_fence_after();
+            const PairEvent e = evq[buf];
+            if (e.has_tile && !(dbg_mode & 4)) {
+                const uint32_t ta = tbase + lane_off + (uint32_t)(buf * C::ACCB);
+                const uint32_t tl = tbase + lane_off + (uint32_t)(C::LL0 + e.a * BP);
+#pragma unroll
+                for (int c0 = 0; c0 < BP; c0 += 8) {
+                    float h0[8], h1[8], acc[8];
+                    tmem_ld8(ta + c0, h0);
+                    tmem_ld8(ta + BP + c0, h1);
+                    if (!e.first) tmem_ld8(tl + c0, acc);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const float v = h0[u] + h1[u];
+                        acc[u] = e.first ? v : acc[u] + v;
+                    }
+                    tmem_st8(tl + c0, acc);
+                }
+                tmem_wait_st();
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
+            uint32_t slot = e.slot;
+            for (uint32_t bits = e.mask; bits; bits &= bits - 1) {
+                const int a = __ffs(bits) - 1;
+                const uint32_t tl = tbase + lane_off + (uint32_t)(C::LL0 + a * BP);
+                float4* dst = reinterpret_cast<float4*>(P + ((int64_t)slot * C::TT + ln) * BP);
+#pragma unroll
+                for (int c0 = 0; c0 < BP; c0 += 8) {
+                    float v[8];
+                    tmem_ld8(tl + c0, v);
+                    tmem_wait_ld();
+                    dst[c0 / 4] = make_float4(v[0], v[1], v[2], v[3]);
+                    dst[c0 / 4 + 1] = make_float4(v[4], v[5], v[6], v[7]);
+                }
+                ++slot;
+            }
+            if (e.last) break;
+        }
+        if (warp == 2) tflush(12);
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();   // no DSMEM store may target an exited CTA
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(C::TMEM_COLS));
+    }
+}
+
+// max |x| over n floats into *out (as ordered uint bits; caller zeroes *out)
+__global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                                                unsigned int* __restrict__ out) {
+    float m = 0.f;
+    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * 256)
+        m = fmaxf(m, fabsf(x[(e / cols) * ld + e % cols]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// exponent e with max * 2^e in [2^14, 2^15) (0 for max = 0 or non-finite)
+__host__ __device__ __forceinline__ int f16_scale_exp(float mx) {
+    if (!(mx > 0.f) || !(mx < 3.0e38f)) return 0;
+    int e;
+    frexpf(mx, &e);          // mx = f * 2^e, f in [0.5, 1)
+    return 15 - e;           // mx * 2^(15-e) in [2^14, 2^15)
+}
+
+// Y1 (l_pad x bp, row-major; R^-1 fold when Rinv) -> folded copy Y1f and per-column max|.|
+__global__ void __launch_bounds__(256) k_y16_prep(int64_t lpad, int b, int bp, const double* __restrict__ Rinv,
+                                                  const float* __restrict__ Y1, float* __restrict__ Y1f,
+                                                  unsigned int* __restrict__ cmax) {
+    __shared__ double Ms[64 * 64];
+    __shared__ float ys[256];
+    __shared__ float mx[256];
+    if (Rinv)
+        for (int e = threadIdx.x; e < b * b; e += blockDim.x) Ms[e] = Rinv[e];
+    const int rb = 256 / bp;
+    const int r = threadIdx.x / bp, c = threadIdx.x % bp;
+    float m = 0.f;
+    for (int64_t k0 = (int64_t)blockIdx.x * rb; k0 < lpad; k0 += (int64_t)gridDim.x * rb) {
+        __syncthreads();
+        const int64_t k = k0 + r;
+        ys[threadIdx.x] = (k < lpad && r < rb) ? Y1[k * bp + c] : 0.f;
+        __syncthreads();
+        if (k < lpad && r < rb) {
+            float v = c < b ? ys[threadIdx.x] : 0.f;
+            if (Rinv && c < b) {
+                double acc = 0.0;
+                for (int p = 0; p <= c; ++p) acc = fma((double)ys[r * bp + p], Ms[p * b + c], acc);
+                v = (float)acc;
+            }
+            Y1f[k * bp + c] = v;
+            m = fmaxf(m, fabsf(v));
+        }
+    }
+    mx[threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.x < bp) {
+        float v = 0.f;
+        for (int q = 0; q < rb; ++q) v = fmaxf(v, mx[q * bp + threadIdx.x]);
+        atomicMax(cmax + threadIdx.x, __float_as_uint(v));
+    }
+}
+
+// folded Y1 -> Y16T (2bp x l_pad fp16): row c = y1 = f16(y 2^e_c), row bp + c = y2 = f16(y 2^e_c - y1)
+__global__ void __launch_bounds__(256) k_y16_split(int64_t lpad, int bp, const float* __restrict__ Y1f,
+                                                   const unsigned int* __restrict__ cmax, __half* __restrict__ Y16T,
+                                                   int* __restrict__ yexp) {
+    const int rb = 256 / bp;
+    const int r = threadIdx.x % rb, c = threadIdx.x / rb;   // consecutive threads: consecutive k
+    const int e = f16_scale_exp(__uint_as_float(cmax[c]));
+    if (blockIdx.x == 0 && r == 0) yexp[c] = e;
+    for (int64_t k = (int64_t)blockIdx.x * rb + r; k < lpad; k += (int64_t)gridDim.x * rb) {
+        const float v = ldexpf(Y1f[k * bp + c], e);
+        const __half h1 = __float2half_rn(v);
+        const __half h2 = __float2half_rn(v - __half2float(h1));
+        Y16T[(int64_t)c * lpad + k] = h1;
+        Y16T[(int64_t)(bp + c) * lpad + k] = h2;
+    }
+}
+
+// Pack the upper tiles of row-major D (l x l, leading dimension ldD), scaled by 2^sD (exact,
+// sD = f16_scale_exp(max |D|)) and split into fp16 planes h1, h2, into 64 KB tiles at
+// upper_tile_index(I, J) in the swizzled image k_dstream_pair copies verbatim into shared
+// memory (see the top of this file); zero outside l.
+__global__ void __launch_bounds__(256) k_pack_upper(const float* __restrict__ D, int64_t ldD, int64_t l,
+                                                    const uint32_t* __restrict__ tiles, int64_t NT, int64_t ntiles,
+                                                    const unsigned int* __restrict__ dmax, __half* __restrict__ Dt) {
+    const int sD = f16_scale_exp(__uint_as_float(*dmax));
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t v = tiles[t];
+        const int I = (int)(v >> 16), J = (int)(v & 0xFFFFu);
+        const int64_t r0 = (int64_t)I * 128, c0 = (int64_t)J * 128;
+        uint8_t* out = reinterpret_cast<uint8_t*>(Dt + upper_tile_index(I, J, (int)NT) * 128 * 128 * 2);
+        for (int e = threadIdx.x; e < 128 * 16; e += 256) {
+            const int r = e >> 4, c8 = (e & 15) * 8;   // 8 consecutive columns (one 16-byte granule) of row r
+            const int64_t gr = r0 + r;
+            __align__(16) __half h1[8], h2[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t gc = c0 + c8 + u;
+                const float x = (gr < l && gc < l) ? ldexpf(D[gr * ldD + gc], sD) : 0.f;
+                h1[u] = __float2half_rn(x);
+                h2[u] = __float2half_rn(x - __half2float(h1[u]));
+            }
+            const int box = c8 >> 6, g = (c8 & 63) >> 3;
+            const int off = box * 16384 + r * 128 + ((g ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4*>(out + off) = *reinterpret_cast<const uint4*>(h1);
+            *reinterpret_cast<uint4*>(out + 32768 + off) = *reinterpret_cast<const uint4*>(h2);
+        }
+    }
+}
+
+// Y2 rows = fixed-order sum of their slots' fp32 partials (fp64) times 2^-(sD + e_c) (the
+// exact scales of D and of Y1's column c), then t = w^T Y2 (A4).
+__global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, const int* __restrict__ xptr,
+                                                      const int* __restrict__ xslot, const float* __restrict__ P,
+                                                      const unsigned int* __restrict__ dmax, const int* __restrict__ yexp,
+                                                      const double* __restrict__ w, float* __restrict__ Y2,
+                                                      double* __restrict__ tpart, double* __restrict__ t,
+                                                      unsigned int* __restrict__ counter) {
+    __shared__ double red[256];
+    const int rows_per_blk = 256 / bp;
+    const int tid = threadIdx.x;
+    const int cidx = tid % bp, rloc = tid / bp;
+    double acc_t = 0.0;
+    const double unscale = ldexp(1.0, -(f16_scale_exp(__uint_as_float(*dmax)) + yexp[cidx]));
+    for (int64_t r0 = (int64_t)blockIdx.x * rows_per_blk; r0 < l; r0 += (int64_t)gridDim.x * rows_per_blk) {
+        const int64_t r = r0 + rloc;
+        if (rloc < rows_per_blk && r < l) {
+            const int X = (int)(r >> 7), rr = (int)(r & 127);
+            const int q0 = xptr[X], q1 = xptr[X + 1];
+            double v = 0.0;
+            int q = q0;
+            for (; q + 8 <= q1; q += 8) {
+                float pv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) pv[u] = P[((int64_t)xslot[q + u] * 128 + rr) * bp + cidx];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v += (double)pv[u];
+            }
+            for (; q < q1; ++q) v += (double)P[((int64_t)xslot[q] * 128 + rr) * bp + cidx];
+            v *= unscale;
+            Y2[r * bp + cidx] = (float)v;
+            if (cidx < b) acc_t += w[r] * v;
+        }
+    }
+    red[tid] = (rloc < rows_per_blk) ? acc_t : 0.0;
+    __syncthreads();
+    if (tid < bp) {
+        double v = 0.0;
+        for (int q = 0; q < rows_per_blk; ++q) v += red[q * bp + tid];
+        tpart[blockIdx.x * kMaxB + tid] = v;
+    }
+    if (last_block_done(counter)) {
+        if (tid < bp) t[tid] = ordered_sum(tpart + tid, gridDim.x, kMaxB);
+        if (tid == 0) *counter = 0;
+    }
+}
+
+}  // namespace sbmds

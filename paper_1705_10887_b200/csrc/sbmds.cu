@@ -18,7 +18,7 @@
 #include "common.cuh"
 #include "k_dstream.cuh"
 #include "k_dstream_tc.cuh"
-#include "k_dstream_sym.cuh"
+#include "k_dstream_pair.cuh"
 #include "k_small.cuh"
 #include "k_sparse.cuh"
 #include "k_blocked.cuh"
@@ -268,7 +268,6 @@ struct sbmds_ctx {
     bool blocked = false;
     int use_blocked = 1;   // bit 0: S Y2 through the blocked kernel, bit 1: S^T X too
     int gram_tc = 1;       // Gram on the FP64 tensor cores (b <= 32)
-    int sym_dbg = 0;
     // D_ll
     float* D = nullptr;
     int64_t ldD = 0;
@@ -280,7 +279,22 @@ struct sbmds_ctx {
     bool amap_ok = false;
     CUtensorMap bmap[7];         // Y1T = [Y_hi; Y_lo] as the B operand
     void* bmap_ptr[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    DevBuf Y1T, PT;
+    DevBuf Y1T;
+    // symmetric-half stream (k_dstream_pair.cuh): D packed as upper-triangle 128 x 128 tiles,
+    // and one schedule per tensor width bp in {8, 16, 32}
+    DevBuf Dt, Y16T, Y1f, y16aux;
+    bool dt_ok = false;
+    struct PairPlan {
+        bool ok = false;
+        int S = 0, NT = 0, P = 0, nslots = 0;
+        int64_t ntiles = 0;
+        DevBuf tiles, pbeg, sbase, xptr, xslot;
+        CUtensorMap bmap16;
+        void* b16_enc = nullptr;
+    } pplan[3];
+    int pair_dbg = 0;
+    DevBuf pdbg;
+    double pdbg_avg[2][16] = {};
     int last_dpath = 0;          // D-stream path of the last apply: 1 ffma, 2 tcgen05, 3 tcgen05 symmetric half
     int64_t last_dbytes = 0;     // its bytes per launch (bench roofline)
     // apply workspace
@@ -377,17 +391,21 @@ void run_dstream(sbmds_ctx* h, int b, cudaStream_t st) {
     });
 }
 
-void encode_tiled(CUtensorMap* map, void* ptr, uint64_t inner, uint64_t outer, uint64_t pitch_bytes, uint32_t box0,
-                  uint32_t box1, CUtensorMapSwizzle sw) {
+void encode_tiled_dt(CUtensorMap* map, void* ptr, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                     uint64_t pitch_bytes, uint32_t box0, uint32_t box1, CUtensorMapSwizzle sw) {
     EncodeFn enc = get_encode();
     if (!enc) throw CudaError{cudaErrorNotSupported, "cuTensorMapEncodeTiled entry point"};
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
     cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
     cuuint32_t box[2] = {box0, box1};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(map, dt, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue, "cuTensorMapEncodeTiled"};
+}
+void encode_tiled(CUtensorMap* map, void* ptr, uint64_t inner, uint64_t outer, uint64_t pitch_bytes, uint32_t box0,
+                  uint32_t box1, CUtensorMapSwizzle sw) {
+    encode_tiled_dt(map, ptr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, inner, outer, pitch_bytes, box0, box1, sw);
 }
 
 // A3 + A4 on the tensor cores (3xTF32, tcgen05): split Y1, stream D, reduce partials.
@@ -440,61 +458,185 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
     });
 }
 
-// A3 + A4 streaming only the upper triangle of D (NEXT-1, k_dstream_sym.cuh).
+// A3 + A4 streaming only the upper triangle of D (NEXT-1, k_dstream_pair.cuh).
+
+// Host schedule of the pair kernel: the walk (blocks of S x S tiles, block rows bi, block
+// columns bj >= bi, row-major inside a block), balanced contiguous ranges per CTA pair, the
+// partial slots each role writes (simulating exactly the kernel's flush rule: a segment ends
+// when the walk enters another block; its touched accumulators flush in index order), and
+// per row tile X the list of its slots in slot order (the fixed reduction order).
 template <int BP>
-void run_dstream_sym(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
-    using C = SymCfg<BP>;
-    const int i = bp_index(BP);
-    const int64_t lpad = y1t_lpad(h);
-    if (!h->amap_ok) {
-        encode_tiled(&h->amap, h->D, h->l, h->l, h->ldD * sizeof(float), 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-        h->amap_ok = true;
+void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs) {
+    using C = PairCfg<BP>;
+    const int S = C::S;
+    const int NT = (int)((h->l + 127) / 128);
+    if (NT > 65535) throw std::runtime_error("l too large for the symmetric-half stream");
+    const int NBk = (NT + S - 1) / S;
+    std::vector<uint32_t> tiles;
+    tiles.reserve((size_t)NT * (NT + 1) / 2);
+    for (int bi = 0; bi < NBk; ++bi)
+        for (int bj = bi; bj < NBk; ++bj)
+            for (int r = 0; r < S; ++r)
+                for (int c = 0; c < S; ++c) {
+                    const int I = bi * S + r, J = bj * S + c;
+                    if (I < NT && J < NT && J >= I) tiles.push_back(((uint32_t)I << 16) | (uint32_t)J);
+                }
+    const int64_t T = (int64_t)tiles.size();
+    const int P = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs, T / 8));
+    std::vector<int64_t> pbeg(P + 1);
+    for (int p = 0; p <= P; ++p) pbeg[p] = (int64_t)p * T / P;
+    std::vector<int> sbase(2 * P), slot_x;
+    for (int p = 0; p < P; ++p)
+        for (int role = 0; role < 2; ++role) {
+            sbase[2 * p + role] = (int)slot_x.size();
+            uint32_t mask = 0;
+            int cbi = -1, cbj = -1;
+            auto emit = [&]() {
+                for (int a = 0; a < S; ++a)
+                    if (mask & (1u << a)) slot_x.push_back(role ? cbj * S + a : cbi * S + a);
+                mask = 0;
+            };
+            for (int64_t t = pbeg[p]; t < pbeg[p + 1]; ++t) {
+                const int I = (int)(tiles[t] >> 16), J = (int)(tiles[t] & 0xFFFFu);
+                const int bi = I / S, bj = J / S;
+                if ((bi != cbi || bj != cbj) && mask) emit();
+                cbi = bi;
+                cbj = bj;
+                if (role == 1 && I == J) continue;
+                mask |= 1u << (role ? J - bj * S : I - bi * S);
+            }
+            emit();
+        }
+    const int nslots = (int)slot_x.size();
+    std::vector<int> xptr(NT + 1, 0), xslot(nslots);
+    for (int q = 0; q < nslots; ++q) ++xptr[slot_x[q] + 1];
+    for (int X = 0; X < NT; ++X) xptr[X + 1] += xptr[X];
+    {
+        std::vector<int> fill(xptr.begin(), xptr.end() - 1);
+        for (int q = 0; q < nslots; ++q) xslot[fill[slot_x[q]]++] = q;   // ascending slot ids per X
     }
-    h->Y1T.ensure((size_t)2 * kMaxB * lpad * sizeof(float));
-    if (h->bmap_ptr[i] != h->Y1T.p) {
-        encode_tiled(&h->bmap[i], h->Y1T.p, lpad, C::NB, lpad * sizeof(float), 32, C::NB, CU_TENSOR_MAP_SWIZZLE_128B);
-        h->bmap_ptr[i] = h->Y1T.p;
+    pl.tiles.ensure(tiles.size() * sizeof(uint32_t));
+    pl.pbeg.ensure(pbeg.size() * sizeof(int64_t));
+    pl.sbase.ensure(sbase.size() * sizeof(int));
+    pl.xptr.ensure(xptr.size() * sizeof(int));
+    pl.xslot.ensure(std::max<size_t>(1, xslot.size()) * sizeof(int));
+    CK(cudaMemcpy(pl.tiles.p, tiles.data(), tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pl.pbeg.p, pbeg.data(), pbeg.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pl.sbase.p, sbase.data(), sbase.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pl.xptr.p, xptr.data(), xptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (nslots) CK(cudaMemcpy(pl.xslot.p, xslot.data(), xslot.size() * sizeof(int), cudaMemcpyHostToDevice));
+    pl.S = S;
+    pl.NT = NT;
+    pl.P = P;
+    pl.ntiles = T;
+    pl.nslots = nslots;
+    pl.ok = true;
+}
+
+template <int BP>
+void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
+    using C = PairCfg<BP>;
+    const int pi = BP == 8 ? 0 : (BP == 16 ? 1 : 2);
+    auto& pl = h->pplan[pi];
+    static bool attr_set[3] = {false, false, false};
+    static int max_clusters[3] = {0, 0, 0};
+    if (!attr_set[pi]) {
+        CK(cudaFuncSetAttribute(k_dstream_pair<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * (h->num_sms / 2));
+        cfg.blockDim = dim3(C::THREADS);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        CK(cudaOccupancyMaxActiveClusters(&nc, k_dstream_pair<BP>, &cfg));
+        max_clusters[pi] = std::max(1, std::min(nc, h->num_sms / 2));
+        attr_set[pi] = true;
+    }
+    const int64_t lpad = y1t_lpad(h);
+    if (!pl.ok) build_pair_plan<BP>(h, pl, max_clusters[pi]);
+    // aux: [0] max |D| bits, [64..128) per-column max |Y1| bits, [128..192) column exponents
+    h->y16aux.ensure(192 * sizeof(unsigned int));
+    unsigned int* dmax = h->y16aux.as<unsigned int>();
+    unsigned int* ymax = dmax + 64;
+    int* yexp = reinterpret_cast<int*>(dmax + 128);
+    if (!h->dt_ok) {
+        h->Dt.ensure((size_t)pl.ntiles * 128 * 128 * 2 * sizeof(__half));
+        CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), st));
+        launch(k_absmax, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, (h->l * h->l + 255) / 256)), dim3(256),
+               0, st, (const float*)h->D, h->l, h->l, h->ldD, dmax);
+        launch(k_pack_upper, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
+               (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
+               (const unsigned int*)dmax, h->Dt.as<__half>());
+        h->dt_ok = true;
+    }
+    h->Y16T.ensure((size_t)2 * kMaxB * lpad * sizeof(__half));
+    h->Y1f.ensure((size_t)lpad * kMaxB * sizeof(float));
+    if (pl.b16_enc != h->Y16T.p) {
+        encode_tiled_dt(&pl.bmap16, h->Y16T.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, lpad, C::NB, lpad * sizeof(__half), 64,
+                        C::NB, CU_TENSOR_MAP_SWIZZLE_128B);
+        pl.b16_enc = h->Y16T.p;
     }
     profiled(h->prof, PK_SPLIT, st, [&] {
-        launch(k_split_y1, dim3((unsigned)std::min<int64_t>(8 * 148, (lpad + 255) / 256 * BP)), dim3(256), 0, st,
-               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1T.as<float>());
+        CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
+        launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax);
+        launch(k_y16_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
+               lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y16T.as<__half>(), yexp);
     });
-    SymSched sk;
-    sk.RT = (int)((h->l + C::T - 1) / C::T);
-    sk.NT = (int64_t)sk.RT * (sk.RT + 1) / 2;
-    sk.grid = (int)std::min<int64_t>(h->num_sms, sk.NT);
-    int maxseg = 1;
-    for (int I = 0; I < sk.RT; ++I)
-        maxseg = std::max(maxseg, sk.cta_of(sk.strip0(I) + (sk.RT - I) - 1) - sk.cta_of(sk.strip0(I)) + 1);
-    h->P.ensure((size_t)sk.RT * maxseg * C::T * BP * sizeof(double));
-    h->PT.ensure((size_t)std::max<int64_t>(1, (int64_t)sk.RT * (sk.RT - 1) / 2) * C::T * BP * sizeof(float));
-    static bool attr_set[7] = {false};
-    if (!attr_set[i]) {
-        CK(cudaFuncSetAttribute(k_dstream_sym<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_set[i] = true;
+    h->P.ensure((size_t)std::max(1, pl.nslots) * 128 * BP * sizeof(float));
+    if (h->pair_dbg) {
+        h->pdbg.ensure((size_t)2 * pl.P * 16 * sizeof(unsigned long long));
+        CK(cudaMemsetAsync(h->pdbg.p, 0, (size_t)2 * pl.P * 16 * sizeof(unsigned long long), st));
     }
     profiled(h->prof, PK_DSTREAM, st, [&] {
-        launch(k_dstream_sym<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->amap, h->bmap[i], sk, maxseg,
-               h->P.as<double>(), h->PT.as<float>());
+        launch(k_dstream_pair<BP>, dim3(2 * pl.P), dim3(C::THREADS), (size_t)C::SMEM, st, (const __half*)h->Dt.p,
+               pl.bmap16, (const uint32_t*)pl.tiles.p, (const int64_t*)pl.pbeg.p, (const int*)pl.sbase.p,
+               (int)pl.NT, h->P.as<float>(), h->pair_dbg ? h->pdbg.as<unsigned long long>() : nullptr,
+               h->pair_dbg >> 1);
     });
+    if (h->pair_dbg) {   // per-role average wait cycles (sites: see k_dstream_pair)
+        std::vector<unsigned long long> d((size_t)2 * pl.P * 16);
+        CK(cudaStreamSynchronize(st));
+        CK(cudaMemcpy(d.data(), h->pdbg.p, d.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        for (int r = 0; r < 2; ++r)
+            for (int k = 0; k < 16; ++k) {
+                double acc = 0;
+                for (int p = 0; p < pl.P; ++p) acc += (double)d[(size_t)(2 * p + r) * 16 + k];
+                h->pdbg_avg[r][k] = acc / pl.P;
+            }
+    }
     const int rows_per_blk = 256 / BP;
     const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     profiled(h->prof, PK_DREDUCE, st, [&] {
-        launch(k_dreduce_sym, dim3(grid), dim3(256), 0, st, h->l, BP, b, sk, maxseg, (const double*)h->P.as<double>(),
-               (const float*)h->PT.as<float>(), (const double*)h->w.as<double>(), h->Y2.as<float>(),
-               h->tpart.as<double>(), h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
+        launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
+               (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const unsigned int*)dmax,
+               (const int*)yexp, (const double*)h->w.as<double>(), h->Y2.as<float>(), h->tpart.as<double>(),
+               h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
     });
     h->last_dpath = 3;
-    h->last_dbytes = sk.NT * (int64_t)C::T * C::T * 4 + (sk.NT - sk.RT) * (int64_t)C::T * BP * 4;
+    h->last_dbytes = pl.ntiles * (int64_t)128 * 128 * 4 + 12 * h->l * (int64_t)b;
 }
-
 bool uses_tc(const sbmds_ctx* h, int bp) { return bp >= 8 && (h->dstream == 2 || h->dstream == 0 || h->dstream == 3); }
-bool uses_sym(const sbmds_ctx* h, int bp) { return (bp == 8 || bp == 16) && h->dstream == 3; }
+// symmetric-half stream: forced by dstream = 3, chosen by auto (0) once D has >= 8 tiles per
+// CTA pair (below that D is L2-resident and the full stream on all SMs wins)
+bool uses_sym(const sbmds_ctx* h, int bp) {
+    if (!(bp == 8 || bp == 16 || bp == 32)) return false;
+    if (h->dstream == 3) return true;
+    const int64_t nt = (h->l + 127) / 128;
+    return h->dstream == 0 && nt * (nt + 1) / 2 >= 8 * (int64_t)(h->num_sms / 2);
+}
 
 void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
     if (uses_sym(h, bp)) {
-        if (bp == 8) run_dstream_sym<8>(h, b, st, Rinv);
-        else run_dstream_sym<16>(h, b, st, Rinv);
+        if (bp == 8) run_dstream_pair<8>(h, b, st, Rinv);
+        else if (bp == 16) run_dstream_pair<16>(h, b, st, Rinv);
+        else run_dstream_pair<32>(h, b, st, Rinv);
         return;
     }
     if (uses_tc(h, bp)) {
@@ -760,7 +902,10 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->PT};
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux,
+                      &h->pplan[0].tiles, &h->pplan[0].pbeg, &h->pplan[0].sbase, &h->pplan[0].xptr, &h->pplan[0].xslot,
+                      &h->pplan[1].tiles, &h->pplan[1].pbeg, &h->pplan[1].sbase, &h->pplan[1].xptr, &h->pplan[1].xslot,
+                      &h->pplan[2].tiles, &h->pplan[2].pbeg, &h->pplan[2].sbase, &h->pplan[2].xptr, &h->pplan[2].xslot};
     for (DevBuf* b : bufs) f(b);
 }
 
@@ -1255,8 +1400,6 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "blocked")) {
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "blocked is a bit mask in [0, 3]");
         h->use_blocked = (int)value;
-    } else if (!strcmp(key, "sym_dbg")) {
-        h->sym_dbg = (int)value;
     } else if (!strcmp(key, "gram_tc")) {
         h->gram_tc = value ? 1 : 0;
     } else if (!strcmp(key, "order_columns")) {
@@ -1270,6 +1413,8 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "dstream")) {
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric}");
         h->dstream = (int)value;
+    } else if (!strcmp(key, "pair_dbg")) {
+        h->pair_dbg = (int)value;   // bit 0: wait-cycle instrumentation; bits 1..: experiment modes
     } else {
         return fail(SBMDS_EINVAL, "unknown option '%s'", key);
     }
@@ -1286,6 +1431,11 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "blocked_umax")) *value = h->blocked ? (int64_t)h->umax : -1;
     else if (!strcmp(key, "dstream_path")) *value = h->last_dpath;
     else if (!strcmp(key, "dstream_bytes")) *value = h->last_dbytes;
+    else if (!strncmp(key, "pair_dbg_", 9) && (key[9] == 'N' || key[9] == 'T') && key[10] == '_') {
+        const int site = atoi(key + 11);
+        if (site < 0 || site > 15) return fail(SBMDS_EINVAL, "pair_dbg site in 0..15");
+        *value = (int64_t)std::llround(h->pdbg_avg[key[9] == 'T'][site]);
+    }
     else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
     else if (!strcmp(key, "csc_bytes")) *value = (int64_t)(h->cptr.bytes + h->ridx.bytes + h->cval.bytes);
     else if (!strcmp(key, "workspace_bytes"))

@@ -196,10 +196,11 @@ def test_apply_blocked_and_plain_sparse_paths(blocked, b):
     assert relerr(Y, oracle_apply(p, X)) <= TOL
 
 
-@pytest.mark.parametrize("b", [16, 12, 8, 5])
+@pytest.mark.parametrize("b", [16, 12, 8, 5, 32, 20])
 def test_apply_symmetric_half_stream(b):
-    """NEXT-1: streaming only the upper triangle of D (k_dstream_sym) meets the bar; l = 2003
-    gives 16 row tiles with a ragged last one, so every off-diagonal/transposed case occurs."""
+    """NEXT-1: streaming only the upper triangle of D (k_dstream_pair, CTA pairs) meets the
+    bar; l = 2003 gives 16 row tiles with a ragged last one, so diagonal, off-diagonal and
+    transposed tiles, blocks split between pairs and (b = 8) a single block all occur."""
     p = configs.random_problem(30_011, 2_003, 16, seed=b + 100, name="cfg5_small")
     X = configs.x_block(p.n, b, seed=b)
     with make_handle(p) as h:
@@ -207,6 +208,21 @@ def test_apply_symmetric_half_stream(b):
         Y = run_apply(h, X)
         assert h.stat("dstream_path") == 3
     assert relerr(Y, oracle_apply(p, X)) <= TOL
+
+
+def test_apply_symmetric_half_many_blocks():
+    """l = 9001: 71 row tiles, 5 block rows of 16 at b = 8, 9 of 8 at b = 16, 18 of 4 at
+    b = 32; every pair's range crosses blocks. Bitwise deterministic, and one handle can
+    switch widths (one packed D, one schedule per width)."""
+    p = configs.random_problem(40_000, 9_001, 8, seed=7, name="cfg5_mid")
+    with make_handle(p) as h:
+        h.set_option("dstream", 3)
+        for b in (16, 8, 32):
+            X = configs.x_block(p.n, b, seed=b)
+            Y = run_apply(h, X)
+            assert h.stat("dstream_path") == 3
+            assert relerr(Y, oracle_apply(p, X)) <= TOL
+            assert np.array_equal(Y, run_apply(h, X))
 
 
 def test_symmetric_half_eigs_config2():
