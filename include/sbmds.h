@@ -128,11 +128,29 @@ void sbmds_destroy(sbmds_t h);
 const char* sbmds_last_error(void);
 
 /*
- * Tuning / introspection (tests and bench):
- *   sbmds_set_option keys: "rr_period" (>=1), "use_graph" (0/1), "dstream"
- *   (0 = auto, 1 = FFMA stream), "order_columns" (0/1: spatial CSC column order).
+ * Tuning / introspection (tests and bench). Options change how, never what, is computed.
+ *   sbmds_set_option keys:
+ *     "rr_period"      (>= 1) Rayleigh-Ritz every r iterations (default 5)
+ *     "use_graph"      (0/1)
+ *     "order_columns"  (0/1) spatial CSC column order for the S^T X gathers
+ *     "dstream"        D-stream kernel for A3: 0 auto (symmetric half on CTA pairs when b in
+ *                      5..32 and D has >= 8 tiles per pair, else full-D tcgen05 for b >= 5,
+ *                      else FFMA), 1 FFMA, 2 full-D tcgen05 3xTF32, 3 symmetric half
+ *                      (k_dstream_pair, 2xFP16; b in 5..32, else as 2)
+ *     "blocked"        bit mask: 1 = S Y2 through the row-blocked kernel, 2 = S^T X too
+ *     "gram_tc"        (0/1) Gram on the FP64 tensor cores (b <= 32)
+ *     "profile"        bit mask of kernel families timed with CUDA events on the launching
+ *                      stream (bit k = family k of: colsum csc dstream dreduce csr gram chol
+ *                      rotate rr split); "profile_reset" (any value) zeroes the counters
+ *     "pair_dbg"       diagnostics of k_dstream_pair: bit 0 per-role wait-cycle counters
+ *                      (stats "pair_dbg_N_<site>", "pair_dbg_T_<site>"), higher bits disable
+ *                      parts of the kernel for experiments (results then invalid)
  *   sbmds_get_stat keys: "n", "l", "nnz", "rowsum_dev_e9" (max |row sum - 1| * 1e9),
- *   "d_borrowed", "csc_bytes", "workspace_bytes".
+ *     "d_borrowed", "csc_bytes", "workspace_bytes", "blocked_umax" (largest per-block
+ *     landmark dictionary, -1 if the row-blocked structure is off), "blocked_slots",
+ *     "dstream_path" (1 FFMA, 2 full-D tcgen05, 3 symmetric half; of the last apply),
+ *     "dstream_bytes" (its algorithmic bytes per launch), "<family>_ns" / "<family>_launches"
+ *     (profiled device time in ns / launch count per family since the last reset).
  * Both return SBMDS_EINVAL for an unknown key.
  */
 sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t value);

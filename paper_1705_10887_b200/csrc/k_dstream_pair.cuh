@@ -66,7 +66,7 @@ struct PairCfg {
     static constexpr int A_BYTES = 2 * TT * KC * 2;  // 32 KB: the chunk of both fp16 planes
     static constexpr int BOX_B = NB * 128;           // the chunk's 64-k slice of [y1; y2]
     static constexpr int STAGE = A_BYTES + BOX_B;
-    static constexpr int NS = (208 * 1024) / STAGE > 8 ? 8 : (208 * 1024) / STAGE;
+    static constexpr int NS = (216 * 1024) / STAGE > 8 ? 8 : (216 * 1024) / STAGE;   // b = 16: 6 x 36 KB
     static constexpr int THREADS = 6 * 32;           // producer, MMA, 4 epilogue warps
     static constexpr int SMEM = NS * STAGE + 1024 + 1024;
     static_assert(STAGE % 1024 == 0, "stage alignment");
@@ -144,7 +144,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BP>::THREADS
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t role = cluster_ctarank();  // 0 = N (D_IJ Y1_J), 1 = T (D_IJ^T Y1_I)
     const int pair = blockIdx.x >> 1;
-    const int64_t t0 = pbeg[pair], t1 = (dbg_mode & 32) && role == 1 ? pbeg[pair] : pbeg[pair + 1];
+    const int64_t t0 = pbeg[pair],
+                  t1 = ((dbg_mode & 32) && role == 1) || ((dbg_mode & 64) && role == 0) ? pbeg[pair] : pbeg[pair + 1];
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::NS; ++s) {
@@ -369,12 +370,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BP>::THREADS
     }
 }
 
-// max |x| over n floats into *out (as ordered uint bits; caller zeroes *out)
+// max |x| over a rows x cols matrix (leading dimension ld) into *out as ordered uint bits
+// (caller zeroes *out; max is order-independent, so the result is deterministic)
 __global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
                                                 unsigned int* __restrict__ out) {
     float m = 0.f;
-    for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < rows * cols; e += (int64_t)gridDim.x * 256)
-        m = fmaxf(m, fabsf(x[(e / cols) * ld + e % cols]));
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const float* row = x + r * ld;
+        for (int64_t c = threadIdx.x; c < cols; c += 256) m = fmaxf(m, fabsf(__ldcs(row + c)));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));

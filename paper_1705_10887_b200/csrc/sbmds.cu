@@ -568,7 +568,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     if (!h->dt_ok) {
         h->Dt.ensure((size_t)pl.ntiles * 128 * 128 * 2 * sizeof(__half));
         CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), st));
-        launch(k_absmax, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, (h->l * h->l + 255) / 256)), dim3(256),
+        launch(k_absmax, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256),
                0, st, (const float*)h->D, h->l, h->l, h->ldD, dmax);
         launch(k_pack_upper, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
                (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
