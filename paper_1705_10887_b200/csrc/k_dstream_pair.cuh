@@ -499,12 +499,12 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
             const int q0 = xptr[X], q1 = xptr[X + 1];
             double v = 0.0;
             int q = q0;
-            for (; q + 8 <= q1; q += 8) {
-                float pv[8];
+            for (; q + 16 <= q1; q += 16) {
+                float pv[16];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) pv[u] = P[((int64_t)xslot[q + u] * 128 + rr) * bp + cidx];
+                for (int u = 0; u < 16; ++u) pv[u] = P[((int64_t)xslot[q + u] * 128 + rr) * bp + cidx];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v += (double)pv[u];
+                for (int u = 0; u < 16; ++u) v += (double)pv[u];
             }
             for (; q < q1; ++q) v += (double)P[((int64_t)xslot[q] * 128 + rr) * bp + cidx];
             v *= unscale;
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
         tpart[blockIdx.x * kMaxB + tid] = v;
     }
     if (last_block_done(counter)) {
-        if (tid < bp) t[tid] = ordered_sum(tpart + tid, gridDim.x, kMaxB);
+        ordered_colsum_block(tpart, gridDim.x, kMaxB, bp, t);
         if (tid == 0) *counter = 0;
     }
 }

@@ -22,6 +22,7 @@
 #include "k_small.cuh"
 #include "k_sparse.cuh"
 #include "k_blocked.cuh"
+#include "k_fused.cuh"
 
 namespace sbmds {
 std::atomic<int64_t> g_launches{0};
@@ -268,6 +269,7 @@ struct sbmds_ctx {
     bool blocked = false;
     int use_blocked = 1;   // bit 0: S Y2 through the blocked kernel, bit 1: S^T X too
     int gram_tc = 1;       // Gram on the FP64 tensor cores (b <= 32)
+    int fuse = 1;          // eigs: 1 = A5 fused with the Gram, 2 = also the next A2's S^T partials (k_fused.cuh)
     // D_ll
     float* D = nullptr;
     int64_t ldD = 0;
@@ -612,7 +614,8 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
             }
     }
     const int rows_per_blk = 256 / BP;
-    const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
+    const int grid = (int)std::min<int64_t>(4 * kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
+    h->tpart.ensure((size_t)4 * kRedBlocks * kMaxB * sizeof(double));
     profiled(h->prof, PK_DREDUCE, st, [&] {
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const unsigned int*)dmax,
@@ -740,8 +743,43 @@ void ensure_apply_ws(sbmds_ctx* h, int bp) {
 }
 
 // The whole operator apply on device buffers (stream-ordered, no host sync).
+// Fused-step flags (eigs only, row-blocked S, b in {4, 8, 16, 32}):
+//   kApplyY1Ready: A2 comes from the S^T partials P1 the previous fused step wrote (k_blk_reduce)
+//   kApplyFused:   A5 runs as k_blk_spmm_fused, which also writes the next P1 (unless
+//                  kApplyNoP1) and G = Y^T Y, s = 1^T Y (and H' = Yprev^T Y when Yprev != NULL)
+constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4;
+
+bool fused_ok(const sbmds_ctx* h, int b) {
+    return h->fuse && h->blocked && (h->use_blocked & 1) && (b == 4 || b == 8 || b == 16 || b == 32) &&
+           (size_t)h->umax * b * sizeof(float) <= kBlkSmem;
+}
+
+template <int LPR>
+void launch_fused(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st) {
+    const bool with_h = Yprev != nullptr;
+    const size_t smem = fused_smem_bytes(h->umax, b, with_h);
+    static int occ[2][5] = {};
+    const int li = LPR == 1 ? 0 : (LPR == 2 ? 1 : (LPR == 4 ? 2 : 3));
+    auto kern = with_h ? k_blk_spmm_fused<LPR, true> : k_blk_spmm_fused<LPR, false>;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    occ[with_h][li] = per_sm;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nblk, (int64_t)std::max(1, per_sm) * h->num_sms));
+    h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
+    h->P1.ensure((size_t)std::max<int32_t>(1, h->total_u) * kMaxB * sizeof(float));
+    launch(kern, dim3(grid), dim3(256), smem, st, h->n, h->nblk, b, (const int32_t*)h->rp.as<int32_t>(),
+           (const uint16_t*)h->blcol.as<uint16_t>(), (const float*)h->val.as<float>(),
+           (const int32_t*)h->bdict.as<int32_t>(), (const int32_t*)h->bdoff.as<int32_t>(), (uint32_t)h->umax,
+           (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), Y,
+           (const int32_t*)h->blcp.as<int32_t>(), (const uint8_t*)h->blrow.as<uint8_t>(),
+           (const float*)h->blval.as<float>(), want_p1 ? h->P1.as<float>() : nullptr, Yprev,
+           h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
+           h->counters.as<unsigned int>() + CNT_GRAM);
+}
+
 void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st, bool s_ready = false,
-                  const double* Rinv = nullptr) {
+                  const double* Rinv = nullptr, int flags = 0, const float* Yprev = nullptr) {
     const int bp = next_pow2(b);
     ensure_apply_ws(h, bp);
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
@@ -761,8 +799,24 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         }
     }
     // A2: Y1 = S^T X - w s^T   (CSC SpMM by default; row-blocked partials + landmark
-    // reduction when enabled: both are bound by the 64-B-per-nonzero gather traffic)
-    if (blk && (h->use_blocked & 2)) {
+    // reduction when enabled: both are bound by the 64-B-per-nonzero gather traffic; inside
+    // eigs the partials come from the previous fused step, leaving only the reduction)
+    if (flags & kApplyY1Ready) {
+        auto go_r = [&](auto kern) {
+            launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
+                   (const int32_t*)h->bjptr.as<int32_t>(), (const int32_t*)h->bjlist.as<int32_t>(),
+                   (const float*)h->P1.as<float>(), (const double*)h->w.as<double>(), (const double*)h->s.as<double>(),
+                   h->Y1.as<float>());
+        };
+        profiled(h->prof, PK_CSC, st, [&] {
+            switch (b / 4) {
+                case 1: go_r(k_blk_reduce<1>); break;
+                case 2: go_r(k_blk_reduce<2>); break;
+                case 4: go_r(k_blk_reduce<4>); break;
+                default: go_r(k_blk_reduce<8>); break;
+            }
+        });
+    } else if (blk && (h->use_blocked & 2)) {
         h->P1.ensure((size_t)std::max<int32_t>(1, h->total_u) * kMaxB * sizeof(float));
         const size_t smem_t = (size_t)kRB * bp * sizeof(float);
         auto go_t = [&](auto kern) {
@@ -791,7 +845,17 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     dstream(h, b, bp, st, Rinv);
     // A5: Y = -1/2 (S Y2 - 1 t^T)
-    if (blk && (h->use_blocked & 1)) {
+    if (flags & kApplyFused) {
+        const bool want_p1 = !(flags & kApplyNoP1);
+        profiled(h->prof, PK_CSR, st, [&] {
+            switch (b / 4) {
+                case 1: launch_fused<1>(h, b, Y, Yprev, want_p1, st); break;
+                case 2: launch_fused<2>(h, b, Y, Yprev, want_p1, st); break;
+                case 4: launch_fused<4>(h, b, Y, Yprev, want_p1, st); break;
+                default: launch_fused<8>(h, b, Y, Yprev, want_p1, st); break;
+            }
+        });
+    } else if (blk && (h->use_blocked & 1)) {
         const size_t smem = (size_t)h->umax * bp * sizeof(float);
         auto go = [&](auto kern) {
             launch(kern, dim3((unsigned)h->nblk), dim3(256), smem, st, h->n, b, bp, (const int32_t*)h->rp.as<int32_t>(),
@@ -1273,12 +1337,21 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         RrOut rr_host;
         int it = 0;
         bool converged = false;
+        const bool fused = fused_ok(h, b) && blocked_ok(h, b, b, Yc, Yn);
         for (it = 1; it <= max_iters; ++it) {
-            // Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1};  s = 1^T Y_k came from the last Gram
-            apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>());
             const bool do_rr = (it % h->rr_period == 0) || it == max_iters;
-            // G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, and H' = Y_k^T Y_{k+1} for Rayleigh-Ritz
-            gram(h, b, Yn, do_rr ? Yc : nullptr, st, true);
+            // Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1};  s = 1^T Y_k came from the last Gram
+            if (fused) {
+                // A5 fused with G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, H' = Y_k^T Y_{k+1} (RR) and
+                // the next apply's S^T Y_{k+1} partials (k_fused.cuh)
+                const bool p1 = h->fuse >= 2;
+                const int fl = kApplyFused | (p1 && it > 1 ? kApplyY1Ready : 0) | (!p1 || it == max_iters ? kApplyNoP1 : 0);
+                apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
+            } else {
+                apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>());
+                // G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, and H' = Y_k^T Y_{k+1} for Rayleigh-Ritz
+                gram(h, b, Yn, do_rr ? Yc : nullptr, st, true);
+            }
             if (do_rr) {
                 // H = X_k^T B~ X_k = R_k^{-T} H'
                 profiled(h->prof, PK_RR, st, [&] {
@@ -1413,6 +1486,9 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "dstream")) {
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric}");
         h->dstream = (int)value;
+    } else if (!strcmp(key, "fuse")) {
+        if (value < 0 || value > 2) return fail(SBMDS_EINVAL, "fuse in {0, 1 Gram, 2 Gram + S^T}");
+        h->fuse = (int)value;
     } else if (!strcmp(key, "pair_dbg")) {
         h->pair_dbg = (int)value;   // bit 0: wait-cycle instrumentation; bits 1..: experiment modes
     } else {
