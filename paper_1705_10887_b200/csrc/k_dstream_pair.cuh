@@ -384,6 +384,40 @@ __global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ x, int
     if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
 }
 
+// max |x| over the block upper triangle of D (row r: columns >= 128 floor(r / 128)), which is
+// all of D that is present when create uploaded only the upper strips (and all the packed
+// path reads); D is symmetric (R12), so this is max |D|.
+__global__ void __launch_bounds__(256) k_absmax_upper(const float* __restrict__ x, int64_t l, int64_t ld,
+                                                      unsigned int* __restrict__ out) {
+    float m = 0.f;
+    for (int64_t r = blockIdx.x; r < l; r += gridDim.x) {
+        const float* row = x + r * ld;
+        for (int64_t c = (r >> 7) * 128 + threadIdx.x; c < l; c += 256) m = fmaxf(m, fabsf(__ldcs(row + c)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+// Fill the block lower triangle (row r, columns < 128 floor(r / 128)) from the upper one:
+// D[r][c] = D[c][r]. 32 x 32 tiles through shared memory; only tiles wholly in the missing
+// region do work.
+__global__ void __launch_bounds__(256) k_mirror_lower(float* __restrict__ D, int64_t l, int64_t ld) {
+    __shared__ float tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    if (r0 >= l || c0 + 32 > (r0 >> 7) * 128) return;   // not (wholly) in the missing region
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int k = ty; k < 32; k += 8) {   // read D[c0 + k][r0 + tx] (upper part, present)
+        const int64_t rr = c0 + k, cc = r0 + tx;
+        tile[k][tx] = cc < l ? D[rr * ld + cc] : 0.f;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {   // write D[r0 + k][c0 + tx]
+        const int64_t rr = r0 + k;
+        if (rr < l) D[rr * ld + c0 + tx] = tile[tx][k];
+    }
+}
+
 // exponent e with max * 2^e in [2^14, 2^15) (0 for max = 0 or non-finite)
 __host__ __device__ __forceinline__ int f16_scale_exp(float mx) {
     if (!(mx > 0.f) || !(mx < 3.0e38f)) return 0;

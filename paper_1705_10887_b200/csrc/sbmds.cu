@@ -294,6 +294,8 @@ struct sbmds_ctx {
         CUtensorMap bmap16;
         void* b16_enc = nullptr;
     } pplan[3];
+    bool d_lower_missing = false;   // create uploaded only the block upper triangle of D
+    int64_t h2d_bytes = 0;          // host -> device bytes moved by create (D)
     int pair_dbg = 0;
     DevBuf pdbg;
     double pdbg_avg[2][16] = {};
@@ -570,8 +572,8 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     if (!h->dt_ok) {
         h->Dt.ensure((size_t)pl.ntiles * 128 * 128 * 2 * sizeof(__half));
         CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), st));
-        launch(k_absmax, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256),
-               0, st, (const float*)h->D, h->l, h->l, h->ldD, dmax);
+        launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256),
+               0, st, (const float*)h->D, h->l, h->ldD, dmax);
         launch(k_pack_upper, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
                (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
                (const unsigned int*)dmax, h->Dt.as<__half>());
@@ -635,6 +637,14 @@ bool uses_sym(const sbmds_ctx* h, int bp) {
     return h->dstream == 0 && nt * (nt + 1) / 2 >= 8 * (int64_t)(h->num_sms / 2);
 }
 
+// Mirror the lower triangle of D on the device before the first full-D kernel (see create).
+void ensure_full_d(sbmds_ctx* h, cudaStream_t st) {
+    if (!h->d_lower_missing) return;
+    const unsigned t = (unsigned)((h->l + 31) / 32);
+    launch(k_mirror_lower, dim3(t, t), dim3(256), 0, st, h->D, h->l, h->ldD);
+    h->d_lower_missing = false;
+}
+
 void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
     if (uses_sym(h, bp)) {
         if (bp == 8) run_dstream_pair<8>(h, b, st, Rinv);
@@ -642,6 +652,7 @@ void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
         else run_dstream_pair<32>(h, b, st, Rinv);
         return;
     }
+    ensure_full_d(h, st);
     if (uses_tc(h, bp)) {
         switch (bp) {
             case 8: run_dstream_tc<8>(h, b, st, Rinv); return;
@@ -1123,8 +1134,24 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             h->d_borrowed = true;
         } else {
             h->Dbuf.ensure((size_t)l * h->ldD * sizeof(float));
-            CK(cudaMemcpy2DAsync(h->Dbuf.p, h->ldD * sizeof(float), D_ll, l * sizeof(float), l * sizeof(float), l,
-                                 cudaMemcpyDefault, st));
+            if (!d_dev && !(flags & SBMDS_VALIDATE)) {
+                // host D: only the block upper triangle crosses the host link (D is symmetric,
+                // R12; the default D stream reads only these tiles). Row strip I (rows 128I ..)
+                // from column 128I on; the lower part is mirrored on the device if a full-D
+                // path is ever used (ensure_full_d).
+                for (int64_t r0 = 0; r0 < l; r0 += 128) {
+                    const int64_t rows = std::min<int64_t>(128, l - r0);
+                    CK(cudaMemcpy2DAsync(h->Dbuf.as<float>() + r0 * h->ldD + r0, h->ldD * sizeof(float),
+                                         D_ll + r0 * l + r0, l * sizeof(float), (size_t)(l - r0) * sizeof(float),
+                                         (size_t)rows, cudaMemcpyHostToDevice, st));
+                    h->h2d_bytes += rows * (l - r0) * (int64_t)sizeof(float);
+                }
+                h->d_lower_missing = true;
+            } else {
+                CK(cudaMemcpy2DAsync(h->Dbuf.p, h->ldD * sizeof(float), D_ll, l * sizeof(float), l * sizeof(float), l,
+                                     cudaMemcpyDefault, st));
+                if (!d_dev) h->h2d_bytes += l * l * (int64_t)sizeof(float);
+            }
             h->D = h->Dbuf.as<float>();
             h->own_D = true;
         }
@@ -1507,6 +1534,8 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "blocked_umax")) *value = h->blocked ? (int64_t)h->umax : -1;
     else if (!strcmp(key, "dstream_path")) *value = h->last_dpath;
     else if (!strcmp(key, "dstream_bytes")) *value = h->last_dbytes;
+    else if (!strcmp(key, "h2d_bytes")) *value = h->h2d_bytes;
+    else if (!strcmp(key, "d_lower_missing")) *value = h->d_lower_missing ? 1 : 0;
     else if (!strncmp(key, "pair_dbg_", 9) && (key[9] == 'N' || key[9] == 'T') && key[10] == '_') {
         const int site = atoi(key + 11);
         if (site < 0 || site > 15) return fail(SBMDS_EINVAL, "pair_dbg site in 0..15");

@@ -291,3 +291,26 @@ def test_invalid_eigs_arguments():
     from paper_1705_10887_b200 import Sbmds
     with pytest.raises(SbmdsError, match="non-finite"):
         Sbmds(p.n, p.l, p.row_ptr, p.col_idx, p.val32(), Dbad, validate=True)
+
+
+def test_host_d_upper_upload_and_mirror():
+    """A host D crosses the host link as its block upper triangle only (D is symmetric); the
+    symmetric-half path needs nothing else, and the first full-D apply mirrors the lower
+    triangle on the device. Both paths meet the bar; VALIDATE uploads (and checks) all of D."""
+    p = configs.random_problem(30_011, 2_003, 16, seed=5, name="cfg5_small")
+    X = configs.x_block(p.n, 16, seed=2)
+    ref = oracle_apply(p, X)
+    l = p.l
+    upper = sum(min(128, l - r0) * (l - r0) for r0 in range(0, l, 128)) * 4
+    with make_handle(p, device="numpy") as h:
+        assert h.stat("h2d_bytes") == upper and h.stat("d_lower_missing") == 1
+        h.set_option("dstream", 3)
+        assert relerr(run_apply(h, X), ref) <= TOL
+        assert h.stat("d_lower_missing") == 1
+        h.set_option("dstream", 2)
+        assert relerr(run_apply(h, X), ref) <= TOL
+        assert h.stat("d_lower_missing") == 0
+        h.set_option("dstream", 1)
+        assert relerr(run_apply(h, X[:, :4].copy()), oracle_apply(p, X[:, :4].copy())) <= TOL
+    with make_handle(p, device="numpy", validate=True) as h:
+        assert h.stat("h2d_bytes") == 4 * l * l and h.stat("d_lower_missing") == 0
