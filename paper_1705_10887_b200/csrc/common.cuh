@@ -215,18 +215,20 @@ __device__ __forceinline__ double ordered_sum(const double* __restrict__ p, int 
 }
 
 // Block-wide fixed-order column sums for a last block: out[c] = sum over q < count of
-// p[q * stride + c], c < ncols (ncols divides 256). Thread (c, k) sums chunk k of the q range
-// in order, then thread c adds the 256/ncols chunk results in order: a fixed order, so the
-// result is bitwise reproducible, with 256 threads' loads in flight instead of ncols.
+// p[q * stride + c], 1 <= ncols <= 256. Thread (c, k), k < 256 / ncols, sums chunk k of the q
+// range in order, then thread c adds the chunk results in order: a fixed order, so the result
+// is bitwise reproducible, with up to 256 loads in flight instead of ncols.
 __device__ __forceinline__ void ordered_colsum_block(const double* __restrict__ p, int count, int64_t stride, int ncols,
                                                      double* __restrict__ out) {
     __shared__ double chunk[256];
     const int tid = threadIdx.x, nk = 256 / ncols;
     const int c = tid % ncols, k = tid / ncols;
-    const int per = (count + nk - 1) / nk, q0 = k * per, q1 = min(count, q0 + per);
-    double a = 0.0;
-    for (int q = q0; q < q1; ++q) a += p[(int64_t)q * stride + c];
-    chunk[tid] = a;
+    if (k < nk) {
+        const int per = (count + nk - 1) / nk, q0 = k * per, q1 = min(count, q0 + per);
+        double a = 0.0;
+        for (int q = q0; q < q1; ++q) a += p[(int64_t)q * stride + c];
+        chunk[k * ncols + c] = a;
+    }
     __syncthreads();
     if (tid < ncols) {
         double v = 0.0;

@@ -132,18 +132,27 @@ __global__ void k_check_sym(int64_t l, int64_t ld, const float* __restrict__ D,
 
 // ------------------------------------------------------------------ A1: s = 1^T X  (fp64)
 // Block partials over row ranges, then the last block sums them in block order.
-__global__ void k_colsum(int64_t n, int b, const float* __restrict__ X, double* __restrict__ part,
-                         double* __restrict__ s, unsigned int* __restrict__ counter) {
+__global__ void __launch_bounds__(256) k_colsum(int64_t n, int b, const float* __restrict__ X, double* __restrict__ part,
+                                                double* __restrict__ s, unsigned int* __restrict__ counter) {
     __shared__ double red[256];
     const int rps = blockDim.x / b;                 // rows per step (b <= 64 -> >= 4)
     const int t = threadIdx.x;
     const int c = t % b, r0 = t / b;
     const int64_t rows_per_blk = (n + gridDim.x - 1) / gridDim.x;
     const int64_t beg = blockIdx.x * rows_per_blk, end = min(n, beg + rows_per_blk);
-    double acc = 0.0;
-    if (r0 < rps)
-        for (int64_t i = beg + r0; i < end; i += rps) acc += (double)X[i * b + c];
-    red[t] = (r0 < rps) ? acc : 0.0;
+    // four independent partial sums (rows i, i + rps, i + 2 rps, i + 3 rps of each step of
+    // 4 rps) keep four loads in flight; they are combined in a fixed order
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (r0 < rps) {
+        int64_t i = beg + r0;
+        for (; i + 3 * rps < end; i += 4 * rps) {
+            const float x0 = X[i * b + c], x1 = X[(i + rps) * b + c];
+            const float x2 = X[(i + 2 * rps) * b + c], x3 = X[(i + 3 * rps) * b + c];
+            a0 += (double)x0; a1 += (double)x1; a2 += (double)x2; a3 += (double)x3;
+        }
+        for (; i < end; i += rps) a0 += (double)X[i * b + c];
+    }
+    red[t] = (r0 < rps) ? (a0 + a1) + (a2 + a3) : 0.0;
     __syncthreads();
     if (t < b) {
         double v = 0.0;
@@ -151,7 +160,7 @@ __global__ void k_colsum(int64_t n, int b, const float* __restrict__ X, double* 
         part[blockIdx.x * kMaxB + t] = v;
     }
     if (last_block_done(counter)) {
-        if (t < b) s[t] = ordered_sum(part + t, gridDim.x, kMaxB);
+        ordered_colsum_block(part, gridDim.x, kMaxB, b, s);
         if (t == 0) *counter = 0;
     }
 }
@@ -321,6 +330,55 @@ __global__ void __launch_bounds__(256) k_spmm_csr_gen(
     for (int u = 0; u < NC; ++u) {
         const int cc = q + u * LPR;
         if (cc < b) Y[i * b + cc] = (float)(-0.5 * ((double)acc[u] - t[cc]));
+    }
+}
+
+// Narrow blocks (bp <= 4): L lanes per row stride over the row's nonzeros, so the col / val
+// reads of a warp are contiguous (one lane per row would read 32 rows' entries with a
+// stride of the row length), then a fixed shuffle tree adds the L partial sums (bitwise
+// reproducible). L ~ the mean row length (4 .. 32), BW = bp values per gathered Y2 row.
+template <int L, int BW>
+__global__ void __launch_bounds__(256) k_spmm_csr_sub(
+    int64_t n, int b, int bp, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+    const float* __restrict__ val, const float* __restrict__ Y2, const double* __restrict__ t,
+    float* __restrict__ Y) {
+    constexpr int G = 32 / L;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / L, q = lane % L;
+    const int64_t i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G + g;
+    const bool live = i < n;
+    float acc[BW];
+#pragma unroll
+    for (int u = 0; u < BW; ++u) acc[u] = 0.f;
+    if (live) {
+        const int32_t beg = rp[i], end = rp[i + 1];
+#pragma unroll 2
+        for (int32_t e = beg + q; e < end; e += L) {
+            const int32_t c = __ldg(col + e);
+            const float v = __ldg(val + e);
+            if constexpr (BW == 4) {
+                const float4 y = __ldg(reinterpret_cast<const float4*>(Y2 + (int64_t)c * 4));
+                acc[0] = fmaf(v, y.x, acc[0]);
+                acc[1] = fmaf(v, y.y, acc[1]);
+                acc[2] = fmaf(v, y.z, acc[2]);
+                acc[3] = fmaf(v, y.w, acc[3]);
+            } else if constexpr (BW == 2) {
+                const float2 y = __ldg(reinterpret_cast<const float2*>(Y2 + (int64_t)c * 2));
+                acc[0] = fmaf(v, y.x, acc[0]);
+                acc[1] = fmaf(v, y.y, acc[1]);
+            } else {
+                acc[0] = fmaf(v, __ldg(Y2 + c), acc[0]);
+            }
+        }
+    }
+#pragma unroll
+    for (int off = L / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int u = 0; u < BW; ++u) acc[u] += __shfl_down_sync(0xffffffffu, acc[u], off, L);
+    if (live && q == 0) {
+#pragma unroll
+        for (int u = 0; u < BW; ++u)
+            if (u < b) Y[i * b + u] = (float)(-0.5 * ((double)acc[u] - t[u]));
     }
 }
 

@@ -269,6 +269,8 @@ struct sbmds_ctx {
     bool blocked = false;
     int use_blocked = 1;   // bit 0: S Y2 through the blocked kernel, bit 1: S^T X too
     int gram_tc = 1;       // Gram on the FP64 tensor cores (b <= 32)
+    int csr_nnz_per_lane = 4;   // narrow CSR SpMM: nonzeros per lane when choosing lanes per row
+    int csr_sub_L = 0;          // (tuning) force lanes per row
     int fuse = 1;          // eigs: 1 = A5 fused with the Gram, 2 = also the next A2's S^T partials (k_fused.cuh)
     // D_ll
     float* D = nullptr;
@@ -712,6 +714,29 @@ void spmm_csc(sbmds_ctx* h, int b, int bp, const float* X, cudaStream_t st) {
 }
 
 void spmm_csr(sbmds_ctx* h, int b, int bp, float* Y, cudaStream_t st) {
+    if (bp <= 4) {   // narrow: L lanes per row over its nonzeros (k_spmm_csr_sub)
+        const double avg = (double)h->nnz / (double)std::max<int64_t>(1, h->n);
+        int L = 1;   // ~4 nonzeros per lane, at most 8 lanes per row (measured on the config-5 sweep)
+        while (L < 8 && L * h->csr_nnz_per_lane < avg) L *= 2;
+        if (h->csr_sub_L) L = h->csr_sub_L;
+        const int64_t warps = (h->n + (32 / L) - 1) / (32 / L);
+        const int grid = (int)((warps + 7) / 8);
+        auto go = [&](auto kern) {
+            launch(kern, dim3(grid), dim3(256), 0, st, h->n, b, bp, (const int32_t*)h->rp.as<int32_t>(),
+                   (const int32_t*)h->col.as<int32_t>(), (const float*)h->val.as<float>(),
+                   (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), Y);
+        };
+        auto by_bw = [&](auto l4, auto l2, auto l1) { bp == 4 ? go(l4) : (bp == 2 ? go(l2) : go(l1)); };
+        switch (L) {
+            case 32: by_bw(k_spmm_csr_sub<32, 4>, k_spmm_csr_sub<32, 2>, k_spmm_csr_sub<32, 1>); break;
+            case 16: by_bw(k_spmm_csr_sub<16, 4>, k_spmm_csr_sub<16, 2>, k_spmm_csr_sub<16, 1>); break;
+            case 8: by_bw(k_spmm_csr_sub<8, 4>, k_spmm_csr_sub<8, 2>, k_spmm_csr_sub<8, 1>); break;
+            case 4: by_bw(k_spmm_csr_sub<4, 4>, k_spmm_csr_sub<4, 2>, k_spmm_csr_sub<4, 1>); break;
+            case 2: by_bw(k_spmm_csr_sub<2, 4>, k_spmm_csr_sub<2, 2>, k_spmm_csr_sub<2, 1>); break;
+            default: by_bw(k_spmm_csr_sub<1, 4>, k_spmm_csr_sub<1, 2>, k_spmm_csr_sub<1, 1>); break;
+        }
+        return;
+    }
     const bool vec = (b == bp) && (b % 4 == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
     const int lpr = vec ? b / 4 : std::min(bp, 32);
     const int G = 32 / lpr;
@@ -795,7 +820,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     ensure_apply_ws(h, bp);
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
     if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] {
-        launch(k_colsum, dim3(kRedBlocks), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(),
+        launch(k_colsum, dim3((unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256)), dim3(256), 0, st,
+               h->n, b, X, h->colpart.as<double>(),
                h->s.as<double>(), h->counters.as<unsigned int>() + CNT_COLSUM);
     });
     const bool blk = blocked_ok(h, b, bp, X, Y);
@@ -968,7 +994,9 @@ void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
     CK(cudaMemcpyAsync(&umax, um.p, sizeof umax, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     h->umax = umax;
-    h->blocked = true;
+    // staging pays only when a staged landmark row is reused: mean uses per dictionary entry
+    // >= 4 (config 4: ~40; random rows over wide column windows: ~1)
+    h->blocked = (double)h->nnz >= 4.0 * (double)std::max<int32_t>(1, h->total_u);
 }
 
 template <typename F>
@@ -1023,7 +1051,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         h->cval.ensure(nz * sizeof(float));
         h->order.ensure(l * sizeof(int32_t));
         h->w.ensure(l * sizeof(double));
-        h->colpart.ensure(kRedBlocks * kMaxB * sizeof(double));
+        h->colpart.ensure(4 * kRedBlocks * kMaxB * sizeof(double));
         h->tpart.ensure(kRedBlocks * kMaxB * sizeof(double));
         h->s.ensure(kMaxB * sizeof(double));
         h->t.ensure(kMaxB * sizeof(double));
@@ -1513,6 +1541,10 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "dstream")) {
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric}");
         h->dstream = (int)value;
+    } else if (!strcmp(key, "csr_sub_L")) {
+        if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16 || value == 32))
+            return fail(SBMDS_EINVAL, "csr_sub_L in {0 auto, 1, 2, 4, 8, 16, 32}");
+        h->csr_sub_L = (int)value;
     } else if (!strcmp(key, "fuse")) {
         if (value < 0 || value > 2) return fail(SBMDS_EINVAL, "fuse in {0, 1 Gram, 2 Gram + S^T}");
         h->fuse = (int)value;

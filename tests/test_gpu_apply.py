@@ -314,3 +314,22 @@ def test_host_d_upper_upload_and_mirror():
         assert relerr(run_apply(h, X[:, :4].copy()), oracle_apply(p, X[:, :4].copy())) <= TOL
     with make_handle(p, device="numpy", validate=True) as h:
         assert h.stat("h2d_bytes") == 4 * l * l and h.stat("d_lower_missing") == 0
+
+
+@pytest.mark.parametrize("l", [1, 5, 127, 128, 129, 300, 1025])
+@pytest.mark.parametrize("b", [8, 16, 32])
+def test_symmetric_half_small_l(l, b):
+    """Forced symmetric-half stream at tile-boundary sizes: one tile (the T CTA sees only a
+    diagonal tile and emits an empty flush), l = 127 / 128 / 129, more pairs than blocks."""
+    n = max(4 * l, 64)
+    p = configs.random_problem(n, l, min(8, l), seed=l + b, window=min(256, l), name="small_l")
+    X = configs.x_block(p.n, b, seed=l)
+    with make_handle(p) as h:
+        h.set_option("dstream", 3)
+        Y = run_apply(h, X)
+        assert h.stat("dstream_path") == 3
+    ref = oracle_apply(p, X)
+    if l == 1:
+        assert np.abs(Y).max() <= 1e-6 * max(1.0, np.abs(X).max())
+    else:
+        assert relerr(Y, ref) <= TOL
