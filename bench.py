@@ -152,7 +152,8 @@ def algorithmic_bytes(p, b):
 
 
 DSTREAM_KERNELS = {1: "k_dstream_ffma", 2: "k_dstream_tc (tcgen05 3xTF32, full D)",
-                   3: "k_dstream_pair (tcgen05 2xFP16, symmetric half of D, CTA pairs)"}
+                   3: "k_dstream_sym8 (tcgen05 kind::i8, 24-bit fixed point, symmetric half of D)",
+                   4: "k_dstream_pair (tcgen05 2xFP16, symmetric half of D, CTA pairs)"}
 
 
 def log(msg):
@@ -264,7 +265,8 @@ def run_ours(args, ws, rank, local):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if ds_path != 3 else "f32 (D Y1 as a 2xfp16 split, fp32 accumulate; DESIGN.md §4)",
+        "dtype": {3: "f32 (D Y1 as 24-bit fixed point on int8 tensor cores, exact int32 accumulate; DESIGN.md §4)",
+                  4: "f32 (D Y1 as a 2xfp16 split, fp32 accumulate; DESIGN.md §4)"}.get(ds_path, "f32"),
         "data": "synthetic (seeded torus mesh stand-in for Dragon1800k; DESIGN.md §3)",
         "config": {"workload": f"config {args.config}: {p.name}", "n": p.n, "l": p.l, "k": 32,
                    "nnz": p.nnz, "block": b, "m": m, "iters_per_step": iters,

@@ -486,8 +486,10 @@ __global__ void __launch_bounds__(256) k_y16_split(int64_t lpad, int bp, const f
 // memory (see the top of this file); zero outside l.
 __global__ void __launch_bounds__(256) k_pack_upper(const float* __restrict__ D, int64_t ldD, int64_t l,
                                                     const uint32_t* __restrict__ tiles, int64_t NT, int64_t ntiles,
-                                                    const unsigned int* __restrict__ dmax, __half* __restrict__ Dt) {
+                                                    const unsigned int* __restrict__ dmax, int* __restrict__ dexp,
+                                                    __half* __restrict__ Dt) {
     const int sD = f16_scale_exp(__uint_as_float(*dmax));
+    if (blockIdx.x == 0 && threadIdx.x == 0) *dexp = sD;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint32_t v = tiles[t];
         const int I = (int)(v >> 16), J = (int)(v & 0xFFFFu);
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(256) k_pack_upper(const float* __restrict__ D,
 // exact scales of D and of Y1's column c), then t = w^T Y2 (A4).
 __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, const int* __restrict__ xptr,
                                                       const int* __restrict__ xslot, const float* __restrict__ P,
-                                                      const unsigned int* __restrict__ dmax, const int* __restrict__ yexp,
+                                                      const int* __restrict__ dexp, const int* __restrict__ yexp,
                                                       const double* __restrict__ w, float* __restrict__ Y2,
                                                       double* __restrict__ tpart, double* __restrict__ t,
                                                       unsigned int* __restrict__ counter) {
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
     const int tid = threadIdx.x;
     const int cidx = tid % bp, rloc = tid / bp;
     double acc_t = 0.0;
-    const double unscale = ldexp(1.0, -(f16_scale_exp(__uint_as_float(*dmax)) + yexp[cidx]));
+    const double unscale = ldexp(1.0, -(*dexp + yexp[cidx]));
     for (int64_t r0 = (int64_t)blockIdx.x * rows_per_blk; r0 < l; r0 += (int64_t)gridDim.x * rows_per_blk) {
         const int64_t r = r0 + rloc;
         if (rloc < rows_per_blk && r < l) {

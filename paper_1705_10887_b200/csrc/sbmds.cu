@@ -19,6 +19,7 @@
 #include "k_dstream.cuh"
 #include "k_dstream_tc.cuh"
 #include "k_dstream_pair.cuh"
+#include "k_dstream_sym8.cuh"
 #include "k_small.cuh"
 #include "k_sparse.cuh"
 #include "k_blocked.cuh"
@@ -288,6 +289,9 @@ struct sbmds_ctx {
     // and one schedule per tensor width bp in {8, 16, 32}
     DevBuf Dt, Y16T, Y1f, y16aux;
     bool dt_ok = false;
+    // int8 symmetric-half stream (k_dstream_sym8.cuh): D as three digit planes per upper tile
+    DevBuf Dt8, Y8T;
+    bool dt8_ok = false;
     struct PairPlan {
         bool ok = false;
         int S = 0, NT = 0, P = 0, nslots = 0;
@@ -295,7 +299,7 @@ struct sbmds_ctx {
         DevBuf tiles, pbeg, sbase, xptr, xslot;
         CUtensorMap bmap16;
         void* b16_enc = nullptr;
-    } pplan[3];
+    } pplan[3], s8plan[3];
     bool d_lower_missing = false;   // create uploaded only the block upper triangle of D
     int64_t h2d_bytes = 0;          // host -> device bytes moved by create (D)
     int pair_dbg = 0;
@@ -471,10 +475,7 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
 // partial slots each role writes (simulating exactly the kernel's flush rule: a segment ends
 // when the walk enters another block; its touched accumulators flush in index order), and
 // per row tile X the list of its slots in slot order (the fixed reduction order).
-template <int BP>
-void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs) {
-    using C = PairCfg<BP>;
-    const int S = C::S;
+void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S) {
     const int NT = (int)((h->l + 127) / 128);
     if (NT > 65535) throw std::runtime_error("l too large for the symmetric-half stream");
     const int NBk = (NT + S - 1) / S;
@@ -565,10 +566,12 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         attr_set[pi] = true;
     }
     const int64_t lpad = y1t_lpad(h);
-    if (!pl.ok) build_pair_plan<BP>(h, pl, max_clusters[pi]);
-    // aux: [0] max |D| bits, [64..128) per-column max |Y1| bits, [128..192) column exponents
+    if (!pl.ok) build_pair_plan(h, pl, max_clusters[pi], C::S);
+    // aux: [0] max |D| bits, [1] D exponent, [64..128) per-column max |Y1| bits, [128..192)
+    // column exponents; [2] max |D| of the int8 packing, [3] its exponent
     h->y16aux.ensure(192 * sizeof(unsigned int));
     unsigned int* dmax = h->y16aux.as<unsigned int>();
+    int* dexp = reinterpret_cast<int*>(dmax + 1);
     unsigned int* ymax = dmax + 64;
     int* yexp = reinterpret_cast<int*>(dmax + 128);
     if (!h->dt_ok) {
@@ -578,7 +581,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
                0, st, (const float*)h->D, h->l, h->ldD, dmax);
         launch(k_pack_upper, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
                (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
-               (const unsigned int*)dmax, h->Dt.as<__half>());
+               (const unsigned int*)dmax, dexp, h->Dt.as<__half>());
         h->dt_ok = true;
     }
     h->Y16T.ensure((size_t)2 * kMaxB * lpad * sizeof(__half));
@@ -622,19 +625,82 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     h->tpart.ensure((size_t)4 * kRedBlocks * kMaxB * sizeof(double));
     profiled(h->prof, PK_DREDUCE, st, [&] {
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
-               (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const unsigned int*)dmax,
+               (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const int*)dexp,
                (const int*)yexp, (const double*)h->w.as<double>(), h->Y2.as<float>(), h->tpart.as<double>(),
                h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
     });
-    h->last_dpath = 3;
+    h->last_dpath = 4;
     h->last_dbytes = pl.ntiles * (int64_t)128 * 128 * 4 + 12 * h->l * (int64_t)b;
 }
+
+// A3 + A4 on the int8 tensor cores over the symmetric half of D (k_dstream_sym8.cuh).
+template <int BP>
+void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
+    using C = Sym8Cfg<BP>;
+    const int pi = BP == 8 ? 0 : (BP == 16 ? 1 : 2);
+    auto& pl = h->s8plan[pi];
+    static bool attr_set[3] = {false, false, false};
+    if (!attr_set[pi]) {
+        CK(cudaFuncSetAttribute(k_dstream_sym8<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        attr_set[pi] = true;
+    }
+    const int64_t lpad = y1t_lpad(h);
+    if (!pl.ok) build_pair_plan(h, pl, h->num_sms, C::S);   // one CTA per SM; both roles in every CTA
+    h->y16aux.ensure(192 * sizeof(unsigned int));
+    unsigned int* aux = h->y16aux.as<unsigned int>();
+    unsigned int* dmax8 = aux + 2;
+    int* dexp8 = reinterpret_cast<int*>(aux + 3);
+    unsigned int* ymax = aux + 64;
+    int* yexp = reinterpret_cast<int*>(aux + 128);
+    if (!h->dt8_ok) {
+        h->Dt8.ensure((size_t)pl.ntiles * C::A_BYTES);
+        CK(cudaMemsetAsync(dmax8, 0, sizeof(unsigned int), st));
+        launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256), 0, st,
+               (const float*)h->D, h->l, h->ldD, dmax8);
+        launch(k_pack_sym8, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
+               (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
+               (const unsigned int*)dmax8, dexp8, h->Dt8.as<int8_t>());
+        h->dt8_ok = true;
+    }
+    h->Y8T.ensure((size_t)3 * kMaxB * lpad);
+    h->Y1f.ensure((size_t)lpad * kMaxB * sizeof(float));
+    if (pl.b16_enc != h->Y8T.p) {
+        encode_tiled_dt(&pl.bmap16, h->Y8T.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, lpad, C::NB, lpad, 128, C::NB,
+                        CU_TENSOR_MAP_SWIZZLE_128B);
+        pl.b16_enc = h->Y8T.p;
+    }
+    profiled(h->prof, PK_SPLIT, st, [&] {
+        CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
+        launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax);
+        launch(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
+               lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
+    });
+    h->P.ensure((size_t)std::max(1, pl.nslots) * 128 * BP * sizeof(float));
+    profiled(h->prof, PK_DSTREAM, st, [&] {
+        launch(k_dstream_sym8<BP>, dim3(pl.P), dim3(C::THREADS), (size_t)C::SMEM, st, (const int8_t*)h->Dt8.p,
+               pl.bmap16, (const uint32_t*)pl.tiles.p, (const int64_t*)pl.pbeg.p, (const int*)pl.sbase.p,
+               (int)pl.NT, h->P.as<float>());
+    });
+    const int rows_per_blk = 256 / BP;
+    const int grid = (int)std::min<int64_t>(4 * kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
+    h->tpart.ensure((size_t)4 * kRedBlocks * kMaxB * sizeof(double));
+    profiled(h->prof, PK_DREDUCE, st, [&] {
+        launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
+               (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
+               (const double*)h->w.as<double>(), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
+               h->counters.as<unsigned int>() + CNT_DRED);
+    });
+    h->last_dpath = 3;
+    h->last_dbytes = pl.ntiles * (int64_t)C::A_BYTES + 12 * h->l * (int64_t)b;
+}
+
 bool uses_tc(const sbmds_ctx* h, int bp) { return bp >= 8 && (h->dstream == 2 || h->dstream == 0 || h->dstream == 3); }
 // symmetric-half stream: forced by dstream = 3, chosen by auto (0) once D has >= 8 tiles per
 // CTA pair (below that D is L2-resident and the full stream on all SMs wins)
 bool uses_sym(const sbmds_ctx* h, int bp) {
     if (!(bp == 8 || bp == 16 || bp == 32)) return false;
-    if (h->dstream == 3) return true;
+    if (h->dstream == 3 || h->dstream == 4) return true;
     const int64_t nt = (h->l + 127) / 128;
     return h->dstream == 0 && nt * (nt + 1) / 2 >= 8 * (int64_t)(h->num_sms / 2);
 }
@@ -649,9 +715,15 @@ void ensure_full_d(sbmds_ctx* h, cudaStream_t st) {
 
 void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
     if (uses_sym(h, bp)) {
-        if (bp == 8) run_dstream_pair<8>(h, b, st, Rinv);
-        else if (bp == 16) run_dstream_pair<16>(h, b, st, Rinv);
-        else run_dstream_pair<32>(h, b, st, Rinv);
+        if (h->dstream == 4) {   // 2xFP16 on CTA pairs (k_dstream_pair), kept for comparison
+            if (bp == 8) run_dstream_pair<8>(h, b, st, Rinv);
+            else if (bp == 16) run_dstream_pair<16>(h, b, st, Rinv);
+            else run_dstream_pair<32>(h, b, st, Rinv);
+        } else {
+            if (bp == 8) run_dstream_sym8<8>(h, b, st, Rinv);
+            else if (bp == 16) run_dstream_sym8<16>(h, b, st, Rinv);
+            else run_dstream_sym8<32>(h, b, st, Rinv);
+        }
         return;
     }
     ensure_full_d(h, st);
@@ -1005,7 +1077,10 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
+                      &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot,
+                      &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot,
+                      &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot,
                       &h->pplan[0].tiles, &h->pplan[0].pbeg, &h->pplan[0].sbase, &h->pplan[0].xptr, &h->pplan[0].xslot,
                       &h->pplan[1].tiles, &h->pplan[1].pbeg, &h->pplan[1].sbase, &h->pplan[1].xptr, &h->pplan[1].xslot,
                       &h->pplan[2].tiles, &h->pplan[2].pbeg, &h->pplan[2].sbase, &h->pplan[2].xptr, &h->pplan[2].xslot};
@@ -1539,7 +1614,8 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         h->prof.drain();
         for (int k = 0; k < PK_N; ++k) { h->prof.ns[k] = 0; h->prof.cnt[k] = 0; }
     } else if (!strcmp(key, "dstream")) {
-        if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric}");
+        if (value < 0 || value > 4)
+            return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric int8, 4 symmetric 2xfp16 pairs}");
         h->dstream = (int)value;
     } else if (!strcmp(key, "csr_sub_L")) {
         if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16 || value == 32))

@@ -65,7 +65,23 @@ __global__ void probe(int M, int N, int mode, int nacc, unsigned long long* out)
             out[1] = (unsigned long long)(c2 - c0);
         }
     }
-    if (threadIdx.x == 0 && nacc > 0 && mode >= 10) {
+    if (threadIdx.x == 0 && nacc > 0 && mode >= 20) {
+        // kind::i8 (signed 8-bit A and B, s32 accumulate): a/b_format = 1 (signed), c_format = 2 (S32)
+        const uint32_t sa = smem_u32(sm), sb = sa + 64 * 1024;
+        const uint32_t id = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+        const uint64_t da = desc(sa, 16, 1024, 2), db = desc(sb, 16, 1024, 2);
+        const long long c0 = clock64();
+        for (int i = 0; i < NMMA; ++i)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                         ::"r"(tb), "l"(da), "l"(db), "r"(id), "r"(1));
+        const long long c1 = clock64();
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+        asm volatile("{\n\t.reg .pred P1;\n\tW4:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W4;\n\t}" ::"r"(smem_u32(&bar)) : "memory");
+        const long long c2 = clock64();
+        out[0] = (unsigned long long)(c1 - c0);
+        out[1] = (unsigned long long)(c2 - c0);
+    }
+    if (threadIdx.x == 0 && nacc > 0 && mode >= 10 && mode < 20) {
         const uint32_t sa = smem_u32(sm), sb = sa + 64 * 1024;
         const uint32_t id = idesc(M, N, 0, 0, 1);
         const uint64_t da = desc(sa, 16, 1024, 2), db = desc(sb, 16, 1024, 2);
@@ -118,11 +134,12 @@ int main() {
     unsigned long long* d;
     cudaMalloc(&d, 16);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-    const char* nmv[13] = {"tf32 SS", "tf32 SS-MN", "tf32 TS", "tf32 SS-BMN", "", "", "", "", "", "", "bf16 SS", "", "bf16 TS"};
+    const char* nmv[21] = {"tf32 SS", "tf32 SS-MN", "tf32 TS", "tf32 SS-BMN", "", "", "", "", "", "", "bf16 SS", "", "bf16 TS",
+                           "", "", "", "", "", "", "", "i8 SS"};
     const char** nm = nmv;
     for (int nacc : {1})
-    for (int mode : {0, 2, 10, 12})
-        for (int M : {64, 128})
+    for (int mode : {0, 10, 20})
+        for (int M : {128})
             for (int N : {16, 32, 48, 64, 128, 256}) {
                 if (N * (nacc < 0 ? -nacc : nacc) > 256) continue;
                 probe<<<1, 128, 128 * 1024>>>(M, N, mode, nacc, d);

@@ -196,17 +196,18 @@ def test_apply_blocked_and_plain_sparse_paths(blocked, b):
     assert relerr(Y, oracle_apply(p, X)) <= TOL
 
 
+@pytest.mark.parametrize("dstream", [3, 4])
 @pytest.mark.parametrize("b", [16, 12, 8, 5, 32, 20])
-def test_apply_symmetric_half_stream(b):
-    """NEXT-1: streaming only the upper triangle of D (k_dstream_pair, CTA pairs) meets the
+def test_apply_symmetric_half_stream(b, dstream):
+    """NEXT-1: streaming only the upper triangle of D (3: k_dstream_sym8, 4: k_dstream_pair) meets the
     bar; l = 2003 gives 16 row tiles with a ragged last one, so diagonal, off-diagonal and
     transposed tiles, blocks split between pairs and (b = 8) a single block all occur."""
     p = configs.random_problem(30_011, 2_003, 16, seed=b + 100, name="cfg5_small")
     X = configs.x_block(p.n, b, seed=b)
     with make_handle(p) as h:
-        h.set_option("dstream", 3)
+        h.set_option("dstream", dstream)
         Y = run_apply(h, X)
-        assert h.stat("dstream_path") == 3
+        assert h.stat("dstream_path") == dstream
     assert relerr(Y, oracle_apply(p, X)) <= TOL
 
 
