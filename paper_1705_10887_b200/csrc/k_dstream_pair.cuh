@@ -538,11 +538,11 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
             for (; q + 16 <= q1; q += 16) {
                 float pv[16];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) pv[u] = P[((int64_t)xslot[q + u] * 128 + rr) * bp + cidx];
+                for (int u = 0; u < 16; ++u) pv[u] = P[((int64_t)(xslot ? xslot[q + u] : q + u) * 128 + rr) * bp + cidx];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) v += (double)pv[u];
             }
-            for (; q < q1; ++q) v += (double)P[((int64_t)xslot[q] * 128 + rr) * bp + cidx];
+            for (; q < q1; ++q) v += (double)P[((int64_t)(xslot ? xslot[q] : q) * 128 + rr) * bp + cidx];
             v *= unscale;
             Y2[r * bp + cidx] = (float)v;
             if (cidx < b) acc_t += w[r] * v;

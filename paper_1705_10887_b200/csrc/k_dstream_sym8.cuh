@@ -30,8 +30,10 @@
 // balanced range. Inside a block the N accumulators are the S tile rows, the T accumulators
 // the S tile columns (TMEM, int32, exact); when the walk leaves a block every touched
 // accumulator becomes one fp32 partial (c0 + c1/256 + c2/65536, formed in fp64) in a slot
-// numbered by the host schedule, and k_dreduce_pair adds each row tile's slots in slot order
-// in fp64 and undoes the scales (deterministic).
+// numbered by the host schedule; row accumulators persist across up to GN blocks of a block
+// row (halving the partials), and the slots are laid out row tile by row tile, so
+// k_dreduce_pair reads each row tile's partials contiguously, in slot order, in fp64 and
+// undoes the scales (deterministic).
 //
 // Roles (192 threads): warp 0 producer, warp 1 TMEM alloc + MMA issue (converged warp, one
 // elected lane issues), warps 2-5 epilogue. Each mbarrier has one producer role and one
@@ -50,6 +52,9 @@ struct Sym8Cfg {
     static constexpr int ACCW = BP < 16 ? 32 : 3 * BP;     // TMEM columns per accumulator: c0 | c1 | c2
     static constexpr int S = (256 / ACCW) > 16 ? 16 : (256 / ACCW);   // accumulators per role
     static constexpr int T0 = S * ACCW;                     // first column of the T accumulators
+    // a row accumulator spans at most GN blocks (GN * S <= 256 tiles = 32,768 k): the int32 sums
+    // of up to 3 digit products (|.| <= 16,129) stay below 2^31
+    static constexpr int GN = 256 / S;
     static constexpr int PLANE = TT * 128;                  // 16 KB: 128 rows x 128 int8
     static constexpr int A_BYTES = 3 * PLANE;               // 48 KB packed tile
     static constexpr int BOX_B = NB * 128;                  // 128 k of [y0; y1; y2]
@@ -104,7 +109,7 @@ template <int BP>
 __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
     k_dstream_sym8(const int8_t* __restrict__ Dt, const __grid_constant__ CUtensorMap bmap,
                    const uint32_t* __restrict__ tiles, const int64_t* __restrict__ cbeg,
-                   const int* __restrict__ sbase, int NT, float* __restrict__ P) {
+                   const int* __restrict__ sbase, const int* __restrict__ smap, int NT, float* __restrict__ P) {
     using C = Sym8Cfg<BP>;
     constexpr int S = C::S;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -184,11 +189,14 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
             int I, J;
             tile_of(t, I, J);
             const int bi = I / S, bj = J / S;
-            bool end_seg = (t + 1 == t1);
+            // segment ends: T (column accumulators) at every block change, N (row accumulators)
+            // when the block row or the group of GN block columns changes
+            bool end_seg = (t + 1 == t1), end_n = end_seg;
             if (!end_seg) {
                 int I2, J2;
                 tile_of(t + 1, I2, J2);
                 end_seg = (I2 / S != bi) || (J2 / S != bj);
+                end_n = (I2 / S != bi) || ((J2 / S) / C::GN != bj / C::GN);
             }
             const bool diag = (I == J);
             const int aN = I - bi * S, aT = J - bj * S;
@@ -240,15 +248,17 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
             if (end_seg) {
                 const int eb = ev & 1;
                 mbar_wait(&ev_empty[eb], ((ev >> 1) & 1u) ^ 1u, 125 * 65536 + (int)(ev & 0xFFFF));
+                const uint32_t mN = end_n ? maskN : 0u;
                 if (elect_one()) {
-                    evq[eb] = Sym8Event{maskN, maskT, slotN, slotT, (t + 1 == t1) ? 1u : 0u, 0u, 0u, 0u};
+                    evq[eb] = Sym8Event{mN, maskT, slotN, slotT, (t + 1 == t1) ? 1u : 0u, 0u, 0u, 0u};
                     tc_commit(&ev_full[eb]);
                     mbar_arrive(&ev_full[eb]);
                 }
                 __syncwarp();
-                slotN += (uint32_t)__popc(maskN);
+                slotN += (uint32_t)__popc(mN);
                 slotT += (uint32_t)__popc(maskT);
-                maskN = maskT = 0;
+                if (end_n) maskN = 0;
+                maskT = 0;
                 ++ev;
             }
         }
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
             }
             tc_fence_before();
             mbar_arrive(emp);
-            float4* dst = reinterpret_cast<float4*>(P + ((int64_t)slot * C::TT + ln) * BP);
+            float4* dst = reinterpret_cast<float4*>(P + ((int64_t)__ldg(smap + slot) * C::TT + ln) * BP);
 #pragma unroll
             for (int c0 = 0; c0 < BP; c0 += 4) dst[c0 / 4] = make_float4(out[c0], out[c0 + 1], out[c0 + 2], out[c0 + 3]);
         };

@@ -296,7 +296,7 @@ struct sbmds_ctx {
         bool ok = false;
         int S = 0, NT = 0, P = 0, nslots = 0;
         int64_t ntiles = 0;
-        DevBuf tiles, pbeg, sbase, xptr, xslot;
+        DevBuf tiles, pbeg, sbase, xptr, xslot, smap;
         CUtensorMap bmap16;
         void* b16_enc = nullptr;
     } pplan[3], s8plan[3];
@@ -475,7 +475,11 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
 // partial slots each role writes (simulating exactly the kernel's flush rule: a segment ends
 // when the walk enters another block; its touched accumulators flush in index order), and
 // per row tile X the list of its slots in slot order (the fixed reduction order).
-void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S) {
+// gN > 1 (k_dstream_sym8): the row ("N") accumulators live across gN consecutive blocks of a
+// block row (their segments end when (bi, bj / gN) changes), the column ("T") ones per block.
+// contiguous: physical slot = rank of (X, logical slot), so each row tile's partials are
+// contiguous for k_dreduce_pair; the kernel maps logical -> physical through pl.smap.
+void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S, int gN = 1, bool contiguous = false) {
     const int NT = (int)((h->l + 127) / 128);
     if (NT > 65535) throw std::runtime_error("l too large for the symmetric-half stream");
     const int NBk = (NT + S - 1) / S;
@@ -497,7 +501,7 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
         for (int role = 0; role < 2; ++role) {
             sbase[2 * p + role] = (int)slot_x.size();
             uint32_t mask = 0;
-            int cbi = -1, cbj = -1;
+            int cbi = -1, cbj = -1, ckey = -1;
             auto emit = [&]() {
                 for (int a = 0; a < S; ++a)
                     if (mask & (1u << a)) slot_x.push_back(role ? cbj * S + a : cbi * S + a);
@@ -506,9 +510,11 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
             for (int64_t t = pbeg[p]; t < pbeg[p + 1]; ++t) {
                 const int I = (int)(tiles[t] >> 16), J = (int)(tiles[t] & 0xFFFFu);
                 const int bi = I / S, bj = J / S;
-                if ((bi != cbi || bj != cbj) && mask) emit();
+                const int key = role ? bj : bj / gN;
+                if ((bi != cbi || key != ckey) && mask) emit();
                 cbi = bi;
                 cbj = bj;
+                ckey = key;
                 if (role == 1 && I == J) continue;
                 mask |= 1u << (role ? J - bj * S : I - bi * S);
             }
@@ -521,6 +527,13 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
     {
         std::vector<int> fill(xptr.begin(), xptr.end() - 1);
         for (int q = 0; q < nslots; ++q) xslot[fill[slot_x[q]]++] = q;   // ascending slot ids per X
+    }
+    if (contiguous) {   // smap[logical] = physical (X-major, then logical order); xslot = identity
+        std::vector<int> smap(std::max(1, nslots));
+        for (int pq = 0; pq < nslots; ++pq) smap[xslot[pq]] = pq;
+        for (int pq = 0; pq < nslots; ++pq) xslot[pq] = pq;
+        pl.smap.ensure(smap.size() * sizeof(int));
+        CK(cudaMemcpy(pl.smap.p, smap.data(), smap.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     pl.tiles.ensure(tiles.size() * sizeof(uint32_t));
     pl.pbeg.ensure(pbeg.size() * sizeof(int64_t));
@@ -645,7 +658,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         attr_set[pi] = true;
     }
     const int64_t lpad = y1t_lpad(h);
-    if (!pl.ok) build_pair_plan(h, pl, h->num_sms, C::S);   // one CTA per SM; both roles in every CTA
+    if (!pl.ok) build_pair_plan(h, pl, h->num_sms, C::S, C::GN, true);   // one CTA per SM, both roles
     h->y16aux.ensure(192 * sizeof(unsigned int));
     unsigned int* aux = h->y16aux.as<unsigned int>();
     unsigned int* dmax8 = aux + 2;
@@ -680,14 +693,14 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_DSTREAM, st, [&] {
         launch(k_dstream_sym8<BP>, dim3(pl.P), dim3(C::THREADS), (size_t)C::SMEM, st, (const int8_t*)h->Dt8.p,
                pl.bmap16, (const uint32_t*)pl.tiles.p, (const int64_t*)pl.pbeg.p, (const int*)pl.sbase.p,
-               (int)pl.NT, h->P.as<float>());
+               (const int*)pl.smap.p, (int)pl.NT, h->P.as<float>());
     });
     const int rows_per_blk = 256 / BP;
     const int grid = (int)std::min<int64_t>(4 * kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     h->tpart.ensure((size_t)4 * kRedBlocks * kMaxB * sizeof(double));
     profiled(h->prof, PK_DREDUCE, st, [&] {
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
-               (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
+               (const int*)nullptr, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
                (const double*)h->w.as<double>(), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
                h->counters.as<unsigned int>() + CNT_DRED);
     });
@@ -1078,9 +1091,9 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
-                      &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot,
-                      &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot,
-                      &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot,
+                      &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
+                      &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
+                      &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
                       &h->pplan[0].tiles, &h->pplan[0].pbeg, &h->pplan[0].sbase, &h->pplan[0].xptr, &h->pplan[0].xslot,
                       &h->pplan[1].tiles, &h->pplan[1].pbeg, &h->pplan[1].sbase, &h->pplan[1].xptr, &h->pplan[1].xslot,
                       &h->pplan[2].tiles, &h->pplan[2].pbeg, &h->pplan[2].sbase, &h->pplan[2].xptr, &h->pplan[2].xslot};
