@@ -79,6 +79,43 @@ __global__ void k_blk_scatter(int32_t nnz, const int32_t* __restrict__ scol, con
 // One CTA per 256-row block: Y2[dict_B] -> smem, then LPR lanes per row (float4 each);
 // a row's nnz metadata is read LPR entries at a time (one coalesced load per lane) and
 // broadcast within the lane group by shuffles.
+// Sum over one row of S of val * Y2[dict[lcol]] (staged in shared memory as float4 rows), LPR
+// lanes per row (lane q owns float4 q of the b values). The loop is warp-uniform (maxlen = the
+// warp's longest row) so the shuffles are full-warp; each lane first loads 8 of the row's
+// (column, value) pairs with independent loads, then the group consumes them in entry order
+// (beg, beg + 1, ...): the summation order is fixed, so results are bitwise reproducible.
+template <int LPR>
+__device__ __forceinline__ float4 blk_row_sum(int32_t beg, int32_t end, int maxlen, int q,
+                                              const uint16_t* __restrict__ lcol, const float* __restrict__ val,
+                                              const float4* __restrict__ ys4, int nv) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = 0; c0 < maxlen; c0 += 8 * LPR) {
+        int lc[8];
+        float vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int32_t e = beg + c0 + u * LPR + q;
+            const bool ok = e < end;
+            lc[u] = ok ? (int)__ldg(lcol + e) : 0;
+            vv[u] = ok ? __ldg(val + e) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+            for (int tq = 0; tq < LPR; ++tq) {
+                const int c = __shfl_sync(0xffffffffu, lc[u], tq, LPR);
+                const float v = __shfl_sync(0xffffffffu, vv[u], tq, LPR);
+                const float4 y = ys4[c * nv + q];
+                acc.x = fmaf(v, y.x, acc.x);
+                acc.y = fmaf(v, y.y, acc.y);
+                acc.z = fmaf(v, y.z, acc.z);
+                acc.w = fmaf(v, y.w, acc.w);
+            }
+        }
+    }
+    return acc;
+}
+
 template <int LPR>
 __global__ void __launch_bounds__(256) k_blk_spmm(int64_t n, int b, int bp, const int32_t* __restrict__ rp,
                                                   const uint16_t* __restrict__ lcol, const float* __restrict__ val,
@@ -99,26 +136,13 @@ __global__ void __launch_bounds__(256) k_blk_spmm(int64_t n, int b, int bp, cons
     const int g = lane / LPR, q = lane % LPR;
     const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (g * LPR));
     const double t0 = t[4 * q], t1 = t[4 * q + 1], t2 = t[4 * q + 2], t3 = t[4 * q + 3];
-    for (int r = warp * G + g; r < kRB; r += 8 * G) {
+    for (int r = warp * G + g; r < kRB; r += 8 * G) {   // the same trip count for every lane
         const int64_t i = B * kRB + r;
-        if (i >= n) break;
-        const int32_t beg = rp[i], end = rp[i + 1];
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int32_t e0 = beg; e0 < end; e0 += LPR) {
-            const int32_t e = e0 + q;
-            const int lc_l = (e < end) ? (int)lcol[e] : 0;
-            const float v_l = (e < end) ? val[e] : 0.f;
-#pragma unroll
-            for (int tq = 0; tq < LPR; ++tq) {
-                const int lc = __shfl_sync(gmask, lc_l, tq, LPR);
-                const float v = __shfl_sync(gmask, v_l, tq, LPR);
-                const float4 y = ys4[lc * nv + q];
-                acc.x = fmaf(v, y.x, acc.x);
-                acc.y = fmaf(v, y.y, acc.y);
-                acc.z = fmaf(v, y.z, acc.z);
-                acc.w = fmaf(v, y.w, acc.w);
-            }
-        }
+        const bool live = i < n;
+        const int32_t beg = live ? rp[i] : 0, end = live ? rp[i + 1] : 0;
+        const int maxlen = __reduce_max_sync(0xffffffffu, (unsigned)(end - beg));
+        const float4 acc = blk_row_sum<LPR>(beg, end, maxlen, q, lcol, val, ys4, nv);
+        if (!live) continue;
         float4 out;
         out.x = (float)(-0.5 * ((double)acc.x - t0));
         out.y = (float)(-0.5 * ((double)acc.y - t1));

@@ -75,27 +75,14 @@ __global__ void __launch_bounds__(256) k_blk_spmm_fused(
         }
         __syncthreads();
         // 2. rows of Y = -1/2 (S Y2 - 1 t^T): HBM once, shared memory for 3 and 4
-        for (int r = warp * G_ + g; r < kRB; r += 8 * G_) {
+        for (int r = warp * G_ + g; r < kRB; r += 8 * G_) {   // the same trip count for every lane
+            const bool live = r < rows;
+            const int64_t i = r0 + r;
+            const int32_t beg = live ? rp[i] : 0, end = live ? rp[i + 1] : 0;
+            const int maxlen = __reduce_max_sync(0xffffffffu, (unsigned)(end - beg));
+            const float4 acc = blk_row_sum<LPR>(beg, end, maxlen, q, lcol, val, ys4, NV);
             float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (r < rows) {
-                const int64_t i = r0 + r;
-                const int32_t beg = rp[i], end = rp[i + 1];
-                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (int32_t e0 = beg; e0 < end; e0 += LPR) {
-                    const int32_t e = e0 + q;
-                    const int lc_l = (e < end) ? (int)lcol[e] : 0;
-                    const float v_l = (e < end) ? val[e] : 0.f;
-#pragma unroll
-                    for (int tq = 0; tq < LPR; ++tq) {
-                        const int lc = __shfl_sync(gmask, lc_l, tq, LPR);
-                        const float v = __shfl_sync(gmask, v_l, tq, LPR);
-                        const float4 y = ys4[lc * NV + q];
-                        acc.x = fmaf(v, y.x, acc.x);
-                        acc.y = fmaf(v, y.y, acc.y);
-                        acc.z = fmaf(v, y.z, acc.z);
-                        acc.w = fmaf(v, y.w, acc.w);
-                    }
-                }
+            if (live) {
                 out.x = (float)(-0.5 * ((double)acc.x - t0));
                 out.y = (float)(-0.5 * ((double)acc.y - t1));
                 out.z = (float)(-0.5 * ((double)acc.z - t2));
