@@ -1124,6 +1124,19 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     h->n = n;
     h->l = l;
     h->nnz = nnz;
+    cudaStream_t dside = nullptr;      // host-D upload stream (see below)
+    cudaEvent_t dside_done = nullptr;
+    auto join_dside = [&]() {          // wait for and release it (idempotent; also on errors)
+        if (dside) {
+            cudaStreamSynchronize(dside);
+            cudaStreamDestroy(dside);
+            dside = nullptr;
+        }
+        if (dside_done) {
+            cudaEventDestroy(dside_done);
+            dside_done = nullptr;
+        }
+    };
     try {
         CK(cudaGetDevice(&h->dev));
         CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->dev));
@@ -1146,6 +1159,38 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         h->counters.ensure(kCounters * sizeof(unsigned int));
         CK(cudaMemsetAsync(h->counters.p, 0, h->counters.bytes, st));
 
+        // A host D (the bulk of create's input) starts crossing the host link on an internal
+        // stream now, so the transfer overlaps C1/C2's kernels on `st`; `st` joins it below.
+        const bool d_dev = is_device_ptr(D_ll);
+        h->ldD = (l + 3) / 4 * 4;
+        if (!d_dev) {
+            h->Dbuf.ensure((size_t)l * h->ldD * sizeof(float));
+            CK(cudaStreamCreateWithFlags(&dside, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&dside_done, cudaEventDisableTiming));
+            CK(cudaEventRecord(dside_done, st));   // the device buffers above are ready
+            CK(cudaStreamWaitEvent(dside, dside_done, 0));
+            if (!(flags & SBMDS_VALIDATE)) {
+                // only the block upper triangle crosses the host link (D is symmetric, R12; the
+                // default D stream reads only these tiles): row strip I from column 128 I on;
+                // the lower part is mirrored on the device if a full-D path is ever used
+                for (int64_t r0 = 0; r0 < l; r0 += 128) {
+                    const int64_t rows = std::min<int64_t>(128, l - r0);
+                    CK(cudaMemcpy2DAsync(h->Dbuf.as<float>() + r0 * h->ldD + r0, h->ldD * sizeof(float),
+                                         D_ll + r0 * l + r0, l * sizeof(float), (size_t)(l - r0) * sizeof(float),
+                                         (size_t)rows, cudaMemcpyHostToDevice, dside));
+                    h->h2d_bytes += rows * (l - r0) * (int64_t)sizeof(float);
+                }
+                h->d_lower_missing = true;
+            } else {
+                CK(cudaMemcpy2DAsync(h->Dbuf.p, h->ldD * sizeof(float), D_ll, l * sizeof(float), l * sizeof(float), l,
+                                     cudaMemcpyHostToDevice, dside));
+                h->h2d_bytes += l * l * (int64_t)sizeof(float);
+            }
+            CK(cudaEventRecord(dside_done, dside));
+            h->D = h->Dbuf.as<float>();
+            h->own_D = true;
+        }
+
         // ---- C1: upload (or borrow) S, check structure
         DevBuf rp64, tmpA, tmpB, tmpC, flags_d;
         rp64.ensure((n + 1) * sizeof(int64_t));
@@ -1164,7 +1209,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         CK(cudaStreamSynchronize(st));
         rp64.release();
         if (hbad) {
-            destroy_ctx(h);
+            join_dside(); destroy_ctx(h);
             return fail(SBMDS_EINVAL, "row_ptr must start at 0, be nondecreasing and end at nnz");
         }
 
@@ -1176,7 +1221,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             if (hbad) {
-                destroy_ctx(h);
+                join_dside(); destroy_ctx(h);
                 return fail(SBMDS_EINVAL, "col_idx out of [0, l) or non-finite val");
             }
             tmpB.ensure(2 * (size_t)nnz * sizeof(int32_t));  // iota | sorted perm
@@ -1242,32 +1287,17 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         tmpB.release();
         tmpC.release();
 
-        // ---- D_ll: borrow (device, l % 4 == 0) or copy into a 16-byte-pitched buffer
-        const bool d_dev = is_device_ptr(D_ll);
-        h->ldD = (l + 3) / 4 * 4;
-        if ((flags & SBMDS_BORROW_D) && d_dev && h->ldD == l && (reinterpret_cast<uintptr_t>(D_ll) & 15) == 0) {
+        // ---- D_ll: borrow (device, l % 4 == 0), copy a device D into a 16-byte-pitched buffer, or
+        // join the host upload started above
+        if (!d_dev) {
+            CK(cudaStreamWaitEvent(st, dside_done, 0));
+        } else if ((flags & SBMDS_BORROW_D) && h->ldD == l && (reinterpret_cast<uintptr_t>(D_ll) & 15) == 0) {
             h->D = const_cast<float*>(D_ll);
             h->d_borrowed = true;
         } else {
             h->Dbuf.ensure((size_t)l * h->ldD * sizeof(float));
-            if (!d_dev && !(flags & SBMDS_VALIDATE)) {
-                // host D: only the block upper triangle crosses the host link (D is symmetric,
-                // R12; the default D stream reads only these tiles). Row strip I (rows 128I ..)
-                // from column 128I on; the lower part is mirrored on the device if a full-D
-                // path is ever used (ensure_full_d).
-                for (int64_t r0 = 0; r0 < l; r0 += 128) {
-                    const int64_t rows = std::min<int64_t>(128, l - r0);
-                    CK(cudaMemcpy2DAsync(h->Dbuf.as<float>() + r0 * h->ldD + r0, h->ldD * sizeof(float),
-                                         D_ll + r0 * l + r0, l * sizeof(float), (size_t)(l - r0) * sizeof(float),
-                                         (size_t)rows, cudaMemcpyHostToDevice, st));
-                    h->h2d_bytes += rows * (l - r0) * (int64_t)sizeof(float);
-                }
-                h->d_lower_missing = true;
-            } else {
-                CK(cudaMemcpy2DAsync(h->Dbuf.p, h->ldD * sizeof(float), D_ll, l * sizeof(float), l * sizeof(float), l,
-                                     cudaMemcpyDefault, st));
-                if (!d_dev) h->h2d_bytes += l * l * (int64_t)sizeof(float);
-            }
+            CK(cudaMemcpy2DAsync(h->Dbuf.p, h->ldD * sizeof(float), D_ll, l * sizeof(float), l * sizeof(float), l,
+                                 cudaMemcpyDeviceToDevice, st));
             h->D = h->Dbuf.as<float>();
             h->own_D = true;
         }
@@ -1286,17 +1316,18 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             memcpy(&mdiff, &hv[0], 4);
             memcpy(&mabs, &hv[1], 4);
             if (hv[2]) {
-                destroy_ctx(h);
+                join_dside(); destroy_ctx(h);
                 return fail(SBMDS_EINVAL, "D_ll has non-finite entries");
             }
             if (mdiff > 1e-6f * mabs) {
-                destroy_ctx(h);
+                join_dside(); destroy_ctx(h);
                 return fail(SBMDS_EINVAL, "D_ll not symmetric: max|D-D^T| = %g, max|D| = %g", mdiff, mabs);
             }
         }
         CK(cudaStreamSynchronize(st));
+        join_dside();
     } catch (const CudaError& e) {
-        destroy_ctx(h);
+        join_dside(); destroy_ctx(h);
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
         return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
     }
