@@ -370,7 +370,6 @@ __global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const doub
     double (*V)[kMaxB + 1] = reinterpret_cast<double (*)[kMaxB + 1]>(rr_smem + kMaxB * (kMaxB + 1));
     __shared__ double cs[kMaxB / 2 + 1], sn[kMaxB / 2 + 1];
     __shared__ int pp[kMaxB / 2 + 1], qq[kMaxB / 2 + 1];
-    __shared__ int perm[kMaxB + 1];
     __shared__ double offn, nrm;
     __shared__ int order[kMaxB];
     const int tid = threadIdx.x;
@@ -404,26 +403,51 @@ __global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const doub
             V[i][j] = (i == j) ? 1.0 : 0.0;
         }
     }
-    if (tid < be) perm[tid] = tid;
     __syncthreads();
+    __shared__ double red_o[8], red_f[8];
     int sweep = 0;
     for (; sweep < 40; ++sweep) {
-        if (tid == 0) {
+        {   // off-diagonal and total squared norms: every thread, then fixed-order warp / block sums
             double o = 0.0, f = 0.0;
-            for (int i = 0; i < b; ++i)
-                for (int j = 0; j < b; ++j) {
-                    const double v = A[i][j] * A[i][j];
-                    f += v;
-                    if (i != j) o += v;
+            for (int e = tid; e < b * b; e += blockDim.x) {
+                const int i = e / b, j = e % b;
+                const double v = A[i][j] * A[i][j];
+                f += v;
+                if (i != j) o += v;
+            }
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) {
+                o += __shfl_xor_sync(0xffffffffu, o, w);
+                f += __shfl_xor_sync(0xffffffffu, f, w);
+            }
+            if ((tid & 31) == 0) {
+                red_o[tid >> 5] = o;
+                red_f[tid >> 5] = f;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double so = 0.0, sf = 0.0;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                    so += red_o[w];
+                    sf += red_f[w];
                 }
-            offn = o;
-            nrm = f;
+                offn = so;
+                nrm = sf;
+            }
+            __syncthreads();
         }
-        __syncthreads();
         if (!(offn > 1e-30 * nrm) || nrm == 0.0) break;
         for (int round = 0; round < be - 1; ++round) {
             if (tid < np) {
-                int p = perm[tid], q = perm[be - 1 - tid];
+                // round-robin tournament in closed form: player be-1 is fixed, the others rotate
+                int p, q;
+                if (tid == 0) {
+                    p = round;
+                    q = be - 1;
+                } else {
+                    p = (round + tid) % (be - 1);
+                    q = (round - tid + be - 1) % (be - 1);
+                }
                 if (p > q) { const int t = p; p = q; q = t; }
                 pp[tid] = p;
                 qq[tid] = q;
@@ -466,13 +490,6 @@ __global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const doub
                     V[k][p] = c * vp - s * vq;
                     V[k][q] = s * vp + c * vq;
                 }
-            }
-            __syncthreads();
-            // rotate the tournament: position 0 fixed, others shift by one
-            if (tid == 0) {
-                const int last = perm[be - 1];
-                for (int i = be - 1; i > 1; --i) perm[i] = perm[i - 1];
-                perm[1] = last;
             }
             __syncthreads();
         }
