@@ -314,7 +314,9 @@ struct sbmds_ctx {
     DevBuf X, Y, gpart, G, H, Rinv, status, rr, vtmp, ztmp, sign, apval, apidx, xhost, yhost, vsel;
     // options / stats
     int rr_period = 5;
-    int use_graph = 0;
+    int use_graph = 0;   // CUDA-graph replay of eigs segments (measured: no gain)
+    cudaStream_t gstream = nullptr;   // graph capture / replay stream (the caller's may be legacy 0)
+    cudaEvent_t gev[2] = {nullptr, nullptr};
     int order_columns = 1;
     int dstream = 0;
     double rowsum_dev = 0.0;
@@ -879,13 +881,17 @@ template <int LPR>
 void launch_fused(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st) {
     const bool with_h = Yprev != nullptr;
     const size_t smem = fused_smem_bytes(h->umax, b, with_h);
+    // attribute and occupancy per (variant, smem), queried once: never inside a graph capture
     static int occ[2][5] = {};
+    static size_t occ_smem[2][5] = {};
     const int li = LPR == 1 ? 0 : (LPR == 2 ? 1 : (LPR == 4 ? 2 : 3));
     auto kern = with_h ? k_blk_spmm_fused<LPR, true> : k_blk_spmm_fused<LPR, false>;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-    occ[with_h][li] = per_sm;
+    if (occ_smem[with_h][li] != smem) {
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[with_h][li], kern, 256, smem));
+        occ_smem[with_h][li] = smem;
+    }
+    const int per_sm = occ[with_h][li];
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nblk, (int64_t)std::max(1, per_sm) * h->num_sms));
     h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
     h->P1.ensure((size_t)std::max<int32_t>(1, h->total_u) * kMaxB * sizeof(float));
@@ -1102,6 +1108,16 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
 
 void destroy_ctx(sbmds_ctx* h) {
     if (!h) return;
+    if (h->gstream) {
+        cudaStreamSynchronize(h->gstream);
+        cudaStreamDestroy(h->gstream);
+        h->gstream = nullptr;
+    }
+    for (auto& e : h->gev)
+        if (e) {
+            cudaEventDestroy(e);
+            e = nullptr;
+        }
     for_each_buf(h, [](DevBuf* b) { b->release(); });
     cudaStreamSynchronize(0);
     delete h;
@@ -1512,14 +1528,14 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         int it = 0;
         bool converged = false;
         const bool fused = fused_ok(h, b) && blocked_ok(h, b, b, Yc, Yn);
-        for (it = 1; it <= max_iters; ++it) {
-            const bool do_rr = (it % h->rr_period == 0) || it == max_iters;
-            // Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1};  s = 1^T Y_k came from the last Gram
+        // one iteration's device work: Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1} (s = 1^T Y_k came from
+        // the last Gram), the Grams, and at Rayleigh-Ritz steps the Jacobi solve (no host syncs)
+        auto enqueue_iteration = [&](int itx, bool do_rr) {
             if (fused) {
                 // A5 fused with G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, H' = Y_k^T Y_{k+1} (RR) and
-                // the next apply's S^T Y_{k+1} partials (k_fused.cuh)
+                // (fuse = 2) the next apply's S^T Y_{k+1} partials (k_fused.cuh)
                 const bool p1 = h->fuse >= 2;
-                const int fl = kApplyFused | (p1 && it > 1 ? kApplyY1Ready : 0) | (!p1 || it == max_iters ? kApplyNoP1 : 0);
+                const int fl = kApplyFused | (p1 && itx > 1 ? kApplyY1Ready : 0) | (!p1 || itx == max_iters ? kApplyNoP1 : 0);
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
             } else {
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>());
@@ -1532,6 +1548,83 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                     launch(k_rr, dim3(1), dim3(256), (size_t)kRrSmem, st, b, m, tol, (const double*)h->H.as<double>(),
                            (const double*)h->G.as<double>(), (const double*)h->Rinv.as<double>(), h->rr.as<RrOut>());
                 });
+            }
+        };
+        // CUDA graphs (option use_graph): after the first Rayleigh-Ritz segment
+        // (which also warms every buffer and tensor map), a segment of rr_period iterations -- the
+        // first rr_period - 1 with their Cholesky-QR, the last ending with the Jacobi solve -- is
+        // captured once per buffer parity and replayed; the host only reads the convergence flag
+        // between segments, exactly where the eager loop reads it. Off while kernels are profiled.
+        const int R = std::max(1, h->rr_period);
+        const bool graphs = h->use_graph && h->prof.mask == 0 && !(fused && h->fuse >= 2) && R >= 2;
+        cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+        int64_t gnodes[2] = {0, 0};
+        struct GraphGuard {
+            cudaGraphExec_t* g;
+            ~GraphGuard() {
+                for (int k = 0; k < 2; ++k)
+                    if (g[k]) cudaGraphExecDestroy(g[k]);
+            }
+        } graph_guard{gexec};
+        it = 1;
+        while (it <= max_iters) {
+            const bool seg = graphs && it > R && (it - 1) % R == 0 && it + R - 1 <= max_iters;
+            bool do_rr;
+            if (seg) {
+                const int par = (Yc == h->X.as<float>()) ? 0 : 1;
+                if (!h->gstream) {
+                    CK(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+                    CK(cudaEventCreateWithFlags(&h->gev[0], cudaEventDisableTiming));
+                    CK(cudaEventCreateWithFlags(&h->gev[1], cudaEventDisableTiming));
+                }
+                cudaStream_t const st_caller = st;
+                if (!gexec[par]) {
+                    float* const Yc0 = Yc;
+                    float* const Yn0 = Yn;
+                    st = h->gstream;   // the lambdas enqueue on `st`
+                    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                    const int64_t n0 = g_launches.load();
+                    try {
+                        for (int k = 0; k < R; ++k) {
+                            enqueue_iteration(it + k, k == R - 1);
+                            if (k < R - 1) {
+                                chol(h, b, st);
+                                std::swap(Yc, Yn);
+                            }
+                        }
+                    } catch (...) {   // end (and drop) the capture, restore the caller's stream
+                        cudaGraph_t gbad = nullptr;
+                        cudaStreamEndCapture(h->gstream, &gbad);
+                        if (gbad) cudaGraphDestroy(gbad);
+                        st = st_caller;
+                        throw;
+                    }
+                    cudaGraph_t g = nullptr;
+                    CK(cudaStreamEndCapture(st, &g));
+                    const cudaError_t ie = cudaGraphInstantiate(&gexec[par], g, 0);
+                    cudaGraphDestroy(g);
+                    CK(ie);
+                    gnodes[par] = g_launches.load() - n0;   // captured, not yet run
+                    g_launches.fetch_sub(gnodes[par]);
+                    Yc = Yc0;
+                    Yn = Yn0;
+                    st = st_caller;
+                }
+                // replay on the graph stream, ordered after and before the caller's stream work
+                CK(cudaEventRecord(h->gev[0], st));
+                CK(cudaStreamWaitEvent(h->gstream, h->gev[0], 0));
+                CK(cudaGraphLaunch(gexec[par], h->gstream));
+                CK(cudaEventRecord(h->gev[1], h->gstream));
+                CK(cudaStreamWaitEvent(st, h->gev[1], 0));
+                g_launches.fetch_add(gnodes[par]);
+                for (int k = 0; k < R - 1; ++k) std::swap(Yc, Yn);
+                it += R - 1;   // the segment's Rayleigh-Ritz iteration
+                do_rr = true;
+            } else {
+                do_rr = (it % R == 0) || it == max_iters;
+                enqueue_iteration(it, do_rr);
+            }
+            if (do_rr) {
                 int conv = 0;
                 CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
@@ -1547,6 +1640,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                 CK(cudaStreamSynchronize(st));
                 if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR broke down at iteration %d", it);
             }
+            ++it;
         }
         if (it > max_iters) it = max_iters;
         CK(cudaMemcpyAsync(&rr_host, h->rr.p, sizeof(RrOut), cudaMemcpyDeviceToHost, st));

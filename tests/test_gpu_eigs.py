@@ -172,3 +172,23 @@ def test_fused_sparse_step_matches_unfused(cfg, block):
     assert O.principal_angle(Va, Vb) <= 1e-4
     assert abs(ia["max_residual"] - ib["max_residual"]) <= 1e-4 * max(1.0, abs(ib["max_residual"])) + 1e-9
     assert np.array_equal(la, rep[0]) and np.array_equal(Va, rep[1])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_graph_replay_matches_eager(cfg):
+    """The eigs loop replayed from CUDA graphs (option use_graph) and launched eagerly compute
+    the same iteration bitwise: graph capture changes how kernels are launched, not what runs."""
+    p = configs.config(cfg)
+    m, block = p.m, p.block
+    iters = 23 if cfg != 4 else 12
+    with handle(p) as h:
+        out = {}
+        for g in (1, 0):
+            h.set_option("use_graph", g)
+            out[g] = gpu_eigs(h, m, block, max_iters=iters, tol=0.0, seed=5)
+        h.set_option("use_graph", 1)
+        conv = gpu_eigs(h, m, block, max_iters=500, tol=1e-6, seed=5)
+        h.set_option("use_graph", 0)
+    assert np.array_equal(out[1][0], out[0][0]) and np.array_equal(out[1][1], out[0][1])
+    assert out[1][3]["iters"] == out[0][3]["iters"] == iters
+    assert conv[3]["converged"] == 1
