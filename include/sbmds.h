@@ -139,6 +139,13 @@ const char* sbmds_last_error(void);
  *                      (k_dstream_pair, 2xFP16; b in 5..32, else as 2)
  *     "blocked"        bit mask: 1 = S Y2 through the row-blocked kernel, 2 = S^T X too
  *     "gram_tc"        (0/1) Gram on the FP64 tensor cores (b <= 32)
+ *     "center"         (0/1, default 1) 0: sbmds_apply returns the uncentred E^ X = S D S^T X
+ *                      (the BHA approximation of the squared-distance matrix;
+ *                      its rows are what the error estimate of PAPER.md:309/317 compares);
+ *                      sbmds_eigs always uses the centred operator
+ *     "fuse"           eigs: 0 separate kernels, 1 (default) A5 fused with the Gram,
+ *                      2 also the next apply's S^T partials
+ *     "use_graph"      (0/1, default 0) eigs: replay Rayleigh-Ritz segments from CUDA graphs
  *     "profile"        bit mask of kernel families timed with CUDA events on the launching
  *                      stream (bit k = family k of: colsum csc dstream dreduce csr gram chol
  *                      rotate rr split); "profile_reset" (any value) zeroes the counters

@@ -93,6 +93,29 @@ def apply(S, D, X) -> np.ndarray:
     return Y[:, 0] if vec else Y
 
 
+def apply_raw(S, D, X) -> np.ndarray:
+    """E^ X = S D S^T X (no centring, no -1/2), right to left, fp64.
+
+    PAPER.md:152-156: K_BHA = P W P^T, "two interpolation operations"; with W = D_ll of squared
+    distances (reading R2) this is the approximation E^ of the squared-distance matrix whose
+    rows the paper's error estimate compares with exact rows.
+    """
+    S = sp.csr_matrix(S, dtype=np.float64)
+    X = np.asarray(X, dtype=np.float64)
+    vec = X.ndim == 1
+    if vec:
+        X = X[:, None]
+    Y = np.asarray(S @ _dense_times(D, np.asarray(S.T @ X)))
+    return Y[:, 0] if vec else Y
+
+
+def rel_sq_error(A, B) -> float:
+    """epsilon(A) = ||A - B||_F^2 / ||B||_F^2 (PAPER.md:309), fp64."""
+    A = np.asarray(A, dtype=np.float64)
+    B = np.asarray(B, dtype=np.float64)
+    return float(np.sum((A - B) ** 2) / np.sum(B ** 2))
+
+
 # ----------------------------------------------------------------------------- MDS
 def embedding(V: np.ndarray, lam: np.ndarray) -> np.ndarray:
     """Z = V_m Λ_m^{1/2}; a negative λ gets a zero column."""

@@ -314,6 +314,9 @@ struct sbmds_ctx {
     DevBuf X, Y, gpart, G, H, Rinv, status, rr, vtmp, ztmp, sign, apval, apidx, xhost, yhost, vsel;
     // options / stats
     int rr_period = 5;
+    int center = 1;          // 0: sbmds_apply computes the uncentred S D S^T X
+    bool raw_now = false;
+    DevBuf w0, rawR;         // zeros(l); -2 I (b x b) folded into Y1 for the uncentred apply
     int use_graph = 0;   // CUDA-graph replay of eigs segments (measured: no gain)
     cudaStream_t gstream = nullptr;   // graph capture / replay stream (the caller's may be legacy 0)
     cudaEvent_t gev[2] = {nullptr, nullptr};
@@ -363,6 +366,9 @@ void encode_dmap(sbmds_ctx* h) {
     h->dmap_ok[i] = true;
 }
 
+// the w of the rank-one centring terms: zeros while an uncentred apply runs (center = 0)
+const double* wvec(const sbmds_ctx* h) { return h->raw_now ? h->w0.as<double>() : h->w.as<double>(); }
+
 constexpr size_t kBlkSmem = 96 * 1024;   // shared-memory budget of one staged dictionary
 
 bool blocked_ok(const sbmds_ctx* h, int b, int bp, const void* X, const void* Y) {
@@ -398,7 +404,7 @@ void run_dstream(sbmds_ctx* h, int b, cudaStream_t st) {
     const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     profiled(h->prof, PK_DREDUCE, st, [&] {
         launch(k_dreduce, dim3(grid), dim3(256), 0, st, h->l, BP, b, C::TM, sk, maxseg,
-               (const double*)h->P.as<double>(), (const double*)h->w.as<double>(), h->Y2.as<float>(),
+               (const double*)h->P.as<double>(), wvec(h), h->Y2.as<float>(),
                h->tpart.as<double>(), h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
     });
 }
@@ -465,7 +471,7 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
     const int grid = (int)std::min<int64_t>(kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     profiled(h->prof, PK_DREDUCE, st, [&] {
         launch(k_dreduce, dim3(grid), dim3(256), 0, st, h->l, BP, b, C::TM, sk, maxseg,
-               (const double*)h->P.as<double>(), (const double*)h->w.as<double>(), h->Y2.as<float>(),
+               (const double*)h->P.as<double>(), wvec(h), h->Y2.as<float>(),
                h->tpart.as<double>(), h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
     });
 }
@@ -641,7 +647,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_DREDUCE, st, [&] {
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const int*)dexp,
-               (const int*)yexp, (const double*)h->w.as<double>(), h->Y2.as<float>(), h->tpart.as<double>(),
+               (const int*)yexp, wvec(h), h->Y2.as<float>(), h->tpart.as<double>(),
                h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
     });
     h->last_dpath = 4;
@@ -703,7 +709,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_DREDUCE, st, [&] {
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)nullptr, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
-               (const double*)h->w.as<double>(), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
+               wvec(h), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
                h->counters.as<unsigned int>() + CNT_DRED);
     });
     h->last_dpath = 3;
@@ -774,7 +780,7 @@ void spmm_csc(sbmds_ctx* h, int b, int bp, const float* X, cudaStream_t st) {
     const bool vec = (b == bp) && (b % 4 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     auto args = std::make_tuple(h->l, b, bp, (const int32_t*)h->cptr.as<int32_t>(),
                                 (const int32_t*)h->ridx.as<int32_t>(), (const float*)h->cval.as<float>(), ord, X,
-                                (const double*)h->w.as<double>(), (const double*)h->s.as<double>(),
+                                wvec(h), (const double*)h->s.as<double>(),
                                 h->Y1.as<float>());
     auto go = [&](auto kern) {
         std::apply([&](auto... a) { launch(kern, dim3(grid), dim3(256), 0, st, a...); }, args);
@@ -933,7 +939,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         auto go_r = [&](auto kern) {
             launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
                    (const int32_t*)h->bjptr.as<int32_t>(), (const int32_t*)h->bjlist.as<int32_t>(),
-                   (const float*)h->P1.as<float>(), (const double*)h->w.as<double>(), (const double*)h->s.as<double>(),
+                   (const float*)h->P1.as<float>(), wvec(h), (const double*)h->s.as<double>(),
                    h->Y1.as<float>());
         };
         profiled(h->prof, PK_CSC, st, [&] {
@@ -955,7 +961,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         auto go_r = [&](auto kern) {
             launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
                    (const int32_t*)h->bjptr.as<int32_t>(), (const int32_t*)h->bjlist.as<int32_t>(),
-                   (const float*)h->P1.as<float>(), (const double*)h->w.as<double>(), (const double*)h->s.as<double>(),
+                   (const float*)h->P1.as<float>(), wvec(h), (const double*)h->s.as<double>(),
                    h->Y1.as<float>());
         };
         profiled(h->prof, PK_CSC, st, [&] {
@@ -1096,7 +1102,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
@@ -1390,7 +1396,28 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
             h->yhost.ensure(bytes);
             Yd = h->yhost.as<float>();
         }
-        apply_device(h, b, Xd, Yd, st);
+        if (h->center) {
+            apply_device(h, b, Xd, Yd, st);
+        } else {
+            // uncentred E^ X = S D S^T X: the centred machinery with s = 0 and w = 0 (both rank-one
+            // terms vanish) and R^-1 = -2 I folded into Y1 (cancels the -1/2; exact)
+            h->w0.ensure((size_t)h->l * sizeof(double));
+            h->rawR.ensure((size_t)kMaxB * kMaxB * sizeof(double));
+            std::vector<double> m2((size_t)b * b, 0.0);
+            for (int c = 0; c < b; ++c) m2[(size_t)c * b + c] = -2.0;
+            CK(cudaMemsetAsync(h->w0.p, 0, (size_t)h->l * sizeof(double), st));
+            CK(cudaMemcpyAsync(h->rawR.p, m2.data(), m2.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+            CK(cudaMemsetAsync(h->s.p, 0, kMaxB * sizeof(double), st));
+            h->raw_now = true;
+            try {
+                apply_device(h, b, Xd, Yd, st, true, h->rawR.as<double>());
+            } catch (...) {
+                h->raw_now = false;
+                throw;
+            }
+            h->raw_now = false;
+            CK(cudaStreamSynchronize(st));   // m2 (host) must outlive its copy
+        }
         if (!yd) CK(cudaMemcpyAsync(Y, Yd, bytes, cudaMemcpyDeviceToHost, st));
         if (!xd || !yd) CK(cudaStreamSynchronize(st));
     } catch (const CudaError& e) {
@@ -1755,6 +1782,8 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         if (value < 0 || value > 4)
             return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric int8, 4 symmetric 2xfp16 pairs}");
         h->dstream = (int)value;
+    } else if (!strcmp(key, "center")) {
+        h->center = value ? 1 : 0;
     } else if (!strcmp(key, "csr_sub_L")) {
         if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16 || value == 32))
             return fail(SBMDS_EINVAL, "csr_sub_L in {0 auto, 1, 2, 4, 8, 16, 32}");

@@ -334,3 +334,22 @@ def test_symmetric_half_small_l(l, b):
         assert np.abs(Y).max() <= 1e-6 * max(1.0, np.abs(X).max())
     else:
         assert relerr(Y, ref) <= TOL
+
+
+@pytest.mark.parametrize("dstream", [0, 1, 2, 3])
+@pytest.mark.parametrize("b", [1, 4, 12, 16, 64])
+def test_uncentred_apply(dstream, b):
+    """center = 0: sbmds_apply returns E^ X = S D S^T X (the paper's error
+    workload, :317) on every D-stream path, to the same bar as the centred apply."""
+    p = configs.random_problem(30_011, 2_003, 16, seed=b + 7, name="cfg5_small")
+    X = configs.x_block(p.n, b, seed=b + 1)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    ref = O.apply_raw(S, p.D, X.astype(np.float64))
+    with make_handle(p) as h:
+        h.set_option("center", 0)
+        h.set_option("dstream", dstream)
+        Y = run_apply(h, X)
+        h.set_option("center", 1)
+        Yc = run_apply(h, X)
+    assert relerr(Y, ref) <= TOL
+    assert relerr(Yc, oracle_apply(p, X)) <= TOL   # the centred apply is untouched afterwards

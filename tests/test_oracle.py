@@ -259,3 +259,30 @@ def test_mutations_are_caught():
     assert np.linalg.norm(good - ref) < 1e-10 * np.linalg.norm(ref)
     for name, Ym in muts.items():
         assert np.linalg.norm(Ym - ref) > 1e-3 * np.linalg.norm(ref), name
+
+
+def test_apply_raw_pins():
+    """apply_raw (E^ X = S D S^T X) is pinned three ways: S = I gives D X
+    (closed form); columns of E^ e_j equal the dense product S D S^T built entry by entry on a
+    tiny case (brute force); and -1/2 J (apply_raw) J equals the centred apply (pinned above)."""
+    rng = np.random.default_rng(3)
+    l = 7
+    A = rng.uniform(0, 10, (l, l))
+    D = (A + A.T) / 2
+    X = rng.standard_normal((l, 3))
+    assert np.allclose(O.apply_raw(sp.identity(l, format="csr"), D, X), D @ X)
+    n = 11
+    Sd = np.zeros((n, l))
+    for i in range(n):
+        cols = rng.choice(l, 3, replace=False)
+        Sd[i, cols] = rng.uniform(-1, 1, 3)
+    S = sp.csr_matrix(Sd)
+    E = np.zeros((n, n))
+    for i in range(n):
+        for j in range(n):
+            E[i, j] = sum(Sd[i, a] * D[a, c] * Sd[j, c] for a in range(l) for c in range(l))
+    Xn = rng.standard_normal((n, 2))
+    assert np.allclose(O.apply_raw(S, D, Xn), E @ Xn)
+    J = np.eye(n) - np.ones((n, n)) / n
+    assert np.allclose(-0.5 * J @ O.apply_raw(S, D, J @ Xn), O.apply(S, D, Xn))
+    assert O.rel_sq_error(E, E) == 0.0 and abs(O.rel_sq_error(2 * E, E) - 1.0) < 1e-12
