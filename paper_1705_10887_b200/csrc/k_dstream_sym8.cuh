@@ -109,7 +109,8 @@ template <int BP>
 __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
     k_dstream_sym8(const int8_t* __restrict__ Dt, const __grid_constant__ CUtensorMap bmap,
                    const uint32_t* __restrict__ tiles, const int64_t* __restrict__ cbeg,
-                   const int* __restrict__ sbase, const int* __restrict__ smap, int NT, float* __restrict__ P) {
+                   const int* __restrict__ sbase, const int* __restrict__ smap, int NT, float* __restrict__ P,
+                   int dbg_mode) {
     using C = Sym8Cfg<BP>;
     constexpr int S = C::S;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
             if (elect_one()) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {   // K = 32 per MMA
+                    if (dbg_mode & 1) break;     // diagnostics: stream only
                     // N: A = plane p, K-major (k = column j: 32 bytes per step inside the 128-byte rows)
                     const uint64_t bj0 = umma_desc_sw128(sbN + 32 * j, 16, 1024);
                     tc_mma_i8(dN, umma_desc_sw128(sa + 32 * j, 16, 1024), bj0, id1n, (firstN && j == 0) ? 0u : 1u);

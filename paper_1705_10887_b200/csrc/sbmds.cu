@@ -701,7 +701,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_DSTREAM, st, [&] {
         launch(k_dstream_sym8<BP>, dim3(pl.P), dim3(C::THREADS), (size_t)C::SMEM, st, (const int8_t*)h->Dt8.p,
                pl.bmap16, (const uint32_t*)pl.tiles.p, (const int64_t*)pl.pbeg.p, (const int*)pl.sbase.p,
-               (const int*)pl.smap.p, (int)pl.NT, h->P.as<float>());
+               (const int*)pl.smap.p, (int)pl.NT, h->P.as<float>(), h->pair_dbg >> 1);
     });
     const int rows_per_blk = 256 / BP;
     const int grid = (int)std::min<int64_t>(4 * kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);

@@ -11,7 +11,7 @@ modes = [int(m) for m in sys.argv[3:]] or [0, 1, 2, 4, 8, 5, 7]
 p = configs.config(cfg)
 out = {}
 with from_problem(p) as h:
-    h.set_option("dstream", 3)
+    h.set_option("dstream", int(os.environ.get("DS", "3")))
     X = torch.randn((p.n, b), device="cuda")
     Y = torch.empty_like(X)
     for _ in range(3):
