@@ -183,12 +183,17 @@ __global__ void __launch_bounds__(256) k_spmm_csc_vec4(
     const int64_t j = order ? order[wid] : wid;
     const int32_t beg = col_ptr[j], end = col_ptr[j + 1];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    // software-pipelined: the next 32 (row, value) pairs load while this chunk's gathers run
+    int32_t r_n = beg + lane < end ? row_idx[beg + lane] : 0;
+    float v_n = beg + lane < end ? cval[beg + lane] : 0.f;
     for (int32_t base = beg; base < end; base += 32) {
-        const int32_t e = base + lane;
-        const int32_t r_l = e < end ? row_idx[e] : 0;
-        const float v_l = e < end ? cval[e] : 0.f;
+        const int32_t r_l = r_n;
+        const float v_l = v_n;
+        const int32_t en = base + 32 + lane;
+        r_n = en < end ? row_idx[en] : 0;
+        v_n = en < end ? cval[en] : 0.f;
         const int cnt = min(32, end - base);
-#pragma unroll 4
+#pragma unroll
         for (int tq = g; tq < 32; tq += G) {
             const int32_t r = __shfl_sync(0xffffffffu, r_l, tq);
             const float v = __shfl_sync(0xffffffffu, v_l, tq);
@@ -236,10 +241,14 @@ __global__ void __launch_bounds__(256) k_spmm_csc_gen(
     float acc[NC];
 #pragma unroll
     for (int u = 0; u < NC; ++u) acc[u] = 0.f;
+    int32_t r_n = beg + lane < end ? row_idx[beg + lane] : 0;   // software-pipelined (as vec4)
+    float v_n = beg + lane < end ? cval[beg + lane] : 0.f;
     for (int32_t base = beg; base < end; base += 32) {
-        const int32_t e = base + lane;
-        const int32_t r_l = e < end ? row_idx[e] : 0;
-        const float v_l = e < end ? cval[e] : 0.f;
+        const int32_t r_l = r_n;
+        const float v_l = v_n;
+        const int32_t en = base + 32 + lane;
+        r_n = en < end ? row_idx[en] : 0;
+        v_n = en < end ? cval[en] : 0.f;
         const int cnt = min(32, end - base);
 #pragma unroll 4
         for (int tq = g; tq < 32; tq += G) {
