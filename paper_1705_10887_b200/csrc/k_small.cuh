@@ -358,6 +358,41 @@ struct RrOut {
     int sweeps;
 };
 
+// E6 selection (one block): the top-m algebraic Ritz pairs with the exact null pair (0, 1/sqrt(n))
+// merged in (it enters when fewer than m Ritz values are >= 0; reading R10), the R^-1 fold of
+// the Ritz vectors V = Y_k (R_k^{-1} U) as the b x m selection matrix Msel, the added constant
+// column addc (1/sqrt(n) for the null pair) and the selected eigenvalues theta_out.
+__global__ void __launch_bounds__(256) k_select(int b, int m, int64_t n, const RrOut* __restrict__ rr,
+                                                const double* __restrict__ Rinv, double* __restrict__ Msel,
+                                                double* __restrict__ addc, double* __restrict__ theta_out) {
+    __shared__ int src[kMaxB];
+    if (threadIdx.x == 0) {
+        int r = 0;
+        bool zero_used = false;
+        for (int j = 0; j < m; ++j) {
+            if (!zero_used && (r >= b || rr->theta[r] < 0.0)) {
+                zero_used = true;
+                src[j] = -1;
+            } else {
+                src[j] = r++;
+            }
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < b * m; e += blockDim.x) {
+        const int p = e / m, j = e % m;
+        double acc = 0.0;
+        if (src[j] >= 0)
+            for (int q = p; q < b; ++q) acc += Rinv[p * b + q] * rr->U[q * b + src[j]];
+        Msel[p * m + j] = acc;
+    }
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        addc[j] = src[j] < 0 ? 1.0 / sqrt((double)n) : 0.0;
+        theta_out[j] = src[j] < 0 ? 0.0 : rr->theta[src[j]];
+    }
+}
+
+
 // Parallel cyclic Jacobi (round-robin pair ordering) on sym(H); residuals from the Gram
 // G = Y^T Y with Y = B~ X: r_j^2 = u_j^T G u_j - θ_j^2 for orthonormal X.
 // With Rinv != null the iterate is X = Y_prev Rinv and Hg holds Y_prev^T (B~X), so

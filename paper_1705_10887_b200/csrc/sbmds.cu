@@ -1674,36 +1674,13 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         CK(cudaStreamSynchronize(st));
         // E6: select the top-m algebraic pairs. B~ 1 = 0 exactly (J 1 = 0), but the iterate
         // lives in 1^perp after the first apply, so the known pair (0, 1/sqrt(n)) is merged
-        // into the Ritz list: it enters the top m when fewer than m Ritz values are >= 0.
-        std::vector<double> Msel((size_t)b * m, 0.0), addc(m, 0.0), theta_out(m, 0.0);
-        std::vector<double> Rinv_h((size_t)b * b);
-        CK(cudaMemcpyAsync(Rinv_h.data(), h->Rinv.p, Rinv_h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        {
-            int r = 0;
-            bool zero_used = false;
-            for (int j = 0; j < m; ++j) {
-                if (!zero_used && (r >= b || rr_host.theta[r] < 0.0)) {
-                    zero_used = true;
-                    addc[j] = 1.0 / std::sqrt((double)n);
-                    theta_out[j] = 0.0;
-                    continue;
-                }
-                // V = X_k U = Y_k (R_k^{-1} U): fold R^{-1} into the selection matrix
-                for (int p = 0; p < b; ++p) {
-                    double acc = 0.0;
-                    for (int q = p; q < b; ++q) acc += Rinv_h[(size_t)p * b + q] * rr_host.U[q * b + r];
-                    Msel[(size_t)p * m + j] = acc;
-                }
-                theta_out[j] = rr_host.theta[r];
-                ++r;
-            }
-        }
+        // into the Ritz list: it enters the top m when fewer than m Ritz values are >= 0 (k_select).
         h->vsel.ensure(((size_t)b * m + 2 * m) * sizeof(double));
         double* Msel_d = h->vsel.as<double>();
-        CK(cudaMemcpyAsync(Msel_d, Msel.data(), Msel.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(Msel_d + (size_t)b * m, addc.data(), m * sizeof(double), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(Msel_d + (size_t)b * m + m, theta_out.data(), m * sizeof(double), cudaMemcpyHostToDevice,
+        launch(k_select, dim3(1), dim3(256), 0, st, b, m, n, (const RrOut*)h->rr.as<RrOut>(),
+               (const double*)h->Rinv.as<double>(), Msel_d, Msel_d + (size_t)b * m, Msel_d + (size_t)b * m + m);
+        std::vector<double> theta_out(m, 0.0);
+        CK(cudaMemcpyAsync(theta_out.data(), Msel_d + (size_t)b * m + m, m * sizeof(double), cudaMemcpyDeviceToHost,
                            st));
         const bool vdev = V && is_device_ptr(V), zdev = Z && is_device_ptr(Z);
         const size_t vbytes = (size_t)n * m * sizeof(float);
