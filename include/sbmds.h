@@ -167,6 +167,13 @@ sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* value);
    each captured kernel). Monotone; for bench.py's gpu_launches. */
 int64_t sbmds_launch_count(void);
 
+/* Diagnostics (host only, no GPU needed): builds the symmetric-half D-stream schedule for l,
+   block edge S (1..16), row-accumulator group gN (>= 1), at most max_ctas CTAs (or CTA pairs),
+   contiguous slot layout (0/1), replays the kernels' accumulate/flush rules against it and
+   returns the number of violated invariants (0 = consistent; < 0 = bad arguments). Used by the
+   CPU tests; see k_dstream_sym8.cuh / k_dstream_pair.cuh and DESIGN.md §4. */
+int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous);
+
 /* ABI version: 1. */
 int32_t sbmds_abi_version(void);
 

@@ -18,7 +18,8 @@ STATUS_NAMES = {0: "SBMDS_OK", 1: "SBMDS_EINVAL", 2: "SBMDS_ENOMEM", 3: "SBMDS_E
 
 # Every symbol include/sbmds.h declares (checked by tests/test_abi.py on CPU).
 EXPORTS = ("sbmds_create", "sbmds_apply", "sbmds_eigs", "sbmds_destroy", "sbmds_last_error",
-           "sbmds_set_option", "sbmds_get_stat", "sbmds_launch_count", "sbmds_abi_version")
+           "sbmds_set_option", "sbmds_get_stat", "sbmds_launch_count", "sbmds_abi_version",
+           "sbmds_plan_selfcheck")
 
 
 class SbmdsInfo(ctypes.Structure):
@@ -65,6 +66,8 @@ def lib() -> ctypes.CDLL:
             L.sbmds_launch_count.restype = i64
             L.sbmds_abi_version.argtypes = []
             L.sbmds_abi_version.restype = i32
+            L.sbmds_plan_selfcheck.argtypes = [i64, i32, i32, i32, i32]
+            L.sbmds_plan_selfcheck.restype = i64
             _lib = L
     return _lib
 

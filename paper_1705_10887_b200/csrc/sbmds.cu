@@ -487,11 +487,20 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
 // block row (their segments end when (bi, bj / gN) changes), the column ("T") ones per block.
 // contiguous: physical slot = rank of (X, logical slot), so each row tile's partials are
 // contiguous for k_dreduce_pair; the kernel maps logical -> physical through pl.smap.
-void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S, int gN = 1, bool contiguous = false) {
-    const int NT = (int)((h->l + 127) / 128);
+struct PlanHost {
+    int S = 0, NT = 0, P = 0;
+    int64_t T = 0;
+    std::vector<uint32_t> tiles;
+    std::vector<int64_t> pbeg;
+    std::vector<int> sbase, slot_x, xptr, xslot, smap;
+};
+
+PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous) {
+    PlanHost ph;
+    const int NT = (int)((l + 127) / 128);
     if (NT > 65535) throw std::runtime_error("l too large for the symmetric-half stream");
     const int NBk = (NT + S - 1) / S;
-    std::vector<uint32_t> tiles;
+    auto& tiles = ph.tiles;
     tiles.reserve((size_t)NT * (NT + 1) / 2);
     for (int bi = 0; bi < NBk; ++bi)
         for (int bj = bi; bj < NBk; ++bj)
@@ -502,9 +511,12 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
                 }
     const int64_t T = (int64_t)tiles.size();
     const int P = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs, T / 8));
-    std::vector<int64_t> pbeg(P + 1);
+    auto& pbeg = ph.pbeg;
+    pbeg.resize(P + 1);
     for (int p = 0; p <= P; ++p) pbeg[p] = (int64_t)p * T / P;
-    std::vector<int> sbase(2 * P), slot_x;
+    auto& sbase = ph.sbase;
+    auto& slot_x = ph.slot_x;
+    sbase.resize(2 * P);
     for (int p = 0; p < P; ++p)
         for (int role = 0; role < 2; ++role) {
             sbase[2 * p + role] = (int)slot_x.size();
@@ -529,7 +541,10 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
             emit();
         }
     const int nslots = (int)slot_x.size();
-    std::vector<int> xptr(NT + 1, 0), xslot(nslots);
+    auto& xptr = ph.xptr;
+    auto& xslot = ph.xslot;
+    xptr.assign(NT + 1, 0);
+    xslot.resize(nslots);
     for (int q = 0; q < nslots; ++q) ++xptr[slot_x[q] + 1];
     for (int X = 0; X < NT; ++X) xptr[X + 1] += xptr[X];
     {
@@ -537,29 +552,146 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
         for (int q = 0; q < nslots; ++q) xslot[fill[slot_x[q]]++] = q;   // ascending slot ids per X
     }
     if (contiguous) {   // smap[logical] = physical (X-major, then logical order); xslot = identity
-        std::vector<int> smap(std::max(1, nslots));
-        for (int pq = 0; pq < nslots; ++pq) smap[xslot[pq]] = pq;
+        ph.smap.assign(std::max(1, nslots), 0);
+        for (int pq = 0; pq < nslots; ++pq) ph.smap[xslot[pq]] = pq;
         for (int pq = 0; pq < nslots; ++pq) xslot[pq] = pq;
-        pl.smap.ensure(smap.size() * sizeof(int));
-        CK(cudaMemcpy(pl.smap.p, smap.data(), smap.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
-    pl.tiles.ensure(tiles.size() * sizeof(uint32_t));
-    pl.pbeg.ensure(pbeg.size() * sizeof(int64_t));
-    pl.sbase.ensure(sbase.size() * sizeof(int));
-    pl.xptr.ensure(xptr.size() * sizeof(int));
-    pl.xslot.ensure(std::max<size_t>(1, xslot.size()) * sizeof(int));
-    CK(cudaMemcpy(pl.tiles.p, tiles.data(), tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(pl.pbeg.p, pbeg.data(), pbeg.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(pl.sbase.p, sbase.data(), sbase.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(pl.xptr.p, xptr.data(), xptr.size() * sizeof(int), cudaMemcpyHostToDevice));
-    if (nslots) CK(cudaMemcpy(pl.xslot.p, xslot.data(), xslot.size() * sizeof(int), cudaMemcpyHostToDevice));
+    ph.S = S;
+    ph.NT = NT;
+    ph.P = P;
+    ph.T = T;
+    return ph;
+}
+
+void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S, int gN = 1, bool contiguous = false) {
+    const PlanHost ph = plan_host(h->l, max_pairs, S, gN, contiguous);
+    const int nslots = (int)ph.slot_x.size();
+    if (contiguous) {
+        pl.smap.ensure(ph.smap.size() * sizeof(int));
+        CK(cudaMemcpy(pl.smap.p, ph.smap.data(), ph.smap.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    pl.tiles.ensure(ph.tiles.size() * sizeof(uint32_t));
+    pl.pbeg.ensure(ph.pbeg.size() * sizeof(int64_t));
+    pl.sbase.ensure(ph.sbase.size() * sizeof(int));
+    pl.xptr.ensure(ph.xptr.size() * sizeof(int));
+    pl.xslot.ensure(std::max<size_t>(1, ph.xslot.size()) * sizeof(int));
+    CK(cudaMemcpy(pl.tiles.p, ph.tiles.data(), ph.tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pl.pbeg.p, ph.pbeg.data(), ph.pbeg.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pl.sbase.p, ph.sbase.data(), ph.sbase.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pl.xptr.p, ph.xptr.data(), ph.xptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (nslots) CK(cudaMemcpy(pl.xslot.p, ph.xslot.data(), ph.xslot.size() * sizeof(int), cudaMemcpyHostToDevice));
     pl.S = S;
-    pl.NT = NT;
-    pl.P = P;
-    pl.ntiles = T;
+    pl.NT = ph.NT;
+    pl.P = ph.P;
+    pl.ntiles = ph.T;
     pl.nslots = nslots;
     pl.ok = true;
 }
+
+}  // namespace
+
+// Self-check of the symmetric-half schedule on the host (no GPU): replays the kernels'
+// accumulate / flush rules tile by tile (end-of-segment lookahead as in k_dstream_sym8, gN > 1,
+// and k_dstream_pair, gN = 1) against the plan plan_host emitted, and counts violations: every
+// upper tile exactly once; every (tile, N) contribution in exactly one slot of row tile I and
+// every (tile, T), I < J, in exactly one slot of row tile J; slot -> row tile as recorded; the
+// reduction lists (or the contiguous slot map) consistent.
+extern "C" int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous) {
+    if (l < 1 || S < 1 || S > 16 || gN < 1 || max_ctas < 1) return -1;
+    int64_t err = 0;
+    PlanHost ph;
+    try {
+        ph = plan_host(l, max_ctas, S, gN, contiguous != 0);
+    } catch (...) {
+        return -2;
+    }
+    const int NT = ph.NT;
+    const int64_t T = ph.T;
+    if (T != (int64_t)NT * (NT + 1) / 2) ++err;
+    std::vector<uint8_t> seen((size_t)NT * NT, 0);
+    for (int64_t t = 0; t < T; ++t) {
+        const int I = (int)(ph.tiles[t] >> 16), J = (int)(ph.tiles[t] & 0xFFFFu);
+        if (I > J || J >= NT || seen[(size_t)I * NT + J]++) ++err;
+    }
+    if (ph.pbeg.front() != 0 || ph.pbeg.back() != T) ++err;
+    for (size_t p = 0; p + 1 < ph.pbeg.size(); ++p)
+        if (ph.pbeg[p] > ph.pbeg[p + 1]) ++err;
+    const int nslots = (int)ph.slot_x.size();
+    std::vector<int> used_n(T, 0), used_t(T, 0);
+    std::vector<int> slot_seen(nslots, 0);
+    for (int p = 0; p < ph.P; ++p) {
+        std::vector<std::vector<int64_t>> accN(S), accT(S);
+        uint32_t maskN = 0, maskT = 0;
+        int slotN = ph.sbase[2 * p], slotT = ph.sbase[2 * p + 1];
+        auto flush = [&](uint32_t mask, std::vector<std::vector<int64_t>>& acc, int& slot, int role, int bi, int bj) {
+            for (int a = 0; a < S; ++a) {
+                if (!(mask & (1u << a))) continue;
+                const int X = role ? bj * S + a : bi * S + a;
+                if (slot < 0 || slot >= nslots || ph.slot_x[slot] != X) ++err;
+                if (slot >= 0 && slot < nslots) ++slot_seen[slot];
+                for (const int64_t t : acc[a]) {
+                    const int I = (int)(ph.tiles[t] >> 16), J = (int)(ph.tiles[t] & 0xFFFFu);
+                    if ((role ? J : I) != X) ++err;
+                    ++(role ? used_t : used_n)[t];
+                }
+                acc[a].clear();
+                ++slot;
+            }
+        };
+        for (int64_t t = ph.pbeg[p]; t < ph.pbeg[p + 1]; ++t) {
+            const int I = (int)(ph.tiles[t] >> 16), J = (int)(ph.tiles[t] & 0xFFFFu);
+            const int bi = I / S, bj = J / S;
+            bool end_seg = (t + 1 == ph.pbeg[p + 1]), end_n = end_seg;
+            if (!end_seg) {
+                const int I2 = (int)(ph.tiles[t + 1] >> 16), J2 = (int)(ph.tiles[t + 1] & 0xFFFFu);
+                end_seg = (I2 / S != bi) || (J2 / S != bj);
+                end_n = (I2 / S != bi) || ((J2 / S) / gN != bj / gN);
+            }
+            const int aN = I - bi * S, aT = J - bj * S;
+            accN[aN].push_back(t);
+            maskN |= 1u << aN;
+            if (I != J) {
+                accT[aT].push_back(t);
+                maskT |= 1u << aT;
+            }
+            if (end_seg) {
+                if (end_n) {
+                    flush(maskN, accN, slotN, 0, bi, bj);
+                    maskN = 0;
+                }
+                flush(maskT, accT, slotT, 1, bi, bj);
+                maskT = 0;
+            }
+        }
+        if (p + 1 < ph.P && (slotN != ph.sbase[2 * p + 1] || slotT != ph.sbase[2 * p + 2])) ++err;
+    }
+    for (int64_t t = 0; t < T; ++t) {
+        const int I = (int)(ph.tiles[t] >> 16), J = (int)(ph.tiles[t] & 0xFFFFu);
+        if (used_n[t] != 1) ++err;
+        if (used_t[t] != (I < J ? 1 : 0)) ++err;
+    }
+    for (int q = 0; q < nslots; ++q)
+        if (slot_seen[q] != 1) ++err;
+    // reduction lists: row tile X owns exactly its slots
+    for (int X = 0; X < NT; ++X)
+        for (int q = ph.xptr[X]; q < ph.xptr[X + 1]; ++q) {
+            const int logical = contiguous ? -1 : ph.xslot[q];
+            if (!contiguous && ph.slot_x[logical] != X) ++err;
+        }
+    if (contiguous) {
+        std::vector<int> inv(nslots, -1);
+        for (int q = 0; q < nslots; ++q) {
+            const int phys = ph.smap[q];
+            if (phys < 0 || phys >= nslots || inv[phys] >= 0) { ++err; continue; }
+            inv[phys] = q;
+            const int X = ph.slot_x[q];
+            if (phys < ph.xptr[X] || phys >= ph.xptr[X + 1]) ++err;
+        }
+    }
+    return err;
+}
+
+namespace {
 
 template <int BP>
 void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
