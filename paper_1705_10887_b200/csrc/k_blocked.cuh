@@ -22,17 +22,17 @@ namespace sbmds {
 constexpr int kRB = 256;   // rows per block (local row fits in 8 bits)
 
 // ------------------------------------------------------------------ create-time build
-__global__ void k_blk_offsets(int64_t n, int64_t nblk, const int32_t* __restrict__ rp, int32_t* __restrict__ off) {
+__global__ void k_blk_offsets(int64_t n, int64_t nblk, int rb, const int32_t* __restrict__ rp, int32_t* __restrict__ off) {
     for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B <= nblk; B += (int64_t)gridDim.x * blockDim.x)
-        off[B] = rp[min(B * kRB, n)];
+        off[B] = rp[min(B * rb, n)];
 }
 
 // flag[p] = 1 where a new (block, column) pair starts in the block-segmented col sort.
-__global__ void k_blk_flags(int32_t nnz, const int32_t* __restrict__ scol, const int32_t* __restrict__ perm,
+__global__ void k_blk_flags(int32_t nnz, int rb, const int32_t* __restrict__ scol, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ rowof, const int32_t* __restrict__ off,
                             int32_t* __restrict__ flag) {
     for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x) {
-        const int32_t B = rowof[perm[p]] / kRB;
+        const int32_t B = rowof[perm[p]] / rb;
         flag[p] = (p == off[B] || scol[p] != scol[p - 1]) ? 1 : 0;
     }
 }
@@ -54,7 +54,8 @@ __global__ void k_blk_umax(int64_t nblk, const int32_t* __restrict__ dict_off, u
     atomicMax(umax, m);
 }
 
-__global__ void k_blk_scatter(int32_t nnz, const int32_t* __restrict__ scol, const int32_t* __restrict__ perm,
+// (rb: rows per block; lcp, lrow, lval may be NULL when the block-local CSC is not wanted)
+__global__ void k_blk_scatter(int32_t nnz, int rb, const int32_t* __restrict__ scol, const int32_t* __restrict__ perm,
                               const int32_t* __restrict__ rowof, const float* __restrict__ val,
                               const int32_t* __restrict__ flag, const int32_t* __restrict__ incl,
                               const int32_t* __restrict__ dict_off, int32_t* __restrict__ dict,
@@ -63,15 +64,17 @@ __global__ void k_blk_scatter(int32_t nnz, const int32_t* __restrict__ scol, con
     for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x) {
         const int32_t e = perm[p];
         const int32_t row = rowof[e];
-        const int32_t B = row / kRB;
+        const int32_t B = row / rb;
         const int32_t d = incl[p] - 1;
         if (flag[p]) {
             dict[d] = scol[p];
-            lcp[d] = p;
+            if (lcp) lcp[d] = p;
         }
         lcol[e] = (uint16_t)(d - dict_off[B]);
-        lrow[p] = (uint8_t)(row - B * kRB);
-        lval[p] = val[e];
+        if (lrow) {
+            lrow[p] = (uint8_t)(row - B * rb);
+            lval[p] = val[e];
+        }
     }
 }
 

@@ -429,8 +429,10 @@ __host__ __device__ __forceinline__ int f16_scale_exp(float mx) {
 // Y1 (l_pad x bp, row-major; R^-1 fold when Rinv) -> folded copy Y1f and per-column max|.|
 __global__ void __launch_bounds__(256) k_y16_prep(int64_t lpad, int b, int bp, const double* __restrict__ Rinv,
                                                   const float* __restrict__ Y1, float* __restrict__ Y1f,
-                                                  unsigned int* __restrict__ cmax) {
+                                                  unsigned int* __restrict__ cmax, unsigned int* __restrict__ zero64) {
     __shared__ double Ms[64 * 64];
+    // zero64 (optional): the Y2 column maxima the following k_dreduce_pair accumulates
+    if (zero64 && blockIdx.x == 0 && threadIdx.x < 64) zero64[threadIdx.x] = 0u;
     __shared__ float ys[256];
     __shared__ float mx[256];
     if (Rinv)
@@ -521,8 +523,10 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
                                                       const int* __restrict__ dexp, const int* __restrict__ yexp,
                                                       const double* __restrict__ w, float* __restrict__ Y2,
                                                       double* __restrict__ tpart, double* __restrict__ t,
-                                                      unsigned int* __restrict__ counter) {
+                                                      unsigned int* __restrict__ counter, unsigned int* __restrict__ y2max) {
     __shared__ double red[256];
+    __shared__ float cmx[256];
+    float m = 0.f;   // |Y2| column maxima (optional; the tensor-core sparse step's digit scales)
     const int rows_per_blk = 256 / bp;
     const int tid = threadIdx.x;
     const int cidx = tid % bp, rloc = tid / bp;
@@ -545,11 +549,18 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
             for (; q < q1; ++q) v += (double)P[((int64_t)(xslot ? xslot[q] : q) * 128 + rr) * bp + cidx];
             v *= unscale;
             Y2[r * bp + cidx] = (float)v;
+            m = fmaxf(m, fabsf((float)v));
             if (cidx < b) acc_t += w[r] * v;
         }
     }
     red[tid] = (rloc < rows_per_blk) ? acc_t : 0.0;
+    cmx[tid] = m;
     __syncthreads();
+    if (y2max && tid < bp) {
+        float mm = 0.f;
+        for (int q = 0; q < rows_per_blk; ++q) mm = fmaxf(mm, cmx[q * bp + tid]);
+        atomicMax(y2max + tid, __float_as_uint(mm));
+    }
     if (tid < bp) {
         double v = 0.0;
         for (int q = 0; q < rows_per_blk; ++q) v += red[q * bp + tid];

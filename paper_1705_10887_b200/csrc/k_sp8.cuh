@@ -1,0 +1,617 @@
+// The eigensolver's sparse step on the int8 tensor cores ("tensor-core sparse
+// step"): A5 of this apply, the Gram step, and A2 of the next apply, per 128-row block of S.
+//
+// Inside sbmds_eigs the block Y = B~X formed by A5 (Y = -1/2 (S Y2 - 1 t^T)
+// "left-multiplying by P", PAPER.md:113 the -1/2) is consumed by the Gram step and by the next
+// apply's A2 (S^T Y, "right-multiplying by P^T"), both linear in Y's rows. S is
+// local: the 128 consecutive vertices of a block touch d_B <= 128 landmarks
+// (config 4: 115 on average), so the block's slice S_B (128 x d_B) is stored as a DENSE image
+// and both products become tensor-core GEMMs with no gathers at all:
+//   N:  Y_B   = S_B   Y2[dict_B]    (M = 128 rows,  K = d_pad, N = 3 b)   A K-major
+//   T:  P1_B  = S_B^T Y_B           (M = 128 dict,  K = 128 rows, N = 3 b) A MN-major
+// One shared-memory image serves both: with the no-swizzle core-matrix layout (core = 8 rows x
+// 16 contiguous bytes; core (row group rg, column chunk kc) at (kc * 16 + rg) * 128 bytes) an
+// 8-bit image is a K-major A for N (LBO = 2048 along K, SBO = 128 along M) and an MN-major A
+// for T (LBO = 128 along K, SBO = 2048 along M) -- scripts/sp8_probe.cu checks both.
+//
+// Arithmetic (as k_dstream_sym8.cuh): S_B is scaled by 2^eS_B (per block) and stored as three
+// balanced signed digits per entry (3 planes, k_sp8_build, once per handle); the B operands are
+// digitised on the fly: Y2 with one scale 2^ey_c per column (from its column maxima), Y_B with
+// per-block column scales. kind::i8 products and int32 sums are exact; the three accumulator
+// column groups give c0 + c1/256 + c2/65536, undone in fp64 (error <= ~2^-23 of the scaled
+// maxima per product, the same bound as the D stream).
+//
+// Per block (persistent CTAs, contiguous block ranges):
+//   warp 0      producer: the block's image (one bulk copy, 384 d_pad bytes) into a 3-stage ring;
+//               at Rayleigh-Ritz steps also the block's rows of Y_prev (bulk copy)
+//   warp 1      MMA issue, order N(i), T(i-1)
+//   warps 2-5   epilogue: N accumulator -> Y rows (HBM once, smem for the Gram), the block's
+//               column maxima, Y_B digits (B operand of T); T accumulator -> P1 partials
+//   warps 6-9   B operand of N (Y2[dict_B] digits), then the FP64-tensor-core Gram of the
+//               previous block (G = Y^T Y, 1^T Y, and H' = Y_prev^T Y at RR steps)
+// Every sum has a fixed order: Y, P1 and the Grams are bitwise reproducible.
+#pragma once
+#include "common.cuh"
+#include "k_dstream_sym8.cuh"
+#include "k_small.cuh"
+
+namespace sbmds {
+
+constexpr int kSp8RB = 128;   // rows per block (the MMA M of N)
+constexpr int kSp8DK = 128;   // largest padded dictionary (the MMA M of T)
+
+__device__ __forceinline__ uint64_t umma_desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+
+// byte offset of (row r, column k) in a core-matrix image with `rgroups` 8-row groups per
+// 16-column chunk: ((k / 16) * rgroups + r / 8) * 128 + (r % 8) * 16 + k % 16
+__host__ __device__ __forceinline__ int sp8_off(int r, int k, int rgroups) {
+    return (((k >> 4) * rgroups + (r >> 3)) << 7) + ((r & 7) << 4) + (k & 15);
+}
+
+__host__ __device__ __forceinline__ int sp8_dpad(int d) { return d <= 32 ? 32 : (d + 31) / 32 * 32; }
+
+// B operands are MN-major core-matrix images: core = 8 K-rows x 16 contiguous N bytes, core
+// (K group kg, N group ng) at (kg * NB/16 + ng) * 128 (LBO = K stride, SBO = 128 along N;
+// scripts/sp8_probe.cu mode 2). A thread owning K-row k writes digit plane p's 16 columns as
+// one 16-byte store at sp8_boff(k, p).
+template <int NB>
+__device__ __forceinline__ int sp8_boff(int k, int p) {
+    return (((k >> 3) * (NB / 16) + p) << 7) + ((k & 7) << 4);
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8_bmn(int M, int N, int a_mn) {
+    return idesc_i8_s32acc(M, N, a_mn) | (1u << 16);   // B MN-major
+}
+
+// 2^e as a double (|e| <= 1022)
+__device__ __forceinline__ double pow2d(int e) { return __hiloint2double((1023 + e) << 20, 0); }
+
+// balanced base-256 digits of x (|x| <= 8,355,711), x = d0 2^16 + d1 2^8 + d2 (as digits3);
+// p_k holds digit k in its low byte (the upper bytes are don't-care)
+__device__ __forceinline__ void digits3_lo(int x, int& p0, int& p1, int& p2) {
+    p2 = x;
+    const int v1 = (x - ((x << 24) >> 24)) >> 8;
+    p1 = v1;
+    p0 = (v1 - ((v1 << 24) >> 24)) >> 8;
+}
+
+// the low bytes of a, b, c, d as one little-endian word
+__device__ __forceinline__ uint32_t pack4_lo(int a, int b, int c, int d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// digits of round(v_c 2^e_c) for 16 columns -> the three 16-byte plane rows of one K-row
+__device__ __forceinline__ void digit_rows16(const float (&v)[16], const double (&sc)[16], uint4& r0, uint4& r1,
+                                             uint4& r2) {
+    int a0[16], a1[16], a2[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) digits3_lo(__double2int_rn((double)v[c] * sc[c]), a0[c], a1[c], a2[c]);
+    r0 = make_uint4(pack4_lo(a0[0], a0[1], a0[2], a0[3]), pack4_lo(a0[4], a0[5], a0[6], a0[7]),
+                    pack4_lo(a0[8], a0[9], a0[10], a0[11]), pack4_lo(a0[12], a0[13], a0[14], a0[15]));
+    r1 = make_uint4(pack4_lo(a1[0], a1[1], a1[2], a1[3]), pack4_lo(a1[4], a1[5], a1[6], a1[7]),
+                    pack4_lo(a1[8], a1[9], a1[10], a1[11]), pack4_lo(a1[12], a1[13], a1[14], a1[15]));
+    r2 = make_uint4(pack4_lo(a2[0], a2[1], a2[2], a2[3]), pack4_lo(a2[4], a2[5], a2[6], a2[7]),
+                    pack4_lo(a2[8], a2[9], a2[10], a2[11]), pack4_lo(a2[12], a2[13], a2[14], a2[15]));
+}
+
+// exact c0 + c1/256 + c2/65536 of the three accumulator groups, times 2^16 (an integer)
+__device__ __forceinline__ long long acc3(int g0, int g1, int g2) {
+    return ((long long)g0 << 16) + (long long)(g1 * 256 + g2);
+}
+
+__device__ __forceinline__ void named_bar(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// ------------------------------------------------------------------ create: images
+// One CTA (128 threads) per 128-row block: eS_B from the block's largest |S_ij|, then each
+// thread writes the three digits of its row's entries into the zero-filled image (planes of
+// 128 x d_pad bytes at img + off[B]).
+__global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, const int32_t* __restrict__ rp,
+                                                   const float* __restrict__ val, const uint16_t* __restrict__ lcol,
+                                                   const int32_t* __restrict__ doff, const int64_t* __restrict__ ioff,
+                                                   int8_t* __restrict__ img, int* __restrict__ escale) {
+    __shared__ float red[4];
+    for (int64_t B = blockIdx.x; B < nblk; B += gridDim.x) {
+        const int64_t r0 = B * kSp8RB;
+        const int rows = (int)((n - r0) < kSp8RB ? (n - r0) : kSp8RB);
+        const int r = threadIdx.x;
+        const int32_t beg = r < rows ? rp[r0 + r] : 0, end = r < rows ? rp[r0 + r + 1] : 0;
+        float m = 0.f;
+        for (int32_t e = beg; e < end; ++e) m = fmaxf(m, fabsf(val[e]));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        __syncthreads();
+        const int eS = i8_scale_exp(fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3])));
+        if (threadIdx.x == 0) escale[B] = eS;
+        const int dp = sp8_dpad(doff[B + 1] - doff[B]);
+        int8_t* out = img + ioff[B];
+        for (int32_t e = beg; e < end; ++e) {
+            int d0, d1, d2;
+            digits3(__float2int_rn(ldexpf(val[e], eS)), d0, d1, d2);
+            const int o = sp8_off(r, (int)lcol[e], kSp8RB / 8);
+            out[o] = (int8_t)d0;
+            out[kSp8RB * dp + o] = (int8_t)d1;
+            out[2 * kSp8RB * dp + o] = (int8_t)d2;
+        }
+    }
+}
+
+__global__ void k_sp8_sizes(int64_t nblk, const int32_t* __restrict__ doff, int64_t* __restrict__ bytes) {
+    for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B < nblk; B += (int64_t)gridDim.x * blockDim.x)
+        bytes[B] = (int64_t)3 * kSp8RB * sp8_dpad(doff[B + 1] - doff[B]);
+}
+
+// |Y2| column maxima when the D path's reduction did not produce them (full-D paths)
+__global__ void __launch_bounds__(256) k_colabsmax(int64_t l, int bp, const float* __restrict__ Y2,
+                                                   unsigned int* __restrict__ cmax) {
+    __shared__ float m[256];
+    const int rb = 256 / bp, c = threadIdx.x % bp, r = threadIdx.x / bp;
+    float v = 0.f;
+    for (int64_t k = (int64_t)blockIdx.x * rb + r; k < l; k += (int64_t)gridDim.x * rb) v = fmaxf(v, fabsf(Y2[k * bp + c]));
+    m[threadIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x < bp) {
+        for (int q = 1; q < rb; ++q) v = fmaxf(v, m[q * bp + threadIdx.x]);
+        atomicMax(cmax + threadIdx.x, __float_as_uint(v));
+    }
+}
+
+// ------------------------------------------------------------------ the step kernel
+template <int BP>
+struct Sp8Cfg {
+    static constexpr int NB = 3 * BP;                    // B rows [y0; y1; y2]
+    static constexpr int IMG = 3 * kSp8RB * kSp8DK;      // 48 KB: largest image
+    static constexpr int NS = 3;                         // image stages
+    static constexpr int BN = NB * kSp8DK;               // B of N: d_pad x NB (MN-major)
+    static constexpr int BT = NB * kSp8RB;               // B of T: 128 rows x NB (MN-major)
+    static constexpr int YR = kSp8RB * BP * 4;           // fp32 rows of a block
+    static constexpr int OFF_BN = NS * IMG;
+    static constexpr int OFF_BT = OFF_BN + 2 * BN;
+    static constexpr int OFF_YR = OFF_BT + 2 * BT;
+    static constexpr int OFF_YP = OFF_YR + 2 * YR;
+    static constexpr int OFF_BAR = OFF_YP + 2 * YR;
+    static constexpr int SMEM = OFF_BAR + 1024 + 1024;   // + barriers, scales; + alignment slack
+    static constexpr int THREADS = 10 * 32;
+    static constexpr int ACCN = 0, ACCT = 2 * NB;        // TMEM columns: N[2], T[2]
+    static_assert(BP == 16, "the tensor-core sparse step is built for b = 16");
+    static_assert(4 * NB <= 256, "tmem");
+};
+
+template <int BP, bool WITH_H>
+__global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
+    k_sp8_step(int64_t n, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
+               const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
+               const float* __restrict__ Y2, const unsigned int* __restrict__ y2max, const double* __restrict__ t,
+               float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
+               double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
+               unsigned int* __restrict__ counter) {
+    using C = Sp8Cfg<BP>;
+    constexpr int NB = C::NB;
+    constexpr int NCB = BP / 8;
+    constexpr int NPG = NCB * (NCB + 1) / 2;
+    constexpr int NPH = WITH_H ? NCB * NCB : 1;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
+    uint64_t* full_img = bars;          // [3]
+    uint64_t* empty_img = bars + 3;     // [3]
+    uint64_t* bn_full = bars + 6;       // [2]
+    uint64_t* bn_empty = bars + 8;
+    uint64_t* an_full = bars + 10;
+    uint64_t* an_empty = bars + 12;
+    uint64_t* bt_full = bars + 14;
+    uint64_t* bt_empty = bars + 16;
+    uint64_t* at_full = bars + 18;
+    uint64_t* at_empty = bars + 20;
+    uint64_t* yr_full = bars + 22;
+    uint64_t* yr_empty = bars + 24;
+    uint64_t* yp_full = bars + 26;
+    uint64_t* yp_empty = bars + 28;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
+    int* ey2 = reinterpret_cast<int*>(bars + 32);          // [BP] scale exponents of Y2's columns
+    int* eyb = ey2 + BP;                                   // [2][BP] per-block exponents of Y_B
+    float* cmx = reinterpret_cast<float*>(eyb + 2 * BP);   // [2][4][BP] epilogue warps' column maxima
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b0 = blockIdx.x * nblk / gridDim.x, b1 = (blockIdx.x + 1) * nblk / gridDim.x;
+    const int nb = (int)(b1 - b0);
+    const bool want_t = P1 != nullptr;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 3; ++s) {
+            mbar_init(&full_img[s], 1);
+            mbar_init(&empty_img[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&bn_full[a], 128);
+            mbar_init(&bn_empty[a], 1);
+            mbar_init(&an_full[a], 1);
+            mbar_init(&an_empty[a], 128);
+            mbar_init(&bt_full[a], 128);
+            mbar_init(&bt_empty[a], 1);
+            mbar_init(&at_full[a], 1);
+            mbar_init(&at_empty[a], 128);
+            mbar_init(&yr_full[a], 128);
+            mbar_init(&yr_empty[a], 128);
+            mbar_init(&yp_full[a], 1);
+            mbar_init(&yp_empty[a], 128);
+        }
+        fence_barrier_init();
+    }
+    if (threadIdx.x < BP) ey2[threadIdx.x] = i8_scale_exp(__uint_as_float(y2max[threadIdx.x]));
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+    auto dpad_of = [&](int64_t B) { return sp8_dpad(__ldg(doff + B + 1) - __ldg(doff + B)); };
+    auto rows_of = [&](int64_t B) {
+        const int64_t r0 = B * kSp8RB;
+        return (int)((n - r0) < kSp8RB ? (n - r0) : kSp8RB);
+    };
+
+    // Gram accumulators live in warps 6-9 (per-warp DMMA fragments, as k_fused.cuh)
+    double gacc[NPG][2], hacc[NPH][2], csum[NCB];
+#pragma unroll
+    for (int i = 0; i < NPG; ++i) gacc[i][0] = gacc[i][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NPH; ++i) hacc[i][0] = hacc[i][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCB; ++c) csum[c] = 0.0;
+
+    if (warp == 0) {
+        // ------------------------------------------------ producer
+        if (lane == 0) {
+            for (int i = 0; i < nb; ++i) {
+                const int64_t B = b0 + i;
+                const int s = i % 3;
+                const uint32_t ph = (uint32_t)((i / 3) & 1);
+                const uint32_t bytes = (uint32_t)(3 * kSp8RB * dpad_of(B));
+                mbar_wait(&empty_img[s], ph ^ 1u, 141 * 65536 + (i & 0xFFFF));
+                mbar_arrive_expect_tx(&full_img[s], bytes);
+                bulk_load(base + s * C::IMG, gimg + __ldg(ioff + B), bytes, &full_img[s]);
+                if constexpr (WITH_H) {
+                    const int a = i & 1;
+                    const uint32_t pa = (uint32_t)((i >> 1) & 1);
+                    const uint32_t yb = (uint32_t)(rows_of(B) * BP * 4);
+                    mbar_wait(&yp_empty[a], pa ^ 1u, 142 * 65536 + (i & 0xFFFF));
+                    mbar_arrive_expect_tx(&yp_full[a], yb);
+                    bulk_load(base + C::OFF_YP + a * C::YR, Yprev + B * kSp8RB * BP, yb, &yp_full[a]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issue: N(i), then T(i - 1)
+        constexpr uint32_t id1n = idesc_i8_bmn(128, NB, 0), id2n = idesc_i8_bmn(128, 2 * BP, 0),
+                           id3n = idesc_i8_bmn(128, BP, 0);
+        constexpr uint32_t id1t = idesc_i8_bmn(128, NB, 1), id2t = idesc_i8_bmn(128, 2 * BP, 1),
+                           id3t = idesc_i8_bmn(128, BP, 1);
+        constexpr uint32_t KG = NB / 16 * 128;   // B: bytes per 8-row K group (the LBO)
+        auto issue_t = [&](int i) {
+            const int64_t B = b0 + i;
+            const int s = i % 3, a = i & 1;
+            const uint32_t pa = (uint32_t)((i >> 1) & 1);
+            const int dp = dpad_of(B);
+            mbar_wait(&bt_full[a], pa, 143 * 65536 + (i & 0xFFFF));
+            mbar_wait(&at_empty[a], pa ^ 1u, 144 * 65536 + (i & 0xFFFF));
+            tc_fence_after();
+            const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BT + a * C::BT);
+            const uint32_t d = tbase + (uint32_t)(C::ACCT + a * NB);
+            const uint32_t plane = (uint32_t)(kSp8RB * dp);
+            if (elect_one()) {
+#pragma unroll
+                for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows per MMA
+                    const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
+                    tc_mma_i8(d, umma_desc_none(sa + 512 * j, 128, 2048), bd, id1t, j > 0 ? 1u : 0u);
+                    tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
+                    tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
+                }
+                tc_commit(&at_full[a]);
+                tc_commit(&bt_empty[a]);
+                tc_commit(&empty_img[s]);
+            }
+            __syncwarp();
+        };
+        for (int i = 0; i < nb; ++i) {
+            const int64_t B = b0 + i;
+            const int s = i % 3, a = i & 1;
+            const uint32_t ph = (uint32_t)((i / 3) & 1), pa = (uint32_t)((i >> 1) & 1);
+            const int dp = dpad_of(B);
+            mbar_wait(&full_img[s], ph, 145 * 65536 + (i & 0xFFFF));
+            mbar_wait(&bn_full[a], pa, 146 * 65536 + (i & 0xFFFF));
+            mbar_wait(&an_empty[a], pa ^ 1u, 147 * 65536 + (i & 0xFFFF));
+            tc_fence_after();
+            const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BN + a * C::BN);
+            const uint32_t d = tbase + (uint32_t)(C::ACCN + a * NB);
+            const uint32_t plane = (uint32_t)(kSp8RB * dp);
+            if (elect_one()) {
+                for (int j = 0; j < dp / 32; ++j) {   // K = 32 dictionary entries per MMA
+                    const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
+                    tc_mma_i8(d, umma_desc_none(sa + 4096 * j, 2048, 128), bd, id1n, j > 0 ? 1u : 0u);
+                    tc_mma_i8(d + BP, umma_desc_none(sa + plane + 4096 * j, 2048, 128), bd, id2n, 1u);
+                    tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 4096 * j, 2048, 128), bd, id3n, 1u);
+                }
+                tc_commit(&an_full[a]);
+                tc_commit(&bn_empty[a]);
+                if (!want_t) tc_commit(&empty_img[s]);
+            }
+            __syncwarp();
+            if (want_t && i > 0) issue_t(i - 1);
+        }
+        if (want_t && nb > 0) issue_t(nb - 1);
+    } else if (warp < 6) {
+        // ------------------------------------------------ epilogue (TMEM lane = row / dictionary entry)
+        const int q = warp & 3;
+        const int r = 32 * q + lane;
+        const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+        double ht[BP];   // t / 2
+#pragma unroll
+        for (int c = 0; c < BP; ++c) ht[c] = 0.5 * t[c];
+        auto load_acc = [&](uint32_t col, int (&g0)[BP], int (&g1)[BP], int (&g2)[BP]) {
+#pragma unroll
+            for (int c0 = 0; c0 < BP; c0 += 8) {
+                tmem_ld8_u(tbase + lane_off + col + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
+                tmem_ld8_u(tbase + lane_off + col + BP + c0, *reinterpret_cast<int(*)[8]>(&g1[c0]));
+                tmem_ld8_u(tbase + lane_off + col + 2 * BP + c0, *reinterpret_cast<int(*)[8]>(&g2[c0]));
+            }
+            tmem_wait_ld();
+        };
+        // block metadata, one block ahead: (d0, du, eS) of the block whose T accumulator is next
+        int32_t t_d0 = 0, t_du = 0;
+        int t_eS = 0;
+        int eS_cur = nb > 0 ? __ldg(escale + b0) : 0;
+        auto drain_t = [&](int i) {
+            const int a = i & 1;
+            const uint32_t pa = (uint32_t)((i >> 1) & 1);
+            mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
+            tc_fence_after();
+            int g0[BP], g1[BP], g2[BP];
+            load_acc((uint32_t)(C::ACCT + a * NB), g0, g1, g2);
+            tc_fence_before();
+            mbar_arrive(&at_empty[a]);
+            if (r < t_du) {
+                float out[BP];
+#pragma unroll
+                for (int c = 0; c < BP; ++c)
+                    out[c] = (float)((double)acc3(g0[c], g1[c], g2[c]) * pow2d(16 - t_eS - eyb[a * BP + c]));
+                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)(t_d0 + r) * BP);
+#pragma unroll
+                for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]);
+            }
+        };
+        for (int i = 0; i < nb; ++i) {
+            const int64_t B = b0 + i;
+            const int a = i & 1;
+            const uint32_t pa = (uint32_t)((i >> 1) & 1);
+            const int rows = rows_of(B);
+            const int eS = eS_cur;
+            const int32_t nd0 = __ldg(doff + B), ndu = __ldg(doff + B + 1) - nd0;   // for drain_t(i) next round
+            if (i + 1 < nb) eS_cur = __ldg(escale + B + 1);
+            double sc[BP];   // 2^(16 - eS - ey2_c): acc3 -> S Y2
+#pragma unroll
+            for (int c = 0; c < BP; ++c) sc[c] = pow2d(16 - eS - ey2[c]);
+            mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
+            tc_fence_after();
+            int g0[BP], g1[BP], g2[BP];
+            load_acc((uint32_t)(C::ACCN + a * NB), g0, g1, g2);
+            tc_fence_before();
+            mbar_arrive(&an_empty[a]);
+            // Y = -1/2 (S Y2 - 1 t^T) for this row
+            float y[BP];
+            const bool live = r < rows;
+#pragma unroll
+            for (int c = 0; c < BP; ++c)
+                y[c] = live ? (float)fma(-0.5, (double)acc3(g0[c], g1[c], g2[c]) * sc[c], ht[c]) : 0.f;
+            if (live) {
+                float4* dst = reinterpret_cast<float4*>(Y + (B * kSp8RB + r) * BP);
+#pragma unroll
+                for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+            }
+            mbar_wait(&yr_empty[a], pa ^ 1u, 150 * 65536 + (i & 0xFFFF));
+            {
+                float4* yr = reinterpret_cast<float4*>(base + C::OFF_YR + a * C::YR) + r * (BP / 4);
+#pragma unroll
+                for (int c = 0; c < BP; c += 4) yr[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+            }
+            mbar_arrive(&yr_full[a]);
+            if (want_t) {
+                // the block's column maxima (warp butterfly: lane ends with the maximum of column
+                // cl over its 32 rows), then per-column exponents ey (thread c < 16), then the
+                // digits of Y_B as the B operand of T
+                float m[BP];
+#pragma unroll
+                for (int c = 0; c < BP; ++c) m[c] = fabsf(y[c]);
+#pragma unroll
+                for (int h = BP / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+                    const bool up = (lane & o) != 0;
+#pragma unroll
+                    for (int j = 0; j < h; ++j) {
+                        const float send = up ? m[j] : m[j + h], keep = up ? m[j + h] : m[j];
+                        m[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
+                    }
+                }
+                m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 1));
+                const int cl = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+                if ((lane & 1) == 0) cmx[(a * 4 + q) * BP + cl] = m[0];
+                named_bar(1, 128);
+                if (r < BP) {
+                    const float* cm = cmx + a * 4 * BP;
+                    eyb[a * BP + r] = i8_scale_exp(fmaxf(fmaxf(cm[r], cm[BP + r]), fmaxf(cm[2 * BP + r], cm[3 * BP + r])));
+                }
+                named_bar(1, 128);
+                double ysc[BP];
+#pragma unroll
+                for (int c = 0; c < BP; ++c) ysc[c] = pow2d(eyb[a * BP + c]);
+                uint4 w0, w1, w2;
+                digit_rows16(y, ysc, w0, w1, w2);
+                mbar_wait(&bt_empty[a], pa ^ 1u, 151 * 65536 + (i & 0xFFFF));
+                uint8_t* bt = base + C::OFF_BT + a * C::BT;
+                *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 0)) = w0;
+                *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 1)) = w1;
+                *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 2)) = w2;
+                fence_proxy_async();
+                mbar_arrive(&bt_full[a]);
+                if (i > 0) drain_t(i - 1);
+                t_d0 = nd0;
+                t_du = ndu;
+                t_eS = eS;
+            }
+        }
+        if (want_t && nb > 0) drain_t(nb - 1);
+    } else {
+        // ------------------------------------------------ B operand of N, then the Gram of the previous block
+        const int gt = threadIdx.x - 192;   // 0..127
+        const int gw = warp - 6;            // 0..3
+        double y2sc[BP];                    // 2^ey2_c
+#pragma unroll
+        for (int c = 0; c < BP; ++c) y2sc[c] = pow2d(ey2[c]);
+        const int kr = lane & 3, cc = lane >> 2;
+        auto gram = [&](int i) {
+            const int64_t B = b0 + i;
+            const int a = i & 1;
+            const uint32_t pa = (uint32_t)((i >> 1) & 1);
+            const int rows = rows_of(B);
+            mbar_wait(&yr_full[a], pa, 152 * 65536 + (i & 0xFFFF));
+            if constexpr (WITH_H) mbar_wait(&yp_full[a], pa, 153 * 65536 + (i & 0xFFFF));
+            const float* yr = reinterpret_cast<const float*>(base + C::OFF_YR + a * C::YR);
+            const float* yp = reinterpret_cast<const float*>(base + C::OFF_YP + a * C::YR);
+#pragma unroll 2
+            for (int s4 = 0; s4 < 8; ++s4) {
+                const int rr = 32 * gw + 4 * s4 + kr;
+                double yv[NCB], xv[NCB];
+#pragma unroll
+                for (int c = 0; c < NCB; ++c) {
+                    const int col = 8 * c + cc;
+                    yv[c] = (double)yr[rr * BP + col];
+                    csum[c] += yv[c];
+                    if constexpr (WITH_H) xv[c] = rr < rows ? (double)yp[rr * BP + col] : 0.0;
+                }
+                int pi = 0;
+#pragma unroll
+                for (int c = 0; c < NCB; ++c)
+#pragma unroll
+                    for (int c2 = c; c2 < NCB; ++c2) dmma_8x8x4(gacc[pi++], yv[c], yv[c2]);
+                if constexpr (WITH_H) {
+#pragma unroll
+                    for (int c = 0; c < NCB; ++c)
+#pragma unroll
+                        for (int c2 = 0; c2 < NCB; ++c2) dmma_8x8x4(hacc[c * NCB + c2], xv[c], yv[c2]);
+                }
+            }
+            mbar_arrive(&yr_empty[a]);
+            if constexpr (WITH_H) mbar_arrive(&yp_empty[a]);
+        };
+        for (int i = 0; i < nb; ++i) {
+            const int64_t B = b0 + i;
+            const int a = i & 1;
+            const uint32_t pa = (uint32_t)((i >> 1) & 1);
+            const int32_t d0 = __ldg(doff + B), du = __ldg(doff + B + 1) - d0;
+            mbar_wait(&bn_empty[a], pa ^ 1u, 154 * 65536 + (i & 0xFFFF));
+            uint8_t* bn = base + C::OFF_BN + a * C::BN;
+            // thread k: dictionary entry k, its Y2 row as four float4 loads (two dependent L2
+            // round trips per block), digits as three 16-byte plane rows
+            if (gt < du) {
+                const float4* src = reinterpret_cast<const float4*>(Y2 + (int64_t)__ldg(dict + d0 + gt) * BP);
+                float v[BP];
+#pragma unroll
+                for (int c4 = 0; c4 < BP / 4; ++c4) {
+                    const float4 x = __ldg(src + c4);
+                    v[4 * c4] = x.x;
+                    v[4 * c4 + 1] = x.y;
+                    v[4 * c4 + 2] = x.z;
+                    v[4 * c4 + 3] = x.w;
+                }
+                uint4 w0, w1, w2;
+                digit_rows16(v, y2sc, w0, w1, w2);
+                *reinterpret_cast<uint4*>(bn + sp8_boff<NB>(gt, 0)) = w0;
+                *reinterpret_cast<uint4*>(bn + sp8_boff<NB>(gt, 1)) = w1;
+                *reinterpret_cast<uint4*>(bn + sp8_boff<NB>(gt, 2)) = w2;
+            }
+            fence_proxy_async();
+            mbar_arrive(&bn_full[a]);
+            if (i > 0) gram(i - 1);
+        }
+        if (nb > 0) gram(nb - 1);
+    }
+
+    // ---- CTA partial of the Grams (fixed warp order), then the last CTA sums them in CTA order
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256));
+    }
+    auto red = reinterpret_cast<double (*)[NCB * 8][NCB * 8 + 1]>(base);   // the image stages are free now
+    auto cred = reinterpret_cast<double (*)[NCB * 8]>(reinterpret_cast<double*>(base) + 4 * (NCB * 8) * (NCB * 8 + 1));
+    const int gw = warp - 6;
+    const int kr = lane & 3, cc = lane >> 2, fr = lane >> 2, fc = 2 * (lane & 3);
+    if (warp >= 6) {
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) {
+            double v = csum[c];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if (kr == 0) cred[gw][8 * c + cc] = v;
+        }
+        int pi = 0;
+#pragma unroll
+        for (int c = 0; c < NCB; ++c)
+#pragma unroll
+            for (int c2 = c; c2 < NCB; ++c2) {
+                red[gw][8 * c + fr][8 * c2 + fc] = gacc[pi][0];
+                red[gw][8 * c + fr][8 * c2 + fc + 1] = gacc[pi][1];
+                red[gw][8 * c2 + fc][8 * c + fr] = gacc[pi][0];
+                red[gw][8 * c2 + fc + 1][8 * c + fr] = gacc[pi][1];
+                ++pi;
+            }
+    }
+    __syncthreads();
+    double* pg = part + (int64_t)blockIdx.x * kGramPart;
+    for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
+        const int p = pq / BP, qq = pq % BP;
+        pg[pq] = red[0][p][qq] + red[1][p][qq] + red[2][p][qq] + red[3][p][qq];
+    }
+    for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
+        pg[2 * kMaxB * kMaxB + qq] = cred[0][qq] + cred[1][qq] + cred[2][qq] + cred[3][qq];
+    if constexpr (WITH_H) {
+        __syncthreads();
+        if (warp >= 6) {
+#pragma unroll
+            for (int c = 0; c < NCB; ++c)
+#pragma unroll
+                for (int c2 = 0; c2 < NCB; ++c2) {
+                    red[gw][8 * c + fr][8 * c2 + fc] = hacc[c * NCB + c2][0];
+                    red[gw][8 * c + fr][8 * c2 + fc + 1] = hacc[c * NCB + c2][1];
+                }
+        }
+        __syncthreads();
+        for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
+            const int p = pq / BP, qq = pq % BP;
+            pg[kMaxB * kMaxB + pq] = red[0][p][qq] + red[1][p][qq] + red[2][p][qq] + red[3][p][qq];
+        }
+    }
+    if (last_block_done(counter)) {
+        for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
+            cs[qq] = ordered_sum(part + 2 * kMaxB * kMaxB + qq, gridDim.x, kGramPart);
+        for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
+            G[pq] = ordered_sum(part + pq, gridDim.x, kGramPart);
+            if constexpr (WITH_H) H[pq] = ordered_sum(part + kMaxB * kMaxB + pq, gridDim.x, kGramPart);
+        }
+        if (threadIdx.x == 0) *counter = 0;
+    }
+}
+
+}  // namespace sbmds

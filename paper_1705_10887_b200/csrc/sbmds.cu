@@ -24,6 +24,7 @@
 #include "k_sparse.cuh"
 #include "k_blocked.cuh"
 #include "k_fused.cuh"
+#include "k_sp8.cuh"
 
 namespace sbmds {
 std::atomic<int64_t> g_launches{0};
@@ -174,6 +175,28 @@ struct DevBuf {
     }
     template <typename T>
     T* as() const { return reinterpret_cast<T*>(p); }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(bytes, o.bytes);
+        std::swap(pooled, o.pooled);
+    }
+};
+
+// Row-blocked index of S (k_blocked.cuh) for blocks of rb rows: dictionaries, 16-bit local
+// columns (CSR order), optional block-local CSC, and landmark -> dictionary-slot lists.
+struct BlkIdx {
+    DevBuf doff, dict, lcol, lcp, lrow, lval, jptr, jlist;
+    int rb = 0;
+    int64_t nblk = 0;
+    int32_t total_u = 0;
+    uint32_t umax = 0;
+    void reset() {
+        for (DevBuf* b : {&doff, &dict, &lcol, &lcp, &lrow, &lval, &jptr, &jlist}) b->release();
+        rb = 0;
+        nblk = 0;
+        total_u = 0;
+        umax = 0;
+    }
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
@@ -272,7 +295,13 @@ struct sbmds_ctx {
     int gram_tc = 1;       // Gram on the FP64 tensor cores (b <= 32)
     int csr_nnz_per_lane = 4;   // narrow CSR SpMM: nonzeros per lane when choosing lanes per row
     int csr_sub_L = 0;          // (tuning) force lanes per row
-    int fuse = 1;          // eigs: 1 = A5 fused with the Gram, 2 = also the next A2's S^T partials (k_fused.cuh)
+    int fuse = 3;          // eigs: 1 = A5 fused with the Gram, 2 = also the next A2's S^T partials (k_fused.cuh),
+                           // 3 = the tensor-core sparse step where it applies (k_sp8.cuh), else 1
+    // tensor-core sparse step (k_sp8.cuh): 128-row blocks, dense three-plane digit images of S_B
+    BlkIdx s8;
+    DevBuf s8img, s8ioff, s8esc;
+    int sp8_state = 0;     // 0 not built, 1 built, -1 not applicable (a dictionary > 128 entries)
+    int64_t s8_bytes = 0;
     // D_ll
     float* D = nullptr;
     int64_t ldD = 0;
@@ -722,7 +751,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     if (!pl.ok) build_pair_plan(h, pl, max_clusters[pi], C::S);
     // aux: [0] max |D| bits, [1] D exponent, [64..128) per-column max |Y1| bits, [128..192)
     // column exponents; [2] max |D| of the int8 packing, [3] its exponent
-    h->y16aux.ensure(192 * sizeof(unsigned int));
+    h->y16aux.ensure(256 * sizeof(unsigned int));   // + [192, 256): |Y2| column maxima
     unsigned int* dmax = h->y16aux.as<unsigned int>();
     int* dexp = reinterpret_cast<int*>(dmax + 1);
     unsigned int* ymax = dmax + 64;
@@ -747,7 +776,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_SPLIT, st, [&] {
         CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
         launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
-               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax);
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, dmax + 192);
         launch(k_y16_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
                lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y16T.as<__half>(), yexp);
     });
@@ -780,7 +809,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const int*)dexp,
                (const int*)yexp, wvec(h), h->Y2.as<float>(), h->tpart.as<double>(),
-               h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED);
+               h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED, dmax + 192);
     });
     h->last_dpath = 4;
     h->last_dbytes = pl.ntiles * (int64_t)128 * 128 * 4 + 12 * h->l * (int64_t)b;
@@ -799,7 +828,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     }
     const int64_t lpad = y1t_lpad(h);
     if (!pl.ok) build_pair_plan(h, pl, h->num_sms, C::S, C::GN, true);   // one CTA per SM, both roles
-    h->y16aux.ensure(192 * sizeof(unsigned int));
+    h->y16aux.ensure(256 * sizeof(unsigned int));   // + [192, 256): |Y2| column maxima
     unsigned int* aux = h->y16aux.as<unsigned int>();
     unsigned int* dmax8 = aux + 2;
     int* dexp8 = reinterpret_cast<int*>(aux + 3);
@@ -825,7 +854,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_SPLIT, st, [&] {
         CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
         launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
-               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax);
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, aux + 192);
         launch(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
                lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
     });
@@ -842,7 +871,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)nullptr, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
                wvec(h), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
-               h->counters.as<unsigned int>() + CNT_DRED);
+               h->counters.as<unsigned int>() + CNT_DRED, aux + 192);
     });
     h->last_dpath = 3;
     h->last_dbytes = pl.ntiles * (int64_t)C::A_BYTES + 12 * h->l * (int64_t)b;
@@ -1008,7 +1037,42 @@ void ensure_apply_ws(sbmds_ctx* h, int bp) {
 //   kApplyY1Ready: A2 comes from the S^T partials P1 the previous fused step wrote (k_blk_reduce)
 //   kApplyFused:   A5 runs as k_blk_spmm_fused, which also writes the next P1 (unless
 //                  kApplyNoP1) and G = Y^T Y, s = 1^T Y (and H' = Yprev^T Y when Yprev != NULL)
-constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4;
+//   kApplySp8:     (with kApplyFused) the tensor-core sparse step k_sp8_step instead, and the
+//                  partials of kApplyY1Ready are its 128-row-block slots
+constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8;
+
+bool ensure_sp8(sbmds_ctx* h, cudaStream_t st);
+
+bool sp8_ok(sbmds_ctx* h, int b, cudaStream_t st) {
+    return h->fuse == 3 && b == 16 && h->blocked && (h->use_blocked & 1) && ensure_sp8(h, st);
+}
+
+void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st) {
+    using C = Sp8Cfg<16>;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_sp8_step<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        CK(cudaFuncSetAttribute(k_sp8_step<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        attr = true;
+    }
+    h->y16aux.ensure(256 * sizeof(unsigned int));
+    unsigned int* y2max = h->y16aux.as<unsigned int>() + 192;
+    if (h->last_dpath != 3 && h->last_dpath != 4) {   // the full-D reductions do not form the maxima
+        CK(cudaMemsetAsync(y2max, 0, 64 * sizeof(unsigned int), st));
+        launch(k_colabsmax, dim3((unsigned)std::min<int64_t>(2 * 148, (h->l + 15) / 16)), dim3(256), 0, st, h->l, 16,
+               (const float*)h->Y2.as<float>(), y2max);
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->s8.nblk, h->num_sms));
+    h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
+    h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
+    auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
+    launch(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->s8.nblk, (const int8_t*)h->s8img.as<int8_t>(),
+           (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
+           (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const float*)h->Y2.as<float>(),
+           (const unsigned int*)y2max, (const double*)h->t.as<double>(), Y, want_p1 ? h->P1.as<float>() : nullptr,
+           Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
+           h->counters.as<unsigned int>() + CNT_GRAM);
+}
 
 bool fused_ok(const sbmds_ctx* h, int b) {
     return h->fuse && h->blocked && (h->use_blocked & 1) && (b == 4 || b == 8 || b == 16 || b == 32) &&
@@ -1068,9 +1132,11 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     // reduction when enabled: both are bound by the 64-B-per-nonzero gather traffic; inside
     // eigs the partials come from the previous fused step, leaving only the reduction)
     if (flags & kApplyY1Ready) {
+        const bool s8 = (flags & kApplySp8) != 0;
         auto go_r = [&](auto kern) {
             launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
-                   (const int32_t*)h->bjptr.as<int32_t>(), (const int32_t*)h->bjlist.as<int32_t>(),
+                   (const int32_t*)(s8 ? h->s8.jptr : h->bjptr).as<int32_t>(),
+                   (const int32_t*)(s8 ? h->s8.jlist : h->bjlist).as<int32_t>(),
                    (const float*)h->P1.as<float>(), wvec(h), (const double*)h->s.as<double>(),
                    h->Y1.as<float>());
         };
@@ -1111,7 +1177,9 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     dstream(h, b, bp, st, Rinv);
     // A5: Y = -1/2 (S Y2 - 1 t^T)
-    if (flags & kApplyFused) {
+    if ((flags & kApplyFused) && (flags & kApplySp8)) {
+        profiled(h->prof, PK_CSR, st, [&] { launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1), st); });
+    } else if (flags & kApplyFused) {
         const bool want_p1 = !(flags & kApplyNoP1);
         profiled(h->prof, PK_CSR, st, [&] {
             switch (b / 4) {
@@ -1143,13 +1211,14 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     }
 }
 
-// Row-blocked S (k_blocked.cuh): segmented stable sort of each 256-row block's entries by
-// column, unique -> per-block dictionary, 16-bit local columns (CSR order), the block-local
-// CSC (sorted order), and for each landmark its dictionary slots in block order.
-void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
+// Row-blocked S (k_blocked.cuh): segmented stable sort of each rb-row block's entries by
+// column, unique -> per-block dictionary, 16-bit local columns (CSR order), optionally the
+// block-local CSC (sorted order), and for each landmark its dictionary slots in block order.
+void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, BlkIdx& o, cudaStream_t st) {
     const int64_t n = h->n, l = h->l, nnz = h->nnz;
-    h->nblk = (n + kRB - 1) / kRB;
-    const int64_t nb = h->nblk;
+    o.rb = rb;
+    o.nblk = (n + rb - 1) / rb;
+    const int64_t nb = o.nblk;
     DevBuf off, scol, iota_perm, flag, incl, tmp, keys2;
     off.ensure((nb + 1) * sizeof(int32_t));
     scol.ensure(nnz * sizeof(int32_t));
@@ -1158,7 +1227,7 @@ void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
     incl.ensure(nnz * sizeof(int32_t));
     int32_t* iota = iota_perm.as<int32_t>();
     int32_t* perm = iota + nnz;
-    launch(k_blk_offsets, dim3((unsigned)std::min<int64_t>(1024, (nb + 256) / 256)), dim3(256), 0, st, n, nb,
+    launch(k_blk_offsets, dim3((unsigned)std::min<int64_t>(1024, (nb + 256) / 256)), dim3(256), 0, st, n, nb, rb,
            (const int32_t*)h->rp.as<int32_t>(), off.as<int32_t>());
     launch(k_iota, dim3(1024), dim3(256), 0, st, (int32_t)nnz, iota);
     size_t tb = 0;
@@ -1168,7 +1237,7 @@ void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
     CK(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb, h->col.as<int32_t>(), scol.as<int32_t>(), iota, perm,
                                                  (int)nnz, (int)nb, off.as<int32_t>(), off.as<int32_t>() + 1, st));
     g_launches.fetch_add(1);
-    launch(k_blk_flags, dim3(1024), dim3(256), 0, st, (int32_t)nnz, (const int32_t*)scol.as<int32_t>(),
+    launch(k_blk_flags, dim3(1024), dim3(256), 0, st, (int32_t)nnz, rb, (const int32_t*)scol.as<int32_t>(),
            (const int32_t*)perm, rowof, (const int32_t*)off.as<int32_t>(), flag.as<int32_t>());
     tb = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)nnz, st));
@@ -1179,29 +1248,33 @@ void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
     int32_t total_u = 0;
     CK(cudaMemcpyAsync(&total_u, incl.as<int32_t>() + nnz - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    h->total_u = total_u;
-    h->bdoff.ensure((nb + 1) * sizeof(int32_t));
-    h->bdict.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
-    h->blcp.ensure((total_u + 1) * sizeof(int32_t));
-    h->blcol.ensure(nnz * sizeof(uint16_t));
-    h->blrow.ensure(nnz * sizeof(uint8_t));
-    h->blval.ensure(nnz * sizeof(float));
-    h->bjptr.ensure((l + 1) * sizeof(int32_t));
-    h->bjlist.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
+    o.total_u = total_u;
+    o.doff.ensure((nb + 1) * sizeof(int32_t));
+    o.dict.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
+    o.lcol.ensure(nnz * sizeof(uint16_t));
+    if (want_csc) {
+        o.lcp.ensure((total_u + 1) * sizeof(int32_t));
+        o.lrow.ensure(nnz * sizeof(uint8_t));
+        o.lval.ensure(nnz * sizeof(float));
+    }
+    o.jptr.ensure((l + 1) * sizeof(int32_t));
+    o.jlist.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
     launch(k_blk_dictoff, dim3((unsigned)std::min<int64_t>(1024, (nb + 256) / 256)), dim3(256), 0, st, nb,
            (int32_t)nnz, (const int32_t*)off.as<int32_t>(), (const int32_t*)flag.as<int32_t>(),
-           (const int32_t*)incl.as<int32_t>(), total_u, h->bdoff.as<int32_t>());
-    launch(k_blk_scatter, dim3(1024), dim3(256), 0, st, (int32_t)nnz, (const int32_t*)scol.as<int32_t>(),
+           (const int32_t*)incl.as<int32_t>(), total_u, o.doff.as<int32_t>());
+    launch(k_blk_scatter, dim3(1024), dim3(256), 0, st, (int32_t)nnz, rb, (const int32_t*)scol.as<int32_t>(),
            (const int32_t*)perm, rowof, (const float*)h->val.as<float>(), (const int32_t*)flag.as<int32_t>(),
-           (const int32_t*)incl.as<int32_t>(), (const int32_t*)h->bdoff.as<int32_t>(), h->bdict.as<int32_t>(),
-           h->blcp.as<int32_t>(), h->blcol.as<uint16_t>(), h->blrow.as<uint8_t>(), h->blval.as<float>());
+           (const int32_t*)incl.as<int32_t>(), (const int32_t*)o.doff.as<int32_t>(), o.dict.as<int32_t>(),
+           want_csc ? o.lcp.as<int32_t>() : nullptr, o.lcol.as<uint16_t>(), want_csc ? o.lrow.as<uint8_t>() : nullptr,
+           want_csc ? o.lval.as<float>() : nullptr);
     const int32_t nnz32 = (int32_t)nnz;
-    CK(cudaMemcpyAsync(h->blcp.as<int32_t>() + total_u, &nnz32, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    if (want_csc)
+        CK(cudaMemcpyAsync(o.lcp.as<int32_t>() + total_u, &nnz32, sizeof(int32_t), cudaMemcpyHostToDevice, st));
     // largest dictionary (decides which block widths fit in shared memory)
     DevBuf um;
     um.ensure(sizeof(unsigned int));
     CK(cudaMemsetAsync(um.p, 0, sizeof(unsigned int), st));
-    launch(k_blk_umax, dim3(256), dim3(256), 0, st, nb, (const int32_t*)h->bdoff.as<int32_t>(), um.as<unsigned int>());
+    launch(k_blk_umax, dim3(256), dim3(256), 0, st, nb, (const int32_t*)o.doff.as<int32_t>(), um.as<unsigned int>());
     // landmark -> dictionary slots, ascending slot (= block) order: stable sort of (dict, slot)
     keys2.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
     DevBuf slot;
@@ -1210,22 +1283,85 @@ void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
     int end_bit = 1;
     while ((int64_t(1) << end_bit) <= l) ++end_bit;
     tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, h->bdict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
-                                       h->bjlist.as<int32_t>(), total_u, 0, end_bit, st));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, o.dict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
+                                       o.jlist.as<int32_t>(), total_u, 0, end_bit, st));
     DevBuf tmp3;
     tmp3.ensure(tb + 16);
-    CK(cub::DeviceRadixSort::SortPairs(tmp3.p, tb, h->bdict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
-                                       h->bjlist.as<int32_t>(), total_u, 0, end_bit, st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp3.p, tb, o.dict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
+                                       o.jlist.as<int32_t>(), total_u, 0, end_bit, st));
     g_launches.fetch_add(1);
     launch(k_col_ptr, dim3((unsigned)((l + 256) / 256)), dim3(256), 0, st, l, total_u,
-           (const int32_t*)keys2.as<int32_t>(), h->bjptr.as<int32_t>());
+           (const int32_t*)keys2.as<int32_t>(), o.jptr.as<int32_t>());
     unsigned int umax = 0;
     CK(cudaMemcpyAsync(&umax, um.p, sizeof umax, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    h->umax = umax;
+    o.umax = umax;
+}
+
+void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
+    BlkIdx o;
+    build_blk_index(h, rowof, kRB, true, o, st);
+    h->nblk = o.nblk;
+    h->total_u = o.total_u;
+    h->umax = o.umax;
+    h->bdoff.swap(o.doff);
+    h->bdict.swap(o.dict);
+    h->blcp.swap(o.lcp);
+    h->blcol.swap(o.lcol);
+    h->blrow.swap(o.lrow);
+    h->blval.swap(o.lval);
+    h->bjptr.swap(o.jptr);
+    h->bjlist.swap(o.jlist);
     // staging pays only when a staged landmark row is reused: mean uses per dictionary entry
     // >= 4 (config 4: ~40; random rows over wide column windows: ~1)
     h->blocked = (double)h->nnz >= 4.0 * (double)std::max<int32_t>(1, h->total_u);
+}
+
+// Tensor-core sparse step (k_sp8.cuh): 128-row blocks whose dictionaries all fit 128 entries,
+// S_B stored once as a dense three-plane digit image. Built at the first eigs that can use it
+// (the row index of every entry is re-expanded from the row pointers).
+bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
+    if (h->sp8_state != 0) return h->sp8_state > 0;
+    h->sp8_state = -1;
+    if (!h->blocked || h->nnz == 0) return false;
+    DevBuf rowof, bad;
+    rowof.ensure(h->nnz * sizeof(int32_t));
+    bad.ensure(sizeof(int));
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    launch(k_expand_rows, dim3(1024), dim3(256), 0, st, h->n, (const int32_t*)h->rp.as<int32_t>(),
+           (const int32_t*)h->col.as<int32_t>(), (const float*)h->val.as<float>(), h->l, rowof.as<int32_t>(),
+           bad.as<int>());
+    BlkIdx& o = h->s8;
+    build_blk_index(h, rowof.as<int32_t>(), kSp8RB, false, o, st);
+    if (o.umax > (uint32_t)kSp8DK) {   // a block touches more landmarks than one image holds
+        o.reset();
+        return false;
+    }
+    h->s8ioff.ensure((o.nblk + 1) * sizeof(int64_t));
+    DevBuf sizes, tmp;
+    sizes.ensure((o.nblk + 1) * sizeof(int64_t));
+    launch(k_sp8_sizes, dim3((unsigned)std::min<int64_t>(1024, (o.nblk + 255) / 256)), dim3(256), 0, st, o.nblk,
+           (const int32_t*)o.doff.as<int32_t>(), sizes.as<int64_t>());
+    CK(cudaMemsetAsync(sizes.as<int64_t>() + o.nblk, 0, sizeof(int64_t), st));
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, sizes.as<int64_t>(), h->s8ioff.as<int64_t>(), (int)(o.nblk + 1), st));
+    tmp.ensure(tb + 16);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, sizes.as<int64_t>(), h->s8ioff.as<int64_t>(), (int)(o.nblk + 1), st));
+    g_launches.fetch_add(1);
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, h->s8ioff.as<int64_t>() + o.nblk, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h->s8img.ensure((size_t)total + 64 * 1024);   // + slack: the T product's M = 128 rows read past a short image
+    CK(cudaMemsetAsync(h->s8img.p, 0, h->s8img.bytes, st));
+    h->s8esc.ensure(o.nblk * sizeof(int));
+    launch(k_sp8_build, dim3((unsigned)std::min<int64_t>(o.nblk, 32 * (int64_t)h->num_sms)), dim3(128), 0, st, h->n,
+           o.nblk, (const int32_t*)h->rp.as<int32_t>(), (const float*)h->val.as<float>(),
+           (const uint16_t*)o.lcol.as<uint16_t>(), (const int32_t*)o.doff.as<int32_t>(),
+           (const int64_t*)h->s8ioff.as<int64_t>(), h->s8img.as<int8_t>(), h->s8esc.as<int>());
+    o.lcol.release();   // only the images are read from now on
+    h->s8_bytes = total;
+    h->sp8_state = 1;
+    return true;
 }
 
 template <typename F>
@@ -1234,6 +1370,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
+                      &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
@@ -1687,13 +1824,18 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         int it = 0;
         bool converged = false;
         const bool fused = fused_ok(h, b) && blocked_ok(h, b, b, Yc, Yn);
+        const bool sp8 = fused && sp8_ok(h, b, st);   // tensor-core sparse step (fuse = 3)
         // one iteration's device work: Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1} (s = 1^T Y_k came from
         // the last Gram), the Grams, and at Rayleigh-Ritz steps the Jacobi solve (no host syncs)
         auto enqueue_iteration = [&](int itx, bool do_rr) {
-            if (fused) {
+            if (sp8) {
+                // A5 + Grams + the next apply's S^T Y_{k+1} partials on the int8 tensor cores (k_sp8.cuh)
+                const int fl = kApplyFused | kApplySp8 | (itx > 1 ? kApplyY1Ready : 0) | (itx == max_iters ? kApplyNoP1 : 0);
+                apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
+            } else if (fused) {
                 // A5 fused with G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, H' = Y_k^T Y_{k+1} (RR) and
                 // (fuse = 2) the next apply's S^T Y_{k+1} partials (k_fused.cuh)
-                const bool p1 = h->fuse >= 2;
+                const bool p1 = h->fuse == 2;
                 const int fl = kApplyFused | (p1 && itx > 1 ? kApplyY1Ready : 0) | (!p1 || itx == max_iters ? kApplyNoP1 : 0);
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
             } else {
@@ -1715,7 +1857,8 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         // captured once per buffer parity and replayed; the host only reads the convergence flag
         // between segments, exactly where the eager loop reads it. Off while kernels are profiled.
         const int R = std::max(1, h->rr_period);
-        const bool graphs = h->use_graph && h->prof.mask == 0 && !(fused && h->fuse >= 2) && R >= 2;
+        const bool graphs = h->use_graph && h->prof.mask == 0 && !(fused && h->fuse >= 2) && R >= 2;   // (the partial
+        // chains of fuse 2/3 depend on the iteration index: eager only)
         cudaGraphExec_t gexec[2] = {nullptr, nullptr};
         int64_t gnodes[2] = {0, 0};
         struct GraphGuard {
@@ -1898,7 +2041,7 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
             return fail(SBMDS_EINVAL, "csr_sub_L in {0 auto, 1, 2, 4, 8, 16, 32}");
         h->csr_sub_L = (int)value;
     } else if (!strcmp(key, "fuse")) {
-        if (value < 0 || value > 2) return fail(SBMDS_EINVAL, "fuse in {0, 1 Gram, 2 Gram + S^T}");
+        if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "fuse in {0, 1 Gram, 2 Gram + S^T, 3 tensor-core step}");
         h->fuse = (int)value;
     } else if (!strcmp(key, "pair_dbg")) {
         h->pair_dbg = (int)value;   // bit 0: wait-cycle instrumentation; bits 1..: experiment modes
@@ -1926,6 +2069,9 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
         *value = (int64_t)std::llround(h->pdbg_avg[key[9] == 'T'][site]);
     }
     else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
+    else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a
+    else if (!strcmp(key, "sp8_bytes")) *value = h->s8_bytes;           // its S images (HBM bytes per pass)
+    else if (!strcmp(key, "sp8_umax")) *value = h->sp8_state > 0 ? (int64_t)h->s8.umax : -1;
     else if (!strcmp(key, "csc_bytes")) *value = (int64_t)(h->cptr.bytes + h->ridx.bytes + h->cval.bytes);
     else if (!strcmp(key, "workspace_bytes"))
         *value = (int64_t)(h->Y1.bytes + h->Y2.bytes + h->P.bytes + h->X.bytes + h->Y.bytes + h->gpart.bytes);

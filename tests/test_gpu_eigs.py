@@ -192,3 +192,27 @@ def test_graph_replay_matches_eager(cfg):
     assert np.array_equal(out[1][0], out[0][0]) and np.array_equal(out[1][1], out[0][1])
     assert out[1][3]["iters"] == out[0][3]["iters"] == iters
     assert conv[3]["converged"] == 1
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_tensor_core_sparse_step(cfg):
+    """The eigs sparse step on the int8 tensor cores (k_sp8.cuh: A5 + Grams + next A2 from
+    dense 128-row digit images of S) computes the same iteration as the separate fp32 kernels:
+    eigenvalues, residuals and the Ritz subspace agree after a fixed number of iterations (the
+    24-bit fixed point of S and of the B operands perturbs products by <= ~2^-23 of the scaled
+    maxima), and the step is bitwise deterministic."""
+    p = configs.config(cfg)
+    it = 25 if cfg == 2 else 12
+    with handle(p) as h:
+        h.set_option("fuse", 0)
+        ref = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=3)
+        h.set_option("fuse", 3)
+        a = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=3)
+        assert h.stat("sp8_state") == 1 and h.stat("sp8_umax") <= 128
+        rep = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=3)
+    (la, Va, _, ia), (lb, Vb, _, ib) = a, ref
+    assert np.allclose(la, lb, rtol=1e-5), (la, lb)
+    # the degenerate leading torus pair is compared as a pair: the subspace of all m
+    assert O.principal_angle(Va, Vb) <= 1e-3
+    assert abs(ia["max_residual"] - ib["max_residual"]) <= 1e-3 * max(1.0, abs(ib["max_residual"])) + 1e-7
+    assert np.array_equal(la, rep[0]) and np.array_equal(Va, rep[1])
