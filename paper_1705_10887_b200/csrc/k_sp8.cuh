@@ -66,40 +66,51 @@ __host__ __device__ constexpr uint32_t idesc_i8_bmn(int M, int N, int a_mn) {
     return idesc_i8_s32acc(M, N, a_mn) | (1u << 16);   // B MN-major
 }
 
-// 2^e as a double (|e| <= 1022)
-__device__ __forceinline__ double pow2d(int e) { return __hiloint2double((1023 + e) << 20, 0); }
-
-// balanced base-256 digits of x (|x| <= 8,355,711), x = d0 2^16 + d1 2^8 + d2 (as digits3);
-// p_k holds digit k in its low byte (the upper bytes are don't-care)
-__device__ __forceinline__ void digits3_lo(int x, int& p0, int& p1, int& p2) {
-    p2 = x;
-    const int v1 = (x - ((x << 24) >> 24)) >> 8;
-    p1 = v1;
-    p0 = (v1 - ((v1 << 24) >> 24)) >> 8;
+// 2^e as two normal floats whose product is 2^e (|e| <= 252): x 2^e = (x f.x) f.y, exact
+// while the result is normal, no branches
+__device__ __forceinline__ float2 pow2f2(int e) {
+    const int e1 = e / 2, e2 = e - e / 2;
+    return make_float2(__int_as_float((127 + e1) << 23), __int_as_float((127 + e2) << 23));
 }
 
-// the low bytes of a, b, c, d as one little-endian word
-__device__ __forceinline__ uint32_t pack4_lo(int a, int b, int c, int d) {
-    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+// 2^e as a float, e clamped to the normal range (a column whose maximum is below 2^-105 keeps
+// fewer digits; nothing overflows)
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + max(-126, min(127, e))) << 23); }
+
+// byte k of a, b, c, d as one little-endian word
+template <int K>
+__device__ __forceinline__ uint32_t pack4_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    constexpr uint32_t sel = (uint32_t)K | ((4u + K) << 4);
+    return __byte_perm(__byte_perm(a, b, sel), __byte_perm(c, d, sel), 0x5410);
 }
 
-// digits of round(v_c 2^e_c) for 16 columns -> the three 16-byte plane rows of one K-row
-__device__ __forceinline__ void digit_rows16(const float (&v)[16], const double (&sc)[16], uint4& r0, uint4& r1,
+// Balanced base-256 digits of x = rint(v_c 2^e_c) (|x| <= 2^22 by the choice of e_c), for 16
+// columns, as the three 16-byte plane rows of one K-row: x = d0 2^16 + d1 2^8 + d2 (as digits3).
+// fmaf(v, 2^e, 1.5 2^23) rounds v 2^e to the nearest integer (ties to even, as __float2int_rn)
+// and leaves it in the low mantissa bits: with bits = that float's bits, d2 is byte 0 of bits,
+// d1 = byte 1 of x + 128 = byte 1 of bits + 128, d0 = byte 2 of x + 32896 (signed bytes).
+__device__ __forceinline__ void digit_rows16(const float (&v)[16], const float (&sc)[16], uint4& r0, uint4& r1,
                                              uint4& r2) {
-    int a0[16], a1[16], a2[16];
+    uint32_t b2[16], b1[16], b0[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) digits3_lo(__double2int_rn((double)v[c] * sc[c]), a0[c], a1[c], a2[c]);
-    r0 = make_uint4(pack4_lo(a0[0], a0[1], a0[2], a0[3]), pack4_lo(a0[4], a0[5], a0[6], a0[7]),
-                    pack4_lo(a0[8], a0[9], a0[10], a0[11]), pack4_lo(a0[12], a0[13], a0[14], a0[15]));
-    r1 = make_uint4(pack4_lo(a1[0], a1[1], a1[2], a1[3]), pack4_lo(a1[4], a1[5], a1[6], a1[7]),
-                    pack4_lo(a1[8], a1[9], a1[10], a1[11]), pack4_lo(a1[12], a1[13], a1[14], a1[15]));
-    r2 = make_uint4(pack4_lo(a2[0], a2[1], a2[2], a2[3]), pack4_lo(a2[4], a2[5], a2[6], a2[7]),
-                    pack4_lo(a2[8], a2[9], a2[10], a2[11]), pack4_lo(a2[12], a2[13], a2[14], a2[15]));
+    for (int c = 0; c < 16; ++c) {
+        const uint32_t bits = __float_as_uint(fmaf(v[c], sc[c], 12582912.0f));
+        b2[c] = bits;
+        b1[c] = bits + 128u;
+        b0[c] = bits + (32896u - 0x4B400000u);
+    }
+    r0 = make_uint4(pack4_byte<2>(b0[0], b0[1], b0[2], b0[3]), pack4_byte<2>(b0[4], b0[5], b0[6], b0[7]),
+                    pack4_byte<2>(b0[8], b0[9], b0[10], b0[11]), pack4_byte<2>(b0[12], b0[13], b0[14], b0[15]));
+    r1 = make_uint4(pack4_byte<1>(b1[0], b1[1], b1[2], b1[3]), pack4_byte<1>(b1[4], b1[5], b1[6], b1[7]),
+                    pack4_byte<1>(b1[8], b1[9], b1[10], b1[11]), pack4_byte<1>(b1[12], b1[13], b1[14], b1[15]));
+    r2 = make_uint4(pack4_byte<0>(b2[0], b2[1], b2[2], b2[3]), pack4_byte<0>(b2[4], b2[5], b2[6], b2[7]),
+                    pack4_byte<0>(b2[8], b2[9], b2[10], b2[11]), pack4_byte<0>(b2[12], b2[13], b2[14], b2[15]));
 }
 
-// exact c0 + c1/256 + c2/65536 of the three accumulator groups, times 2^16 (an integer)
-__device__ __forceinline__ long long acc3(int g0, int g1, int g2) {
-    return ((long long)g0 << 16) + (long long)(g1 * 256 + g2);
+// (c0 + c1/256 + c2/65536) 2^16 of the three accumulator groups, times 2^e = f.x f.y (fp32: two
+// roundings, like an fp32 accumulation)
+__device__ __forceinline__ float acc3f(int g0, int g1, int g2, float2 f) {
+    return fmaf(__int2float_rn(g0), 65536.0f * f.x, __int2float_rn(g1 * 256 + g2) * f.x) * f.y;
 }
 
 __device__ __forceinline__ void named_bar(int id, int count) {
@@ -165,6 +176,44 @@ __global__ void __launch_bounds__(256) k_colabsmax(int64_t l, int bp, const floa
     }
 }
 
+// Y2 -> its digit planes Yd[p][j][0..15] (p = 0, 1, 2: d0, d1, d2 of rint(Y2[j][c] 2^ey_c),
+// ey_c from the column maxima), once per apply: the step kernel copies dictionary rows of
+// these planes (16 bytes each) instead of digitising every landmark once per block it touches
+template <int BP>
+__global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2,
+                                                   const unsigned int* __restrict__ y2max, uint8_t* __restrict__ Yd) {
+    static_assert(BP == 16, "b = 16");
+    float sc[BP];
+#pragma unroll
+    for (int c = 0; c < BP; ++c) sc[c] = pow2f(i8_scale_exp(__uint_as_float(y2max[c])));
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < l; j += (int64_t)gridDim.x * blockDim.x) {
+        float v[BP];
+        const float4* src = reinterpret_cast<const float4*>(Y2 + j * BP);
+#pragma unroll
+        for (int c4 = 0; c4 < BP / 4; ++c4) {
+            const float4 x = src[c4];
+            v[4 * c4] = x.x;
+            v[4 * c4 + 1] = x.y;
+            v[4 * c4 + 2] = x.z;
+            v[4 * c4 + 3] = x.w;
+        }
+        uint4 w0, w1, w2;
+        digit_rows16(v, sc, w0, w1, w2);
+        reinterpret_cast<uint4*>(Yd)[j] = w0;
+        reinterpret_cast<uint4*>(Yd)[l + j] = w1;
+        reinterpret_cast<uint4*>(Yd)[2 * l + j] = w2;
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+// arrive on `bar` once this thread's earlier cp.async copies have landed (counts as one of the
+// barrier's expected arrivals)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // ------------------------------------------------------------------ the step kernel
 template <int BP>
 struct Sp8Cfg {
@@ -175,11 +224,12 @@ struct Sp8Cfg {
     static constexpr int BT = NB * kSp8RB;               // B of T: 128 rows x NB (MN-major)
     static constexpr int YR = kSp8RB * BP * 4;           // fp32 rows of a block
     static constexpr int OFF_BN = NS * IMG;
-    static constexpr int OFF_BT = OFF_BN + 2 * BN;
+    static constexpr int NBN = 4;                        // B_N ring (staged two blocks ahead)
+    static constexpr int OFF_BT = OFF_BN + NBN * BN;
     static constexpr int OFF_YR = OFF_BT + 2 * BT;
     static constexpr int OFF_YP = OFF_YR + 2 * YR;
     static constexpr int OFF_BAR = OFF_YP + 2 * YR;
-    static constexpr int SMEM = OFF_BAR + 1024 + 1024;   // + barriers, scales; + alignment slack
+    static constexpr int SMEM = OFF_BAR + 2048 + 1024;   // + barriers, scales; + alignment slack
     static constexpr int THREADS = 10 * 32;
     static constexpr int ACCN = 0, ACCT = 2 * NB;        // TMEM columns: N[2], T[2]
     static_assert(BP == 16, "the tensor-core sparse step is built for b = 16");
@@ -188,9 +238,9 @@ struct Sp8Cfg {
 
 template <int BP, bool WITH_H>
 __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
-    k_sp8_step(int64_t n, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
+    k_sp8_step(int64_t n, int64_t l_rows, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
                const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
-               const float* __restrict__ Y2, const unsigned int* __restrict__ y2max, const double* __restrict__ t,
+               const uint8_t* __restrict__ Yd, const unsigned int* __restrict__ y2max, const double* __restrict__ t,
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
                unsigned int* __restrict__ counter) {
@@ -204,8 +254,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
     uint64_t* full_img = bars;          // [3]
     uint64_t* empty_img = bars + 3;     // [3]
-    uint64_t* bn_full = bars + 6;       // [2]
-    uint64_t* bn_empty = bars + 8;
+    uint64_t* bn_full = bars + 30;      // [4]
+    uint64_t* bn_empty = bars + 34;     // [4]
     uint64_t* an_full = bars + 10;
     uint64_t* an_empty = bars + 12;
     uint64_t* bt_full = bars + 14;
@@ -216,10 +266,11 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* yr_empty = bars + 24;
     uint64_t* yp_full = bars + 26;
     uint64_t* yp_empty = bars + 28;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
-    int* ey2 = reinterpret_cast<int*>(bars + 32);          // [BP] scale exponents of Y2's columns
-    int* eyb = ey2 + BP;                                   // [2][BP] per-block exponents of Y_B
-    float* cmx = reinterpret_cast<float*>(eyb + 2 * BP);   // [2][4][BP] epilogue warps' column maxima
+    uint64_t* ey_full = bars + 38;      // [4] eyb[k % 4] written (A's threads c < BP)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
+    int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
+    int* eyb = ey2 + BP;                                   // [4][BP] per-block exponents of Y_B (ring)
+    float* cmx = reinterpret_cast<float*>(eyb + 4 * BP);   // [2][4][BP] epilogue warps' column maxima
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b0 = blockIdx.x * nblk / gridDim.x, b1 = (blockIdx.x + 1) * nblk / gridDim.x;
@@ -231,9 +282,12 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_init(&full_img[s], 1);
             mbar_init(&empty_img[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < C::NBN; ++a) {
             mbar_init(&bn_full[a], 128);
             mbar_init(&bn_empty[a], 1);
+            mbar_init(&ey_full[a], BP);
+        }
+        for (int a = 0; a < 2; ++a) {
             mbar_init(&an_full[a], 1);
             mbar_init(&an_empty[a], 128);
             mbar_init(&bt_full[a], 128);
@@ -331,10 +385,11 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             const uint32_t ph = (uint32_t)((i / 3) & 1), pa = (uint32_t)((i >> 1) & 1);
             const int dp = dpad_of(B);
             mbar_wait(&full_img[s], ph, 145 * 65536 + (i & 0xFFFF));
-            mbar_wait(&bn_full[a], pa, 146 * 65536 + (i & 0xFFFF));
+            mbar_wait(&bn_full[i % C::NBN], (uint32_t)((i / C::NBN) & 1), 146 * 65536 + (i & 0xFFFF));
             mbar_wait(&an_empty[a], pa ^ 1u, 147 * 65536 + (i & 0xFFFF));
+            fence_proxy_async();   // B_N arrived by cp.async (generic proxy) -> visible to the MMA (async proxy)
             tc_fence_after();
-            const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BN + a * C::BN);
+            const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BN + (i % C::NBN) * C::BN);
             const uint32_t d = tbase + (uint32_t)(C::ACCN + a * NB);
             const uint32_t plane = (uint32_t)(kSp8RB * dp);
             if (elect_one()) {
@@ -345,7 +400,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                     tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 4096 * j, 2048, 128), bd, id3n, 1u);
                 }
                 tc_commit(&an_full[a]);
-                tc_commit(&bn_empty[a]);
+                tc_commit(&bn_empty[i % C::NBN]);
                 if (!want_t) tc_commit(&empty_img[s]);
             }
             __syncwarp();
@@ -357,9 +412,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         const int q = warp & 3;
         const int r = 32 * q + lane;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-        double ht[BP];   // t / 2
+        float ht[BP];   // t / 2
 #pragma unroll
-        for (int c = 0; c < BP; ++c) ht[c] = 0.5 * t[c];
+        for (int c = 0; c < BP; ++c) ht[c] = (float)(0.5 * t[c]);
         auto load_acc = [&](uint32_t col, int (&g0)[BP], int (&g1)[BP], int (&g2)[BP]) {
 #pragma unroll
             for (int c0 = 0; c0 < BP; c0 += 8) {
@@ -369,40 +424,17 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             }
             tmem_wait_ld();
         };
-        // block metadata, one block ahead: (d0, du, eS) of the block whose T accumulator is next
-        int32_t t_d0 = 0, t_du = 0;
-        int t_eS = 0;
         int eS_cur = nb > 0 ? __ldg(escale + b0) : 0;
-        auto drain_t = [&](int i) {
-            const int a = i & 1;
-            const uint32_t pa = (uint32_t)((i >> 1) & 1);
-            mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
-            tc_fence_after();
-            int g0[BP], g1[BP], g2[BP];
-            load_acc((uint32_t)(C::ACCT + a * NB), g0, g1, g2);
-            tc_fence_before();
-            mbar_arrive(&at_empty[a]);
-            if (r < t_du) {
-                float out[BP];
-#pragma unroll
-                for (int c = 0; c < BP; ++c)
-                    out[c] = (float)((double)acc3(g0[c], g1[c], g2[c]) * pow2d(16 - t_eS - eyb[a * BP + c]));
-                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)(t_d0 + r) * BP);
-#pragma unroll
-                for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]);
-            }
-        };
         for (int i = 0; i < nb; ++i) {
             const int64_t B = b0 + i;
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
             const int rows = rows_of(B);
             const int eS = eS_cur;
-            const int32_t nd0 = __ldg(doff + B), ndu = __ldg(doff + B + 1) - nd0;   // for drain_t(i) next round
             if (i + 1 < nb) eS_cur = __ldg(escale + B + 1);
-            double sc[BP];   // 2^(16 - eS - ey2_c): acc3 -> S Y2
+            float2 sce[BP];   // accumulator 2^(16 - eS - ey2_c) -> S Y2
 #pragma unroll
-            for (int c = 0; c < BP; ++c) sc[c] = pow2d(16 - eS - ey2[c]);
+            for (int c = 0; c < BP; ++c) sce[c] = pow2f2(16 - eS - ey2[c]);
             mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             int g0[BP], g1[BP], g2[BP];
@@ -414,19 +446,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             const bool live = r < rows;
 #pragma unroll
             for (int c = 0; c < BP; ++c)
-                y[c] = live ? (float)fma(-0.5, (double)acc3(g0[c], g1[c], g2[c]) * sc[c], ht[c]) : 0.f;
-            if (live) {
-                float4* dst = reinterpret_cast<float4*>(Y + (B * kSp8RB + r) * BP);
-#pragma unroll
-                for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
-            }
-            mbar_wait(&yr_empty[a], pa ^ 1u, 150 * 65536 + (i & 0xFFFF));
-            {
-                float4* yr = reinterpret_cast<float4*>(base + C::OFF_YR + a * C::YR) + r * (BP / 4);
-#pragma unroll
-                for (int c = 0; c < BP; c += 4) yr[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
-            }
-            mbar_arrive(&yr_full[a]);
+                y[c] = live ? fmaf(-0.5f, acc3f(g0[c], g1[c], g2[c], sce[c]), ht[c]) : 0.f;
             if (want_t) {
                 // the block's column maxima (warp butterfly: lane ends with the maximum of column
                 // cl over its 32 rows), then per-column exponents ey (thread c < 16), then the
@@ -447,14 +467,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 const int cl = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
                 if ((lane & 1) == 0) cmx[(a * 4 + q) * BP + cl] = m[0];
                 named_bar(1, 128);
+                int* ey = eyb + (i & 3) * BP;
                 if (r < BP) {
                     const float* cm = cmx + a * 4 * BP;
-                    eyb[a * BP + r] = i8_scale_exp(fmaxf(fmaxf(cm[r], cm[BP + r]), fmaxf(cm[2 * BP + r], cm[3 * BP + r])));
+                    ey[r] = i8_scale_exp(fmaxf(fmaxf(cm[r], cm[BP + r]), fmaxf(cm[2 * BP + r], cm[3 * BP + r])));
                 }
                 named_bar(1, 128);
-                double ysc[BP];
+                if (r < BP) mbar_arrive(&ey_full[i & 3]);   // published for B's T drain of this block
+                float ysc[BP];
 #pragma unroll
-                for (int c = 0; c < BP; ++c) ysc[c] = pow2d(eyb[a * BP + c]);
+                for (int c = 0; c < BP; ++c) ysc[c] = pow2f(ey[c]);
                 uint4 w0, w1, w2;
                 digit_rows16(y, ysc, w0, w1, w2);
                 mbar_wait(&bt_empty[a], pa ^ 1u, 151 * 65536 + (i & 0xFFFF));
@@ -464,20 +486,55 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 2)) = w2;
                 fence_proxy_async();
                 mbar_arrive(&bt_full[a]);
-                if (i > 0) drain_t(i - 1);
-                t_d0 = nd0;
-                t_du = ndu;
-                t_eS = eS;
             }
+            // (after the digits, which gate the T product and the image's release)
+            if (live) {
+                float4* dst = reinterpret_cast<float4*>(Y + (B * kSp8RB + r) * BP);
+#pragma unroll
+                for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+            }
+            mbar_wait(&yr_empty[a], pa ^ 1u, 150 * 65536 + (i & 0xFFFF));
+            {
+                float4* yr = reinterpret_cast<float4*>(base + C::OFF_YR + a * C::YR) + r * (BP / 4);
+#pragma unroll
+                for (int c = 0; c < BP; c += 4) yr[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+            }
+            mbar_arrive(&yr_full[a]);
         }
-        if (want_t && nb > 0) drain_t(nb - 1);
     } else {
         // ------------------------------------------------ B operand of N, then the Gram of the previous block
-        const int gt = threadIdx.x - 192;   // 0..127
+        const int gt = threadIdx.x - 192;   // 0..127 (T accumulator: TMEM lane = dictionary entry gt)
         const int gw = warp - 6;            // 0..3
-        double y2sc[BP];                    // 2^ey2_c
+        const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+        // T accumulator of block i -> P1 partials, scaled by A's exponents of Y_B (ey ring of 4:
+        // A runs at most two blocks ahead of this group, so neither the ring slot nor the phase
+        // of ey_full can be reused before it is read); d0 / du / eS of that block are passed in
+        auto drain_t = [&](int i, int32_t d0, int32_t du, int eS) {
+            const int a = i & 1;
+            const uint32_t pa = (uint32_t)((i >> 1) & 1);
+            mbar_wait(&ey_full[i & 3], (uint32_t)((i >> 2) & 1), 155 * 65536 + (i & 0xFFFF));
+            mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
+            tc_fence_after();
+            int g0[BP], g1[BP], g2[BP];
 #pragma unroll
-        for (int c = 0; c < BP; ++c) y2sc[c] = pow2d(ey2[c]);
+            for (int c0 = 0; c0 < BP; c0 += 8) {
+                tmem_ld8_u(tbase + lane_off + C::ACCT + a * NB + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
+                tmem_ld8_u(tbase + lane_off + C::ACCT + a * NB + BP + c0, *reinterpret_cast<int(*)[8]>(&g1[c0]));
+                tmem_ld8_u(tbase + lane_off + C::ACCT + a * NB + 2 * BP + c0, *reinterpret_cast<int(*)[8]>(&g2[c0]));
+            }
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&at_empty[a]);
+            const int lrow = 32 * (warp & 3) + lane;   // the TMEM lane this thread drained
+            if (lrow < du) {
+                float out[BP];
+#pragma unroll
+                for (int c = 0; c < BP; ++c) out[c] = acc3f(g0[c], g1[c], g2[c], pow2f2(16 - eS - eyb[(i & 3) * BP + c]));
+                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)(d0 + lrow) * BP);
+#pragma unroll
+                for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]);
+            }
+        };
         const int kr = lane & 3, cc = lane >> 2;
         auto gram = [&](int i) {
             const int64_t B = b0 + i;
@@ -514,37 +571,43 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_arrive(&yr_empty[a]);
             if constexpr (WITH_H) mbar_arrive(&yp_empty[a]);
         };
-        for (int i = 0; i < nb; ++i) {
-            const int64_t B = b0 + i;
-            const int a = i & 1;
-            const uint32_t pa = (uint32_t)((i >> 1) & 1);
-            const int32_t d0 = __ldg(doff + B), du = __ldg(doff + B + 1) - d0;
-            mbar_wait(&bn_empty[a], pa ^ 1u, 154 * 65536 + (i & 0xFFFF));
-            uint8_t* bn = base + C::OFF_BN + a * C::BN;
-            // thread k: dictionary entry k, its Y2 row as four float4 loads (two dependent L2
-            // round trips per block), digits as three 16-byte plane rows
-            if (gt < du) {
-                const float4* src = reinterpret_cast<const float4*>(Y2 + (int64_t)__ldg(dict + d0 + gt) * BP);
-                float v[BP];
-#pragma unroll
-                for (int c4 = 0; c4 < BP / 4; ++c4) {
-                    const float4 x = __ldg(src + c4);
-                    v[4 * c4] = x.x;
-                    v[4 * c4 + 1] = x.y;
-                    v[4 * c4 + 2] = x.z;
-                    v[4 * c4 + 3] = x.w;
-                }
-                uint4 w0, w1, w2;
-                digit_rows16(v, y2sc, w0, w1, w2);
-                *reinterpret_cast<uint4*>(bn + sp8_boff<NB>(gt, 0)) = w0;
-                *reinterpret_cast<uint4*>(bn + sp8_boff<NB>(gt, 1)) = w1;
-                *reinterpret_cast<uint4*>(bn + sp8_boff<NB>(gt, 2)) = w2;
+        // B_N of block k: thread g copies dictionary entry g's three 16-byte digit rows
+        // asynchronously; bn_full completes when every thread's copies have landed. The
+        // dictionary index of the next block is loaded one staging ahead.
+        int32_t s_d0 = nb > 0 ? __ldg(doff + b0) : 0, s_du = nb > 0 ? __ldg(doff + b0 + 1) - s_d0 : 0;
+        int64_t s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
+        auto stage = [&](int k) {
+            const int64_t B = b0 + k;
+            const int32_t d0 = s_d0, du = s_du;
+            const int64_t j = s_j;
+            if (k + 1 < nb) {   // prefetch the next block's dictionary row of this thread
+                s_d0 = __ldg(doff + B + 1);
+                s_du = __ldg(doff + B + 2) - s_d0;
+                s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
             }
-            fence_proxy_async();
-            mbar_arrive(&bn_full[a]);
-            if (i > 0) gram(i - 1);
+            const int sb = k % C::NBN;
+            mbar_wait(&bn_empty[sb], ((uint32_t)((k / C::NBN) & 1)) ^ 1u, 154 * 65536 + (k & 0xFFFF));
+            uint8_t* bn = base + C::OFF_BN + sb * C::BN;
+            if (gt < du) {
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl) cp_async16(bn + sp8_boff<NB>(gt, pl), Yd + (pl * l_rows + j) * 16);
+            }
+            cp_async_arrive_noinc(&bn_full[sb]);
+        };
+        if (nb > 0) stage(0);
+        if (nb > 1) stage(1);
+        int32_t p_d0 = nb > 0 ? __ldg(doff + b0) : 0, p_du = nb > 0 ? __ldg(doff + b0 + 1) - p_d0 : 0;
+        int p_eS = nb > 0 ? __ldg(escale + b0) : 0;
+        for (int i = 0; i < nb; ++i) {
+            if (i + 2 < nb) stage(i + 2);
+            gram(i);
+            if (want_t) drain_t(i, p_d0, p_du, p_eS);
+            if (i + 1 < nb) {
+                p_d0 = __ldg(doff + b0 + i + 1);
+                p_du = __ldg(doff + b0 + i + 2) - p_d0;
+                p_eS = __ldg(escale + b0 + i + 1);
+            }
         }
-        if (nb > 0) gram(nb - 1);
     }
 
     // ---- CTA partial of the Grams (fixed warp order), then the last CTA sums them in CTA order

@@ -299,8 +299,9 @@ struct sbmds_ctx {
                            // 3 = the tensor-core sparse step where it applies (k_sp8.cuh), else 1
     // tensor-core sparse step (k_sp8.cuh): 128-row blocks, dense three-plane digit images of S_B
     BlkIdx s8;
-    DevBuf s8img, s8ioff, s8esc;
+    DevBuf s8img, s8ioff, s8esc, s8yd;
     int sp8_state = 0;     // 0 not built, 1 built, -1 not applicable (a dictionary > 128 entries)
+    int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product
     int64_t s8_bytes = 0;
     // D_ll
     float* D = nullptr;
@@ -1065,10 +1066,15 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->s8.nblk, h->num_sms));
     h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
     h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
+    // Y2's digit planes (one pass over l x 16), then the step
+    h->s8yd.ensure((size_t)3 * h->l * 16);
+    launch(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
+           (const float*)h->Y2.as<float>(), (const unsigned int*)y2max, h->s8yd.as<uint8_t>());
     auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
-    launch(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->s8.nblk, (const int8_t*)h->s8img.as<int8_t>(),
+    launch(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
+           (const int8_t*)h->s8img.as<int8_t>(),
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
-           (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const float*)h->Y2.as<float>(),
+           (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
            (const unsigned int*)y2max, (const double*)h->t.as<double>(), Y, want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
            h->counters.as<unsigned int>() + CNT_GRAM);
@@ -1178,7 +1184,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     dstream(h, b, bp, st, Rinv);
     // A5: Y = -1/2 (S Y2 - 1 t^T)
     if ((flags & kApplyFused) && (flags & kApplySp8)) {
-        profiled(h->prof, PK_CSR, st, [&] { launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1), st); });
+        profiled(h->prof, PK_CSR, st, [&] { launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1) && !(h->sp8_dbg & 1), st); });
     } else if (flags & kApplyFused) {
         const bool want_p1 = !(flags & kApplyNoP1);
         profiled(h->prof, PK_CSR, st, [&] {
@@ -1370,7 +1376,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc,
+                      &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
@@ -2040,6 +2046,8 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16 || value == 32))
             return fail(SBMDS_EINVAL, "csr_sub_L in {0 auto, 1, 2, 4, 8, 16, 32}");
         h->csr_sub_L = (int)value;
+    } else if (!strcmp(key, "sp8_dbg")) {
+        h->sp8_dbg = (int)value;
     } else if (!strcmp(key, "fuse")) {
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "fuse in {0, 1 Gram, 2 Gram + S^T, 3 tensor-core step}");
         h->fuse = (int)value;
