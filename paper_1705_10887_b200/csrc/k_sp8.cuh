@@ -69,9 +69,12 @@ __host__ __device__ constexpr uint32_t idesc_i8_bmn(int M, int N, int a_mn) {
 // 2^e as two normal floats whose product is 2^e (|e| <= 252): x 2^e = (x f.x) f.y, exact
 // while the result is normal, no branches
 __device__ __forceinline__ float2 pow2f2(int e) {
-    const int e1 = e / 2, e2 = e - e / 2;
+    const int e1 = e >> 1, e2 = e - e1;
     return make_float2(__int_as_float((127 + e1) << 23), __int_as_float((127 + e2) << 23));
 }
+
+// exact int -> float for |g| <= 2^22 without a conversion instruction (1.5 2^23 magic)
+__device__ __forceinline__ float i22_to_f(int g) { return __int_as_float(0x4B400000 + g) - 12582912.0f; }
 
 // 2^e as a float, e clamped to the normal range (a column whose maximum is below 2^-105 keeps
 // fewer digits; nothing overflows)
@@ -107,10 +110,11 @@ __device__ __forceinline__ void digit_rows16(const float (&v)[16], const float (
                     pack4_byte<0>(b2[8], b2[9], b2[10], b2[11]), pack4_byte<0>(b2[12], b2[13], b2[14], b2[15]));
 }
 
-// (c0 + c1/256 + c2/65536) 2^16 of the three accumulator groups, times 2^e = f.x f.y (fp32: two
-// roundings, like an fp32 accumulation)
+// (c0 + c1/256 + c2/65536) 2^16 of the three accumulator groups, times 2^e = f.x f.y (fp32,
+// like an fp32 accumulation). |c0| <= K 2^14 <= 2^21 and |c1| <= 2^22 (K <= 128) convert exactly
+// by the magic add; c2 (up to 3 2^21) takes the one conversion instruction.
 __device__ __forceinline__ float acc3f(int g0, int g1, int g2, float2 f) {
-    return fmaf(__int2float_rn(g0), 65536.0f * f.x, __int2float_rn(g1 * 256 + g2) * f.x) * f.y;
+    return fmaf(i22_to_f(g0), 65536.0f, fmaf(i22_to_f(g1), 256.0f, __int2float_rn(g2))) * f.x * f.y;
 }
 
 __device__ __forceinline__ void named_bar(int id, int count) {
@@ -229,11 +233,16 @@ struct Sp8Cfg {
     static constexpr int OFF_YR = OFF_BT + 2 * BT;
     static constexpr int OFF_YP = OFF_YR + 2 * YR;
     static constexpr int OFF_BAR = OFF_YP + 2 * YR;
-    static constexpr int SMEM = OFF_BAR + 2048 + 1024;   // + barriers, scales; + alignment slack
-    static constexpr int THREADS = 10 * 32;
-    static constexpr int ACCN = 0, ACCT = 2 * NB;        // TMEM columns: N[2], T[2]
+    static constexpr int MAXNB = 256;                    // blocks per CTA (per-CTA metadata table)
+    static constexpr int OFF_META = OFF_BAR + 2048;      // int64 ioff[256], int32 doff[257], int32 eS[256]
+    static constexpr int SMEM = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 16 + 1024;   // + alignment slack
+    static constexpr int THREADS = 12 * 32;   // 3 warps per scheduler (<= 168 registers)
+    static constexpr int NGW = 2;                        // Gram warps (group C)
+    // TMEM columns: N[2] (NB each), then T[2][4]: one T accumulator per 32-row K step, since
+    // each epilogue warp scales its own 32 rows of Y_B (no cross-warp reduction on the path)
+    static constexpr int ACCN = 0, ACCT = 2 * NB;
+    static_assert(ACCT + 8 * NB <= 512, "tmem");
     static_assert(BP == 16, "the tensor-core sparse step is built for b = 16");
-    static_assert(4 * NB <= 256, "tmem");
 };
 
 template <int BP, bool WITH_H>
@@ -243,8 +252,15 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                const uint8_t* __restrict__ Yd, const unsigned int* __restrict__ y2max, const double* __restrict__ t,
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
-               unsigned int* __restrict__ counter) {
+               unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int stream_only) {
     using C = Sp8Cfg<BP>;
+    // (diagnostics) trace[ev * 64 + i]: globaltimer of event ev for block i < 64 of CTA 0
+#define SP8_TR(ev, i)                                                                          \
+    if (trace && blockIdx.x == 0 && (i) < 64) {                                                \
+        unsigned long long t_;                                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                 \
+        trace[(ev) * 64 + (i)] = t_;                                                           \
+    }
     constexpr int NB = C::NB;
     constexpr int NCB = BP / 8;
     constexpr int NPG = NCB * (NCB + 1) / 2;
@@ -266,11 +282,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* yr_empty = bars + 24;
     uint64_t* yp_full = bars + 26;
     uint64_t* yp_empty = bars + 28;
-    uint64_t* ey_full = bars + 38;      // [4] eyb[k % 4] written (A's threads c < BP)
+    uint64_t* ey_full = bars + 38;      // [4] eyb[k % 4] written (lanes c < BP of the 4 epilogue warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
     int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
-    int* eyb = ey2 + BP;                                   // [4][BP] per-block exponents of Y_B (ring)
-    float* cmx = reinterpret_cast<float*>(eyb + 4 * BP);   // [2][4][BP] epilogue warps' column maxima
+    int* eyb = ey2 + BP;                                   // [4][4][BP] exponents of Y_B per block (ring) and warp
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b0 = blockIdx.x * nblk / gridDim.x, b1 = (blockIdx.x + 1) * nblk / gridDim.x;
@@ -285,7 +300,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         for (int a = 0; a < C::NBN; ++a) {
             mbar_init(&bn_full[a], 128);
             mbar_init(&bn_empty[a], 1);
-            mbar_init(&ey_full[a], BP);
+            mbar_init(&ey_full[a], 4 * BP);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&an_full[a], 1);
@@ -295,34 +310,45 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_init(&at_full[a], 1);
             mbar_init(&at_empty[a], 128);
             mbar_init(&yr_full[a], 128);
-            mbar_init(&yr_empty[a], 128);
-            mbar_init(&yp_full[a], 1);
-            mbar_init(&yp_empty[a], 128);
+            mbar_init(&yr_empty[a], 32 * C::NGW);
+            mbar_init(&yp_full[a], 32 * C::NGW);   // the Gram group's cp.async rows of Y_prev
         }
         fence_barrier_init();
     }
     if (threadIdx.x < BP) ey2[threadIdx.x] = i8_scale_exp(__uint_as_float(y2max[threadIdx.x]));
+    // the CTA's block metadata, once: no role waits on an L2 round trip per block
+    int64_t* m_ioff = reinterpret_cast<int64_t*>(base + C::OFF_META);
+    int32_t* m_doff = reinterpret_cast<int32_t*>(m_ioff + C::MAXNB);
+    int32_t* m_es = m_doff + C::MAXNB + 1;
+    for (int k = threadIdx.x; k <= nb; k += blockDim.x) {
+        m_doff[k] = __ldg(doff + b0 + k);
+        if (k < nb) {
+            m_ioff[k] = __ldg(ioff + b0 + k);
+            m_es[k] = __ldg(escale + b0 + k);
+        }
+    }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(256));
+                     "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
-    auto dpad_of = [&](int64_t B) { return sp8_dpad(__ldg(doff + B + 1) - __ldg(doff + B)); };
+    auto dpad_of = [&](int64_t B) { return sp8_dpad(m_doff[B - b0 + 1] - m_doff[B - b0]); };
     auto rows_of = [&](int64_t B) {
         const int64_t r0 = B * kSp8RB;
         return (int)((n - r0) < kSp8RB ? (n - r0) : kSp8RB);
     };
 
-    // Gram accumulators live in warps 6-9 (per-warp DMMA fragments, as k_fused.cuh)
-    double gacc[NPG][2], hacc[NPH][2], csum[NCB];
+    // Gram accumulators live in warps 10-11 (per-warp DMMA fragments, as k_fused.cuh)
+    // two interleaved accumulator sets (even / odd 4-row steps) halve the DMMA dependency chains
+    double gacc[NPG][2], hacc[NPH][2], csum[NCB], gacc1[NPG][2], hacc1[NPH][2];
 #pragma unroll
-    for (int i = 0; i < NPG; ++i) gacc[i][0] = gacc[i][1] = 0.0;
+    for (int i = 0; i < NPG; ++i) gacc[i][0] = gacc[i][1] = gacc1[i][0] = gacc1[i][1] = 0.0;
 #pragma unroll
-    for (int i = 0; i < NPH; ++i) hacc[i][0] = hacc[i][1] = 0.0;
+    for (int i = 0; i < NPH; ++i) hacc[i][0] = hacc[i][1] = hacc1[i][0] = hacc1[i][1] = 0.0;
 #pragma unroll
     for (int c = 0; c < NCB; ++c) csum[c] = 0.0;
 
@@ -335,18 +361,21 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 const uint32_t ph = (uint32_t)((i / 3) & 1);
                 const uint32_t bytes = (uint32_t)(3 * kSp8RB * dpad_of(B));
                 mbar_wait(&empty_img[s], ph ^ 1u, 141 * 65536 + (i & 0xFFFF));
+                SP8_TR(8, i);
                 mbar_arrive_expect_tx(&full_img[s], bytes);
-                bulk_load(base + s * C::IMG, gimg + __ldg(ioff + B), bytes, &full_img[s]);
-                if constexpr (WITH_H) {
-                    const int a = i & 1;
-                    const uint32_t pa = (uint32_t)((i >> 1) & 1);
-                    const uint32_t yb = (uint32_t)(rows_of(B) * BP * 4);
-                    mbar_wait(&yp_empty[a], pa ^ 1u, 142 * 65536 + (i & 0xFFFF));
-                    mbar_arrive_expect_tx(&yp_full[a], yb);
-                    bulk_load(base + C::OFF_YP + a * C::YR, Yprev + B * kSp8RB * BP, yb, &yp_full[a]);
-                }
+                bulk_load(base + s * C::IMG, gimg + m_ioff[i], bytes, &full_img[s]);
+                SP8_TR(0, i);
             }
         }
+    } else if (warp == 1 && stream_only) {
+        // (diagnostics) consume the images without any MMA; the other roles idle
+        for (int i = 0; i < nb; ++i) {
+            mbar_wait(&full_img[i % 3], (uint32_t)((i / 3) & 1), 156 * 65536 + (i & 0xFFFF));
+            if (lane == 0) SP8_TR(1, i);
+            if (elect_one()) mbar_arrive(&empty_img[i % 3]);
+            __syncwarp();
+        }
+    } else if (stream_only) {
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issue: N(i), then T(i - 1)
         constexpr uint32_t id1n = idesc_i8_bmn(128, NB, 0), id2n = idesc_i8_bmn(128, 2 * BP, 0),
@@ -354,22 +383,31 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         constexpr uint32_t id1t = idesc_i8_bmn(128, NB, 1), id2t = idesc_i8_bmn(128, 2 * BP, 1),
                            id3t = idesc_i8_bmn(128, BP, 1);
         constexpr uint32_t KG = NB / 16 * 128;   // B: bytes per 8-row K group (the LBO)
+        // Both products are issued as soon as their operands are ready (polled, non-blocking):
+        // T(i) does not wait behind N(i + 1), so an image stage is released as early as possible.
+        auto ready_t = [&](int i) {
+            const uint32_t pa = (uint32_t)((i >> 1) & 1);
+            return mbar_test(&bt_full[i & 1], pa) && mbar_test(&at_empty[i & 1], pa ^ 1u);
+        };
+        auto ready_n = [&](int i) {
+            const uint32_t ph = (uint32_t)((i / 3) & 1), pa = (uint32_t)((i >> 1) & 1);
+            return mbar_test(&full_img[i % 3], ph) && mbar_test(&bn_full[i % C::NBN], (uint32_t)((i / C::NBN) & 1)) &&
+                   mbar_test(&an_empty[i & 1], pa ^ 1u);
+        };
         auto issue_t = [&](int i) {
             const int64_t B = b0 + i;
             const int s = i % 3, a = i & 1;
-            const uint32_t pa = (uint32_t)((i >> 1) & 1);
             const int dp = dpad_of(B);
-            mbar_wait(&bt_full[a], pa, 143 * 65536 + (i & 0xFFFF));
-            mbar_wait(&at_empty[a], pa ^ 1u, 144 * 65536 + (i & 0xFFFF));
             tc_fence_after();
+            if (lane == 0) SP8_TR(2, i);
             const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BT + a * C::BT);
-            const uint32_t d = tbase + (uint32_t)(C::ACCT + a * NB);
             const uint32_t plane = (uint32_t)(kSp8RB * dp);
             if (elect_one()) {
 #pragma unroll
-                for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows per MMA
+                for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue warp j's) per MMA
+                    const uint32_t d = tbase + (uint32_t)(C::ACCT + (4 * a + j) * NB);
                     const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
-                    tc_mma_i8(d, umma_desc_none(sa + 512 * j, 128, 2048), bd, id1t, j > 0 ? 1u : 0u);
+                    tc_mma_i8(d, umma_desc_none(sa + 512 * j, 128, 2048), bd, id1t, 0u);
                     tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
                     tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
                 }
@@ -378,17 +416,15 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 tc_commit(&empty_img[s]);
             }
             __syncwarp();
+            if (lane == 0) SP8_TR(10, i);
         };
-        for (int i = 0; i < nb; ++i) {
+        auto issue_n = [&](int i) {
             const int64_t B = b0 + i;
             const int s = i % 3, a = i & 1;
-            const uint32_t ph = (uint32_t)((i / 3) & 1), pa = (uint32_t)((i >> 1) & 1);
             const int dp = dpad_of(B);
-            mbar_wait(&full_img[s], ph, 145 * 65536 + (i & 0xFFFF));
-            mbar_wait(&bn_full[i % C::NBN], (uint32_t)((i / C::NBN) & 1), 146 * 65536 + (i & 0xFFFF));
-            mbar_wait(&an_empty[a], pa ^ 1u, 147 * 65536 + (i & 0xFFFF));
             fence_proxy_async();   // B_N arrived by cp.async (generic proxy) -> visible to the MMA (async proxy)
             tc_fence_after();
+            if (lane == 0) SP8_TR(1, i);
             const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BN + (i % C::NBN) * C::BN);
             const uint32_t d = tbase + (uint32_t)(C::ACCN + a * NB);
             const uint32_t plane = (uint32_t)(kSp8RB * dp);
@@ -404,9 +440,27 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 if (!want_t) tc_commit(&empty_img[s]);
             }
             __syncwarp();
-            if (want_t && i > 0) issue_t(i - 1);
+        };
+        int nN = 0, nT = 0;
+        const int nt_total = want_t ? nb : 0;
+        uint64_t t_start;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        for (uint32_t spin = 0; nN < nb || nT < nt_total; ++spin) {
+            // (warp-uniform: every lane tests the same barriers)
+            if (nT < nN && nT < nt_total && __all_sync(0xffffffffu, ready_t(nT))) {
+                issue_t(nT++);
+                spin = 0;
+            } else if (nN < nb && __all_sync(0xffffffffu, ready_n(nN))) {
+                issue_n(nN++);
+                spin = 0;
+            } else if ((spin & 4095u) == 4095u) {   // watchdog, as mbar_wait
+                uint64_t t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t_start > 4000000000ull)
+                    mbar_hang(nT < nN ? &bt_full[nT & 1] : &full_img[nN % 3], 0, 145 * 65536 + (nN & 0xFF) * 256 + (nT & 0xFF));
+            }
+            if (spin == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         }
-        if (want_t && nb > 0) issue_t(nb - 1);
     } else if (warp < 6) {
         // ------------------------------------------------ epilogue (TMEM lane = row / dictionary entry)
         const int q = warp & 3;
@@ -424,19 +478,18 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             }
             tmem_wait_ld();
         };
-        int eS_cur = nb > 0 ? __ldg(escale + b0) : 0;
         for (int i = 0; i < nb; ++i) {
             const int64_t B = b0 + i;
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
             const int rows = rows_of(B);
-            const int eS = eS_cur;
-            if (i + 1 < nb) eS_cur = __ldg(escale + B + 1);
+            const int eS = m_es[i];
             float2 sce[BP];   // accumulator 2^(16 - eS - ey2_c) -> S Y2
 #pragma unroll
             for (int c = 0; c < BP; ++c) sce[c] = pow2f2(16 - eS - ey2[c]);
             mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
             tc_fence_after();
+            if (r == 0) SP8_TR(3, i);
             int g0[BP], g1[BP], g2[BP];
             load_acc((uint32_t)(C::ACCN + a * NB), g0, g1, g2);
             tc_fence_before();
@@ -448,9 +501,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             for (int c = 0; c < BP; ++c)
                 y[c] = live ? fmaf(-0.5f, acc3f(g0[c], g1[c], g2[c], sce[c]), ht[c]) : 0.f;
             if (want_t) {
-                // the block's column maxima (warp butterfly: lane ends with the maximum of column
-                // cl over its 32 rows), then per-column exponents ey (thread c < 16), then the
-                // digits of Y_B as the B operand of T
+                // this warp's column maxima over its 32 rows (butterfly reduce-scatter: lane ends
+                // with column cl, then an all-gather of the exponents), the per-warp exponents ey
+                // (K step q of the T product has its own accumulator), the digits of Y_B
                 float m[BP];
 #pragma unroll
                 for (int c = 0; c < BP; ++c) m[c] = fabsf(y[c]);
@@ -465,15 +518,15 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 }
                 m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 1));
                 const int cl = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-                if ((lane & 1) == 0) cmx[(a * 4 + q) * BP + cl] = m[0];
-                named_bar(1, 128);
-                int* ey = eyb + (i & 3) * BP;
-                if (r < BP) {
-                    const float* cm = cmx + a * 4 * BP;
-                    ey[r] = i8_scale_exp(fmaxf(fmaxf(cm[r], cm[BP + r]), fmaxf(cm[2 * BP + r], cm[3 * BP + r])));
+                const int my_e = i8_scale_exp(m[0]);   // exponent of column cl
+                int ey[BP];
+#pragma unroll
+                for (int c = 0; c < BP; ++c)   // lane holding column c: bits 4..1 = c's bits 3..0
+                    ey[c] = __shfl_sync(0xffffffffu, my_e, ((c >> 3) & 1) << 4 | ((c >> 2) & 1) << 3 | ((c >> 1) & 1) << 2 | (c & 1) << 1);
+                if ((lane & 1) == 0) {   // published for group B's T drain of this block
+                    eyb[((i & 3) * 4 + q) * BP + cl] = my_e;
+                    mbar_arrive(&ey_full[i & 3]);
                 }
-                named_bar(1, 128);
-                if (r < BP) mbar_arrive(&ey_full[i & 3]);   // published for B's T drain of this block
                 float ysc[BP];
 #pragma unroll
                 for (int c = 0; c < BP; ++c) ysc[c] = pow2f(ey[c]);
@@ -486,6 +539,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 2)) = w2;
                 fence_proxy_async();
                 mbar_arrive(&bt_full[a]);
+                if (r == 0) SP8_TR(4, i);
             }
             // (after the digits, which gate the T product and the image's release)
             if (live) {
@@ -501,10 +555,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             }
             mbar_arrive(&yr_full[a]);
         }
-    } else {
-        // ------------------------------------------------ B operand of N, then the Gram of the previous block
+    } else if (warp < 10) {
+        // ------------------------------------------------ group B (warps 6-9): B operand of N, T accumulator -> P1
         const int gt = threadIdx.x - 192;   // 0..127 (T accumulator: TMEM lane = dictionary entry gt)
-        const int gw = warp - 6;            // 0..3
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
         // T accumulator of block i -> P1 partials, scaled by A's exponents of Y_B (ey ring of 4:
         // A runs at most two blocks ahead of this group, so neither the ring slot nor the phase
@@ -515,26 +568,75 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_wait(&ey_full[i & 3], (uint32_t)((i >> 2) & 1), 155 * 65536 + (i & 0xFFFF));
             mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
             tc_fence_after();
-            int g0[BP], g1[BP], g2[BP];
+            const int lrow = 32 * (warp & 3) + lane;   // the TMEM lane (dictionary entry) this thread drains
+            float out[BP];
 #pragma unroll
-            for (int c0 = 0; c0 < BP; c0 += 8) {
-                tmem_ld8_u(tbase + lane_off + C::ACCT + a * NB + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
-                tmem_ld8_u(tbase + lane_off + C::ACCT + a * NB + BP + c0, *reinterpret_cast<int(*)[8]>(&g1[c0]));
-                tmem_ld8_u(tbase + lane_off + C::ACCT + a * NB + 2 * BP + c0, *reinterpret_cast<int(*)[8]>(&g2[c0]));
+            for (int c = 0; c < BP; ++c) out[c] = 0.f;
+#pragma unroll 1
+            for (int j = 0; j < 4; ++j) {   // K step j = rows of epilogue warp j, with its own exponents
+                int g0[BP], g1[BP], g2[BP];
+                const uint32_t col = (uint32_t)(C::ACCT + (4 * a + j) * NB);
+#pragma unroll
+                for (int c0 = 0; c0 < BP; c0 += 8) {
+                    tmem_ld8_u(tbase + lane_off + col + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
+                    tmem_ld8_u(tbase + lane_off + col + BP + c0, *reinterpret_cast<int(*)[8]>(&g1[c0]));
+                    tmem_ld8_u(tbase + lane_off + col + 2 * BP + c0, *reinterpret_cast<int(*)[8]>(&g2[c0]));
+                }
+                tmem_wait_ld();
+                const int* ey = eyb + ((i & 3) * 4 + j) * BP;
+#pragma unroll
+                for (int c = 0; c < BP; ++c) out[c] += acc3f(g0[c], g1[c], g2[c], pow2f2(16 - eS - ey[c]));
             }
-            tmem_wait_ld();
             tc_fence_before();
             mbar_arrive(&at_empty[a]);
-            const int lrow = 32 * (warp & 3) + lane;   // the TMEM lane this thread drained
             if (lrow < du) {
-                float out[BP];
-#pragma unroll
-                for (int c = 0; c < BP; ++c) out[c] = acc3f(g0[c], g1[c], g2[c], pow2f2(16 - eS - eyb[(i & 3) * BP + c]));
                 float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)(d0 + lrow) * BP);
 #pragma unroll
                 for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]);
             }
         };
+        // B_N of block k: thread g copies dictionary entry g's three 16-byte digit rows
+        // asynchronously; bn_full completes when every thread's copies have landed. The
+        // dictionary index of the next block is loaded one staging ahead.
+        int32_t s_d0 = m_doff[0], s_du = nb > 0 ? m_doff[1] - s_d0 : 0;
+        int64_t s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
+        auto stage = [&](int k) {
+            const int64_t B = b0 + k;
+            const int32_t d0 = s_d0, du = s_du;
+            const int64_t j = s_j;
+            if (k + 1 < nb) {   // prefetch the next block's dictionary row of this thread
+                s_d0 = m_doff[k + 1];
+                s_du = m_doff[k + 2] - s_d0;
+                s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
+            }
+            const int sb = k % C::NBN;
+            mbar_wait(&bn_empty[sb], ((uint32_t)((k / C::NBN) & 1)) ^ 1u, 154 * 65536 + (k & 0xFFFF));
+            uint8_t* bn = base + C::OFF_BN + sb * C::BN;
+            if (gt < du) {
+#pragma unroll
+                for (int pl = 0; pl < 3; ++pl) cp_async16(bn + sp8_boff<NB>(gt, pl), Yd + (pl * l_rows + j) * 16);
+            }
+            cp_async_arrive_noinc(&bn_full[sb]);
+            if (gt == 0) SP8_TR(7, k);
+        };
+        if (nb > 0) stage(0);
+        if (nb > 1) stage(1);
+        int32_t p_d0 = m_doff[0], p_du = nb > 0 ? m_doff[1] - p_d0 : 0;
+        int p_eS = nb > 0 ? m_es[0] : 0;
+        for (int i = 0; i < nb; ++i) {
+            if (i + 2 < nb) stage(i + 2);
+            if (want_t) drain_t(i, p_d0, p_du, p_eS);
+            if (gt == 0) SP8_TR(6, i);
+            if (i + 1 < nb) {
+                p_d0 = m_doff[i + 1];
+                p_du = m_doff[i + 2] - p_d0;
+                p_eS = m_es[i + 1];
+            }
+        }
+    } else {
+        // ------------------------------------------------ group C (warps 10-11): the Grams on the FP64 tensor cores
+        const int gt = threadIdx.x - 320;   // 0..63: rows gt, gt + 64 of Y_prev this thread stages
+        const int gw = warp - 10;           // 0..1
         const int kr = lane & 3, cc = lane >> 2;
         auto gram = [&](int i) {
             const int64_t B = b0 + i;
@@ -545,9 +647,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             if constexpr (WITH_H) mbar_wait(&yp_full[a], pa, 153 * 65536 + (i & 0xFFFF));
             const float* yr = reinterpret_cast<const float*>(base + C::OFF_YR + a * C::YR);
             const float* yp = reinterpret_cast<const float*>(base + C::OFF_YP + a * C::YR);
-#pragma unroll 2
-            for (int s4 = 0; s4 < 8; ++s4) {
-                const int rr = 32 * gw + 4 * s4 + kr;
+            auto step = [&](int s4, double (&ga)[NPG][2], double (&ha)[NPH][2]) {
+                const int rr = 64 * gw + 4 * s4 + kr;
                 double yv[NCB], xv[NCB];
 #pragma unroll
                 for (int c = 0; c < NCB; ++c) {
@@ -560,68 +661,74 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
 #pragma unroll
                 for (int c = 0; c < NCB; ++c)
 #pragma unroll
-                    for (int c2 = c; c2 < NCB; ++c2) dmma_8x8x4(gacc[pi++], yv[c], yv[c2]);
+                    for (int c2 = c; c2 < NCB; ++c2) dmma_8x8x4(ga[pi++], yv[c], yv[c2]);
                 if constexpr (WITH_H) {
 #pragma unroll
                     for (int c = 0; c < NCB; ++c)
 #pragma unroll
-                        for (int c2 = 0; c2 < NCB; ++c2) dmma_8x8x4(hacc[c * NCB + c2], xv[c], yv[c2]);
+                        for (int c2 = 0; c2 < NCB; ++c2) dmma_8x8x4(ha[c * NCB + c2], xv[c], yv[c2]);
                 }
+            };
+#pragma unroll 2
+            for (int s4 = 0; s4 < 16; s4 += 2) {
+                step(s4, gacc, hacc);
+                step(s4 + 1, gacc1, hacc1);
             }
             mbar_arrive(&yr_empty[a]);
-            if constexpr (WITH_H) mbar_arrive(&yp_empty[a]);
         };
-        // B_N of block k: thread g copies dictionary entry g's three 16-byte digit rows
-        // asynchronously; bn_full completes when every thread's copies have landed. The
-        // dictionary index of the next block is loaded one staging ahead.
-        int32_t s_d0 = nb > 0 ? __ldg(doff + b0) : 0, s_du = nb > 0 ? __ldg(doff + b0 + 1) - s_d0 : 0;
-        int64_t s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
-        auto stage = [&](int k) {
-            const int64_t B = b0 + k;
-            const int32_t d0 = s_d0, du = s_du;
-            const int64_t j = s_j;
-            if (k + 1 < nb) {   // prefetch the next block's dictionary row of this thread
-                s_d0 = __ldg(doff + B + 1);
-                s_du = __ldg(doff + B + 2) - s_d0;
-                s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
-            }
-            const int sb = k % C::NBN;
-            mbar_wait(&bn_empty[sb], ((uint32_t)((k / C::NBN) & 1)) ^ 1u, 154 * 65536 + (k & 0xFFFF));
-            uint8_t* bn = base + C::OFF_BN + sb * C::BN;
-            if (gt < du) {
+        // Y_prev rows of block k (Rayleigh-Ritz steps) -> yp[k & 1], cp.async, thread g = row g
+        auto stage_yp = [&](int k) {
+            if constexpr (WITH_H) {
+                const int64_t B = b0 + k;
+                uint8_t* yp = base + C::OFF_YP + (k & 1) * C::YR;
+                const int rows = rows_of(B);
 #pragma unroll
-                for (int pl = 0; pl < 3; ++pl) cp_async16(bn + sp8_boff<NB>(gt, pl), Yd + (pl * l_rows + j) * 16);
+                for (int h = 0; h < 2; ++h) {
+                    const int rr = gt + 64 * h;
+                    if (rr < rows) {
+                        const uint8_t* src = reinterpret_cast<const uint8_t*>(Yprev + (B * kSp8RB + rr) * BP);
+#pragma unroll
+                        for (int u = 0; u < BP / 4; ++u) cp_async16(yp + rr * BP * 4 + 16 * u, src + 16 * u);
+                    }
+                }
+                cp_async_arrive_noinc(&yp_full[k & 1]);
             }
-            cp_async_arrive_noinc(&bn_full[sb]);
         };
-        if (nb > 0) stage(0);
-        if (nb > 1) stage(1);
-        int32_t p_d0 = nb > 0 ? __ldg(doff + b0) : 0, p_du = nb > 0 ? __ldg(doff + b0 + 1) - p_d0 : 0;
-        int p_eS = nb > 0 ? __ldg(escale + b0) : 0;
+        stage_yp(0);
+        if (nb > 1) stage_yp(1);
         for (int i = 0; i < nb; ++i) {
-            if (i + 2 < nb) stage(i + 2);
             gram(i);
-            if (want_t) drain_t(i, p_d0, p_du, p_eS);
-            if (i + 1 < nb) {
-                p_d0 = __ldg(doff + b0 + i + 1);
-                p_du = __ldg(doff + b0 + i + 2) - p_d0;
-                p_eS = __ldg(escale + b0 + i + 1);
+            if (gt == 0) SP8_TR(5, i);
+            if (WITH_H && i + 2 < nb) {
+                named_bar(2, 32 * C::NGW);   // every row of yp[i & 1] has been read by gram(i)
+                stage_yp(i + 2);
             }
         }
     }
 
+#undef SP8_TR
     // ---- CTA partial of the Grams (fixed warp order), then the last CTA sums them in CTA order
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
     }
     auto red = reinterpret_cast<double (*)[NCB * 8][NCB * 8 + 1]>(base);   // the image stages are free now
     auto cred = reinterpret_cast<double (*)[NCB * 8]>(reinterpret_cast<double*>(base) + 4 * (NCB * 8) * (NCB * 8 + 1));
-    const int gw = warp - 6;
+    const int gw = warp - 10;
     const int kr = lane & 3, cc = lane >> 2, fr = lane >> 2, fc = 2 * (lane & 3);
-    if (warp >= 6) {
+#pragma unroll
+    for (int i = 0; i < NPG; ++i) {
+        gacc[i][0] += gacc1[i][0];
+        gacc[i][1] += gacc1[i][1];
+    }
+#pragma unroll
+    for (int i = 0; i < NPH; ++i) {
+        hacc[i][0] += hacc1[i][0];
+        hacc[i][1] += hacc1[i][1];
+    }
+    if (warp >= 10) {
 #pragma unroll
         for (int c = 0; c < NCB; ++c) {
             double v = csum[c];
@@ -645,13 +752,13 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     double* pg = part + (int64_t)blockIdx.x * kGramPart;
     for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
         const int p = pq / BP, qq = pq % BP;
-        pg[pq] = red[0][p][qq] + red[1][p][qq] + red[2][p][qq] + red[3][p][qq];
+        pg[pq] = red[0][p][qq] + red[1][p][qq];
     }
     for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
-        pg[2 * kMaxB * kMaxB + qq] = cred[0][qq] + cred[1][qq] + cred[2][qq] + cred[3][qq];
+        pg[2 * kMaxB * kMaxB + qq] = cred[0][qq] + cred[1][qq];
     if constexpr (WITH_H) {
         __syncthreads();
-        if (warp >= 6) {
+        if (warp >= 10) {
 #pragma unroll
             for (int c = 0; c < NCB; ++c)
 #pragma unroll
@@ -663,7 +770,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         __syncthreads();
         for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
             const int p = pq / BP, qq = pq % BP;
-            pg[kMaxB * kMaxB + pq] = red[0][p][qq] + red[1][p][qq] + red[2][p][qq] + red[3][p][qq];
+            pg[kMaxB * kMaxB + pq] = red[0][p][qq] + red[1][p][qq];
         }
     }
     if (last_block_done(counter)) {

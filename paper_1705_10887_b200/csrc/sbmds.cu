@@ -299,9 +299,11 @@ struct sbmds_ctx {
                            // 3 = the tensor-core sparse step where it applies (k_sp8.cuh), else 1
     // tensor-core sparse step (k_sp8.cuh): 128-row blocks, dense three-plane digit images of S_B
     BlkIdx s8;
-    DevBuf s8img, s8ioff, s8esc, s8yd;
+    DevBuf s8img, s8ioff, s8esc, s8yd, s8trace;
     int sp8_state = 0;     // 0 not built, 1 built, -1 not applicable (a dictionary > 128 entries)
-    int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product
+    int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product,
+                           // 2 = timeline of CTA 0, 4 = stream the images only, 8 = T product in the last iteration too,
+                           // 16 = no H' (as between Rayleigh-Ritz steps)
     int64_t s8_bytes = 0;
     // D_ll
     float* D = nullptr;
@@ -1070,6 +1072,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     h->s8yd.ensure((size_t)3 * h->l * 16);
     launch(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
            (const float*)h->Y2.as<float>(), (const unsigned int*)y2max, h->s8yd.as<uint8_t>());
+    if (h->sp8_dbg & 2) h->s8trace.ensure(12 * 64 * sizeof(unsigned long long));
     auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
     launch(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
            (const int8_t*)h->s8img.as<int8_t>(),
@@ -1077,7 +1080,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
            (const unsigned int*)y2max, (const double*)h->t.as<double>(), Y, want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
-           h->counters.as<unsigned int>() + CNT_GRAM);
+           h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr, (h->sp8_dbg & 4) ? 1 : 0);
 }
 
 bool fused_ok(const sbmds_ctx* h, int b) {
@@ -1339,7 +1342,8 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
            bad.as<int>());
     BlkIdx& o = h->s8;
     build_blk_index(h, rowof.as<int32_t>(), kSp8RB, false, o, st);
-    if (o.umax > (uint32_t)kSp8DK) {   // a block touches more landmarks than one image holds
+    if (o.umax > (uint32_t)kSp8DK ||   // a block touches more landmarks than one image holds, or
+        (o.nblk + h->num_sms - 1) / h->num_sms > Sp8Cfg<16>::MAXNB) {   // a CTA's metadata table overflows
         o.reset();
         return false;
     }
@@ -1836,8 +1840,10 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         auto enqueue_iteration = [&](int itx, bool do_rr) {
             if (sp8) {
                 // A5 + Grams + the next apply's S^T Y_{k+1} partials on the int8 tensor cores (k_sp8.cuh)
-                const int fl = kApplyFused | kApplySp8 | (itx > 1 ? kApplyY1Ready : 0) | (itx == max_iters ? kApplyNoP1 : 0);
-                apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
+                const int fl = kApplyFused | kApplySp8 | (itx > 1 ? kApplyY1Ready : 0) |
+                               (itx == max_iters && !(h->sp8_dbg & 8) ? kApplyNoP1 : 0);
+                apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl,
+                             do_rr && !(h->sp8_dbg & 16) ? Yc : nullptr);
             } else if (fused) {
                 // A5 fused with G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, H' = Y_k^T Y_{k+1} (RR) and
                 // (fuse = 2) the next apply's S^T Y_{k+1} partials (k_fused.cuh)
@@ -2080,6 +2086,14 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a
     else if (!strcmp(key, "sp8_bytes")) *value = h->s8_bytes;           // its S images (HBM bytes per pass)
     else if (!strcmp(key, "sp8_umax")) *value = h->sp8_state > 0 ? (int64_t)h->s8.umax : -1;
+    else if (!strncmp(key, "sp8_trace_", 10)) {   // (diagnostics, sp8_dbg & 2) event timestamps of CTA 0
+        const int k = atoi(key + 10);
+        if (k < 0 || k >= 12 * 64 || !h->s8trace.p) return fail(SBMDS_EINVAL, "no sp8 trace");
+        unsigned long long v = 0;
+        if (cudaMemcpy(&v, h->s8trace.as<unsigned long long>() + k, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(SBMDS_ECUDA, "sp8 trace read");
+        *value = (int64_t)v;
+    }
     else if (!strcmp(key, "csc_bytes")) *value = (int64_t)(h->cptr.bytes + h->ridx.bytes + h->cval.bytes);
     else if (!strcmp(key, "workspace_bytes"))
         *value = (int64_t)(h->Y1.bytes + h->Y2.bytes + h->P.bytes + h->X.bytes + h->Y.bytes + h->gpart.bytes);
