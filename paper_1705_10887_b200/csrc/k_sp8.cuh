@@ -117,6 +117,21 @@ __device__ __forceinline__ float acc3f(int g0, int g1, int g2, float2 f) {
     return fmaf(i22_to_f(g0), 65536.0f, fmaf(i22_to_f(g1), 256.0f, __int2float_rn(g2))) * f.x * f.y;
 }
 
+// with the fourth group c3 = d1 y2 + d2 y1 (weight 2^-8; |c3| <= 2 K 2^14 <= 2^22): the only
+// dropped term is d2 y2, <= 2^-30 of the product of the two scaled maxima
+__device__ __forceinline__ float acc4f(int g0, int g1, int g2, int g3, float2 f) {
+    return fmaf(i22_to_f(g0), 65536.0f, fmaf(i22_to_f(g1), 256.0f, fmaf(i22_to_f(g3), 0.00390625f, __int2float_rn(g2)))) *
+           f.x * f.y;
+}
+
+// zero 16 TMEM columns of this warp's 32 lanes (group c3 of an accumulator: the first MMA of
+// a chain initialises only groups 0-2, so c3 must start at zero)
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+                 "r"(0u));
+}
+__device__ __forceinline__ void tmem_wait_st_() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -160,18 +175,29 @@ __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, cons
     }
 }
 
+// rs1[i] = (sum_j S_ij) - 1 (fp64 sum), the row-sum deviation the centred step adds back
+__global__ void k_rowsum_m1(int64_t n, const int32_t* __restrict__ rp, const float* __restrict__ val,
+                            float* __restrict__ rs1) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double a = 0.0;
+        for (int32_t e = rp[i]; e < rp[i + 1]; ++e) a += (double)val[e];
+        rs1[i] = (float)(a - 1.0);
+    }
+}
+
 __global__ void k_sp8_sizes(int64_t nblk, const int32_t* __restrict__ doff, int64_t* __restrict__ bytes) {
     for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B < nblk; B += (int64_t)gridDim.x * blockDim.x)
         bytes[B] = (int64_t)3 * kSp8RB * sp8_dpad(doff[B + 1] - doff[B]);
 }
 
-// |Y2| column maxima when the D path's reduction did not produce them (full-D paths)
+// column maxima of |Y2 - 1 t^T| (the centred Y2 the step digitises; t = w^T Y2)
 __global__ void __launch_bounds__(256) k_colabsmax(int64_t l, int bp, const float* __restrict__ Y2,
-                                                   unsigned int* __restrict__ cmax) {
+                                                   const double* __restrict__ t, unsigned int* __restrict__ cmax) {
     __shared__ float m[256];
     const int rb = 256 / bp, c = threadIdx.x % bp, r = threadIdx.x / bp;
+    const float tc = (float)t[c];
     float v = 0.f;
-    for (int64_t k = (int64_t)blockIdx.x * rb + r; k < l; k += (int64_t)gridDim.x * rb) v = fmaxf(v, fabsf(Y2[k * bp + c]));
+    for (int64_t k = (int64_t)blockIdx.x * rb + r; k < l; k += (int64_t)gridDim.x * rb) v = fmaxf(v, fabsf(Y2[k * bp + c] - tc));
     m[threadIdx.x] = v;
     __syncthreads();
     if (threadIdx.x < bp) {
@@ -180,26 +206,32 @@ __global__ void __launch_bounds__(256) k_colabsmax(int64_t l, int bp, const floa
     }
 }
 
-// Y2 -> its digit planes Yd[p][j][0..15] (p = 0, 1, 2: d0, d1, d2 of rint(Y2[j][c] 2^ey_c),
-// ey_c from the column maxima), once per apply: the step kernel copies dictionary rows of
-// these planes (16 bytes each) instead of digitising every landmark once per block it touches
+// centred Y2 -> its digit planes Yd[p][j][0..15] (p = 0, 1, 2: d0, d1, d2 of
+// rint((Y2[j][c] - t_c) 2^ey_c), ey_c from the column maxima of |Y2 - t|), once per apply: the
+// step kernel copies dictionary rows of these planes (16 bytes each) instead of digitising every
+// landmark once per block it touches. Centring by t = w^T Y2 removes the large common part of
+// Y2 that the second J cancels anyway (S Y2 - 1 t^T = S (Y2 - 1 t^T) + (S 1 - 1) t^T), so the 24
+// bits of the digits cover what survives the centring.
 template <int BP>
-__global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2,
+__global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
                                                    const unsigned int* __restrict__ y2max, uint8_t* __restrict__ Yd) {
     static_assert(BP == 16, "b = 16");
-    float sc[BP];
+    float sc[BP], tc[BP];
 #pragma unroll
-    for (int c = 0; c < BP; ++c) sc[c] = pow2f(i8_scale_exp(__uint_as_float(y2max[c])));
+    for (int c = 0; c < BP; ++c) {
+        sc[c] = pow2f(i8_scale_exp(__uint_as_float(y2max[c])));
+        tc[c] = (float)t[c];
+    }
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < l; j += (int64_t)gridDim.x * blockDim.x) {
         float v[BP];
         const float4* src = reinterpret_cast<const float4*>(Y2 + j * BP);
 #pragma unroll
         for (int c4 = 0; c4 < BP / 4; ++c4) {
             const float4 x = src[c4];
-            v[4 * c4] = x.x;
-            v[4 * c4 + 1] = x.y;
-            v[4 * c4 + 2] = x.z;
-            v[4 * c4 + 3] = x.w;
+            v[4 * c4] = x.x - tc[4 * c4];
+            v[4 * c4 + 1] = x.y - tc[4 * c4 + 1];
+            v[4 * c4 + 2] = x.z - tc[4 * c4 + 2];
+            v[4 * c4 + 3] = x.w - tc[4 * c4 + 3];
         }
         uint4 w0, w1, w2;
         digit_rows16(v, sc, w0, w1, w2);
@@ -240,8 +272,11 @@ struct Sp8Cfg {
     static constexpr int NGW = 2;                        // Gram warps (group C)
     // TMEM columns: N[2] (NB each), then T[2][4]: one T accumulator per 32-row K step, since
     // each epilogue warp scales its own 32 rows of Y_B (no cross-warp reduction on the path)
-    static constexpr int ACCN = 0, ACCT = 2 * NB;
-    static_assert(ACCT + 8 * NB <= 512, "tmem");
+    // Accumulators have four 16-column groups (c0 = d0 y0, c1, c2, c3 = d1 y2 + d2 y1): N[2] and a
+    // single-buffered T[4] (one per K step).
+    static constexpr int ACCW = 4 * BP;
+    static constexpr int ACCN = 0, ACCT = 2 * ACCW;
+    static_assert(ACCT + 4 * ACCW <= 512, "tmem");
     static_assert(BP == 16, "the tensor-core sparse step is built for b = 16");
 };
 
@@ -250,6 +285,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     k_sp8_step(int64_t n, int64_t l_rows, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
                const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
                const uint8_t* __restrict__ Yd, const unsigned int* __restrict__ y2max, const double* __restrict__ t,
+               const float* __restrict__ rs1,
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
                unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int stream_only) {
@@ -307,8 +343,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_init(&an_empty[a], 128);
             mbar_init(&bt_full[a], 128);
             mbar_init(&bt_empty[a], 1);
-            mbar_init(&at_full[a], 1);
-            mbar_init(&at_empty[a], 128);
+            if (a == 0) {
+                mbar_init(&at_full[a], 1);
+                mbar_init(&at_empty[a], 128);
+            }
             mbar_init(&yr_full[a], 128);
             mbar_init(&yr_empty[a], 32 * C::NGW);
             mbar_init(&yp_full[a], 32 * C::NGW);   // the Gram group's cp.async rows of Y_prev
@@ -336,6 +374,20 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    if (warp >= 2 && warp < 10) {   // c3 groups of every accumulator start at zero
+        const uint32_t lo = (uint32_t)(32 * (warp & 3)) << 16;
+        if (warp < 6) {
+            tmem_zero16(tbase + lo + C::ACCN + 3 * BP);
+            tmem_zero16(tbase + lo + C::ACCN + C::ACCW + 3 * BP);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tmem_zero16(tbase + lo + C::ACCT + j * C::ACCW + 3 * BP);
+        }
+        tmem_wait_st_();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
     auto dpad_of = [&](int64_t B) { return sp8_dpad(m_doff[B - b0 + 1] - m_doff[B - b0]); };
     auto rows_of = [&](int64_t B) {
         const int64_t r0 = B * kSp8RB;
@@ -378,16 +430,17 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     } else if (stream_only) {
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issue: N(i), then T(i - 1)
-        constexpr uint32_t id1n = idesc_i8_bmn(128, NB, 0), id2n = idesc_i8_bmn(128, 2 * BP, 0),
-                           id3n = idesc_i8_bmn(128, BP, 0);
-        constexpr uint32_t id1t = idesc_i8_bmn(128, NB, 1), id2t = idesc_i8_bmn(128, 2 * BP, 1),
-                           id3t = idesc_i8_bmn(128, BP, 1);
+        // d0 x [y0|y1|y2] -> groups 0-2, d1 x [y0|y1|y2] -> 1-3, d2 x [y0|y1] -> 2-3
+        constexpr uint32_t id1n = idesc_i8_bmn(128, NB, 0), id2n = idesc_i8_bmn(128, NB, 0),
+                           id3n = idesc_i8_bmn(128, 2 * BP, 0);
+        constexpr uint32_t id1t = idesc_i8_bmn(128, NB, 1), id2t = idesc_i8_bmn(128, NB, 1),
+                           id3t = idesc_i8_bmn(128, 2 * BP, 1);
         constexpr uint32_t KG = NB / 16 * 128;   // B: bytes per 8-row K group (the LBO)
         // Both products are issued as soon as their operands are ready (polled, non-blocking):
         // T(i) does not wait behind N(i + 1), so an image stage is released as early as possible.
         auto ready_t = [&](int i) {
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
-            return mbar_test(&bt_full[i & 1], pa) && mbar_test(&at_empty[i & 1], pa ^ 1u);
+            return mbar_test(&bt_full[i & 1], pa) && mbar_test(&at_empty[0], (uint32_t)(i & 1) ^ 1u);
         };
         auto ready_n = [&](int i) {
             const uint32_t ph = (uint32_t)((i / 3) & 1), pa = (uint32_t)((i >> 1) & 1);
@@ -405,13 +458,13 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             if (elect_one()) {
 #pragma unroll
                 for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue warp j's) per MMA
-                    const uint32_t d = tbase + (uint32_t)(C::ACCT + (4 * a + j) * NB);
+                    const uint32_t d = tbase + (uint32_t)(C::ACCT + j * C::ACCW);
                     const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
                     tc_mma_i8(d, umma_desc_none(sa + 512 * j, 128, 2048), bd, id1t, 0u);
                     tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
                     tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
                 }
-                tc_commit(&at_full[a]);
+                tc_commit(&at_full[0]);
                 tc_commit(&bt_empty[a]);
                 tc_commit(&empty_img[s]);
             }
@@ -426,7 +479,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             tc_fence_after();
             if (lane == 0) SP8_TR(1, i);
             const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BN + (i % C::NBN) * C::BN);
-            const uint32_t d = tbase + (uint32_t)(C::ACCN + a * NB);
+            const uint32_t d = tbase + (uint32_t)(C::ACCN + a * C::ACCW);
             const uint32_t plane = (uint32_t)(kSp8RB * dp);
             if (elect_one()) {
                 for (int j = 0; j < dp / 32; ++j) {   // K = 32 dictionary entries per MMA
@@ -466,15 +519,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         const int q = warp & 3;
         const int r = 32 * q + lane;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-        float ht[BP];   // t / 2
+        float mht[BP];   // -t / 2
 #pragma unroll
-        for (int c = 0; c < BP; ++c) ht[c] = (float)(0.5 * t[c]);
-        auto load_acc = [&](uint32_t col, int (&g0)[BP], int (&g1)[BP], int (&g2)[BP]) {
+        for (int c = 0; c < BP; ++c) mht[c] = (float)(-0.5 * t[c]);
+        auto load_acc = [&](uint32_t col, int (&g0)[BP], int (&g1)[BP], int (&g2)[BP], int (&g3)[BP]) {
 #pragma unroll
             for (int c0 = 0; c0 < BP; c0 += 8) {
                 tmem_ld8_u(tbase + lane_off + col + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
                 tmem_ld8_u(tbase + lane_off + col + BP + c0, *reinterpret_cast<int(*)[8]>(&g1[c0]));
                 tmem_ld8_u(tbase + lane_off + col + 2 * BP + c0, *reinterpret_cast<int(*)[8]>(&g2[c0]));
+                tmem_ld8_u(tbase + lane_off + col + 3 * BP + c0, *reinterpret_cast<int(*)[8]>(&g3[c0]));
             }
             tmem_wait_ld();
         };
@@ -490,16 +544,19 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             if (r == 0) SP8_TR(3, i);
-            int g0[BP], g1[BP], g2[BP];
-            load_acc((uint32_t)(C::ACCN + a * NB), g0, g1, g2);
+            int g0[BP], g1[BP], g2[BP], g3[BP];
+            load_acc((uint32_t)(C::ACCN + a * C::ACCW), g0, g1, g2, g3);
+            tmem_zero16(tbase + lane_off + C::ACCN + a * C::ACCW + 3 * BP);
+            tmem_wait_st_();
             tc_fence_before();
             mbar_arrive(&an_empty[a]);
-            // Y = -1/2 (S Y2 - 1 t^T) for this row
+            // Y = -1/2 (S Y2 - 1 t^T) = -1/2 (S (Y2 - 1 t^T) + (S 1 - 1) t^T) for this row
+            const float rsm1 = r < rows ? __ldg(rs1 + B * kSp8RB + r) : 0.f;
             float y[BP];
             const bool live = r < rows;
 #pragma unroll
             for (int c = 0; c < BP; ++c)
-                y[c] = live ? fmaf(-0.5f, acc3f(g0[c], g1[c], g2[c], sce[c]), ht[c]) : 0.f;
+                y[c] = live ? fmaf(-0.5f, acc4f(g0[c], g1[c], g2[c], g3[c], sce[c]), rsm1 * mht[c]) : 0.f;
             if (want_t) {
                 // this warp's column maxima over its 32 rows (butterfly reduce-scatter: lane ends
                 // with column cl, then an all-gather of the exponents), the per-warp exponents ey
@@ -566,7 +623,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
             mbar_wait(&ey_full[i & 3], (uint32_t)((i >> 2) & 1), 155 * 65536 + (i & 0xFFFF));
-            mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
+            mbar_wait(&at_full[0], (uint32_t)(i & 1), 148 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             const int lrow = 32 * (warp & 3) + lane;   // the TMEM lane (dictionary entry) this thread drains
             float out[BP];
@@ -574,21 +631,24 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             for (int c = 0; c < BP; ++c) out[c] = 0.f;
 #pragma unroll 1
             for (int j = 0; j < 4; ++j) {   // K step j = rows of epilogue warp j, with its own exponents
-                int g0[BP], g1[BP], g2[BP];
-                const uint32_t col = (uint32_t)(C::ACCT + (4 * a + j) * NB);
+                int g0[BP], g1[BP], g2[BP], g3[BP];
+                const uint32_t col = (uint32_t)(C::ACCT + j * C::ACCW);
 #pragma unroll
                 for (int c0 = 0; c0 < BP; c0 += 8) {
                     tmem_ld8_u(tbase + lane_off + col + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
                     tmem_ld8_u(tbase + lane_off + col + BP + c0, *reinterpret_cast<int(*)[8]>(&g1[c0]));
                     tmem_ld8_u(tbase + lane_off + col + 2 * BP + c0, *reinterpret_cast<int(*)[8]>(&g2[c0]));
+                    tmem_ld8_u(tbase + lane_off + col + 3 * BP + c0, *reinterpret_cast<int(*)[8]>(&g3[c0]));
                 }
                 tmem_wait_ld();
+                tmem_zero16(tbase + lane_off + col + 3 * BP);
+                tmem_wait_st_();
                 const int* ey = eyb + ((i & 3) * 4 + j) * BP;
 #pragma unroll
-                for (int c = 0; c < BP; ++c) out[c] += acc3f(g0[c], g1[c], g2[c], pow2f2(16 - eS - ey[c]));
+                for (int c = 0; c < BP; ++c) out[c] += acc4f(g0[c], g1[c], g2[c], g3[c], pow2f2(16 - eS - ey[c]));
             }
             tc_fence_before();
-            mbar_arrive(&at_empty[a]);
+            mbar_arrive(&at_empty[0]);
             if (lrow < du) {
                 float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)(d0 + lrow) * BP);
 #pragma unroll
