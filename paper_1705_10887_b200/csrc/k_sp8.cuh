@@ -110,6 +110,21 @@ __device__ __forceinline__ void digit_rows16(const float (&v)[16], const float (
                     pack4_byte<0>(b2[8], b2[9], b2[10], b2[11]), pack4_byte<0>(b2[12], b2[13], b2[14], b2[15]));
 }
 
+// as digit_rows16 for 8 columns (three 8-byte plane half-rows)
+__device__ __forceinline__ void digit_rows8(const float (&v)[8], const float (&sc)[8], uint2& r0, uint2& r1, uint2& r2) {
+    uint32_t b2[8], b1[8], b0[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t bits = __float_as_uint(fmaf(v[c], sc[c], 12582912.0f));
+        b2[c] = bits;
+        b1[c] = bits + 128u;
+        b0[c] = bits + (32896u - 0x4B400000u);
+    }
+    r0 = make_uint2(pack4_byte<2>(b0[0], b0[1], b0[2], b0[3]), pack4_byte<2>(b0[4], b0[5], b0[6], b0[7]));
+    r1 = make_uint2(pack4_byte<1>(b1[0], b1[1], b1[2], b1[3]), pack4_byte<1>(b1[4], b1[5], b1[6], b1[7]));
+    r2 = make_uint2(pack4_byte<0>(b2[0], b2[1], b2[2], b2[3]), pack4_byte<0>(b2[4], b2[5], b2[6], b2[7]));
+}
+
 // (c0 + c1/256 + c2/65536) 2^16 of the three accumulator groups, times 2^e = f.x f.y (fp32,
 // like an fp32 accumulation). |c0| <= K 2^14 <= 2^21 and |c1| <= 2^22 (K <= 128) convert exactly
 // by the magic add; c2 (up to 3 2^21) takes the one conversion instruction.
@@ -129,6 +144,9 @@ __device__ __forceinline__ float acc4f(int g0, int g1, int g2, int g3, float2 f)
 __device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
                  "r"(0u));
+}
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(0u));
 }
 __device__ __forceinline__ void tmem_wait_st_() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -268,12 +286,13 @@ struct Sp8Cfg {
     static constexpr int MAXNB = 256;                    // blocks per CTA (per-CTA metadata table)
     static constexpr int OFF_META = OFF_BAR + 2048;      // int64 ioff[256], int32 doff[257], int32 eS[256]
     static constexpr int SMEM = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 16 + 1024;   // + alignment slack
-    static constexpr int THREADS = 12 * 32;   // 3 warps per scheduler (<= 168 registers)
+    static constexpr int THREADS = 16 * 32;   // 4 warps per scheduler (<= 128 registers)
     static constexpr int NGW = 2;                        // Gram warps (group C)
     // TMEM columns: N[2] (NB each), then T[2][4]: one T accumulator per 32-row K step, since
     // each epilogue warp scales its own 32 rows of Y_B (no cross-warp reduction on the path)
-    // Accumulators have four 16-column groups (c0 = d0 y0, c1, c2, c3 = d1 y2 + d2 y1): N[2] and a
-    // single-buffered T[4] (one per K step).
+    // Accumulators have four 16-column groups (c0 = d0 y0, c1, c2, c3 = d1 y2 + d2 y1): N[2] and
+    // T[2][2] (double-buffered; one per 64-row K half, rows of an epilogue warp pair, which
+    // share their column scales).
     static constexpr int ACCW = 4 * BP;
     static constexpr int ACCN = 0, ACCT = 2 * ACCW;
     static_assert(ACCT + 4 * ACCW <= 512, "tmem");
@@ -336,18 +355,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         for (int a = 0; a < C::NBN; ++a) {
             mbar_init(&bn_full[a], 128);
             mbar_init(&bn_empty[a], 1);
-            mbar_init(&ey_full[a], 4 * BP);
+            mbar_init(&ey_full[a], 2 * BP);   // one warp per pair, 8 lanes per half
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&an_full[a], 1);
-            mbar_init(&an_empty[a], 128);
-            mbar_init(&bt_full[a], 128);
+            mbar_init(&an_empty[a], 256);
+            mbar_init(&bt_full[a], 256);
             mbar_init(&bt_empty[a], 1);
-            if (a == 0) {
-                mbar_init(&at_full[a], 1);
-                mbar_init(&at_empty[a], 128);
-            }
-            mbar_init(&yr_full[a], 128);
+            mbar_init(&at_full[a], 1);
+            mbar_init(&at_empty[a], 128);
+            mbar_init(&yr_full[a], 256);
             mbar_init(&yr_empty[a], 32 * C::NGW);
             mbar_init(&yp_full[a], 32 * C::NGW);   // the Gram group's cp.async rows of Y_prev
         }
@@ -374,14 +391,15 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
-    if (warp >= 2 && warp < 10) {   // c3 groups of every accumulator start at zero
+    if (warp >= 2 && warp < 14) {   // c3 groups of every accumulator start at zero
         const uint32_t lo = (uint32_t)(32 * (warp & 3)) << 16;
-        if (warp < 6) {
-            tmem_zero16(tbase + lo + C::ACCN + 3 * BP);
-            tmem_zero16(tbase + lo + C::ACCN + C::ACCW + 3 * BP);
+        if (warp < 10) {
+            const uint32_t cb = (uint32_t)(8 * ((warp - 2) >> 2));
+            tmem_zero8(tbase + lo + C::ACCN + 3 * BP + cb);
+            tmem_zero8(tbase + lo + C::ACCN + C::ACCW + 3 * BP + cb);
         } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) tmem_zero16(tbase + lo + C::ACCT + j * C::ACCW + 3 * BP);
+            for (int j = 0; j < 4; ++j) tmem_zero16(tbase + lo + C::ACCT + j * C::ACCW + 3 * BP);   // T[2][2]
         }
         tmem_wait_st_();
     }
@@ -440,7 +458,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         // T(i) does not wait behind N(i + 1), so an image stage is released as early as possible.
         auto ready_t = [&](int i) {
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
-            return mbar_test(&bt_full[i & 1], pa) && mbar_test(&at_empty[0], (uint32_t)(i & 1) ^ 1u);
+            return mbar_test(&bt_full[i & 1], pa) && mbar_test(&at_empty[i & 1], pa ^ 1u);
         };
         auto ready_n = [&](int i) {
             const uint32_t ph = (uint32_t)((i / 3) & 1), pa = (uint32_t)((i >> 1) & 1);
@@ -457,14 +475,14 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             const uint32_t plane = (uint32_t)(kSp8RB * dp);
             if (elect_one()) {
 #pragma unroll
-                for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue warp j's) per MMA
-                    const uint32_t d = tbase + (uint32_t)(C::ACCT + j * C::ACCW);
+                for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue quadrant j's) per MMA
+                    const uint32_t d = tbase + (uint32_t)(C::ACCT + (2 * a + (j >> 1)) * C::ACCW);
                     const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
-                    tc_mma_i8(d, umma_desc_none(sa + 512 * j, 128, 2048), bd, id1t, 0u);
+                    tc_mma_i8(d, umma_desc_none(sa + 512 * j, 128, 2048), bd, id1t, (j & 1) ? 1u : 0u);
                     tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
                     tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
                 }
-                tc_commit(&at_full[0]);
+                tc_commit(&at_full[a]);
                 tc_commit(&bt_empty[a]);
                 tc_commit(&empty_img[s]);
             }
@@ -514,58 +532,59 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             }
             if (spin == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         }
-    } else if (warp < 6) {
-        // ------------------------------------------------ epilogue (TMEM lane = row / dictionary entry)
+    } else if (warp < 10) {
+        // ------------------------------------------------ epilogue A (warps 2-9, TMEM lane = row): two
+        // halves of four warps, half hf owning columns 8 hf .. 8 hf + 7 of every row
+        constexpr int HC = BP / 2;
         const int q = warp & 3;
+        const int hf = (warp - 2) >> 2;
+        const int cb = HC * hf;
         const int r = 32 * q + lane;
         const uint32_t lane_off = (uint32_t)(32 * q) << 16;
-        float mht[BP];   // -t / 2
+        float mht[HC];   // -t / 2
 #pragma unroll
-        for (int c = 0; c < BP; ++c) mht[c] = (float)(-0.5 * t[c]);
-        auto load_acc = [&](uint32_t col, int (&g0)[BP], int (&g1)[BP], int (&g2)[BP], int (&g3)[BP]) {
-#pragma unroll
-            for (int c0 = 0; c0 < BP; c0 += 8) {
-                tmem_ld8_u(tbase + lane_off + col + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
-                tmem_ld8_u(tbase + lane_off + col + BP + c0, *reinterpret_cast<int(*)[8]>(&g1[c0]));
-                tmem_ld8_u(tbase + lane_off + col + 2 * BP + c0, *reinterpret_cast<int(*)[8]>(&g2[c0]));
-                tmem_ld8_u(tbase + lane_off + col + 3 * BP + c0, *reinterpret_cast<int(*)[8]>(&g3[c0]));
-            }
-            tmem_wait_ld();
-        };
+        for (int c = 0; c < HC; ++c) mht[c] = (float)(-0.5 * t[cb + c]);
         for (int i = 0; i < nb; ++i) {
             const int64_t B = b0 + i;
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
             const int rows = rows_of(B);
             const int eS = m_es[i];
-            float2 sce[BP];   // accumulator 2^(16 - eS - ey2_c) -> S Y2
+            float2 sce[HC];   // accumulator 2^(16 - eS - ey2_c) -> S Y2
 #pragma unroll
-            for (int c = 0; c < BP; ++c) sce[c] = pow2f2(16 - eS - ey2[c]);
+            for (int c = 0; c < HC; ++c) sce[c] = pow2f2(16 - eS - ey2[cb + c]);
+            const float rsm1 = r < rows ? __ldg(rs1 + B * kSp8RB + r) : 0.f;
             mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
             tc_fence_after();
-            if (r == 0) SP8_TR(3, i);
-            int g0[BP], g1[BP], g2[BP], g3[BP];
-            load_acc((uint32_t)(C::ACCN + a * C::ACCW), g0, g1, g2, g3);
-            tmem_zero16(tbase + lane_off + C::ACCN + a * C::ACCW + 3 * BP);
-            tmem_wait_st_();
+            if (r == 0 && hf == 0) SP8_TR(3, i);
+            int g0[HC], g1[HC], g2[HC], g3[HC];
+            {
+                const uint32_t col = tbase + lane_off + (uint32_t)(C::ACCN + a * C::ACCW + cb);
+                tmem_ld8_u(col, g0);
+                tmem_ld8_u(col + BP, g1);
+                tmem_ld8_u(col + 2 * BP, g2);
+                tmem_ld8_u(col + 3 * BP, g3);
+                tmem_wait_ld();
+                tmem_zero8(col + 3 * BP);
+                tmem_wait_st_();
+            }
             tc_fence_before();
             mbar_arrive(&an_empty[a]);
             // Y = -1/2 (S Y2 - 1 t^T) = -1/2 (S (Y2 - 1 t^T) + (S 1 - 1) t^T) for this row
-            const float rsm1 = r < rows ? __ldg(rs1 + B * kSp8RB + r) : 0.f;
-            float y[BP];
+            float y[HC];
             const bool live = r < rows;
 #pragma unroll
-            for (int c = 0; c < BP; ++c)
+            for (int c = 0; c < HC; ++c)
                 y[c] = live ? fmaf(-0.5f, acc4f(g0[c], g1[c], g2[c], g3[c], sce[c]), rsm1 * mht[c]) : 0.f;
             if (want_t) {
                 // this warp's column maxima over its 32 rows (butterfly reduce-scatter: lane ends
                 // with column cl, then an all-gather of the exponents), the per-warp exponents ey
                 // (K step q of the T product has its own accumulator), the digits of Y_B
-                float m[BP];
+                float m[HC];
 #pragma unroll
-                for (int c = 0; c < BP; ++c) m[c] = fabsf(y[c]);
+                for (int c = 0; c < HC; ++c) m[c] = fabsf(y[c]);
 #pragma unroll
-                for (int h = BP / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
+                for (int h = HC / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
                     const bool up = (lane & o) != 0;
 #pragma unroll
                     for (int j = 0; j < h; ++j) {
@@ -573,48 +592,55 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                         m[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
                     }
                 }
+                m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 2));
                 m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 1));
-                const int cl = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-                const int my_e = i8_scale_exp(m[0]);   // exponent of column cl
-                int ey[BP];
+                const int cl = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                // the warp pair (quadrants 2p, 2p + 1) shares its column maxima: one K half
+                const int pr = q >> 1;
+                float* pm = reinterpret_cast<float*>(eyb + 4 * 2 * BP) + ((a * 2 + hf) * 4 + q) * HC;   // [2][2][4][HC]
+                if ((lane & 3) == 0) pm[cl] = m[0];
+                named_bar(1 + 2 * hf + pr, 64);
+                const float mp = fmaxf(m[0], pm[((q ^ 1) - q) * HC + cl]);
+                const int my_e = i8_scale_exp(mp);   // exponent of column cb + cl for the pair's 64 rows
+                int ey[HC];
 #pragma unroll
-                for (int c = 0; c < BP; ++c)   // lane holding column c: bits 4..1 = c's bits 3..0
-                    ey[c] = __shfl_sync(0xffffffffu, my_e, ((c >> 3) & 1) << 4 | ((c >> 2) & 1) << 3 | ((c >> 1) & 1) << 2 | (c & 1) << 1);
-                if ((lane & 1) == 0) {   // published for group B's T drain of this block
-                    eyb[((i & 3) * 4 + q) * BP + cl] = my_e;
+                for (int c = 0; c < HC; ++c)   // lane holding column c: bits 4..2 = c's bits 2..0
+                    ey[c] = __shfl_sync(0xffffffffu, my_e, ((c >> 2) & 1) << 4 | ((c >> 1) & 1) << 3 | (c & 1) << 2);
+                if ((q & 1) == 0 && (lane & 3) == 0) {   // published for group B's T drain of this block
+                    eyb[((i & 3) * 2 + pr) * BP + cb + cl] = my_e;
                     mbar_arrive(&ey_full[i & 3]);
                 }
-                float ysc[BP];
+                float ysc[HC];
 #pragma unroll
-                for (int c = 0; c < BP; ++c) ysc[c] = pow2f(ey[c]);
-                uint4 w0, w1, w2;
-                digit_rows16(y, ysc, w0, w1, w2);
+                for (int c = 0; c < HC; ++c) ysc[c] = pow2f(ey[c]);
+                uint2 w0, w1, w2;
+                digit_rows8(y, ysc, w0, w1, w2);
                 mbar_wait(&bt_empty[a], pa ^ 1u, 151 * 65536 + (i & 0xFFFF));
                 uint8_t* bt = base + C::OFF_BT + a * C::BT;
-                *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 0)) = w0;
-                *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 1)) = w1;
-                *reinterpret_cast<uint4*>(bt + sp8_boff<NB>(r, 2)) = w2;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 0) + cb) = w0;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 1) + cb) = w1;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 2) + cb) = w2;
                 fence_proxy_async();
                 mbar_arrive(&bt_full[a]);
-                if (r == 0) SP8_TR(4, i);
+                if (r == 0 && hf == 0) SP8_TR(4, i);
             }
             // (after the digits, which gate the T product and the image's release)
             if (live) {
-                float4* dst = reinterpret_cast<float4*>(Y + (B * kSp8RB + r) * BP);
-#pragma unroll
-                for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+                float4* dst = reinterpret_cast<float4*>(Y + (B * kSp8RB + r) * BP + cb);
+                dst[0] = make_float4(y[0], y[1], y[2], y[3]);
+                dst[1] = make_float4(y[4], y[5], y[6], y[7]);
             }
             mbar_wait(&yr_empty[a], pa ^ 1u, 150 * 65536 + (i & 0xFFFF));
             {
-                float4* yr = reinterpret_cast<float4*>(base + C::OFF_YR + a * C::YR) + r * (BP / 4);
-#pragma unroll
-                for (int c = 0; c < BP; c += 4) yr[c / 4] = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+                float4* yr = reinterpret_cast<float4*>(reinterpret_cast<float*>(base + C::OFF_YR + a * C::YR) + r * BP + cb);
+                yr[0] = make_float4(y[0], y[1], y[2], y[3]);
+                yr[1] = make_float4(y[4], y[5], y[6], y[7]);
             }
             mbar_arrive(&yr_full[a]);
         }
-    } else if (warp < 10) {
-        // ------------------------------------------------ group B (warps 6-9): B operand of N, T accumulator -> P1
-        const int gt = threadIdx.x - 192;   // 0..127 (T accumulator: TMEM lane = dictionary entry gt)
+    } else if (warp < 14) {
+        // ------------------------------------------------ group B (warps 10-13): B operand of N, T accumulator -> P1
+        const int gt = threadIdx.x - 320;   // 0..127 (T accumulator: TMEM lane = dictionary entry gt)
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
         // T accumulator of block i -> P1 partials, scaled by A's exponents of Y_B (ey ring of 4:
         // A runs at most two blocks ahead of this group, so neither the ring slot nor the phase
@@ -623,16 +649,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
             mbar_wait(&ey_full[i & 3], (uint32_t)((i >> 2) & 1), 155 * 65536 + (i & 0xFFFF));
-            mbar_wait(&at_full[0], (uint32_t)(i & 1), 148 * 65536 + (i & 0xFFFF));
+            mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             const int lrow = 32 * (warp & 3) + lane;   // the TMEM lane (dictionary entry) this thread drains
             float out[BP];
 #pragma unroll
             for (int c = 0; c < BP; ++c) out[c] = 0.f;
 #pragma unroll 1
-            for (int j = 0; j < 4; ++j) {   // K step j = rows of epilogue warp j, with its own exponents
+            for (int j = 0; j < 2; ++j) {   // K half j = rows of epilogue quadrants 2j, 2j + 1 (their exponents)
                 int g0[BP], g1[BP], g2[BP], g3[BP];
-                const uint32_t col = (uint32_t)(C::ACCT + j * C::ACCW);
+                const uint32_t col = (uint32_t)(C::ACCT + (2 * a + j) * C::ACCW);
 #pragma unroll
                 for (int c0 = 0; c0 < BP; c0 += 8) {
                     tmem_ld8_u(tbase + lane_off + col + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
@@ -643,12 +669,12 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 tmem_wait_ld();
                 tmem_zero16(tbase + lane_off + col + 3 * BP);
                 tmem_wait_st_();
-                const int* ey = eyb + ((i & 3) * 4 + j) * BP;
+                const int* ey = eyb + ((i & 3) * 2 + j) * BP;
 #pragma unroll
                 for (int c = 0; c < BP; ++c) out[c] += acc4f(g0[c], g1[c], g2[c], g3[c], pow2f2(16 - eS - ey[c]));
             }
             tc_fence_before();
-            mbar_arrive(&at_empty[0]);
+            mbar_arrive(&at_empty[a]);
             if (lrow < du) {
                 float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)(d0 + lrow) * BP);
 #pragma unroll
@@ -694,9 +720,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             }
         }
     } else {
-        // ------------------------------------------------ group C (warps 10-11): the Grams on the FP64 tensor cores
-        const int gt = threadIdx.x - 320;   // 0..63: rows gt, gt + 64 of Y_prev this thread stages
-        const int gw = warp - 10;           // 0..1
+        // ------------------------------------------------ group C (warps 14-15): the Grams on the FP64 tensor cores
+        const int gt = threadIdx.x - 448;   // 0..63: rows gt, gt + 64 of Y_prev this thread stages
+        const int gw = warp - 14;           // 0..1
         const int kr = lane & 3, cc = lane >> 2;
         auto gram = [&](int i) {
             const int64_t B = b0 + i;
@@ -760,7 +786,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             gram(i);
             if (gt == 0) SP8_TR(5, i);
             if (WITH_H && i + 2 < nb) {
-                named_bar(2, 32 * C::NGW);   // every row of yp[i & 1] has been read by gram(i)
+                named_bar(5, 32 * C::NGW);   // every row of yp[i & 1] has been read by gram(i)
                 stage_yp(i + 2);
             }
         }
@@ -776,7 +802,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     }
     auto red = reinterpret_cast<double (*)[NCB * 8][NCB * 8 + 1]>(base);   // the image stages are free now
     auto cred = reinterpret_cast<double (*)[NCB * 8]>(reinterpret_cast<double*>(base) + 4 * (NCB * 8) * (NCB * 8 + 1));
-    const int gw = warp - 10;
+    const int gw = warp - 14;
     const int kr = lane & 3, cc = lane >> 2, fr = lane >> 2, fc = 2 * (lane & 3);
 #pragma unroll
     for (int i = 0; i < NPG; ++i) {
@@ -788,7 +814,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         hacc[i][0] += hacc1[i][0];
         hacc[i][1] += hacc1[i][1];
     }
-    if (warp >= 10) {
+    if (warp >= 14) {
 #pragma unroll
         for (int c = 0; c < NCB; ++c) {
             double v = csum[c];
@@ -818,7 +844,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         pg[2 * kMaxB * kMaxB + qq] = cred[0][qq] + cred[1][qq];
     if constexpr (WITH_H) {
         __syncthreads();
-        if (warp >= 10) {
+        if (warp >= 14) {
 #pragma unroll
             for (int c = 0; c < NCB; ++c)
 #pragma unroll

@@ -112,7 +112,68 @@ __global__ void probe(const int8_t* S, const int8_t* Yd, const int8_t* Z, int mo
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb));
 }
 
+// timing: one thread issues nm MMAs (mode 0: N product, A K-major; 1: T product, A MN-major;
+// 2: N product with MN-major B), commit, wait; cycles per MMA
+__global__ void timing(int mode, int nm, int N, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 7);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tb = tslot;
+    if (threadIdx.x == 0) {
+        const uint32_t sa = smem_u32(sm), sb = sa + 48 * 1024;
+        uint64_t a, b;
+        uint32_t id;
+        if (mode == 0) { a = desc_none(sa, 2048, 128); b = desc_none(sb, 384, 128); id = idesc_i8b(128, N, 0, 1); }
+        else if (mode == 1) { a = desc_none(sa, 128, 2048); b = desc_none(sb, 384, 128); id = idesc_i8b(128, N, 1, 1); }
+        else { a = desc_none(sa, 2048, 128); b = desc_none(sb, 768, 128); id = idesc_i8b(128, N, 0, 0); }
+        const long long c0 = clock64();
+        for (int i = 0; i < nm; ++i)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tb + 64 * (i & 3)),
+                         "l"(a), "l"(b), "r"(id), "r"(1u));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], 0;\n\tselp.u32 %0,1,0,P1;\n\t}"
+                         : "=r"(ok) : "r"(smem_u32(&bar)));
+        out[0] = (unsigned long long)(clock64() - c0);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb));
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && argv[1][0] == 't') {
+        unsigned long long* d;
+        cudaMalloc(&d, 8);
+        cudaFuncSetAttribute(timing, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        for (int mode = 0; mode < 3; ++mode)
+            for (int N : {16, 32, 48, 64}) {
+                unsigned long long c = 0;
+                timing<<<1, 128, 64 * 1024>>>(mode, 2048, N, d);
+                cudaDeviceSynchronize();
+                cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+                printf("mode %d (%s) N=%d: %.1f cycles per MMA\n", mode,
+                       mode == 0 ? "N: A K-major, B MN-major" : (mode == 1 ? "T: A MN-major, B MN-major" : "N: A K-major, B K-major"),
+                       N, (double)c / 2048);
+            }
+        return 0;
+    }
     const int only_mode = argc > 1 ? atoi(argv[1]) : -1, only_var = argc > 2 ? atoi(argv[2]) : -1;
     std::vector<int8_t> S(128 * KD), Yd(KD * NB), Z(128 * NB);
     srand(1);
