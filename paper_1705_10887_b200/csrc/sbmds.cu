@@ -144,6 +144,7 @@ struct DevBuf {
     size_t bytes = 0;
     bool pooled = false;
     DevBuf() = default;
+    explicit DevBuf(bool pool) : pooled(pool) {}   // pool = true: stream-ordered pool allocation
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
@@ -185,7 +186,7 @@ struct DevBuf {
 // Row-blocked index of S (k_blocked.cuh) for blocks of rb rows: dictionaries, 16-bit local
 // columns (CSR order), optional block-local CSC, and landmark -> dictionary-slot lists.
 struct BlkIdx {
-    DevBuf doff, dict, lcol, lcp, lrow, lval, jptr, jlist;
+    DevBuf doff{true}, dict{true}, lcol{true}, lcp{true}, lrow{true}, lval{true}, jptr{true}, jlist{true};
     int rb = 0;
     int64_t nblk = 0;
     int32_t total_u = 0;
@@ -1229,7 +1230,8 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
     o.rb = rb;
     o.nblk = (n + rb - 1) / rb;
     const int64_t nb = o.nblk;
-    DevBuf off, scol, iota_perm, flag, incl, tmp, keys2;
+    // temporaries from the stream-ordered pool (every use completes before the stream syncs below)
+    DevBuf off{true}, scol{true}, iota_perm{true}, flag{true}, incl{true}, tmp{true}, keys2{true};
     off.ensure((nb + 1) * sizeof(int32_t));
     scol.ensure(nnz * sizeof(int32_t));
     iota_perm.ensure(2 * nnz * sizeof(int32_t));
@@ -1251,7 +1253,7 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
            (const int32_t*)perm, rowof, (const int32_t*)off.as<int32_t>(), flag.as<int32_t>());
     tb = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)nnz, st));
-    DevBuf tmp2;
+    DevBuf tmp2{true};
     tmp2.ensure(tb + 16);
     CK(cub::DeviceScan::InclusiveSum(tmp2.p, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)nnz, st));
     g_launches.fetch_add(1);
@@ -1281,13 +1283,13 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
     if (want_csc)
         CK(cudaMemcpyAsync(o.lcp.as<int32_t>() + total_u, &nnz32, sizeof(int32_t), cudaMemcpyHostToDevice, st));
     // largest dictionary (decides which block widths fit in shared memory)
-    DevBuf um;
+    DevBuf um{true};
     um.ensure(sizeof(unsigned int));
     CK(cudaMemsetAsync(um.p, 0, sizeof(unsigned int), st));
     launch(k_blk_umax, dim3(256), dim3(256), 0, st, nb, (const int32_t*)o.doff.as<int32_t>(), um.as<unsigned int>());
     // landmark -> dictionary slots, ascending slot (= block) order: stable sort of (dict, slot)
     keys2.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
-    DevBuf slot;
+    DevBuf slot{true};
     slot.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
     launch(k_iota, dim3(256), dim3(256), 0, st, total_u, slot.as<int32_t>());
     int end_bit = 1;
@@ -1295,7 +1297,7 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
     tb = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, o.dict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
                                        o.jlist.as<int32_t>(), total_u, 0, end_bit, st));
-    DevBuf tmp3;
+    DevBuf tmp3{true};
     tmp3.ensure(tb + 16);
     CK(cub::DeviceRadixSort::SortPairs(tmp3.p, tb, o.dict.as<int32_t>(), keys2.as<int32_t>(), slot.as<int32_t>(),
                                        o.jlist.as<int32_t>(), total_u, 0, end_bit, st));
@@ -1334,7 +1336,7 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     if (h->sp8_state != 0) return h->sp8_state > 0;
     h->sp8_state = -1;
     if (!h->blocked || h->nnz == 0) return false;
-    DevBuf rowof, bad;
+    DevBuf rowof{true}, bad{true};
     rowof.ensure(h->nnz * sizeof(int32_t));
     bad.ensure(sizeof(int));
     CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
@@ -1349,7 +1351,7 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
         return false;
     }
     h->s8ioff.ensure((o.nblk + 1) * sizeof(int64_t));
-    DevBuf sizes, tmp;
+    DevBuf sizes{true}, tmp{true};
     sizes.ensure((o.nblk + 1) * sizeof(int64_t));
     launch(k_sp8_sizes, dim3((unsigned)std::min<int64_t>(1024, (o.nblk + 255) / 256)), dim3(256), 0, st, o.nblk,
            (const int32_t*)o.doff.as<int32_t>(), sizes.as<int64_t>());
