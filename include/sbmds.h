@@ -107,7 +107,8 @@ sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float* Y, void* c
  *   max_iters  : >= 1 subspace iterations (one apply each).
  *   tol        : > 0: stop when max_i<m ||B~v_i - θ_i v_i|| <= tol * max_j |θ_j|
  *                (SPEC.md:52 form), checked every rr_period (default 5) iterations;
- *                <= 0: run exactly max_iters iterations (status OK).
+ *                <= 0: run exactly max_iters iterations (status OK); Rayleigh-Ritz then runs
+ *                once, after the last iteration (it only feeds the convergence test).
  *   seed       : initial block X0 ~ N(0,1) from a counter-based Philox generator.
  *   X0         : optional n x block warm start (host or device), or NULL.
  *   eigvals    : HOST double[m], descending.

@@ -1941,7 +1941,9 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                 it += R - 1;   // the segment's Rayleigh-Ritz iteration
                 do_rr = true;
             } else {
-                do_rr = (it % R == 0) || it == max_iters;
+                // Rayleigh-Ritz only feeds the convergence test (the iterate is never rotated), so a
+                // fixed-iteration solve (tol <= 0, BASELINE config 4) needs it only at the end
+                do_rr = (tol > 0.0 && it % R == 0) || it == max_iters;
                 enqueue_iteration(it, do_rr);
             }
             if (do_rr) {
