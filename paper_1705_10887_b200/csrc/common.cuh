@@ -212,6 +212,19 @@ __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
+// order-preserving unsigned keys of floats (atomicMax / atomicMin over signed values)
+__host__ __device__ __forceinline__ unsigned int f32_order_key(float f) {
+    unsigned int u;
+    memcpy(&u, &f, 4);
+    return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ __forceinline__ float f32_from_order_key(unsigned int k) {
+    const unsigned int u = (k >> 31) ? (k & 0x7FFFFFFFu) : ~k;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
 // Fixed-order sum of p[0], p[stride], ..., p[(count-1)*stride] with 16 loads in flight:
 // the additions happen in index order (bitwise reproducible) but the L2 latency of the
 // partials is overlapped instead of serialised.

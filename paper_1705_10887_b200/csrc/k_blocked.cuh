@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) k_blk_spmmt(int64_t n, int b, int bp, con
 
 // ------------------------------------------------------------------ A2 part 2: Y1 = sum_B P1 - w s^T
 // One warp per landmark j: the dictionary slots holding j (ascending block order) are
-// summed in fp64, LPR lanes per slot row, a fixed shuffle tree across the G slot groups.
+// summed in fp64 (jlist == NULL: the partials are already stored landmark-major, slot k = k), LPR lanes per slot row, a fixed shuffle tree across the G slot groups.
 template <int LPR>
 __global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, const int32_t* __restrict__ jptr,
                                                     const int32_t* __restrict__ jlist, const float* __restrict__ P1,
@@ -216,8 +216,19 @@ __global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, co
     if (j >= l) return;
     const int32_t beg = jptr[j], end = jptr[j + 1];
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int32_t k = beg + g; k < end; k += G) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)jlist[k] * bp) + q);
+    int32_t k = beg + g;
+    for (; k + 3 * G < end; k += 4 * G) {   // four loads in flight, added in slot order
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            v[u] = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)(jlist ? jlist[k + u * G] : k + u * G) * bp) + q);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+        }
+    }
+    for (; k < end; k += G) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)(jlist ? jlist[k] : k) * bp) + q);
         a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
     }
 #pragma unroll

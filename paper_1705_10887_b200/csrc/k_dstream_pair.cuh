@@ -431,8 +431,9 @@ __global__ void __launch_bounds__(256) k_y16_prep(int64_t lpad, int b, int bp, c
                                                   const float* __restrict__ Y1, float* __restrict__ Y1f,
                                                   unsigned int* __restrict__ cmax, unsigned int* __restrict__ zero64) {
     __shared__ double Ms[64 * 64];
-    // zero64 (optional): the Y2 column maxima the following k_dreduce_pair accumulates
-    if (zero64 && blockIdx.x == 0 && threadIdx.x < 64) zero64[threadIdx.x] = 0u;
+    // zero64 (optional): reset the Y2 column max / min keys the following k_dreduce_pair
+    // accumulates ([0, 64) max keys start at 0, [64, 128) min keys at ~0)
+    if (zero64 && blockIdx.x == 0 && threadIdx.x < 128) zero64[threadIdx.x] = threadIdx.x < 64 ? 0u : 0xFFFFFFFFu;
     __shared__ float ys[256];
     __shared__ float mx[256];
     if (Rinv)
@@ -523,10 +524,12 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
                                                       const int* __restrict__ dexp, const int* __restrict__ yexp,
                                                       const double* __restrict__ w, float* __restrict__ Y2,
                                                       double* __restrict__ tpart, double* __restrict__ t,
-                                                      unsigned int* __restrict__ counter, unsigned int* __restrict__ y2max) {
+                                                      unsigned int* __restrict__ counter, unsigned int* __restrict__ y2mm) {
     __shared__ double red[256];
-    __shared__ float cmx[256];
-    float m = 0.f;   // |Y2| column maxima (optional; the tensor-core sparse step's digit scales)
+    __shared__ float cmx[256], cmn[256];
+    // column max / min of Y2 as order-preserving keys (optional; the tensor-core sparse step
+    // derives max |Y2 - t| = max(max - t, t - min) from them once t is known)
+    float m = -3.0e38f, mn = 3.0e38f;
     const int rows_per_blk = 256 / bp;
     const int tid = threadIdx.x;
     const int cidx = tid % bp, rloc = tid / bp;
@@ -549,17 +552,23 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
             for (; q < q1; ++q) v += (double)P[((int64_t)(xslot ? xslot[q] : q) * 128 + rr) * bp + cidx];
             v *= unscale;
             Y2[r * bp + cidx] = (float)v;
-            m = fmaxf(m, fabsf((float)v));
+            m = fmaxf(m, (float)v);
+            mn = fminf(mn, (float)v);
             if (cidx < b) acc_t += w[r] * v;
         }
     }
     red[tid] = (rloc < rows_per_blk) ? acc_t : 0.0;
     cmx[tid] = m;
+    cmn[tid] = mn;
     __syncthreads();
-    if (y2max && tid < bp) {
-        float mm = 0.f;
-        for (int q = 0; q < rows_per_blk; ++q) mm = fmaxf(mm, cmx[q * bp + tid]);
-        atomicMax(y2max + tid, __float_as_uint(mm));
+    if (y2mm && tid < bp) {
+        float mm = -3.0e38f, mi = 3.0e38f;
+        for (int q = 0; q < rows_per_blk; ++q) {
+            mm = fmaxf(mm, cmx[q * bp + tid]);
+            mi = fminf(mi, cmn[q * bp + tid]);
+        }
+        atomicMax(y2mm + tid, f32_order_key(mm));
+        atomicMin(y2mm + 64 + tid, f32_order_key(mi));
     }
     if (tid < bp) {
         double v = 0.0;

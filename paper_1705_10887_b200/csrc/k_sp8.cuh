@@ -203,24 +203,37 @@ __global__ void k_rowsum_m1(int64_t n, const int32_t* __restrict__ rp, const flo
     }
 }
 
+// pos[jlist[k]] = k: where the T drain stores the partial of dictionary slot d (landmark-major,
+// so the landmark reduction reads each landmark's partials contiguously)
+__global__ void k_inverse_perm(int32_t count, const int32_t* __restrict__ jlist, int32_t* __restrict__ pos) {
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) pos[jlist[k]] = k;
+}
+
 __global__ void k_sp8_sizes(int64_t nblk, const int32_t* __restrict__ doff, int64_t* __restrict__ bytes) {
     for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B < nblk; B += (int64_t)gridDim.x * blockDim.x)
         bytes[B] = (int64_t)3 * kSp8RB * sp8_dpad(doff[B + 1] - doff[B]);
 }
 
-// column maxima of |Y2 - 1 t^T| (the centred Y2 the step digitises; t = w^T Y2)
-__global__ void __launch_bounds__(256) k_colabsmax(int64_t l, int bp, const float* __restrict__ Y2,
-                                                   const double* __restrict__ t, unsigned int* __restrict__ cmax) {
-    __shared__ float m[256];
+// column max / min keys of Y2 (for D paths whose reduction does not form them)
+__global__ void __launch_bounds__(256) k_colminmax(int64_t l, int bp, const float* __restrict__ Y2,
+                                                   unsigned int* __restrict__ y2mm) {
+    __shared__ float m[256], n_[256];
     const int rb = 256 / bp, c = threadIdx.x % bp, r = threadIdx.x / bp;
-    const float tc = (float)t[c];
-    float v = 0.f;
-    for (int64_t k = (int64_t)blockIdx.x * rb + r; k < l; k += (int64_t)gridDim.x * rb) v = fmaxf(v, fabsf(Y2[k * bp + c] - tc));
+    float v = -3.0e38f, w = 3.0e38f;
+    for (int64_t k = (int64_t)blockIdx.x * rb + r; k < l; k += (int64_t)gridDim.x * rb) {
+        v = fmaxf(v, Y2[k * bp + c]);
+        w = fminf(w, Y2[k * bp + c]);
+    }
     m[threadIdx.x] = v;
+    n_[threadIdx.x] = w;
     __syncthreads();
     if (threadIdx.x < bp) {
-        for (int q = 1; q < rb; ++q) v = fmaxf(v, m[q * bp + threadIdx.x]);
-        atomicMax(cmax + threadIdx.x, __float_as_uint(v));
+        for (int q = 1; q < rb; ++q) {
+            v = fmaxf(v, m[q * bp + threadIdx.x]);
+            w = fminf(w, n_[q * bp + threadIdx.x]);
+        }
+        atomicMax(y2mm + threadIdx.x, f32_order_key(v));
+        atomicMin(y2mm + 64 + threadIdx.x, f32_order_key(w));
     }
 }
 
@@ -230,15 +243,21 @@ __global__ void __launch_bounds__(256) k_colabsmax(int64_t l, int bp, const floa
 // landmark once per block it touches. Centring by t = w^T Y2 removes the large common part of
 // Y2 that the second J cancels anyway (S Y2 - 1 t^T = S (Y2 - 1 t^T) + (S 1 - 1) t^T), so the 24
 // bits of the digits cover what survives the centring.
+// (max |Y2_c - t_c| = max(max_c - t_c, t_c - min_c) from the column max / min keys; block 0
+// records the exponents for the step kernel)
 template <int BP>
 __global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
-                                                   const unsigned int* __restrict__ y2max, uint8_t* __restrict__ Yd) {
+                                                   const unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
+                                                   uint8_t* __restrict__ Yd) {
     static_assert(BP == 16, "b = 16");
     float sc[BP], tc[BP];
 #pragma unroll
     for (int c = 0; c < BP; ++c) {
-        sc[c] = pow2f(i8_scale_exp(__uint_as_float(y2max[c])));
         tc[c] = (float)t[c];
+        const float mx = fmaxf(f32_from_order_key(y2mm[c]) - tc[c], tc[c] - f32_from_order_key(y2mm[64 + c]));
+        const int e = i8_scale_exp(mx);
+        sc[c] = pow2f(e);
+        if (blockIdx.x == 0 && threadIdx.x == c) ey2_out[c] = e;
     }
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < l; j += (int64_t)gridDim.x * blockDim.x) {
         float v[BP];
@@ -303,8 +322,8 @@ template <int BP, bool WITH_H>
 __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     k_sp8_step(int64_t n, int64_t l_rows, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
                const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
-               const uint8_t* __restrict__ Yd, const unsigned int* __restrict__ y2max, const double* __restrict__ t,
-               const float* __restrict__ rs1,
+               const uint8_t* __restrict__ Yd, const int* __restrict__ ey2in, const double* __restrict__ t,
+               const float* __restrict__ rs1, const int32_t* __restrict__ ppos,
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
                unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int stream_only) {
@@ -370,7 +389,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         }
         fence_barrier_init();
     }
-    if (threadIdx.x < BP) ey2[threadIdx.x] = i8_scale_exp(__uint_as_float(y2max[threadIdx.x]));
+    if (threadIdx.x < BP) ey2[threadIdx.x] = ey2in[threadIdx.x];
     // the CTA's block metadata, once: no role waits on an L2 round trip per block
     int64_t* m_ioff = reinterpret_cast<int64_t*>(base + C::OFF_META);
     int32_t* m_doff = reinterpret_cast<int32_t*>(m_ioff + C::MAXNB);
@@ -676,7 +695,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             tc_fence_before();
             mbar_arrive(&at_empty[a]);
             if (lrow < du) {
-                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)(d0 + lrow) * BP);
+                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)__ldg(ppos + d0 + lrow) * BP);
 #pragma unroll
                 for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]);
             }

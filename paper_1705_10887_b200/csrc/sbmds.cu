@@ -300,7 +300,7 @@ struct sbmds_ctx {
                            // 3 = the tensor-core sparse step where it applies (k_sp8.cuh), else 1
     // tensor-core sparse step (k_sp8.cuh): 128-row blocks, dense three-plane digit images of S_B
     BlkIdx s8;
-    DevBuf s8img, s8ioff, s8esc, s8yd, s8trace, s8rs1;
+    DevBuf s8img, s8ioff, s8esc, s8yd, s8trace, s8rs1, s8pos;
     int sp8_state = 0;     // 0 not built, 1 built, -1 not applicable (a dictionary > 128 entries)
     int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product,
                            // 2 = timeline of CTA 0, 4 = stream the images only, 8 = T product in the last iteration too,
@@ -755,7 +755,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     if (!pl.ok) build_pair_plan(h, pl, max_clusters[pi], C::S);
     // aux: [0] max |D| bits, [1] D exponent, [64..128) per-column max |Y1| bits, [128..192)
     // column exponents; [2] max |D| of the int8 packing, [3] its exponent
-    h->y16aux.ensure(256 * sizeof(unsigned int));   // + [192, 256): |Y2| column maxima
+    h->y16aux.ensure(352 * sizeof(unsigned int));   // + [192, 320): Y2 column max / min keys, [320, 336) exponents
     unsigned int* dmax = h->y16aux.as<unsigned int>();
     int* dexp = reinterpret_cast<int*>(dmax + 1);
     unsigned int* ymax = dmax + 64;
@@ -780,7 +780,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_SPLIT, st, [&] {
         CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
         launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
-               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, (unsigned int*)nullptr);
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, dmax + 192);
         launch(k_y16_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
                lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y16T.as<__half>(), yexp);
     });
@@ -813,7 +813,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)pl.xslot.p, (const float*)h->P.as<float>(), (const int*)dexp,
                (const int*)yexp, wvec(h), h->Y2.as<float>(), h->tpart.as<double>(),
-               h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED, (unsigned int*)nullptr);
+               h->t.as<double>(), h->counters.as<unsigned int>() + CNT_DRED, dmax + 192);
     });
     h->last_dpath = 4;
     h->last_dbytes = pl.ntiles * (int64_t)128 * 128 * 4 + 12 * h->l * (int64_t)b;
@@ -832,7 +832,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     }
     const int64_t lpad = y1t_lpad(h);
     if (!pl.ok) build_pair_plan(h, pl, h->num_sms, C::S, C::GN, true);   // one CTA per SM, both roles
-    h->y16aux.ensure(256 * sizeof(unsigned int));   // + [192, 256): |Y2| column maxima
+    h->y16aux.ensure(352 * sizeof(unsigned int));   // + [192, 320): Y2 column max / min keys, [320, 336) exponents
     unsigned int* aux = h->y16aux.as<unsigned int>();
     unsigned int* dmax8 = aux + 2;
     int* dexp8 = reinterpret_cast<int*>(aux + 3);
@@ -858,7 +858,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     profiled(h->prof, PK_SPLIT, st, [&] {
         CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
         launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
-               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, (unsigned int*)nullptr);
+               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, aux + 192);
         launch(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
                lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
     });
@@ -875,7 +875,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)nullptr, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
                wvec(h), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
-               h->counters.as<unsigned int>() + CNT_DRED, (unsigned int*)nullptr);
+               h->counters.as<unsigned int>() + CNT_DRED, aux + 192);
     });
     h->last_dpath = 3;
     h->last_dbytes = pl.ntiles * (int64_t)C::A_BYTES + 12 * h->l * (int64_t)b;
@@ -1059,19 +1059,22 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
         CK(cudaFuncSetAttribute(k_sp8_step<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr = true;
     }
-    h->y16aux.ensure(256 * sizeof(unsigned int));
-    unsigned int* y2max = h->y16aux.as<unsigned int>() + 192;
-    // column maxima of |Y2 - t| (the centred Y2 the step digitises)
-    CK(cudaMemsetAsync(y2max, 0, 64 * sizeof(unsigned int), st));
-    launch(k_colabsmax, dim3((unsigned)std::min<int64_t>(2 * 148, (h->l + 15) / 16)), dim3(256), 0, st, h->l, 16,
-           (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), y2max);
+    h->y16aux.ensure(352 * sizeof(unsigned int));
+    unsigned int* y2mm = h->y16aux.as<unsigned int>() + 192;   // Y2 column max [0, 64) / min [64, 128) keys
+    int* ey2 = reinterpret_cast<int*>(h->y16aux.as<unsigned int>() + 320);
+    if (h->last_dpath != 3 && h->last_dpath != 4) {   // the full-D reductions do not form the keys
+        CK(cudaMemsetAsync(y2mm, 0, 64 * sizeof(unsigned int), st));
+        CK(cudaMemsetAsync(y2mm + 64, 0xFF, 64 * sizeof(unsigned int), st));
+        launch(k_colminmax, dim3((unsigned)std::min<int64_t>(2 * 148, (h->l + 15) / 16)), dim3(256), 0, st, h->l, 16,
+               (const float*)h->Y2.as<float>(), y2mm);
+    }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->s8.nblk, h->num_sms));
     h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
     h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
     // Y2's digit planes (one pass over l x 16), then the step
     h->s8yd.ensure((size_t)3 * h->l * 16);
     launch(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
-           (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2max,
+           (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2mm, ey2,
            h->s8yd.as<uint8_t>());
     if (h->sp8_dbg & 2) h->s8trace.ensure(12 * 64 * sizeof(unsigned long long));
     auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
@@ -1079,7 +1082,8 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            (const int8_t*)h->s8img.as<int8_t>(),
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
            (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
-           (const unsigned int*)y2max, (const double*)h->t.as<double>(), (const float*)h->s8rs1.as<float>(), Y,
+           (const int*)ey2, (const double*)h->t.as<double>(), (const float*)h->s8rs1.as<float>(),
+           (const int32_t*)h->s8pos.as<int32_t>(), Y,
            want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
            h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr, (h->sp8_dbg & 4) ? 1 : 0);
@@ -1147,7 +1151,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         auto go_r = [&](auto kern) {
             launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
                    (const int32_t*)(s8 ? h->s8.jptr : h->bjptr).as<int32_t>(),
-                   (const int32_t*)(s8 ? h->s8.jlist : h->bjlist).as<int32_t>(),
+                   s8 ? (const int32_t*)nullptr : (const int32_t*)h->bjlist.as<int32_t>(),   // sp8: landmark-major
                    (const float*)h->P1.as<float>(), wvec(h), (const double*)h->s.as<double>(),
                    h->Y1.as<float>());
         };
@@ -1372,6 +1376,9 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
            (const uint16_t*)o.lcol.as<uint16_t>(), (const int32_t*)o.doff.as<int32_t>(),
            (const int64_t*)h->s8ioff.as<int64_t>(), h->s8img.as<int8_t>(), h->s8esc.as<int>());
     o.lcol.release();   // only the images are read from now on
+    h->s8pos.ensure(std::max<int32_t>(1, o.total_u) * sizeof(int32_t));
+    launch(k_inverse_perm, dim3(1024), dim3(256), 0, st, o.total_u, (const int32_t*)o.jlist.as<int32_t>(),
+           h->s8pos.as<int32_t>());
     h->s8rs1.ensure(h->n * sizeof(float));
     launch(k_rowsum_m1, dim3((unsigned)std::min<int64_t>(4 * 148, (h->n + 255) / 256)), dim3(256), 0, st, h->n,
            (const int32_t*)h->rp.as<int32_t>(), (const float*)h->val.as<float>(), h->s8rs1.as<float>());
@@ -1386,7 +1393,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1,
+                      &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,

@@ -216,3 +216,30 @@ def test_tensor_core_sparse_step(cfg):
     assert O.principal_angle(Va, Vb) <= 1e-3
     assert abs(ia["max_residual"] - ib["max_residual"]) <= 1e-3 * max(1.0, abs(ib["max_residual"])) + 1e-7
     assert np.array_equal(la, rep[0]) and np.array_equal(Va, rep[1])
+
+
+def test_tensor_core_sparse_step_general_s():
+    """The tensor-core sparse step with a general S (signed weights, rows not summing to 1, as the
+    paper's thresholded P_sparse): the (S 1 - 1) t^T correction and signed digits give
+    the same iteration as the fp32 kernels, and the solve converges to the oracle's eigenpairs."""
+    p = configs.config(2)
+    rng = np.random.default_rng(11)
+    val = p.val * (1.0 + 0.3 * rng.standard_normal(p.val.shape))   # some weights change sign
+    q = configs.Problem("cfg2_signed", p.n, p.l, p.row_ptr, p.col_idx, val, p.D)
+    S = O.csr(q.n, q.l, q.row_ptr, q.col_idx, q.val32())
+    assert (q.val32() < 0).any()
+    rs = np.asarray(S.sum(axis=1)).ravel()
+    assert np.abs(rs - 1).max() > 0.1
+    with handle(q) as h:
+        h.set_option("fuse", 0)
+        ref = gpu_eigs(h, 3, 16, max_iters=20, tol=0.0, seed=4)
+        h.set_option("fuse", 3)
+        a = gpu_eigs(h, 3, 16, max_iters=20, tol=0.0, seed=4)
+        assert h.stat("sp8_state") == 1
+        lam, V, Z, info = gpu_eigs(h, 3, 16, max_iters=500, tol=1e-6)
+    assert np.allclose(a[0], ref[0], rtol=1e-5), (a[0], ref[0])
+    assert O.principal_angle(a[1], ref[1]) <= 1e-3
+    assert info["converged"] == 1
+    lam_o, V_o, Z_o, _ = O.eigs_matfree(S, q.D, 3)
+    assert np.all(np.abs(lam - lam_o) <= EIG_TOL * np.abs(lam_o)), (lam, lam_o)
+    assert O.principal_angle(V, V_o) <= ANGLE_TOL
