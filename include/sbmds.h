@@ -134,18 +134,26 @@ const char* sbmds_last_error(void);
  *     "rr_period"      (>= 1) Rayleigh-Ritz every r iterations (default 5)
  *     "use_graph"      (0/1)
  *     "order_columns"  (0/1) spatial CSC column order for the S^T X gathers
- *     "dstream"        D-stream kernel for A3: 0 auto (symmetric half on CTA pairs when b in
- *                      5..32 and D has >= 8 tiles per pair, else full-D tcgen05 for b >= 5,
- *                      else FFMA), 1 FFMA, 2 full-D tcgen05 3xTF32, 3 symmetric half
- *                      (k_dstream_pair, 2xFP16; b in 5..32, else as 2)
+ *     "dstream"        D-stream kernel for A3: 0 auto (symmetric half as 24-bit fixed point on
+ *                      the int8 tensor cores when b in 5..32 and D has >= 8 tiles per 2 SMs,
+ *                      else full-D tcgen05 for b >= 5, else FFMA), 1 FFMA, 2 full-D tcgen05
+ *                      3xTF32, 3 symmetric half int8 (k_dstream_sym8), 4 symmetric half 2xFP16
+ *                      on CTA pairs (k_dstream_pair; b in 5..32, else as 2)
  *     "blocked"        bit mask: 1 = S Y2 through the row-blocked kernel, 2 = S^T X too
  *     "gram_tc"        (0/1) Gram on the FP64 tensor cores (b <= 32)
  *     "center"         (0/1, default 1) 0: sbmds_apply returns the uncentred E^ X = S D S^T X
  *                      (the BHA approximation of the squared-distance matrix;
  *                      its rows are what the error estimate of PAPER.md:309/317 compares);
  *                      sbmds_eigs always uses the centred operator
- *     "fuse"           eigs: 0 separate kernels, 1 (default) A5 fused with the Gram,
- *                      2 also the next apply's S^T partials
+ *     "fuse"           eigs: 0 separate kernels, 1 A5 fused with the Gram, 2 also the next
+ *                      apply's S^T partials, 3 (default) the tensor-core sparse step
+ *                      (k_sp8.cuh: A5 + Grams + next A2 on the int8 tensor cores from dense
+ *                      128-row digit images of S) where it applies -- b = 16 and every
+ *                      128-row block touching <= 128 landmarks -- else as 1
+ *     "sp8_dbg"        diagnostics of the tensor-core step (timing only; bits 1, 4, 8, 16 make
+ *                      results invalid): 1 skip the T product, 2 record a timeline of CTA 0
+ *                      (stats "sp8_trace_<event * 64 + block>"), 4 stream the images only,
+ *                      8 T product in the last iteration too, 16 no H' term
  *     "use_graph"      (0/1, default 0) eigs: replay Rayleigh-Ritz segments from CUDA graphs
  *     "profile"        bit mask of kernel families timed with CUDA events on the launching
  *                      stream (bit k = family k of: colsum csc dstream dreduce csr gram chol
@@ -157,7 +165,9 @@ const char* sbmds_last_error(void);
  *     "d_borrowed", "csc_bytes", "workspace_bytes", "blocked_umax" (largest per-block
  *     landmark dictionary, -1 if the row-blocked structure is off), "blocked_slots",
  *     "dstream_path" (1 FFMA, 2 full-D tcgen05, 3 symmetric half; of the last apply),
- *     "dstream_bytes" (its algorithmic bytes per launch), "<family>_ns" / "<family>_launches"
+ *     "dstream_bytes" (its algorithmic bytes per launch), "sp8_state" (tensor-core step: 1
+ *     built, -1 not applicable, 0 not tried yet), "sp8_bytes" (its S images), "sp8_umax"
+ *     (largest 128-row dictionary), "<family>_ns" / "<family>_launches"
  *     (profiled device time in ns / launch count per family since the last reset).
  * Both return SBMDS_EINVAL for an unknown key.
  */
