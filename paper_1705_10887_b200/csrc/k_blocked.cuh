@@ -250,4 +250,77 @@ __global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, co
     }
 }
 
+// A2 part 2 fused with the R^-1 fold of the eigs iteration (b = 16, LPR = 4): as k_blk_reduce
+// (landmark-major partials, fixed order), then Y1f[j] = (Y1[j] R^-1) exactly as k_y16_prep
+// forms it (fp64 fma over p <= c in order), the per-column max |Y1f| (atomicMax on the float
+// bits; cmax zeroed by the caller) and zero pad rows l..lpad; block 0 also resets the Y2 max /
+// min keys of the pair reduce (zero64, as k_y16_prep). One kernel instead of two.
+__global__ void __launch_bounds__(256) k_blk_reduce_fold(int64_t l, int64_t lpad, const int32_t* __restrict__ jptr,
+                                                         const float* __restrict__ P1, const double* __restrict__ w,
+                                                         const double* __restrict__ s, const double* __restrict__ Rinv,
+                                                         float* __restrict__ Y1f, unsigned int* __restrict__ cmax,
+                                                         unsigned int* __restrict__ zero64) {
+    constexpr int BP = 16, LPR = 4, G = 32 / LPR;
+    __shared__ double Ms[BP * BP];
+    __shared__ float mx[8][BP];
+    if (zero64 && blockIdx.x == 0 && threadIdx.x < 128) zero64[threadIdx.x] = threadIdx.x < 64 ? 0u : 0xFFFFFFFFu;
+    for (int e = threadIdx.x; e < BP * BP; e += blockDim.x) Ms[e] = Rinv[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = lane / LPR, q = lane % LPR;
+    const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    float y[4] = {0.f, 0.f, 0.f, 0.f};
+    if (j < l) {
+        const int32_t beg = jptr[j], end = jptr[j + 1];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int32_t k = beg + g;
+        for (; k + 3 * G < end; k += 4 * G) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)(k + u * G) * BP) + q);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+            }
+        }
+        for (; k < end; k += G) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)k * BP) + q);
+            a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+        }
+#pragma unroll
+        for (int o = LPR; o < 32; o <<= 1) {
+            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+            a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+        }
+        const double wj = w[j];
+        y[0] = (float)(a0 - wj * s[4 * q + 0]);
+        y[1] = (float)(a1 - wj * s[4 * q + 1]);
+        y[2] = (float)(a2 - wj * s[4 * q + 2]);
+        y[3] = (float)(a3 - wj * s[4 * q + 3]);
+    }
+    // all 16 values of the row in every lane (lane q' holds columns 4q'..4q'+3)
+    float yr[BP];
+#pragma unroll
+    for (int p = 0; p < BP; ++p) yr[p] = __shfl_sync(0xffffffffu, y[p & 3], p >> 2);
+    // lane c < 16 forms column c of the folded row (fp64 fma over p <= c, in order)
+    float f = 0.f;
+    if (lane < BP) {
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < BP; ++p)
+            if (p <= lane) acc = fma((double)yr[p], Ms[p * BP + lane], acc);
+        f = (float)acc;
+        if (j < lpad) Y1f[j * BP + lane] = f;
+        mx[wid][lane] = (j < lpad) ? fabsf(f) : 0.f;
+    }
+    __syncthreads();
+    if (threadIdx.x < BP) {
+        float m = 0.f;
+        for (int ww = 0; ww < 8; ++ww) m = fmaxf(m, mx[ww][threadIdx.x]);
+        atomicMax(cmax + threadIdx.x, __float_as_uint(m));
+    }
+}
+
 }  // namespace sbmds

@@ -284,11 +284,13 @@ inline size_t gram_smem_bytes(int b) {
 
 // ------------------------------------------------------------------ E3: Cholesky + R^-1
 // status: 0 ok, 1 ok after the shifted retry, 2 breakdown. G, Rinv are b x b row-major.
-__global__ void __launch_bounds__(256) k_chol(int b, const double* __restrict__ G, double* __restrict__ Rinv,
-                                              int* __restrict__ status) {
-    __shared__ double A[kMaxB][kMaxB + 1];
-    __shared__ int fail;
-    __shared__ double shift;
+// G = R^T R in one thread block (any blockDim >= b; every thread of the block calls it): the
+// body of k_chol, also run by the last CTA of the tensor-core sparse step (k_sp8.cuh) right
+// after it forms G. A: b x (kMaxB + 1) doubles of shared memory; fail / shift: shared scalars.
+__device__ void chol_block(int b, const double* __restrict__ G, double* __restrict__ Rinv, int* __restrict__ status,
+                           double (*A)[kMaxB + 1], int* fail_s, double* shift_s) {
+    int& fail = *fail_s;
+    double& shift = *shift_s;
     const int tid = threadIdx.x;
     for (int attempt = 0; attempt < 2; ++attempt) {
         for (int e = tid; e < b * b; e += blockDim.x) {
@@ -343,6 +345,14 @@ __global__ void __launch_bounds__(256) k_chol(int b, const double* __restrict__ 
         for (int i = 0; i < b; ++i) Rinv[i * b + c] = x[i];
     }
     if (tid == 0) *status = (shift > 0.0) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(256) k_chol(int b, const double* __restrict__ G, double* __restrict__ Rinv,
+                                              int* __restrict__ status) {
+    __shared__ double A[kMaxB][kMaxB + 1];
+    __shared__ int fail;
+    __shared__ double shift;
+    chol_block(b, G, Rinv, status, A, &fail, &shift);
 }
 
 // ------------------------------------------------------------------ E5: Rayleigh-Ritz

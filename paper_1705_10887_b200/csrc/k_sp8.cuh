@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                const float* __restrict__ rs1, const int32_t* __restrict__ ppos,
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
-               unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int stream_only) {
+               unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int stream_only,
+               double* __restrict__ Rinv_next, int* __restrict__ status) {
     using C = Sp8Cfg<BP>;
     // (diagnostics) trace[ev * 64 + i]: globaltimer of event ev for block i < 64 of CTA 0
 #define SP8_TR(ev, i)                                                                          \
@@ -886,6 +887,13 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             if constexpr (WITH_H) H[pq] = ordered_sum(part + kMaxB * kMaxB + pq, gridDim.x, kGramPart);
         }
         if (threadIdx.x == 0) *counter = 0;
+        if (Rinv_next) {   // E3 here too: G = R^T R and R^-1 for the next iteration (no extra launch)
+            __syncthreads();
+            auto A = reinterpret_cast<double (*)[kMaxB + 1]>(base);
+            int* fail = reinterpret_cast<int*>(base + kMaxB * (kMaxB + 1) * sizeof(double));
+            double* shift = reinterpret_cast<double*>(base + kMaxB * (kMaxB + 1) * sizeof(double) + 16);
+            chol_block(BP, G, Rinv_next, status, A, fail, shift);
+        }
     }
 }
 

@@ -302,6 +302,7 @@ struct sbmds_ctx {
     BlkIdx s8;
     DevBuf s8img, s8ioff, s8esc, s8yd, s8trace, s8rs1, s8pos;
     int sp8_state = 0;     // 0 not built, 1 built, -1 not applicable (a dictionary > 128 entries)
+    bool y1f_ready = false;   // the fused landmark reduce already formed Y1f (+ its column max) this apply
     int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product,
                            // 2 = timeline of CTA 0, 4 = stream the images only, 8 = T product in the last iteration too,
                            // 16 = no H' (as between Rayleigh-Ritz steps)
@@ -344,7 +345,7 @@ struct sbmds_ctx {
     DevBuf Y1, Y2, P, colpart, s, t, tpart, counters;
     int64_t y1_rows = 0;
     // eigs workspace
-    DevBuf X, Y, gpart, G, H, Rinv, status, rr, vtmp, ztmp, sign, apval, apidx, xhost, yhost, vsel;
+    DevBuf X, Y, gpart, G, H, Rinv, Rinv2, status, rr, vtmp, ztmp, sign, apval, apidx, xhost, yhost, vsel;
     // options / stats
     int rr_period = 5;
     int center = 1;          // 0: sbmds_apply computes the uncentred S D S^T X
@@ -856,9 +857,12 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         pl.b16_enc = h->Y8T.p;
     }
     profiled(h->prof, PK_SPLIT, st, [&] {
-        CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
-        launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
-               lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, aux + 192);
+        if (!h->y1f_ready) {   // (else k_blk_reduce_fold formed Y1f and its column max)
+            CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
+            launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
+                   lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, aux + 192);
+        }
+        h->y1f_ready = false;
         launch(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
                lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
     });
@@ -1043,7 +1047,8 @@ void ensure_apply_ws(sbmds_ctx* h, int bp) {
 //                  kApplyNoP1) and G = Y^T Y, s = 1^T Y (and H' = Yprev^T Y when Yprev != NULL)
 //   kApplySp8:     (with kApplyFused) the tensor-core sparse step k_sp8_step instead, and the
 //                  partials of kApplyY1Ready are its 128-row-block slots
-constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8;
+//   kApplyChol:    (with kApplySp8) the step's last CTA also factors G = R^T R into h->Rinv2
+constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8, kApplyChol = 16;
 
 bool ensure_sp8(sbmds_ctx* h, cudaStream_t st);
 
@@ -1051,7 +1056,7 @@ bool sp8_ok(sbmds_ctx* h, int b, cudaStream_t st) {
     return h->fuse == 3 && b == 16 && h->blocked && (h->use_blocked & 1) && ensure_sp8(h, st);
 }
 
-void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st) {
+void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st, bool with_chol) {
     using C = Sp8Cfg<16>;
     static bool attr = false;
     if (!attr) {
@@ -1086,7 +1091,8 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            (const int32_t*)h->s8pos.as<int32_t>(), Y,
            want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
-           h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr, (h->sp8_dbg & 4) ? 1 : 0);
+           h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr, (h->sp8_dbg & 4) ? 1 : 0,
+           with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>());
 }
 
 bool fused_ok(const sbmds_ctx* h, int b) {
@@ -1146,7 +1152,20 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     // A2: Y1 = S^T X - w s^T   (CSC SpMM by default; row-blocked partials + landmark
     // reduction when enabled: both are bound by the 64-B-per-nonzero gather traffic; inside
     // eigs the partials come from the previous fused step, leaving only the reduction)
-    if (flags & kApplyY1Ready) {
+    if ((flags & kApplyY1Ready) && (flags & kApplySp8) && b == 16 && Rinv && uses_sym(h, 16) && h->dstream != 4) {
+        // landmark reduce of the step's T partials fused with the R^-1 fold of the int8 D stream
+        const int64_t lpad = y1t_lpad(h);
+        h->Y1f.ensure((size_t)lpad * kMaxB * sizeof(float));
+        h->y16aux.ensure(352 * sizeof(unsigned int));
+        unsigned int* aux = h->y16aux.as<unsigned int>();
+        profiled(h->prof, PK_CSC, st, [&] {
+            CK(cudaMemsetAsync(aux + 64, 0, 64 * sizeof(unsigned int), st));
+            launch(k_blk_reduce_fold, dim3((unsigned)((lpad + 7) / 8)), dim3(256), 0, st, h->l, lpad,
+                   (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
+                   (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192);
+        });
+        h->y1f_ready = true;
+    } else if (flags & kApplyY1Ready) {
         const bool s8 = (flags & kApplySp8) != 0;
         auto go_r = [&](auto kern) {
             launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
@@ -1193,7 +1212,9 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     dstream(h, b, bp, st, Rinv);
     // A5: Y = -1/2 (S Y2 - 1 t^T)
     if ((flags & kApplyFused) && (flags & kApplySp8)) {
-        profiled(h->prof, PK_CSR, st, [&] { launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1) && !(h->sp8_dbg & 1), st); });
+        profiled(h->prof, PK_CSR, st, [&] {
+            launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1) && !(h->sp8_dbg & 1), st, (flags & kApplyChol) != 0);
+        });
     } else if (flags & kApplyFused) {
         const bool want_p1 = !(flags & kApplyNoP1);
         profiled(h->prof, PK_CSR, st, [&] {
@@ -1392,7 +1413,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
     DevBuf* bufs[] = {&h->rp, &h->col, &h->val, &h->cptr, &h->ridx, &h->cval, &h->order, &h->w, &h->Dbuf,
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
-                      &h->gpart, &h->G, &h->H, &h->Rinv, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
+                      &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
@@ -1819,6 +1840,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         h->G.ensure(kMaxB * kMaxB * sizeof(double));
         h->H.ensure(kMaxB * kMaxB * sizeof(double));
         h->Rinv.ensure(kMaxB * kMaxB * sizeof(double));
+        h->Rinv2.ensure(kMaxB * kMaxB * sizeof(double));
         h->status.ensure(16);
         h->rr.ensure(sizeof(RrOut));
         // Two n x b buffers alternate as Y_k (current, unnormalised) and Y_{k+1}; the
@@ -1853,7 +1875,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         auto enqueue_iteration = [&](int itx, bool do_rr) {
             if (sp8) {
                 // A5 + Grams + the next apply's S^T Y_{k+1} partials on the int8 tensor cores (k_sp8.cuh)
-                const int fl = kApplyFused | kApplySp8 | (itx > 1 ? kApplyY1Ready : 0) |
+                const int fl = kApplyFused | kApplySp8 | kApplyChol | (itx > 1 ? kApplyY1Ready : 0) |
                                (itx == max_iters && !(h->sp8_dbg & 8) ? kApplyNoP1 : 0);
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl,
                              do_rr && !(h->sp8_dbg & 16) ? Yc : nullptr);
@@ -1962,7 +1984,8 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                     break;   // Ritz vectors are X_k U = Y_k (R_k^{-1} U): Yc and Rinv stay valid
                 }
             }
-            chol(h, b, st);   // R_{k+1}^{-1}
+            if (sp8) h->Rinv.swap(h->Rinv2);   // R_{k+1}^{-1}, factored by the step's last CTA
+            else chol(h, b, st);               // R_{k+1}^{-1}
             std::swap(Yc, Yn);
             if (do_rr || it % 16 == 0) {
                 CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
