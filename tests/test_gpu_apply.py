@@ -353,3 +353,17 @@ def test_uncentred_apply(dstream, b):
         Yc = run_apply(h, X)
     assert relerr(Y, ref) <= TOL
     assert relerr(Yc, oracle_apply(p, X)) <= TOL   # the centred apply is untouched afterwards
+
+
+def test_apply_config4_full_size():
+    """Parity at BASELINE's full size (config 4: n = 1.8M, l = 50,000, k = 32, b = 16) in the
+    launch configuration the library picks by default (CSC SpMM, int8 symmetric-half D stream,
+    row-blocked CSR SpMM): every output element against the fp64 oracle's apply (~5 s on the
+    host), relative Frobenius error <= 1e-5."""
+    p = configs.config(4)
+    X = configs.x_block(p.n, 16, seed=21)
+    with make_handle(p) as h:
+        Y = run_apply(h, X)
+        assert h.stat("dstream_path") == 3
+    Yo = oracle_apply(p, X)
+    assert relerr(Y, Yo) <= TOL, relerr(Y, Yo)

@@ -243,3 +243,21 @@ def test_tensor_core_sparse_step_general_s():
     lam_o, V_o, Z_o, _ = O.eigs_matfree(S, q.D, 3)
     assert np.all(np.abs(lam - lam_o) <= EIG_TOL * np.abs(lam_o)), (lam, lam_o)
     assert O.principal_angle(V, V_o) <= ANGLE_TOL
+
+
+def test_eigs_config4_bench_configuration():
+    """The bench's solve at full size (config 4: 50 fixed iterations, m = 3, b = 16, the
+    tensor-core sparse step): the returned pairs satisfy B~ v = θ v to <= 1e-5 of |θ_1| when the
+    residual is formed by the fp64 ORACLE's apply (so each θ is within that distance of an
+    eigenvalue of B~), V is orthonormal, Z = V Λ^{1/2}, and the solve is deterministic."""
+    p = configs.config(4)
+    with handle(p) as h:
+        lam, V, Z, info = gpu_eigs(h, 3, 16, max_iters=50, tol=0.0, seed=0)
+        assert h.stat("sp8_state") == 1
+        lam2, V2, _, _ = gpu_eigs(h, 3, 16, max_iters=50, tol=0.0, seed=0)
+    assert np.array_equal(lam, lam2) and np.array_equal(V, V2)
+    assert np.abs(V.T @ V - np.eye(3)).max() < 1e-5
+    assert np.allclose(Z, V * np.sqrt(np.maximum(lam, 0))[None, :], rtol=1e-5, atol=1e-7)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    r = O.residuals(S, p.D, lam, V)
+    assert np.all(r <= 1e-5 * abs(lam[0])), (r, lam)
