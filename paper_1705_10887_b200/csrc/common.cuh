@@ -155,6 +155,14 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the eigs chain are launched with programmatic stream serialization: a kernel lets
+// its successor start launching at once (trigger) and waits for its predecessor's completion
+// and memory (wait) before touching anything an earlier kernel produced. Both are no-ops for a
+// normal launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- thread-block clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;

@@ -260,6 +260,8 @@ __global__ void __launch_bounds__(256) k_blk_reduce_fold(int64_t l, int64_t lpad
                                                          const double* __restrict__ s, const double* __restrict__ Rinv,
                                                          float* __restrict__ Y1f, unsigned int* __restrict__ cmax,
                                                          unsigned int* __restrict__ zero64) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int BP = 16, LPR = 4, G = 32 / LPR;
     __shared__ double Ms[BP * BP];
     __shared__ float mx[8][BP];

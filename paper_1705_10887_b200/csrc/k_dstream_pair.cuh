@@ -525,6 +525,8 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
                                                       const double* __restrict__ w, float* __restrict__ Y2,
                                                       double* __restrict__ tpart, double* __restrict__ t,
                                                       unsigned int* __restrict__ counter, unsigned int* __restrict__ y2mm) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double red[256];
     __shared__ float cmx[256], cmn[256];
     // column max / min of Y2 as order-preserving keys (optional; the tensor-core sparse step

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
     Sym8Event* evq = reinterpret_cast<Sym8Event*>(emptyT + S);   // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(evq + 2);
 
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t0 = cbeg[blockIdx.x], t1 = cbeg[blockIdx.x + 1];
 
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    pdl_wait();   // Y8T (k_y8_split) and the partial slots are written by earlier kernels
 
     auto tile_of = [&](int64_t t, int& I, int& J) {
         const uint32_t v = __ldg(tiles + t);
@@ -359,6 +361,8 @@ __global__ void __launch_bounds__(256) k_pack_sym8(const float* __restrict__ D, 
 __global__ void __launch_bounds__(256) k_y8_split(int64_t lpad, int bp, const float* __restrict__ Y1f,
                                                   const unsigned int* __restrict__ cmax, int8_t* __restrict__ Y8T,
                                                   int* __restrict__ yexp) {
+    pdl_trigger();
+    pdl_wait();
     const int rb = 256 / bp;
     const int r = threadIdx.x % rb, c = threadIdx.x / rb;   // consecutive threads: consecutive k
     const int e = i8_scale_exp(__uint_as_float(cmax[c]));

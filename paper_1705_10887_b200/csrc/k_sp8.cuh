@@ -248,8 +248,13 @@ __global__ void __launch_bounds__(256) k_colminmax(int64_t l, int bp, const floa
 template <int BP>
 __global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
                                                    const unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
-                                                   uint8_t* __restrict__ Yd) {
+                                                   uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
+    pdl_trigger();
+    pdl_wait();
     static_assert(BP == 16, "b = 16");
+    // zero_next: the Y1f column maxima the next iteration's k_blk_reduce_fold accumulates (this
+    // iteration's k_y8_split has read them)
+    if (zero_next && blockIdx.x == 0 && threadIdx.x < 64) zero_next[threadIdx.x] = 0u;
     float sc[BP], tc[BP];
 #pragma unroll
     for (int c = 0; c < BP; ++c) {
@@ -362,6 +367,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
     int* eyb = ey2 + BP;                                   // [4][4][BP] exponents of Y_B per block (ring) and warp
 
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b0 = blockIdx.x * nblk / gridDim.x, b1 = (blockIdx.x + 1) * nblk / gridDim.x;
     const int nb = (int)(b1 - b0);
@@ -390,7 +396,6 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         }
         fence_barrier_init();
     }
-    if (threadIdx.x < BP) ey2[threadIdx.x] = ey2in[threadIdx.x];
     // the CTA's block metadata, once: no role waits on an L2 round trip per block
     int64_t* m_ioff = reinterpret_cast<int64_t*>(base + C::OFF_META);
     int32_t* m_doff = reinterpret_cast<int32_t*>(m_ioff + C::MAXNB);
@@ -411,6 +416,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    pdl_wait();   // everything below reads what earlier kernels wrote (Y2 digits, exponents, t, P1 slots)
+    if (threadIdx.x < BP) ey2[threadIdx.x] = ey2in[threadIdx.x];
     if (warp >= 2 && warp < 14) {   // c3 groups of every accumulator start at zero
         const uint32_t lo = (uint32_t)(32 * (warp & 3)) << 16;
         if (warp < 10) {

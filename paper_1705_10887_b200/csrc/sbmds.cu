@@ -64,6 +64,24 @@ void launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args.
     CK(cudaGetLastError());
 }
 
+// Launch with programmatic stream serialization (the eigs chain kernels call pdl_trigger /
+// pdl_wait, common.cuh): the launch overlaps the predecessor's tail.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 HangRecord* g_hang_host = nullptr;
 
 // Host-mapped record the device watchdog writes before trapping (common.cuh mbar_wait).
@@ -863,12 +881,12 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
                    lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, aux + 192);
         }
         h->y1f_ready = false;
-        launch(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
-               lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
+        launch_pdl(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
+                   lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
     });
     h->P.ensure((size_t)std::max(1, pl.nslots) * 128 * BP * sizeof(float));
     profiled(h->prof, PK_DSTREAM, st, [&] {
-        launch(k_dstream_sym8<BP>, dim3(pl.P), dim3(C::THREADS), (size_t)C::SMEM, st, (const int8_t*)h->Dt8.p,
+        launch_pdl(k_dstream_sym8<BP>, dim3(pl.P), dim3(C::THREADS), (size_t)C::SMEM, st, (const int8_t*)h->Dt8.p,
                pl.bmap16, (const uint32_t*)pl.tiles.p, (const int64_t*)pl.pbeg.p, (const int*)pl.sbase.p,
                (const int*)pl.smap.p, (int)pl.NT, h->P.as<float>(), h->pair_dbg >> 1);
     });
@@ -876,7 +894,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     const int grid = (int)std::min<int64_t>(4 * kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     h->tpart.ensure((size_t)4 * kRedBlocks * kMaxB * sizeof(double));
     profiled(h->prof, PK_DREDUCE, st, [&] {
-        launch(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
+        launch_pdl(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
                (const int*)nullptr, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
                wvec(h), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
                h->counters.as<unsigned int>() + CNT_DRED, aux + 192);
@@ -1078,12 +1096,12 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
     // Y2's digit planes (one pass over l x 16), then the step
     h->s8yd.ensure((size_t)3 * h->l * 16);
-    launch(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
+    launch_pdl(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
            (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2mm, ey2,
-           h->s8yd.as<uint8_t>());
+           h->s8yd.as<uint8_t>(), h->y16aux.as<unsigned int>() + 64);
     if (h->sp8_dbg & 2) h->s8trace.ensure(12 * 64 * sizeof(unsigned long long));
     auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
-    launch(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
+    launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
            (const int8_t*)h->s8img.as<int8_t>(),
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
            (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
@@ -1159,8 +1177,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         h->y16aux.ensure(352 * sizeof(unsigned int));
         unsigned int* aux = h->y16aux.as<unsigned int>();
         profiled(h->prof, PK_CSC, st, [&] {
-            CK(cudaMemsetAsync(aux + 64, 0, 64 * sizeof(unsigned int), st));
-            launch(k_blk_reduce_fold, dim3((unsigned)((lpad + 7) / 8)), dim3(256), 0, st, h->l, lpad,
+            // (aux[64, 128), the column maxima, were zeroed by the last k_y2_digits)
+            launch_pdl(k_blk_reduce_fold, dim3((unsigned)((lpad + 7) / 8)), dim3(256), 0, st, h->l, lpad,
                    (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
                    (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192);
         });
