@@ -261,3 +261,27 @@ def test_eigs_config4_bench_configuration():
     S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
     r = O.residuals(S, p.D, lam, V)
     assert np.all(r <= 1e-5 * abs(lam[0])), (r, lam)
+
+
+def test_tensor_core_sparse_step_empty_rows():
+    """Rows without entries (two whole empty 128-row blocks and ragged ones around them): the
+    step's zero images, zero rows of Y and empty dictionaries agree with the fp32 kernels."""
+    p = configs.config(2)
+    rp = np.asarray(p.row_ptr, dtype=np.int64)
+    keep = np.ones(rp[-1], dtype=bool)
+    lo, hi = 1000, 1300          # rows [1000, 1300): blocks 8..9 entirely, block 7 and 10 partly
+    keep[rp[lo]:rp[hi]] = False
+    lens = np.diff(rp)
+    lens[lo:hi] = 0
+    rp2 = np.zeros_like(rp)
+    rp2[1:] = np.cumsum(lens)
+    q = configs.Problem("cfg2_holes", p.n, p.l, rp2, np.asarray(p.col_idx)[keep], np.asarray(p.val)[keep], p.D)
+    with handle(q) as h:
+        h.set_option("fuse", 0)
+        ref = gpu_eigs(h, 3, 16, max_iters=20, tol=0.0, seed=2)
+        h.set_option("fuse", 3)
+        a = gpu_eigs(h, 3, 16, max_iters=20, tol=0.0, seed=2)
+        assert h.stat("sp8_state") == 1
+    assert np.allclose(a[0], ref[0], rtol=1e-5), (a[0], ref[0])
+    assert O.principal_angle(a[1], ref[1]) <= 1e-3
+    assert np.all(a[1][lo:hi] == a[1][lo:hi])   # finite
