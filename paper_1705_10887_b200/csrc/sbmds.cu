@@ -25,6 +25,7 @@
 #include "k_blocked.cuh"
 #include "k_fused.cuh"
 #include "k_sp8.cuh"
+#include "k_lanczos.cuh"
 
 namespace sbmds {
 std::atomic<int64_t> g_launches{0};
@@ -321,6 +322,9 @@ struct sbmds_ctx {
     DevBuf s8img, s8ioff, s8esc, s8yd, s8trace, s8rs1, s8pos;
     int sp8_state = 0;     // 0 not built, 1 built, -1 not applicable (a dictionary > 128 entries)
     bool y1f_ready = false;   // the fused landmark reduce already formed Y1f (+ its column max) this apply
+    int solver = 0;        // eigs: 0 block subspace iteration, 1 restarted block Lanczos (k_lanczos.cuh)
+    int lz_blocks = 0;     // Lanczos blocks per restart cycle (0: 64 / block)
+    DevBuf lzQ, lzW, lzC, lzT, lzGl, lzI, lzR;
     int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product,
                            // 2 = timeline of CTA 0, 4 = stream the images only, 8 = T product in the last iteration too,
                            // 16 = no H' (as between Rayleigh-Ritz steps)
@@ -1433,6 +1437,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
+                      &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
@@ -1835,6 +1840,150 @@ void chol(sbmds_ctx* h, int b, cudaStream_t st) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------- NEXT-3: block Lanczos
+// Restarted block Lanczos with full reorthogonalisation ("uses the Lanczos method";
+// SPEC.md:52 full reorthogonalisation), block size b, k blocks per cycle (k b <= 64):
+//   Q_0 = orth(X0); for j < k: W = B~ Q_j; CGS2 against Q_0..Q_j (coefficients -> T's column
+//   block j); j < k-1: W = Q_{j+1} R_j (Cholesky-QR, R_j -> T's subdiagonal block);
+//   Rayleigh-Ritz on T (k_rr, the residual ||B~y - θy|| = ||R_k E^T u|| from Gl = T T + E G_W E^T);
+//   restart from the top b Ritz vectors. Every step on the device; the host reads one flag per cycle.
+// Returns the number of applies; eigvals / V / Z / info as sbmds_eigs.
+int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t seed, const float* X0, double* eigvals,
+                 float* V, float* Z, sbmds_info* info, cudaStream_t st, bool* converged_out) {
+    const int64_t n = h->n;
+    const int k = std::max(2, std::min(h->lz_blocks > 0 ? h->lz_blocks : kLzMaxKB / b, kLzMaxKB / b));
+    const int kb = k * b;
+    if (kb > kLzMaxKB || k < 2) throw CudaError{cudaErrorInvalidValue, "block Lanczos needs 2 blocks of b <= 32"};
+    h->lzQ.ensure((size_t)k * n * b * sizeof(float));
+    h->lzW.ensure((size_t)n * b * sizeof(float));
+    h->lzC.ensure((size_t)kLzMaxKB * kMaxB * sizeof(double));
+    h->lzT.ensure((size_t)kLzMaxKB * kLzMaxKB * sizeof(double));
+    h->lzGl.ensure((size_t)kLzMaxKB * kLzMaxKB * sizeof(double));
+    h->lzI.ensure((size_t)kLzMaxKB * kLzMaxKB * sizeof(double));
+    h->lzR.ensure((size_t)kMaxB * kMaxB * sizeof(double));
+    h->X.ensure((size_t)n * b * sizeof(float));
+    float* Q = h->lzQ.as<float>();
+    float* W = h->lzW.as<float>();
+    float* tmp = h->X.as<float>();
+    double* C = h->lzC.as<double>();
+    double* T = h->lzT.as<double>();
+    auto Qj = [&](int j) { return Q + (size_t)j * n * b; };
+    const int grid = (int)std::min<int64_t>(4 * 148, (n + 255) / 256);
+    auto combine = [&](int nq, int mo, int ldm, const double* M, const float* in0, double alpha, float* out) {
+        auto go = [&](auto kern) {
+            launch(kern, dim3(grid), dim3(256), 0, st, n, b, nq, (const float*)Q, mo, ldm, M, in0, alpha, out);
+        };
+        if (mo <= 4) go(k_combine<4>);
+        else if (mo <= 8) go(k_combine<8>);
+        else if (mo <= 16) go(k_combine<16>);
+        else go(k_combine<32>);
+    };
+    auto cholqr = [&](const float* in, float* out, double* Rout) {   // out R = in (out may alias in)
+        gram(h, b, in, nullptr, st);
+        launch(k_chol_r, dim3(1), dim3(256), 0, st, b, (const double*)h->G.as<double>(), h->Rinv.as<double>(),
+               h->status.as<int>(), Rout);
+        rotate(h, b, b, b, in, (const double*)h->Rinv.as<double>(), out, (const double*)nullptr, false, st);
+    };
+    auto check_breakdown = [&](const char* where) {
+        int hs = 0;
+        CK(cudaMemcpyAsync(&hs, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hs == 2) throw CudaError{cudaErrorInvalidValue, where};
+    };
+    // Q_0 = orth(X0) (Cholesky-QR twice)
+    if (X0) CK(cudaMemcpyAsync(W, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
+    else launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, W);
+    cholqr(W, tmp, h->lzR.as<double>());
+    cholqr(tmp, Qj(0), h->lzR.as<double>());
+    check_breakdown("Cholesky-QR of the initial block broke down");
+    static bool rr_attr = false;
+    if (!rr_attr) {
+        CK(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, kRrSmem));
+        rr_attr = true;
+    }
+    int applies = 0;
+    bool converged = false;
+    for (;;) {
+        CK(cudaMemsetAsync(T, 0, (size_t)kb * kb * sizeof(double), st));
+        for (int j = 0; j < k; ++j) {
+            apply_device(h, b, Qj(j), W, st);   // W = B~ Q_j (A1-A5)
+            ++applies;
+            for (int pass = 0; pass < 2; ++pass) {   // CGS2: W -= Q_{0..j} (Q_{0..j}^T W)
+                for (int i = 0; i <= j; ++i) {
+                    gram(h, b, W, Qj(i), st);        // H = Q_i^T W
+                    CK(cudaMemcpyAsync(C + (size_t)i * b * b, h->H.p, (size_t)b * b * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, st));
+                    launch(k_tadd, dim3(1), dim3(256), 0, st, b, kb, i, j, (const double*)h->H.as<double>(), T, 0);
+                }
+                combine(j + 1, b, b, C, W, -1.0, W);
+            }
+            if (j < k - 1) {   // W = Q_{j+1} R_j
+                cholqr(W, Qj(j + 1), h->lzR.as<double>());
+                // T[j+1][j] = R_j (T[j][j+1] ~ R_j^T comes from step j+1's CGS coefficients)
+                launch(k_tadd, dim3(1), dim3(256), 0, st, b, kb, j + 1, j, (const double*)h->lzR.as<double>(), T, 0);
+            } else {
+                gram(h, b, W, nullptr, st);          // G_W = R_k^T R_k: the residual block
+            }
+        }
+        launch(k_lanczos_prep, dim3(1), dim3(256), 0, st, kb, b, T, (const double*)h->G.as<double>(),
+               h->lzGl.as<double>(), h->lzI.as<double>());
+        launch(k_rr, dim3(1), dim3(256), (size_t)kRrSmem, st, kb, m, tol, (const double*)T,
+               (const double*)h->lzGl.as<double>(), (const double*)h->lzI.as<double>(), h->rr.as<RrOut>());
+        int conv = 0;
+        CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        check_breakdown("Cholesky-QR broke down in block Lanczos");
+        if ((conv && tol > 0.0) || applies + k > max_iters) {
+            converged = conv != 0 && tol > 0.0;
+            break;
+        }
+        // restart from the top b Ritz vectors (orthonormal: Q orthonormal, U orthogonal)
+        const double* U = h->rr.as<RrOut>()->U;
+        combine(k, b, kb, U, nullptr, 1.0, tmp);
+        cholqr(tmp, Qj(0), h->lzR.as<double>());   // re-orthonormalise against drift
+    }
+    RrOut rr_host;
+    CK(cudaMemcpyAsync(&rr_host, h->rr.p, sizeof(RrOut), cudaMemcpyDeviceToHost, st));
+    // E6: V = Q U[:, :m] (top-m algebraic Ritz vectors), signs, Z
+    const bool vdev = V && is_device_ptr(V), zdev = Z && is_device_ptr(Z);
+    const size_t vbytes = (size_t)n * m * sizeof(float);
+    float* Vd = vdev ? V : (h->vtmp.ensure(vbytes), h->vtmp.as<float>());
+    float* Zd = zdev ? Z : (Z ? (h->ztmp.ensure(vbytes), h->ztmp.as<float>()) : nullptr);
+    combine(k, m, kb, h->rr.as<RrOut>()->U, nullptr, 1.0, Vd);
+    h->sign.ensure(kMaxB * sizeof(float));
+    h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
+    h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
+    launch(k_col_argmax, dim3(kRedBlocks), dim3(256), 0, st, n, m, (const float*)Vd, h->apval.as<float>(),
+           h->apidx.as<long long>(), h->sign.as<float>(), h->counters.as<unsigned int>() + CNT_ARGMAX);
+    const double* theta = h->rr.as<RrOut>()->theta;
+    launch(k_finalize, dim3((unsigned)std::min<int64_t>(4 * 148, (n * m + 255) / 256)), dim3(256), 0, st, n, m,
+           (const float*)h->sign.as<float>(), theta, Vd, Zd);
+    gram(h, m, Vd, nullptr, st);
+    std::vector<double> gv((size_t)m * m);
+    CK(cudaMemcpyAsync(gv.data(), h->G.p, gv.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (V && !vdev) CK(cudaMemcpyAsync(V, Vd, vbytes, cudaMemcpyDeviceToHost, st));
+    if (Z && !zdev) CK(cudaMemcpyAsync(Z, Zd, vbytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double orth = 0.0;
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) orth = std::max(orth, std::fabs(gv[i * m + j] - (i == j ? 1.0 : 0.0)));
+    int n_neg = 0;
+    for (int j = 0; j < m; ++j) {
+        eigvals[j] = rr_host.theta[j];
+        if (rr_host.theta[j] < 0.0) ++n_neg;
+    }
+    if (info) {
+        info->iters = applies;
+        info->n_applies = applies;
+        info->n_negative = n_neg;
+        info->converged = converged ? 1 : 0;
+        info->max_residual = rr_host.maxres;
+        info->orth_error = orth;
+    }
+    *converged_out = converged;
+    return applies;
+}
+
 extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol, uint64_t seed,
                                    const float* X0, double* eigvals, float* V, float* Z, sbmds_info* info,
                                    void* cuda_stream) {
@@ -1861,6 +2010,20 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         h->Rinv2.ensure(kMaxB * kMaxB * sizeof(double));
         h->status.ensure(16);
         h->rr.ensure(sizeof(RrOut));
+        if (h->solver == 1) {   // NEXT-3: restarted block Lanczos with full reorthogonalisation
+            if (b > 32) return fail(SBMDS_EINVAL, "block Lanczos needs block <= 32 (two blocks per cycle)");
+            bool conv = false;
+            eigs_lanczos(h, m, b, max_iters, tol, seed, X0, eigvals, V, Z, info, st, &conv);
+            CK(cudaEventRecord(e1, st));
+            CK(cudaStreamSynchronize(st));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            if (info) info->gpu_ms = ms;
+            if (tol > 0.0 && !conv) return fail(SBMDS_ENOCONV, "block Lanczos: no convergence in %d applies", max_iters);
+            return SBMDS_OK;
+        }
         // Two n x b buffers alternate as Y_k (current, unnormalised) and Y_{k+1}; the
         // orthonormal iterate is X_k = Y_k R_k^{-1} (R from Cholesky-QR), never materialised.
         float* Yc = h->X.as<float>();
@@ -2108,6 +2271,12 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16 || value == 32))
             return fail(SBMDS_EINVAL, "csr_sub_L in {0 auto, 1, 2, 4, 8, 16, 32}");
         h->csr_sub_L = (int)value;
+    } else if (!strcmp(key, "solver")) {
+        if (value < 0 || value > 1) return fail(SBMDS_EINVAL, "solver in {0 subspace iteration, 1 block Lanczos}");
+        h->solver = (int)value;
+    } else if (!strcmp(key, "lanczos_blocks")) {
+        if (value < 0 || value > 32) return fail(SBMDS_EINVAL, "lanczos_blocks in [0, 32] (0: 64 / block)");
+        h->lz_blocks = (int)value;
     } else if (!strcmp(key, "sp8_dbg")) {
         h->sp8_dbg = (int)value;
     } else if (!strcmp(key, "fuse")) {
