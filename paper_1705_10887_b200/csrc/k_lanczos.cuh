@@ -90,4 +90,30 @@ __global__ void __launch_bounds__(256) k_lanczos_prep(int kb, int b, double* __r
     }
 }
 
+// Lanczos residuals without cancellation: B~ (Q u_i) - θ_i (Q u_i) = W_k R_k E^T u_i with W_k
+// orthonormal, so r_i = ||R_k u_i[last block]|| (R_k from the Cholesky-QR of the final
+// residual block); overwrites k_rr's residuals, max residual and convergence flag.
+__global__ void k_lanczos_resid(int kb, int b, int m, double tol, const double* __restrict__ R, RrOut* __restrict__ rr) {
+    __shared__ double res[kLzMaxKB];
+    const int o = kb - b;
+    for (int i = threadIdx.x; i < kb; i += blockDim.x) {
+        double s2 = 0.0;
+        for (int p = 0; p < b; ++p) {
+            double acc = 0.0;
+            for (int q = p; q < b; ++q) acc = fma(R[p * b + q], rr->U[(o + q) * kb + i], acc);
+            s2 = fma(acc, acc, s2);
+        }
+        res[i] = sqrt(s2);
+        rr->resid[i] = res[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tmax = 0.0, rmax = 0.0;
+        for (int i = 0; i < kb; ++i) tmax = fmax(tmax, fabs(rr->theta[i]));
+        for (int i = 0; i < m; ++i) rmax = fmax(rmax, res[i]);
+        rr->maxres = tmax > 0.0 ? rmax / tmax : rmax;
+        rr->converged = (tol > 0.0 && rr->maxres <= tol) ? 1 : 0;
+    }
+}
+
 }  // namespace sbmds

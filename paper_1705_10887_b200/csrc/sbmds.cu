@@ -1921,14 +1921,18 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
                 cholqr(W, Qj(j + 1), h->lzR.as<double>());
                 // T[j+1][j] = R_j (T[j][j+1] ~ R_j^T comes from step j+1's CGS coefficients)
                 launch(k_tadd, dim3(1), dim3(256), 0, st, b, kb, j + 1, j, (const double*)h->lzR.as<double>(), T, 0);
-            } else {
-                gram(h, b, W, nullptr, st);          // G_W = R_k^T R_k: the residual block
+            } else {   // the residual block: G_W = R_k^T R_k (for Gl) and R_k itself
+                gram(h, b, W, nullptr, st);
+                launch(k_chol_r, dim3(1), dim3(256), 0, st, b, (const double*)h->G.as<double>(), h->Rinv2.as<double>(),
+                       h->status.as<int>() + 1, h->lzR.as<double>());
             }
         }
         launch(k_lanczos_prep, dim3(1), dim3(256), 0, st, kb, b, T, (const double*)h->G.as<double>(),
                h->lzGl.as<double>(), h->lzI.as<double>());
         launch(k_rr, dim3(1), dim3(256), (size_t)kRrSmem, st, kb, m, tol, (const double*)T,
                (const double*)h->lzGl.as<double>(), (const double*)h->lzI.as<double>(), h->rr.as<RrOut>());
+        launch(k_lanczos_resid, dim3(1), dim3(64), 0, st, kb, b, m, tol, (const double*)h->lzR.as<double>(),
+               h->rr.as<RrOut>());
         int conv = 0;
         CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
