@@ -150,6 +150,10 @@ const char* sbmds_last_error(void);
  *                      (k_sp8.cuh: A5 + Grams + next A2 on the int8 tensor cores from dense
  *                      128-row digit images of S) where it applies -- b = 16 and every
  *                      128-row block touching <= 128 landmarks -- else as 1
+ *     "solver"         eigs: 0 (default) block subspace iteration; 1 restarted block Lanczos with
+ *                      full reorthogonalisation (block <= 32, k
+ *                      blocks of b per cycle with k b <= 64; max_iters counts block applies)
+ *     "lanczos_blocks" blocks per Lanczos cycle (0 = 64 / block, at least 2)
  *     "sp8_dbg"        diagnostics of the tensor-core step (timing only; bits 1, 4, 8, 16 make
  *                      results invalid): 1 skip the T product, 2 record a timeline of CTA 0
  *                      (stats "sp8_trace_<event * 64 + block>"), 4 stream the images only,
