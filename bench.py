@@ -216,6 +216,26 @@ def run_ours(args, ws, rank, local):
     # parity spot check at full size: eigenvalues of the timed solves are deterministic
     lam, _, _, info = step()
 
+    # the second-largest kernel family, outside the timed region: the tensor-core sparse step
+    # (A5 + Grams + next A2), CUDA events around its launches during one more solve
+    sparse = None
+    if h.stat("sp8_state") == 1:
+        h.set_option("profile", 1 << 4)       # family "csr" = the sparse step (+ its Y2-digit pass)
+        h.set_option("profile_reset", 1)
+        step()
+        torch.cuda.synchronize()
+        sp_ns, sp_n = h.stat("csr_ns"), h.stat("csr_launches")
+        h.set_option("profile", 0)
+        slots = h.stat("sp8_slots")
+        # bytes the step must move per launch: the S images once, Y written once (n x b fp32), the
+        # T partials written (one fp32 row of b per 128-row dictionary entry) and the gathered Y2
+        # digit rows (48 B per entry)
+        sp_bytes = h.stat("sp8_bytes") + 4 * p.n * b + (4 * b + 48) * slots
+        sp_s = sp_ns / max(sp_n, 1) / 1e9
+        sparse = {"kernel": "k_sp8_step (tcgen05 kind::i8 on dense 128-row images of S)", "launches": int(sp_n),
+                  "avg_launch_ms": sp_s * 1e3, "algorithmic_bytes_per_launch": int(sp_bytes),
+                  "achieved_gbs": sp_bytes / sp_s / 1e9, "frac_of_hbm_peak": sp_bytes / sp_s / 1e9 / hbm_peak}
+
     # ---- end to end through the C ABI from pinned HOST buffers (create + eigs + D2H)
     e2e = None
     if not args.no_e2e:
@@ -284,6 +304,8 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": int(n_launch),
         "clocks": clk.summary(),
     }
+    if sparse:
+        out["sparse_step"] = sparse
     if e2e:
         out["e2e"] = e2e
     if cpu:

@@ -1848,6 +1848,10 @@ void chol(sbmds_ctx* h, int b, cudaStream_t st) {
 //   Rayleigh-Ritz on T (k_rr, the residual ||B~y - θy|| = ||R_k E^T u|| from Gl = T T + E G_W E^T);
 //   restart from the top b Ritz vectors. Every step on the device; the host reads one flag per cycle.
 // Returns the number of applies; eigvals / V / Z / info as sbmds_eigs.
+struct LanczosBreakdown {
+    const char* what;
+};
+
 int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t seed, const float* X0, double* eigvals,
                  float* V, float* Z, sbmds_info* info, cudaStream_t st, bool* converged_out) {
     const int64_t n = h->n;
@@ -1888,7 +1892,7 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
         int hs = 0;
         CK(cudaMemcpyAsync(&hs, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (hs == 2) throw CudaError{cudaErrorInvalidValue, where};
+        if (hs == 2) throw LanczosBreakdown{where};
     };
     // Q_0 = orth(X0) (Cholesky-QR twice)
     if (X0) CK(cudaMemcpyAsync(W, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
@@ -2015,15 +2019,24 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         h->status.ensure(16);
         h->rr.ensure(sizeof(RrOut));
         if (h->solver == 1) {   // NEXT-3: restarted block Lanczos with full reorthogonalisation
+            struct EvGuard {
+                cudaEvent_t a, b;
+                ~EvGuard() {
+                    cudaEventDestroy(a);
+                    cudaEventDestroy(b);
+                }
+            } evg{e0, e1};
             if (b > 32) return fail(SBMDS_EINVAL, "block Lanczos needs block <= 32 (two blocks per cycle)");
             bool conv = false;
-            eigs_lanczos(h, m, b, max_iters, tol, seed, X0, eigvals, V, Z, info, st, &conv);
+            try {
+                eigs_lanczos(h, m, b, max_iters, tol, seed, X0, eigvals, V, Z, info, st, &conv);
+            } catch (const LanczosBreakdown& e) {
+                return fail(SBMDS_EBREAKDOWN, "%s", e.what);
+            }
             CK(cudaEventRecord(e1, st));
             CK(cudaStreamSynchronize(st));
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, e0, e1));
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
             if (info) info->gpu_ms = ms;
             if (tol > 0.0 && !conv) return fail(SBMDS_ENOCONV, "block Lanczos: no convergence in %d applies", max_iters);
             return SBMDS_OK;
@@ -2315,6 +2328,7 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a
     else if (!strcmp(key, "sp8_bytes")) *value = h->s8_bytes;           // its S images (HBM bytes per pass)
     else if (!strcmp(key, "sp8_umax")) *value = h->sp8_state > 0 ? (int64_t)h->s8.umax : -1;
+    else if (!strcmp(key, "sp8_slots")) *value = h->sp8_state > 0 ? (int64_t)h->s8.total_u : -1;   // 128-row dictionary entries
     else if (!strncmp(key, "sp8_trace_", 10)) {   // (diagnostics, sp8_dbg & 2) event timestamps of CTA 0
         const int k = atoi(key + 10);
         if (k < 0 || k >= 12 * 64 || !h->s8trace.p) return fail(SBMDS_EINVAL, "no sp8 trace");
