@@ -260,9 +260,13 @@ __global__ void __launch_bounds__(256) k_blk_reduce_fold(int64_t l, int64_t lpad
                                                          const double* __restrict__ s, const double* __restrict__ Rinv,
                                                          float* __restrict__ Y1f, unsigned int* __restrict__ cmax,
                                                          unsigned int* __restrict__ zero64) {
+    // Persistent: warp W takes landmarks j = W, W + nw, ... and software-pipelines them -- the
+    // first 6 slot groups of the next landmark (48 slots) are in flight while the current one is
+    // summed and folded, and its slot range two landmarks ahead. The per-landmark summation order
+    // is the plain kernel's (lane group g: slots g, g + 8, ... in order; then the group tree).
     pdl_trigger();
     pdl_wait();
-    constexpr int BP = 16, LPR = 4, G = 32 / LPR;
+    constexpr int BP = 16, LPR = 4, G = 32 / LPR, PF = 6;
     __shared__ double Ms[BP * BP];
     __shared__ float mx[8][BP];
     if (zero64 && blockIdx.x == 0 && threadIdx.x < 128) zero64[threadIdx.x] = threadIdx.x < 64 ? 0u : 0xFFFFFFFFu;
@@ -270,53 +274,83 @@ __global__ void __launch_bounds__(256) k_blk_reduce_fold(int64_t l, int64_t lpad
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = lane / LPR, q = lane % LPR;
-    const int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    float y[4] = {0.f, 0.f, 0.f, 0.f};
-    if (j < l) {
-        const int32_t beg = jptr[j], end = jptr[j + 1];
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int32_t k = beg + g;
-        for (; k + 3 * G < end; k += 4 * G) {
-            float4 v[4];
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    float cm = 0.f;   // this lane's running max |Y1f| of column `lane` (lanes < 16)
+    auto range = [&](int64_t jj, int32_t& b0, int32_t& e0) {
+        if (jj < l) {
+            b0 = __ldg(jptr + jj);
+            e0 = __ldg(jptr + jj + 1);
+        } else {
+            b0 = e0 = 0;
+        }
+    };
+    auto prefetch = [&](int32_t b0, int32_t e0, float4 (&v)[PF]) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)(k + u * G) * BP) + q);
+        for (int u = 0; u < PF; ++u) {
+            const int32_t k = b0 + g + u * G;
+            v[u] = k < e0 ? __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)k * BP) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    int32_t beg, end, nbeg, nend;
+    range(j, beg, end);
+    range(j + nw, nbeg, nend);
+    float4 v[PF];
+    prefetch(beg, end, v);
+    for (; j < lpad; j += nw) {
+        // next landmark's slots in flight, the one after next's range requested
+        float4 vn[PF];
+        prefetch(nbeg, nend, vn);
+        int32_t nnbeg, nnend;
+        range(j + 2 * nw, nnbeg, nnend);
+        float y[4] = {0.f, 0.f, 0.f, 0.f};
+        if (j < l) {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+            for (int u = 0; u < PF; ++u) {
+                if (beg + g + u * G < end) {
+                    a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+                }
             }
+            for (int32_t k = beg + g + PF * G; k < end; k += G) {   // beyond the prefetched slots
+                const float4 t = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)k * BP) + q);
+                a0 += t.x; a1 += t.y; a2 += t.z; a3 += t.w;
+            }
+#pragma unroll
+            for (int o = LPR; o < 32; o <<= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+                a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+            }
+            const double wj = w[j];
+            y[0] = (float)(a0 - wj * s[4 * q + 0]);
+            y[1] = (float)(a1 - wj * s[4 * q + 1]);
+            y[2] = (float)(a2 - wj * s[4 * q + 2]);
+            y[3] = (float)(a3 - wj * s[4 * q + 3]);
         }
-        for (; k < end; k += G) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)k * BP) + q);
-            a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+        // all 16 values of the row in every lane (lane q' holds columns 4q'..4q'+3)
+        float yr[BP];
+#pragma unroll
+        for (int p = 0; p < BP; ++p) yr[p] = __shfl_sync(0xffffffffu, y[p & 3], p >> 2);
+        // lane c < 16 forms column c of the folded row (fp64 fma over p <= c, in order)
+        if (lane < BP) {
+            double acc = 0.0;
+#pragma unroll
+            for (int p = 0; p < BP; ++p)
+                if (p <= lane) acc = fma((double)yr[p], Ms[p * BP + lane], acc);
+            const float f = (float)acc;
+            Y1f[j * BP + lane] = f;
+            cm = fmaxf(cm, fabsf(f));
         }
 #pragma unroll
-        for (int o = LPR; o < 32; o <<= 1) {
-            a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-            a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-            a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-            a3 += __shfl_xor_sync(0xffffffffu, a3, o);
-        }
-        const double wj = w[j];
-        y[0] = (float)(a0 - wj * s[4 * q + 0]);
-        y[1] = (float)(a1 - wj * s[4 * q + 1]);
-        y[2] = (float)(a2 - wj * s[4 * q + 2]);
-        y[3] = (float)(a3 - wj * s[4 * q + 3]);
+        for (int u = 0; u < PF; ++u) v[u] = vn[u];
+        beg = nbeg;
+        end = nend;
+        nbeg = nnbeg;
+        nend = nnend;
     }
-    // all 16 values of the row in every lane (lane q' holds columns 4q'..4q'+3)
-    float yr[BP];
-#pragma unroll
-    for (int p = 0; p < BP; ++p) yr[p] = __shfl_sync(0xffffffffu, y[p & 3], p >> 2);
-    // lane c < 16 forms column c of the folded row (fp64 fma over p <= c, in order)
-    float f = 0.f;
-    if (lane < BP) {
-        double acc = 0.0;
-#pragma unroll
-        for (int p = 0; p < BP; ++p)
-            if (p <= lane) acc = fma((double)yr[p], Ms[p * BP + lane], acc);
-        f = (float)acc;
-        if (j < lpad) Y1f[j * BP + lane] = f;
-        mx[wid][lane] = (j < lpad) ? fabsf(f) : 0.f;
-    }
+    if (lane < BP) mx[wid][lane] = cm;
     __syncthreads();
     if (threadIdx.x < BP) {
         float m = 0.f;

@@ -1182,7 +1182,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         unsigned int* aux = h->y16aux.as<unsigned int>();
         profiled(h->prof, PK_CSC, st, [&] {
             // (aux[64, 128), the column maxima, were zeroed by the last k_y2_digits)
-            launch_pdl(k_blk_reduce_fold, dim3((unsigned)((lpad + 7) / 8)), dim3(256), 0, st, h->l, lpad,
+            launch_pdl(k_blk_reduce_fold, dim3((unsigned)std::min<int64_t>(3 * (int64_t)h->num_sms, (lpad + 7) / 8)),
+                       dim3(256), 0, st, h->l, lpad,
                    (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
                    (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192);
         });
