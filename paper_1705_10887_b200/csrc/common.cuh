@@ -262,7 +262,15 @@ __device__ __forceinline__ void ordered_colsum_block(const double* __restrict__ 
     if (k < nk) {
         const int per = (count + nk - 1) / nk, q0 = k * per, q1 = min(count, q0 + per);
         double a = 0.0;
-        for (int q = q0; q < q1; ++q) a += p[(int64_t)q * stride + c];
+        int q = q0;
+        for (; q + 8 <= q1; q += 8) {   // eight loads in flight, added in index order (same result)
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = p[(int64_t)(q + u) * stride + c];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a += v[u];
+        }
+        for (; q < q1; ++q) a += p[(int64_t)q * stride + c];
         chunk[k * ncols + c] = a;
     }
     __syncthreads();

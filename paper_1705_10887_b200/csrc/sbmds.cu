@@ -2329,6 +2329,7 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a
     else if (!strcmp(key, "sp8_bytes")) *value = h->s8_bytes;           // its S images (HBM bytes per pass)
     else if (!strcmp(key, "sp8_umax")) *value = h->sp8_state > 0 ? (int64_t)h->s8.umax : -1;
+    else if (!strcmp(key, "dstream_slots")) *value = h->s8plan[1].nslots;   // int8 D stream partial slots (b = 16)
     else if (!strcmp(key, "sp8_slots")) *value = h->sp8_state > 0 ? (int64_t)h->s8.total_u : -1;   // 128-row dictionary entries
     else if (!strncmp(key, "sp8_trace_", 10)) {   // (diagnostics, sp8_dbg & 2) event timestamps of CTA 0
         const int k = atoi(key + 10);
