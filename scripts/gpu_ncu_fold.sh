@@ -1,5 +1,5 @@
 export SBMDS_GEN_CACHE=/root/.cache/sbmds_gen
 mkdir -p gpurun_out
 python scripts/eigs_once.py 4 6 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_blk_reduce_fold -s 2 -c 1 -o gpurun_out/prof_fold python scripts/eigs_once.py 4 6 > gpurun_out/ncu_fold.log 2>&1
-tail -2 gpurun_out/ncu_fold.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dreduce_pair -s 2 -c 1 -o gpurun_out/prof_dred python scripts/eigs_once.py 4 6 > gpurun_out/ncu_dred.log 2>&1
+tail -2 gpurun_out/ncu_dred.log
