@@ -157,7 +157,23 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 // ------------------------------------------------------------------ create: images
 // One CTA (128 threads) per 128-row block: eS_B from the block's largest |S_ij|, then each
 // thread writes the three digits of its row's entries into the zero-filled image (planes of
-// 128 x d_pad bytes at img + off[B]).
+// 128 x d_pad bytes at img + off[B]). Repeated (row, column) entries are summed first (as the
+// CSR SpMM does), in entry order, before digitising.
+__device__ __forceinline__ bool sp8_first_of_col(const uint16_t* __restrict__ lcol, int32_t beg, int32_t e) {
+    const uint16_t c = lcol[e];
+    for (int32_t e2 = beg; e2 < e; ++e2)
+        if (lcol[e2] == c) return false;
+    return true;
+}
+__device__ __forceinline__ float sp8_col_sum(const uint16_t* __restrict__ lcol, const float* __restrict__ val,
+                                             int32_t e, int32_t end) {
+    const uint16_t c = lcol[e];
+    float v = 0.f;
+    for (int32_t e2 = e; e2 < end; ++e2)
+        if (lcol[e2] == c) v += val[e2];
+    return v;
+}
+
 __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, const int32_t* __restrict__ rp,
                                                    const float* __restrict__ val, const uint16_t* __restrict__ lcol,
                                                    const int32_t* __restrict__ doff, const int64_t* __restrict__ ioff,
@@ -169,7 +185,8 @@ __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, cons
         const int r = threadIdx.x;
         const int32_t beg = r < rows ? rp[r0 + r] : 0, end = r < rows ? rp[r0 + r + 1] : 0;
         float m = 0.f;
-        for (int32_t e = beg; e < end; ++e) m = fmaxf(m, fabsf(val[e]));
+        for (int32_t e = beg; e < end; ++e)
+            if (sp8_first_of_col(lcol, beg, e)) m = fmaxf(m, fabsf(sp8_col_sum(lcol, val, e, end)));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
@@ -183,8 +200,9 @@ __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, cons
         const int dp = sp8_dpad(doff[B + 1] - doff[B]);
         int8_t* out = img + ioff[B];
         for (int32_t e = beg; e < end; ++e) {
+            if (!sp8_first_of_col(lcol, beg, e)) continue;
             int d0, d1, d2;
-            digits3(__float2int_rn(ldexpf(val[e], eS)), d0, d1, d2);
+            digits3(__float2int_rn(ldexpf(sp8_col_sum(lcol, val, e, end), eS)), d0, d1, d2);
             const int o = sp8_off(r, (int)lcol[e], kSp8RB / 8);
             out[o] = (int8_t)d0;
             out[kSp8RB * dp + o] = (int8_t)d1;

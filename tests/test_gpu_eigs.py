@@ -306,3 +306,26 @@ def test_block_lanczos_matches_oracle(cfg):
     assert info["status"] == 0 and info["converged"] == 1
     check_against(lam, V, Z, lam_o, V_o, Z_o)
     assert np.array_equal(lam, lam2) and np.array_equal(V, V2)
+
+
+def test_tensor_core_sparse_step_duplicate_entries():
+    """Repeated (row, column) entries in S (allowed by the CSR input, summed by every SpMM): the
+    tensor-core step's images sum them too, so its iteration matches the fp32 kernels."""
+    p = configs.config(2)
+    rp = np.asarray(p.row_ptr, dtype=np.int64)
+    ci = np.asarray(p.col_idx).copy()
+    val = np.asarray(p.val, dtype=np.float64).copy()
+    rows = np.arange(0, p.n, 7)                      # every 7th row: its 2nd entry repeats its 1st column
+    has2 = (rp[rows + 1] - rp[rows]) >= 2
+    e1 = rp[rows[has2]]
+    ci[e1 + 1] = ci[e1]
+    val[e1 + 1] *= 0.5
+    q = configs.Problem("cfg2_dups", p.n, p.l, rp, ci, val, p.D)
+    with handle(q) as h:
+        h.set_option("fuse", 0)
+        ref = gpu_eigs(h, 3, 16, max_iters=20, tol=0.0, seed=6)
+        h.set_option("fuse", 3)
+        a = gpu_eigs(h, 3, 16, max_iters=20, tol=0.0, seed=6)
+        assert h.stat("sp8_state") == 1
+    assert np.allclose(a[0], ref[0], rtol=1e-5), (a[0], ref[0])
+    assert O.principal_angle(a[1], ref[1]) <= 1e-3
