@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -103,6 +104,27 @@ void install_hang_record() {
     }
     g_hang_host = hp;
     done = true;
+}
+
+// Small device -> host readbacks during create go through a host-mapped buffer written by a
+// kernel, not a copy: a D2H copy would queue behind the host D's multi-GB upload on the copy
+// engines and stall the S-side builds that overlap it.
+__global__ void k_peek(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst, int bytes) {
+    for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+
+void peek_to_host(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
+    static unsigned char* hbuf = nullptr;
+    static unsigned char* dbuf = nullptr;
+    if (!hbuf) {
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&hbuf), 4096, cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dbuf), hbuf, 0));
+    }
+    if (bytes > 4096) throw CudaError{cudaErrorInvalidValue, "peek_to_host"};
+    k_peek<<<1, 128, 0, st>>>(reinterpret_cast<const unsigned char*>(dev_src), dbuf, (int)bytes);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    memcpy(host_dst, hbuf, bytes);
 }
 
 std::string hang_note() {
@@ -1306,8 +1328,7 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
     CK(cub::DeviceScan::InclusiveSum(tmp2.p, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)nnz, st));
     g_launches.fetch_add(1);
     int32_t total_u = 0;
-    CK(cudaMemcpyAsync(&total_u, incl.as<int32_t>() + nnz - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    peek_to_host(&total_u, incl.as<int32_t>() + nnz - 1, sizeof(int32_t), st);
     o.total_u = total_u;
     o.doff.ensure((nb + 1) * sizeof(int32_t));
     o.dict.ensure(std::max<int64_t>(1, total_u) * sizeof(int32_t));
@@ -1353,8 +1374,7 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
     launch(k_col_ptr, dim3((unsigned)((l + 256) / 256)), dim3(256), 0, st, l, total_u,
            (const int32_t*)keys2.as<int32_t>(), o.jptr.as<int32_t>());
     unsigned int umax = 0;
-    CK(cudaMemcpyAsync(&umax, um.p, sizeof umax, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    peek_to_host(&umax, um.p, sizeof umax, st);
     o.umax = umax;
 }
 
@@ -1410,8 +1430,7 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, sizes.as<int64_t>(), h->s8ioff.as<int64_t>(), (int)(o.nblk + 1), st));
     g_launches.fetch_add(1);
     int64_t total = 0;
-    CK(cudaMemcpyAsync(&total, h->s8ioff.as<int64_t>() + o.nblk, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    peek_to_host(&total, h->s8ioff.as<int64_t>() + o.nblk, sizeof(int64_t), st);
     h->s8img.ensure((size_t)total + 64 * 1024);   // + slack: the T product's M = 128 rows read past a short image
     CK(cudaMemsetAsync(h->s8img.p, 0, h->s8img.bytes, st));
     h->s8esc.ensure(o.nblk * sizeof(int));
@@ -1472,6 +1491,15 @@ void destroy_ctx(sbmds_ctx* h) {
 extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const int64_t* row_ptr,
                                      const int32_t* col_idx, const float* val, const float* D_ll, uint32_t flags,
                                      void* cuda_stream, sbmds_t* out) {
+    // (diagnostics) SBMDS_TRACE_CREATE=1: host-clock phase times of this create on stderr
+    static const bool trace_create = getenv("SBMDS_TRACE_CREATE") != nullptr;
+    const auto t_create0 = std::chrono::steady_clock::now();
+    auto tphase = [&](const char* what) {
+        if (!trace_create) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create0).count();
+        fprintf(stderr, "[sbmds_create] %8.2f ms  %s\n", ms, what);
+    };
+
     if (!out) return fail(SBMDS_EINVAL, "out is NULL");
     *out = nullptr;
     if (n < 1 || l < 1 || l > n) return fail(SBMDS_EINVAL, "need 1 <= l <= n (n=%lld, l=%lld)", (long long)n, (long long)l);
@@ -1518,15 +1546,25 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         h->counters.ensure(kCounters * sizeof(unsigned int));
         CK(cudaMemsetAsync(h->counters.p, 0, h->counters.bytes, st));
 
-        // A host D (the bulk of create's input) starts crossing the host link on an internal
-        // stream now, so the transfer overlaps C1/C2's kernels on `st`; `st` joins it below.
+        // S crosses the host link first (0.5 GB at config 4), then a host D (the bulk of create's
+        // input) on an internal stream, so D's transfer overlaps C1/C2's kernels on `st` (which
+        // need only S); `st` joins it below.
+        // (temporaries from the stream-ordered pool: a cudaFree would synchronise the device and
+        // wait for the D upload)
+        DevBuf rp64{true}, tmpA{true}, tmpB{true}, tmpC{true}, flags_d{true};
+        rp64.ensure((n + 1) * sizeof(int64_t));
+        CK(cudaMemcpyAsync(rp64.p, row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
+        if (nnz > 0) {
+            CK(cudaMemcpyAsync(h->col.p, col_idx, nnz * sizeof(int32_t), cudaMemcpyDefault, st));
+            CK(cudaMemcpyAsync(h->val.p, val, nnz * sizeof(float), cudaMemcpyDefault, st));
+        }
         const bool d_dev = is_device_ptr(D_ll);
         h->ldD = (l + 3) / 4 * 4;
         if (!d_dev) {
             h->Dbuf.ensure((size_t)l * h->ldD * sizeof(float));
             CK(cudaStreamCreateWithFlags(&dside, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&dside_done, cudaEventDisableTiming));
-            CK(cudaEventRecord(dside_done, st));   // the device buffers above are ready
+            CK(cudaEventRecord(dside_done, st));   // the device buffers above are ready and S has crossed
             CK(cudaStreamWaitEvent(dside, dside_done, 0));
             if (!(flags & SBMDS_VALIDATE)) {
                 // only the block upper triangle crosses the host link (D is symmetric, R12; the
@@ -1550,35 +1588,28 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             h->own_D = true;
         }
 
-        // ---- C1: upload (or borrow) S, check structure
-        DevBuf rp64, tmpA, tmpB, tmpC, flags_d;
-        rp64.ensure((n + 1) * sizeof(int64_t));
-        CK(cudaMemcpyAsync(rp64.p, row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
-        if (nnz > 0) {
-            CK(cudaMemcpyAsync(h->col.p, col_idx, nnz * sizeof(int32_t), cudaMemcpyDefault, st));
-            CK(cudaMemcpyAsync(h->val.p, val, nnz * sizeof(float), cudaMemcpyDefault, st));
-        }
+        tphase("allocated, D upload issued");
+        // ---- C1: check S's structure (uploaded above)
         flags_d.ensure(64);
         CK(cudaMemsetAsync(flags_d.p, 0, 64, st));
         int* bad = flags_d.as<int>();
         launch(k_rowptr_to_i32, dim3(256), dim3(256), 0, st, n, (const int64_t*)rp64.as<int64_t>(),
                h->rp.as<int32_t>(), nnz, bad);
         int hbad = 0;
-        CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        peek_to_host(&hbad, bad, sizeof(int), st);
         rp64.release();
         if (hbad) {
             join_dside(); destroy_ctx(h);
             return fail(SBMDS_EINVAL, "row_ptr must start at 0, be nondecreasing and end at nnz");
         }
 
+        tphase("S uploaded and checked");
         // ---- C2: CSC (stable radix sort of (col, entry) pairs keeps rows ascending)
         if (nnz > 0) {
             tmpA.ensure(nnz * sizeof(int32_t));  // rowof
             launch(k_expand_rows, dim3(1024), dim3(256), 0, st, n, (const int32_t*)h->rp.as<int32_t>(),
                    (const int32_t*)h->col.as<int32_t>(), (const float*)h->val.as<float>(), l, tmpA.as<int32_t>(), bad);
-            CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            peek_to_host(&hbad, bad, sizeof(int), st);
             if (hbad) {
                 join_dside(); destroy_ctx(h);
                 return fail(SBMDS_EINVAL, "col_idx out of [0, l) or non-finite val");
@@ -1593,7 +1624,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             size_t tmp_bytes = 0;
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, h->col.as<int32_t>(), tmpC.as<int32_t>(), iota, perm,
                                                (int)nnz, 0, end_bit, st));
-            DevBuf cubtmp;
+            DevBuf cubtmp{true};
             cubtmp.ensure(tmp_bytes + 16);
             CK(cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, h->col.as<int32_t>(), tmpC.as<int32_t>(), iota, perm,
                                                (int)nnz, 0, end_bit, st));
@@ -1605,13 +1636,21 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
                    (const int32_t*)tmpC.as<int32_t>(), h->cptr.as<int32_t>());
             CK(cudaStreamSynchronize(st));
             cubtmp.release();
+            tphase("CSC built");
             build_blocked(h, tmpA.as<int32_t>(), st);
+            tphase("row blocks built");
+            // the tensor-core sparse step's S images depend on S only: built here, inside a host
+            // D's upload window, instead of in the first eigs
+            if (h->blocked && !d_dev) {
+                ensure_sp8(h, st);
+                tphase("sparse-step images built");
+            }
         } else {
             CK(cudaMemsetAsync(h->cptr.p, 0, (l + 1) * sizeof(int32_t), st));
         }
         // w, column keys, spatial column order (sort columns by their median row)
         {
-            DevBuf keys, keys2, ord0;
+            DevBuf keys{true}, keys2{true}, ord0{true};
             keys.ensure(l * sizeof(int32_t));
             keys2.ensure(l * sizeof(int32_t));
             ord0.ensure(l * sizeof(int32_t));
@@ -1624,20 +1663,19 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             size_t tmp_bytes = 0;
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.as<int32_t>(), keys2.as<int32_t>(),
                                                ord0.as<int32_t>(), h->order.as<int32_t>(), (int)l, 0, end_bit, st));
-            DevBuf cubtmp;
+            DevBuf cubtmp{true};
             cubtmp.ensure(tmp_bytes + 16);
             CK(cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, keys.as<int32_t>(), keys2.as<int32_t>(),
                                                ord0.as<int32_t>(), h->order.as<int32_t>(), (int)l, 0, end_bit, st));
             g_launches.fetch_add(1);
             // rowsum deviation (diagnostic)
-            DevBuf rs;
+            DevBuf rs{true};
             rs.ensure(sizeof(unsigned long long));
             CK(cudaMemsetAsync(rs.p, 0, sizeof(unsigned long long), st));
             launch(k_rowsum_dev, dim3(1024), dim3(256), 0, st, n, (const int32_t*)h->rp.as<int32_t>(),
                    (const float*)h->val.as<float>(), rs.as<unsigned long long>());
             unsigned long long bits = 0;
-            CK(cudaMemcpyAsync(&bits, rs.p, sizeof bits, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            peek_to_host(&bits, rs.p, sizeof bits, st);
             double d;
             memcpy(&d, &bits, sizeof d);
             h->rowsum_dev = d;
@@ -1646,6 +1684,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         tmpB.release();
         tmpC.release();
 
+        tphase("S side done");
         // ---- D_ll: borrow (device, l % 4 == 0), copy a device D into a 16-byte-pitched buffer, or
         // join the host upload started above
         if (!d_dev) {
@@ -1661,7 +1700,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             h->own_D = true;
         }
         if (flags & SBMDS_VALIDATE) {
-            DevBuf cb;
+            DevBuf cb{true};
             cb.ensure(64);
             CK(cudaMemsetAsync(cb.p, 0, 64, st));
             unsigned int* md = cb.as<unsigned int>();
@@ -1684,7 +1723,9 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             }
         }
         CK(cudaStreamSynchronize(st));
+        tphase("S-side stream idle");
         join_dside();
+        tphase("D upload joined");
     } catch (const CudaError& e) {
         join_dside(); destroy_ctx(h);
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
