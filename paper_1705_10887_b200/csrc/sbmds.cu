@@ -2037,6 +2037,16 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
 extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol, uint64_t seed,
                                    const float* X0, double* eigvals, float* V, float* Z, sbmds_info* info,
                                    void* cuda_stream) {
+    // (diagnostics) SBMDS_TRACE_EIGS=1: host-clock phase times of this eigs on stderr
+    static const bool trace_eigs = getenv("SBMDS_TRACE_EIGS") != nullptr;
+    const auto t_eigs0 = std::chrono::steady_clock::now();
+    auto ephase = [&](const char* what, cudaStream_t sst) {
+        if (!trace_eigs) return;
+        cudaStreamSynchronize(sst);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_eigs0).count();
+        fprintf(stderr, "[sbmds_eigs] %8.2f ms  %s\n", ms, what);
+    };
+
     if (!h) return fail(SBMDS_EINVAL, "NULL handle");
     if (block < 1 || block > kMaxB || block >= h->n) return fail(SBMDS_EINVAL, "need 1 <= block <= 64, block < n");
     if (m < 1 || m > block) return fail(SBMDS_EINVAL, "need 1 <= m <= block");
@@ -2099,6 +2109,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR of the initial block broke down");
+        ephase("initial block", st);
 
         static bool rr_attr = false;
         if (!rr_attr) {
@@ -2215,6 +2226,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                 do_rr = (tol > 0.0 && it % R == 0) || it == max_iters;
                 enqueue_iteration(it, do_rr);
             }
+            if (it <= 2) ephase(it == 1 ? "iteration 1" : "iteration 2", st);
             if (do_rr) {
                 int conv = 0;
                 CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2235,6 +2247,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
             ++it;
         }
         if (it > max_iters) it = max_iters;
+        ephase("iterations done", st);
         CK(cudaMemcpyAsync(&rr_host, h->rr.p, sizeof(RrOut), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         // E6: select the top-m algebraic pairs. B~ 1 = 0 exactly (J 1 = 0), but the iterate
@@ -2269,6 +2282,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         if (Z && !zdev) CK(cudaMemcpyAsync(Z, Zd, vbytes, cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(e1, st));
         CK(cudaStreamSynchronize(st));
+        ephase("outputs on the host", st);
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, e0, e1));
         cudaEventDestroy(e0);
