@@ -16,6 +16,9 @@
 // Every sum has a fixed order: results are bitwise reproducible.
 #pragma once
 #include "common.cuh"
+#include "k_dstream_sym8.cuh"   // digits3, i8_scale_exp (the fused Y1 digit split)
+
+#include <cooperative_groups.h>
 
 namespace sbmds {
 
@@ -259,7 +262,8 @@ __global__ void __launch_bounds__(256) k_blk_reduce_fold(int64_t l, int64_t lpad
                                                          const float* __restrict__ P1, const double* __restrict__ w,
                                                          const double* __restrict__ s, const double* __restrict__ Rinv,
                                                          float* __restrict__ Y1f, unsigned int* __restrict__ cmax,
-                                                         unsigned int* __restrict__ zero64) {
+                                                         unsigned int* __restrict__ zero64, int8_t* __restrict__ Y8T,
+                                                         int* __restrict__ yexp) {
     // Persistent: warp W takes landmarks j = W, W + nw, ... and software-pipelines them -- the
     // first 6 slot groups of the next landmark (48 slots) are in flight while the current one is
     // summed and folded, and its slot range two landmarks ahead. The per-landmark summation order
@@ -356,6 +360,22 @@ __global__ void __launch_bounds__(256) k_blk_reduce_fold(int64_t l, int64_t lpad
         float m = 0.f;
         for (int ww = 0; ww < 8; ++ww) m = fmaxf(m, mx[ww][threadIdx.x]);
         atomicMax(cmax + threadIdx.x, __float_as_uint(m));
+    }
+    if (Y8T) {
+        // (cooperative launch) every block's maxima are in: the int8 D stream's digits of Y1f
+        // (k_y8_split's work) right here, from L2-hot Y1f, without another launch
+        cooperative_groups::this_grid().sync();
+        const int rb = 256 / BP;
+        const int r = threadIdx.x % rb, c = threadIdx.x / rb;
+        const int e = i8_scale_exp(__uint_as_float(((volatile unsigned int*)cmax)[c]));
+        if (blockIdx.x == 0 && r == 0) yexp[c] = e;
+        for (int64_t k = (int64_t)blockIdx.x * rb + r; k < lpad; k += (int64_t)gridDim.x * rb) {
+            int d0, d1, d2;
+            digits3(__float2int_rn(ldexpf(__ldcg(Y1f + k * BP + c), e)), d0, d1, d2);
+            Y8T[(int64_t)c * lpad + k] = (int8_t)d0;
+            Y8T[(int64_t)(BP + c) * lpad + k] = (int8_t)d1;
+            Y8T[(int64_t)(2 * BP + c) * lpad + k] = (int8_t)d2;
+        }
     }
 }
 

@@ -84,6 +84,23 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+// Cooperative launch (all blocks co-resident; the kernel may call grid.sync()).
+template <typename... KArgs, typename... Args>
+void launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 HangRecord* g_hang_host = nullptr;
 
 // Host-mapped record the device watchdog writes before trapping (common.cuh mbar_wait).
@@ -901,14 +918,14 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         pl.b16_enc = h->Y8T.p;
     }
     profiled(h->prof, PK_SPLIT, st, [&] {
-        if (!h->y1f_ready) {   // (else k_blk_reduce_fold formed Y1f and its column max)
+        if (!h->y1f_ready) {   // (else k_blk_reduce_fold formed Y1f, its column max and the digits)
             CK(cudaMemsetAsync(ymax, 0, 64 * sizeof(unsigned int), st));
             launch(k_y16_prep, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
                    lpad, b, BP, Rinv, (const float*)h->Y1.as<float>(), h->Y1f.as<float>(), ymax, aux + 192);
+            launch_pdl(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
+                       lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
         }
         h->y1f_ready = false;
-        launch_pdl(k_y8_split, dim3((unsigned)std::min<int64_t>(4 * 148, (lpad * BP + 255) / 256)), dim3(256), 0, st,
-                   lpad, BP, (const float*)h->Y1f.as<float>(), (const unsigned int*)ymax, h->Y8T.as<int8_t>(), yexp);
     });
     h->P.ensure((size_t)std::max(1, pl.nslots) * 128 * BP * sizeof(float));
     profiled(h->prof, PK_DSTREAM, st, [&] {
@@ -1203,11 +1220,16 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         h->y16aux.ensure(352 * sizeof(unsigned int));
         unsigned int* aux = h->y16aux.as<unsigned int>();
         profiled(h->prof, PK_CSC, st, [&] {
-            // (aux[64, 128), the column maxima, were zeroed by the last k_y2_digits)
-            launch_pdl(k_blk_reduce_fold, dim3((unsigned)std::min<int64_t>(3 * (int64_t)h->num_sms, (lpad + 7) / 8)),
-                       dim3(256), 0, st, h->l, lpad,
-                   (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
-                   (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192);
+            // (aux[64, 128), the column maxima, were zeroed by the last k_y2_digits); one cooperative
+            // launch also splits Y1f into the D stream's digits (k_y8_split's work)
+            static int per_sm = 0;
+            if (!per_sm) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blk_reduce_fold, 256, 0));
+            h->Y8T.ensure((size_t)3 * kMaxB * lpad);
+            const int64_t grid = std::min<int64_t>(std::min(3, std::max(1, per_sm)) * (int64_t)h->num_sms, (lpad + 7) / 8);
+            launch_coop(k_blk_reduce_fold, dim3((unsigned)grid), dim3(256), 0, st, h->l, lpad,
+                        (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
+                        (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192,
+                        h->Y8T.as<int8_t>(), reinterpret_cast<int*>(aux + 128));
         });
         h->y1f_ready = true;
     } else if (flags & kApplyY1Ready) {
