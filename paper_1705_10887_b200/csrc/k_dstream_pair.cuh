@@ -519,14 +519,12 @@ __global__ void __launch_bounds__(256) k_pack_upper(const float* __restrict__ D,
 
 // Y2 rows = fixed-order sum of their slots' fp32 partials (fp64) times 2^-(sD + e_c) (the
 // exact scales of D and of Y1's column c), then t = w^T Y2 (A4).
-__global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, const int* __restrict__ xptr,
+__device__ __forceinline__ void dreduce_pair_body(int64_t l, int bp, int b, const int* __restrict__ xptr,
                                                       const int* __restrict__ xslot, const float* __restrict__ P,
                                                       const int* __restrict__ dexp, const int* __restrict__ yexp,
                                                       const double* __restrict__ w, float* __restrict__ Y2,
                                                       double* __restrict__ tpart, double* __restrict__ t,
                                                       unsigned int* __restrict__ counter, unsigned int* __restrict__ y2mm) {
-    pdl_trigger();
-    pdl_wait();
     __shared__ double red[256];
     __shared__ float cmx[256], cmn[256];
     // column max / min of Y2 as order-preserving keys (optional; the tensor-core sparse step
@@ -581,6 +579,17 @@ __global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, 
         ordered_colsum_block(tpart, gridDim.x, kMaxB, bp, t);
         if (tid == 0) *counter = 0;
     }
+}
+
+__global__ void __launch_bounds__(256) k_dreduce_pair(int64_t l, int bp, int b, const int* __restrict__ xptr,
+                                                      const int* __restrict__ xslot, const float* __restrict__ P,
+                                                      const int* __restrict__ dexp, const int* __restrict__ yexp,
+                                                      const double* __restrict__ w, float* __restrict__ Y2,
+                                                      double* __restrict__ tpart, double* __restrict__ t,
+                                                      unsigned int* __restrict__ counter, unsigned int* __restrict__ y2mm) {
+    pdl_trigger();
+    pdl_wait();
+    dreduce_pair_body(l, bp, b, xptr, xslot, P, dexp, yexp, w, Y2, tpart, t, counter, y2mm);
 }
 
 }  // namespace sbmds

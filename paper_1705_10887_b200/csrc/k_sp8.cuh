@@ -34,6 +34,8 @@
 #include "common.cuh"
 #include "k_dstream_sym8.cuh"
 #include "k_small.cuh"
+#include "k_dstream_pair.cuh"
+#include <cooperative_groups.h>
 
 namespace sbmds {
 
@@ -264,11 +266,9 @@ __global__ void __launch_bounds__(256) k_colminmax(int64_t l, int bp, const floa
 // (max |Y2_c - t_c| = max(max_c - t_c, t_c - min_c) from the column max / min keys; block 0
 // records the exponents for the step kernel)
 template <int BP>
-__global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
-                                                   const unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
-                                                   uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
-    pdl_trigger();
-    pdl_wait();
+__device__ __forceinline__ void y2_digits_body(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
+                                               const unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
+                                               uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
     static_assert(BP == 16, "b = 16");
     // zero_next: the Y1f column maxima the next iteration's k_blk_reduce_fold accumulates (this
     // iteration's k_y8_split has read them)
@@ -299,6 +299,34 @@ __global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __res
         reinterpret_cast<uint4*>(Yd)[l + j] = w1;
         reinterpret_cast<uint4*>(Yd)[2 * l + j] = w2;
     }
+}
+
+template <int BP>
+__global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
+                                                   const unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
+                                                   uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
+    pdl_trigger();
+    pdl_wait();
+    y2_digits_body<BP>(l, Y2, t, y2mm, ey2_out, Yd, zero_next);
+}
+
+// k_dreduce_pair and k_y2_digits in one cooperative launch: the grid syncs once t = w^T Y2 and
+// Y2's column max/min keys are complete, then digitises Y2 - 1 t^T (one launch fewer per
+// iteration; the grid is the co-resident block count, so t's fixed partial order is per device).
+template <int BP>
+__global__ void __launch_bounds__(256) k_dreduce_y2d(int64_t l, int b, const int* __restrict__ xptr,
+                                                     const float* __restrict__ P, const int* __restrict__ dexp,
+                                                     const int* __restrict__ yexp, const double* __restrict__ w,
+                                                     float* __restrict__ Y2, double* __restrict__ tpart,
+                                                     double* __restrict__ t, unsigned int* __restrict__ counter,
+                                                     unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
+                                                     uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
+    pdl_trigger();
+    pdl_wait();
+    dreduce_pair_body(l, BP, b, xptr, nullptr, P, dexp, yexp, w, Y2, tpart, t, counter, y2mm);
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+    y2_digits_body<BP>(l, Y2, t, y2mm, ey2_out, Yd, zero_next);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {

@@ -86,19 +86,31 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 
 // Cooperative launch (all blocks co-resident; the kernel may call grid.sync()).
 template <typename... KArgs, typename... Args>
-void launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+void launch_coop_x(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
     g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+template <typename... KArgs, typename... Args>
+void launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    launch_coop_x(false, kernel, grid, block, smem, st, args...);
+}
+// cooperative + programmatic serialization (the kernel calls pdl_trigger / pdl_wait)
+template <typename... KArgs, typename... Args>
+void launch_coop_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    launch_coop_x(true, kernel, grid, block, smem, st, args...);
 }
 
 HangRecord* g_hang_host = nullptr;
@@ -361,6 +373,8 @@ struct sbmds_ctx {
     DevBuf s8img, s8ioff, s8esc, s8yd, s8trace, s8rs1, s8pos;
     int sp8_state = 0;     // 0 not built, 1 built, -1 not applicable (a dictionary > 128 entries)
     bool y1f_ready = false;   // the fused landmark reduce already formed Y1f (+ its column max) this apply
+    bool y2d_want = false;    // the sparse step follows this apply's D stream: digitise Y2 in the reduce
+    bool y2d_ready = false;   // k_dreduce_y2d formed Y2's digit planes (launch_sp8 skips k_y2_digits)
     int solver = 0;        // eigs: 0 block subspace iteration, 1 restarted block Lanczos (k_lanczos.cuh)
     int lz_blocks = 0;     // Lanczos blocks per restart cycle (0: 64 / block)
     DevBuf lzQ, lzW, lzC, lzT, lzGl, lzI, lzR;
@@ -937,10 +951,24 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     const int grid = (int)std::min<int64_t>(4 * kRedBlocks, (h->l + rows_per_blk - 1) / rows_per_blk);
     h->tpart.ensure((size_t)4 * kRedBlocks * kMaxB * sizeof(double));
     profiled(h->prof, PK_DREDUCE, st, [&] {
-        launch_pdl(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
-               (const int*)nullptr, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
-               wvec(h), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
-               h->counters.as<unsigned int>() + CNT_DRED, aux + 192);
+        if (BP == 16 && h->y2d_want) {
+            // one cooperative launch: reduce, grid sync on t and the Y2 keys, Y2's digit planes
+            static int per_sm = 0;
+            if (!per_sm) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dreduce_y2d<16>, 256, 0));
+            const int cg = (int)std::min<int64_t>(grid, std::max(1, per_sm) * (int64_t)h->num_sms);
+            h->s8yd.ensure((size_t)3 * h->l * 16);
+            launch_coop_pdl(k_dreduce_y2d<16>, dim3(cg), dim3(256), 0, st, h->l, b, (const int*)pl.xptr.p,
+                        (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp, wvec(h),
+                        h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
+                        h->counters.as<unsigned int>() + CNT_DRED, aux + 192, reinterpret_cast<int*>(aux + 320),
+                        h->s8yd.as<uint8_t>(), aux + 64);
+            h->y2d_ready = true;
+        } else {
+            launch_pdl(k_dreduce_pair, dim3(grid), dim3(256), 0, st, h->l, BP, b, (const int*)pl.xptr.p,
+                       (const int*)nullptr, (const float*)h->P.as<float>(), (const int*)dexp8, (const int*)yexp,
+                       wvec(h), h->Y2.as<float>(), h->tpart.as<double>(), h->t.as<double>(),
+                       h->counters.as<unsigned int>() + CNT_DRED, aux + 192);
+        }
     });
     h->last_dpath = 3;
     h->last_dbytes = pl.ntiles * (int64_t)C::A_BYTES + 12 * h->l * (int64_t)b;
@@ -1139,6 +1167,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
     // Y2's digit planes (one pass over l x 16), then the step
     h->s8yd.ensure((size_t)3 * h->l * 16);
+    if (!h->y2d_ready)
     launch_pdl(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
            (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2mm, ey2,
            h->s8yd.as<uint8_t>(), h->y16aux.as<unsigned int>() + 64);
@@ -1276,7 +1305,10 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
     }
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
+    h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 4);
+    h->y2d_ready = false;
     dstream(h, b, bp, st, Rinv);
+    h->y2d_want = false;
     // A5: Y = -1/2 (S Y2 - 1 t^T)
     if ((flags & kApplyFused) && (flags & kApplySp8)) {
         profiled(h->prof, PK_CSR, st, [&] {
