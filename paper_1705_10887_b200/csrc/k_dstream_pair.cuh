@@ -388,9 +388,11 @@ __global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ x, int
 // all of D that is present when create uploaded only the upper strips (and all the packed
 // path reads); D is symmetric (R12), so this is max |D|.
 __global__ void __launch_bounds__(256) k_absmax_upper(const float* __restrict__ x, int64_t l, int64_t ld,
-                                                      unsigned int* __restrict__ out) {
+                                                      unsigned int* __restrict__ out, int64_t r_begin = 0,
+                                                      int64_t r_end = -1) {
     float m = 0.f;
-    for (int64_t r = blockIdx.x; r < l; r += gridDim.x) {
+    if (r_end < 0) r_end = l;
+    for (int64_t r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
         const float* row = x + r * ld;
         for (int64_t c = (r >> 7) * 128 + threadIdx.x; c < l; c += 256) m = fmaxf(m, fabsf(__ldcs(row + c)));
     }

@@ -338,10 +338,23 @@ __global__ void __launch_bounds__(256) k_pack_sym8(const float* __restrict__ D, 
             const int r = e >> 3, c16 = (e & 7) * 16;   // 16 consecutive columns (one granule) of row r
             const int64_t gr = r0 + r;
             __align__(16) int8_t p0[16], p1[16], p2[16];
+            // 16-byte loads (ldD % 4 == 0, the granule starts at a multiple of 16 columns; columns
+            // in [l, ldD) are padding and read as 0 below, the rows past l are not read)
+            float xv[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t gc = c0 + c16 + 4 * q;
+                float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (gr < l && gc < l) f = __ldcs(reinterpret_cast<const float4*>(D + gr * ldD + gc));
+                xv[4 * q] = f.x;
+                xv[4 * q + 1] = f.y;
+                xv[4 * q + 2] = f.z;
+                xv[4 * q + 3] = f.w;
+            }
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const int64_t gc = c0 + c16 + u;
-                const float x = (gr < l && gc < l) ? ldexpf(D[gr * ldD + gc], sD) : 0.f;
+                const float x = gc < l ? ldexpf(xv[u], sD) : 0.f;
                 int d0, d1, d2;
                 digits3(__float2int_rn(x), d0, d1, d2);
                 p0[u] = (int8_t)d0;

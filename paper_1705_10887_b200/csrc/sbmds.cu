@@ -401,6 +401,7 @@ struct sbmds_ctx {
     // int8 symmetric-half stream (k_dstream_sym8.cuh): D as three digit planes per upper tile
     DevBuf Dt8, Y8T;
     bool dt8_ok = false;
+    bool dmax8_ok = false;   // aux[2] = max |D| over the block upper triangle (formed in create, overlapping D's upload)
     struct PairPlan {
         bool ok = false;
         int S = 0, NT = 0, P = 0, nslots = 0;
@@ -840,7 +841,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         h->Dt.ensure((size_t)pl.ntiles * 128 * 128 * 2 * sizeof(__half));
         CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), st));
         launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256),
-               0, st, (const float*)h->D, h->l, h->ldD, dmax);
+               0, st, (const float*)h->D, h->l, h->ldD, dmax, (int64_t)0, (int64_t)-1);
         launch(k_pack_upper, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
                (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
                (const unsigned int*)dmax, dexp, h->Dt.as<__half>());
@@ -907,7 +908,15 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         attr_set[pi] = true;
     }
     const int64_t lpad = y1t_lpad(h);
-    if (!pl.ok) build_pair_plan(h, pl, h->num_sms, C::S, C::GN, true);   // one CTA per SM, both roles
+    static const bool trace = getenv("SBMDS_TRACE_EIGS") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto dphase = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[sbmds_dstream]  %8.2f ms  %s\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
+    };
+    if (!pl.ok) { build_pair_plan(h, pl, h->num_sms, C::S, C::GN, true); dphase("pair plan"); }   // one CTA per SM, both roles
     h->y16aux.ensure(352 * sizeof(unsigned int));   // + [192, 320): Y2 column max / min keys, [320, 336) exponents
     unsigned int* aux = h->y16aux.as<unsigned int>();
     unsigned int* dmax8 = aux + 2;
@@ -915,14 +924,20 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     unsigned int* ymax = aux + 64;
     int* yexp = reinterpret_cast<int*>(aux + 128);
     if (!h->dt8_ok) {
-        h->Dt8.ensure((size_t)pl.ntiles * C::A_BYTES);
-        CK(cudaMemsetAsync(dmax8, 0, sizeof(unsigned int), st));
-        launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256), 0, st,
-               (const float*)h->D, h->l, h->ldD, dmax8);
+        h->Dt8.ensure((size_t)pl.ntiles * C::A_BYTES);   // (normally allocated in create)
+        dphase("Dt8 allocated");
+        if (!h->dmax8_ok) {
+            CK(cudaMemsetAsync(dmax8, 0, sizeof(unsigned int), st));
+            launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256), 0, st,
+                   (const float*)h->D, h->l, h->ldD, dmax8, (int64_t)0, (int64_t)-1);
+            h->dmax8_ok = true;
+        }
+        dphase("absmax");
         launch(k_pack_sym8, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
                (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
                (const unsigned int*)dmax8, dexp8, h->Dt8.as<int8_t>());
         h->dt8_ok = true;
+        dphase("pack");
     }
     h->Y8T.ensure((size_t)3 * kMaxB * lpad);
     h->Y1f.ensure((size_t)lpad * kMaxB * sizeof(float));
@@ -1566,6 +1581,8 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     h->l = l;
     h->nnz = nnz;
     cudaStream_t dside = nullptr;      // host-D upload stream (see below)
+    cudaStream_t dabs = nullptr;       // max |D| of the landed strips, behind the upload
+    std::vector<cudaEvent_t> dstrips;  // strip groups landed
     cudaEvent_t dside_done = nullptr;
     auto join_dside = [&]() {          // wait for and release it (idempotent; also on errors)
         if (dside) {
@@ -1573,6 +1590,13 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             cudaStreamDestroy(dside);
             dside = nullptr;
         }
+        if (dabs) {
+            cudaStreamSynchronize(dabs);
+            cudaStreamDestroy(dabs);
+            dabs = nullptr;
+        }
+        for (auto e : dstrips) cudaEventDestroy(e);
+        dstrips.clear();
         if (dside_done) {
             cudaEventDestroy(dside_done);
             dside_done = nullptr;
@@ -1623,13 +1647,47 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             if (!(flags & SBMDS_VALIDATE)) {
                 // only the block upper triangle crosses the host link (D is symmetric, R12; the
                 // default D stream reads only these tiles): row strip I from column 128 I on;
-                // the lower part is mirrored on the device if a full-D path is ever used
+                // the lower part is mirrored on the device if a full-D path is ever used.
+                // Where the int8 symmetric-half stream will pack D (large l), max |D| over the
+                // landed strips is taken on a third stream group by group, hidden behind the
+                // transfer, and the packed copy is allocated here (both were first-eigs work).
+                const bool pre8 = uses_sym(h, 16);
+                unsigned int* dmax8 = nullptr;
+                if (pre8) {
+                    const int64_t NT = (l + 127) / 128;
+                    h->Dt8.ensure((size_t)(NT * (NT + 1) / 2) * Sym8Cfg<16>::A_BYTES);
+                    h->y16aux.ensure(352 * sizeof(unsigned int));
+                    dmax8 = h->y16aux.as<unsigned int>() + 2;
+                    CK(cudaMemsetAsync(dmax8, 0, sizeof(unsigned int), st));
+                    CK(cudaStreamCreateWithFlags(&dabs, cudaStreamNonBlocking));
+                    CK(cudaEventRecord(dside_done, st));
+                    CK(cudaStreamWaitEvent(dabs, dside_done, 0));
+                }
+                constexpr int64_t kGroupRows = 16 * 128;
                 for (int64_t r0 = 0; r0 < l; r0 += 128) {
                     const int64_t rows = std::min<int64_t>(128, l - r0);
                     CK(cudaMemcpy2DAsync(h->Dbuf.as<float>() + r0 * h->ldD + r0, h->ldD * sizeof(float),
                                          D_ll + r0 * l + r0, l * sizeof(float), (size_t)(l - r0) * sizeof(float),
                                          (size_t)rows, cudaMemcpyHostToDevice, dside));
                     h->h2d_bytes += rows * (l - r0) * (int64_t)sizeof(float);
+                    if (pre8 && (r0 + 128 >= l || (r0 + 128) % kGroupRows == 0)) {
+                        const int64_t g0 = r0 / kGroupRows * kGroupRows, g1 = std::min<int64_t>(l, r0 + 128);
+                        cudaEvent_t ev;
+                        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                        dstrips.push_back(ev);
+                        CK(cudaEventRecord(ev, dside));
+                        CK(cudaStreamWaitEvent(dabs, ev, 0));
+                        launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(4 * (int64_t)h->num_sms, g1 - g0)),
+                               dim3(256), 0, dabs, (const float*)h->Dbuf.as<float>(), l, h->ldD, dmax8, g0, g1);
+                    }
+                }
+                if (pre8) {
+                    cudaEvent_t ev;
+                    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                    dstrips.push_back(ev);
+                    CK(cudaEventRecord(ev, dabs));
+                    CK(cudaStreamWaitEvent(dside, ev, 0));   // dside_done below covers the maxima too
+                    h->dmax8_ok = true;
                 }
                 h->d_lower_missing = true;
             } else {
