@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, co
 // forms it (fp64 fma over p <= c in order), the per-column max |Y1f| (atomicMax on the float
 // bits; cmax zeroed by the caller) and zero pad rows l..lpad; block 0 also resets the Y2 max /
 // min keys of the pair reduce (zero64, as k_y16_prep). One kernel instead of two.
-__global__ void __launch_bounds__(256) k_blk_reduce_fold(int64_t l, int64_t lpad, const int32_t* __restrict__ jptr,
+__global__ void __launch_bounds__(256, 4) k_blk_reduce_fold(int64_t l, int64_t lpad, const int32_t* __restrict__ jptr,
                                                          const float* __restrict__ P1, const double* __restrict__ w,
                                                          const double* __restrict__ s, const double* __restrict__ Rinv,
                                                          float* __restrict__ Y1f, unsigned int* __restrict__ cmax,

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __res
 // Y2's column max/min keys are complete, then digitises Y2 - 1 t^T (one launch fewer per
 // iteration; the grid is the co-resident block count, so t's fixed partial order is per device).
 template <int BP>
-__global__ void __launch_bounds__(256) k_dreduce_y2d(int64_t l, int b, const int* __restrict__ xptr,
+__global__ void __launch_bounds__(256, 5) k_dreduce_y2d(int64_t l, int b, const int* __restrict__ xptr,
                                                      const float* __restrict__ P, const int* __restrict__ dexp,
                                                      const int* __restrict__ yexp, const double* __restrict__ w,
                                                      float* __restrict__ Y2, double* __restrict__ tpart,

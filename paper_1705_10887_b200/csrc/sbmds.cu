@@ -1269,7 +1269,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
             static int per_sm = 0;
             if (!per_sm) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blk_reduce_fold, 256, 0));
             h->Y8T.ensure((size_t)3 * kMaxB * lpad);
-            const int64_t grid = std::min<int64_t>(std::min(3, std::max(1, per_sm)) * (int64_t)h->num_sms, (lpad + 7) / 8);
+            // (4 blocks per SM under __launch_bounds__(256, 4): 0.050 vs 0.053 ms with 3 at config 4)
+            const int64_t grid = std::min<int64_t>(std::min(4, std::max(1, per_sm)) * (int64_t)h->num_sms, (lpad + 7) / 8);
             launch_coop(k_blk_reduce_fold, dim3((unsigned)grid), dim3(256), 0, st, h->l, lpad,
                         (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
                         (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192,
