@@ -310,11 +310,96 @@ __global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __res
     y2_digits_body<BP>(l, Y2, t, y2mm, ey2_out, Yd, zero_next);
 }
 
+// k_dreduce_pair's reduction at b = 16 with 16-byte loads: a thread owns four columns of one
+// row (a warp load covers 8 rows x 16 columns = 512 B, against 128 B for the scalar kernel) and
+// keeps 8 slots in flight. Every Y2 element is the same fp64 sum over its slots in slot order
+// as k_dreduce_pair forms it (bitwise-identical Y2); t's per-block partial order differs.
+__device__ __forceinline__ void dreduce16_body(int64_t l, int b, const int* __restrict__ xptr,
+                                               const float* __restrict__ P, const int* __restrict__ dexp,
+                                               const int* __restrict__ yexp, const double* __restrict__ w,
+                                               float* __restrict__ Y2, double* __restrict__ tpart,
+                                               double* __restrict__ t, unsigned int* __restrict__ counter,
+                                               unsigned int* __restrict__ y2mm) {
+    constexpr int BP = 16, RPB = 64, U = 8;
+    __shared__ double red[RPB][BP + 1];
+    __shared__ float cmx[RPB][BP + 1], cmn[RPB][BP + 1];
+    const int tid = threadIdx.x, cq = tid & 3, rloc = tid >> 2;
+    double unscale[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) unscale[u] = ldexp(1.0, -(*dexp + yexp[4 * cq + u]));
+    float m[4] = {-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f}, mn[4] = {3.0e38f, 3.0e38f, 3.0e38f, 3.0e38f};
+    double acc_t[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t r0 = (int64_t)blockIdx.x * RPB; r0 < l; r0 += (int64_t)gridDim.x * RPB) {
+        const int64_t r = r0 + rloc;
+        if (r < l) {
+            const int X = (int)(r >> 7), rr = (int)(r & 127);
+            const int q0 = xptr[X], q1 = xptr[X + 1];
+            const float4* base = reinterpret_cast<const float4*>(P) + (int64_t)rr * (BP / 4) + cq;
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            int q = q0;
+            for (; q + U <= q1; q += U) {
+                float4 pv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) pv[u] = __ldcs(base + (int64_t)(q + u) * (128 * BP / 4));
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    v[0] += (double)pv[u].x;
+                    v[1] += (double)pv[u].y;
+                    v[2] += (double)pv[u].z;
+                    v[3] += (double)pv[u].w;
+                }
+            }
+            for (; q < q1; ++q) {
+                const float4 pv = __ldcs(base + (int64_t)q * (128 * BP / 4));
+                v[0] += (double)pv.x;
+                v[1] += (double)pv.y;
+                v[2] += (double)pv.z;
+                v[3] += (double)pv.w;
+            }
+            float4 o;
+            float* of = &o.x;
+            const double wr = w[r];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double y = v[u] * unscale[u];
+                of[u] = (float)y;
+                m[u] = fmaxf(m[u], of[u]);
+                mn[u] = fminf(mn[u], of[u]);
+                if (4 * cq + u < b) acc_t[u] += wr * y;
+            }
+            reinterpret_cast<float4*>(Y2 + r * BP)[cq] = o;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        red[rloc][4 * cq + u] = acc_t[u];
+        cmx[rloc][4 * cq + u] = m[u];
+        cmn[rloc][4 * cq + u] = mn[u];
+    }
+    __syncthreads();
+    if (tid < BP) {
+        float mm = -3.0e38f, mi = 3.0e38f;
+        double a = 0.0;
+        for (int q = 0; q < RPB; ++q) {
+            mm = fmaxf(mm, cmx[q][tid]);
+            mi = fminf(mi, cmn[q][tid]);
+            a += red[q][tid];
+        }
+        atomicMax(y2mm + tid, f32_order_key(mm));
+        atomicMin(y2mm + 64 + tid, f32_order_key(mi));
+        tpart[blockIdx.x * kMaxB + tid] = a;
+    }
+    if (last_block_done(counter)) {
+        ordered_colsum_block(tpart, gridDim.x, kMaxB, BP, t);
+        if (tid == 0) *counter = 0;
+    }
+}
+
 // k_dreduce_pair and k_y2_digits in one cooperative launch: the grid syncs once t = w^T Y2 and
 // Y2's column max/min keys are complete, then digitises Y2 - 1 t^T (one launch fewer per
 // iteration; the grid is the co-resident block count, so t's fixed partial order is per device).
 template <int BP>
-__global__ void __launch_bounds__(256, 5) k_dreduce_y2d(int64_t l, int b, const int* __restrict__ xptr,
+__global__ void __launch_bounds__(256, 4) k_dreduce_y2d(int64_t l, int b, const int* __restrict__ xptr,
                                                      const float* __restrict__ P, const int* __restrict__ dexp,
                                                      const int* __restrict__ yexp, const double* __restrict__ w,
                                                      float* __restrict__ Y2, double* __restrict__ tpart,
@@ -323,7 +408,7 @@ __global__ void __launch_bounds__(256, 5) k_dreduce_y2d(int64_t l, int b, const 
                                                      uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
     pdl_trigger();
     pdl_wait();
-    dreduce_pair_body(l, BP, b, xptr, nullptr, P, dexp, yexp, w, Y2, tpart, t, counter, y2mm);
+    dreduce16_body(l, b, xptr, P, dexp, yexp, w, Y2, tpart, t, counter, y2mm);
     __threadfence();
     cooperative_groups::this_grid().sync();
     y2_digits_body<BP>(l, Y2, t, y2mm, ey2_out, Yd, zero_next);
