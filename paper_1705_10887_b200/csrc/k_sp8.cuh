@@ -176,39 +176,79 @@ __device__ __forceinline__ float sp8_col_sum(const uint16_t* __restrict__ lcol, 
     return v;
 }
 
+// One warp per row (rows w, w + 4, ... of the block): lane i holds entry beg + i; entries with
+// the same block-local column are found with __match_any_sync and summed in entry order by the
+// first of them (0 + v_first + ... ascending, as sp8_col_sum). Rows longer than 32 entries take
+// the per-entry scans above (lanes striding over the row).
+__device__ __forceinline__ float sp8_row_entry(const uint16_t* __restrict__ lcol, const float* __restrict__ val,
+                                               int32_t beg, int32_t end, int lane, bool& first, int& col) {
+    const int32_t e = beg + lane;
+    const bool have = e < end;
+    col = have ? (int)lcol[e] : -1 - lane;   // absent lanes match nobody
+    const float v = have ? val[e] : 0.f;
+    const unsigned peers = __match_any_sync(0xffffffffu, col);
+    first = have && (__ffs(peers) - 1) == lane;
+    if (__all_sync(0xffffffffu, peers == (1u << lane))) return v;   // no duplicates in this row
+    float acc = 0.f;
+    for (int src = 0; src < 32; ++src) {
+        const float x = __shfl_sync(0xffffffffu, v, src);
+        if ((peers >> src) & 1u) acc += x;
+    }
+    return acc;
+}
+
 __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, const int32_t* __restrict__ rp,
                                                    const float* __restrict__ val, const uint16_t* __restrict__ lcol,
                                                    const int32_t* __restrict__ doff, const int64_t* __restrict__ ioff,
                                                    int8_t* __restrict__ img, int* __restrict__ escale) {
     __shared__ float red[4];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int64_t B = blockIdx.x; B < nblk; B += gridDim.x) {
         const int64_t r0 = B * kSp8RB;
         const int rows = (int)((n - r0) < kSp8RB ? (n - r0) : kSp8RB);
-        const int r = threadIdx.x;
-        const int32_t beg = r < rows ? rp[r0 + r] : 0, end = r < rows ? rp[r0 + r + 1] : 0;
         float m = 0.f;
-        for (int32_t e = beg; e < end; ++e)
-            if (sp8_first_of_col(lcol, beg, e)) m = fmaxf(m, fabsf(sp8_col_sum(lcol, val, e, end)));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        for (int r = wid; r < rows; r += 4) {
+            const int32_t beg = rp[r0 + r], end = rp[r0 + r + 1];
+            const bool longrow = end - beg > 32;   // (warp-uniform; the match runs on every lane)
+            bool first;
+            int col;
+            const float v = sp8_row_entry(lcol, val, beg, longrow ? beg : end, lane, first, col);
+            if (!longrow) {
+                if (first) m = fmaxf(m, fabsf(v));
+            } else {
+                for (int32_t e = beg + lane; e < end; e += 32)
+                    if (sp8_first_of_col(lcol, beg, e)) m = fmaxf(m, fabsf(sp8_col_sum(lcol, val, e, end)));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         __syncthreads();
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+        if (lane == 0) red[wid] = m;
         __syncthreads();
         const int eS = i8_scale_exp(fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3])));
         if (threadIdx.x == 0) escale[B] = eS;
         const int dp = sp8_dpad(doff[B + 1] - doff[B]);
         int8_t* out = img + ioff[B];
-        for (int32_t e = beg; e < end; ++e) {
-            if (!sp8_first_of_col(lcol, beg, e)) continue;
+        auto put = [&](int r, int col, float v) {
             int d0, d1, d2;
-            digits3(__float2int_rn(ldexpf(sp8_col_sum(lcol, val, e, end), eS)), d0, d1, d2);
-            const int o = sp8_off(r, (int)lcol[e], kSp8RB / 8);
+            digits3(__float2int_rn(ldexpf(v, eS)), d0, d1, d2);
+            const int o = sp8_off(r, col, kSp8RB / 8);
             out[o] = (int8_t)d0;
             out[kSp8RB * dp + o] = (int8_t)d1;
             out[2 * kSp8RB * dp + o] = (int8_t)d2;
+        };
+        for (int r = wid; r < rows; r += 4) {
+            const int32_t beg = rp[r0 + r], end = rp[r0 + r + 1];
+            const bool longrow = end - beg > 32;
+            bool first;
+            int col;
+            const float v = sp8_row_entry(lcol, val, beg, longrow ? beg : end, lane, first, col);
+            if (!longrow) {
+                if (first) put(r, col, v);
+            } else {
+                for (int32_t e = beg + lane; e < end; e += 32)
+                    if (sp8_first_of_col(lcol, beg, e)) put(r, (int)lcol[e], sp8_col_sum(lcol, val, e, end));
+            }
         }
     }
 }
