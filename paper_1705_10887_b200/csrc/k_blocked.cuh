@@ -253,112 +253,84 @@ __global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, co
     }
 }
 
-// A2 part 2 fused with the R^-1 fold of the eigs iteration (b = 16, LPR = 4): as k_blk_reduce
-// (landmark-major partials, fixed order), then Y1f[j] = (Y1[j] R^-1) exactly as k_y16_prep
-// forms it (fp64 fma over p <= c in order), the per-column max |Y1f| (atomicMax on the float
-// bits; cmax zeroed by the caller) and zero pad rows l..lpad; block 0 also resets the Y2 max /
-// min keys of the pair reduce (zero64, as k_y16_prep). One kernel instead of two.
+// A2 part 2 fused with the R^-1 fold of the eigs iteration (b = 16): Y1[j] = (sum of landmark
+// j's partials, landmark-major, in slot order, fp64) - w_j s^T, then Y1f[j] = (Y1[j] R^-1) exactly
+// as k_y16_prep forms it (fp64 fma over p <= c in order), the per-column max |Y1f| (atomicMax on
+// the float bits; cmax zeroed by the caller) and zero pad rows l..lpad; block 0 also resets the Y2
+// max / min keys of the pair reduce (zero64, as k_y16_prep). A thread owns four columns of one
+// landmark (16-byte partial loads, 8 slots in flight); the four threads of a landmark exchange
+// their sums by shuffles for the fold.
 __global__ void __launch_bounds__(256, 4) k_blk_reduce_fold(int64_t l, int64_t lpad, const int32_t* __restrict__ jptr,
                                                          const float* __restrict__ P1, const double* __restrict__ w,
                                                          const double* __restrict__ s, const double* __restrict__ Rinv,
                                                          float* __restrict__ Y1f, unsigned int* __restrict__ cmax,
                                                          unsigned int* __restrict__ zero64, int8_t* __restrict__ Y8T,
                                                          int* __restrict__ yexp) {
-    // Persistent: warp W takes landmarks j = W, W + nw, ... and software-pipelines them -- the
-    // first 6 slot groups of the next landmark (48 slots) are in flight while the current one is
-    // summed and folded, and its slot range two landmarks ahead. The per-landmark summation order
-    // is the plain kernel's (lane group g: slots g, g + 8, ... in order; then the group tree).
     pdl_trigger();
     pdl_wait();
-    constexpr int BP = 16, LPR = 4, G = 32 / LPR, PF = 6;
+    constexpr int BP = 16, JPB = 64, U = 8;
     __shared__ double Ms[BP * BP];
-    __shared__ float mx[8][BP];
+    __shared__ float mxs[JPB][BP + 1];
     if (zero64 && blockIdx.x == 0 && threadIdx.x < 128) zero64[threadIdx.x] = threadIdx.x < 64 ? 0u : 0xFFFFFFFFu;
     for (int e = threadIdx.x; e < BP * BP; e += blockDim.x) Ms[e] = Rinv[e];
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = lane / LPR, q = lane % LPR;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    float cm = 0.f;   // this lane's running max |Y1f| of column `lane` (lanes < 16)
-    auto range = [&](int64_t jj, int32_t& b0, int32_t& e0) {
-        if (jj < l) {
-            b0 = __ldg(jptr + jj);
-            e0 = __ldg(jptr + jj + 1);
-        } else {
-            b0 = e0 = 0;
-        }
-    };
-    auto prefetch = [&](int32_t b0, int32_t e0, float4 (&v)[PF]) {
+    const int lane = threadIdx.x & 31, cq = threadIdx.x & 3, jl = threadIdx.x >> 2;
+    float cm[4] = {0.f, 0.f, 0.f, 0.f};
+    double sc[4];
 #pragma unroll
-        for (int u = 0; u < PF; ++u) {
-            const int32_t k = b0 + g + u * G;
-            v[u] = k < e0 ? __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)k * BP) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    };
-    int32_t beg, end, nbeg, nend;
-    range(j, beg, end);
-    range(j + nw, nbeg, nend);
-    float4 v[PF];
-    prefetch(beg, end, v);
-    for (; j < lpad; j += nw) {
-        // next landmark's slots in flight, the one after next's range requested
-        float4 vn[PF];
-        prefetch(nbeg, nend, vn);
-        int32_t nnbeg, nnend;
-        range(j + 2 * nw, nnbeg, nnend);
+    for (int u = 0; u < 4; ++u) sc[u] = s[4 * cq + u];
+    for (int64_t j0 = (int64_t)blockIdx.x * JPB; j0 < lpad; j0 += (int64_t)gridDim.x * JPB) {
+        const int64_t j = j0 + jl;
         float y[4] = {0.f, 0.f, 0.f, 0.f};
         if (j < l) {
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            const int32_t b0 = __ldg(jptr + j), e0 = __ldg(jptr + j + 1);
+            const float4* base = reinterpret_cast<const float4*>(P1) + cq;
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+            int32_t k = b0;
+            for (; k + U <= e0; k += U) {
+                float4 pv[U];
 #pragma unroll
-            for (int u = 0; u < PF; ++u) {
-                if (beg + g + u * G < end) {
-                    a0 += v[u].x; a1 += v[u].y; a2 += v[u].z; a3 += v[u].w;
+                for (int u = 0; u < U; ++u) pv[u] = __ldcs(base + (int64_t)(k + u) * (BP / 4));
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w;
                 }
             }
-            for (int32_t k = beg + g + PF * G; k < end; k += G) {   // beyond the prefetched slots
-                const float4 t = __ldg(reinterpret_cast<const float4*>(P1 + (int64_t)k * BP) + q);
-                a0 += t.x; a1 += t.y; a2 += t.z; a3 += t.w;
-            }
-#pragma unroll
-            for (int o = LPR; o < 32; o <<= 1) {
-                a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-                a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-                a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+            for (; k < e0; ++k) {
+                const float4 t = __ldcs(base + (int64_t)k * (BP / 4));
+                a[0] += t.x; a[1] += t.y; a[2] += t.z; a[3] += t.w;
             }
             const double wj = w[j];
-            y[0] = (float)(a0 - wj * s[4 * q + 0]);
-            y[1] = (float)(a1 - wj * s[4 * q + 1]);
-            y[2] = (float)(a2 - wj * s[4 * q + 2]);
-            y[3] = (float)(a3 - wj * s[4 * q + 3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) y[u] = (float)(a[u] - wj * sc[u]);
         }
-        // all 16 values of the row in every lane (lane q' holds columns 4q'..4q'+3)
+        // the landmark's 16 values in each of its four lanes, then columns 4 cq .. 4 cq + 3 of
+        // the folded row (fp64 fma over p <= c, in order)
         float yr[BP];
 #pragma unroll
-        for (int p = 0; p < BP; ++p) yr[p] = __shfl_sync(0xffffffffu, y[p & 3], p >> 2);
-        // lane c < 16 forms column c of the folded row (fp64 fma over p <= c, in order)
-        if (lane < BP) {
-            double acc = 0.0;
+        for (int p = 0; p < BP; ++p) yr[p] = __shfl_sync(0xffffffffu, y[p & 3], (lane & ~3) | (p >> 2));
+        if (j < lpad) {
+            float4 o;
+            float* of = &o.x;
 #pragma unroll
-            for (int p = 0; p < BP; ++p)
-                if (p <= lane) acc = fma((double)yr[p], Ms[p * BP + lane], acc);
-            const float f = (float)acc;
-            Y1f[j * BP + lane] = f;
-            cm = fmaxf(cm, fabsf(f));
+            for (int u = 0; u < 4; ++u) {
+                const int c = 4 * cq + u;
+                double acc = 0.0;
+#pragma unroll
+                for (int p = 0; p < BP; ++p)
+                    if (p <= c) acc = fma((double)yr[p], Ms[p * BP + c], acc);
+                of[u] = (float)acc;
+                cm[u] = fmaxf(cm[u], fabsf(of[u]));
+            }
+            reinterpret_cast<float4*>(Y1f + j * BP)[cq] = o;
         }
-#pragma unroll
-        for (int u = 0; u < PF; ++u) v[u] = vn[u];
-        beg = nbeg;
-        end = nend;
-        nbeg = nnbeg;
-        nend = nnend;
     }
-    if (lane < BP) mx[wid][lane] = cm;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) mxs[jl][4 * cq + u] = cm[u];
     __syncthreads();
     if (threadIdx.x < BP) {
         float m = 0.f;
-        for (int ww = 0; ww < 8; ++ww) m = fmaxf(m, mx[ww][threadIdx.x]);
+        for (int q = 0; q < JPB; ++q) m = fmaxf(m, mxs[q][threadIdx.x]);
         atomicMax(cmax + threadIdx.x, __float_as_uint(m));
     }
     if (Y8T) {
