@@ -236,17 +236,18 @@ __host__ __device__ __forceinline__ float f32_from_order_key(unsigned int k) {
 // Fixed-order sum of p[0], p[stride], ..., p[(count-1)*stride] with 16 loads in flight:
 // the additions happen in index order (bitwise reproducible) but the L2 latency of the
 // partials is overlapped instead of serialised.
+template <int U = 16>
 __device__ __forceinline__ double ordered_sum(const double* __restrict__ p, int count, int64_t stride) {
+    // U loads in flight per batch, the last batch predicated (no serial tail), added in index order
     double acc = 0.0;
-    int q = 0;
-    for (; q + 16 <= count; q += 16) {
-        double v[16];
+    for (int q = 0; q < count; q += U) {
+        double v[U];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = p[(int64_t)(q + u) * stride];
+        for (int u = 0; u < U; ++u) v[u] = q + u < count ? p[(int64_t)(q + u) * stride] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) acc += v[u];
+        for (int u = 0; u < U; ++u)
+            if (q + u < count) acc += v[u];
     }
-    for (; q < count; ++q) acc += p[(int64_t)q * stride];
     return acc;
 }
 
@@ -284,6 +285,17 @@ __device__ __forceinline__ void ordered_colsum_block(const double* __restrict__ 
 // Last-block-done pattern for deterministic grid reductions: every block writes its
 // partial, fences, and bumps a counter; the block that sees count == grid-1 does the
 // final fixed-order reduction and resets the counter for the next launch.
+// last_block_done among the first `nblocks` blocks only (they alone arrive on `counter`)
+__device__ __forceinline__ bool last_block_of(unsigned int* counter, unsigned int nblocks) {
+    __shared__ bool is_last_of;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last_of = atomicAdd(counter, 1u) == nblocks - 1;
+    __syncthreads();
+    if (is_last_of) __threadfence();
+    return is_last_of;
+}
+
 __device__ __forceinline__ bool last_block_done(unsigned int* counter) {
     __shared__ bool is_last;
     __threadfence();

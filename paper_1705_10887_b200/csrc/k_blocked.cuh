@@ -17,6 +17,7 @@
 #pragma once
 #include "common.cuh"
 #include "k_dstream_sym8.cuh"   // digits3, i8_scale_exp (the fused Y1 digit split)
+#include "k_small.cuh"          // chol_block, ordered_sum (the deferred Gram of the fold)
 
 #include <cooperative_groups.h>
 
@@ -253,6 +254,23 @@ __global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, co
     }
 }
 
+// Deferred E2/E3 of the previous tensor-core sparse step (k_sp8_step with defer_gram): its CTA
+// Gram partials, summed here in CTA order by block 0 (s = 1^T Y, G = Y^T Y) and factored
+// (chol_block -> R^-1, status) while the other blocks sum the landmark partials into `scratch`
+// (fp64); a grid sync, then the fold reads s and R^-1. Off the step's critical path: its last CTA
+// no longer sums and factors after every other CTA has finished.
+struct FoldGram {
+    const double* part = nullptr;   // nullptr: s and Rinv are given (no deferred Gram)
+    int nparts = 0;
+    double* G = nullptr;
+    double* s_out = nullptr;
+    double* Rinv_out = nullptr;
+    int* status = nullptr;
+    double* scratch = nullptr;      // lpad x 16 fp64 landmark sums
+    unsigned int* counter = nullptr;   // zero; the last of the Gram blocks factors
+};
+constexpr int kFoldGramBlocks = 5;   // blocks summing the Gram partials (4 threads per entry)
+
 // A2 part 2 fused with the R^-1 fold of the eigs iteration (b = 16): Y1[j] = (sum of landmark
 // j's partials, landmark-major, in slot order, fp64) - w_j s^T, then Y1f[j] = (Y1[j] R^-1) exactly
 // as k_y16_prep forms it (fp64 fma over p <= c in order), the per-column max |Y1f| (atomicMax on
@@ -262,43 +280,96 @@ __global__ void __launch_bounds__(256) k_blk_reduce(int64_t l, int b, int bp, co
 // their sums by shuffles for the fold.
 __global__ void __launch_bounds__(256, 4) k_blk_reduce_fold(int64_t l, int64_t lpad, const int32_t* __restrict__ jptr,
                                                          const float* __restrict__ P1, const double* __restrict__ w,
-                                                         const double* __restrict__ s, const double* __restrict__ Rinv,
+                                                         const double* s, const double* Rinv,
                                                          float* __restrict__ Y1f, unsigned int* __restrict__ cmax,
                                                          unsigned int* __restrict__ zero64, int8_t* __restrict__ Y8T,
-                                                         int* __restrict__ yexp) {
+                                                         int* __restrict__ yexp, FoldGram fg) {
     pdl_trigger();
     pdl_wait();
     constexpr int BP = 16, JPB = 64, U = 8;
     __shared__ double Ms[BP * BP];
     __shared__ float mxs[JPB][BP + 1];
     if (zero64 && blockIdx.x == 0 && threadIdx.x < 128) zero64[threadIdx.x] = threadIdx.x < 64 ? 0u : 0xFFFFFFFFu;
-    for (int e = threadIdx.x; e < BP * BP; e += blockDim.x) Ms[e] = Rinv[e];
-    __syncthreads();
     const int lane = threadIdx.x & 31, cq = threadIdx.x & 3, jl = threadIdx.x >> 2;
+    // fp64 sum of landmark j's partials (columns 4 cq .. 4 cq + 3), in slot order
+    auto landmark_sum = [&](int64_t j, double (&a)[4]) {
+        const int32_t b0 = __ldg(jptr + j), e0 = __ldg(jptr + j + 1);
+        const float4* base = reinterpret_cast<const float4*>(P1) + cq;
+        a[0] = a[1] = a[2] = a[3] = 0.0;
+        int32_t k = b0;
+        for (; k + U <= e0; k += U) {
+            float4 pv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) pv[u] = __ldcs(base + (int64_t)(k + u) * (BP / 4));
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w;
+            }
+        }
+        for (; k < e0; ++k) {
+            const float4 t = __ldcs(base + (int64_t)k * (BP / 4));
+            a[0] += t.x; a[1] += t.y; a[2] += t.z; a[3] += t.w;
+        }
+    };
+    const bool deferred = fg.part != nullptr;
+    if (deferred) {
+        if (blockIdx.x < kFoldGramBlocks) {
+            // entry e < 272 (G row-major, then s), quarter qt of the CTA range: 4 consecutive lanes,
+            // each sums its quarter in CTA order, the first adds the four in quarter order
+            __shared__ double Ach[BP][kMaxB + 1];
+            __shared__ int chfail;
+            __shared__ double chshift;
+            const int task = blockIdx.x * blockDim.x + threadIdx.x, e = task >> 2, qt = task & 3;
+            const int per = (fg.nparts + 3) / 4, q0 = min(fg.nparts, qt * per), q1 = min(fg.nparts, q0 + per);
+            const int off = e < BP * BP ? e : 2 * kMaxB * kMaxB + (e - BP * BP);
+            double v = 0.0;
+            if (e < BP * BP + BP) v = ordered_sum<32>(fg.part + (int64_t)q0 * kGramPart + off, q1 - q0, kGramPart);
+            const double v1 = __shfl_down_sync(0xffffffffu, v, 1), v2 = __shfl_down_sync(0xffffffffu, v, 2),
+                         v3 = __shfl_down_sync(0xffffffffu, v, 3);
+            if (qt == 0 && e < BP * BP + BP) {
+                const double tot = ((v + v1) + v2) + v3;
+                if (e < BP * BP) fg.G[e] = tot;
+                else fg.s_out[e - BP * BP] = tot;
+            }
+            if (last_block_of(fg.counter, kFoldGramBlocks)) {
+                chol_block(BP, fg.G, fg.Rinv_out, fg.status, Ach, &chfail, &chshift);
+                if (threadIdx.x == 0) *fg.counter = 0;
+            }
+        } else {
+            for (int64_t j0 = (int64_t)(blockIdx.x - kFoldGramBlocks) * JPB; j0 < l;
+                 j0 += (int64_t)(gridDim.x - kFoldGramBlocks) * JPB) {
+                const int64_t j = j0 + jl;
+                if (j < l) {
+                    double a[4];
+                    landmark_sum(j, a);
+                    double2* dst = reinterpret_cast<double2*>(fg.scratch + j * BP + 4 * cq);
+                    dst[0] = make_double2(a[0], a[1]);
+                    dst[1] = make_double2(a[2], a[3]);
+                }
+            }
+        }
+        __threadfence();
+        cooperative_groups::this_grid().sync();
+        s = fg.s_out;
+        Rinv = fg.Rinv_out;
+    }
+    for (int e = threadIdx.x; e < BP * BP; e += blockDim.x) Ms[e] = __ldcg(Rinv + e);
+    __syncthreads();
     float cm[4] = {0.f, 0.f, 0.f, 0.f};
     double sc[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) sc[u] = s[4 * cq + u];
+    for (int u = 0; u < 4; ++u) sc[u] = __ldcg(s + 4 * cq + u);
     for (int64_t j0 = (int64_t)blockIdx.x * JPB; j0 < lpad; j0 += (int64_t)gridDim.x * JPB) {
         const int64_t j = j0 + jl;
         float y[4] = {0.f, 0.f, 0.f, 0.f};
         if (j < l) {
-            const int32_t b0 = __ldg(jptr + j), e0 = __ldg(jptr + j + 1);
-            const float4* base = reinterpret_cast<const float4*>(P1) + cq;
-            double a[4] = {0.0, 0.0, 0.0, 0.0};
-            int32_t k = b0;
-            for (; k + U <= e0; k += U) {
-                float4 pv[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) pv[u] = __ldcs(base + (int64_t)(k + u) * (BP / 4));
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w;
-                }
-            }
-            for (; k < e0; ++k) {
-                const float4 t = __ldcs(base + (int64_t)k * (BP / 4));
-                a[0] += t.x; a[1] += t.y; a[2] += t.z; a[3] += t.w;
+            double a[4];
+            if (deferred) {
+                const double2* src = reinterpret_cast<const double2*>(fg.scratch + j * BP + 4 * cq);
+                const double2 a01 = __ldcg(src), a23 = __ldcg(src + 1);
+                a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
+            } else {
+                landmark_sum(j, a);
             }
             const double wj = w[j];
 #pragma unroll

@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
                unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int stream_only,
-               double* __restrict__ Rinv_next, int* __restrict__ status) {
+               double* __restrict__ Rinv_next, int* __restrict__ status, int defer_gram) {
     using C = Sp8Cfg<BP>;
     // (diagnostics) trace[ev * 64 + i]: globaltimer of event ev for block i < 64 of CTA 0
 #define SP8_TR(ev, i)                                                                          \
@@ -588,6 +588,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
     pdl_wait();   // everything below reads what earlier kernels wrote (Y2 digits, exponents, t, P1 slots)
+    // (diagnostics) trace[768 + c]: CTA c's start, trace[1024 + c]: its blocks done (c < 256),
+    // trace[1279]: the last CTA's end (after the Gram sums and the Cholesky)
+    auto tail_tr = [&](int slot) {
+        if (trace && threadIdx.x == 0) {
+            unsigned long long t_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+            trace[slot] = t_;
+        }
+    };
+    if (blockIdx.x < 256) tail_tr(768 + blockIdx.x);
     if (threadIdx.x < BP) ey2[threadIdx.x] = ey2in[threadIdx.x];
     if (warp >= 2 && warp < 14) {   // c3 groups of every accumulator start at zero
         const uint32_t lo = (uint32_t)(32 * (warp & 3)) << 16;
@@ -991,9 +1001,12 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     }
 
 #undef SP8_TR
+    __syncthreads();
+    if (blockIdx.x < 256) tail_tr(1024 + blockIdx.x);
     // ---- CTA partial of the Grams (fixed warp order), then the last CTA sums them in CTA order
     tc_fence_before();
     __syncthreads();
+    if (blockIdx.x < 256) tail_tr(1536 + blockIdx.x);
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
@@ -1033,6 +1046,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             }
     }
     __syncthreads();
+    if (blockIdx.x < 256) tail_tr(1792 + blockIdx.x);
     double* pg = part + (int64_t)blockIdx.x * kGramPart;
     for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
         const int p = pq / BP, qq = pq % BP;
@@ -1057,14 +1071,19 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             pg[kMaxB * kMaxB + pq] = red[0][p][qq] + red[1][p][qq];
         }
     }
-    if (last_block_done(counter)) {
+    if (blockIdx.x < 256) tail_tr(1280 + blockIdx.x);
+    // defer_gram: the next k_blk_reduce_fold sums these partials and factors G (FoldGram)
+    if (!defer_gram && last_block_done(counter)) {
+        tail_tr(1277);
         for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
-            cs[qq] = ordered_sum(part + 2 * kMaxB * kMaxB + qq, gridDim.x, kGramPart);
+            cs[qq] = ordered_sum<32>(part + 2 * kMaxB * kMaxB + qq, gridDim.x, kGramPart);
         for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
-            G[pq] = ordered_sum(part + pq, gridDim.x, kGramPart);
-            if constexpr (WITH_H) H[pq] = ordered_sum(part + kMaxB * kMaxB + pq, gridDim.x, kGramPart);
+            G[pq] = ordered_sum<32>(part + pq, gridDim.x, kGramPart);
+            if constexpr (WITH_H) H[pq] = ordered_sum<32>(part + kMaxB * kMaxB + pq, gridDim.x, kGramPart);
         }
         if (threadIdx.x == 0) *counter = 0;
+        __syncthreads();
+        tail_tr(1278);
         if (Rinv_next) {   // E3 here too: G = R^T R and R^-1 for the next iteration (no extra launch)
             __syncthreads();
             auto A = reinterpret_cast<double (*)[kMaxB + 1]>(base);
@@ -1072,6 +1091,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             double* shift = reinterpret_cast<double*>(base + kMaxB * (kMaxB + 1) * sizeof(double) + 16);
             chol_block(BP, G, Rinv_next, status, A, fail, shift);
         }
+        __syncthreads();
+        tail_tr(1279);
     }
 }
 

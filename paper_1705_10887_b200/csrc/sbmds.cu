@@ -345,7 +345,7 @@ void profiled(Profiler& pr, int k, cudaStream_t st, F&& f) {
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs for the grid reductions
 constexpr int kCounters = 8;
-enum { CNT_COLSUM = 0, CNT_DRED = 1, CNT_GRAM = 2, CNT_ARGMAX = 3, CNT_ROTATE = 4 };
+enum { CNT_COLSUM = 0, CNT_DRED = 1, CNT_GRAM = 2, CNT_ARGMAX = 3, CNT_ROTATE = 4, CNT_FOLD = 5 };
 
 }  // namespace
 
@@ -375,6 +375,9 @@ struct sbmds_ctx {
     bool y1f_ready = false;   // the fused landmark reduce already formed Y1f (+ its column max) this apply
     bool y2d_want = false;    // the sparse step follows this apply's D stream: digitise Y2 in the reduce
     bool y2d_ready = false;   // k_dreduce_y2d formed Y2's digit planes (launch_sp8 skips k_y2_digits)
+    bool gram_deferred = false;   // the last sparse step left G, s, R^-1 to the next fold (FoldGram)
+    int gram_parts = 0;           // its CTA count
+    DevBuf foldscr;               // lpad x 16 fp64 landmark sums of the deferred-Gram fold
     int solver = 0;        // eigs: 0 block subspace iteration, 1 restarted block Lanczos (k_lanczos.cuh)
     int lz_blocks = 0;     // Lanczos blocks per restart cycle (0: 64 / block)
     DevBuf lzQ, lzW, lzC, lzT, lzGl, lzI, lzR;
@@ -1186,8 +1189,11 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     launch_pdl(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
            (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2mm, ey2,
            h->s8yd.as<uint8_t>(), h->y16aux.as<unsigned int>() + 64);
-    if (h->sp8_dbg & 2) h->s8trace.ensure(12 * 64 * sizeof(unsigned long long));
+    if (h->sp8_dbg & 2) h->s8trace.ensure((12 * 64 + 1280) * sizeof(unsigned long long));
     auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
+    // non-Rayleigh-Ritz eigs steps whose next apply folds through k_blk_reduce_fold (sym8 D
+    // stream) leave E2/E3 to that fold (off this kernel's tail)
+    const bool defer = with_chol && !Yprev && grid >= 1 && uses_sym(h, 16) && h->dstream != 4 && !(h->sp8_dbg & 128);
     launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
            (const int8_t*)h->s8img.as<int8_t>(),
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
@@ -1197,7 +1203,9 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
            h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr, (h->sp8_dbg & 4) ? 1 : 0,
-           with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>());
+           with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>(), defer ? 1 : 0);
+    h->gram_deferred = defer;
+    h->gram_parts = grid;
 }
 
 bool fused_ok(const sbmds_ctx* h, int b) {
@@ -1271,10 +1279,23 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
             h->Y8T.ensure((size_t)3 * kMaxB * lpad);
             // (4 blocks per SM under __launch_bounds__(256, 4): 0.050 vs 0.053 ms with 3 at config 4)
             const int64_t grid = std::min<int64_t>(std::min(4, std::max(1, per_sm)) * (int64_t)h->num_sms, (lpad + 7) / 8);
-            launch_coop(k_blk_reduce_fold, dim3((unsigned)grid), dim3(256), 0, st, h->l, lpad,
+            FoldGram fg;
+            if (h->gram_deferred) {   // E2/E3 of the previous step (R^-1 into the buffer this apply folds with)
+                h->foldscr.ensure((size_t)lpad * 16 * sizeof(double));
+                fg.part = h->gpart.as<double>();
+                fg.nparts = h->gram_parts;
+                fg.G = h->G.as<double>();
+                fg.s_out = h->s.as<double>();
+                fg.Rinv_out = const_cast<double*>(Rinv);
+                fg.status = h->status.as<int>();
+                fg.scratch = h->foldscr.as<double>();
+                fg.counter = h->counters.as<unsigned int>() + CNT_FOLD;
+                h->gram_deferred = false;
+            }
+            launch_coop(k_blk_reduce_fold, dim3((unsigned)std::max<int64_t>(kFoldGramBlocks + 1, grid)), dim3(256), 0, st, h->l, lpad,
                         (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
                         (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192,
-                        h->Y8T.as<int8_t>(), reinterpret_cast<int*>(aux + 128));
+                        h->Y8T.as<int8_t>(), reinterpret_cast<int*>(aux + 128), fg);
         });
         h->y1f_ready = true;
     } else if (flags & kApplyY1Ready) {
@@ -1321,7 +1342,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
     }
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
-    h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 4);
+    h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 64);   // (sp8_dbg & 64: separate k_y2_digits, diagnostics)
     h->y2d_ready = false;
     dstream(h, b, bp, st, Rinv);
     h->y2d_want = false;
@@ -2183,6 +2204,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         h->Rinv2.ensure(kMaxB * kMaxB * sizeof(double));
         h->status.ensure(16);
         h->rr.ensure(sizeof(RrOut));
+        h->gram_deferred = false;
         if (h->solver == 1) {   // NEXT-3: restarted block Lanczos with full reorthogonalisation
             struct EvGuard {
                 cudaEvent_t a, b;
@@ -2501,7 +2523,7 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_slots")) *value = h->sp8_state > 0 ? (int64_t)h->s8.total_u : -1;   // 128-row dictionary entries
     else if (!strncmp(key, "sp8_trace_", 10)) {   // (diagnostics, sp8_dbg & 2) event timestamps of CTA 0
         const int k = atoi(key + 10);
-        if (k < 0 || k >= 12 * 64 || !h->s8trace.p) return fail(SBMDS_EINVAL, "no sp8 trace");
+        if (k < 0 || k >= 12 * 64 + 1280 || !h->s8trace.p) return fail(SBMDS_EINVAL, "no sp8 trace");
         unsigned long long v = 0;
         if (cudaMemcpy(&v, h->s8trace.as<unsigned long long>() + k, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess)
             return fail(SBMDS_ECUDA, "sp8 trace read");
