@@ -10,7 +10,6 @@
 //   k_init_philox X0 ~ N(0,1), counter-based Philox4x32-10 + Box-Muller               E1
 //   k_col_argmax, k_finalize   sign canonicalisation and Z = V diag(sqrt(max θ, 0))  E6
 #pragma once
-#include <type_traits>
 #include "common.cuh"
 
 namespace sbmds {
@@ -288,53 +287,12 @@ inline size_t gram_smem_bytes(int b) {
 // G = R^T R in one thread block (any blockDim >= b; every thread of the block calls it): the
 // body of k_chol, also run by the last CTA of the tensor-core sparse step (k_sp8.cuh) right
 // after it forms G. A: b x (kMaxB + 1) doubles of shared memory; fail / shift: shared scalars.
-// Warp-register Cholesky + R^-1 for b = NB <= 32 (warp 0; lane j holds column j of A in
-// registers, every element index compile-time): b steps of shuffles instead of block barriers and
-// shared-memory round trips. Returns false on a non-positive pivot. R's column j ends in col[],
-// R^-1's column j in x[] (x[i] = -(sum_{k=i+1..j} R_ik x_k) / R_ii, k ascending, as products
-// with 1 / R_ii).
-template <int NB>
-__device__ __forceinline__ bool chol_warp_regs(const double (*A)[kMaxB + 1], int lane, double (&col)[NB],
-                                               double (&x)[NB]) {
-    // branch-free (selects) so the unrolled steps stay converged: one reciprocal per pivot,
-    // products instead of per-lane divisions
-    const int j = lane < NB ? lane : NB - 1;
-#pragma unroll
-    for (int i = 0; i < NB; ++i) col[i] = A[i][j];
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < NB; ++k) {
-        const double d = __shfl_sync(0xffffffffu, col[k], k);   // A[k][k] from lane k
-        ok = ok && d > 0.0 && isfinite(d);
-        const double r = sqrt(d), ri = 1.0 / r;
-        const double v = col[k] * ri;                            // R[k][j] = A[k][j] / R[k][k]
-        col[k] = lane == k ? r : (lane > k ? v : col[k]);
-#pragma unroll
-        for (int i = k + 1; i < NB; ++i) {
-            const double rki = __shfl_sync(0xffffffffu, col[k], i);   // R[k][i] from lane i
-            const double u = fma(-rki, col[k], col[i]);
-            col[i] = lane >= i ? u : col[i];
-        }
-    }
-    // R^-1 column j: x_j = 1 / R_jj, x_i = -(sum_{k=i+1..j} R_ik x_k) / R_ii for i < j
-    double inv[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) inv[i] = 1.0 / __shfl_sync(0xffffffffu, col[i], i);
-#pragma unroll
-    for (int i = NB - 1; i >= 0; --i) {
-        double sacc = 0.0;
-#pragma unroll
-        for (int k = i + 1; k < NB; ++k) {
-            const double rik = __shfl_sync(0xffffffffu, col[i], k);   // R[i][k] from lane k
-            sacc = k <= lane ? fma(rik, x[k], sacc) : sacc;
-        }
-        x[i] = i == lane ? inv[i] : (i < lane ? -sacc * inv[i] : 0.0);
-    }
-    return __all_sync(0xffffffffu, ok);
-}
-
 __device__ void chol_block(int b, const double* __restrict__ G, double* __restrict__ Rinv, int* __restrict__ status,
                            double (*A)[kMaxB + 1], int* fail_s, double* shift_s) {
+    // Warp 0 factors in shared memory with __syncwarp between the b steps (no block barriers);
+    // the loops stay rolled -- this runs once per iteration from a cold instruction cache, where
+    // a fully unrolled register version measured 2x slower than its hot time. One reciprocal per
+    // pivot, products instead of per-element divisions.
     int& fail = *fail_s;
     double& shift = *shift_s;
     const int tid = threadIdx.x;
@@ -352,59 +310,33 @@ __device__ void chol_block(int b, const double* __restrict__ G, double* __restri
         __syncthreads();
         if (attempt == 1 && tid < b) A[tid][tid] += shift;
         __syncthreads();
-        if (b == 8 || b == 16 || b == 32) {   // registers of warp 0
-            if (tid < 32) {
-                bool ok = false;
-                auto run = [&](auto nbc) {
-                    constexpr int NB = decltype(nbc)::value;
-                    double col[NB], x[NB];
-                    ok = chol_warp_regs<NB>(A, tid, col, x);
-                    if (ok && tid < NB) {
-#pragma unroll
-                        for (int i = 0; i < NB; ++i) Rinv[i * NB + tid] = x[i];
-                        __syncwarp(0xffffffffu >> (32 - NB));
-                    }
-                    __syncwarp();
-                    if (ok && tid < NB) {   // R itself back into A's upper triangle (k_chol_r reads it)
-#pragma unroll
-                        for (int i = 0; i < NB; ++i)
-                            if (i <= tid) A[i][tid] = col[i];
-                    }
-                };
-                if (b == 8) run(std::integral_constant<int, 8>{});
-                else if (b == 16) run(std::integral_constant<int, 16>{});
-                else run(std::integral_constant<int, 32>{});
-                if (tid == 0) fail = ok ? 0 : 1;
-            }
-            __syncthreads();
-            if (!fail) {
-                if (tid == 0) *status = (shift > 0.0) ? 1 : 0;
-                return;
-            }
-            __syncthreads();
-            continue;
-        }
-        // right-looking factorization by warp 0 (lane j owns columns j, j + 32: no block-wide
-        // barriers between the b steps); the same operations per element as a block-wide loop
         if (tid < 32) {
             const int lane = tid;
             int f = 0;
+#pragma unroll 1
             for (int k = 0; k < b; ++k) {
                 const double d = A[k][k];
-                if (!(d > 0.0) || !isfinite(d)) {
+                if (!(d > 0.0) || !isfinite(d)) {   // (the same value in every lane)
                     f = 1;
                     break;
                 }
-                const double r = sqrt(d);
+                const double r = sqrt(d), ri = 1.0 / r;
                 __syncwarp();
-                for (int j = lane; j < b; j += 32) {
-                    if (j == k) A[k][k] = r;
-                    else if (j > k) A[k][j] /= r;
+                for (int j = k + 1 + lane; j < b; j += 32) A[k][j] *= ri;   // row k of R
+                if (lane == 0) A[k][k] = r;
+                __syncwarp();
+                // trailing update A[i][j] -= R[k][i] R[k][j], k < i <= j < b: element e of the
+                // m (m + 1) / 2 upper entries, row-major
+                const int m = b - k - 1;
+                for (int e = lane; e < m * (m + 1) / 2; e += 32) {
+                    int i = 0, rem = e;
+                    while (rem >= m - i) {
+                        rem -= m - i;
+                        ++i;
+                    }
+                    const int ii = k + 1 + i, jj = ii + rem;
+                    A[ii][jj] = fma(-A[k][ii], A[k][jj], A[ii][jj]);
                 }
-                __syncwarp();
-                for (int j = lane; j < b; j += 32)
-                    if (j > k)
-                        for (int i = k + 1; i <= j; ++i) A[i][j] -= A[k][i] * A[k][j];
                 __syncwarp();
             }
             if (lane == 0) fail = f;
@@ -424,7 +356,7 @@ __device__ void chol_block(int b, const double* __restrict__ G, double* __restri
         A[c][kMaxB] = 1.0 / A[c][c];
         for (int i = c - 1; i >= 0; --i) {
             double sacc = 0.0;
-            for (int k = i + 1; k <= c; ++k) sacc += A[i][k] * (k == c ? A[c][kMaxB] : A[c][k]);
+            for (int k = i + 1; k <= c; ++k) sacc = fma(A[i][k], k == c ? A[c][kMaxB] : A[c][k], sacc);
             A[c][i] = -sacc / A[i][i];
         }
         for (int i = 0; i < b; ++i) Rinv[i * b + c] = i < c ? A[c][i] : (i == c ? A[c][kMaxB] : 0.0);
