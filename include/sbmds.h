@@ -156,8 +156,13 @@ const char* sbmds_last_error(void);
  *     "lanczos_blocks" blocks per Lanczos cycle (0 = 64 / block, at least 2)
  *     "sp8_dbg"        diagnostics of the tensor-core step (timing only; bits 1, 4, 8, 16 make
  *                      results invalid): 1 skip the T product, 2 record a timeline of CTA 0
- *                      (stats "sp8_trace_<event * 64 + block>"), 4 stream the images only,
- *                      8 T product in the last iteration too, 16 no H' term
+ *                      (stats "sp8_trace_<event * 64 + block>"; entries 768 + c / 1024 + c /
+ *                      1280 + c: CTA c's start / roles done / Gram partials written, 1277-1279
+ *                      the last CTA's Gram sums and Cholesky), 4 stream the images only,
+ *                      8 T product in the last iteration too, 16 no H' term; valid-result
+ *                      switches: 64 Y2's digit planes by a separate k_y2_digits instead of the
+ *                      cooperative reduce, 128 Gram sums + Cholesky in the step's last CTA on
+ *                      every step (not deferred to the next fold)
  *     "use_graph"      (0/1, default 0) eigs: replay Rayleigh-Ritz segments from CUDA graphs
  *     "profile"        bit mask of kernel families timed with CUDA events on the launching
  *                      stream (bit k = family k of: colsum csc dstream dreduce csr gram chol

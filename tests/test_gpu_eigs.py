@@ -329,3 +329,34 @@ def test_tensor_core_sparse_step_duplicate_entries():
         assert h.stat("sp8_state") == 1
     assert np.allclose(a[0], ref[0], rtol=1e-5), (a[0], ref[0])
     assert O.principal_angle(a[1], ref[1]) <= 1e-3
+
+
+def test_deferred_gram_and_fused_y2_digits():
+    """Config 2 on the symmetric-half int8 D stream (dstream = 3), so every eigs iteration after
+    the first runs the cooperative reduces: the non-Rayleigh-Ritz sparse steps leave their Gram
+    sums and Cholesky to the next fold (FoldGram), and the D-partial reduce forms Y2's digit
+    planes (k_dreduce_y2d). Switching either off (sp8_dbg 128: Gram in the step's last CTA; 64:
+    k_dreduce_pair + k_y2_digits) changes only summation orders: the same iteration within the
+    fp32 noise, each path bitwise deterministic, and the solve converges to the oracle."""
+    p = configs.config(2)
+    it = 25
+    with handle(p) as h:
+        h.set_option("dstream", 3)
+        h.set_option("fuse", 3)
+        runs = {}
+        for dbg in (0, 128, 64, 128 | 64):
+            h.set_option("sp8_dbg", dbg)
+            runs[dbg] = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=5)
+            assert h.stat("sp8_state") == 1
+        h.set_option("sp8_dbg", 0)
+        again = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=5)
+        lam, V, Z, info = gpu_eigs(h, p.m, 16, max_iters=500, tol=1e-6, seed=5)
+    base = runs[0]
+    assert np.array_equal(base[0], again[0]) and np.array_equal(base[1], again[1])
+    for dbg, r in runs.items():
+        assert np.allclose(r[0], base[0], rtol=1e-6), (dbg, r[0], base[0])
+        assert O.principal_angle(r[1], base[1]) <= 1e-3, dbg
+    assert info["converged"] == 1
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, p.m)
+    check_against(lam, V, Z, lam_o, V_o, Z_o)
