@@ -351,33 +351,36 @@ __global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __res
 }
 
 // k_dreduce_pair's reduction at b = 16 with 16-byte loads: a thread owns four columns of one
-// row (a warp load covers 8 rows x 16 columns = 512 B, against 128 B for the scalar kernel) and
-// keeps 8 slots in flight. Every Y2 element is the same fp64 sum over its slots in slot order
-// as k_dreduce_pair forms it (bitwise-identical Y2); t's per-block partial order differs.
+// row and one half of its slots (8 in flight); Y2 = (first half + second half) in fp64, each
+// half in slot order -- a fixed order, deterministic, not bitwise k_dreduce_pair's.
 __device__ __forceinline__ void dreduce16_body(int64_t l, int b, const int* __restrict__ xptr,
                                                const float* __restrict__ P, const int* __restrict__ dexp,
                                                const int* __restrict__ yexp, const double* __restrict__ w,
                                                float* __restrict__ Y2, double* __restrict__ tpart,
                                                double* __restrict__ t, unsigned int* __restrict__ counter,
                                                unsigned int* __restrict__ y2mm) {
-    constexpr int BP = 16, RPB = 64, U = 8;
+    // 8 threads per row: column quad cq, and the first / second half of the row tile's slots
+    // (adjacent lanes, summed in slot order each, then first + second); 32 rows per block pass
+    constexpr int BP = 16, RPB = 32, U = 8;
     __shared__ double red[RPB][BP + 1];
     __shared__ float cmx[RPB][BP + 1], cmn[RPB][BP + 1];
-    const int tid = threadIdx.x, cq = tid & 3, rloc = tid >> 2;
+    const int tid = threadIdx.x, hh = tid & 1, cq = (tid >> 1) & 3, rloc = tid >> 3;
     double unscale[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) unscale[u] = ldexp(1.0, -(*dexp + yexp[4 * cq + u]));
     float m[4] = {-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f}, mn[4] = {3.0e38f, 3.0e38f, 3.0e38f, 3.0e38f};
     double acc_t[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t r0 = (int64_t)blockIdx.x * RPB; r0 < l; r0 += (int64_t)gridDim.x * RPB) {
-        const int64_t r = r0 + rloc;
+    const int64_t npass = (l + (int64_t)gridDim.x * RPB - 1) / ((int64_t)gridDim.x * RPB);
+    for (int64_t ps = 0; ps < npass; ++ps) {   // (uniform trip count: the halves meet in shuffles)
+        const int64_t r = (ps * gridDim.x + blockIdx.x) * RPB + rloc;
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
         if (r < l) {
             const int X = (int)(r >> 7), rr = (int)(r & 127);
-            const int q0 = xptr[X], q1 = xptr[X + 1];
+            const int q0 = xptr[X], q1 = xptr[X + 1], qm = q0 + (q1 - q0 + 1) / 2;
+            const int a0 = hh ? qm : q0, a1 = hh ? q1 : qm;
             const float4* base = reinterpret_cast<const float4*>(P) + (int64_t)rr * (BP / 4) + cq;
-            double v[4] = {0.0, 0.0, 0.0, 0.0};
-            int q = q0;
-            for (; q + U <= q1; q += U) {
+            int q = a0;
+            for (; q + U <= a1; q += U) {
                 float4 pv[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) pv[u] = __ldcs(base + (int64_t)(q + u) * (128 * BP / 4));
@@ -389,13 +392,20 @@ __device__ __forceinline__ void dreduce16_body(int64_t l, int b, const int* __re
                     v[3] += (double)pv[u].w;
                 }
             }
-            for (; q < q1; ++q) {
+            for (; q < a1; ++q) {
                 const float4 pv = __ldcs(base + (int64_t)q * (128 * BP / 4));
                 v[0] += (double)pv.x;
                 v[1] += (double)pv.y;
                 v[2] += (double)pv.z;
                 v[3] += (double)pv.w;
             }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double o = __shfl_xor_sync(0xffffffffu, v[u], 1);
+            v[u] = hh ? o + v[u] : v[u] + o;   // first half + second half in both lanes
+        }
+        if (r < l && hh == 0) {
             float4 o;
             float* of = &o.x;
             const double wr = w[r];
@@ -410,11 +420,13 @@ __device__ __forceinline__ void dreduce16_body(int64_t l, int b, const int* __re
             reinterpret_cast<float4*>(Y2 + r * BP)[cq] = o;
         }
     }
+    if (hh == 0) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        red[rloc][4 * cq + u] = acc_t[u];
-        cmx[rloc][4 * cq + u] = m[u];
-        cmn[rloc][4 * cq + u] = mn[u];
+        for (int u = 0; u < 4; ++u) {
+            red[rloc][4 * cq + u] = acc_t[u];
+            cmx[rloc][4 * cq + u] = m[u];
+            cmn[rloc][4 * cq + u] = mn[u];
+        }
     }
     __syncthreads();
     if (tid < BP) {
