@@ -336,13 +336,39 @@ __global__ void __launch_bounds__(256, 4) k_blk_reduce_fold(int64_t l, int64_t l
                 if (threadIdx.x == 0) *fg.counter = 0;
             }
         } else {
-            for (int64_t j0 = (int64_t)(blockIdx.x - kFoldGramBlocks) * JPB; j0 < l;
-                 j0 += (int64_t)(gridDim.x - kFoldGramBlocks) * JPB) {
-                const int64_t j = j0 + jl;
+            // 8 threads per landmark here: column quad and the first / second half of its slots
+            // (each half in slot order, then first + second), 32 landmarks per block pass
+            const int hh = threadIdx.x & 1, cq2 = (threadIdx.x >> 1) & 3, jl2 = threadIdx.x >> 3;
+            const int64_t nlb = gridDim.x - kFoldGramBlocks, npass = (l + nlb * 32 - 1) / (nlb * 32);
+            for (int64_t ps = 0; ps < npass; ++ps) {
+                const int64_t j = (ps * nlb + (blockIdx.x - kFoldGramBlocks)) * 32 + jl2;
+                double a[4] = {0.0, 0.0, 0.0, 0.0};
                 if (j < l) {
-                    double a[4];
-                    landmark_sum(j, a);
-                    double2* dst = reinterpret_cast<double2*>(fg.scratch + j * BP + 4 * cq);
+                    const int32_t b0 = __ldg(jptr + j), e0 = __ldg(jptr + j + 1), bm = b0 + (e0 - b0 + 1) / 2;
+                    const int32_t k0 = hh ? bm : b0, k1 = hh ? e0 : bm;
+                    const float4* base = reinterpret_cast<const float4*>(P1) + cq2;
+                    int32_t k = k0;
+                    for (; k + U <= k1; k += U) {
+                        float4 pv[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) pv[u] = __ldcs(base + (int64_t)(k + u) * (BP / 4));
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w;
+                        }
+                    }
+                    for (; k < k1; ++k) {
+                        const float4 t = __ldcs(base + (int64_t)k * (BP / 4));
+                        a[0] += t.x; a[1] += t.y; a[2] += t.z; a[3] += t.w;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double o = __shfl_xor_sync(0xffffffffu, a[u], 1);
+                    a[u] = hh ? o + a[u] : a[u] + o;
+                }
+                if (j < l && hh == 0) {
+                    double2* dst = reinterpret_cast<double2*>(fg.scratch + j * BP + 4 * cq2);
                     dst[0] = make_double2(a[0], a[1]);
                     dst[1] = make_double2(a[2], a[3]);
                 }
