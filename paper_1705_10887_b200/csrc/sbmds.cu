@@ -1292,7 +1292,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
                 fg.counter = h->counters.as<unsigned int>() + CNT_FOLD;
                 h->gram_deferred = false;
             }
-            launch_coop(k_blk_reduce_fold, dim3((unsigned)std::max<int64_t>(kFoldGramBlocks + 1, grid)), dim3(256), 0, st, h->l, lpad,
+            launch_coop_pdl(k_blk_reduce_fold, dim3((unsigned)std::max<int64_t>(kFoldGramBlocks + 1, grid)), dim3(256), 0, st, h->l, lpad,
                         (const int32_t*)h->s8.jptr.as<int32_t>(), (const float*)h->P1.as<float>(), wvec(h),
                         (const double*)h->s.as<double>(), Rinv, h->Y1f.as<float>(), aux + 64, aux + 192,
                         h->Y8T.as<int8_t>(), reinterpret_cast<int*>(aux + 128), fg);
