@@ -404,7 +404,10 @@ struct sbmds_ctx {
     // int8 symmetric-half stream (k_dstream_sym8.cuh): D as three digit planes per upper tile
     DevBuf Dt8, Y8T;
     bool dt8_ok = false;
-    bool dmax8_ok = false;   // aux[2] = max |D| over the block upper triangle (formed in create, overlapping D's upload)
+    bool dmax8_ok = false;
+    cudaStream_t pack_st = nullptr;   // create's D pack (host D): runs past create's return
+    cudaEvent_t pack_ev = nullptr;
+    bool pack_pending = false;        // the first D-stream launch waits for pack_ev   // aux[2] = max |D| over the block upper triangle (formed in create, overlapping D's upload)
     struct PairPlan {
         bool ok = false;
         int S = 0, NT = 0, P = 0, nslots = 0;
@@ -676,8 +679,9 @@ PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous) {
     return ph;
 }
 
-void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S, int gN = 1, bool contiguous = false) {
-    const PlanHost ph = plan_host(h->l, max_pairs, S, gN, contiguous);
+void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S, int gN = 1, bool contiguous = false,
+                     const PlanHost* pre = nullptr) {
+    const PlanHost ph = pre ? *pre : plan_host(h->l, max_pairs, S, gN, contiguous);
     const int nslots = (int)ph.slot_x.size();
     if (contiguous) {
         pl.smap.ensure(ph.smap.size() * sizeof(int));
@@ -911,6 +915,10 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         attr_set[pi] = true;
     }
     const int64_t lpad = y1t_lpad(h);
+    if (h->pack_pending) {   // create's D pack, still running on its own stream
+        CK(cudaStreamWaitEvent(st, h->pack_ev, 0));
+        h->pack_pending = false;
+    }
     static const bool trace = getenv("SBMDS_TRACE_EIGS") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
     auto dphase = [&](const char* what) {
@@ -1561,6 +1569,15 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
 
 void destroy_ctx(sbmds_ctx* h) {
     if (!h) return;
+    if (h->pack_st) {
+        cudaStreamSynchronize(h->pack_st);
+        cudaStreamDestroy(h->pack_st);
+        h->pack_st = nullptr;
+    }
+    if (h->pack_ev) {
+        cudaEventDestroy(h->pack_ev);
+        h->pack_ev = nullptr;
+    }
     if (h->gstream) {
         cudaStreamSynchronize(h->gstream);
         cudaStreamDestroy(h->gstream);
@@ -1819,6 +1836,10 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         tmpC.release();
 
         tphase("S side done");
+        // the int8 D stream's schedule (host work) while D is still crossing the link
+        PlanHost ph16;
+        const bool pre_plan = h->dmax8_ok && !h->s8plan[1].ok;
+        if (pre_plan) ph16 = plan_host(l, h->num_sms, Sym8Cfg<16>::S, Sym8Cfg<16>::GN, true);
         // ---- D_ll: borrow (device, l % 4 == 0), copy a device D into a 16-byte-pitched buffer, or
         // join the host upload started above
         if (!d_dev) {
@@ -1860,6 +1881,25 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         tphase("S-side stream idle");
         join_dside();
         tphase("D upload joined");
+        if (pre_plan) {
+            // D and max |D| have landed: upload the schedule and pack D (int8 digits of the
+            // upper tiles) on a handle stream that runs on past create's return; the first
+            // D-stream launch waits for it
+            using C8 = Sym8Cfg<16>;
+            auto& pl = h->s8plan[1];
+            build_pair_plan(h, pl, h->num_sms, C8::S, C8::GN, true, &ph16);
+            h->Dt8.ensure((size_t)pl.ntiles * C8::A_BYTES);
+            unsigned int* aux = h->y16aux.as<unsigned int>();
+            CK(cudaStreamCreateWithFlags(&h->pack_st, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&h->pack_ev, cudaEventDisableTiming));
+            launch(k_pack_sym8, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0,
+                   h->pack_st, (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
+                   (const unsigned int*)(aux + 2), reinterpret_cast<int*>(aux + 3), h->Dt8.as<int8_t>());
+            CK(cudaEventRecord(h->pack_ev, h->pack_st));
+            h->dt8_ok = true;
+            h->pack_pending = true;
+            tphase("D pack issued");
+        }
     } catch (const CudaError& e) {
         join_dside(); destroy_ctx(h);
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
