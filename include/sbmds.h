@@ -174,6 +174,8 @@ const char* sbmds_last_error(void);
  *     "d_borrowed", "csc_bytes", "workspace_bytes", "blocked_umax" (largest per-block
  *     landmark dictionary, -1 if the row-blocked structure is off), "blocked_slots",
  *     "dstream_path" (1 FFMA, 2 full-D tcgen05, 3 symmetric half; of the last apply),
+ *     "d_packed_in_create" (1: a host D was packed for the int8 stream by create, on a handle
+ *     stream the first D-stream launch waits for),
  *     "dstream_bytes" (its algorithmic bytes per launch), "sp8_state" (tensor-core step: 1
  *     built, -1 not applicable, 0 not tried yet), "sp8_bytes" (its S images), "sp8_umax"
  *     (largest 128-row dictionary), "<family>_ns" / "<family>_launches"

@@ -2547,6 +2547,7 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "d_borrowed")) *value = h->d_borrowed ? 1 : 0;
     else if (!strcmp(key, "blocked_umax")) *value = h->blocked ? (int64_t)h->umax : -1;
     else if (!strcmp(key, "dstream_path")) *value = h->last_dpath;
+    else if (!strcmp(key, "d_packed_in_create")) *value = h->pack_ev != nullptr ? 1 : 0;
     else if (!strcmp(key, "dstream_bytes")) *value = h->last_dbytes;
     else if (!strcmp(key, "h2d_bytes")) *value = h->h2d_bytes;
     else if (!strcmp(key, "d_lower_missing")) *value = h->d_lower_missing ? 1 : 0;

@@ -367,3 +367,24 @@ def test_apply_config4_full_size():
         assert h.stat("dstream_path") == 3
     Yo = oracle_apply(p, X)
     assert relerr(Y, Yo) <= TOL, relerr(Y, Yo)
+
+
+def test_host_d_pack_issued_in_create():
+    """A host D large enough for the int8 symmetric-half stream (auto path): create takes max |D|
+    over the landed strips, builds the stream's schedule while D crosses the link and packs D on
+    a handle stream past its return; the first D-stream launch waits for that pack. The host-D
+    handle's apply equals the device-D handle's bit for bit (same packing, same max) and meets
+    the oracle bar; so does an eigs solve started right after create."""
+    p = configs.random_problem(40_000, 5_000, 16, seed=9, name="host_d_pack")
+    X = configs.x_block(p.n, 16, seed=4)
+    ref = oracle_apply(p, X)
+    with make_handle(p, device="numpy") as hh, make_handle(p) as hd:
+        assert hh.stat("d_lower_missing") == 1
+        assert hh.stat("d_packed_in_create") == 1 and hd.stat("d_packed_in_create") == 0
+        lam_h = hh.eigs(3, 16, max_iters=8, tol=0.0)[0]   # the first D-stream launch is inside eigs
+        lam_d = hd.eigs(3, 16, max_iters=8, tol=0.0)[0]
+        Yh, Yd = run_apply(hh, X), run_apply(hd, X)
+        assert hh.stat("dstream_path") == 3 and hd.stat("dstream_path") == 3
+    assert np.array_equal(Yh, Yd)
+    assert np.array_equal(np.asarray(lam_h), np.asarray(lam_d))
+    assert relerr(Yh, ref) <= TOL
