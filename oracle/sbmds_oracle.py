@@ -18,9 +18,22 @@ fp32-stored inputs upcast exactly:
     Lanczos on matrix-vector products, as sBMDS does (PAPER.md:221-222);
   * BMDS, the paper's QR route, as a second independent path.
 
-Pins (tests/test_oracle.py, ``-m "not gpu"``): closed forms CF1-CF4 (DESIGN.md
-§5), SPEC.md's worked MDS examples, invariants, and
-brute-force quadruple sums on tiny inputs. No function here is "parity unpinned".
+Pins (tests/test_oracle.py, ``-m "not gpu"``), per function — each against a
+closed form, a worked example or brute force, never against a re-typed formula:
+
+  dense_operator / approx_sqdist  brute-force quadruple sum; CF1-CF4; SPEC examples
+  apply                           brute force; CF2 (rank-3 Gram); mutation test
+  _dense_times (multi-block)      rank-structure closed form of squared distances at
+                                  l = 5000 (> 2048-row blocks, ragged tail), fp32 and fp64
+  apply_raw / rel_sq_error        S = I closed form; brute-force S D S^T; J-sandwich
+  eigs_dense / mds_dense / top_m  SPEC.md:55-57, :414-416 goldens; CF1; CF3 spectrum
+  eigs_matfree / bmds             CF2 (eigenpairs = SVD of JSY); dense agreement, cfg 1
+  embedding                       explicit λ (negative -> zero column)
+  residuals                       CF2: 0 at exact pairs, closed form for a rotated v
+  principal_angle                 1-D and 2-D subspaces with known distinct angles (max)
+  relgap                          explicit spectra
+
+Every function is pinned; none is "parity unpinned" (DESIGN.md §2 lists the pins).
 """
 from __future__ import annotations
 

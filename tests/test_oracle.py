@@ -286,3 +286,79 @@ def test_apply_raw_pins():
     J = np.eye(n) - np.ones((n, n)) / n
     assert np.allclose(-0.5 * J @ O.apply_raw(S, D, J @ Xn), O.apply(S, D, Xn))
     assert O.rel_sq_error(E, E) == 0.0 and abs(O.rel_sq_error(2 * E, E) - 1.0) < 1e-12
+
+
+# --------------------------------------------------------------------------- helper pins
+def test_residuals_closed_form():
+    """residuals() (the SPEC.md:52 residual ||B~v - θv||) on CF2, where B~ = A A^T, A = JSY.
+    Exact eigenpairs (λ_i = σ_i², v_i = u_i) give 0. A rotated v = cos t u_1 + sin t z with
+    z ⊥ range(A) (so B~z = 0) has B~v = cos t σ_1² u_1, hence, for any θ,
+    ||B~v - θv||² = cos²t (σ_1² - θ)² + θ² sin²t — closed form, not the oracle's formula."""
+    S, D, JSY = cf2_problem()
+    U, s, _ = np.linalg.svd(JSY, full_matrices=False)
+    r0 = O.residuals(S, D, s ** 2, U)
+    assert r0.shape == (3,) and np.all(r0 < 1e-10 * s[0] ** 2)
+    rng = np.random.default_rng(11)
+    z = rng.standard_normal(JSY.shape[0])
+    z -= U @ (U.T @ z)                                  # z ⊥ span(U) = range(A)
+    z /= np.linalg.norm(z)
+    for t, theta in ((0.1, s[0] ** 2), (0.4, 0.7 * s[0] ** 2), (1.2, 2.0)):
+        v = np.cos(t) * U[:, 0] + np.sin(t) * z
+        want = np.sqrt((np.cos(t) * (s[0] ** 2 - theta)) ** 2 + (theta * np.sin(t)) ** 2)
+        got = O.residuals(S, D, np.array([theta]), v[:, None])[0]
+        assert abs(got - want) < 1e-9 * s[0] ** 2, (t, got, want)
+
+
+def test_principal_angle_two_dimensional():
+    """Largest principal angle between 2-D subspaces with known distinct angles a < b:
+    span(e1, e2) vs span(cos a e1 + sin a e3, cos b e2 + sin b e4) -> b (not a), independent
+    of the bases chosen (the second is given as a non-orthonormal mix of its vectors)."""
+    a, b = 0.2, 0.7
+    E = np.eye(6)
+    A = E[:, :2]
+    B = np.stack([np.cos(a) * E[:, 0] + np.sin(a) * E[:, 2],
+                  np.cos(b) * E[:, 1] + np.sin(b) * E[:, 3]], axis=1)
+    mix = np.array([[2.0, 1.0], [-0.5, 3.0]])
+    for Bb in (B, B @ mix):
+        assert abs(O.principal_angle(A, Bb) - b) < 1e-12
+        assert abs(O.principal_angle(Bb, A) - b) < 1e-12
+    assert O.principal_angle(A, A @ mix) < 1e-7          # same subspace, different basis
+    # orthogonal complement: π/2
+    assert abs(O.principal_angle(A, E[:, 4:6]) - np.pi / 2) < 1e-12
+
+
+def test_dense_times_multiblock_closed_form():
+    """_dense_times (the D product of the oracle apply) at l = 5000 > 2048 rows per block, with
+    a ragged last block: D = squared distances of integer points (exact in fp32), whose product
+    has the closed form D T = a (1^T T) - 2 Y (Y^T T) + 1 (a^T T), a_i = |y_i|^2. Checked for
+    fp32 and fp64 D, and through the full apply against CF2's rank-3 Gram at the same l."""
+    rng = np.random.default_rng(12)
+    l = 5000
+    Y = rng.integers(-40, 41, size=(l, 3)).astype(np.float64)
+    D64 = sqdist(Y)
+    assert D64.max() < 2 ** 24
+    T = rng.standard_normal((l, 5))
+    a = (Y ** 2).sum(1)
+    want = np.outer(a, T.sum(0)) - 2 * Y @ (Y.T @ T) + np.outer(np.ones(l), a @ T)
+    for D in (D64, D64.astype(np.float32)):
+        got = O._dense_times(D, T)
+        assert np.linalg.norm(got - want) < 1e-12 * np.linalg.norm(want)
+    # full apply: PoU S over these landmarks -> B~ = (JSY)(JSY)^T
+    n = 7000
+    S = random_pou(n, l, 4, rng)
+    X = rng.standard_normal((n, 3))
+    A = S @ Y
+    A = A - A.mean(0)
+    ref = A @ (A.T @ X)
+    got = O.apply(S, D64.astype(np.float32), X)
+    assert np.linalg.norm(got - ref) < 1e-11 * np.linalg.norm(ref)
+
+
+def test_relgap_explicit_spectrum():
+    """relgap = (λ_m - λ_{m+1}) / |λ_1| (R4) on explicit descending spectra,
+    including a negative λ_1 (absolute value in the denominator)."""
+    lam = np.array([10.0, 4.0, 3.5, -20.0])
+    assert abs(O.relgap(lam, 1) - 0.6) < 1e-15
+    assert abs(O.relgap(lam, 2) - 0.05) < 1e-15
+    assert abs(O.relgap(lam, 3) - 2.35) < 1e-15
+    assert abs(O.relgap(np.array([-1.0, -3.0]), 1) - 2.0) < 1e-15
