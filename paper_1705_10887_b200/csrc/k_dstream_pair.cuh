@@ -386,19 +386,41 @@ __global__ void __launch_bounds__(256) k_absmax(const float* __restrict__ x, int
 
 // max |x| over the block upper triangle of D (row r: columns >= 128 floor(r / 128)), which is
 // all of D that is present when create uploaded only the upper strips (and all the packed
-// path reads); D is symmetric (R12), so this is max |D|.
+// path reads); D is symmetric (R12), so this is max |D|. With `hist` (256 counters) it also
+// counts the entries per binade (the biased float exponent of |x|): the int8 stream's
+// precision check compares max |D| with the median entry (sbmds.cu dq_decide).
 __global__ void __launch_bounds__(256) k_absmax_upper(const float* __restrict__ x, int64_t l, int64_t ld,
                                                       unsigned int* __restrict__ out, int64_t r_begin = 0,
-                                                      int64_t r_end = -1) {
+                                                      int64_t r_end = -1, unsigned int* __restrict__ hist = nullptr) {
+    __shared__ unsigned int sh[256];
+    if (hist) {
+        sh[threadIdx.x] = 0u;
+        __syncthreads();
+    }
     float m = 0.f;
     if (r_end < 0) r_end = l;
+    const int lane = threadIdx.x & 31;
     for (int64_t r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
         const float* row = x + r * ld;
-        for (int64_t c = (r >> 7) * 128 + threadIdx.x; c < l; c += 256) m = fmaxf(m, fabsf(__ldcs(row + c)));
+        for (int64_t c0 = (r >> 7) * 128; c0 < l; c0 += 256) {   // (block-uniform trip count)
+            const int64_t c = c0 + threadIdx.x;
+            const bool have = c < l;
+            const float a = have ? fabsf(__ldcs(row + c)) : 0.f;
+            m = fmaxf(m, a);
+            if (hist) {   // one shared-memory add per distinct binade in the warp
+                const unsigned e = have ? __float_as_uint(a) >> 23 : 256u;
+                const unsigned peers = __match_any_sync(0xffffffffu, e);
+                if (have && (__ffs(peers) - 1) == lane) atomicAdd(&sh[e], (unsigned)__popc(peers));
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+    if (lane == 0) atomicMax(out, __float_as_uint(m));
+    if (hist) {
+        __syncthreads();
+        if (sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
+    }
 }
 
 // Fill the block lower triangle (row r, columns < 128 floor(r / 128)) from the upper one:

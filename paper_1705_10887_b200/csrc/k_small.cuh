@@ -305,7 +305,7 @@ __device__ void chol_block(int b, const double* __restrict__ G, double* __restri
             fail = 0;
             double tr = 0.0;
             for (int i = 0; i < b; ++i) tr += fabs(G[i * b + i]);
-            shift = attempt == 0 ? 0.0 : 1e-13 * tr + 1e-300;
+            shift = attempt == 0 ? 0.0 : 1e-13 * tr;   // (an all-zero G stays a breakdown)
         }
         __syncthreads();
         if (attempt == 1 && tid < b) A[tid][tid] += shift;

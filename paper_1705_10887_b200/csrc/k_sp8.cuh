@@ -200,33 +200,52 @@ __device__ __forceinline__ float sp8_row_entry(const uint16_t* __restrict__ lcol
 __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, const int32_t* __restrict__ rp,
                                                    const float* __restrict__ val, const uint16_t* __restrict__ lcol,
                                                    const int32_t* __restrict__ doff, const int64_t* __restrict__ ioff,
-                                                   int8_t* __restrict__ img, int* __restrict__ escale) {
-    __shared__ float red[4];
+                                                   int8_t* __restrict__ img, int* __restrict__ escale,
+                                                   unsigned int* __restrict__ rrange) {
+    __shared__ float red[4], red2[4];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int64_t B = blockIdx.x; B < nblk; B += gridDim.x) {
         const int64_t r0 = B * kSp8RB;
         const int rows = (int)((n - r0) < kSp8RB ? (n - r0) : kSp8RB);
-        float m = 0.f;
+        float m = 0.f, mn = INFINITY;   // block max |S|, smallest nonzero row max (this warp's rows)
         for (int r = wid; r < rows; r += 4) {
             const int32_t beg = rp[r0 + r], end = rp[r0 + r + 1];
             const bool longrow = end - beg > 32;   // (warp-uniform; the match runs on every lane)
             bool first;
             int col;
             const float v = sp8_row_entry(lcol, val, beg, longrow ? beg : end, lane, first, col);
+            float rm = 0.f;
             if (!longrow) {
-                if (first) m = fmaxf(m, fabsf(v));
+                if (first) rm = fabsf(v);
             } else {
                 for (int32_t e = beg + lane; e < end; e += 32)
-                    if (sp8_first_of_col(lcol, beg, e)) m = fmaxf(m, fabsf(sp8_col_sum(lcol, val, e, end)));
+                    if (sp8_first_of_col(lcol, beg, e)) rm = fmaxf(rm, fabsf(sp8_col_sum(lcol, val, e, end)));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rm = fmaxf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+            m = fmaxf(m, rm);
+            if (rm > 0.f) mn = fminf(mn, rm);
+        }
+        __syncthreads();
+        if (lane == 0) {
+            red[wid] = m;
+            red2[wid] = mn;
+        }
+        __syncthreads();
+        const float bmax = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+        const float bmin = fminf(fminf(red2[0], red2[1]), fminf(red2[2], red2[3]));
+        const int eS = i8_scale_exp(bmax);
+        if (threadIdx.x == 0) {
+            escale[B] = eS;
+            // precision check: binades between the block's max and its smallest row maximum (a
+            // row far below the block's scale keeps few significant bits in the shared quantum)
+            if (bmax > 0.f && bmin < INFINITY) {
+                int e1, e2;
+                frexpf(bmax, &e1);
+                frexpf(bmin, &e2);
+                atomicMax(rrange, (unsigned)(e1 - e2));
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        __syncthreads();
-        if (lane == 0) red[wid] = m;
-        __syncthreads();
-        const int eS = i8_scale_exp(fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3])));
-        if (threadIdx.x == 0) escale[B] = eS;
         const int dp = sp8_dpad(doff[B + 1] - doff[B]);
         int8_t* out = img + ioff[B];
         auto put = [&](int r, int col, float v) {

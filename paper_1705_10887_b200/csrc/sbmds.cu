@@ -3,6 +3,7 @@
 #include <cub/cub.cuh>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -11,6 +12,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -115,24 +118,69 @@ void launch_coop_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 HangRecord* g_hang_host = nullptr;
 
-// Host-mapped record the device watchdog writes before trapping (common.cuh mbar_wait).
+// NVTX ranges (SURVEY §5 tracing): one per public call and per eigs / create stage, on the host
+// timeline of nsys / ncu --nvtx; no cost without a tool attached.
+struct Nvtx {
+    explicit Nvtx(const char* what) { nvtxRangePushA(what); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
+
+// Per-device one-time setup. CUDA keeps kernel attributes, the default memory pool and module
+// symbols per device, so every "once" below is keyed by the current device and guarded by a
+// mutex (distinct handles may live on different GPUs and be used from different threads).
+std::mutex g_once_mu;
+
+bool once_per_device(const void* what, int extra = 0) {
+    static std::set<std::tuple<int, const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_once_mu);
+    return done.insert(std::make_tuple(dev, what, extra)).second;
+}
+
+// Opt `kernel` into `bytes` of dynamic shared memory on the current device (once per device
+// and size; a later launch with the same size skips the driver call).
+template <typename K>
+void smem_attr(K* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<int, const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);   // held across the call: no launch sees the key before the attribute
+    const auto key = std::make_tuple(dev, (const void*)kernel, bytes);
+    if (done.count(key)) return;
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert(key);
+}
+
+// Host-mapped record the device watchdog writes before trapping (common.cuh mbar_wait); the
+// symbol g_hang exists once per device, so each device gets the (shared) record's address.
 void install_hang_record() {
-    static bool done = false;
-    if (done) return;
-    HangRecord* hp = nullptr;
-    if (cudaHostAlloc(reinterpret_cast<void**>(&hp), sizeof(HangRecord), cudaHostAllocMapped) != cudaSuccess) {
-        cudaGetLastError();
-        return;
+    static HangRecord* hp = nullptr;
+    static HangRecord* dp = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_once_mu);
+        if (!hp) {
+            if (cudaHostAlloc(reinterpret_cast<void**>(&hp), sizeof(HangRecord), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                hp = nullptr;
+                return;
+            }
+            memset(hp, 0, sizeof(HangRecord));
+            if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), hp, 0) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+        }
     }
-    memset(hp, 0, sizeof(HangRecord));
-    HangRecord* dp = nullptr;
-    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), hp, 0) != cudaSuccess ||
-        cudaMemcpyToSymbol(g_hang, &dp, sizeof(dp)) != cudaSuccess) {
+    if (!dp || !once_per_device((const void*)&install_hang_record)) return;
+    if (cudaMemcpyToSymbol(g_hang, &dp, sizeof(dp)) != cudaSuccess) {
         cudaGetLastError();
         return;
     }
     g_hang_host = hp;
-    done = true;
 }
 
 // Small device -> host readbacks during create go through a host-mapped buffer written by a
@@ -197,8 +245,7 @@ int next_pow2(int b) {
 // device is idle for them (destroy syncs first; a growing ensure() syncs before freeing).
 // Create-time temporaries use plain cudaMalloc/cudaFree.
 void configure_pool_once() {
-    static bool done = false;
-    if (done) return;
+    if (!once_per_device((const void*)&configure_pool_once)) return;
     int dev = 0;
     cudaMemPool_t pool;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -206,7 +253,6 @@ void configure_pool_once() {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
-    done = true;
 }
 
 struct DevBuf {
@@ -404,10 +450,22 @@ struct sbmds_ctx {
     // int8 symmetric-half stream (k_dstream_sym8.cuh): D as three digit planes per upper tile
     DevBuf Dt8, Y8T;
     bool dt8_ok = false;
-    bool dmax8_ok = false;
+    bool dmax8_ok = false;            // aux[2] = max |D| over the block upper triangle (formed in create, overlapping D's upload)
     cudaStream_t pack_st = nullptr;   // create's D pack (host D): runs past create's return
     cudaEvent_t pack_ev = nullptr;
-    bool pack_pending = false;        // the first D-stream launch waits for pack_ev   // aux[2] = max |D| over the block upper triangle (formed in create, overlapping D's upload)
+    bool pack_pending = false;        // D-stream launches wait for pack_ev until it has completed
+    // int8 stream precision check (dq_decide): binades between max |D| and the median |D| over
+    // the block upper triangle; auto (dstream 0) keeps the int8 stream only when <= dq_max_range
+    DevBuf dqhist;                    // 256 per-binade counters (k_absmax_upper)
+    bool dq_hist_ok = false;
+    int dq_state = 0;                 // 0 undecided, 1 int8 stream kept, -1 fell back to the fp32-grade stream
+    int dq_range = -1;
+    int dq_max_range = 6;
+    // sparse-step precision check (ensure_sp8): binades between a 128-row block's max |S| and its
+    // smallest nonzero row maximum; above sp8_max_range the fp32 sparse kernels are used
+    int sp8_range = -1;
+    int sp8_max_range = 7;
+    int chol_retries = 0;             // last eigs: Cholesky-QR factorisations that needed the shifted retry
     struct PairPlan {
         bool ok = false;
         int S = 0, NT = 0, P = 0, nslots = 0;
@@ -505,11 +563,7 @@ void run_dstream(sbmds_ctx* h, int b, cudaStream_t st) {
     sk.grid = (int)std::min<int64_t>(h->num_sms, sk.T);
     const int maxseg = (int)((sk.grid + sk.RT - 1) / sk.RT) + 2;
     h->P.ensure((size_t)sk.RT * maxseg * C::TM * BP * sizeof(double));
-    static bool attr_set[7] = {false};
-    if (!attr_set[bp_index(BP)]) {
-        CK(cudaFuncSetAttribute(k_dstream_ffma<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM + 1024));
-        attr_set[bp_index(BP)] = true;
-    }
+    smem_attr(k_dstream_ffma<BP>, C::SMEM + 1024);
     profiled(h->prof, PK_DSTREAM, st, [&] {
         launch(k_dstream_ffma<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM + 1024, st,
                h->dmap[bp_index(BP)], h->l, (const float*)h->Y1.as<float>(), sk, maxseg, h->P.as<double>());
@@ -572,11 +626,7 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
     sk.grid = (int)std::min<int64_t>(h->num_sms, sk.T);
     const int maxseg = (int)((sk.grid + sk.RT - 1) / sk.RT) + 2;
     h->P.ensure((size_t)sk.RT * maxseg * C::TM * BP * sizeof(double));
-    static bool attr_set[7] = {false};
-    if (!attr_set[i]) {
-        CK(cudaFuncSetAttribute(k_dstream_tc<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_set[i] = true;
-    }
+    smem_attr(k_dstream_tc<BP>, C::SMEM);
     profiled(h->prof, PK_DSTREAM, st, [&] {
         launch(k_dstream_tc<BP>, dim3(sk.grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->amap, h->bmap[i], sk, maxseg,
                h->P.as<double>());
@@ -815,10 +865,9 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     using C = PairCfg<BP>;
     const int pi = BP == 8 ? 0 : (BP == 16 ? 1 : 2);
     auto& pl = h->pplan[pi];
-    static bool attr_set[3] = {false, false, false};
-    static int max_clusters[3] = {0, 0, 0};
-    if (!attr_set[pi]) {
-        CK(cudaFuncSetAttribute(k_dstream_pair<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    static int max_clusters[3] = {0, 0, 0};   // (occupancy: the same on every device of one arch)
+    smem_attr(k_dstream_pair<BP>, C::SMEM);
+    if (!max_clusters[pi]) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * (h->num_sms / 2));
         cfg.blockDim = dim3(C::THREADS);
@@ -833,7 +882,6 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         int nc = 0;
         CK(cudaOccupancyMaxActiveClusters(&nc, k_dstream_pair<BP>, &cfg));
         max_clusters[pi] = std::max(1, std::min(nc, h->num_sms / 2));
-        attr_set[pi] = true;
     }
     const int64_t lpad = y1t_lpad(h);
     if (!pl.ok) build_pair_plan(h, pl, max_clusters[pi], C::S);
@@ -848,7 +896,7 @@ void run_dstream_pair(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         h->Dt.ensure((size_t)pl.ntiles * 128 * 128 * 2 * sizeof(__half));
         CK(cudaMemsetAsync(dmax, 0, sizeof(unsigned int), st));
         launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256),
-               0, st, (const float*)h->D, h->l, h->ldD, dmax, (int64_t)0, (int64_t)-1);
+               0, st, (const float*)h->D, h->l, h->ldD, dmax, (int64_t)0, (int64_t)-1, (unsigned int*)nullptr);
         launch(k_pack_upper, dim3((unsigned)std::min<int64_t>(pl.ntiles, 16 * (int64_t)h->num_sms)), dim3(256), 0, st,
                (const float*)h->D, h->ldD, h->l, (const uint32_t*)pl.tiles.p, (int64_t)pl.NT, pl.ntiles,
                (const unsigned int*)dmax, dexp, h->Dt.as<__half>());
@@ -909,15 +957,13 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     using C = Sym8Cfg<BP>;
     const int pi = BP == 8 ? 0 : (BP == 16 ? 1 : 2);
     auto& pl = h->s8plan[pi];
-    static bool attr_set[3] = {false, false, false};
-    if (!attr_set[pi]) {
-        CK(cudaFuncSetAttribute(k_dstream_sym8<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_set[pi] = true;
-    }
+    smem_attr(k_dstream_sym8<BP>, C::SMEM);
     const int64_t lpad = y1t_lpad(h);
-    if (h->pack_pending) {   // create's D pack, still running on its own stream
+    if (h->pack_pending) {   // create's D pack, possibly still running on its own stream
         CK(cudaStreamWaitEvent(st, h->pack_ev, 0));
-        h->pack_pending = false;
+        const cudaError_t q = cudaEventQuery(h->pack_ev);   // only a completed pack ends the waits
+        if (q == cudaSuccess) h->pack_pending = false;
+        else if (q != cudaErrorNotReady) throw CudaError{q, "D pack (issued by sbmds_create)"};
     }
     static const bool trace = getenv("SBMDS_TRACE_EIGS") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
@@ -940,7 +986,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         if (!h->dmax8_ok) {
             CK(cudaMemsetAsync(dmax8, 0, sizeof(unsigned int), st));
             launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256), 0, st,
-                   (const float*)h->D, h->l, h->ldD, dmax8, (int64_t)0, (int64_t)-1);
+                   (const float*)h->D, h->l, h->ldD, dmax8, (int64_t)0, (int64_t)-1, (unsigned int*)nullptr);
             h->dmax8_ok = true;
         }
         dphase("absmax");
@@ -1003,11 +1049,70 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
 bool uses_tc(const sbmds_ctx* h, int bp) { return bp >= 8 && (h->dstream == 2 || h->dstream == 0 || h->dstream == 3); }
 // symmetric-half stream: forced by dstream = 3, chosen by auto (0) once D has >= 8 tiles per
 // CTA pair (below that D is L2-resident and the full stream on all SMs wins)
+bool sym_size_ok(const sbmds_ctx* h) {
+    const int64_t nt = (h->l + 127) / 128;
+    return nt * (nt + 1) / 2 >= 8 * (int64_t)(h->num_sms / 2);
+}
 bool uses_sym(const sbmds_ctx* h, int bp) {
     if (!(bp == 8 || bp == 16 || bp == 32)) return false;
     if (h->dstream == 3 || h->dstream == 4) return true;
-    const int64_t nt = (h->l + 127) / 128;
-    return h->dstream == 0 && nt * (nt + 1) / 2 >= 8 * (int64_t)(h->num_sms / 2);
+    return h->dstream == 0 && sym_size_ok(h) && h->dq_state >= 0;   // (auto: also the precision check)
+}
+
+// Precision check of the int8 stream's fixed point (DESIGN.md §4 "precision contract"). The
+// stream stores D as integers on one global quantum q = 2^-sD, max|D| 2^-22 < q <= max|D| 2^-21,
+// so an entry |D_ij| keeps a relative precision of q / (2|D_ij|). The check takes the median
+// |D| over the block upper triangle from the per-binade histogram (k_absmax_upper) and keeps
+// the int8 stream only while the median entry lies within dq_max_range binades (default 6) of
+// max |D|: the median entry then keeps >= 15 significant bits (relative rounding <= 2^-16 of
+// it, mean zero). Squared geodesics sit 1-3 binades below their max (configs 1-4: 2), uniform
+// config-5 D 1. A D with a few far outliers or clusters far apart (max / median >= 2^7) would
+// leave most entries with few bits; auto then streams the full D on the fp32-grade 3xTF32
+// kernel instead. Reads the histogram and max back (stream sync).
+void dq_decide(sbmds_ctx* h, cudaStream_t st) {
+    unsigned int hist[256], mbits = 0;
+    peek_to_host(hist, h->dqhist.p, sizeof hist, st);
+    peek_to_host(&mbits, h->y16aux.as<unsigned int>() + 2, sizeof mbits, st);
+    uint64_t total = 0;
+    for (int e = 0; e < 256; ++e) total += hist[e];
+    int range = 0;
+    if (total > 0 && mbits != 0) {
+        uint64_t acc = 0;
+        int emed = 0;
+        for (int e = 0; e < 256; ++e) {
+            acc += hist[e];
+            if (2 * acc >= total) { emed = e; break; }
+        }
+        range = (int)(mbits >> 23) - emed;   // (a zero / subnormal median: emed = 0, a huge range)
+    }
+    h->dq_range = range;
+    h->dq_state = range <= h->dq_max_range ? 1 : -1;
+}
+
+// Decide the precision check before the first apply / eigs of an auto handle that would take
+// the int8 stream (create already did it for a host D large enough for that stream).
+void ensure_dq(sbmds_ctx* h, cudaStream_t st) {
+    if (h->dq_state != 0 || h->dstream != 0 || !sym_size_ok(h)) return;
+    h->y16aux.ensure(352 * sizeof(unsigned int));
+    if (!h->dq_hist_ok) {
+        h->dqhist.ensure(256 * sizeof(unsigned int));
+        unsigned int* aux = h->y16aux.as<unsigned int>();
+        // max |D| into aux[2] unless create (or a pack) already formed it; else a scratch word
+        unsigned int* mx = h->dmax8_ok ? aux + 4 : aux + 2;
+        CK(cudaMemsetAsync(mx, 0, sizeof(unsigned int), st));
+        CK(cudaMemsetAsync(h->dqhist.p, 0, 256 * sizeof(unsigned int), st));
+        launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, h->l)), dim3(256), 0, st,
+               (const float*)h->D, h->l, h->ldD, mx, (int64_t)0, (int64_t)-1, h->dqhist.as<unsigned int>());
+        h->dmax8_ok = true;
+        h->dq_hist_ok = true;
+    }
+    dq_decide(h, st);
+    if (h->dq_state < 0 && h->dt8_ok) {   // (cannot happen after create's check; kept for safety)
+        if (h->pack_st) CK(cudaStreamSynchronize(h->pack_st));
+        h->pack_pending = false;
+        h->Dt8.release();
+        h->dt8_ok = false;
+    }
 }
 
 // Mirror the lower triangle of D on the device before the first full-D kernel (see create).
@@ -1173,12 +1278,8 @@ bool sp8_ok(sbmds_ctx* h, int b, cudaStream_t st) {
 
 void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st, bool with_chol) {
     using C = Sp8Cfg<16>;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(k_sp8_step<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        CK(cudaFuncSetAttribute(k_sp8_step<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr = true;
-    }
+    smem_attr(k_sp8_step<16, false>, C::SMEM);
+    smem_attr(k_sp8_step<16, true>, C::SMEM);
     h->y16aux.ensure(352 * sizeof(unsigned int));
     unsigned int* y2mm = h->y16aux.as<unsigned int>() + 192;   // Y2 column max [0, 64) / min [64, 128) keys
     int* ey2 = reinterpret_cast<int*>(h->y16aux.as<unsigned int>() + 320);
@@ -1230,8 +1331,8 @@ void launch_fused(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p
     static size_t occ_smem[2][5] = {};
     const int li = LPR == 1 ? 0 : (LPR == 2 ? 1 : (LPR == 4 ? 2 : 3));
     auto kern = with_h ? k_blk_spmm_fused<LPR, true> : k_blk_spmm_fused<LPR, false>;
+    if (smem > 48 * 1024) smem_attr(kern, (int)smem);   // (per device)
     if (occ_smem[with_h][li] != smem) {
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[with_h][li], kern, 256, smem));
         occ_smem[with_h][li] = smem;
     }
@@ -1261,14 +1362,11 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     });
     const bool blk = blocked_ok(h, b, bp, X, Y);
     if (blk) {
-        static bool attr = false;   // opt the blocked kernels into > 48 KB of dynamic smem once
-        if (!attr) {
-            for (auto k : {k_blk_spmmt<1>, k_blk_spmmt<2>, k_blk_spmmt<4>, k_blk_spmmt<8>, k_blk_spmmt<16>})
-                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kRB * kMaxB * 4));
-            for (auto k : {k_blk_spmm<1>, k_blk_spmm<2>, k_blk_spmm<4>, k_blk_spmm<8>, k_blk_spmm<16>})
-                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBlkSmem));
-            attr = true;
-        }
+        // opt the blocked kernels into > 48 KB of dynamic smem (once per device)
+        for (auto k : {k_blk_spmmt<1>, k_blk_spmmt<2>, k_blk_spmmt<4>, k_blk_spmmt<8>, k_blk_spmmt<16>})
+            smem_attr(k, kRB * kMaxB * 4);
+        for (auto k : {k_blk_spmm<1>, k_blk_spmm<2>, k_blk_spmm<4>, k_blk_spmm<8>, k_blk_spmm<16>})
+            smem_attr(k, (int)kBlkSmem);
     }
     // A2: Y1 = S^T X - w s^T   (CSC SpMM by default; row-blocked partials + landmark
     // reduction when enabled: both are bound by the 64-B-per-nonzero gather traffic; inside
@@ -1533,10 +1631,25 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     h->s8img.ensure((size_t)total + 64 * 1024);   // + slack: the T product's M = 128 rows read past a short image
     CK(cudaMemsetAsync(h->s8img.p, 0, h->s8img.bytes, st));
     h->s8esc.ensure(o.nblk * sizeof(int));
+    bad.ensure(sizeof(unsigned int));
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(unsigned int), st));
     launch(k_sp8_build, dim3((unsigned)std::min<int64_t>(o.nblk, 32 * (int64_t)h->num_sms)), dim3(128), 0, st, h->n,
            o.nblk, (const int32_t*)h->rp.as<int32_t>(), (const float*)h->val.as<float>(),
            (const uint16_t*)o.lcol.as<uint16_t>(), (const int32_t*)o.doff.as<int32_t>(),
-           (const int64_t*)h->s8ioff.as<int64_t>(), h->s8img.as<int8_t>(), h->s8esc.as<int>());
+           (const int64_t*)h->s8ioff.as<int64_t>(), h->s8img.as<int8_t>(), h->s8esc.as<int>(), bad.as<unsigned int>());
+    unsigned int rrange = 0;
+    peek_to_host(&rrange, bad.p, sizeof rrange, st);
+    h->sp8_range = (int)rrange;
+    if (h->sp8_range > h->sp8_max_range) {
+        // precision check failed (a row's weights sit > sp8_max_range binades below its block's
+        // max): the eigs step keeps the fp32 sparse kernels (DESIGN.md §4 precision contract)
+        o.reset();
+        h->s8img.release();
+        h->s8ioff.release();
+        h->s8esc.release();
+        h->sp8_state = -2;
+        return false;
+    }
     o.lcol.release();   // only the images are read from now on
     h->s8pos.ensure(std::max<int32_t>(1, o.total_u) * sizeof(int32_t));
     launch(k_inverse_perm, dim3(1024), dim3(256), 0, st, o.total_u, (const int32_t*)o.jlist.as<int32_t>(),
@@ -1557,7 +1670,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->foldscr, &h->s8trace,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
@@ -1603,11 +1716,13 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     static const bool trace_create = getenv("SBMDS_TRACE_CREATE") != nullptr;
     const auto t_create0 = std::chrono::steady_clock::now();
     auto tphase = [&](const char* what) {
+        nvtxMarkA(what);   // stage boundary on the NVTX timeline
         if (!trace_create) return;
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create0).count();
         fprintf(stderr, "[sbmds_create] %8.2f ms  %s\n", ms, what);
     };
 
+    Nvtx nv_create("sbmds_create");
     if (!out) return fail(SBMDS_EINVAL, "out is NULL");
     *out = nullptr;
     if (n < 1 || l < 1 || l > n) return fail(SBMDS_EINVAL, "need 1 <= l <= n (n=%lld, l=%lld)", (long long)n, (long long)l);
@@ -1698,6 +1813,8 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
                     h->y16aux.ensure(352 * sizeof(unsigned int));
                     dmax8 = h->y16aux.as<unsigned int>() + 2;
                     CK(cudaMemsetAsync(dmax8, 0, sizeof(unsigned int), st));
+                    h->dqhist.ensure(256 * sizeof(unsigned int));
+                    CK(cudaMemsetAsync(h->dqhist.p, 0, 256 * sizeof(unsigned int), st));
                     CK(cudaStreamCreateWithFlags(&dabs, cudaStreamNonBlocking));
                     CK(cudaEventRecord(dside_done, st));
                     CK(cudaStreamWaitEvent(dabs, dside_done, 0));
@@ -1717,7 +1834,8 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
                         CK(cudaEventRecord(ev, dside));
                         CK(cudaStreamWaitEvent(dabs, ev, 0));
                         launch(k_absmax_upper, dim3((unsigned)std::min<int64_t>(4 * (int64_t)h->num_sms, g1 - g0)),
-                               dim3(256), 0, dabs, (const float*)h->Dbuf.as<float>(), l, h->ldD, dmax8, g0, g1);
+                               dim3(256), 0, dabs, (const float*)h->Dbuf.as<float>(), l, h->ldD, dmax8, g0, g1,
+                               h->dqhist.as<unsigned int>());
                     }
                 }
                 if (pre8) {
@@ -1727,6 +1845,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
                     CK(cudaEventRecord(ev, dabs));
                     CK(cudaStreamWaitEvent(dside, ev, 0));   // dside_done below covers the maxima too
                     h->dmax8_ok = true;
+                    h->dq_hist_ok = true;
                 }
                 h->d_lower_missing = true;
             } else {
@@ -1882,6 +2001,10 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         join_dside();
         tphase("D upload joined");
         if (pre_plan) {
+            dq_decide(h, st);   // the int8 stream's precision check (max |D| vs the median)
+            if (h->dq_state < 0) h->Dt8.release();
+        }
+        if (pre_plan && h->dq_state > 0) {
             // D and max |D| have landed: upload the schedule and pack D (int8 digits of the
             // upper tiles) on a handle stream that runs on past create's return; the first
             // D-stream launch waits for it
@@ -1928,6 +2051,7 @@ static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 }
 
 extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float* Y, void* cuda_stream) {
+    Nvtx nv_apply("sbmds_apply");
     if (!h) return fail(SBMDS_EINVAL, "NULL handle");
     if (b < 1 || b > kMaxB) return fail(SBMDS_EINVAL, "need 1 <= b <= 64 (b=%d)", b);
     if (!X || !Y) return fail(SBMDS_EINVAL, "NULL X or Y");
@@ -1948,6 +2072,7 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
             h->yhost.ensure(bytes);
             Yd = h->yhost.as<float>();
         }
+        ensure_dq(h, st);   // the int8 stream's precision check (once per handle)
         if (h->center) {
             apply_device(h, b, Xd, Yd, st);
         } else {
@@ -1986,23 +2111,15 @@ namespace {
 void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, bool want_s = false) {
     h->gpart.ensure((size_t)kRedBlocks * kGramPart * sizeof(double));
     double* cs = want_s ? h->s.as<double>() : nullptr;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(k_gram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-        CK(cudaFuncSetAttribute(k_gram<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-        attr = true;
-    }
+    smem_attr(k_gram<true>, 80 * 1024);
+    smem_attr(k_gram<false>, 80 * 1024);
     const size_t smem = gram_smem_bytes(b);
     double* Hd = h->H.as<double>();
     double* Gd = h->G.as<double>();
     double* P = h->gpart.as<double>();
     unsigned int* cnt = h->counters.as<unsigned int>() + CNT_GRAM;
-    static bool tc_attr = false;
-    if (!tc_attr) {
-        CK(cudaFuncSetAttribute(k_gram_tc<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tc_smem<4>()));
-        CK(cudaFuncSetAttribute(k_gram_tc<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_tc_smem<4>()));
-        tc_attr = true;
-    }
+    smem_attr(k_gram_tc<4, true>, (int)gram_tc_smem<4>());
+    smem_attr(k_gram_tc<4, false>, (int)gram_tc_smem<4>());
     const size_t smem_tc = b <= 8 ? gram_tc_smem<1>() : (b <= 16 ? gram_tc_smem<2>() : gram_tc_smem<4>());
     auto tc = [&](auto kern) {
         launch(kern, dim3(kRedBlocks), dim3(256), smem_tc, st, h->n, b, Y, X, P, Gd, Hd, cs, cnt);
@@ -2116,11 +2233,7 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
     cholqr(W, tmp, h->lzR.as<double>());
     cholqr(tmp, Qj(0), h->lzR.as<double>());
     check_breakdown("Cholesky-QR of the initial block broke down");
-    static bool rr_attr = false;
-    if (!rr_attr) {
-        CK(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, kRrSmem));
-        rr_attr = true;
-    }
+    smem_attr(k_rr, kRrSmem);
     int applies = 0;
     bool converged = false;
     for (;;) {
@@ -2215,12 +2328,14 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
     static const bool trace_eigs = getenv("SBMDS_TRACE_EIGS") != nullptr;
     const auto t_eigs0 = std::chrono::steady_clock::now();
     auto ephase = [&](const char* what, cudaStream_t sst) {
+        nvtxMarkA(what);   // stage boundary on the NVTX timeline
         if (!trace_eigs) return;
         cudaStreamSynchronize(sst);
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_eigs0).count();
         fprintf(stderr, "[sbmds_eigs] %8.2f ms  %s\n", ms, what);
     };
 
+    Nvtx nv_eigs("sbmds_eigs");
     if (!h) return fail(SBMDS_EINVAL, "NULL handle");
     if (block < 1 || block > kMaxB || block >= h->n) return fail(SBMDS_EINVAL, "need 1 <= block <= 64, block < n");
     if (m < 1 || m > block) return fail(SBMDS_EINVAL, "need 1 <= m <= block");
@@ -2232,6 +2347,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
     const int64_t n = h->n;
     sbmds_status ret = SBMDS_OK;
     try {
+        ensure_dq(h, st);   // the int8 stream's precision check (once per handle)
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
@@ -2284,13 +2400,10 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR of the initial block broke down");
+        h->chol_retries = hstat == 1 ? 1 : 0;
         ephase("initial block", st);
 
-        static bool rr_attr = false;
-        if (!rr_attr) {
-            CK(cudaFuncSetAttribute(k_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, kRrSmem));
-            rr_attr = true;
-        }
+        smem_attr(k_rr, kRrSmem);
         RrOut rr_host;
         int it = 0;
         bool converged = false;
@@ -2418,6 +2531,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                 CK(cudaMemcpyAsync(&hstat, h->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
                 if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR broke down at iteration %d", it);
+                if (hstat == 1) ++h->chol_retries;
             }
             ++it;
         }
@@ -2513,6 +2627,21 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         if (value < 0 || value > 4)
             return fail(SBMDS_EINVAL, "dstream in {0 auto, 1 ffma, 2 tcgen05, 3 symmetric int8, 4 symmetric 2xfp16 pairs}");
         h->dstream = (int)value;
+        if ((value == 1 || value == 2 || value == 4) && h->dt8_ok) {
+            // off the int8 stream: release its packed D (3 l^2 / 2 bytes); re-packed on return
+            DevGuard g(h->dev);
+            if (h->pack_st) cudaStreamSynchronize(h->pack_st);
+            h->pack_pending = false;
+            h->Dt8.release();
+            h->dt8_ok = false;
+        }
+    } else if (!strcmp(key, "dq_max_range")) {
+        if (value < 0 || value > 255) return fail(SBMDS_EINVAL, "dq_max_range in [0, 255] binades");
+        h->dq_max_range = (int)value;
+        if (h->dq_state != 0) h->dq_state = 0;   // re-decided at the next apply / eigs
+    } else if (!strcmp(key, "sp8_max_range")) {
+        if (value < 0 || value > 255) return fail(SBMDS_EINVAL, "sp8_max_range in [0, 255] binades");
+        h->sp8_max_range = (int)value;   // (read when the sparse-step images are built)
     } else if (!strcmp(key, "center")) {
         h->center = value ? 1 : 0;
     } else if (!strcmp(key, "csr_sub_L")) {
@@ -2557,7 +2686,11 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
         *value = (int64_t)std::llround(h->pdbg_avg[key[9] == 'T'][site]);
     }
     else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
-    else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a
+    else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a, -2 precision check
+    else if (!strcmp(key, "sp8_range")) *value = h->sp8_range;          // its binade range (-1 not built)
+    else if (!strcmp(key, "chol_retries")) *value = h->chol_retries;  // last eigs: shifted Cholesky retries seen
+    else if (!strcmp(key, "dq_state")) *value = h->dq_state;            // int8 D stream check: 1 kept, -1 fell back, 0 undecided
+    else if (!strcmp(key, "dq_range")) *value = h->dq_range;            // binades between max |D| and the median |D|
     else if (!strcmp(key, "sp8_bytes")) *value = h->s8_bytes;           // its S images (HBM bytes per pass)
     else if (!strcmp(key, "sp8_umax")) *value = h->sp8_state > 0 ? (int64_t)h->s8.umax : -1;
     else if (!strcmp(key, "dstream_slots")) *value = h->s8plan[1].nslots;   // int8 D stream partial slots (b = 16)
