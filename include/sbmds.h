@@ -167,7 +167,17 @@ const char* sbmds_last_error(void);
  *     "profile"        bit mask of kernel families timed with CUDA events on the launching
  *                      stream (bit k = family k of: colsum csc dstream dreduce csr gram chol
  *                      rotate rr split); "profile_reset" (any value) zeroes the counters
- *     "pair_dbg"       diagnostics of k_dstream_pair: bit 0 per-role wait-cycle counters
+ *     "dq_max_range"   (binades, default 6) precision check of the int8 D stream: auto keeps it only
+                      while the median |D| over the upper tiles lies within this many binades of
+                      max |D| (stat "dq_range"); otherwise the full D on 3xTF32 (stat "dq_state" -1)
+     "dy_max_range"   (binades, default 3) standalone apply on the int8 stream: a Y1 column whose
+                      max |y| exceeds 2^range times its rms sends that apply to the fp32-grade
+                      stream (stat "y_fallbacks")
+     "sp8_max_range"  (binades, default 7) tensor-core sparse step: a 128-row block whose smallest
+                      nonzero row maximum sits more than this many binades below the block's max
+                      keeps the eigs step on the fp32 sparse kernels (stat "sp8_state" -2,
+                      "sp8_range"); read when the images are built
+     "pair_dbg"       diagnostics of k_dstream_pair: bit 0 per-role wait-cycle counters
  *                      (stats "pair_dbg_N_<site>", "pair_dbg_T_<site>"), higher bits disable
  *                      parts of the kernel for experiments (results then invalid)
  *   sbmds_get_stat keys: "n", "l", "nnz", "rowsum_dev_e9" (max |row sum - 1| * 1e9),
@@ -196,7 +206,55 @@ int64_t sbmds_launch_count(void);
    CPU tests; see k_dstream_sym8.cuh / k_dstream_pair.cuh and DESIGN.md §4. */
 int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous);
 
-/* ABI version: 1. */
+/*
+ * Sharded apply. The matvec of PAPER.md:221-222 splits by rows of P (= S)
+ * and by tiles of W (= D_ll): rank g of `world` holds rows [row0, row0 + n_local) of S and
+ * streams the contiguous range g of D's upper 128 x 128 tiles in walk order (sbmds_shard_tiles).
+ * Every exchanged quantity is linear, so the apply is four stages with a SUM over ranks after
+ * each of the first three:
+ *   stage 0  in: X_g (n_local x b)          out: s_g = 1^T X_g              (double[b])
+ *   stage 1  in: X_g, s (summed, double[b])  out: Y1_g = S_g^T X_g - w_g s^T (float[l*b]),
+ *            w_g = S_g^T 1 / n_global (the w_g sum to w = S^T 1 / n)
+ *   stage 2  in: Y1 (summed, float[l*b])     out: Y2_g (float[l*b]) and, at byte offset
+ *            8*ceil(4lb/8), t_g = w^T Y2_g (double[b]): this rank's tiles' D_IJ Y1_J and
+ *            D_IJ^T Y1_I terms (full-D kernels -- b < 5, or the precision fallback -- run
+ *            on rank 0 only; the other ranks return zeros)
+ *   stage 3  in: Y2 | t (summed, stage 2's layout)   out: Y_g = -1/2 (S_g Y2 - 1 t^T) (n_local x b)
+ * Layouts are compact row-major (float[l*b]: row j of Y1 at j*b). sbmds_shard_exchange_bytes
+ * gives each stage's exchange size (stage 1: its output; 2, 3: the Y2 | t buffer).
+ *
+ * sbmds_create_shard — as sbmds_create for the local rows (row_ptr is local: row_ptr[0] = 0,
+ *   row_ptr[n_local] = nnz); D_ll is the full l x l matrix on every rank. 1 <= l <= n_global,
+ *   0 <= row0, row0 + n_local <= n_global, 0 <= rank < world. sbmds_eigs rejects shard handles
+ *   (SBMDS_EINVAL: a sharded eigensolver is not built); sbmds_apply on a shard handle needs an
+ *   attached communicator when world > 1 (SBMDS_EINVAL otherwise).
+ * sbmds_shard_stage — one stage on DEVICE buffers, stream-ordered (a standalone stage 2 on the
+ *   int8 stream reads a small Y1 check back). X for stages 0-1, exch_in for 1-3, exch_out for
+ *   0-2, Y for 3; the others may be NULL.
+ * sbmds_nccl_unique_id / sbmds_shard_attach_nccl — NCCL (dlopen'ed "libnccl.so.2" on first use):
+ *   rank 0 creates the 128-byte id, the caller broadcasts it, and every rank attaches
+ *   (collective: ncclCommInitRank(world, id, rank) blocks until all ranks have joined). After
+ *   that sbmds_apply runs all four stages with ncclAllReduce(sum) on the call's stream. The
+ *   handle owns the communicator (freed by sbmds_destroy). SBMDS_ECUDA when NCCL is missing.
+ * sbmds_shard_plan_selfcheck / sbmds_shard_tiles (host only, no GPU): rank's schedule checked as
+ *   sbmds_plan_selfcheck does; rank's tiles (I << 16 | J) into tiles_out[capacity] (may be NULL),
+ *   returning their count (< 0: bad arguments).
+ */
+sbmds_status sbmds_create_shard(int64_t n_global, int64_t row0, int64_t n_local, int64_t l, int64_t nnz,
+                                const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                const float* D_ll, int32_t rank, int32_t world, uint32_t flags,
+                                void* cuda_stream, sbmds_t* out);
+sbmds_status sbmds_shard_stage(sbmds_t h, int32_t stage, int32_t b, const float* X, const void* exch_in,
+                               void* exch_out, float* Y, void* cuda_stream);
+int64_t sbmds_shard_exchange_bytes(int64_t l, int32_t b, int32_t stage);
+sbmds_status sbmds_nccl_unique_id(void* id_out /* 128 bytes */);
+sbmds_status sbmds_shard_attach_nccl(sbmds_t h, const void* unique_id /* 128 bytes */);
+int64_t sbmds_shard_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous,
+                                   int32_t rank, int32_t world);
+int64_t sbmds_shard_tiles(int64_t l, int32_t S, int32_t rank, int32_t world, uint32_t* tiles_out,
+                          int64_t capacity);
+
+/* ABI version: 2 (1 + the sharded apply). */
 int32_t sbmds_abi_version(void);
 
 #ifdef __cplusplus

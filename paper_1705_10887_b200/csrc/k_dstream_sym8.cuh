@@ -369,6 +369,36 @@ __global__ void __launch_bounds__(256) k_pack_sym8(const float* __restrict__ D, 
     }
 }
 
+// Per-column max |y| and sum of y^2 of Y1 (l x bp, columns < b): the standalone apply's check
+// that the per-column fixed point of the int8 stream keeps the bulk of each column (sbmds.cu
+// apply_device; DESIGN.md §4 precision contract). out: [0, 64) max bits, then 64 doubles.
+__global__ void __launch_bounds__(256) k_ycheck(int64_t l, int b, int bp, const float* __restrict__ Y1,
+                                                unsigned int* __restrict__ out) {
+    __shared__ float smx[256];
+    __shared__ double sss[256];
+    const int rb = 256 / bp;
+    const int r = threadIdx.x / bp, c = threadIdx.x % bp;
+    float m = 0.f;
+    double ss = 0.0;
+    if (r < rb && c < b)
+        for (int64_t k = (int64_t)blockIdx.x * rb + r; k < l; k += (int64_t)gridDim.x * rb) {
+            const float v = Y1[k * bp + c];
+            m = fmaxf(m, fabsf(v));
+            ss += (double)v * v;
+        }
+    smx[threadIdx.x] = m;
+    sss[threadIdx.x] = ss;
+    __syncthreads();
+    if (r == 0 && c < b) {
+        for (int q = 1; q < rb; ++q) {
+            m = fmaxf(m, smx[q * bp + c]);
+            ss += sss[q * bp + c];
+        }
+        atomicMax(out + c, __float_as_uint(m));
+        atomicAdd(reinterpret_cast<double*>(out + 64) + c, ss);
+    }
+}
+
 // folded Y1 (Y1f, l_pad x bp) -> Y8T (3bp x l_pad int8): rows [y0; y1; y2], the balanced digits
 // of rint(y 2^e_c), e_c = i8_scale_exp(max |column c|)
 __global__ void __launch_bounds__(256) k_y8_split(int64_t lpad, int bp, const float* __restrict__ Y1f,

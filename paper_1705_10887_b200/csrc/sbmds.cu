@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
+#include <nccl.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -204,6 +206,56 @@ void peek_to_host(void* host_dst, const void* dev_src, size_t bytes, cudaStream_
     memcpy(host_dst, hbuf, bytes);
 }
 
+// NCCL for the sharded apply, loaded on first use (dlopen "libnccl.so.2": the copy torch already
+// loaded when there is one, so ids from either side match); the single-GPU library does not
+// depend on it.
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!so) {
+            api.why = dlerror() ? dlerror() : "dlopen(libnccl.so.2) failed";
+            return;
+        }
+        auto sym = [&](const char* name) { return dlsym(so, name); };
+        api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
+        api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
+        api.allReduce = reinterpret_cast<decltype(api.allReduce)>(sym("ncclAllReduce"));
+        api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
+        api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
+        api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
+        api.errorString = reinterpret_cast<decltype(api.errorString)>(sym("ncclGetErrorString"));
+        api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.groupStart && api.groupEnd &&
+                 api.commDestroy && api.errorString;
+        if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+    });
+    return api;
+}
+
+struct NcclError {
+    ncclResult_t r;
+    const char* what;
+};
+#define NK(call)                                             \
+    do {                                                     \
+        ncclResult_t _r = (call);                            \
+        if (_r != ncclSuccess) throw NcclError{_r, #call};   \
+    } while (0)
+
 std::string hang_note() {
     if (!g_hang_host || !g_hang_host->flag) return "";
     std::string out = " [pipeline watchdog:";
@@ -398,6 +450,13 @@ enum { CNT_COLSUM = 0, CNT_DRED = 1, CNT_GRAM = 2, CNT_ARGMAX = 3, CNT_ROTATE = 
 // ============================================================================ handle
 struct sbmds_ctx {
     int64_t n = 0, l = 0, nnz = 0;
+    // sharded apply: this handle holds rows [row0, row0 + n) of an n_global-row S
+    // and streams tile range `rank` of `world` of D's upper triangle; comm = NCCL communicator
+    // attached by sbmds_shard_attach_nccl (NULL: the caller drives sbmds_shard_stage)
+    int64_t n_global = 0, row0 = 0;
+    int rank = 0, world = 1;
+    bool shard = false;
+    void* comm = nullptr;
     int dev = 0, num_sms = 148;
     // S (CSR) and its device-built CSC copy
     DevBuf rp, col, val, cptr, ridx, cval, order, w;
@@ -465,7 +524,14 @@ struct sbmds_ctx {
     // smallest nonzero row maximum; above sp8_max_range the fp32 sparse kernels are used
     int sp8_range = -1;
     int sp8_max_range = 7;
-    int chol_retries = 0;             // last eigs: Cholesky-QR factorisations that needed the shifted retry
+    int chol_retries = 0;
+    // standalone apply: per-column check of Y1 before the int8 stream (its per-column quantum is
+    // max |y_c| 2^-23): when max |y_c| > 2^dy_max_range rms(y_c) for some column, this apply
+    // streams D on the fp32-grade kernel instead (y_fallback), counted in y_fallbacks
+    int dy_max_range = 3;
+    bool y_fallback = false;
+    int64_t y_fallbacks = 0;
+    DevBuf ychk;             // last eigs: Cholesky-QR factorisations that needed the shifted retry
     struct PairPlan {
         bool ok = false;
         int S = 0, NT = 0, P = 0, nslots = 0;
@@ -661,7 +727,9 @@ struct PlanHost {
     std::vector<int> sbase, slot_x, xptr, xslot, smap;
 };
 
-PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous) {
+// The upper tiles in walk order (blocks of S x S tiles, block rows, row-major inside a block);
+// a shard (rank of world) keeps the contiguous range [T r / W, T (r + 1) / W).
+PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous, int rank = 0, int world = 1) {
     PlanHost ph;
     const int NT = (int)((l + 127) / 128);
     if (NT > 65535) throw std::runtime_error("l too large for the symmetric-half stream");
@@ -675,6 +743,12 @@ PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous) {
                     const int I = bi * S + r, J = bj * S + c;
                     if (I < NT && J < NT && J >= I) tiles.push_back(((uint32_t)I << 16) | (uint32_t)J);
                 }
+    if (world > 1) {
+        const int64_t Tall = (int64_t)tiles.size();
+        const int64_t t0 = Tall * rank / world, t1 = Tall * (rank + 1) / world;
+        tiles.erase(tiles.begin() + t1, tiles.end());
+        tiles.erase(tiles.begin(), tiles.begin() + t0);
+    }
     const int64_t T = (int64_t)tiles.size();
     const int P = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs, T / 8));
     auto& pbeg = ph.pbeg;
@@ -731,7 +805,7 @@ PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous) {
 
 void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S, int gN = 1, bool contiguous = false,
                      const PlanHost* pre = nullptr) {
-    const PlanHost ph = pre ? *pre : plan_host(h->l, max_pairs, S, gN, contiguous);
+    const PlanHost ph = pre ? *pre : plan_host(h->l, max_pairs, S, gN, contiguous, h->rank, h->world);
     const int nslots = (int)ph.slot_x.size();
     if (contiguous) {
         pl.smap.ensure(ph.smap.size() * sizeof(int));
@@ -763,18 +837,20 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
 // upper tile exactly once; every (tile, N) contribution in exactly one slot of row tile I and
 // every (tile, T), I < J, in exactly one slot of row tile J; slot -> row tile as recorded; the
 // reduction lists (or the contiguous slot map) consistent.
-extern "C" int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous) {
-    if (l < 1 || S < 1 || S > 16 || gN < 1 || max_ctas < 1) return -1;
+namespace {
+int64_t plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous, int rank, int world) {
+    if (l < 1 || S < 1 || S > 16 || gN < 1 || max_ctas < 1 || world < 1 || rank < 0 || rank >= world) return -1;
     int64_t err = 0;
     PlanHost ph;
     try {
-        ph = plan_host(l, max_ctas, S, gN, contiguous != 0);
+        ph = plan_host(l, max_ctas, S, gN, contiguous != 0, rank, world);
     } catch (...) {
         return -2;
     }
     const int NT = ph.NT;
     const int64_t T = ph.T;
-    if (T != (int64_t)NT * (NT + 1) / 2) ++err;
+    const int64_t Tall = (int64_t)NT * (NT + 1) / 2;
+    if (T != Tall * (rank + 1) / world - Tall * rank / world) ++err;
     std::vector<uint8_t> seen((size_t)NT * NT, 0);
     for (int64_t t = 0; t < T; ++t) {
         const int I = (int)(ph.tiles[t] >> 16), J = (int)(ph.tiles[t] & 0xFFFFu);
@@ -856,6 +932,30 @@ extern "C" int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_
         }
     }
     return err;
+}
+}  // namespace
+
+extern "C" int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous) {
+    return plan_selfcheck(l, S, gN, max_ctas, contiguous, 0, 1);
+}
+
+extern "C" int64_t sbmds_shard_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous,
+                                              int32_t rank, int32_t world) {
+    return plan_selfcheck(l, S, gN, max_ctas, contiguous, rank, world);
+}
+
+extern "C" int64_t sbmds_shard_tiles(int64_t l, int32_t S, int32_t rank, int32_t world, uint32_t* tiles_out,
+                                     int64_t capacity) {
+    if (l < 1 || S < 1 || S > 16 || world < 1 || rank < 0 || rank >= world) return -1;
+    PlanHost ph;
+    try {
+        ph = plan_host(l, 1, S, 1, false, rank, world);
+    } catch (...) {
+        return -2;
+    }
+    if (tiles_out)
+        for (int64_t t = 0; t < std::min<int64_t>(capacity, ph.T); ++t) tiles_out[t] = ph.tiles[t];
+    return ph.T;
 }
 
 namespace {
@@ -981,7 +1081,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
     unsigned int* ymax = aux + 64;
     int* yexp = reinterpret_cast<int*>(aux + 128);
     if (!h->dt8_ok) {
-        h->Dt8.ensure((size_t)pl.ntiles * C::A_BYTES);   // (normally allocated in create)
+        h->Dt8.ensure((size_t)((int64_t)pl.NT * (pl.NT + 1) / 2) * C::A_BYTES);   // (normally allocated in create; indexed by upper_tile_index, also on a shard)
         dphase("Dt8 allocated");
         if (!h->dmax8_ok) {
             CK(cudaMemsetAsync(dmax8, 0, sizeof(unsigned int), st));
@@ -1056,7 +1156,7 @@ bool sym_size_ok(const sbmds_ctx* h) {
 bool uses_sym(const sbmds_ctx* h, int bp) {
     if (!(bp == 8 || bp == 16 || bp == 32)) return false;
     if (h->dstream == 3 || h->dstream == 4) return true;
-    return h->dstream == 0 && sym_size_ok(h) && h->dq_state >= 0;   // (auto: also the precision check)
+    return h->dstream == 0 && sym_size_ok(h) && h->dq_state >= 0 && !h->y_fallback;   // (auto: the precision checks)
 }
 
 // Precision check of the int8 stream's fixed point (DESIGN.md §4 "precision contract"). The
@@ -1260,7 +1360,35 @@ void ensure_apply_ws(sbmds_ctx* h, int bp) {
     h->Y2.ensure((size_t)h->l * kMaxB * sizeof(float));
 }
 
-// The whole operator apply on device buffers (stream-ordered, no host sync).
+// Y1's per-column dynamic range against the int8 stream's per-column fixed point: the quantum
+// of column c is ~max |y_c| 2^-23 and the dropped digit products add ~2^-22 max|D| max|y_c| per
+// product, so a column whose max sits far above its rms (an X with a dominant row) keeps its
+// bulk with few bits. Measured: max/rms = 17 gave 2.5e-5 relative error on the apply (bar 1e-5);
+// Gaussian blocks sit at ~4. Above 2^dy_max_range this apply uses the fp32-grade stream.
+void ycheck(sbmds_ctx* h, int b, int bp, cudaStream_t st) {
+    h->ychk.ensure(64 * sizeof(unsigned int) + 64 * sizeof(double));
+    CK(cudaMemsetAsync(h->ychk.p, 0, h->ychk.bytes, st));
+    launch(k_ycheck, dim3((unsigned)std::min<int64_t>(2 * (int64_t)h->num_sms, (h->l * bp + 255) / 256)), dim3(256), 0,
+           st, h->l, b, bp, (const float*)h->Y1.as<float>(), h->ychk.as<unsigned int>());
+    unsigned char buf[64 * 4 + 64 * 8];
+    peek_to_host(buf, h->ychk.p, sizeof buf, st);
+    const unsigned int* mx = reinterpret_cast<const unsigned int*>(buf);
+    const double* ss = reinterpret_cast<const double*>(buf + 256);
+    const double lim = std::ldexp(1.0, h->dy_max_range);
+    for (int c = 0; c < b; ++c) {
+        float m;
+        memcpy(&m, &mx[c], 4);
+        const double rms = std::sqrt(ss[c] / (double)h->l);
+        if (m > 0.f && (double)m > lim * rms) {
+            h->y_fallback = true;
+            ++h->y_fallbacks;
+            return;
+        }
+    }
+}
+
+// The whole operator apply on device buffers (stream-ordered; the standalone apply on the int8
+// stream reads Y1's column check back once, see ycheck).
 // Fused-step flags (eigs only, row-blocked S, b in {4, 8, 16, 32}):
 //   kApplyY1Ready: A2 comes from the S^T partials P1 the previous fused step wrote (k_blk_reduce)
 //   kApplyFused:   A5 runs as k_blk_spmm_fused, which also writes the next P1 (unless
@@ -1447,11 +1575,14 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     } else {
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
     }
+    // standalone apply on the int8 stream (auto): check Y1's columns first (one small readback)
+    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && uses_sym(h, bp)) ycheck(h, b, bp, st);
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 64);   // (sp8_dbg & 64: separate k_y2_digits, diagnostics)
     h->y2d_ready = false;
     dstream(h, b, bp, st, Rinv);
     h->y2d_want = false;
+    h->y_fallback = false;
     // A5: Y = -1/2 (S Y2 - 1 t^T)
     if ((flags & kApplyFused) && (flags & kApplySp8)) {
         profiled(h->prof, PK_CSR, st, [&] {
@@ -1670,7 +1801,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->foldscr, &h->s8trace,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
@@ -1682,6 +1813,11 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
 
 void destroy_ctx(sbmds_ctx* h) {
     if (!h) return;
+    if (h->comm) {
+        cudaDeviceSynchronize();
+        nccl_api().commDestroy(reinterpret_cast<ncclComm_t>(h->comm));
+        h->comm = nullptr;
+    }
     if (h->pack_st) {
         cudaStreamSynchronize(h->pack_st);
         cudaStreamDestroy(h->pack_st);
@@ -1709,9 +1845,10 @@ void destroy_ctx(sbmds_ctx* h) {
 }  // namespace
 
 // ============================================================================ create
-extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const int64_t* row_ptr,
-                                     const int32_t* col_idx, const float* val, const float* D_ll, uint32_t flags,
-                                     void* cuda_stream, sbmds_t* out) {
+namespace {
+sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, int world, int64_t l, int64_t nnz,
+                         const int64_t* row_ptr, const int32_t* col_idx, const float* val, const float* D_ll,
+                         uint32_t flags, void* cuda_stream, sbmds_t* out) {
     // (diagnostics) SBMDS_TRACE_CREATE=1: host-clock phase times of this create on stderr
     static const bool trace_create = getenv("SBMDS_TRACE_CREATE") != nullptr;
     const auto t_create0 = std::chrono::steady_clock::now();
@@ -1725,7 +1862,8 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     Nvtx nv_create("sbmds_create");
     if (!out) return fail(SBMDS_EINVAL, "out is NULL");
     *out = nullptr;
-    if (n < 1 || l < 1 || l > n) return fail(SBMDS_EINVAL, "need 1 <= l <= n (n=%lld, l=%lld)", (long long)n, (long long)l);
+    if (n < 1 || l < 1 || l > n_global)
+        return fail(SBMDS_EINVAL, "need 1 <= l <= n (n=%lld, l=%lld)", (long long)n_global, (long long)l);
     if (nnz < 0 || nnz >= (int64_t(1) << 31)) return fail(SBMDS_EINVAL, "need 0 <= nnz < 2^31");
     if (n >= (int64_t(1) << 31) || l > 46340 * 4) return fail(SBMDS_EINVAL, "n or l too large");
     if (!row_ptr || !D_ll || (nnz > 0 && (!col_idx || !val))) return fail(SBMDS_EINVAL, "NULL input pointer");
@@ -1734,6 +1872,11 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     h->n = n;
     h->l = l;
     h->nnz = nnz;
+    h->n_global = n_global;
+    h->row0 = row0;
+    h->rank = rank;
+    h->world = world;
+    h->shard = world > 1 || n_global != n;
     cudaStream_t dside = nullptr;      // host-D upload stream (see below)
     cudaStream_t dabs = nullptr;       // max |D| of the landed strips, behind the upload
     std::vector<cudaEvent_t> dstrips;  // strip groups landed
@@ -1924,7 +2067,8 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             keys.ensure(l * sizeof(int32_t));
             keys2.ensure(l * sizeof(int32_t));
             ord0.ensure(l * sizeof(int32_t));
-            launch(k_colstats, dim3((unsigned)std::min<int64_t>(4096, (l + 7) / 8)), dim3(256), 0, st, l, n,
+            // (w = S^T 1 / n with the GLOBAL n: a shard's w_g = S_g^T 1 / n sums to w over the ranks)
+            launch(k_colstats, dim3((unsigned)std::min<int64_t>(4096, (l + 7) / 8)), dim3(256), 0, st, l, n_global,
                    (const int32_t*)h->cptr.as<int32_t>(), (const int32_t*)h->ridx.as<int32_t>(),
                    (const float*)h->cval.as<float>(), h->w.as<double>(), keys.as<int32_t>());
             launch(k_iota, dim3(64), dim3(256), 0, st, (int32_t)l, ord0.as<int32_t>());
@@ -1958,7 +2102,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
         // the int8 D stream's schedule (host work) while D is still crossing the link
         PlanHost ph16;
         const bool pre_plan = h->dmax8_ok && !h->s8plan[1].ok;
-        if (pre_plan) ph16 = plan_host(l, h->num_sms, Sym8Cfg<16>::S, Sym8Cfg<16>::GN, true);
+        if (pre_plan) ph16 = plan_host(l, h->num_sms, Sym8Cfg<16>::S, Sym8Cfg<16>::GN, true, h->rank, h->world);
         // ---- D_ll: borrow (device, l % 4 == 0), copy a device D into a 16-byte-pitched buffer, or
         // join the host upload started above
         if (!d_dev) {
@@ -2011,7 +2155,7 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
             using C8 = Sym8Cfg<16>;
             auto& pl = h->s8plan[1];
             build_pair_plan(h, pl, h->num_sms, C8::S, C8::GN, true, &ph16);
-            h->Dt8.ensure((size_t)pl.ntiles * C8::A_BYTES);
+            h->Dt8.ensure((size_t)((int64_t)pl.NT * (pl.NT + 1) / 2) * C8::A_BYTES);
             unsigned int* aux = h->y16aux.as<unsigned int>();
             CK(cudaStreamCreateWithFlags(&h->pack_st, cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&h->pack_ev, cudaEventDisableTiming));
@@ -2031,6 +2175,25 @@ extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const in
     *out = h;
     return SBMDS_OK;
 }
+}  // namespace
+
+extern "C" sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const int64_t* row_ptr,
+                                     const int32_t* col_idx, const float* val, const float* D_ll, uint32_t flags,
+                                     void* cuda_stream, sbmds_t* out) {
+    return create_impl(n, n, 0, 0, 1, l, nnz, row_ptr, col_idx, val, D_ll, flags, cuda_stream, out);
+}
+
+extern "C" sbmds_status sbmds_create_shard(int64_t n_global, int64_t row0, int64_t n_local, int64_t l, int64_t nnz,
+                                           const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                           const float* D_ll, int32_t rank, int32_t world, uint32_t flags,
+                                           void* cuda_stream, sbmds_t* out) {
+    if (out) *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(SBMDS_EINVAL, "need 0 <= rank < world");
+    if (n_local < 1 || row0 < 0 || row0 + n_local > n_global)
+        return fail(SBMDS_EINVAL, "need 0 <= row0, 1 <= n_local, row0 + n_local <= n_global");
+    return create_impl(n_local, n_global, row0, rank, world, l, nnz, row_ptr, col_idx, val, D_ll, flags, cuda_stream,
+                       out);
+}
 
 extern "C" void sbmds_destroy(sbmds_t h) {
     if (!h) return;
@@ -2041,7 +2204,7 @@ extern "C" void sbmds_destroy(sbmds_t h) {
 
 extern "C" const char* sbmds_last_error(void) { return t_err.c_str(); }
 extern "C" int64_t sbmds_launch_count(void) { return g_launches.load(); }
-extern "C" int32_t sbmds_abi_version(void) { return 1; }
+extern "C" int32_t sbmds_abi_version(void) { return 2; }
 
 // ============================================================================ apply
 static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
@@ -2049,6 +2212,12 @@ static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
     const char* y = (const char*)b;
     return x < y + nb && y < x + na;
 }
+
+namespace {
+void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void* exch_in, void* exch_out,
+                     float* Y, cudaStream_t st);
+void shard_apply_nccl(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st);
+}  // namespace
 
 extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float* Y, void* cuda_stream) {
     Nvtx nv_apply("sbmds_apply");
@@ -2073,7 +2242,12 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
             Yd = h->yhost.as<float>();
         }
         ensure_dq(h, st);   // the int8 stream's precision check (once per handle)
-        if (h->center) {
+        if (h->shard) {
+            if (!h->center) return fail(SBMDS_EINVAL, "a shard handle applies the centred operator only");
+            if (h->comm) shard_apply_nccl(h, b, Xd, Yd, st);
+            else if (h->world == 1) for (int sg = 0; sg < 4; ++sg) shard_stage_dev(h, sg, b, Xd, nullptr, nullptr, Yd, st);
+            else return fail(SBMDS_EINVAL, "shard handle (world %d): attach NCCL or drive sbmds_shard_stage", h->world);
+        } else if (h->center) {
             apply_device(h, b, Xd, Yd, st);
         } else {
             // uncentred E^ X = S D S^T X: the centred machinery with s = 0 and w = 0 (both rank-one
@@ -2100,7 +2274,152 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
     } catch (const CudaError& e) {
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
         return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
+    } catch (const NcclError& e) {
+        return fail(SBMDS_ECUDA, "%s: %s", e.what, nccl_api().errorString(e.r));
     }
+    return SBMDS_OK;
+}
+
+// ============================================================================ sharded apply
+// rank g holds rows R_g of S (CSR S_g and its CSC copy) and streams tile range g
+// of D's upper triangle. The apply is linear in every exchanged quantity, so each rank forms
+// partials and a sum over ranks completes them (PAPER.md:221-222's matvec, split by rows of P
+// and by tiles of W):
+//   stage 0  s_g  = 1^T X_g                                   -> sum: s = 1^T X
+//   stage 1  Y1_g = S_g^T X_g - w_g s^T,  w_g = S_g^T 1 / n    -> sum: Y1 = S^T X - w s^T
+//   stage 2  Y2_g = sum over my tiles of D_IJ Y1_J (+ D_IJ^T Y1_I), t_g = w^T Y2_g
+//                                                               -> sum: Y2 = D Y1, t = w^T Y2
+//   stage 3  Y_g  = -1/2 (S_g Y2 - 1 t^T)                       (local rows, no exchange)
+// With an NCCL communicator attached, sbmds_apply runs the stages with in-library allreduces
+// on the call's stream; without one, the caller drives sbmds_shard_stage and sums the
+// exchange buffers itself. Full-D paths (FFMA, 3xTF32: b < 5, or the precision fallback) are
+// not tiled by rank: rank 0 streams all of D and the other ranks contribute zero partials.
+namespace {
+
+int64_t exch_t_offset(int64_t l, int b) { return ((int64_t)4 * l * b + 7) / 8 * 8; }
+
+// One stage on device buffers; the compact exchange layouts are those of sbmds_shard_stage.
+// exch_in / exch_out may be null (the NCCL path works on the internal buffers directly).
+void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void* exch_in, void* exch_out,
+                     float* Y, cudaStream_t st) {
+    const int bp = next_pow2(b);
+    ensure_apply_ws(h, bp);
+    const int64_t l = h->l;
+    if (stage == 0) {
+        launch(k_colsum, dim3((unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256)), dim3(256), 0, st,
+               h->n, b, X, h->colpart.as<double>(), h->s.as<double>(), h->counters.as<unsigned int>() + CNT_COLSUM);
+        if (exch_out) CK(cudaMemcpyAsync(exch_out, h->s.p, (size_t)b * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    } else if (stage == 1) {
+        if (exch_in) CK(cudaMemcpyAsync(h->s.p, exch_in, (size_t)b * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        spmm_csc(h, b, bp, X, st);
+        if (exch_out)
+            CK(cudaMemcpy2DAsync(exch_out, (size_t)b * 4, h->Y1.p, (size_t)bp * 4, (size_t)b * 4, l,
+                                 cudaMemcpyDeviceToDevice, st));
+    } else if (stage == 2) {
+        if (exch_in)
+            CK(cudaMemcpy2DAsync(h->Y1.p, (size_t)bp * 4, exch_in, (size_t)b * 4, (size_t)b * 4, l,
+                                 cudaMemcpyDeviceToDevice, st));
+        if (h->dstream == 0 && uses_sym(h, bp)) ycheck(h, b, bp, st);   // (same Y1, same decision on every rank)
+        if (uses_sym(h, bp) || h->rank == 0) {
+            dstream(h, b, bp, st, nullptr);
+        } else {   // full-D paths are not tiled: rank 0 owns all of D Y1
+            CK(cudaMemsetAsync(h->Y2.p, 0, (size_t)l * bp * sizeof(float), st));
+            CK(cudaMemsetAsync(h->t.p, 0, (size_t)b * sizeof(double), st));
+        }
+        h->y_fallback = false;
+        if (exch_out) {
+            CK(cudaMemcpy2DAsync(exch_out, (size_t)b * 4, h->Y2.p, (size_t)bp * 4, (size_t)b * 4, l,
+                                 cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync((char*)exch_out + exch_t_offset(l, b), h->t.p, (size_t)b * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+        }
+    } else {
+        if (exch_in) {
+            CK(cudaMemcpy2DAsync(h->Y2.p, (size_t)bp * 4, exch_in, (size_t)b * 4, (size_t)b * 4, l,
+                                 cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(h->t.p, (const char*)exch_in + exch_t_offset(l, b), (size_t)b * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+        }
+        spmm_csr(h, b, bp, Y, st);
+    }
+}
+
+// The four stages with NCCL sums in between (sbmds_apply on a handle with a communicator).
+void shard_apply_nccl(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st) {
+    const NcclApi& nc = nccl_api();
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(h->comm);
+    const int bp = next_pow2(b);
+    shard_stage_dev(h, 0, b, X, nullptr, nullptr, nullptr, st);
+    NK(nc.allReduce(h->s.p, h->s.p, (size_t)b, ncclFloat64, ncclSum, comm, st));
+    shard_stage_dev(h, 1, b, X, nullptr, nullptr, nullptr, st);
+    NK(nc.allReduce(h->Y1.p, h->Y1.p, (size_t)h->l * bp, ncclFloat32, ncclSum, comm, st));
+    shard_stage_dev(h, 2, b, nullptr, nullptr, nullptr, nullptr, st);
+    NK(nc.groupStart());
+    NK(nc.allReduce(h->Y2.p, h->Y2.p, (size_t)h->l * bp, ncclFloat32, ncclSum, comm, st));
+    NK(nc.allReduce(h->t.p, h->t.p, (size_t)b, ncclFloat64, ncclSum, comm, st));
+    NK(nc.groupEnd());
+    shard_stage_dev(h, 3, b, nullptr, nullptr, nullptr, Y, st);
+}
+
+}  // namespace
+
+extern "C" int64_t sbmds_shard_exchange_bytes(int64_t l, int32_t b, int32_t stage) {
+    if (l < 1 || b < 1 || b > kMaxB) return -1;
+    switch (stage) {
+        case 0: return (int64_t)b * 8;                       // out: s_g
+        case 1: return (int64_t)4 * l * b;                   // out: Y1_g (in: s)
+        case 2: return exch_t_offset(l, b) + (int64_t)8 * b;  // out: Y2_g | t_g (in: Y1)
+        case 3: return exch_t_offset(l, b) + (int64_t)8 * b;  // in: Y2 | t
+        default: return -1;
+    }
+}
+
+extern "C" sbmds_status sbmds_shard_stage(sbmds_t h, int32_t stage, int32_t b, const float* X, const void* exch_in,
+                                          void* exch_out, float* Y, void* cuda_stream) {
+    Nvtx nv("sbmds_shard_stage");
+    if (!h) return fail(SBMDS_EINVAL, "NULL handle");
+    if (b < 1 || b > kMaxB) return fail(SBMDS_EINVAL, "need 1 <= b <= 64 (b=%d)", b);
+    if (stage < 0 || stage > 3) return fail(SBMDS_EINVAL, "stage in 0..3");
+    const bool need_x = stage <= 1, need_in = stage >= 1, need_out = stage <= 2, need_y = stage == 3;
+    if ((need_x && !X) || (need_in && !exch_in) || (need_out && !exch_out) || (need_y && !Y))
+        return fail(SBMDS_EINVAL, "stage %d: NULL buffer", stage);
+    for (const void* p : {(const void*)X, exch_in, (const void*)exch_out, (const void*)Y})
+        if (p && !is_device_ptr(p)) return fail(SBMDS_EINVAL, "sbmds_shard_stage takes device buffers only");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    DevGuard g(h->dev);
+    try {
+        ensure_dq(h, st);
+        shard_stage_dev(h, stage, b, X, exch_in, exch_out, Y, st);
+    } catch (const CudaError& e) {
+        if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
+        return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
+    }
+    return SBMDS_OK;
+}
+
+extern "C" sbmds_status sbmds_nccl_unique_id(void* id_out) {
+    if (!id_out) return fail(SBMDS_EINVAL, "NULL id");
+    const NcclApi& nc = nccl_api();
+    if (!nc.ok) return fail(SBMDS_ECUDA, "NCCL unavailable: %s", nc.why.c_str());
+    ncclUniqueId id;
+    const ncclResult_t r = nc.getUniqueId(&id);
+    if (r != ncclSuccess) return fail(SBMDS_ECUDA, "ncclGetUniqueId: %s", nc.errorString(r));
+    memcpy(id_out, &id, sizeof id);
+    return SBMDS_OK;
+}
+
+extern "C" sbmds_status sbmds_shard_attach_nccl(sbmds_t h, const void* unique_id) {
+    if (!h || !unique_id) return fail(SBMDS_EINVAL, "NULL handle or id");
+    if (h->comm) return fail(SBMDS_EINVAL, "a communicator is already attached");
+    const NcclApi& nc = nccl_api();
+    if (!nc.ok) return fail(SBMDS_ECUDA, "NCCL unavailable: %s", nc.why.c_str());
+    DevGuard g(h->dev);
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof id);
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = nc.commInitRank(&comm, h->world, id, h->rank);   // collective over the ranks
+    if (r != ncclSuccess) return fail(SBMDS_ECUDA, "ncclCommInitRank: %s", nc.errorString(r));
+    h->comm = comm;
     return SBMDS_OK;
 }
 
@@ -2337,6 +2656,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
 
     Nvtx nv_eigs("sbmds_eigs");
     if (!h) return fail(SBMDS_EINVAL, "NULL handle");
+    if (h->shard) return fail(SBMDS_EINVAL, "sbmds_eigs on a shard handle is not built (sharded apply only)");
     if (block < 1 || block > kMaxB || block >= h->n) return fail(SBMDS_EINVAL, "need 1 <= block <= 64, block < n");
     if (m < 1 || m > block) return fail(SBMDS_EINVAL, "need 1 <= m <= block");
     if (max_iters < 1) return fail(SBMDS_EINVAL, "need max_iters >= 1");
@@ -2639,6 +2959,9 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         if (value < 0 || value > 255) return fail(SBMDS_EINVAL, "dq_max_range in [0, 255] binades");
         h->dq_max_range = (int)value;
         if (h->dq_state != 0) h->dq_state = 0;   // re-decided at the next apply / eigs
+    } else if (!strcmp(key, "dy_max_range")) {
+        if (value < 0 || value > 255) return fail(SBMDS_EINVAL, "dy_max_range in [0, 255] binades");
+        h->dy_max_range = (int)value;
     } else if (!strcmp(key, "sp8_max_range")) {
         if (value < 0 || value > 255) return fail(SBMDS_EINVAL, "sp8_max_range in [0, 255] binades");
         h->sp8_max_range = (int)value;   // (read when the sparse-step images are built)
@@ -2688,7 +3011,8 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a, -2 precision check
     else if (!strcmp(key, "sp8_range")) *value = h->sp8_range;          // its binade range (-1 not built)
-    else if (!strcmp(key, "chol_retries")) *value = h->chol_retries;  // last eigs: shifted Cholesky retries seen
+    else if (!strcmp(key, "chol_retries")) *value = h->chol_retries;
+    else if (!strcmp(key, "y_fallbacks")) *value = h->y_fallbacks;    // standalone applies sent to the fp32-grade stream  // last eigs: shifted Cholesky retries seen
     else if (!strcmp(key, "dq_state")) *value = h->dq_state;            // int8 D stream check: 1 kept, -1 fell back, 0 undecided
     else if (!strcmp(key, "dq_range")) *value = h->dq_range;            // binades between max |D| and the median |D|
     else if (!strcmp(key, "sp8_bytes")) *value = h->s8_bytes;           // its S images (HBM bytes per pass)

@@ -13,7 +13,8 @@ from typing import Optional
 
 import numpy as np
 
-from ._lib import SBMDS_BORROW_D, SBMDS_ENOCONV, SBMDS_VALIDATE, SbmdsError, SbmdsInfo, check, lib
+from ._lib import (NCCL_UNIQUE_ID_BYTES, SBMDS_BORROW_D, SBMDS_ENOCONV, SBMDS_VALIDATE, SbmdsError, SbmdsInfo,
+                   check, lib)
 
 try:
     import torch
@@ -130,6 +131,82 @@ class Sbmds:
         return int(v.value)
 
 
+class SbmdsShard(Sbmds):
+    """Shard handle: rows [row0, row0 + n_local) of an n_global-row S, tile range
+    `rank` of `world` of D's upper triangle (sbmds_create_shard). apply() needs a communicator
+    (attach_nccl) when world > 1; stage() drives one stage with caller-owned exchange buffers."""
+
+    def __init__(self, n_global: int, row0: int, n_local: int, l: int, row_ptr, col_idx, val, D, rank: int,
+                 world: int, *, validate: bool = False, stream=None):
+        self.n, self.l = int(n_local), int(l)
+        self.n_global, self.row0, self.rank, self.world = int(n_global), int(row0), int(rank), int(world)
+        nnz = int(row_ptr[-1])
+        flags = SBMDS_VALIDATE if validate else 0
+        self._keep = ()
+        h = ctypes.c_void_p()
+        check(lib().sbmds_create_shard(self.n_global, self.row0, self.n, self.l, nnz, _ptr(row_ptr, np.int64),
+                                       _ptr(col_idx, np.int32), _ptr(val, np.float32), _ptr(D, np.float32),
+                                       self.rank, self.world, flags, _stream(stream), ctypes.byref(h)))
+        self._h = h
+
+    def attach_nccl(self, unique_id: bytes):
+        buf = ctypes.create_string_buffer(bytes(unique_id), NCCL_UNIQUE_ID_BYTES)
+        check(lib().sbmds_shard_attach_nccl(self._h, buf))
+
+    def exchange_bytes(self, b: int, stage: int) -> int:
+        return int(lib().sbmds_shard_exchange_bytes(self.l, int(b), int(stage)))
+
+    def stage(self, stage: int, b: int, X=None, exch_in=None, exch_out=None, Y=None, stream=None):
+        """One stage of the sharded apply on device tensors (exchange buffers: uint8 tensors of
+        exchange_bytes(b, stage) bytes; the caller sums stage k's out over ranks into stage k+1's in)."""
+        ptr = lambda t: None if t is None else t.data_ptr()   # noqa: E731
+        check(lib().sbmds_shard_stage(self._h, int(stage), int(b), ptr(X), ptr(exch_in), ptr(exch_out), ptr(Y),
+                                      _stream(stream)))
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    check(lib().sbmds_nccl_unique_id(buf))
+    return buf.raw
+
+
+def split_rows(row_ptr, world: int):
+    """Contiguous row ranges [r0, r1) per rank with balanced stored entries (host logic)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    n, nnz = len(rp) - 1, int(rp[-1])
+    cuts = [0]
+    for g in range(1, world):
+        r = int(np.searchsorted(rp, nnz * g / world, side="left"))
+        cuts.append(min(max(r, cuts[-1] + 1), n - (world - g)))
+    cuts.append(n)
+    return [(cuts[g], cuts[g + 1]) for g in range(world)]
+
+
+def shard_tiles(l: int, S: int, rank: int, world: int) -> np.ndarray:
+    """The upper 128 x 128 tiles (I << 16 | J) rank `rank` streams (sbmds_shard_tiles)."""
+    cnt = int(lib().sbmds_shard_tiles(int(l), int(S), int(rank), int(world), None, 0))
+    if cnt < 0:
+        raise ValueError("bad shard plan arguments")
+    out = np.empty(cnt, dtype=np.uint32)
+    lib().sbmds_shard_tiles(int(l), int(S), int(rank), int(world), out.ctypes.data, cnt)
+    return out
+
+
+def shard_from_problem(p, rank: int, world: int, device: Optional[str] = "cuda", **kw) -> SbmdsShard:
+    """Build rank `rank`'s shard of a gen.configs.Problem (rows split by split_rows)."""
+    r0, r1 = split_rows(p.row_ptr, world)[rank]
+    rp = np.asarray(p.row_ptr, dtype=np.int64)
+    lo, hi = int(rp[r0]), int(rp[r1])
+    rpl = np.ascontiguousarray(rp[r0:r1 + 1] - lo)
+    ci = np.ascontiguousarray(np.asarray(p.col_idx)[lo:hi], dtype=np.int32)
+    vv = np.ascontiguousarray(np.asarray(p.val)[lo:hi], dtype=np.float32)
+    D = np.ascontiguousarray(p.D, dtype=np.float32)
+    if device and device != "numpy":
+        rpl, ci, vv, D = (torch.from_numpy(a).to(device) for a in (rpl, ci, vv, D))
+    return SbmdsShard(p.n, r0, r1 - r0, p.l, rpl, ci, vv, D, rank, world, **kw)
+
+
 def from_problem(p, device: Optional[str] = "cuda", **kw) -> Sbmds:
     """Convenience: build a handle from a gen.configs.Problem (host or device upload)."""
     rp = np.ascontiguousarray(p.row_ptr, dtype=np.int64)
@@ -141,4 +218,5 @@ def from_problem(p, device: Optional[str] = "cuda", **kw) -> Sbmds:
     return Sbmds(p.n, p.l, rp, ci, vv, D, **kw)
 
 
-__all__ = ["Sbmds", "SbmdsError", "from_problem", "launch_count"]
+__all__ = ["Sbmds", "SbmdsShard", "SbmdsError", "from_problem", "shard_from_problem", "launch_count",
+           "nccl_unique_id", "split_rows", "shard_tiles"]

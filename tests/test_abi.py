@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(libpath):
 def test_library_loads_and_answers_without_gpu(libpath):
     from paper_1705_10887_b200._lib import lib
     L = lib()
-    assert L.sbmds_abi_version() == 1
+    assert L.sbmds_abi_version() == 2
     assert L.sbmds_launch_count() >= 0
     assert isinstance(L.sbmds_last_error(), bytes)
 
