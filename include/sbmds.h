@@ -122,6 +122,24 @@ sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, 
                         uint64_t seed, const float* X0, double* eigvals, float* V, float* Z,
                         sbmds_info* info, void* cuda_stream);
 
+/*
+ * sbmds_bmds — BMDS, the paper's QR route to the same eigenpairs (§3.3):
+ * Q R = J P, -1/2 R W R^T = V~ Λ V~^T, Z = Q V~_m Λ_m^{1/2}, for small l (SURVEY §8(f) NEXT-3b;
+ * SPEC.md:455 asks for the BMDS / sBMDS path equivalence). On the device in fp64: the Gram
+ * (J P)^T J P from the dense n x l J P (the O(nl) memory the paper notes), its upper Cholesky
+ * factor R (= the R of QR = J P up to column signs), M = -1/2 R W R^T, the top-m algebraic
+ * eigenpairs of the l x l M by block subspace iteration (block, max_iters, tol, seed as in
+ * sbmds_eigs, Rayleigh-Ritz every rr_period iterations), then V = J P R^{-1} V~_m (Q is never
+ * stored) and Z = V Λ^{1/2} with sbmds_eigs' sign rule. M has the nonzero spectrum of B~ (the
+ * rest of B~'s spectrum is 0), so the top-m agree with sbmds_eigs whenever B~ has >= m
+ * positive eigenvalues.
+ *   Limits: l <= 8192, n l <= 2e9, 1 <= m <= block <= min(64, l). V, Z DEVICE (or NULL).
+ *   info->n_applies = 0 (no operator applies). SBMDS_EBREAKDOWN when J P is rank-deficient
+ *   (e.g. a landmark column of S with no entries); SBMDS_ENOCONV as sbmds_eigs.
+ */
+sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol, uint64_t seed,
+                        double* eigvals, float* V, float* Z, sbmds_info* info, void* cuda_stream);
+
 /* Frees everything the library allocated (not borrowed D). NULL-safe. */
 void sbmds_destroy(sbmds_t h);
 
@@ -216,7 +234,8 @@ int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas,
  *   stage 1  in: X_g, s (summed, double[b])  out: Y1_g = S_g^T X_g - w_g s^T (float[l*b]),
  *            w_g = S_g^T 1 / n_global (the w_g sum to w = S^T 1 / n)
  *   stage 2  in: Y1 (summed, float[l*b])     out: Y2_g (float[l*b]) and, at byte offset
- *            8*ceil(4lb/8), t_g = w^T Y2_g (double[b]): this rank's tiles' D_IJ Y1_J and
+ *            8*ceil(4lb/8), t_g = (D w_g)^T Y1 (double[b]; sums to t = w^T D Y1 = w^T Y2
+ *            with no further exchange; D w_g is formed once): this rank's tiles' D_IJ Y1_J and
  *            D_IJ^T Y1_I terms (full-D kernels -- b < 5, or the precision fallback -- run
  *            on rank 0 only; the other ranks return zeros)
  *   stage 3  in: Y2 | t (summed, stage 2's layout)   out: Y_g = -1/2 (S_g Y2 - 1 t^T) (n_local x b)

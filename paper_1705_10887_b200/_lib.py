@@ -20,7 +20,7 @@ STATUS_NAMES = {0: "SBMDS_OK", 1: "SBMDS_EINVAL", 2: "SBMDS_ENOMEM", 3: "SBMDS_E
 EXPORTS = ("sbmds_create", "sbmds_apply", "sbmds_eigs", "sbmds_destroy", "sbmds_last_error",
            "sbmds_set_option", "sbmds_get_stat", "sbmds_launch_count", "sbmds_abi_version",
            "sbmds_plan_selfcheck", "sbmds_create_shard", "sbmds_shard_stage", "sbmds_shard_exchange_bytes",
-           "sbmds_shard_attach_nccl", "sbmds_nccl_unique_id", "sbmds_shard_plan_selfcheck", "sbmds_shard_tiles")
+           "sbmds_shard_attach_nccl", "sbmds_nccl_unique_id", "sbmds_shard_plan_selfcheck", "sbmds_shard_tiles", "sbmds_bmds")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -85,6 +85,8 @@ def lib() -> ctypes.CDLL:
             L.sbmds_shard_plan_selfcheck.restype = i64
             L.sbmds_shard_tiles.argtypes = [i64, i32, i32, i32, p, i64]
             L.sbmds_shard_tiles.restype = i64
+            L.sbmds_bmds.argtypes = [p, i32, i32, i32, d, u64, p, p, p, ctypes.POINTER(SbmdsInfo), p]
+            L.sbmds_bmds.restype = ctypes.c_int
             _lib = L
     return _lib
 

@@ -32,6 +32,7 @@
 #include "k_fused.cuh"
 #include "k_sp8.cuh"
 #include "k_lanczos.cuh"
+#include "k_bmds.cuh"
 
 namespace sbmds {
 std::atomic<int64_t> g_launches{0};
@@ -441,6 +442,7 @@ void profiled(Profiler& pr, int k, cudaStream_t st, F&& f) {
     pr.pend.push_back({k, a, b});
 }
 
+constexpr int kBmdsMaxL = 8192;  // BMDS: dense l x l fp64 factors (512 MB at the limit)
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs for the grid reductions
 constexpr int kCounters = 8;
 enum { CNT_COLSUM = 0, CNT_DRED = 1, CNT_GRAM = 2, CNT_ARGMAX = 3, CNT_ROTATE = 4, CNT_FOLD = 5 };
@@ -457,6 +459,8 @@ struct sbmds_ctx {
     int rank = 0, world = 1;
     bool shard = false;
     void* comm = nullptr;
+    DevBuf vg;                 // shard: v_g = D w_g (t_g = v_g^T Y1, formed at the first stage 2)
+    bool vg_ok = false;
     int dev = 0, num_sms = 148;
     // S (CSR) and its device-built CSC copy
     DevBuf rp, col, val, cptr, ridx, cval, order, w;
@@ -1801,7 +1805,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->foldscr, &h->s8trace,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->vg, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
@@ -2287,8 +2291,8 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
 // and by tiles of W):
 //   stage 0  s_g  = 1^T X_g                                   -> sum: s = 1^T X
 //   stage 1  Y1_g = S_g^T X_g - w_g s^T,  w_g = S_g^T 1 / n    -> sum: Y1 = S^T X - w s^T
-//   stage 2  Y2_g = sum over my tiles of D_IJ Y1_J (+ D_IJ^T Y1_I), t_g = w^T Y2_g
-//                                                               -> sum: Y2 = D Y1, t = w^T Y2
+//   stage 2  Y2_g = sum over my tiles of D_IJ Y1_J (+ D_IJ^T Y1_I), t_g = (D w_g)^T Y1
+//                                                               -> sum: Y2 = D Y1, t = w^T D Y1 = w^T Y2
 //   stage 3  Y_g  = -1/2 (S_g Y2 - 1 t^T)                       (local rows, no exchange)
 // With an NCCL communicator attached, sbmds_apply runs the stages with in-library allreduces
 // on the call's stream; without one, the caller drives sbmds_shard_stage and sums the
@@ -2327,6 +2331,17 @@ void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void*
             CK(cudaMemsetAsync(h->t.p, 0, (size_t)b * sizeof(double), st));
         }
         h->y_fallback = false;
+        // t_g: the reduce formed w_g^T (this rank's Y2 part); the plan needs sum_g t_g = w^T Y2 =
+        // sum_g (D w_g)^T Y1 with the full Y1 every rank holds: overwrite t with v_g^T Y1
+        if (!h->vg_ok) {
+            ensure_full_d(h, st);
+            h->vg.ensure((size_t)l * sizeof(double));
+            launch(k_symv_rows, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, (l + 7) / 8)), dim3(256), 0,
+                   st, l, (const float*)h->D, h->ldD, (const double*)h->w.as<double>(), h->vg.as<double>());
+            h->vg_ok = true;
+        }
+        launch(k_vdot, dim3(1), dim3(256), 0, st, l, b, bp, (const double*)h->vg.as<double>(),
+               (const float*)h->Y1.as<float>(), h->t.as<double>());
         if (exch_out) {
             CK(cudaMemcpy2DAsync(exch_out, (size_t)b * 4, h->Y2.p, (size_t)bp * 4, (size_t)b * 4, l,
                                  cudaMemcpyDeviceToDevice, st));
@@ -2915,6 +2930,180 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         }
         if (tol > 0.0 && !converged) ret = fail(SBMDS_ENOCONV, "no convergence in %d iterations (residual %g)",
                                                 max_iters, rr_host.maxres);
+    } catch (const CudaError& e) {
+        if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
+        return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
+    }
+    return ret;
+}
+
+// ============================================================================ BMDS
+// NEXT-3b: the paper's QR route, k_bmds.cuh. Steps (all on the device, fp64):
+//   G = (J P)^T (J P) from the dense n x l J P; G = R^T R (blocked upper Cholesky, 64-wide panels);
+//   M = -1/2 R W R^T; the top-m algebraic eigenpairs of the l x l M by block subspace iteration
+//   with Cholesky-QR and Rayleigh-Ritz (k_chol, k_rr: the same small kernels as sbmds_eigs);
+//   U = R^{-1} V~_m; V = J P U = S U - 1 (w^T U) (CSR SpMM), Z = V Λ^{1/2}, signs as sbmds_eigs.
+namespace {
+template <bool TA, bool TB>
+void dgemm(cudaStream_t st, int M, int N, int64_t K, double alpha, const double* A, int64_t lda, const double* B,
+           int64_t ldb, double beta, double* C, int64_t ldc) {
+    launch(k_dgemm<TA, TB>, dim3((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64)), dim3(256), 0, st, M, N, K,
+           alpha, A, lda, B, ldb, beta, C, ldc);
+}
+}  // namespace
+
+extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol, uint64_t seed,
+                                   double* eigvals, float* V, float* Z, sbmds_info* info, void* cuda_stream) {
+    Nvtx nv("sbmds_bmds");
+    if (!h) return fail(SBMDS_EINVAL, "NULL handle");
+    if (h->shard) return fail(SBMDS_EINVAL, "sbmds_bmds on a shard handle");
+    const int64_t n = h->n, l = h->l;
+    if (l > kBmdsMaxL || (double)n * (double)l > 2.0e9)
+        return fail(SBMDS_EINVAL, "BMDS needs l <= %d and n l <= 2e9 (dense J P and l x l factors)", kBmdsMaxL);
+    if (block < 1 || block > kMaxB || block > l) return fail(SBMDS_EINVAL, "need 1 <= block <= min(64, l)");
+    if (m < 1 || m > block) return fail(SBMDS_EINVAL, "need 1 <= m <= block");
+    if (max_iters < 1) return fail(SBMDS_EINVAL, "need max_iters >= 1");
+    if (!eigvals) return fail(SBMDS_EINVAL, "eigvals (host) is NULL");
+    if ((V && !is_device_ptr(V)) || (Z && !is_device_ptr(Z))) return fail(SBMDS_EINVAL, "sbmds_bmds: V, Z on the device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    DevGuard g(h->dev);
+    const int b = block;
+    sbmds_status ret = SBMDS_OK;
+    try {
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, st));
+        DevBuf JP{true}, A{true}, W{true}, T{true}, X{true}, Y{true}, small{true};
+        h->status.ensure(16);
+        CK(cudaMemsetAsync(h->status.p, 0, 16, st));
+        int* status = h->status.as<int>();
+        // J P (dense, n x l) and its Gram G (in A)
+        JP.ensure((size_t)n * l * sizeof(double));
+        launch(k_jp_dense, dim3((unsigned)std::min<int64_t>(n, 16 * (int64_t)h->num_sms)), dim3(256), 0, st, n, l,
+               (const int32_t*)h->rp.as<int32_t>(), (const int32_t*)h->col.as<int32_t>(),
+               (const float*)h->val.as<float>(), (const double*)h->w.as<double>(), JP.as<double>());
+        A.ensure((size_t)l * l * sizeof(double));
+        dgemm<true, false>(st, (int)l, (int)l, n, 1.0, JP.as<double>(), l, JP.as<double>(), l, 0.0, A.as<double>(), l);
+        JP.release();
+        // G = R^T R, right-looking, 64-column panels
+        for (int64_t k0 = 0; k0 < l; k0 += 64) {
+            const int nb = (int)std::min<int64_t>(64, l - k0);
+            launch(k_potf2, dim3(1), dim3(256), 0, st, A.as<double>(), l, (int)k0, nb, status);
+            const int64_t rest = l - k0 - nb;
+            if (rest > 0) {
+                launch(k_trsm_rows, dim3((unsigned)((rest + 255) / 256)), dim3(256), 0, st, A.as<double>(), l, l,
+                       (int)k0, nb, (const int*)status);
+                // trailing A[k1:, k1:] -= R[k0:k1, k1:]^T R[k0:k1, k1:]
+                const double* Rp = A.as<double>() + k0 * l + k0 + nb;
+                dgemm<true, false>(st, (int)rest, (int)rest, nb, -1.0, Rp, l, Rp, l, 1.0,
+                                   A.as<double>() + (k0 + nb) * l + k0 + nb, l);
+            }
+        }
+        int hstat = 0;
+        peek_to_host(&hstat, status, sizeof(int), st);
+        if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "BMDS: J P is rank-deficient (Cholesky of (JP)^T JP broke down)");
+        launch(k_zero_lower, dim3((unsigned)std::min<int64_t>(4096, (l * l + 255) / 256)), dim3(256), 0, st,
+               A.as<double>(), l, l);
+        // M = -1/2 R W R^T
+        ensure_full_d(h, st);
+        W.ensure((size_t)l * l * sizeof(double));
+        T.ensure((size_t)l * l * sizeof(double));
+        launch(k_f2d_sym, dim3((unsigned)std::min<int64_t>(4096, (l * l + 255) / 256)), dim3(256), 0, st, l,
+               (const float*)h->D, h->ldD, W.as<double>());
+        dgemm<false, false>(st, (int)l, (int)l, l, 1.0, A.as<double>(), l, W.as<double>(), l, 0.0, T.as<double>(), l);
+        dgemm<false, true>(st, (int)l, (int)l, l, -0.5, T.as<double>(), l, A.as<double>(), l, 0.0, W.as<double>(), l);
+        double* Md = W.as<double>();
+        // top-m of M: block subspace iteration (X orthonormal l x b)
+        X.ensure((size_t)l * b * sizeof(double));
+        Y.ensure((size_t)l * b * sizeof(double));
+        small.ensure((size_t)3 * kMaxB * kMaxB * sizeof(double));
+        double* Gs = small.as<double>();
+        double* Hs = Gs + kMaxB * kMaxB;
+        h->Rinv.ensure(kMaxB * kMaxB * sizeof(double));
+        h->rr.ensure(sizeof(RrOut));
+        launch(k_dinit, dim3(64), dim3(256), 0, st, l * b, (uint64_t)seed, Y.as<double>());
+        auto orth = [&](double* Yin, double* Xout) {   // Xout = Yin R^-1, Yin^T Yin = R^T R
+            dgemm<true, false>(st, b, b, l, 1.0, Yin, b, Yin, b, 0.0, Gs, b);
+            launch(k_chol, dim3(1), dim3(256), 0, st, b, (const double*)Gs, h->Rinv.as<double>(), status);
+            dgemm<false, false>(st, (int)l, b, b, 1.0, Yin, b, h->Rinv.as<double>(), b, 0.0, Xout, b);
+        };
+        orth(Y.as<double>(), X.as<double>());
+        smem_attr(k_rr, kRrSmem);
+        int it = 0;
+        bool converged = false;
+        RrOut rr_host;
+        for (it = 1; it <= max_iters; ++it) {
+            dgemm<false, false>(st, (int)l, b, l, 1.0, Md, l, X.as<double>(), b, 0.0, Y.as<double>(), b);
+            if (it % h->rr_period == 0 || it == max_iters) {
+                dgemm<true, false>(st, b, b, l, 1.0, X.as<double>(), b, Y.as<double>(), b, 0.0, Hs, b);
+                dgemm<true, false>(st, b, b, l, 1.0, Y.as<double>(), b, Y.as<double>(), b, 0.0, Gs, b);
+                launch(k_rr, dim3(1), dim3(256), kRrSmem, st, b, m, tol > 0.0 ? tol : -1.0, (const double*)Hs,
+                       (const double*)Gs, (const double*)nullptr, h->rr.as<RrOut>());
+                int conv = 0;
+                CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if ((tol > 0.0 && conv) || it == max_iters) {
+                    converged = tol > 0.0 && conv;
+                    break;
+                }
+            }
+            orth(Y.as<double>(), X.as<double>());
+        }
+        if (it > max_iters) it = max_iters;
+        peek_to_host(&hstat, status, sizeof(int), st);
+        if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "BMDS: Cholesky-QR of the l x b iterate broke down");
+        CK(cudaMemcpyAsync(&rr_host, h->rr.p, sizeof(RrOut), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        // V~_m = X U[:, :m] (l x m), U_l = R^-1 V~_m, V = J P U_l
+        double* Vt = Y.as<double>();                       // (reuse: l x m)
+        double* Ul = T.as<double>();
+        dgemm<false, false>(st, (int)l, m, b, 1.0, X.as<double>(), b, h->rr.as<RrOut>()->U, b, 0.0, Vt, m);
+        launch(k_backsolve, dim3((unsigned)((m + 7) / 8)), dim3(256), 0, st, l, m, (const double*)A.as<double>(), l,
+               (const double*)Vt, (int64_t)m, Ul);
+        const int bp = next_pow2(m);
+        ensure_apply_ws(h, bp);
+        launch(k_bmds_to_y2, dim3(1), dim3(256), 0, st, l, m, bp, (const double*)Ul, (const double*)h->w.as<double>(),
+               h->Y2.as<float>(), h->t.as<double>());
+        const size_t vbytes = (size_t)n * m * sizeof(float);
+        float* Vd = V ? V : (h->vtmp.ensure(vbytes), h->vtmp.as<float>());
+        spmm_csr(h, m, bp, Vd, st);
+        h->sign.ensure(kMaxB * sizeof(float));
+        h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
+        h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
+        launch(k_col_argmax, dim3(kRedBlocks), dim3(256), 0, st, n, m, (const float*)Vd, h->apval.as<float>(),
+               h->apidx.as<long long>(), h->sign.as<float>(), h->counters.as<unsigned int>() + CNT_ARGMAX);
+        const double* theta = h->rr.as<RrOut>()->theta;
+        launch(k_finalize, dim3((unsigned)std::min<int64_t>(4 * 148, (n * m + 255) / 256)), dim3(256), 0, st, n, m,
+               (const float*)h->sign.as<float>(), theta, Vd, Z);
+        gram(h, m, Vd, nullptr, st);
+        std::vector<double> gv((size_t)m * m);
+        CK(cudaMemcpyAsync(gv.data(), h->G.p, gv.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(e1, st));
+        CK(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        double orth_err = 0.0;
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j) orth_err = std::max(orth_err, std::fabs(gv[i * m + j] - (i == j ? 1.0 : 0.0)));
+        int n_neg = 0;
+        for (int j = 0; j < m; ++j) {
+            eigvals[j] = rr_host.theta[j];
+            if (rr_host.theta[j] < 0.0) ++n_neg;
+        }
+        if (info) {
+            info->iters = it;
+            info->n_applies = 0;   // (no operator applies: the l x l problem only)
+            info->n_negative = n_neg;
+            info->converged = converged ? 1 : 0;
+            info->max_residual = rr_host.maxres;
+            info->orth_error = orth_err;
+            info->gpu_ms = ms;
+        }
+        if (tol > 0.0 && !converged)
+            ret = fail(SBMDS_ENOCONV, "BMDS: no convergence in %d iterations (residual %g)", max_iters, rr_host.maxres);
     } catch (const CudaError& e) {
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
         return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());

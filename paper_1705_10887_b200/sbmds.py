@@ -122,6 +122,21 @@ class Sbmds:
         d["status"] = int(st)
         return ev, V, Z, d
 
+    def bmds(self, m: int, block: int, max_iters: int = 2000, tol: float = 1e-8, seed: int = 0, stream=None,
+             raise_noconv=False):
+        """BMDS (sbmds_bmds): (eigvals, V, Z, info) on the device."""
+        V = torch.empty((self.n, m), dtype=torch.float32, device="cuda")
+        Z = torch.empty((self.n, m), dtype=torch.float32, device="cuda")
+        ev = np.zeros(m, dtype=np.float64)
+        info = SbmdsInfo()
+        st = lib().sbmds_bmds(self._h, int(m), int(block), int(max_iters), float(tol), int(seed), ev.ctypes.data,
+                              V.data_ptr(), Z.data_ptr(), ctypes.byref(info), _stream(stream))
+        if not (st == SBMDS_ENOCONV and not raise_noconv):
+            check(st)
+        d = {k: getattr(info, k) for k, _ in SbmdsInfo._fields_}
+        d["status"] = int(st)
+        return ev, V, Z, d
+
     def set_option(self, key: str, value: int):
         check(lib().sbmds_set_option(self._h, key.encode(), int(value)))
 

@@ -4,8 +4,8 @@
 Each rank asks the library (host code only) for its tile range of D's upper triangle and
 checks its schedule; the ranks then all-gather their tiles (every upper tile exactly once over
 the ranks) and run the four stages of the plan on the CPU in fp64 -- rows split by
-split_rows, w_g = S_g^T 1 / n_global, tile contributions D_IJ Y1_J and D_IJ^T Y1_I, t_g = w^T
-Y2_g -- with gloo all_reduce(sum) between stages. The gathered result must equal the oracle's
+split_rows, w_g = S_g^T 1 / n_global, tile contributions D_IJ Y1_J and D_IJ^T Y1_I, t_g =
+(D w_g)^T Y1 -- with gloo all_reduce(sum) between stages. The gathered result must equal the oracle's
 apply: a wrong w split, a missed or doubled tile, or a wrong rank-one term fails it.
 """
 import os
@@ -55,7 +55,6 @@ def _stages(p, rank, world, tiles, dist, X):
     s = allreduce(Xg.sum(0))                                   # stage 0
     wg = Sg.sum(0) / n
     Y1 = allreduce(Sg.T @ Xg - np.outer(wg, s))                # stage 1
-    w = allreduce(wg.copy())
     Y2g = np.zeros_like(Y1)                                    # stage 2: my tiles only
     for v in tiles:
         I, J = int(v) >> 16, int(v) & 0xFFFF
@@ -63,7 +62,7 @@ def _stages(p, rank, world, tiles, dist, X):
         Y2g[ri] += D[ri, rj] @ Y1[rj]
         if I < J:
             Y2g[rj] += D[ri, rj].T @ Y1[ri]
-    tg = w @ Y2g
+    tg = (D @ wg) @ Y1                                         # t_g = (D w_g)^T Y1 (local w_g)
     Y2 = allreduce(Y2g)
     t = allreduce(tg)
     return r0, r1, -0.5 * (Sg @ Y2 - t[None, :])               # stage 3
