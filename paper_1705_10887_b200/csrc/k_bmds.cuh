@@ -86,21 +86,47 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int64_t K, double a
         }
 }
 
-// Upper Cholesky of the nb x nb diagonal block at (k0, k0) of A (lda), in place: A_kk = R^T R.
-// One block; status = 2 on a non-positive or non-finite pivot (J P rank-deficient).
+// max_i A_ii (one block): the scale of the semi-definite Cholesky's zero-pivot test
+__global__ void __launch_bounds__(256) k_maxdiag(const double* __restrict__ A, int64_t lda, int64_t l,
+                                                 double* __restrict__ out) {
+    __shared__ double red[256];
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < l; i += blockDim.x) m = fmax(m, A[i * lda + i]);
+    red[threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < 256; ++q) m = fmax(m, red[q]);
+        *out = m;
+    }
+}
+
+// Upper Cholesky of the nb x nb diagonal block at (k0, k0) of A (lda), in place: A_kk = R^T R,
+// semi-definite: J P is rank-deficient whenever some combination of S's columns is constant
+// (for a partition of unity J P 1 = J 1 = 0), so a pivot <= 1e-13 max diag is a null direction
+// (counted in *dropped): its row of R is zero (the exact-arithmetic value for a PSD matrix).
+// status = 2 on a negative (< -1e-10 max diag) or non-finite pivot (G not PSD).
 __global__ void __launch_bounds__(256) k_potf2(double* __restrict__ A, int64_t lda, int k0, int nb,
-                                               int* __restrict__ status) {
+                                               int* __restrict__ status, const double* __restrict__ dmax,
+                                               int* __restrict__ dropped) {
     __shared__ double T[64][65];
     __shared__ int fail;
     const int tid = threadIdx.x;
     for (int e = tid; e < nb * nb; e += blockDim.x) T[e / nb][e % nb] = A[(int64_t)(k0 + e / nb) * lda + k0 + e % nb];
     if (tid == 0) fail = 0;
     __syncthreads();
+    const double tol0 = 1e-13 * *dmax;
     for (int k = 0; k < nb; ++k) {
         const double d = T[k][k];
-        if (!(d > 0.0) || !isfinite(d)) {
+        if (!isfinite(d) || d < -1e-10 * *dmax) {
             if (tid == 0) fail = 1;
             break;
+        }
+        if (d <= tol0) {   // null direction: R row k = 0, nothing to eliminate
+            __syncthreads();
+            for (int j = k + tid; j < nb; j += blockDim.x) T[k][j] = 0.0;
+            if (tid == 0) atomicAdd(dropped, 1);
+            __syncthreads();
+            continue;
         }
         const double r = sqrt(d), ri = 1.0 / r;
         __syncthreads();
@@ -141,7 +167,7 @@ __global__ void __launch_bounds__(256) k_trsm_rows(double* __restrict__ A, int64
     for (int i = 0; i < nb; ++i) {
         double acc = A[(int64_t)(k0 + i) * lda + j];
         for (int p = 0; p < i; ++p) acc = fma(-R[p][i], x[p], acc);
-        x[i] = acc / R[i][i];
+        x[i] = R[i][i] != 0.0 ? acc / R[i][i] : 0.0;   // (a dropped pivot's row of R stays 0)
         A[(int64_t)(k0 + i) * lda + j] = x[i];
     }
 }
@@ -163,7 +189,8 @@ __global__ void __launch_bounds__(256) k_backsolve(int64_t l, int m, const doubl
         for (int64_t j = i + 1 + lane; j < l; j += 32) acc = fma(R[i * ldr + j], U[j * ldv + c], acc);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) U[i * ldv + c] = (V[i * ldv + c] - acc) / R[i * ldr + i];
+        const double rii = R[i * ldr + i];   // (a dropped pivot: its equation is vacuous, U_i = 0)
+        if (lane == 0) U[i * ldv + c] = rii != 0.0 ? (V[i * ldv + c] - acc) / rii : 0.0;
         __syncwarp();
     }
 }

@@ -528,6 +528,7 @@ struct sbmds_ctx {
     // smallest nonzero row maximum; above sp8_max_range the fp32 sparse kernels are used
     int sp8_range = -1;
     int sp8_max_range = 7;
+    int bmds_dropped = 0;             // last sbmds_bmds: null pivots of (JP)^T JP (rank deficiency of J P)
     int chol_retries = 0;
     // standalone apply: per-column check of Y1 before the int8 stream (its per-column quantum is
     // max |y_c| 2^-23): when max |y_c| > 2^dy_max_range rms(y_c) for some column, this apply
@@ -1852,7 +1853,7 @@ void destroy_ctx(sbmds_ctx* h) {
 namespace {
 sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, int world, int64_t l, int64_t nnz,
                          const int64_t* row_ptr, const int32_t* col_idx, const float* val, const float* D_ll,
-                         uint32_t flags, void* cuda_stream, sbmds_t* out) {
+                         uint32_t flags, void* cuda_stream, sbmds_t* out, bool create_as_shard = false) {
     // (diagnostics) SBMDS_TRACE_CREATE=1: host-clock phase times of this create on stderr
     static const bool trace_create = getenv("SBMDS_TRACE_CREATE") != nullptr;
     const auto t_create0 = std::chrono::steady_clock::now();
@@ -1880,7 +1881,7 @@ sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, in
     h->row0 = row0;
     h->rank = rank;
     h->world = world;
-    h->shard = world > 1 || n_global != n;
+    h->shard = world > 1 || n_global != n || create_as_shard;
     cudaStream_t dside = nullptr;      // host-D upload stream (see below)
     cudaStream_t dabs = nullptr;       // max |D| of the landed strips, behind the upload
     std::vector<cudaEvent_t> dstrips;  // strip groups landed
@@ -2196,7 +2197,7 @@ extern "C" sbmds_status sbmds_create_shard(int64_t n_global, int64_t row0, int64
     if (n_local < 1 || row0 < 0 || row0 + n_local > n_global)
         return fail(SBMDS_EINVAL, "need 0 <= row0, 1 <= n_local, row0 + n_local <= n_global");
     return create_impl(n_local, n_global, row0, rank, world, l, nnz, row_ptr, col_idx, val, D_ll, flags, cuda_stream,
-                       out);
+                       out, true);
 }
 
 extern "C" void sbmds_destroy(sbmds_t h) {
@@ -2986,10 +2987,15 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         A.ensure((size_t)l * l * sizeof(double));
         dgemm<true, false>(st, (int)l, (int)l, n, 1.0, JP.as<double>(), l, JP.as<double>(), l, 0.0, A.as<double>(), l);
         JP.release();
-        // G = R^T R, right-looking, 64-column panels
+        // G = R^T R, right-looking, 64-column panels (semi-definite: null pivots dropped)
+        small.ensure((size_t)3 * kMaxB * kMaxB * sizeof(double) + 64);
+        double* dmax = reinterpret_cast<double*>(small.as<char>() + (size_t)3 * kMaxB * kMaxB * sizeof(double));
+        int* dropped = status + 2;
+        launch(k_maxdiag, dim3(1), dim3(256), 0, st, (const double*)A.as<double>(), l, l, dmax);
         for (int64_t k0 = 0; k0 < l; k0 += 64) {
             const int nb = (int)std::min<int64_t>(64, l - k0);
-            launch(k_potf2, dim3(1), dim3(256), 0, st, A.as<double>(), l, (int)k0, nb, status);
+            launch(k_potf2, dim3(1), dim3(256), 0, st, A.as<double>(), l, (int)k0, nb, status, (const double*)dmax,
+                   dropped);
             const int64_t rest = l - k0 - nb;
             if (rest > 0) {
                 launch(k_trsm_rows, dim3((unsigned)((rest + 255) / 256)), dim3(256), 0, st, A.as<double>(), l, l,
@@ -3000,9 +3006,11 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
                                    A.as<double>() + (k0 + nb) * l + k0 + nb, l);
             }
         }
-        int hstat = 0;
-        peek_to_host(&hstat, status, sizeof(int), st);
-        if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "BMDS: J P is rank-deficient (Cholesky of (JP)^T JP broke down)");
+        int hst3[3] = {0, 0, 0};
+        peek_to_host(hst3, status, sizeof hst3, st);
+        int hstat = hst3[0];
+        if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "BMDS: (JP)^T JP is not positive semi-definite");
+        h->bmds_dropped = hst3[2];
         launch(k_zero_lower, dim3((unsigned)std::min<int64_t>(4096, (l * l + 255) / 256)), dim3(256), 0, st,
                A.as<double>(), l, l);
         // M = -1/2 R W R^T
@@ -3017,7 +3025,6 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         // top-m of M: block subspace iteration (X orthonormal l x b)
         X.ensure((size_t)l * b * sizeof(double));
         Y.ensure((size_t)l * b * sizeof(double));
-        small.ensure((size_t)3 * kMaxB * kMaxB * sizeof(double));
         double* Gs = small.as<double>();
         double* Hs = Gs + kMaxB * kMaxB;
         h->Rinv.ensure(kMaxB * kMaxB * sizeof(double));
@@ -3201,6 +3208,7 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a, -2 precision check
     else if (!strcmp(key, "sp8_range")) *value = h->sp8_range;          // its binade range (-1 not built)
     else if (!strcmp(key, "chol_retries")) *value = h->chol_retries;
+    else if (!strcmp(key, "bmds_dropped")) *value = h->bmds_dropped;  // last BMDS: rank deficiency of J P
     else if (!strcmp(key, "y_fallbacks")) *value = h->y_fallbacks;    // standalone applies sent to the fp32-grade stream  // last eigs: shifted Cholesky retries seen
     else if (!strcmp(key, "dq_state")) *value = h->dq_state;            // int8 D stream check: 1 kept, -1 fell back, 0 undecided
     else if (!strcmp(key, "dq_range")) *value = h->dq_range;            // binades between max |D| and the median |D|

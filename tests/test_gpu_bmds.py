@@ -27,6 +27,7 @@ def test_bmds_config1_vs_dense_oracle_and_oracle_bmds():
     lam_b, V_b, _ = O.bmds(S, p.D, p.m)
     with handle(p) as h:
         lam, V, Z, info = h.bmds(p.m, p.block, tol=1e-9)
+        assert h.stat("bmds_dropped") == 1              # J P 1 = 0 for rows summing to 1
     V, Z = host(V), host(Z)
     assert info["converged"] == 1 and info["n_applies"] == 0
     for ref in (lam_o, lam_b):
@@ -76,13 +77,20 @@ def test_bmds_cf2_exact():
     assert O.principal_angle(host(V), U) <= 1e-4
 
 
-def test_bmds_rank_deficient_jp_breaks_down():
-    """A landmark column of S with no entries makes J P rank-deficient: SBMDS_EBREAKDOWN."""
-    from paper_1705_10887_b200 import SbmdsError
+def test_bmds_rank_deficient_jp():
+    """J P is rank-deficient by construction for a partition of unity (J P 1 = J 1 = 0): the
+    semi-definite Cholesky drops exactly that null pivot (stat bmds_dropped = 1). A landmark
+    column with no entries adds a second null direction (a zero column of J P); both solves
+    still match the dense oracle."""
     p = configs.config(1)
     col = np.asarray(p.col_idx).copy()
     col[col == 7] = 8                                   # landmark 7 loses every entry
     q = configs.Problem("hole", p.n, p.l, p.row_ptr, col, p.val, p.D)
-    with handle(q) as h:
-        with pytest.raises(SbmdsError, match="EBREAKDOWN"):
-            h.bmds(3, 8)
+    for prob, drops in ((p, 1), (q, 2)):
+        S = O.csr(prob.n, prob.l, prob.row_ptr, prob.col_idx, prob.val32())
+        lam_o, V_o, _ = O.eigs_dense(S, prob.D, 3)
+        with handle(prob) as h:
+            lam, V, Z, info = h.bmds(3, 8, tol=1e-9)
+            assert h.stat("bmds_dropped") == drops
+        assert np.all(np.abs(lam - lam_o) <= 1e-6 * np.abs(lam_o)), (lam, lam_o)
+        assert O.principal_angle(host(V), V_o) <= ANGLE_TOL
