@@ -105,9 +105,10 @@ __global__ void __launch_bounds__(256) k_maxdiag(const double* __restrict__ A, i
 // (for a partition of unity J P 1 = J 1 = 0), so a pivot <= 1e-13 max diag is a null direction
 // (counted in *dropped): its row of R is zero (the exact-arithmetic value for a PSD matrix).
 // status = 2 on a negative (< -1e-10 max diag) or non-finite pivot (G not PSD).
+// (allow_drop = 0, the sBHA solve of the SPD M_uu: a non-positive pivot is a breakdown.)
 __global__ void __launch_bounds__(256) k_potf2(double* __restrict__ A, int64_t lda, int k0, int nb,
                                                int* __restrict__ status, const double* __restrict__ dmax,
-                                               int* __restrict__ dropped) {
+                                               int* __restrict__ dropped, int allow_drop) {
     __shared__ double T[64][65];
     __shared__ int fail;
     const int tid = threadIdx.x;
@@ -117,11 +118,11 @@ __global__ void __launch_bounds__(256) k_potf2(double* __restrict__ A, int64_t l
     const double tol0 = 1e-13 * *dmax;
     for (int k = 0; k < nb; ++k) {
         const double d = T[k][k];
-        if (!isfinite(d) || d < -1e-10 * *dmax) {
+        if (!isfinite(d) || d < -1e-10 * *dmax || (!allow_drop && !(d > 0.0))) {
             if (tid == 0) fail = 1;
             break;
         }
-        if (d <= tol0) {   // null direction: R row k = 0, nothing to eliminate
+        if (allow_drop && d <= tol0) {   // null direction: R row k = 0, nothing to eliminate
             __syncthreads();
             for (int j = k + tid; j < nb; j += blockDim.x) T[k][j] = 0.0;
             if (tid == 0) atomicAdd(dropped, 1);

@@ -2976,6 +2976,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, st));
         DevBuf JP{true}, A{true}, W{true}, T{true}, X{true}, Y{true}, small{true};
+        h->G.ensure(kMaxB * kMaxB * sizeof(double));   // (the final orthogonality Gram)
         h->status.ensure(16);
         CK(cudaMemsetAsync(h->status.p, 0, 16, st));
         int* status = h->status.as<int>();
@@ -2995,7 +2996,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         for (int64_t k0 = 0; k0 < l; k0 += 64) {
             const int nb = (int)std::min<int64_t>(64, l - k0);
             launch(k_potf2, dim3(1), dim3(256), 0, st, A.as<double>(), l, (int)k0, nb, status, (const double*)dmax,
-                   dropped);
+                   dropped, 1);
             const int64_t rest = l - k0 - nb;
             if (rest > 0) {
                 launch(k_trsm_rows, dim3((unsigned)((rest + 255) / 256)), dim3(256), 0, st, A.as<double>(), l, l,
