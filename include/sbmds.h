@@ -140,6 +140,40 @@ sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, 
 sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol, uint64_t seed,
                         double* eigvals, float* V, float* Z, sbmds_info* info, void* cuda_stream);
 
+/*
+ * sBHA build: the sparse biharmonic interpolation operator
+ * S = P_sparse of a triangle mesh, the input of sbmds_create (§2.2, §3, §3.1):
+ *   A_ij = (cot α_ij + cot β_ij) / 2 (a boundary edge: its one cotangent / 2),
+ *   D_ii = 1/3 of the area of the faces incident on i, V = diag(A 1),
+ *   M = (V - A)^T D^{-1} (V - A),
+ *   P = [I_l ; P_u], P_u = -M_uu^{-1} M_ub (Eq. 6; landmark rows are e_t),
+ *   each column of P_u keeps its p largest magnitudes (PAPER.md:175-191 thresholding; ties to
+ *   the lowest vertex index, kept values unchanged), p = sbmds_sbha_p(n, l, p_row)
+ *   = clamp(ceil((n - l) p_row / l), 1, n - l) (ceiling per SPEC.md:380).
+ * Computed on the device in fp64: cotangents and masses per face / vertex, M's rows on the fly,
+ * a band Cholesky of M_uu after a reverse Cuthill-McKee ordering of the free vertices (host),
+ * the l right-hand sides solved panel by panel, a radix select per column.
+ *   verts   : double[n*3] (host or device), faces: int32[nf*3] (host or device), vertex
+ *             indices in [0, n), no zero-area face (SBMDS_EINVAL otherwise).
+ *   landmarks: int32[l], distinct, in [0, n), 1 <= l < n.
+ *   row_ptr : int64[n+1], col_idx: int32[nnz], val: float[nnz] (host or device) receive S in
+ *             CSR (columns ascending per row), nnz = l + l p exactly (info->nnz).
+ * SBMDS_EBREAKDOWN when M_uu is not positive definite (a connected region of free vertices
+ * without a landmark); SBMDS_EINVAL when a vertex has more than 64 neighbours or a row of M
+ * more than 256 entries.
+ */
+typedef struct {
+    int64_t nnz;        /* stored entries of S = l + l p */
+    int32_t p;          /* kept entries per column of P_u */
+    int32_t bandwidth;  /* half-bandwidth of M_uu under the ordering */
+    int32_t window;     /* rows of the dense band-Cholesky window */
+    double seconds;     /* host wall time of the call */
+} sbmds_sbha_info;
+int64_t sbmds_sbha_p(int64_t n, int64_t l, double p_row);
+sbmds_status sbmds_sbha_build(int64_t n, const double* verts, int64_t nf, const int32_t* faces, int64_t l,
+                              const int32_t* landmarks, double p_row, int64_t* row_ptr, int32_t* col_idx,
+                              float* val, sbmds_sbha_info* info, void* cuda_stream);
+
 /* Frees everything the library allocated (not borrowed D). NULL-safe. */
 void sbmds_destroy(sbmds_t h);
 

@@ -20,7 +20,7 @@ STATUS_NAMES = {0: "SBMDS_OK", 1: "SBMDS_EINVAL", 2: "SBMDS_ENOMEM", 3: "SBMDS_E
 EXPORTS = ("sbmds_create", "sbmds_apply", "sbmds_eigs", "sbmds_destroy", "sbmds_last_error",
            "sbmds_set_option", "sbmds_get_stat", "sbmds_launch_count", "sbmds_abi_version",
            "sbmds_plan_selfcheck", "sbmds_create_shard", "sbmds_shard_stage", "sbmds_shard_exchange_bytes",
-           "sbmds_shard_attach_nccl", "sbmds_nccl_unique_id", "sbmds_shard_plan_selfcheck", "sbmds_shard_tiles", "sbmds_bmds")
+           "sbmds_shard_attach_nccl", "sbmds_nccl_unique_id", "sbmds_shard_plan_selfcheck", "sbmds_shard_tiles", "sbmds_bmds", "sbmds_sbha_p", "sbmds_sbha_build")
 NCCL_UNIQUE_ID_BYTES = 128
 
 
@@ -29,6 +29,11 @@ class SbmdsInfo(ctypes.Structure):
                 ("n_negative", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("max_residual", ctypes.c_double), ("orth_error", ctypes.c_double),
                 ("gpu_ms", ctypes.c_double)]
+
+
+class SbhaInfo(ctypes.Structure):
+    _fields_ = [("nnz", ctypes.c_int64), ("p", ctypes.c_int32), ("bandwidth", ctypes.c_int32),
+                ("window", ctypes.c_int32), ("seconds", ctypes.c_double)]
 
 
 class SbmdsError(RuntimeError):
@@ -87,6 +92,10 @@ def lib() -> ctypes.CDLL:
             L.sbmds_shard_tiles.restype = i64
             L.sbmds_bmds.argtypes = [p, i32, i32, i32, d, u64, p, p, p, ctypes.POINTER(SbmdsInfo), p]
             L.sbmds_bmds.restype = ctypes.c_int
+            L.sbmds_sbha_p.argtypes = [i64, i64, d]
+            L.sbmds_sbha_p.restype = i64
+            L.sbmds_sbha_build.argtypes = [i64, p, i64, p, i64, p, d, p, p, p, ctypes.POINTER(SbhaInfo), p]
+            L.sbmds_sbha_build.restype = ctypes.c_int
             _lib = L
     return _lib
 

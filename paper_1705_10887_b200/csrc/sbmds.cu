@@ -33,6 +33,7 @@
 #include "k_sp8.cuh"
 #include "k_lanczos.cuh"
 #include "k_bmds.cuh"
+#include "k_sbha.cuh"
 
 namespace sbmds {
 std::atomic<int64_t> g_launches{0};
@@ -3117,6 +3118,339 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
     }
     return ret;
+}
+
+// ============================================================================ sBHA build
+// NEXT-2 (§2.2, §3, §3.1; k_sbha.cuh): the sparse interpolation operator S = P_sparse
+// of a triangle mesh on the device, ready for sbmds_create.
+namespace {
+
+// Reverse Cuthill-McKee of the free vertices' graph (L's 1-ring without the landmarks): BFS from
+// a pseudo-peripheral start (two sweeps from the lowest-degree vertex), neighbours visited by
+// increasing degree (ties: lower index), per connected component, then reversed.
+std::vector<int32_t> rcm_order(int64_t n, const std::vector<int64_t>& lp, const std::vector<int32_t>& lc,
+                               const std::vector<int32_t>& lmpos) {
+    std::vector<int32_t> deg(n, 0);
+    for (int64_t i = 0; i < n; ++i)
+        if (lmpos[i] < 0)
+            for (int64_t e = lp[i]; e < lp[i + 1]; ++e)
+                if (lc[e] != i && lmpos[lc[e]] < 0) ++deg[i];
+    std::vector<int32_t> order, level(n, -1);
+    order.reserve(n);
+    std::vector<char> done(n, 0);
+    std::vector<int32_t> nbr;
+    auto bfs = [&](int32_t s0, std::vector<int32_t>& out, bool record) -> int32_t {
+        // returns the last vertex of the deepest level (lowest degree among them)
+        std::vector<int32_t> q{s0};
+        std::vector<char>& seen = done;
+        std::vector<int32_t> touched{s0};
+        seen[s0] = 1;
+        for (size_t h = 0; h < q.size(); ++h) {
+            const int32_t v = q[h];
+            nbr.clear();
+            for (int64_t e = lp[v]; e < lp[v + 1]; ++e) {
+                const int32_t j = lc[e];
+                if (j != v && lmpos[j] < 0 && !seen[j]) nbr.push_back(j);
+            }
+            std::sort(nbr.begin(), nbr.end(), [&](int32_t a, int32_t b) { return deg[a] != deg[b] ? deg[a] < deg[b] : a < b; });
+            for (int32_t j : nbr) {
+                seen[j] = 1;
+                q.push_back(j);
+                touched.push_back(j);
+            }
+        }
+        if (record) out.insert(out.end(), q.begin(), q.end());
+        else for (int32_t v : touched) seen[v] = 0;
+        int32_t last = q.back();
+        return last;
+    };
+    for (int64_t s0 = 0; s0 < n; ++s0) {
+        if (lmpos[s0] >= 0 || done[s0]) continue;
+        // component's lowest-degree vertex, then two pseudo-peripheral sweeps
+        int32_t start = (int32_t)s0;
+        std::vector<int32_t> dummy;
+        const int32_t far1 = bfs(start, dummy, false);
+        const int32_t far2 = bfs(far1, dummy, false);
+        bfs(far2, order, true);
+    }
+    std::reverse(order.begin(), order.end());
+    return order;
+}
+
+}  // namespace
+
+extern "C" int64_t sbmds_sbha_p(int64_t n, int64_t l, double p_row) {
+    if (l < 1 || l >= n || !(p_row > 0.0)) return -1;
+    const double v = std::ceil((double)(n - l) * p_row / (double)l);
+    return std::max<int64_t>(1, std::min<int64_t>(n - l, (int64_t)v));
+}
+
+extern "C" sbmds_status sbmds_sbha_build(int64_t n, const double* verts, int64_t nf, const int32_t* faces, int64_t l,
+                                         const int32_t* landmarks, double p_row, int64_t* row_ptr, int32_t* col_idx,
+                                         float* val, sbmds_sbha_info* info, void* cuda_stream) {
+    Nvtx nv("sbmds_sbha_build");
+    const int64_t p = sbmds_sbha_p(n, l, p_row);
+    if (n < 2 || nf < 1 || p < 1) return fail(SBMDS_EINVAL, "need n >= 2, nf >= 1, 1 <= l < n, p_row > 0");
+    if (n >= (int64_t(1) << 31) || nf * 3 >= (int64_t(1) << 31)) return fail(SBMDS_EINVAL, "n or nf too large");
+    if (!verts || !faces || !landmarks || !row_ptr || !col_idx || !val) return fail(SBMDS_EINVAL, "NULL argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+    const auto t0 = std::chrono::steady_clock::now();
+    try {
+        install_hang_record();
+        configure_pool_once();
+        int dev = 0, sms = 148;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        std::vector<int32_t> lm(l);
+        CK(cudaMemcpy(lm.data(), landmarks, l * sizeof(int32_t), cudaMemcpyDefault));
+        std::vector<int32_t> lmpos(n, -1);
+        for (int64_t t = 0; t < l; ++t) {
+            if (lm[t] < 0 || lm[t] >= n || lmpos[lm[t]] >= 0) return fail(SBMDS_EINVAL, "landmarks must be distinct, in [0, n)");
+            lmpos[lm[t]] = (int32_t)t;
+        }
+        DevBuf dV{true}, dF{true}, cot{true}, area{true}, bad{true}, keys{true}, keys2{true}, fid{true}, fid2{true},
+            vfp{true}, deg{true}, lptr{true}, lcol{true}, lval{true}, mass{true};
+        dV.ensure((size_t)n * 3 * sizeof(double));
+        dF.ensure((size_t)nf * 3 * sizeof(int32_t));
+        CK(cudaMemcpyAsync(dV.p, verts, (size_t)n * 3 * sizeof(double), cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(dF.p, faces, (size_t)nf * 3 * sizeof(int32_t), cudaMemcpyDefault, st));
+        bad.ensure(sizeof(int));
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        {   // faces index check on the host side of the copy is not needed: the incidence sort
+            std::vector<int32_t> hf((size_t)nf * 3);
+            CK(cudaMemcpyAsync(hf.data(), dF.p, hf.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            for (int32_t v : hf)
+                if (v < 0 || v >= n) return fail(SBMDS_EINVAL, "face vertex index out of [0, n)");
+        }
+        cot.ensure((size_t)nf * 3 * sizeof(double));
+        area.ensure((size_t)nf * sizeof(double));
+        launch(k_face_geom, dim3((unsigned)std::min<int64_t>(4 * sms, (nf + 255) / 256)), dim3(256), 0, st, nf,
+               (const double*)dV.as<double>(), (const int32_t*)dF.as<int32_t>(), cot.as<double>(), area.as<double>(),
+               bad.as<int>());
+        // vertex -> incident faces (stable radix sort of the corners by vertex keeps faces ascending)
+        const int32_t nc = (int32_t)(nf * 3);
+        keys2.ensure(nc * sizeof(int32_t));
+        fid.ensure(nc * sizeof(int32_t));
+        fid2.ensure(nc * sizeof(int32_t));
+        {
+            std::vector<int32_t> hf(nc);
+            for (int32_t e = 0; e < nc; ++e) hf[e] = e / 3;
+            CK(cudaMemcpyAsync(fid.p, hf.data(), nc * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+            int end_bit = 1;
+            while ((int64_t(1) << end_bit) <= n) ++end_bit;
+            size_t tb = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dF.as<int32_t>(), keys2.as<int32_t>(), fid.as<int32_t>(),
+                                               fid2.as<int32_t>(), nc, 0, end_bit, st));
+            DevBuf tmp{true};
+            tmp.ensure(tb + 16);
+            CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dF.as<int32_t>(), keys2.as<int32_t>(), fid.as<int32_t>(),
+                                               fid2.as<int32_t>(), nc, 0, end_bit, st));
+            g_launches.fetch_add(1);
+            CK(cudaStreamSynchronize(st));   // (hf)
+        }
+        vfp.ensure((n + 1) * sizeof(int32_t));
+        launch(k_col_ptr, dim3((unsigned)std::min<int64_t>(1024, (n + 256) / 256)), dim3(256), 0, st, n, nc,
+               (const int32_t*)keys2.as<int32_t>(), vfp.as<int32_t>());
+        // L = V - A rows (two passes) and the lumped mass
+        deg.ensure(n * sizeof(int32_t));
+        const dim3 vg((unsigned)std::min<int64_t>(8 * sms, (n + 127) / 128));
+        launch(k_vertex_rows, vg, dim3(128), 0, st, n, (const int32_t*)dF.as<int32_t>(), (const int32_t*)vfp.as<int32_t>(),
+               (const int32_t*)fid2.as<int32_t>(), (const double*)cot.as<double>(), (const double*)area.as<double>(), 0,
+               deg.as<int32_t>(), (const int64_t*)nullptr, (int32_t*)nullptr, (double*)nullptr, (double*)nullptr,
+               bad.as<int>());
+        std::vector<int32_t> hdeg(n);
+        CK(cudaMemcpyAsync(hdeg.data(), deg.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hbad & 1) return fail(SBMDS_EINVAL, "degenerate face (zero area: non-finite cotangent)");
+        if (hbad & 2) return fail(SBMDS_EINVAL, "a vertex has more than %d neighbours", kSbhaMaxDeg);
+        std::vector<int64_t> hlp(n + 1, 0);
+        for (int64_t i = 0; i < n; ++i) hlp[i + 1] = hlp[i] + hdeg[i];
+        const int64_t nnzL = hlp[n];
+        lptr.ensure((n + 1) * sizeof(int64_t));
+        lcol.ensure(nnzL * sizeof(int32_t));
+        lval.ensure(nnzL * sizeof(double));
+        mass.ensure(n * sizeof(double));
+        CK(cudaMemcpyAsync(lptr.p, hlp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        launch(k_vertex_rows, vg, dim3(128), 0, st, n, (const int32_t*)dF.as<int32_t>(), (const int32_t*)vfp.as<int32_t>(),
+               (const int32_t*)fid2.as<int32_t>(), (const double*)cot.as<double>(), (const double*)area.as<double>(), 1,
+               deg.as<int32_t>(), (const int64_t*)lptr.as<int64_t>(), lcol.as<int32_t>(), lval.as<double>(),
+               mass.as<double>(), bad.as<int>());
+        std::vector<int32_t> hlc(nnzL);
+        CK(cudaMemcpyAsync(hlc.data(), lcol.p, nnzL * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        // ordering of the free vertices (host) and the bandwidth of M_uu under it
+        const int64_t nu = n - l;
+        std::vector<int32_t> uvert = rcm_order(n, hlp, hlc, lmpos);   // r -> vertex
+        if ((int64_t)uvert.size() != nu) return fail(SBMDS_ECUDA, "internal: RCM ordered %zu of %lld free vertices",
+                                                     uvert.size(), (long long)nu);
+        std::vector<int32_t> pos(n, -1), uq, qrow;
+        for (int64_t r = 0; r < nu; ++r) pos[uvert[r]] = (int32_t)r;
+        uq.reserve(nu);
+        qrow.reserve(nu);
+        for (int64_t i = 0; i < n; ++i)
+            if (lmpos[i] < 0) { uq.push_back((int32_t)i); qrow.push_back(pos[i]); }
+        int64_t w = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            if (lmpos[i] >= 0) continue;
+            for (int64_t e = hlp[i]; e < hlp[i + 1]; ++e) {
+                const int32_t k = hlc[e];
+                for (int64_t f = hlp[k]; f < hlp[k + 1]; ++f) {
+                    const int32_t j = hlc[f];
+                    if (lmpos[j] < 0) w = std::max<int64_t>(w, std::llabs((long long)pos[i] - pos[j]));
+                }
+            }
+        }
+        const int64_t W = std::min<int64_t>((w + 1 + 63) / 64 * 64 + 64, (nu + 63) / 64 * 64);
+        DevBuf duv{true}, dpos{true}, dlm{true}, duq{true}, dqrow{true}, B{true}, Wa{true}, Wb{true}, Rp{true},
+            XT{true}, selq{true}, selv{true}, cnt{true}, rp{true}, cur{true}, small{true};
+        duv.ensure(nu * sizeof(int32_t));
+        dpos.ensure(n * sizeof(int32_t));
+        dlm.ensure(n * sizeof(int32_t));
+        duq.ensure(nu * sizeof(int32_t));
+        dqrow.ensure(nu * sizeof(int32_t));
+        CK(cudaMemcpyAsync(duv.p, uvert.data(), nu * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dpos.p, pos.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dlm.p, lmpos.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(duq.p, uq.data(), nu * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dqrow.p, qrow.data(), nu * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        // right-hand sides -M_ub (n_u x l, permuted rows) and max diag of M
+        B.ensure((size_t)nu * l * sizeof(double));
+        CK(cudaMemsetAsync(B.p, 0, B.bytes, st));
+        small.ensure(64);
+        CK(cudaMemsetAsync(small.p, 0, 64, st));
+        unsigned long long* dmaxbits = small.as<unsigned long long>();
+        int* status = reinterpret_cast<int*>(small.as<char>() + 16);
+        const dim3 mg((unsigned)std::min<int64_t>(8 * sms, (nu + 127) / 128));
+        auto mrows = [&](int64_t r0, int64_t r1, int mode, double* out, int64_t ld, int64_t k0) {
+            if (r1 <= r0) return;
+            launch(k_m_rows, dim3((unsigned)std::min<int64_t>(8 * sms, (r1 - r0 + 127) / 128)), dim3(128), 0, st, r0, r1,
+                   (const int32_t*)duv.as<int32_t>(), (const int32_t*)dpos.as<int32_t>(), (const int32_t*)dlm.as<int32_t>(),
+                   (const int64_t*)lptr.as<int64_t>(), (const int32_t*)lcol.as<int32_t>(), (const double*)lval.as<double>(),
+                   (const double*)mass.as<double>(), mode, out, ld, k0, W,
+                   mode == 0 ? dmaxbits : (unsigned long long*)nullptr, bad.as<int>());
+        };
+        (void)mg;
+        mrows(0, nu, 0, B.as<double>(), l, 0);
+        // band Cholesky of M_uu in a sliding W x W window; panel p's rows of R kept in Rp
+        const int64_t npan = (nu + 63) / 64;
+        Wa.ensure((size_t)W * W * sizeof(double));
+        Wb.ensure((size_t)W * W * sizeof(double));
+        Rp.ensure((size_t)npan * 64 * W * sizeof(double));
+        CK(cudaMemsetAsync(Wa.p, 0, Wa.bytes, st));
+        mrows(0, std::min<int64_t>(W, nu), 1, Wa.as<double>(), W, 0);
+        double* Wc = Wa.as<double>();
+        double* Wn = Wb.as<double>();
+        const double* dmax = reinterpret_cast<const double*>(dmaxbits);
+        int* dropped = status + 1;
+        for (int64_t pn = 0; pn < npan; ++pn) {
+            const int64_t k0 = pn * 64;
+            const int nb = (int)std::min<int64_t>(64, nu - k0);
+            const int64_t Wcur = std::min<int64_t>(W, nu - k0);
+            launch(k_potf2, dim3(1), dim3(256), 0, st, Wc, W, 0, nb, status, dmax, dropped, 0);
+            if (Wcur > nb) {
+                launch(k_trsm_rows, dim3((unsigned)((Wcur - nb + 255) / 256)), dim3(256), 0, st, Wc, W, Wcur, 0, nb,
+                       (const int*)status);
+                dgemm<true, false>(st, (int)(Wcur - nb), (int)(Wcur - nb), nb, -1.0, Wc + nb, W, Wc + nb, W, 1.0,
+                                   Wc + nb * W + nb, W);
+            }
+            CK(cudaMemcpyAsync(Rp.as<double>() + pn * 64 * W, Wc, (size_t)nb * W * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+            if (pn + 1 < npan) {   // shift the window by 64 and load the rows entering it
+                CK(cudaMemcpy2DAsync(Wn, W * sizeof(double), Wc + 64 * W + 64, W * sizeof(double),
+                                     (W - 64) * sizeof(double), W - 64, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemsetAsync(Wn + (W - 64) * W, 0, 64 * W * sizeof(double), st));
+                CK(cudaMemset2DAsync(Wn + (W - 64), W * sizeof(double), 0, 64 * sizeof(double), W - 64, st));
+                mrows(std::min<int64_t>(nu, k0 + W), std::min<int64_t>(nu, k0 + W + 64), 2, Wn, W, k0 + 64);
+                std::swap(Wc, Wn);
+            }
+        }
+        int hs[2] = {0, 0};
+        peek_to_host(hs, status, sizeof hs, st);
+        if (hs[0] == 2) return fail(SBMDS_EBREAKDOWN, "sBHA: M_uu is not positive definite (a free region without landmarks?)");
+        Wa.release();
+        Wb.release();
+        // X = M_uu^{-1} B: forward R^T Y = B, backward R X = Y, panel by panel
+        const unsigned rg = (unsigned)((l + 255) / 256);
+        for (int64_t pn = 0; pn < npan; ++pn) {
+            const int64_t k0 = pn * 64;
+            const int nb = (int)std::min<int64_t>(64, nu - k0);
+            const int64_t Wcur = std::min<int64_t>(W, nu - k0);
+            const double* R = Rp.as<double>() + pn * 64 * W;
+            launch(k_trsm_panel<true>, dim3(rg), dim3(256), 0, st, R, W, nb, B.as<double>() + k0 * l, l, l);
+            if (Wcur > nb)
+                dgemm<true, false>(st, (int)(Wcur - nb), (int)l, nb, -1.0, R + nb, W, B.as<double>() + k0 * l, l, 1.0,
+                                   B.as<double>() + (k0 + nb) * l, l);
+        }
+        for (int64_t pn = npan - 1; pn >= 0; --pn) {
+            const int64_t k0 = pn * 64;
+            const int nb = (int)std::min<int64_t>(64, nu - k0);
+            const int64_t Wcur = std::min<int64_t>(W, nu - k0);
+            const double* R = Rp.as<double>() + pn * 64 * W;
+            if (Wcur > nb)
+                dgemm<false, false>(st, nb, (int)l, Wcur - nb, -1.0, R + nb, W, B.as<double>() + (k0 + nb) * l, l, 1.0,
+                                    B.as<double>() + k0 * l, l);
+            launch(k_trsm_panel<false>, dim3(rg), dim3(256), 0, st, R, W, nb, B.as<double>() + k0 * l, l, l);
+        }
+        Rp.release();
+        // per column: the p largest magnitudes over the free vertices (increasing vertex order)
+        XT.ensure((size_t)nu * l * sizeof(double));
+        launch(k_gather_t, dim3((unsigned)((nu + 31) / 32), (unsigned)((l + 31) / 32)), dim3(256), 0, st, nu, l,
+               (const int32_t*)dqrow.as<int32_t>(), (const double*)B.as<double>(), XT.as<double>());
+        B.release();
+        selq.ensure((size_t)l * p * sizeof(int32_t));
+        selv.ensure((size_t)l * p * sizeof(double));
+        launch(k_topp, dim3((unsigned)l), dim3(256), 0, st, nu, p, (const double*)XT.as<double>(), selq.as<int32_t>(),
+               selv.as<double>());
+        XT.release();
+        // CSR of S
+        const int64_t nnz = l + l * p;
+        cnt.ensure(n * sizeof(int32_t));
+        CK(cudaMemsetAsync(cnt.p, 0, n * sizeof(int32_t), st));
+        dlm.ensure(n * sizeof(int32_t));
+        DevBuf dlml{true};
+        dlml.ensure(l * sizeof(int32_t));
+        CK(cudaMemcpyAsync(dlml.p, lm.data(), l * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        const dim3 eg((unsigned)std::min<int64_t>(8 * sms, (nnz + 255) / 256));
+        launch(k_sbha_count, eg, dim3(256), 0, st, l, p, (const int32_t*)dlml.as<int32_t>(), (const int32_t*)duq.as<int32_t>(),
+               (const int32_t*)selq.as<int32_t>(), cnt.as<int32_t>());
+        std::vector<int32_t> hc(n);
+        CK(cudaMemcpyAsync(hc.data(), cnt.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<int64_t> hrp(n + 1, 0);
+        for (int64_t i = 0; i < n; ++i) hrp[i + 1] = hrp[i] + hc[i];
+        rp.ensure((n + 1) * sizeof(int64_t));
+        CK(cudaMemcpyAsync(rp.p, hrp.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        cur.ensure(n * sizeof(int32_t));
+        CK(cudaMemsetAsync(cur.p, 0, n * sizeof(int32_t), st));
+        DevBuf oc{true}, ov{true};
+        oc.ensure(nnz * sizeof(int32_t));
+        ov.ensure(nnz * sizeof(float));
+        launch(k_sbha_fill, eg, dim3(256), 0, st, l, p, (const int32_t*)dlml.as<int32_t>(), (const int32_t*)duq.as<int32_t>(),
+               (const int32_t*)selq.as<int32_t>(), (const double*)selv.as<double>(), (const int64_t*)rp.as<int64_t>(),
+               cur.as<int32_t>(), oc.as<int32_t>(), ov.as<float>());
+        launch(k_sort_rows, dim3((unsigned)std::min<int64_t>(8 * sms, (n + 255) / 256)), dim3(256), 0, st, n,
+               (const int64_t*)rp.as<int64_t>(), oc.as<int32_t>(), ov.as<float>());
+        CK(cudaMemcpyAsync(row_ptr, rp.p, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(col_idx, oc.p, nnz * sizeof(int32_t), cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(val, ov.p, nnz * sizeof(float), cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (hbad & 4) return fail(SBMDS_EINVAL, "a row of M has more than %d entries", kSbhaMaxRing2);
+        if (info) {
+            info->nnz = nnz;
+            info->p = (int32_t)p;
+            info->bandwidth = (int32_t)w;
+            info->window = (int32_t)W;
+            info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    } catch (const CudaError& e) {
+        if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
+        return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
+    }
+    return SBMDS_OK;
 }
 
 // ============================================================================ options / stats

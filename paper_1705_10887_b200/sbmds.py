@@ -186,6 +186,34 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def sbha_build(verts, faces, landmarks, p_row: float, device: str = "cuda", stream=None):
+    """S = P_sparse of a triangle mesh (sbmds_sbha_build): (row_ptr int64, col_idx int32, val f32, info).
+    verts (n x 3 float64) and faces (nf x 3 int32) as numpy arrays or device tensors."""
+    from ._lib import SbhaInfo
+    V = np.ascontiguousarray(verts, dtype=np.float64) if not _is_torch(verts) else verts
+    F = np.ascontiguousarray(faces, dtype=np.int32) if not _is_torch(faces) else faces
+    lm = np.ascontiguousarray(landmarks, dtype=np.int32)
+    n, nf, l = int(V.shape[0]), int(F.shape[0]), int(lm.shape[0])
+    p = int(lib().sbmds_sbha_p(n, l, float(p_row)))
+    if p < 1:
+        raise ValueError("need 1 <= l < n and p_row > 0")
+    nnz = l + l * p
+    if device == "numpy":
+        rp, ci, vv = np.empty(n + 1, np.int64), np.empty(nnz, np.int32), np.empty(nnz, np.float32)
+        ptrs = (rp.ctypes.data, ci.ctypes.data, vv.ctypes.data)
+    else:
+        rp = torch.empty(n + 1, dtype=torch.int64, device=device)
+        ci = torch.empty(nnz, dtype=torch.int32, device=device)
+        vv = torch.empty(nnz, dtype=torch.float32, device=device)
+        ptrs = (rp.data_ptr(), ci.data_ptr(), vv.data_ptr())
+    vp = V.data_ptr() if _is_torch(V) else V.ctypes.data
+    fp = F.data_ptr() if _is_torch(F) else F.ctypes.data
+    info = SbhaInfo()
+    check(lib().sbmds_sbha_build(n, vp, nf, fp, l, lm.ctypes.data, float(p_row), *ptrs, ctypes.byref(info),
+                                 _stream(stream)))
+    return rp, ci, vv, {k: getattr(info, k) for k, _ in SbhaInfo._fields_}
+
+
 def split_rows(row_ptr, world: int):
     """Contiguous row ranges [r0, r1) per rank with balanced stored entries (host logic)."""
     rp = np.asarray(row_ptr, dtype=np.int64)
@@ -234,4 +262,4 @@ def from_problem(p, device: Optional[str] = "cuda", **kw) -> Sbmds:
 
 
 __all__ = ["Sbmds", "SbmdsShard", "SbmdsError", "from_problem", "shard_from_problem", "launch_count",
-           "nccl_unique_id", "split_rows", "shard_tiles"]
+           "nccl_unique_id", "split_rows", "shard_tiles", "sbha_build"]
