@@ -43,6 +43,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="eigs", choices=["eigs", "apply"],
+                    help="eigs: one step = one 50-iteration sbmds_eigs (the headline); apply: one step = "
+                         "one standalone sbmds_apply of an n x b block (SURVEY §8(d) per-config lines)")
+    ap.add_argument("--b", type=int, default=0, help="apply mode: block width (default: the config's block)")
+    ap.add_argument("--k5", type=int, default=16, help="config 5: nonzeros per row of S (8, 16, 64)")
     return ap.parse_args()
 
 
@@ -83,16 +88,20 @@ def job_throughput(ws: int, units_per_rank: float, seconds_max: float) -> float:
     return ws * units_per_rank / seconds_max
 
 
-def load_problem(cfg: int, ws: int, rank: int):
+def load_problem(cfg: int, ws: int, rank: int, k5: int = 16):
     """Rank 0 generates (and caches) first; the other ranks then load the cache."""
     from gen import configs
     if rank == 0:
-        p = configs.config(cfg)
+        p = configs.config(cfg, k5=k5)
         barrier(ws)
     else:
         barrier(ws)
-        p = configs.config(cfg)
+        p = configs.config(cfg, k5=k5)
     return p
+
+
+def nnz_per_row(p) -> float:
+    return round(p.nnz / p.n, 3)
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -166,7 +175,9 @@ def run_ours(args, ws, rank, local):
     import torch
     from paper_1705_10887_b200 import from_problem, launch_count
     torch.cuda.set_device(local)
-    p = load_problem(args.config, ws, rank)
+    p = load_problem(args.config, ws, rank, args.k5)
+    if args.mode == "apply":
+        return run_apply_mode(args, ws, rank, local, p)
     m, b, iters = p.m, p.block, args.iters
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -290,11 +301,11 @@ def run_ours(args, ws, rank, local):
         "dtype": {3: "f32 (D Y1 as 24-bit fixed point on int8 tensor cores, exact int32 accumulate; DESIGN.md §4)",
                   4: "f32 (D Y1 as a 2xfp16 split, fp32 accumulate; DESIGN.md §4)"}.get(ds_path, "f32"),
         "data": "synthetic (seeded torus mesh stand-in for Dragon1800k; DESIGN.md §3)",
-        "config": {"workload": f"config {args.config}: {p.name}", "n": p.n, "l": p.l, "k": 32,
+        "config": {"workload": f"config {args.config}: {p.name}", "n": p.n, "l": p.l, "nnz_per_row": nnz_per_row(p),
                    "nnz": p.nnz, "block": b, "m": m, "iters_per_step": iters,
                    "parallelism": f"replicas x{ws}", "l2": "inputs (10 GB D) >> 126 MB L2, no flush"},
         "top_p_mds_seconds": eigs_s,
-        "apply_algorithmic_gbs": apply_gbs,
+        "apply_full_d_equivalent_gbs": apply_gbs,   # SURVEY §8(d) full-D bytes per apply / apply time
         "eigenvalues": [float(x) for x in lam],
         "max_residual": info["max_residual"], "orth_error": info["orth_error"],
         "roofline": {"bound": "hbm", "achieved": ds_gbs, "peak": hbm_peak, "unit": "GB/s",
@@ -313,6 +324,68 @@ def run_ours(args, ws, rank, local):
     if cpu:
         out["cpu_baseline"] = cpu
     return out
+
+
+def run_apply_mode(args, ws, rank, local, p):
+    """One step = one standalone sbmds_apply (the public call) of an n x b block on HBM-resident
+    inputs: the per-config operator-apply lines of SURVEY §8(d) (configs 3, 4 and the config-5
+    sweep). Roofline on the whole apply: the bytes the path it takes must move (its D stream's
+    bytes + S via CSR and CSC + X, Y + pointers) over the apply time; the D stream alone as in the
+    eigs mode."""
+    import torch
+    from gen import configs
+    from paper_1705_10887_b200 import from_problem, launch_count
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    b = args.b or p.block or 16
+    h = from_problem(p, device="cuda")
+    X = torch.from_numpy(configs.x_block(p.n, b, seed=3)).cuda()
+    Y = torch.empty_like(X)
+    st = torch.cuda.current_stream()
+    for _ in range(max(3, args.warmup)):
+        h.apply(X, out=Y)
+    torch.cuda.synchronize()
+    barrier(ws)
+    h.set_option("profile", 1 << 2)
+    h.set_option("profile_reset", 1)
+    n0 = launch_count()
+    steps = max(args.steps, 20)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0.record(st)
+        for _ in range(steps):
+            h.apply(X, out=Y)
+        e1.record(st)
+        torch.cuda.synchronize()
+    n_launch = launch_count() - n0
+    ms = e0.elapsed_time(e1)
+    ds_ns, ds_n = h.stat("dstream_ns"), h.stat("dstream_launches")
+    ds_path, ds_bytes = h.stat("dstream_path"), h.stat("dstream_bytes")
+    h.set_option("profile", 0)
+    ms_max = max_over_ranks(ms, ws, device="cuda")
+    apply_s = ms / 1e3 / steps
+    path_bytes = ds_bytes + 16 * p.nnz + 4 * (p.n + 1) + 4 * (p.l + 1) + 8 * p.n * b
+    ds_s = ds_ns / max(ds_n, 1) / 1e9
+    return {
+        "metric": "sBMDS operator applies/s (standalone sbmds_apply)", "value": job_throughput(ws, steps, ms_max / 1e3),
+        "unit": "applies/s", "n_gpus": ws, "steps": steps, "warmup": max(3, args.warmup),
+        "ms_per_step": ms_max / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config {args.config}: {p.name}", "mode": "apply", "n": p.n, "l": p.l,
+                   "nnz_per_row": nnz_per_row(p), "b": b, "parallelism": f"replicas x{ws}",
+                   "l2": "no flush: S, D and X, Y exceed the 126 MB L2 at configs 3-5"},
+        "roofline": {"bound": "hbm", "achieved": path_bytes / apply_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": path_bytes / apply_s / 1e9 / hbm_peak, "traffic": None,
+                     "kernel": "whole apply (" + DSTREAM_KERNELS.get(ds_path, str(ds_path)) + " + CSC/CSR SpMMs)",
+                     "algorithmic_bytes_per_launch": int(path_bytes)},
+        "dstream": {"kernel": DSTREAM_KERNELS.get(ds_path, str(ds_path)), "avg_launch_ms": ds_s * 1e3,
+                    "bytes_per_launch": ds_bytes, "gbs": ds_bytes / ds_s / 1e9, "frac": ds_bytes / ds_s / 1e9 / hbm_peak},
+        "apply_full_d_equivalent_gbs": algorithmic_bytes(p, b) / apply_s / 1e9,
+        "gpu_launches": int(n_launch), "clocks": clk.summary(),
+    }
 
 
 def load_traffic(path_id):

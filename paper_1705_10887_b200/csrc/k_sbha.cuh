@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(256) k_topp(int64_t nu, int64_t p, const doubl
         const bool take = gt || (eq && tie_rank < need);
         __syncthreads();
         const int ties_here = s_scan[255];
+        __syncthreads();   // (every thread has read the tie total before the array is reused)
         s_scan[threadIdx.x] = take ? 1 : 0;
         __syncthreads();
         for (int o = 1; o < 256; o <<= 1) {
