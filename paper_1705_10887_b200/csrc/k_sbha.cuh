@@ -15,7 +15,7 @@
 //                   V_i = sum_j A_ij (pass 0 counts, pass 1 writes L = V - A with the diagonal)
 //   k_m_rows        rows of M = L D^{-1} L (per row, k then j ascending: deterministic, symmetric)
 //                   scattered into the window (and its mirror) or the right-hand sides -M_ub
-//   k_trsm_fwd/bwd  64 x 64 triangular solves with R_kk for all l right-hand sides
+//   k_trsm_panel    64 x 64 triangular solves with R_kk (forward / backward) for all l right-hand sides
 //   k_gather_t      X (permuted rows x l) -> XT (l x free vertices in increasing order)
 //   k_topp          per column: radix select of the p-th largest |x|, ties to the lowest row
 //   k_sbha_count / k_sbha_fill / k_sort_rows   the CSR of S (landmark rows e_t + kept entries)
