@@ -55,7 +55,12 @@ enum {
     /* Full input checks at create: row_ptr monotone with row_ptr[0] = 0 and
        row_ptr[n] = nnz, 0 <= col_idx < l, all values finite, D symmetric
        (|D_ij - D_ji| <= 1e-6 max|D|). Without it only sizes are checked. */
-    SBMDS_VALIDATE = 1u << 1
+    SBMDS_VALIDATE = 1u << 1,
+    /* Keep S's rows in the caller's order. By default create sorts the rows by their two
+       smallest column indices and keeps that order internally when sampled 128-row blocks then
+       touch < 3/4 of the landmarks (stat "row_permuted"); X, Y, X0, V and Z always use the
+       caller's order (the handle permutes at the boundary, DESIGN.md §4 "Row order"). */
+    SBMDS_NATURAL_ORDER = 1u << 2
 };
 
 typedef struct {
@@ -82,6 +87,9 @@ typedef struct {
  * The library copies S (and D unless borrowed) into device memory it owns, builds a
  * row-sorted CSC copy of S on the device (for S^T X without atomics) and the vector
  * w = S^T 1 / n used by the rank-one centring (J S = S - 1 w^T).
+ * With a host D large enough for the int8 stream, create returns while that stream's packing of
+ * D (and max |D|) may still run on a handle-owned stream: every later D-stream launch waits on its
+ * event until it has completed, and a fault in it is reported by the call that first waits.
  * Returns SBMDS_OK and *out, or an error with *out = NULL.
  */
 sbmds_status sbmds_create(int64_t n, int64_t l, int64_t nnz, const int64_t* row_ptr,

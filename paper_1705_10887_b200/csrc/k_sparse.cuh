@@ -391,4 +391,93 @@ __global__ void __launch_bounds__(256) k_spmm_csr_sub(
     }
 }
 
+// ------------------------------------------------------------------ row order (create)
+// S's rows are reordered at create when that makes 128-row blocks touch fewer landmarks
+// (sbmds.cu reorder_rows; DESIGN.md §4 "Row order"). Key of a row: its two smallest column
+// indices (c0 << 32 | c1): rows sharing their lowest landmarks are adjacent, and since FPS
+// landmark indices are coarse-to-fine, the order is a hierarchy of landmark neighbourhoods.
+__global__ void k_row_keys(int64_t n, int64_t l, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                           uint64_t* __restrict__ keys, int32_t* __restrict__ iota) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t c0 = (uint32_t)l, c1 = (uint32_t)l;   // (an empty row sorts last)
+        for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+            const uint32_t c = (uint32_t)col[e];
+            if (c < c0) { c1 = c0; c0 = c; }
+            else if (c < c1 && c != c0) c1 = c;
+        }
+        if (c1 == (uint32_t)l) c1 = c0;
+        keys[i] = ((uint64_t)c0 << 32) | c1;
+        iota[i] = (int32_t)i;
+    }
+}
+
+// Distinct columns of sampled 128-row blocks (block s * stride) in the natural (perm = null) or
+// a permuted order: a bitmap of l bits in shared memory per block.
+__global__ void __launch_bounds__(256) k_block_distinct(int64_t n, int64_t l, int64_t stride, const int32_t* __restrict__ perm,
+                                                        const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                        int32_t* __restrict__ counts) {
+    extern __shared__ unsigned int bits[];
+    const int64_t words = (l + 31) / 32;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) bits[w] = 0u;
+    __syncthreads();
+    const int64_t r0 = blockIdx.x * stride * 128;
+    for (int rr = threadIdx.x / 8; rr < 128; rr += blockDim.x / 8) {
+        const int64_t r = r0 + rr;
+        if (r >= n) break;
+        const int64_t i = perm ? perm[r] : r;
+        for (int32_t e = rp[i] + (threadIdx.x & 7); e < rp[i + 1]; e += 8) {
+            const uint32_t c = (uint32_t)col[e];
+            atomicOr(&bits[c >> 5], 1u << (c & 31));
+        }
+    }
+    __syncthreads();
+    int cnt = 0;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) cnt += __popc(bits[w]);
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    __shared__ int red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int q = 0; q < 8; ++q) t += red[q];
+        counts[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_perm_lengths(int64_t n, const int32_t* __restrict__ perm, const int32_t* __restrict__ rp,
+                               int32_t* __restrict__ len) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        len[r] = rp[perm[r] + 1] - rp[perm[r]];
+}
+
+// new row r = old row perm[r] (one warp per row)
+__global__ void __launch_bounds__(256) k_perm_rows(int64_t n, const int32_t* __restrict__ perm,
+                                                   const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                   const float* __restrict__ val, const int32_t* __restrict__ nrp,
+                                                   int32_t* __restrict__ ncol, float* __restrict__ nval) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t i = perm[r], b0 = rp[i], len = rp[i + 1] - b0, d0 = nrp[r];
+        for (int e = lane; e < len; e += 32) {
+            ncol[d0 + e] = col[b0 + e];
+            nval[d0 + e] = val[b0 + e];
+        }
+    }
+}
+
+// n x b blocks between the caller's row order and the handle's: out[r] = in[perm[r]] (gather)
+// or out[perm[r]] = in[r] (scatter); one thread per element, rows of b contiguous floats.
+template <bool SCATTER>
+__global__ void k_permute_rows(int64_t n, int b, const int32_t* __restrict__ perm, const float* __restrict__ in,
+                               float* __restrict__ out) {
+    const int64_t total = n * b;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / b, c = e - r * b;
+        const int64_t i = perm[r];
+        if (SCATTER) out[i * b + c] = in[e];
+        else out[e] = in[i * b + c];
+    }
+}
+
 }  // namespace sbmds

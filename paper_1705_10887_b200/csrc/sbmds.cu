@@ -461,6 +461,11 @@ struct sbmds_ctx {
     bool shard = false;
     void* comm = nullptr;
     DevBuf vg;                 // shard: v_g = D w_g (t_g = v_g^T Y1, formed at the first stage 2)
+    // row order (reorder_rows): the handle keeps S's rows permuted when 128-row blocks then touch
+    // fewer landmarks; perm[r] = caller's row of handle row r. X / Y / V cross it at the ABI.
+    bool permuted = false;
+    DevBuf perm, xperm, yperm;
+    int64_t order_distinct[2] = {0, 0};   // sampled blocks' distinct columns: natural, permuted
     bool vg_ok = false;
     int dev = 0, num_sms = 148;
     // S (CSR) and its device-built CSC copy
@@ -1807,7 +1812,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->vg, &h->foldscr, &h->s8trace,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
@@ -1852,6 +1857,91 @@ void destroy_ctx(sbmds_ctx* h) {
 
 // ============================================================================ create
 namespace {
+// Row order (DESIGN.md §4 "Row order"): sort S's rows by their two smallest column indices and
+// keep the permuted order when sampled 128-row blocks then touch < 3/4 of the distinct landmarks
+// they touch in the caller's order (torus grids keep theirs; the icosphere and the random-window
+// rows of config 5 do not). The CSR is rewritten in place; h->perm maps back.
+void reorder_rows(sbmds_ctx* h, cudaStream_t st) {
+    const int64_t n = h->n, l = h->l, nnz = h->nnz;
+    const int64_t nblk = (n + 127) / 128;
+    if (nblk < 4 || nnz == 0) return;
+    DevBuf keys{true}, keys2{true}, iota{true}, perm{true}, tot{true};
+    keys.ensure(n * sizeof(uint64_t));
+    keys2.ensure(n * sizeof(uint64_t));
+    iota.ensure(n * sizeof(int32_t));
+    perm.ensure(n * sizeof(int32_t));
+    launch(k_row_keys, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, (n + 255) / 256)), dim3(256), 0, st,
+           n, l, (const int32_t*)h->rp.as<int32_t>(), (const int32_t*)h->col.as<int32_t>(), keys.as<uint64_t>(),
+           iota.as<int32_t>());
+    int lbits = 1;
+    while ((int64_t(1) << lbits) <= l) ++lbits;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint64_t>(), keys2.as<uint64_t>(), iota.as<int32_t>(),
+                                       perm.as<int32_t>(), (int)n, 0, 32 + lbits, st));
+    DevBuf tmp{true};
+    tmp.ensure(tb + 16);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint64_t>(), keys2.as<uint64_t>(), iota.as<int32_t>(),
+                                       perm.as<int32_t>(), (int)n, 0, 32 + lbits, st));
+    g_launches.fetch_add(1);
+    const int64_t stride = std::max<int64_t>(1, nblk / 1024);
+    const int64_t ns = (nblk + stride - 1) / stride;
+    tot.ensure(2 * ns * sizeof(int32_t));
+    const size_t smem = (size_t)((l + 31) / 32) * sizeof(unsigned int);
+    if (smem > 48 * 1024) smem_attr(k_block_distinct, (int)smem);
+    launch(k_block_distinct, dim3((unsigned)ns), dim3(256), smem, st, n, l, stride, (const int32_t*)nullptr,
+           (const int32_t*)h->rp.as<int32_t>(), (const int32_t*)h->col.as<int32_t>(), tot.as<int32_t>());
+    launch(k_block_distinct, dim3((unsigned)ns), dim3(256), smem, st, n, l, stride, (const int32_t*)perm.as<int32_t>(),
+           (const int32_t*)h->rp.as<int32_t>(), (const int32_t*)h->col.as<int32_t>(), tot.as<int32_t>() + ns);
+    std::vector<int32_t> hc(2 * ns);
+    for (int64_t o = 0; o < 2 * ns; o += 1024)   // (small readbacks through the mapped buffer)
+        peek_to_host(hc.data() + o, tot.as<int32_t>() + o, (size_t)std::min<int64_t>(1024, 2 * ns - o) * 4, st);
+    int64_t nat = 0, prm = 0;
+    for (int64_t q = 0; q < ns; ++q) { nat += hc[q]; prm += hc[ns + q]; }
+    h->order_distinct[0] = nat;
+    h->order_distinct[1] = prm;
+    if (4 * prm >= 3 * nat) return;
+    // rewrite the CSR in the new row order
+    DevBuf len{true}, nrp{true}, ncol{true}, nval{true};
+    len.ensure((n + 1) * sizeof(int32_t));
+    CK(cudaMemsetAsync(len.as<int32_t>() + n, 0, sizeof(int32_t), st));
+    launch(k_perm_lengths, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, (n + 255) / 256)), dim3(256), 0, st,
+           n, (const int32_t*)perm.as<int32_t>(), (const int32_t*)h->rp.as<int32_t>(), len.as<int32_t>());
+    nrp.ensure((n + 1) * sizeof(int32_t));
+    ncol.ensure(nnz * sizeof(int32_t));
+    nval.ensure(nnz * sizeof(float));
+    tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.as<int32_t>(), nrp.as<int32_t>(), (int)(n + 1), st));
+    tmp.ensure(tb + 16);
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, len.as<int32_t>(), nrp.as<int32_t>(), (int)(n + 1), st));
+    g_launches.fetch_add(1);
+    launch(k_perm_rows, dim3((unsigned)std::min<int64_t>(16 * (int64_t)h->num_sms, (n + 7) / 8)), dim3(256), 0, st, n,
+           (const int32_t*)perm.as<int32_t>(), (const int32_t*)h->rp.as<int32_t>(), (const int32_t*)h->col.as<int32_t>(),
+           (const float*)h->val.as<float>(), (const int32_t*)nrp.as<int32_t>(), ncol.as<int32_t>(), nval.as<float>());
+    CK(cudaStreamSynchronize(st));
+    h->rp.swap(nrp);
+    h->col.swap(ncol);
+    h->val.swap(nval);
+    h->perm.swap(perm);
+    h->permuted = true;
+}
+
+// n x b block between the caller's row order and the handle's (no-op copies avoided by callers)
+void permute_block(sbmds_ctx* h, int b, const float* in, float* out, bool scatter, cudaStream_t st) {
+    const int64_t total = h->n * b;
+    const dim3 g((unsigned)std::min<int64_t>(16 * (int64_t)h->num_sms, (total + 255) / 256));
+    if (scatter) launch(k_permute_rows<true>, g, dim3(256), 0, st, h->n, b, (const int32_t*)h->perm.as<int32_t>(), in, out);
+    else launch(k_permute_rows<false>, g, dim3(256), 0, st, h->n, b, (const int32_t*)h->perm.as<int32_t>(), in, out);
+}
+
+// V (n x m, handle order, in place) -> the caller's order, before the sign rule (ties: lowest
+// caller index) and Z
+void unpermute_v(sbmds_ctx* h, int m, float* V, cudaStream_t st) {
+    if (!h->permuted) return;
+    h->yperm.ensure((size_t)h->n * m * sizeof(float));
+    permute_block(h, m, V, h->yperm.as<float>(), true, st);
+    CK(cudaMemcpyAsync(V, h->yperm.p, (size_t)h->n * m * sizeof(float), cudaMemcpyDeviceToDevice, st));
+}
+
 sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, int world, int64_t l, int64_t nnz,
                          const int64_t* row_ptr, const int32_t* col_idx, const float* val, const float* D_ll,
                          uint32_t flags, void* cuda_stream, sbmds_t* out, bool create_as_shard = false) {
@@ -2032,6 +2122,14 @@ sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, in
             if (hbad) {
                 join_dside(); destroy_ctx(h);
                 return fail(SBMDS_EINVAL, "col_idx out of [0, l) or non-finite val");
+            }
+            if (!create_as_shard && !(flags & SBMDS_NATURAL_ORDER)) {
+                reorder_rows(h, st);
+                if (h->permuted)   // (the row of every entry, in the new order)
+                    launch(k_expand_rows, dim3(1024), dim3(256), 0, st, n, (const int32_t*)h->rp.as<int32_t>(),
+                           (const int32_t*)h->col.as<int32_t>(), (const float*)h->val.as<float>(), l,
+                           tmpA.as<int32_t>(), bad);
+                tphase("row order decided");
             }
             tmpB.ensure(2 * (size_t)nnz * sizeof(int32_t));  // iota | sorted perm
             tmpC.ensure((size_t)nnz * sizeof(int32_t));      // sorted keys
@@ -2248,6 +2346,14 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
             Yd = h->yhost.as<float>();
         }
         ensure_dq(h, st);   // the int8 stream's precision check (once per handle)
+        float* Yuser = Yd;
+        if (h->permuted) {   // caller's row order -> the handle's (and back below)
+            h->xperm.ensure(bytes);
+            h->yperm.ensure(bytes);
+            permute_block(h, b, Xd, h->xperm.as<float>(), false, st);
+            Xd = h->xperm.as<float>();
+            Yd = h->yperm.as<float>();
+        }
         if (h->shard) {
             if (!h->center) return fail(SBMDS_EINVAL, "a shard handle applies the centred operator only");
             if (h->comm) shard_apply_nccl(h, b, Xd, Yd, st);
@@ -2275,7 +2381,8 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
             h->raw_now = false;
             CK(cudaStreamSynchronize(st));   // m2 (host) must outlive its copy
         }
-        if (!yd) CK(cudaMemcpyAsync(Y, Yd, bytes, cudaMemcpyDeviceToHost, st));
+        if (h->permuted) permute_block(h, b, Yd, Yuser, true, st);
+        if (!yd) CK(cudaMemcpyAsync(Y, Yuser, bytes, cudaMemcpyDeviceToHost, st));
         if (!xd || !yd) CK(cudaStreamSynchronize(st));
     } catch (const CudaError& e) {
         if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
@@ -2564,7 +2671,14 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
         if (hs == 2) throw LanczosBreakdown{where};
     };
     // Q_0 = orth(X0) (Cholesky-QR twice)
-    if (X0) CK(cudaMemcpyAsync(W, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
+    if (X0) {
+        CK(cudaMemcpyAsync(W, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
+        if (h->permuted) {
+            h->xperm.ensure((size_t)n * b * sizeof(float));
+            CK(cudaMemcpyAsync(h->xperm.p, W, (size_t)n * b * sizeof(float), cudaMemcpyDeviceToDevice, st));
+            permute_block(h, b, h->xperm.as<float>(), W, false, st);
+        }
+    }
     else launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, W);
     cholqr(W, tmp, h->lzR.as<double>());
     cholqr(tmp, Qj(0), h->lzR.as<double>());
@@ -2623,6 +2737,7 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
     float* Vd = vdev ? V : (h->vtmp.ensure(vbytes), h->vtmp.as<float>());
     float* Zd = zdev ? Z : (Z ? (h->ztmp.ensure(vbytes), h->ztmp.as<float>()) : nullptr);
     combine(k, m, kb, h->rr.as<RrOut>()->U, nullptr, 1.0, Vd);
+    unpermute_v(h, m, Vd, st);
     h->sign.ensure(kMaxB * sizeof(float));
     h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
     h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
@@ -2727,6 +2842,11 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         float* Yn = h->Y.as<float>();
         // E1: initial block Y_0 (Philox N(0,1) or the warm start), G_0, s_0, R_0^{-1}
         if (X0) {
+            if (h->permuted) {   // warm start in the caller's order -> the handle's
+                h->xperm.ensure((size_t)n * b * sizeof(float));
+                CK(cudaMemcpyAsync(h->xperm.p, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
+                permute_block(h, b, h->xperm.as<float>(), Yc, false, st);
+            } else
             CK(cudaMemcpyAsync(Yc, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
         } else {
             launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, Yc);
@@ -2894,6 +3014,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         const double* theta = Msel_d + (size_t)b * m + m;
         rotate(h, b, m, m, (const float*)Yc, (const double*)Msel_d, Vd, (const double*)(Msel_d + (size_t)b * m),
                false, st);
+        unpermute_v(h, m, Vd, st);
         h->sign.ensure(kMaxB * sizeof(float));
         h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
         h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
@@ -3077,6 +3198,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         const size_t vbytes = (size_t)n * m * sizeof(float);
         float* Vd = V ? V : (h->vtmp.ensure(vbytes), h->vtmp.as<float>());
         spmm_csr(h, m, bp, Vd, st);
+        unpermute_v(h, m, Vd, st);
         h->sign.ensure(kMaxB * sizeof(float));
         h->apval.ensure(kRedBlocks * kMaxB * sizeof(float));
         h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
@@ -3543,6 +3665,9 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a, -2 precision check
     else if (!strcmp(key, "sp8_range")) *value = h->sp8_range;          // its binade range (-1 not built)
     else if (!strcmp(key, "chol_retries")) *value = h->chol_retries;
+    else if (!strcmp(key, "row_permuted")) *value = h->permuted ? 1 : 0;     // create kept a reordered S
+    else if (!strcmp(key, "order_distinct_natural")) *value = h->order_distinct[0];
+    else if (!strcmp(key, "order_distinct_permuted")) *value = h->order_distinct[1];
     else if (!strcmp(key, "bmds_dropped")) *value = h->bmds_dropped;  // last BMDS: rank deficiency of J P
     else if (!strcmp(key, "y_fallbacks")) *value = h->y_fallbacks;    // standalone applies sent to the fp32-grade stream  // last eigs: shifted Cholesky retries seen
     else if (!strcmp(key, "dq_state")) *value = h->dq_state;            // int8 D stream check: 1 kept, -1 fell back, 0 undecided
