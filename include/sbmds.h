@@ -56,11 +56,12 @@ enum {
        row_ptr[n] = nnz, 0 <= col_idx < l, all values finite, D symmetric
        (|D_ij - D_ji| <= 1e-6 max|D|). Without it only sizes are checked. */
     SBMDS_VALIDATE = 1u << 1,
-    /* Keep S's rows in the caller's order. By default create sorts the rows by their two
-       smallest column indices and keeps that order internally when sampled 128-row blocks then
-       touch < 3/4 of the landmarks (stat "row_permuted"); X, Y, X0, V and Z always use the
-       caller's order (the handle permutes at the boundary, DESIGN.md §4 "Row order"). */
-    SBMDS_NATURAL_ORDER = 1u << 2
+    /* Let create reorder S's rows: sorted by their two smallest column indices, the order is
+       kept internally when sampled 128-row blocks then touch < 3/4 of the landmarks (stat
+       "row_permuted"); X, Y, X0, V and Z keep the caller's order (the handle permutes at the
+       boundary). Off by default: measured slower with the current sparse kernels on every
+       config (DESIGN.md §4 "Row order"). */
+    SBMDS_REORDER_ROWS = 1u << 2
 };
 
 typedef struct {

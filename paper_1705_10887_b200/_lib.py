@@ -13,7 +13,7 @@ _lib = None
 SBMDS_OK, SBMDS_EINVAL, SBMDS_ENOMEM, SBMDS_ECUDA, SBMDS_ENOCONV, SBMDS_EBREAKDOWN = range(6)
 SBMDS_BORROW_D = 1 << 0
 SBMDS_VALIDATE = 1 << 1
-SBMDS_NATURAL_ORDER = 1 << 2
+SBMDS_REORDER_ROWS = 1 << 2
 STATUS_NAMES = {0: "SBMDS_OK", 1: "SBMDS_EINVAL", 2: "SBMDS_ENOMEM", 3: "SBMDS_ECUDA",
                 4: "SBMDS_ENOCONV", 5: "SBMDS_EBREAKDOWN"}
 

@@ -2123,7 +2123,7 @@ sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, in
                 join_dside(); destroy_ctx(h);
                 return fail(SBMDS_EINVAL, "col_idx out of [0, l) or non-finite val");
             }
-            if (!create_as_shard && !(flags & SBMDS_NATURAL_ORDER)) {
+            if (!create_as_shard && (flags & SBMDS_REORDER_ROWS)) {
                 reorder_rows(h, st);
                 if (h->permuted)   // (the row of every entry, in the new order)
                     launch(k_expand_rows, dim3(1024), dim3(256), 0, st, n, (const int32_t*)h->rp.as<int32_t>(),

@@ -13,8 +13,8 @@ from typing import Optional
 
 import numpy as np
 
-from ._lib import (NCCL_UNIQUE_ID_BYTES, SBMDS_BORROW_D, SBMDS_ENOCONV, SBMDS_VALIDATE, SbmdsError, SbmdsInfo,
-                   check, lib)
+from ._lib import (NCCL_UNIQUE_ID_BYTES, SBMDS_BORROW_D, SBMDS_ENOCONV, SBMDS_REORDER_ROWS, SBMDS_VALIDATE,
+                   SbmdsError, SbmdsInfo, check, lib)
 
 try:
     import torch
@@ -58,10 +58,11 @@ class Sbmds:
     """
 
     def __init__(self, n: int, l: int, row_ptr, col_idx, val, D, *, validate: bool = False,
-                 borrow_d: bool = False, stream=None):
+                 borrow_d: bool = False, reorder_rows: bool = False, stream=None):
         self.n, self.l = int(n), int(l)
         nnz = int(row_ptr[-1])
-        flags = (SBMDS_VALIDATE if validate else 0) | (SBMDS_BORROW_D if borrow_d else 0)
+        flags = ((SBMDS_VALIDATE if validate else 0) | (SBMDS_BORROW_D if borrow_d else 0) |
+                 (SBMDS_REORDER_ROWS if reorder_rows else 0))
         self._keep = (row_ptr, col_idx, val, D) if borrow_d else ()
         h = ctypes.c_void_p()
         check(lib().sbmds_create(self.n, self.l, nnz, _ptr(row_ptr, np.int64),

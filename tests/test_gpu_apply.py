@@ -388,3 +388,30 @@ def test_host_d_pack_issued_in_create():
     assert np.array_equal(Yh, Yd)
     assert np.array_equal(np.asarray(lam_h), np.asarray(lam_d))
     assert relerr(Yh, ref) <= TOL
+
+
+@pytest.mark.parametrize("cfgname", ["random", "config3_like"])
+def test_reordered_rows_keep_the_callers_order(cfgname):
+    """SBMDS_REORDER_ROWS: the handle keeps S's rows in its own order (here a real permutation:
+    random-window rows reorder), X / Y / X0 / V / Z stay in the caller's order. Apply, eigs (with a
+    warm start) and BMDS agree with the oracle and with a natural-order handle."""
+    import torch
+    if cfgname == "random":
+        p = configs.random_problem(60_001, 2_003, 16, seed=77, name="cfg5_small")
+    else:
+        p = synth_problem(n=20_000, l=700, k=10, seed=78)
+    X = configs.x_block(p.n, 16, seed=5)
+    ref = oracle_apply(p, X)
+    with make_handle(p, reorder_rows=True) as hr, make_handle(p) as hn:
+        assert hr.stat("row_permuted") == 1 and hn.stat("row_permuted") == 0
+        Yr = run_apply(hr, X)
+        lam_r, V_r, Z_r, _ = hr.eigs(3, 16, max_iters=300, tol=1e-6)
+        lam_n, V_n, Z_n, _ = hn.eigs(3, 16, max_iters=300, tol=1e-6)
+        X0 = torch.from_numpy(configs.x_block(p.n, 16, seed=9)).cuda()
+        lam_w, V_w, _, _ = hr.eigs(3, 16, max_iters=300, tol=1e-6, X0=X0)
+    assert relerr(Yr, ref) <= TOL
+    assert np.allclose(lam_r, lam_n, rtol=1e-5) and np.allclose(lam_w, lam_n, rtol=1e-5)
+    Vr, Vn = V_r.cpu().numpy().astype(np.float64), V_n.cpu().numpy().astype(np.float64)
+    assert O.principal_angle(Vr, Vn) <= 1e-3
+    for j in range(3):                              # the sign rule in the caller's row order
+        assert Vr[np.argmax(np.abs(Vr[:, j])), j] > 0
