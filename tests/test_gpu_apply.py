@@ -390,7 +390,7 @@ def test_host_d_pack_issued_in_create():
     assert relerr(Yh, ref) <= TOL
 
 
-@pytest.mark.parametrize("cfgname", ["random", "config3_like"])
+@pytest.mark.parametrize("cfgname", ["random", "narrow_window"])
 def test_reordered_rows_keep_the_callers_order(cfgname):
     """SBMDS_REORDER_ROWS: the handle keeps S's rows in its own order (here a real permutation:
     random-window rows reorder), X / Y / X0 / V / Z stay in the caller's order. Apply, eigs (with a
@@ -399,7 +399,7 @@ def test_reordered_rows_keep_the_callers_order(cfgname):
     if cfgname == "random":
         p = configs.random_problem(60_001, 2_003, 16, seed=77, name="cfg5_small")
     else:
-        p = synth_problem(n=20_000, l=700, k=10, seed=78)
+        p = configs.random_problem(30_011, 1_029, 8, seed=78, window=100, name="narrow")
     X = configs.x_block(p.n, 16, seed=5)
     ref = oracle_apply(p, X)
     with make_handle(p, reorder_rows=True) as hr, make_handle(p) as hn:
