@@ -372,6 +372,81 @@ __global__ void __launch_bounds__(256) k_chol(int b, const double* __restrict__ 
     chol_block(b, G, Rinv, status, A, &fail, &shift);
 }
 
+// k_chol for wider blocks (b > 16; round 2): the whole block factors, one barrier-separated
+// step per pivot (the trailing update spread over all threads), and R^{-1} row by row from the
+// bottom (row i of X = R^{-1} is final once the rows below it are; each step then adds
+// R[j][i] X[i][c] into the rows j < i, all (j, c) in parallel). Same status and shifted retry as
+// chol_block; deterministic (one thread per element and step). At b = 32 the warp-0 form of
+// chol_block took ~0.07 ms (its triangular index decode is O(b) per element per step).
+constexpr int kCholParSmem = 2 * kMaxB * (kMaxB + 1) * sizeof(double);
+__global__ void __launch_bounds__(256) k_chol_par(int b, const double* __restrict__ G, double* __restrict__ Rinv,
+                                                  int* __restrict__ status) {
+    extern __shared__ double chol_smem[];
+    double (*A)[kMaxB + 1] = reinterpret_cast<double (*)[kMaxB + 1]>(chol_smem);
+    double (*X)[kMaxB + 1] = reinterpret_cast<double (*)[kMaxB + 1]>(chol_smem + kMaxB * (kMaxB + 1));
+    __shared__ int fail;
+    __shared__ double shift;
+    const int tid = threadIdx.x;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        for (int e = tid; e < b * b; e += blockDim.x) {
+            const int i = e / b, j = e % b;
+            A[i][j] = 0.5 * (G[i * b + j] + G[j * b + i]);
+        }
+        if (tid == 0) {
+            fail = 0;
+            double tr = 0.0;
+            for (int i = 0; i < b; ++i) tr += fabs(G[i * b + i]);
+            shift = attempt == 0 ? 0.0 : 1e-13 * tr;
+        }
+        __syncthreads();
+        if (attempt == 1 && tid < b) A[tid][tid] += shift;
+        __syncthreads();
+        for (int k = 0; k < b; ++k) {
+            const double d = A[k][k];
+            if (!(d > 0.0) || !isfinite(d)) {   // (every thread reads the same value)
+                if (tid == 0) fail = 1;
+                break;
+            }
+            const double r = sqrt(d), ri = 1.0 / r;
+            __syncthreads();   // A[k][k] read by all
+            for (int j = k + 1 + tid; j < b; j += blockDim.x) A[k][j] *= ri;
+            if (tid == 0) A[k][k] = r;
+            __syncthreads();
+            const int m = b - k - 1;
+            for (int e = tid; e < m * m; e += blockDim.x) {
+                const int i = k + 1 + e / m, j = k + 1 + e % m;
+                if (j >= i) A[i][j] = fma(-A[k][i], A[k][j], A[i][j]);
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (!fail) break;
+        __syncthreads();
+    }
+    if (fail) {
+        if (tid == 0) *status = 2;
+        return;
+    }
+    for (int e = tid; e < b * b; e += blockDim.x) X[e / b][e % b] = 0.0;
+    __syncthreads();
+    for (int i = b - 1; i >= 0; --i) {
+        const double rii = 1.0 / A[i][i];
+        for (int c = i + tid; c < b; c += blockDim.x) X[i][c] = ((c == i ? 1.0 : 0.0) - X[i][c]) * rii;
+        __syncthreads();
+        const int w = b - i;   // columns c in [i, b)
+        for (int e = tid; e < i * w; e += blockDim.x) {
+            const int j = e / w, c = i + e % w;
+            X[j][c] = fma(A[j][i], X[i][c], X[j][c]);
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < b * b; e += blockDim.x) {
+        const int i = e / b, c = e % b;
+        Rinv[e] = c >= i ? X[i][c] : 0.0;
+    }
+    if (tid == 0) *status = (shift > 0.0) ? 1 : 0;
+}
+
 // ------------------------------------------------------------------ E5: Rayleigh-Ritz
 constexpr int kRrSmem = 2 * kMaxB * (kMaxB + 1) * sizeof(double);
 

@@ -2607,10 +2607,20 @@ void rotate(sbmds_ctx* h, int b, int mo, int ldm, const float* in, const double*
 
 // R^-1 from G = Y^T Y = R^T R (status read later). The orthonormal X = Y R^-1 is never
 // formed: the next apply folds R^-1 into its l x b stage.
+// G = R^T R -> Rinv (b x b): the warp form up to b = 16 (also run inside the sparse step and
+// the fold), the block-parallel one above
+void chol_launch(int b, const double* G, double* Rinv, int* status, cudaStream_t st) {
+    if (b <= 16) {
+        launch(k_chol, dim3(1), dim3(256), 0, st, b, G, Rinv, status);
+    } else {
+        smem_attr(k_chol_par, kCholParSmem);
+        launch(k_chol_par, dim3(1), dim3(256), (size_t)kCholParSmem, st, b, G, Rinv, status);
+    }
+}
+
 void chol(sbmds_ctx* h, int b, cudaStream_t st) {
     profiled(h->prof, PK_CHOL, st, [&] {
-        launch(k_chol, dim3(1), dim3(256), 0, st, b, (const double*)h->G.as<double>(), h->Rinv.as<double>(),
-               h->status.as<int>());
+        chol_launch(b, (const double*)h->G.as<double>(), h->Rinv.as<double>(), h->status.as<int>(), st);
     });
 }
 
@@ -3155,7 +3165,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         launch(k_dinit, dim3(64), dim3(256), 0, st, l * b, (uint64_t)seed, Y.as<double>());
         auto orth = [&](double* Yin, double* Xout) {   // Xout = Yin R^-1, Yin^T Yin = R^T R
             dgemm<true, false>(st, b, b, l, 1.0, Yin, b, Yin, b, 0.0, Gs, b);
-            launch(k_chol, dim3(1), dim3(256), 0, st, b, (const double*)Gs, h->Rinv.as<double>(), status);
+            chol_launch(b, (const double*)Gs, h->Rinv.as<double>(), status, st);
             dgemm<false, false>(st, (int)l, b, b, 1.0, Yin, b, h->Rinv.as<double>(), b, 0.0, Xout, b);
         };
         orth(Y.as<double>(), X.as<double>());
