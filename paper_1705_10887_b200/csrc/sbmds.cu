@@ -1398,6 +1398,17 @@ void ycheck(sbmds_ctx* h, int b, int bp, cudaStream_t st) {
     }
 }
 
+// A1: s = 1^T X (fp64, fixed order): float4 loads where b % 4 == 0 and X is 16-byte aligned
+void colsum(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
+    const unsigned grid = (unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256);
+    if (b % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0)
+        launch(k_colsum4, dim3(grid), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(), h->s.as<double>(),
+               h->counters.as<unsigned int>() + CNT_COLSUM);
+    else
+        launch(k_colsum, dim3(grid), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(), h->s.as<double>(),
+               h->counters.as<unsigned int>() + CNT_COLSUM);
+}
+
 // The whole operator apply on device buffers (stream-ordered; the standalone apply on the int8
 // stream reads Y1's column check back once, see ycheck).
 // Fused-step flags (eigs only, row-blocked S, b in {4, 8, 16, 32}):
@@ -1494,11 +1505,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     const int bp = next_pow2(b);
     ensure_apply_ws(h, bp);
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
-    if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] {
-        launch(k_colsum, dim3((unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256)), dim3(256), 0, st,
-               h->n, b, X, h->colpart.as<double>(),
-               h->s.as<double>(), h->counters.as<unsigned int>() + CNT_COLSUM);
-    });
+    if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] { colsum(h, b, X, st); });
     const bool blk = blocked_ok(h, b, bp, X, Y);
     if (blk) {
         // opt the blocked kernels into > 48 KB of dynamic smem (once per device)
@@ -2419,8 +2426,7 @@ void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void*
     ensure_apply_ws(h, bp);
     const int64_t l = h->l;
     if (stage == 0) {
-        launch(k_colsum, dim3((unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256)), dim3(256), 0, st,
-               h->n, b, X, h->colpart.as<double>(), h->s.as<double>(), h->counters.as<unsigned int>() + CNT_COLSUM);
+        colsum(h, b, X, st);
         if (exch_out) CK(cudaMemcpyAsync(exch_out, h->s.p, (size_t)b * sizeof(double), cudaMemcpyDeviceToDevice, st));
     } else if (stage == 1) {
         if (exch_in) CK(cudaMemcpyAsync(h->s.p, exch_in, (size_t)b * sizeof(double), cudaMemcpyDeviceToDevice, st));
