@@ -100,6 +100,115 @@ __global__ void __launch_bounds__(256) k_maxdiag(const double* __restrict__ A, i
     }
 }
 
+// The same product for large shapes (round 2): 128 x 128 tiles, 8 x 8 outputs per thread, the
+// next K slice of A and B loaded into registers while the current one is multiplied out of
+// shared memory. gridDim.z > 1 splits K into gridDim.z contiguous ranges: slice z writes its
+// partial (alpha = 1, beta = 0) to W + z * M * N (row-major, ld N) and k_sum_splits adds the
+// slices in z order into C (deterministic). At BMDS's Gram (1000 x 1000, K = 100,000) the 64 x 64
+// kernel above ran at ~4.5 TFLOP/s.
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256, 1) k_dgemm128(int M, int N, int64_t K, double alpha, const double* __restrict__ A,
+                                                     int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
+                                                     double* __restrict__ C, int64_t ldc, double* __restrict__ Wsplit) {
+    constexpr int BK = 8;
+    __shared__ double As[2][BK][128 + 2];
+    __shared__ double Bs[2][BK][128 + 2];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 128;
+    const int64_t kchunk = (K + gridDim.z - 1) / gridDim.z;
+    const int64_t kb = blockIdx.z * kchunk, ke = min(K, kb + kchunk);
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    // each thread loads 4 elements of A's and 4 of B's 128 x 8 slice
+    double ra[4], rb[4];
+    auto load = [&](int64_t k0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = threadIdx.x + 256 * u;   // 0..1023
+            int mm, kk;
+            if (TA) { mm = e & 127; kk = e >> 7; } else { kk = e & 7; mm = e >> 3; }
+            const int64_t gm = m0 + mm, gk = k0 + kk;
+            ra[u] = (gm < M && gk < ke) ? (TA ? A[gk * lda + gm] : A[gm * lda + gk]) : 0.0;
+            int nn, kb2;
+            if (TB) { kb2 = e & 7; nn = e >> 3; } else { nn = e & 127; kb2 = e >> 7; }
+            const int64_t gn = n0 + nn, gkb = k0 + kb2;
+            rb[u] = (gn < N && gkb < ke) ? (TB ? B[gn * ldb + gkb] : B[gkb * ldb + gn]) : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = threadIdx.x + 256 * u;
+            int mm, kk;
+            if (TA) { mm = e & 127; kk = e >> 7; } else { kk = e & 7; mm = e >> 3; }
+            As[buf][kk][mm] = ra[u];
+            int nn, kb2;
+            if (TB) { kb2 = e & 7; nn = e >> 3; } else { nn = e & 127; kb2 = e >> 7; }
+            Bs[buf][kb2][nn] = rb[u];
+        }
+    };
+    if (kb < ke) {
+        load(kb);
+        store(0);
+    }
+    __syncthreads();
+    int buf = 0;
+    for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+        const bool more = k0 + BK < ke;
+        if (more) load(k0 + BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            double a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {   // rows ty*4 .. +3 and 64 + ty*4 .. +3 (conflict-free halves)
+                a[i] = As[buf][kk][ty * 4 + i];
+                a[4 + i] = As[buf][kk][64 + ty * 4 + i];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                b[j] = Bs[buf][kk][tx * 4 + j];
+                b[4 + j] = Bs[buf][kk][64 + tx * 4 + j];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        if (more) store(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+            const int64_t gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+            if (gm < M && gn < N) {
+                if (gridDim.z > 1) {
+                    Wsplit[(int64_t)blockIdx.z * M * N + gm * N + gn] = acc[i][j];
+                } else {
+                    double* c = C + gm * ldc + gn;
+                    *c = beta == 0.0 ? alpha * acc[i][j] : fma(alpha, acc[i][j], beta * *c);
+                }
+            }
+        }
+}
+
+__global__ void k_sum_splits(int M, int N, int splits, double alpha, const double* __restrict__ Wsplit, double beta,
+                             double* __restrict__ C, int64_t ldc) {
+    const int64_t total = (int64_t)M * N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int z = 0; z < splits; ++z) v += Wsplit[(int64_t)z * total + e];
+        double* c = C + (e / N) * ldc + e % N;
+        *c = beta == 0.0 ? alpha * v : fma(alpha, v, beta * *c);
+    }
+}
+
 // Upper Cholesky of the nb x nb diagonal block at (k0, k0) of A (lda), in place: A_kk = R^T R,
 // semi-definite: J P is rank-deficient whenever some combination of S's columns is constant
 // (for a partition of unity J P 1 = J 1 = 0), so a pivot <= 1e-13 max diag is a null direction

@@ -3083,11 +3083,30 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
 //   with Cholesky-QR and Rayleigh-Ritz (k_chol, k_rr: the same small kernels as sbmds_eigs);
 //   U = R^{-1} V~_m; V = J P U = S U - 1 (w^T U) (CSR SpMM), Z = V Λ^{1/2}, signs as sbmds_eigs.
 namespace {
+// fp64 GEMM dispatch: small shapes on the 64 x 64 kernel; shapes with >= 64 big tiles or a long
+// K on the 128 x 128 one, splitting K (fixed-order sum of the slices) until ~2 CTAs per SM
+// (ws: the caller's split-K workspace, grown on demand and reused across calls)
 template <bool TA, bool TB>
-void dgemm(cudaStream_t st, int M, int N, int64_t K, double alpha, const double* A, int64_t lda, const double* B,
-           int64_t ldb, double beta, double* C, int64_t ldc) {
-    launch(k_dgemm<TA, TB>, dim3((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64)), dim3(256), 0, st, M, N, K,
-           alpha, A, lda, B, ldb, beta, C, ldc);
+void dgemm(cudaStream_t st, DevBuf& ws, int M, int N, int64_t K, double alpha, const double* A, int64_t lda,
+           const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+    const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + 127) / 128);
+    if ((int64_t)M * N < 128 * 128 || K < 64) {
+        launch(k_dgemm<TA, TB>, dim3((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64)), dim3(256), 0, st, M, N, K,
+               alpha, A, lda, B, ldb, beta, C, ldc);
+        return;
+    }
+    int splits = 1;
+    while (tiles * splits < 296 && K / (splits * 2) >= 512) splits *= 2;
+    if (splits > 1) {
+        ws.ensure((size_t)splits * M * N * sizeof(double));
+        launch(k_dgemm128<TA, TB>, dim3((unsigned)((N + 127) / 128), (unsigned)((M + 127) / 128), (unsigned)splits),
+               dim3(256), 0, st, M, N, K, 1.0, A, lda, B, ldb, 0.0, C, ldc, ws.as<double>());
+        launch(k_sum_splits, dim3((unsigned)std::min<int64_t>(4096, ((int64_t)M * N + 255) / 256)), dim3(256), 0, st, M,
+               N, splits, alpha, (const double*)ws.as<double>(), beta, C, ldc);
+    } else {
+        launch(k_dgemm128<TA, TB>, dim3((unsigned)((N + 127) / 128), (unsigned)((M + 127) / 128), 1u), dim3(256), 0, st,
+               M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, (double*)nullptr);
+    }
 }
 }  // namespace
 
@@ -3113,7 +3132,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, st));
-        DevBuf JP{true}, A{true}, W{true}, T{true}, X{true}, Y{true}, small{true};
+        DevBuf JP{true}, A{true}, W{true}, T{true}, X{true}, Y{true}, small{true}, gws{true};
         h->G.ensure(kMaxB * kMaxB * sizeof(double));   // (the final orthogonality Gram)
         h->status.ensure(16);
         CK(cudaMemsetAsync(h->status.p, 0, 16, st));
@@ -3124,7 +3143,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
                (const int32_t*)h->rp.as<int32_t>(), (const int32_t*)h->col.as<int32_t>(),
                (const float*)h->val.as<float>(), (const double*)h->w.as<double>(), JP.as<double>());
         A.ensure((size_t)l * l * sizeof(double));
-        dgemm<true, false>(st, (int)l, (int)l, n, 1.0, JP.as<double>(), l, JP.as<double>(), l, 0.0, A.as<double>(), l);
+        dgemm<true, false>(st, gws, (int)l, (int)l, n, 1.0, JP.as<double>(), l, JP.as<double>(), l, 0.0, A.as<double>(), l);
         JP.release();
         // G = R^T R, right-looking, 64-column panels (semi-definite: null pivots dropped)
         small.ensure((size_t)3 * kMaxB * kMaxB * sizeof(double) + 64);
@@ -3141,7 +3160,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
                        (int)k0, nb, (const int*)status);
                 // trailing A[k1:, k1:] -= R[k0:k1, k1:]^T R[k0:k1, k1:]
                 const double* Rp = A.as<double>() + k0 * l + k0 + nb;
-                dgemm<true, false>(st, (int)rest, (int)rest, nb, -1.0, Rp, l, Rp, l, 1.0,
+                dgemm<true, false>(st, gws, (int)rest, (int)rest, nb, -1.0, Rp, l, Rp, l, 1.0,
                                    A.as<double>() + (k0 + nb) * l + k0 + nb, l);
             }
         }
@@ -3158,8 +3177,8 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         T.ensure((size_t)l * l * sizeof(double));
         launch(k_f2d_sym, dim3((unsigned)std::min<int64_t>(4096, (l * l + 255) / 256)), dim3(256), 0, st, l,
                (const float*)h->D, h->ldD, W.as<double>());
-        dgemm<false, false>(st, (int)l, (int)l, l, 1.0, A.as<double>(), l, W.as<double>(), l, 0.0, T.as<double>(), l);
-        dgemm<false, true>(st, (int)l, (int)l, l, -0.5, T.as<double>(), l, A.as<double>(), l, 0.0, W.as<double>(), l);
+        dgemm<false, false>(st, gws, (int)l, (int)l, l, 1.0, A.as<double>(), l, W.as<double>(), l, 0.0, T.as<double>(), l);
+        dgemm<false, true>(st, gws, (int)l, (int)l, l, -0.5, T.as<double>(), l, A.as<double>(), l, 0.0, W.as<double>(), l);
         double* Md = W.as<double>();
         // top-m of M: block subspace iteration (X orthonormal l x b)
         X.ensure((size_t)l * b * sizeof(double));
@@ -3170,9 +3189,9 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         h->rr.ensure(sizeof(RrOut));
         launch(k_dinit, dim3(64), dim3(256), 0, st, l * b, (uint64_t)seed, Y.as<double>());
         auto orth = [&](double* Yin, double* Xout) {   // Xout = Yin R^-1, Yin^T Yin = R^T R
-            dgemm<true, false>(st, b, b, l, 1.0, Yin, b, Yin, b, 0.0, Gs, b);
+            dgemm<true, false>(st, gws, b, b, l, 1.0, Yin, b, Yin, b, 0.0, Gs, b);
             chol_launch(b, (const double*)Gs, h->Rinv.as<double>(), status, st);
-            dgemm<false, false>(st, (int)l, b, b, 1.0, Yin, b, h->Rinv.as<double>(), b, 0.0, Xout, b);
+            dgemm<false, false>(st, gws, (int)l, b, b, 1.0, Yin, b, h->Rinv.as<double>(), b, 0.0, Xout, b);
         };
         orth(Y.as<double>(), X.as<double>());
         smem_attr(k_rr, kRrSmem);
@@ -3180,10 +3199,10 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         bool converged = false;
         RrOut rr_host;
         for (it = 1; it <= max_iters; ++it) {
-            dgemm<false, false>(st, (int)l, b, l, 1.0, Md, l, X.as<double>(), b, 0.0, Y.as<double>(), b);
+            dgemm<false, false>(st, gws, (int)l, b, l, 1.0, Md, l, X.as<double>(), b, 0.0, Y.as<double>(), b);
             if (it % h->rr_period == 0 || it == max_iters) {
-                dgemm<true, false>(st, b, b, l, 1.0, X.as<double>(), b, Y.as<double>(), b, 0.0, Hs, b);
-                dgemm<true, false>(st, b, b, l, 1.0, Y.as<double>(), b, Y.as<double>(), b, 0.0, Gs, b);
+                dgemm<true, false>(st, gws, b, b, l, 1.0, X.as<double>(), b, Y.as<double>(), b, 0.0, Hs, b);
+                dgemm<true, false>(st, gws, b, b, l, 1.0, Y.as<double>(), b, Y.as<double>(), b, 0.0, Gs, b);
                 launch(k_rr, dim3(1), dim3(256), kRrSmem, st, b, m, tol > 0.0 ? tol : -1.0, (const double*)Hs,
                        (const double*)Gs, (const double*)nullptr, h->rr.as<RrOut>());
                 int conv = 0;
@@ -3204,7 +3223,7 @@ extern "C" sbmds_status sbmds_bmds(sbmds_t h, int32_t m, int32_t block, int32_t 
         // V~_m = X U[:, :m] (l x m), U_l = R^-1 V~_m, V = J P U_l
         double* Vt = Y.as<double>();                       // (reuse: l x m)
         double* Ul = T.as<double>();
-        dgemm<false, false>(st, (int)l, m, b, 1.0, X.as<double>(), b, h->rr.as<RrOut>()->U, b, 0.0, Vt, m);
+        dgemm<false, false>(st, gws, (int)l, m, b, 1.0, X.as<double>(), b, h->rr.as<RrOut>()->U, b, 0.0, Vt, m);
         launch(k_backsolve, dim3((unsigned)((m + 7) / 8)), dim3(256), 0, st, l, m, (const double*)A.as<double>(), l,
                (const double*)Vt, (int64_t)m, Ul);
         const int bp = next_pow2(m);
@@ -3442,6 +3461,7 @@ extern "C" sbmds_status sbmds_sbha_build(int64_t n, const double* verts, int64_t
             }
         }
         const int64_t W = std::min<int64_t>((w + 1 + 63) / 64 * 64 + 64, (nu + 63) / 64 * 64);
+        DevBuf gws{true};   // split-K workspace of the GEMMs below
         DevBuf duv{true}, dpos{true}, dlm{true}, duq{true}, dqrow{true}, B{true}, Wa{true}, Wb{true}, Rp{true},
             XT{true}, selq{true}, selv{true}, cnt{true}, rp{true}, cur{true}, small{true};
         duv.ensure(nu * sizeof(int32_t));
@@ -3491,7 +3511,7 @@ extern "C" sbmds_status sbmds_sbha_build(int64_t n, const double* verts, int64_t
             if (Wcur > nb) {
                 launch(k_trsm_rows, dim3((unsigned)((Wcur - nb + 255) / 256)), dim3(256), 0, st, Wc, W, Wcur, 0, nb,
                        (const int*)status);
-                dgemm<true, false>(st, (int)(Wcur - nb), (int)(Wcur - nb), nb, -1.0, Wc + nb, W, Wc + nb, W, 1.0,
+                dgemm<true, false>(st, gws, (int)(Wcur - nb), (int)(Wcur - nb), nb, -1.0, Wc + nb, W, Wc + nb, W, 1.0,
                                    Wc + nb * W + nb, W);
             }
             CK(cudaMemcpyAsync(Rp.as<double>() + pn * 64 * W, Wc, (size_t)nb * W * sizeof(double),
@@ -3519,7 +3539,7 @@ extern "C" sbmds_status sbmds_sbha_build(int64_t n, const double* verts, int64_t
             const double* R = Rp.as<double>() + pn * 64 * W;
             launch(k_trsm_panel<true>, dim3(rg), dim3(256), 0, st, R, W, nb, B.as<double>() + k0 * l, l, l);
             if (Wcur > nb)
-                dgemm<true, false>(st, (int)(Wcur - nb), (int)l, nb, -1.0, R + nb, W, B.as<double>() + k0 * l, l, 1.0,
+                dgemm<true, false>(st, gws, (int)(Wcur - nb), (int)l, nb, -1.0, R + nb, W, B.as<double>() + k0 * l, l, 1.0,
                                    B.as<double>() + (k0 + nb) * l, l);
         }
         for (int64_t pn = npan - 1; pn >= 0; --pn) {
@@ -3528,7 +3548,7 @@ extern "C" sbmds_status sbmds_sbha_build(int64_t n, const double* verts, int64_t
             const int64_t Wcur = std::min<int64_t>(W, nu - k0);
             const double* R = Rp.as<double>() + pn * 64 * W;
             if (Wcur > nb)
-                dgemm<false, false>(st, nb, (int)l, Wcur - nb, -1.0, R + nb, W, B.as<double>() + (k0 + nb) * l, l, 1.0,
+                dgemm<false, false>(st, gws, nb, (int)l, Wcur - nb, -1.0, R + nb, W, B.as<double>() + (k0 + nb) * l, l, 1.0,
                                     B.as<double>() + k0 * l, l);
             launch(k_trsm_panel<false>, dim3(rg), dim3(256), 0, st, R, W, nb, B.as<double>() + k0 * l, l, l);
         }
