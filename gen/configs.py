@@ -149,8 +149,8 @@ def sphere_problem(s: int, l: int, k: int, seed: int = 0, name: str = "bumpy_sph
     def build():
         verts, faces = bumpy_sphere(s, seed=seed)
         return mesh_problem(verts, mesh_edges(faces), l, k, seed)
-    arrs, meta = _cached(f"sphere/{s}/{l}/{k}/{seed}/v1", build)
-    meta.update(mesh=f"bumpy icosphere s={s}", s=s, seed=seed)
+    arrs, meta = _cached(f"sphere/{s}/{l}/{k}/{seed}/v2-morton", build)
+    meta.update(mesh=f"bumpy icosphere s={s} (vertices in Morton order)", s=s, seed=seed)
     return Problem(name, 10 * 4 ** s + 2, l, arrs["row_ptr"], arrs["col_idx"], arrs["val"],
                    arrs["D"], landmarks=arrs["landmarks"], meta=meta)
 

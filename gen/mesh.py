@@ -84,8 +84,33 @@ def real_sph_harm(ell: int, m: int, xyz: np.ndarray) -> np.ndarray:
     return np.sqrt(2.0) * (np.imag(y) if m < 0 else np.real(y))
 
 
-def bumpy_sphere(s: int, n_harm: int = 8, amp: float = 0.05, seed: int = 0):
-    """Icosphere radius r = 1 + amp * sum_i Y_i / max|Y_i|, seeded ell in [2,8], m in [-ell, ell]."""
+def morton_order(v: np.ndarray) -> np.ndarray:
+    """Vertex order along the Z-order (Morton) curve of the coordinates, 20 bits per axis
+    (ties by index): the spatially coherent numbering scanned and remeshed meshes carry."""
+    v = np.asarray(v, dtype=np.float64)
+    span = float((v.max(0) - v.min(0)).max()) or 1.0
+    q = ((v - v.min(0)) / span * (2 ** 20 - 1)).astype(np.uint64)
+
+    def spread(x):
+        x = x & np.uint64(0x1FFFFF)
+        x = (x | (x << np.uint64(32))) & np.uint64(0x1F00000000FFFF)
+        x = (x | (x << np.uint64(16))) & np.uint64(0x1F0000FF0000FF)
+        x = (x | (x << np.uint64(8))) & np.uint64(0x100F00F00F00F00F)
+        x = (x | (x << np.uint64(4))) & np.uint64(0x10C30C30C30C30C3)
+        x = (x | (x << np.uint64(2))) & np.uint64(0x1249249249249249)
+        return x
+
+    code = spread(q[:, 0]) | (spread(q[:, 1]) << np.uint64(1)) | (spread(q[:, 2]) << np.uint64(2))
+    return np.argsort(code, kind="stable")
+
+
+def bumpy_sphere(s: int, n_harm: int = 8, amp: float = 0.05, seed: int = 0, order: str = "morton"):
+    """Icosphere radius r = 1 + amp * sum_i Y_i / max|Y_i|, seeded ell in [2,8], m in [-ell, ell].
+
+    order "morton" (default) numbers the vertices along the Z-order curve of their positions
+    (faces remapped), like the coherent orders of real mesh files; "subdivision" keeps the
+    icosphere's construction order (midpoints appended per level), in which 128 consecutive
+    vertices of s = 8 touch up to 4,611 of 5,000 landmarks."""
     v, f = icosphere(s)
     rng = np.random.default_rng(seed)
     radius = np.ones(len(v))
@@ -94,4 +119,12 @@ def bumpy_sphere(s: int, n_harm: int = 8, amp: float = 0.05, seed: int = 0):
         m = int(rng.integers(-ell, ell + 1))
         y = real_sph_harm(ell, m, v)
         radius += amp * y / np.max(np.abs(y))
-    return v * radius[:, None], f
+    v = v * radius[:, None]
+    if order == "morton":
+        perm = morton_order(v)                   # new index i holds old vertex perm[i]
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(len(perm))
+        v, f = v[perm], inv[f]
+    elif order != "subdivision":
+        raise ValueError(order)
+    return v, f

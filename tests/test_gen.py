@@ -127,3 +127,17 @@ def test_random_rows_structure():
     assert np.allclose(val.sum(1), 1.0, atol=1e-6) and np.all(val > 0)
     D = _native.random_sym(300, 4)
     assert np.array_equal(D, D.T) and D.min() >= 0 and D.max() <= 100
+
+
+def test_bumpy_sphere_morton_order_is_a_renumbering():
+    """Config 3's vertex order (Morton) renumbers the same mesh: the same triangles in space, and
+    consecutive vertices are spatially close (mean distance between index neighbours far below
+    the subdivision order's)."""
+    import numpy as np
+    from gen.mesh import bumpy_sphere
+    v, f = bumpy_sphere(4)
+    v0, f0 = bumpy_sphere(4, order="subdivision")
+    key = lambda V, F: np.sort(np.sort(np.round(V[F], 12).reshape(-1, 9), axis=1), axis=0)   # noqa: E731
+    assert np.array_equal(key(v, f), key(v0, f0))
+    step = lambda V: np.linalg.norm(np.diff(V, axis=0), axis=1).mean()   # noqa: E731
+    assert step(v) < 0.3 * step(v0)
