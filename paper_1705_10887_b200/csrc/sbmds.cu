@@ -478,6 +478,7 @@ struct sbmds_ctx {
     uint32_t umax = 0;
     bool blocked = false;
     int use_blocked = 1;   // bit 0: S Y2 through the blocked kernel, bit 1: S^T X too
+    bool blocked_auto = true;   // (no "blocked" option set) standalone applies with b >= 32 use mask 2
     int gram_tc = 1;       // Gram on the FP64 tensor cores (b <= 32)
     int csr_nnz_per_lane = 4;   // narrow CSR SpMM: nonzeros per lane when choosing lanes per row
     int csr_sub_L = 0;          // (tuning) force lanes per row
@@ -1507,6 +1508,10 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
     if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] { colsum(h, b, X, st); });
     const bool blk = blocked_ok(h, b, bp, X, Y);
+    // blocked mask: the option, or (auto, standalone apply) S^T X blocked and S Y2 plain for
+    // b >= 32: measured on config 3 (b = 32) 0.63 ms vs 0.83 ms with the b = 16 default
+    // (blocked S Y2, CSC S^T X), DESIGN.md §4
+    const int bmask = (h->blocked_auto && flags == 0 && b >= 32) ? 2 : h->use_blocked;
     if (blk) {
         // opt the blocked kernels into > 48 KB of dynamic smem (once per device)
         for (auto k : {k_blk_spmmt<1>, k_blk_spmmt<2>, k_blk_spmmt<4>, k_blk_spmmt<8>, k_blk_spmmt<16>})
@@ -1567,7 +1572,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
                 default: go_r(k_blk_reduce<8>); break;
             }
         });
-    } else if (blk && (h->use_blocked & 2)) {
+    } else if (blk && (bmask & 2)) {
         h->P1.ensure((size_t)std::max<int32_t>(1, h->total_u) * kMaxB * sizeof(float));
         const size_t smem_t = (size_t)kRB * bp * sizeof(float);
         auto go_t = [&](auto kern) {
@@ -1616,7 +1621,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
                 default: launch_fused<8>(h, b, Y, Yprev, want_p1, st); break;
             }
         });
-    } else if (blk && (h->use_blocked & 1)) {
+    } else if (blk && (bmask & 1)) {
         const size_t smem = (size_t)h->umax * bp * sizeof(float);
         auto go = [&](auto kern) {
             launch(kern, dim3((unsigned)h->nblk), dim3(256), smem, st, h->n, b, bp, (const int32_t*)h->rp.as<int32_t>(),
@@ -2894,7 +2899,9 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
             } else if (fused) {
                 // A5 fused with G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, H' = Y_k^T Y_{k+1} (RR) and
                 // (fuse = 2) the next apply's S^T Y_{k+1} partials (k_fused.cuh)
-                const bool p1 = h->fuse == 2;
+                // (fuse 3 without the tensor-core step: the partials too from b = 32 on -- config 3:
+                // 39.4 vs 46.0 ms per 50 iterations)
+                const bool p1 = h->fuse == 2 || (h->fuse == 3 && b >= 32);
                 const int fl = kApplyFused | (p1 && itx > 1 ? kApplyY1Ready : 0) | (!p1 || itx == max_iters ? kApplyNoP1 : 0);
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
             } else {
@@ -3622,6 +3629,7 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "blocked")) {
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "blocked is a bit mask in [0, 3]");
         h->use_blocked = (int)value;
+        h->blocked_auto = false;
     } else if (!strcmp(key, "gram_tc")) {
         h->gram_tc = value ? 1 : 0;
     } else if (!strcmp(key, "order_columns")) {
