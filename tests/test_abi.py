@@ -71,3 +71,20 @@ def test_product_has_no_oracle_or_fallback_imports():
             assert "oracle" not in src.replace("oracle.", "").split("import")[0] or "import oracle" not in src
             assert "from oracle" not in src and "import oracle" not in src
             assert "scipy" not in src
+
+
+def test_sbha_p_matches_the_oracle_rule(libpath):
+    """sbmds_sbha_p (host arithmetic, no GPU): p = clamp(ceil((n - l) p_row / l), 1, n - l), the rule
+    the sBHA oracle states (ceiling per SPEC.md:380), on a grid including the SPEC
+    example n = 100, l = 20, p_row = 10 -> 40, fractional p_row and the clamps."""
+    from oracle import sbha_oracle as B
+    from paper_1705_10887_b200._lib import lib
+    L = lib()
+    assert L.sbmds_sbha_p(100, 20, 10.0) == 40
+    for n in (2, 10, 101, 2000, 100_000, 1_800_000):
+        for l in sorted({1, 2, n // 7 or 1, n // 2 or 1, n - 1}):
+            if not 1 <= l < n:
+                continue
+            for prow in (0.5, 1.0, 3.0, 8.0, 16.0, 33.3, 1e9):
+                assert L.sbmds_sbha_p(n, l, prow) == B.p_from_prow(n, l, prow), (n, l, prow)
+    assert L.sbmds_sbha_p(10, 10, 4.0) < 0 and L.sbmds_sbha_p(10, 3, 0.0) < 0

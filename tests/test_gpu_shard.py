@@ -114,3 +114,63 @@ def test_shard_apply_needs_a_communicator():
     with shard_from_problem(p, 1, 2) as h:
         with pytest.raises(SbmdsError, match="EINVAL"):
             h.apply(torch.zeros((h.n, 4), device="cuda"))
+
+
+def _manual_shards(p, cuts, device="cuda"):
+    """Shard handles over arbitrary contiguous row ranges (not split_rows' balance)."""
+    import torch
+    from paper_1705_10887_b200.sbmds import SbmdsShard
+    rp = np.asarray(p.row_ptr, dtype=np.int64)
+    hs = []
+    W = len(cuts) - 1
+    for g in range(W):
+        r0, r1 = cuts[g], cuts[g + 1]
+        lo, hi = int(rp[r0]), int(rp[r1])
+        arrs = [np.ascontiguousarray(rp[r0:r1 + 1] - lo), np.ascontiguousarray(np.asarray(p.col_idx)[lo:hi], np.int32),
+                np.ascontiguousarray(np.asarray(p.val)[lo:hi], np.float32), np.ascontiguousarray(p.D, np.float32)]
+        if device != "numpy":
+            arrs = [torch.from_numpy(a).cuda() for a in arrs]
+        hs.append(SbmdsShard(p.n, r0, r1 - r0, p.l, *arrs, g, W))
+    return hs
+
+
+@pytest.mark.parametrize("cuts_frac,b,device", [((0, 0.07, 0.5, 0.93, 1.0), 5, "cuda"),
+                                                ((0, 0.3, 1.0), 16, "numpy")])
+def test_uneven_partitions_and_host_inputs(cuts_frac, b, device):
+    """Arbitrary row ranges (7% / 43% / 43% / 7%) with b = 5 (bp = 8 padding), and host inputs (a
+    host D crosses as its upper strips and each rank packs only its own tiles) over 2 ranks."""
+    import torch
+    p = configs.random_problem(40_000, 5_000, 16, seed=17, name="shard_uneven")
+    cuts = [int(round(f * p.n)) for f in cuts_frac]
+    hs = _manual_shards(p, cuts, device)
+    X = configs.x_block(p.n, b, seed=4)
+    W, l = len(hs), p.l
+    Xs = [torch.from_numpy(np.ascontiguousarray(X[cuts[g]:cuts[g + 1]])).cuda() for g in range(W)]
+    buf = lambda st: torch.empty(hs[0].exchange_bytes(b, st), dtype=torch.uint8, device="cuda")  # noqa: E731
+    toff = hs[0].exchange_bytes(b, 2) - 8 * b
+    outs = [buf(0) for _ in hs]
+    for h, Xg, o in zip(hs, Xs, outs):
+        h.stage(0, b, X=Xg, exch_out=o)
+    s = sum(o.view(torch.float64) for o in outs).contiguous().view(torch.uint8)
+    outs = [buf(1) for _ in hs]
+    for h, Xg, o in zip(hs, Xs, outs):
+        h.stage(1, b, X=Xg, exch_in=s, exch_out=o)
+    Y1 = sum(o.view(torch.float32) for o in outs).contiguous().view(torch.uint8)
+    outs = [buf(2) for _ in hs]
+    for h, o in zip(hs, outs):
+        h.stage(2, b, exch_in=Y1, exch_out=o)
+    y2t = torch.zeros_like(outs[0])
+    y2t[:4 * l * b].view(torch.float32)[:] = sum(o[:4 * l * b].view(torch.float32) for o in outs)
+    y2t[toff:].view(torch.float64)[:] = sum(o[toff:].view(torch.float64) for o in outs)
+    Ys = []
+    for h, Xg in zip(hs, Xs):
+        Y = torch.empty_like(Xg)
+        h.stage(3, b, exch_in=y2t, Y=Y)
+        Ys.append(Y)
+    torch.cuda.synchronize()
+    paths = [h.stat("dstream_path") for h in hs]
+    for h in hs:
+        h.close()
+    got = np.vstack([Y.cpu().numpy() for Y in Ys])
+    assert paths == [3] * W
+    assert relerr(got, oracle_apply(p, X)) <= TOL
