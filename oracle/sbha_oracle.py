@@ -11,6 +11,8 @@ where the paper's formula is a matrix expression (small meshes only):
     the graph variant D = I, A = 0/1 adjacency (PAPER.md:100);
   * the interpolation operator P = [I_l ; -M_uu^{-1} M_ub] (Eq. 6), with the
     rows of the landmarks b the identity and u the remaining rows in increasing order;
+  * the same columns for large meshes by a sparse LU of M_uu (interpolation_columns; M from
+    scipy sparse products, biharmonic_sparse);
   * thresholding: each column of P_u keeps its p largest-magnitude entries (PAPER.md:175-191
     "chooses the p biggest elements in magnitude ... for each column"), ties to the lowest row
     (SPEC.md:325), kept values unchanged; p = ceil((n - l) p_row / l).
@@ -19,7 +21,9 @@ Pins (tests/test_sbha_oracle.py, ``-m "not gpu"``): SPEC.md:178-188 worked examp
 triangle, split square), the path-graph M of SPEC.md:204 written out by hand, total area,
 linear precision of the cotangent Laplacian on a flat grid, M 1 = 0 and symmetry, P's
 constant reproduction and identity rows, the variational characterisation of P (every
-perturbation of P_u g raises g^T M g-energy), brute-force thresholding, p = n - l keeping all.
+perturbation of P_u g raises g^T M g-energy), brute-force thresholding, p = n - l keeping all;
+biharmonic_sparse / interpolation_columns / threshold_column by the path-graph M of SPEC.md:204,
+M 1 = 0, constant reproduction of the solved columns and the energy minimality above.
 Every function here is pinned; none is "parity unpinned".
 """
 from __future__ import annotations
@@ -107,6 +111,36 @@ def threshold(P: np.ndarray, landmarks, p: int) -> np.ndarray:
         order = sorted(range(len(u)), key=lambda r: (-abs(col[r]), u[r]))[:p]
         out[u[order], c] = col[order]
     return out
+
+
+def biharmonic_sparse(A: sp.spmatrix, mass: np.ndarray) -> sp.csr_matrix:
+    """M = (V - A)^T D^{-1} (V - A) with scipy sparse products (large meshes; the same formula as
+    biharmonic, kept sparse)."""
+    A = sp.csr_matrix(A, dtype=np.float64)
+    L = sp.diags(np.asarray(A.sum(axis=1)).ravel()) - A
+    return sp.csr_matrix(L.T @ sp.diags(1.0 / np.asarray(mass, dtype=np.float64)) @ L)
+
+
+def interpolation_columns(M: sp.spmatrix, landmarks, cols) -> np.ndarray:
+    """Columns `cols` of P_u = -M_uu^{-1} M_ub by a sparse LU of M_uu (scipy
+    SuperLU, a library factorisation), for meshes whose dense M does not fit. Returns
+    (n - l) x len(cols), rows = the free vertices in increasing order."""
+    import scipy.sparse.linalg as spla
+    M = sp.csc_matrix(M, dtype=np.float64)
+    n = M.shape[0]
+    b = np.asarray(landmarks, dtype=np.int64)
+    u = np.setdiff1d(np.arange(n), b)
+    Muu = M[u][:, u].tocsc()
+    rhs = -M[u][:, b[np.asarray(cols)]].toarray()
+    return spla.splu(Muu).solve(rhs)
+
+
+def threshold_column(col: np.ndarray, u: np.ndarray, p: int):
+    """One column's kept (row, value) pairs: the p largest |col| over the free rows u (ties: lowest
+    row), in increasing row order."""
+    order = sorted(range(len(u)), key=lambda r: (-abs(col[r]), u[r]))[:p]
+    order = sorted(order, key=lambda r: u[r])
+    return u[order], col[order]
 
 
 def sbha_interpolation(verts, faces, landmarks, p_row: float):

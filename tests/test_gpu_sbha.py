@@ -123,3 +123,38 @@ def test_sbha_rejects_degenerate_faces():
     V[F[0, 1]] = V[F[0, 0]]                               # collapse one edge: zero-area faces
     with pytest.raises(SbmdsError, match="degenerate"):
         gpu_sbha(V, F, np.arange(0, 120, 9, dtype=np.int32), 4)
+
+
+def test_sbha_config2_full_size_sampled_columns():
+    """At config 2's full size (torus 250 x 400, n = 100,000, its 1,000 FPS landmarks, p_row 16):
+    sampled columns of the GPU's S against the oracle's sparse-LU solve of the same columns
+    (oracle.interpolation_columns) thresholded to the same p -- the sampled-output check at a size
+    the dense oracle cannot reach."""
+    from oracle import sbha_oracle as Bo
+    p = configs.config(2)
+    V, F, _ = torus_grid(250, 400, seed=0)
+    from paper_1705_10887_b200.sbmds import sbha_build
+    rp, ci, vv, info = sbha_build(V, F.astype(np.int32), p.landmarks, 16, device="numpy")
+    n, l = p.n, p.l
+    assert info["nnz"] == l + l * info["p"] and info["p"] == Bo.p_from_prow(n, l, 16)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    is_lm = np.zeros(n, bool)
+    is_lm[p.landmarks] = True
+    u = np.flatnonzero(~is_lm)
+    cols = [0, 1, 137, 500, 999]
+    M = Bo.biharmonic_sparse(Bo.cotan_adjacency(V, F), Bo.lumped_mass(V, F))
+    Pu = Bo.interpolation_columns(M, p.landmarks, cols)
+    for j, c in enumerate(cols):
+        sel = (ci == c) & ~is_lm[rows]
+        g_rows, g_vals = rows[sel], vv[sel]
+        o_rows, o_vals = Bo.threshold_column(Pu[:, j], u, info["p"])
+        a = np.abs(Pu[:, j])
+        kth = np.sort(a)[::-1][info["p"] - 1]
+        pos = {r: q for q, r in enumerate(u)}
+        for r in set(g_rows.tolist()) ^ set(o_rows.tolist()):   # only near-ties may differ
+            assert abs(a[pos[r]] - kth) <= 1e-9 * a.max(), (c, r)
+        common = np.intersect1d(g_rows, o_rows)
+        gv = dict(zip(g_rows.tolist(), g_vals.tolist()))
+        ov = dict(zip(o_rows.tolist(), o_vals.tolist()))
+        err = max(abs(gv[r] - ov[r]) for r in common.tolist())
+        assert err <= 1e-6 * a.max(), (c, err)

@@ -147,3 +147,37 @@ def test_sbha_interpolation_budget():
     u = np.setdiff1d(np.arange(120), lm)
     assert (np.count_nonzero(Ps[u], axis=0) <= p).all()
     assert np.array_equal(Ps[lm], np.eye(len(lm)))
+
+
+def test_sparse_path_pins():
+    """The large-mesh oracle path (biharmonic_sparse, interpolation_columns, threshold_column) on its
+    own pins: the SPEC.md:204 path-graph M, M 1 = 0 and symmetry on a torus, the solved columns
+    reproduce constants (their sum over the landmark columns is 1 on every free row) and minimise
+    the biharmonic energy (perturbations raise it), and thresholding keeps the p largest."""
+    import scipy.sparse as sp
+    from gen.mesh import torus_grid
+    g = golden()
+    adj = sp.csr_matrix(np.array([[0, 1, 0], [1, 0, 1], [0, 1, 0]], dtype=float))
+    assert np.array_equal(B.biharmonic_sparse(adj, np.ones(3)).toarray(), g["path_M"].reshape(3, 3))
+    V, F, _ = torus_grid(20, 24, seed=9)
+    n = len(V)
+    M = B.biharmonic_sparse(B.cotan_adjacency(V, F), B.lumped_mass(V, F))
+    s = abs(M).max()
+    assert abs(M - M.T).max() <= 1e-12 * s and np.abs(M @ np.ones(n)).max() <= 1e-10 * s
+    lm = np.arange(0, n, 11)
+    Pu = B.interpolation_columns(M, lm, np.arange(len(lm)))
+    assert np.abs(Pu.sum(1) - 1).max() < 1e-9                         # constants reproduced
+    u = np.setdiff1d(np.arange(n), lm)
+    Md = M.toarray()
+    rng = np.random.default_rng(2)
+    gvec = rng.standard_normal(len(lm))
+    f = np.zeros(n)
+    f[lm] = gvec
+    f[u] = Pu @ gvec
+    E0 = f @ Md @ f
+    for _ in range(10):
+        d = np.zeros(n)
+        d[u] = rng.standard_normal(len(u))
+        assert (f + 1e-2 * d) @ Md @ (f + 1e-2 * d) > E0
+    rows, vals = B.threshold_column(np.array([0.1, -0.9, 0.5, 0.9]), np.array([3, 5, 8, 9]), 2)
+    assert rows.tolist() == [5, 9] and vals.tolist() == [-0.9, 0.9]   # tie -> both (p = 2), row order
