@@ -18,7 +18,9 @@
  *     cudaPointerGetAttributes). Host inputs are staged through library-owned device
  *     buffers and the call synchronises `cuda_stream` before returning; with all
  *     pointers on the device the call is asynchronous on `cuda_stream` (eigs reads a
- *     small convergence flag back every rr_period iterations).
+ *     small convergence flag back every rr_period iterations; the first call of a handle
+ *     reads D's precision check back once; a standalone apply on the int8 stream reads
+ *     its Y1 column check back unless "dy_max_range" >= 64).
  *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
  *   - Dense blocks (X, Y, V, Z) are row-major n x b fp32: the b values of vertex i
  *     are contiguous at offset i*b.
@@ -233,7 +235,8 @@ const char* sbmds_last_error(void);
                       max |D| (stat "dq_range"); otherwise the full D on 3xTF32 (stat "dq_state" -1)
      "dy_max_range"   (binades, default 3) standalone apply on the int8 stream: a Y1 column whose
                       max |y| exceeds 2^range times its rms sends that apply to the fp32-grade
-                      stream (stat "y_fallbacks")
+                      stream (stat "y_fallbacks"); the check reads 0.8 KB back (a stream sync),
+                      >= 64 turns it off (no host sync: the apply can then be graph-captured)
      "sp8_max_range"  (binades, default 7) tensor-core sparse step: a 128-row block whose smallest
                       nonzero row maximum sits more than this many binades below the block's max
                       keeps the eigs step on the fp32 sparse kernels (stat "sp8_state" -2,

@@ -195,6 +195,8 @@ __global__ void k_peek(const unsigned char* __restrict__ src, unsigned char* __r
 }
 
 void peek_to_host(void* host_dst, const void* dev_src, size_t bytes, cudaStream_t st) {
+    static std::mutex mu;   // one mapped buffer for all handles and threads
+    std::lock_guard<std::mutex> g(mu);
     static unsigned char* hbuf = nullptr;
     static unsigned char* dbuf = nullptr;
     if (!hbuf) {
@@ -1599,7 +1601,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
     }
     // standalone apply on the int8 stream (auto): check Y1's columns first (one small readback)
-    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && uses_sym(h, bp)) ycheck(h, b, bp, st);
+    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 && uses_sym(h, bp))
+        ycheck(h, b, bp, st);
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 64);   // (sp8_dbg & 64: separate k_y2_digits, diagnostics)
     h->y2d_ready = false;
@@ -2443,7 +2446,8 @@ void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void*
         if (exch_in)
             CK(cudaMemcpy2DAsync(h->Y1.p, (size_t)bp * 4, exch_in, (size_t)b * 4, (size_t)b * 4, l,
                                  cudaMemcpyDeviceToDevice, st));
-        if (h->dstream == 0 && uses_sym(h, bp)) ycheck(h, b, bp, st);   // (same Y1, same decision on every rank)
+        if (h->dstream == 0 && h->dy_max_range < 64 && uses_sym(h, bp))
+            ycheck(h, b, bp, st);   // (same Y1, same decision on every rank)
         if (uses_sym(h, bp) || h->rank == 0) {
             dstream(h, b, bp, st, nullptr);
         } else {   // full-D paths are not tiled: rank 0 owns all of D Y1
