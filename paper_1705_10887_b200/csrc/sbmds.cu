@@ -200,7 +200,7 @@ void peek_to_host(void* host_dst, const void* dev_src, size_t bytes, cudaStream_
     static unsigned char* hbuf = nullptr;
     static unsigned char* dbuf = nullptr;
     if (!hbuf) {
-        CK(cudaHostAlloc(reinterpret_cast<void**>(&hbuf), 4096, cudaHostAllocMapped));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&hbuf), 4096, cudaHostAllocMapped | cudaHostAllocPortable));
         CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dbuf), hbuf, 0));
     }
     if (bytes > 4096) throw CudaError{cudaErrorInvalidValue, "peek_to_host"};
