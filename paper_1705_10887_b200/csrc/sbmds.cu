@@ -462,6 +462,7 @@ struct sbmds_ctx {
     int rank = 0, world = 1;
     bool shard = false;
     void* comm = nullptr;
+    DevBuf Y1w, Y2w;           // b <= 4 on the int8 stream: Y1 / Y2 at pitch 8
     DevBuf vg;                 // shard: v_g = D w_g (t_g = v_g^T Y1, formed at the first stage 2)
     // row order (reorder_rows): the handle keeps S's rows permuted when 128-row blocks then touch
     // fewer landmarks; perm[r] = caller's row of handle row r. X / Y / V cross it at the ABI.
@@ -1237,7 +1238,33 @@ void ensure_full_d(sbmds_ctx* h, cudaStream_t st) {
     h->d_lower_missing = false;
 }
 
+// whether dstream() takes a symmetric-half stream (tile-partitioned on a shard) at width bp
+bool takes_sym(const sbmds_ctx* h, int bp) {
+    return bp < 8 ? (h->dstream == 0 && uses_sym(h, 8)) : uses_sym(h, bp);
+}
+
 void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
+    if (bp < 8 && h->dstream == 0 && uses_sym(h, 8)) {
+        // b <= 4 (round 2): the symmetric int8 stream at width 8 reads 3 l^2 / 2 bytes where the
+        // FFMA stream reads 4 l^2 (config 5, l = 20k: 0.61 vs 1.6 GB). Y1 is widened to pitch 8
+        // (zero columns) around it and Y2 narrowed back to pitch bp for the CSR SpMM.
+        const int64_t lpad = y1t_lpad(h);
+        h->Y1w.ensure((size_t)lpad * kMaxB * sizeof(float));
+        h->Y2w.ensure((size_t)h->l * kMaxB * sizeof(float));
+        CK(cudaMemsetAsync(h->Y1w.p, 0, (size_t)lpad * 8 * sizeof(float), st));
+        CK(cudaMemcpy2DAsync(h->Y1w.p, 8 * sizeof(float), h->Y1.p, bp * sizeof(float), b * sizeof(float), h->l,
+                             cudaMemcpyDeviceToDevice, st));
+        h->Y1.swap(h->Y1w);
+        h->Y2.swap(h->Y2w);
+        struct Back {
+            sbmds_ctx* h;
+            ~Back() { h->Y1.swap(h->Y1w); h->Y2.swap(h->Y2w); }
+        } back{h};
+        run_dstream_sym8<8>(h, b, st, Rinv);
+        CK(cudaMemcpy2DAsync(h->Y2w.p, bp * sizeof(float), h->Y2.p, 8 * sizeof(float), b * sizeof(float), h->l,
+                             cudaMemcpyDeviceToDevice, st));   // (Y2w is the caller's Y2 until the swap back)
+        return;
+    }
     if (uses_sym(h, bp)) {
         if (h->dstream == 4) {   // 2xFP16 on CTA pairs (k_dstream_pair), kept for comparison
             if (bp == 8) run_dstream_pair<8>(h, b, st, Rinv);
@@ -1601,7 +1628,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
     }
     // standalone apply on the int8 stream (auto): check Y1's columns first (one small readback)
-    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 && uses_sym(h, bp))
+    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp))
         ycheck(h, b, bp, st);
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 64);   // (sp8_dbg & 64: separate k_y2_digits, diagnostics)
@@ -1827,7 +1854,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->Y1w, &h->Y2w, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
@@ -2446,9 +2473,9 @@ void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void*
         if (exch_in)
             CK(cudaMemcpy2DAsync(h->Y1.p, (size_t)bp * 4, exch_in, (size_t)b * 4, (size_t)b * 4, l,
                                  cudaMemcpyDeviceToDevice, st));
-        if (h->dstream == 0 && h->dy_max_range < 64 && uses_sym(h, bp))
+        if (h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp))
             ycheck(h, b, bp, st);   // (same Y1, same decision on every rank)
-        if (uses_sym(h, bp) || h->rank == 0) {
+        if (takes_sym(h, bp) || h->rank == 0) {
             dstream(h, b, bp, st, nullptr);
         } else {   // full-D paths are not tiled: rank 0 owns all of D Y1
             CK(cudaMemsetAsync(h->Y2.p, 0, (size_t)l * bp * sizeof(float), st));

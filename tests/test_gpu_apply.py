@@ -415,3 +415,20 @@ def test_reordered_rows_keep_the_callers_order(cfgname):
     assert O.principal_angle(Vr, Vn) <= 1e-3
     for j in range(3):                              # the sign rule in the caller's row order
         assert Vr[np.argmax(np.abs(Vr[:, j])), j] > 0
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+def test_narrow_blocks_on_the_int8_stream(b):
+    """b <= 4 at a D large enough for the symmetric half (l = 5000): the int8 stream at width 8 with
+    Y1 widened and Y2 narrowed around it (3 l^2 / 2 bytes instead of the FFMA stream's 4 l^2),
+    centred and uncentred, against the oracle."""
+    p = configs.random_problem(40_000, 5_000, 16, seed=90 + b, name="narrow_b")
+    X = configs.x_block(p.n, b, seed=b)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    with make_handle(p) as h:
+        Y = run_apply(h, X)
+        assert h.stat("dstream_path") == 3
+        h.set_option("center", 0)
+        Yr = run_apply(h, X)
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
+    assert relerr(Yr, O.apply_raw(S, p.D, X.astype(np.float64))) <= TOL
