@@ -70,12 +70,17 @@ def staged_apply(p, world, X, **opts):
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("b", [16, 8, 32, 4])
 def test_staged_shards_match_oracle(world, b):
-    """l = 5000 (40 row tiles, 820 upper tiles): b in {8, 16, 32} stream each rank's tile range
-    on the int8 symmetric-half kernel; b = 4 takes the FFMA full-D stream on rank 0."""
+    """l = 5000 (40 row tiles, 820 upper tiles): every width streams each rank's tile range on the
+    int8 symmetric-half kernel (b = 4 at width 8, Y1 widened and Y2 narrowed around it); with
+    dstream = 1 (FFMA, not tiled by rank) rank 0 streams all of D and the others add zeros."""
     p = configs.random_problem(40_000, 5_000, 16, seed=b + world, name="shard")
     X = configs.x_block(p.n, b, seed=b)
     Y, paths = staged_apply(p, world, X)
-    assert paths == [3] * world if b >= 5 else paths[0] == 1
+    assert paths == [3] * world
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
+    if b == 4:
+        Yf, pf = staged_apply(p, world, X, dstream=1)
+        assert pf[0] == 1 and relerr(Yf, oracle_apply(p, X)) <= TOL
     assert relerr(Y, oracle_apply(p, X)) <= TOL
 
 
