@@ -462,7 +462,7 @@ struct sbmds_ctx {
     int rank = 0, world = 1;
     bool shard = false;
     void* comm = nullptr;
-    DevBuf Y1w, Y2w;           // b <= 4 on the int8 stream: Y1 / Y2 at pitch 8
+    DevBuf Y1w, Y2w, tsave;    // b <= 4 / b > 32 on the int8 stream: Y1 / Y2 at pitch 8 / 32, t halves
     DevBuf vg;                 // shard: v_g = D w_g (t_g = v_g^T Y1, formed at the first stage 2)
     // row order (reorder_rows): the handle keeps S's rows permuted when 128-row blocks then touch
     // fewer landmarks; perm[r] = caller's row of handle row r. X / Y / V cross it at the ABI.
@@ -1239,8 +1239,11 @@ void ensure_full_d(sbmds_ctx* h, cudaStream_t st) {
 }
 
 // whether dstream() takes a symmetric-half stream (tile-partitioned on a shard) at width bp
+// (b = 64 only without an R^-1 fold: the fold couples the two column halves)
 bool takes_sym(const sbmds_ctx* h, int bp) {
-    return bp < 8 ? (h->dstream == 0 && uses_sym(h, 8)) : uses_sym(h, bp);
+    if (bp < 8) return h->dstream == 0 && uses_sym(h, 8);
+    if (bp == 64) return h->dstream == 0 && uses_sym(h, 32);
+    return uses_sym(h, bp);
 }
 
 void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
@@ -1263,6 +1266,36 @@ void dstream(sbmds_ctx* h, int b, int bp, cudaStream_t st, const double* Rinv) {
         run_dstream_sym8<8>(h, b, st, Rinv);
         CK(cudaMemcpy2DAsync(h->Y2w.p, bp * sizeof(float), h->Y2.p, 8 * sizeof(float), b * sizeof(float), h->l,
                              cudaMemcpyDeviceToDevice, st));   // (Y2w is the caller's Y2 until the swap back)
+        return;
+    }
+    if (bp == 64 && !Rinv && h->dstream == 0 && uses_sym(h, 32)) {
+        // b in 33..64 without a fold (round 2): two passes of the width-32 int8 stream over the
+        // column halves, 2 x 3 l^2 / 2 bytes instead of the 3xTF32 stream's 4 l^2 (config 5:
+        // 1.2 vs 1.6 GB); Y1's halves at pitch 32, Y2's halves and t merged back
+        const int64_t lpad = y1t_lpad(h);
+        h->Y1w.ensure((size_t)lpad * kMaxB * sizeof(float));
+        h->Y2w.ensure((size_t)h->l * kMaxB * sizeof(float));
+        h->tsave.ensure(kMaxB * sizeof(double));
+        int64_t bytes2 = 0;
+        for (int half = 0; half < 2; ++half) {
+            const int c0 = 32 * half, bh = std::min(32, b - c0);
+            CK(cudaMemsetAsync(h->Y1w.p, 0, (size_t)lpad * 32 * sizeof(float), st));
+            CK(cudaMemcpy2DAsync(h->Y1w.p, 32 * sizeof(float), h->Y1.as<float>() + c0, 64 * sizeof(float),
+                                 bh * sizeof(float), h->l, cudaMemcpyDeviceToDevice, st));
+            h->Y1.swap(h->Y1w);
+            h->Y2.swap(h->Y2w);
+            struct Back {
+                sbmds_ctx* h;
+                ~Back() { h->Y1.swap(h->Y1w); h->Y2.swap(h->Y2w); }
+            } back{h};
+            run_dstream_sym8<32>(h, bh, st, nullptr);
+            bytes2 += h->last_dbytes;
+            CK(cudaMemcpy2DAsync(h->Y2w.as<float>() + c0, 64 * sizeof(float), h->Y2.p, 32 * sizeof(float),
+                                 bh * sizeof(float), h->l, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(h->tsave.as<double>() + c0, h->t.p, bh * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        }
+        CK(cudaMemcpyAsync(h->t.p, h->tsave.p, b * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        h->last_dbytes = bytes2 / 2;   // (per launch, as the profile counts launches)
         return;
     }
     if (uses_sym(h, bp)) {
@@ -1854,7 +1887,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->Y1w, &h->Y2w, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->Y1w, &h->Y2w, &h->tsave, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,

@@ -432,3 +432,21 @@ def test_narrow_blocks_on_the_int8_stream(b):
         Yr = run_apply(h, X)
     assert relerr(Y, oracle_apply(p, X)) <= TOL
     assert relerr(Yr, O.apply_raw(S, p.D, X.astype(np.float64))) <= TOL
+
+
+@pytest.mark.parametrize("b", [33, 48, 64])
+def test_wide_blocks_in_two_int8_passes(b):
+    """33 <= b <= 64 in a standalone apply at a D large enough for the symmetric half: two passes
+    of the width-32 int8 stream over the column halves (Y2 and t merged), vs the oracle; the
+    uncentred apply (an R^-1 fold of -2 I) keeps the 3xTF32 stream."""
+    p = configs.random_problem(40_000, 5_000, 16, seed=70 + b, name="wide_b")
+    X = configs.x_block(p.n, b, seed=b)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    with make_handle(p) as h:
+        Y = run_apply(h, X)
+        assert h.stat("dstream_path") == 3
+        h.set_option("center", 0)
+        Yr = run_apply(h, X)
+        assert h.stat("dstream_path") == 2
+    assert relerr(Y, oracle_apply(p, X)) <= TOL
+    assert relerr(Yr, O.apply_raw(S, p.D, X.astype(np.float64))) <= TOL
