@@ -290,9 +290,13 @@ int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas,
  *
  * sbmds_create_shard — as sbmds_create for the local rows (row_ptr is local: row_ptr[0] = 0,
  *   row_ptr[n_local] = nnz); D_ll is the full l x l matrix on every rank. 1 <= l <= n_global,
- *   0 <= row0, row0 + n_local <= n_global, 0 <= rank < world. sbmds_eigs rejects shard handles
- *   (SBMDS_EINVAL: a sharded eigensolver is not built); sbmds_apply on a shard handle needs an
- *   attached communicator when world > 1 (SBMDS_EINVAL otherwise).
+ *   0 <= row0, row0 + n_local <= n_global, 0 <= rank < world. sbmds_apply and sbmds_eigs on a
+ *   shard handle need an attached communicator when world > 1 (SBMDS_EINVAL otherwise). On a
+ *   shard, sbmds_eigs runs the block subspace iteration on the rank's rows (X0, V, Z are the
+ *   rank's n_local x b / x m rows): the sharded apply with the R^{-1} fold, the Grams summed over
+ *   the ranks (every rank factors and solves the same small problems), the sign rule over all
+ *   rows; every rank must call it with the same arguments. The Lanczos solver and sbmds_bmds
+ *   reject shard handles.
  * sbmds_shard_stage — one stage on DEVICE buffers, stream-ordered (a standalone stage 2 on the
  *   int8 stream reads a small Y1 check back). X for stages 0-1, exch_in for 1-3, exch_out for
  *   0-2, Y for 3; the others may be NULL.

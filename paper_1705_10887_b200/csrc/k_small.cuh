@@ -797,11 +797,13 @@ __device__ __forceinline__ void philox4x32_10(uint32_t ctr[4], uint32_t k0, uint
     }
 }
 
-__global__ void k_init_philox(int64_t n, int b, uint64_t seed, float* __restrict__ X) {
+// (e0: the counter of the first element -- a shard's rows continue the global sequence)
+__global__ void k_init_philox(int64_t n, int b, uint64_t seed, float* __restrict__ X, int64_t e0) {
     const int64_t total = n * b;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t ctr[4] = {(uint32_t)e, (uint32_t)(e >> 32), 0x5eed5eedu, 0u};
+        const int64_t ge = e0 + e;
+        uint32_t ctr[4] = {(uint32_t)ge, (uint32_t)(ge >> 32), 0x5eed5eedu, 0u};
         philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
         const double u1 = ((double)ctr[0] + 1.0) * (1.0 / 4294967296.0);  // (0, 1]
         const double u2 = (double)ctr[1] * (1.0 / 4294967296.0);
@@ -853,6 +855,36 @@ __global__ void __launch_bounds__(256) k_col_argmax(int64_t n, int mo, const flo
         }
         if (tid == 0) *counter = 0;
     }
+}
+
+// Sharded E6 (sbmds.cu eigs_shard): per column the key (|v| bits << 32 | (2^31 - 1 - global row))
+// of this rank's rows -- its max over the ranks is the global largest |v|, ties to the lowest
+// row -- and then the sign of V at that row from the rank that holds it (0 elsewhere).
+__global__ void __launch_bounds__(256) k_col_key(int64_t n, int mo, const float* __restrict__ V, int64_t row0,
+                                                 unsigned long long* __restrict__ key) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * mo; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / mo;
+        const int c = (int)(e % mo);
+        const unsigned long long k = ((unsigned long long)__float_as_uint(fabsf(V[e])) << 32) |
+                                     (unsigned long long)(0x7FFFFFFFll - (row0 + r));
+        atomicMax(key + c, k);
+    }
+}
+
+__global__ void k_key_sign(int64_t n, int mo, const float* __restrict__ V, int64_t row0,
+                           const unsigned long long* __restrict__ key, float* __restrict__ sgn) {
+    const int c = threadIdx.x;
+    if (c >= mo) return;
+    const int64_t r = 0x7FFFFFFFll - (int64_t)(key[c] & 0xFFFFFFFFull) - row0;
+    sgn[c] = (r >= 0 && r < n) ? (V[r * mo + c] < 0.f ? -1.f : 1.f) : 0.f;
+}
+
+__global__ void k_vec_rinv(int b, const double* __restrict__ v, const double* __restrict__ Rinv, double* __restrict__ t) {
+    const int c = threadIdx.x;
+    if (c >= b) return;
+    double acc = 0.0;
+    for (int p = 0; p <= c; ++p) acc = fma(v[p], Rinv[p * b + c], acc);   // Rinv upper triangular
+    t[c] = acc;
 }
 
 __global__ void k_finalize(int64_t n, int mo, const float* __restrict__ sign, const double* __restrict__ theta,

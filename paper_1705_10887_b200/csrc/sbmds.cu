@@ -1240,9 +1240,9 @@ void ensure_full_d(sbmds_ctx* h, cudaStream_t st) {
 
 // whether dstream() takes a symmetric-half stream (tile-partitioned on a shard) at width bp
 // (b = 64 only without an R^-1 fold: the fold couples the two column halves)
-bool takes_sym(const sbmds_ctx* h, int bp) {
+bool takes_sym(const sbmds_ctx* h, int bp, bool fold) {
     if (bp < 8) return h->dstream == 0 && uses_sym(h, 8);
-    if (bp == 64) return h->dstream == 0 && uses_sym(h, 32);
+    if (bp == 64) return !fold && h->dstream == 0 && uses_sym(h, 32);
     return uses_sym(h, bp);
 }
 
@@ -1661,7 +1661,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
     }
     // standalone apply on the int8 stream (auto): check Y1's columns first (one small readback)
-    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp))
+    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp, Rinv != nullptr))
         ycheck(h, b, bp, st);
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 64);   // (sp8_dbg & 64: separate k_y2_digits, diagnostics)
@@ -2506,9 +2506,9 @@ void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void*
         if (exch_in)
             CK(cudaMemcpy2DAsync(h->Y1.p, (size_t)bp * 4, exch_in, (size_t)b * 4, (size_t)b * 4, l,
                                  cudaMemcpyDeviceToDevice, st));
-        if (h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp))
+        if (h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp, false))
             ycheck(h, b, bp, st);   // (same Y1, same decision on every rank)
-        if (takes_sym(h, bp) || h->rank == 0) {
+        if (takes_sym(h, bp, false) || h->rank == 0) {
             dstream(h, b, bp, st, nullptr);
         } else {   // full-D paths are not tiled: rank 0 owns all of D Y1
             CK(cudaMemsetAsync(h->Y2.p, 0, (size_t)l * bp * sizeof(float), st));
@@ -2764,7 +2764,7 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
             permute_block(h, b, h->xperm.as<float>(), W, false, st);
         }
     }
-    else launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, W);
+    else launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, W, (int64_t)0);
     cholqr(W, tmp, h->lzR.as<double>());
     cholqr(tmp, Qj(0), h->lzR.as<double>());
     check_breakdown("Cholesky-QR of the initial block broke down");
@@ -2857,6 +2857,161 @@ int eigs_lanczos(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t
     return applies;
 }
 
+// ---------------------------------------------------------------------------- sharded eigensolver
+// The block subspace iteration on a shard handle (round 2): each rank holds its
+// rows of the iterate. The apply is the four sharded stages with the R^{-1} fold (t_g = (v_g^T Y1)
+// R^{-1}); the Grams G = Y^T Y, 1^T Y and, at Rayleigh-Ritz steps, H' = Y_k^T Y_{k+1} are local
+// partials summed with ncclAllReduce, so every rank factors the same G and solves the same
+// Rayleigh-Ritz problem (the same convergence decision on every rank); V's rows stay local; the
+// sign rule takes the global largest |v| (ties: lowest global row) by a max-allreduce of packed
+// keys. Non-fused kernels (the row-blocked / tensor-core steps are not sharded).
+namespace {
+sbmds_status eigs_shard(sbmds_ctx* h, int m, int b, int max_iters, double tol, uint64_t seed, const float* X0,
+                        double* eigvals, float* V, float* Z, sbmds_info* info, cudaStream_t st) {
+    const NcclApi* nc = h->comm ? &nccl_api() : nullptr;
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(h->comm);
+    auto sum = [&](void* p, size_t count, ncclDataType_t ty) {
+        if (h->comm) NK(nc->allReduce(p, p, count, ty, ncclSum, comm, st));
+    };
+    const int64_t n = h->n;
+    const int bp = next_pow2(b);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    h->X.ensure((size_t)n * b * sizeof(float));
+    h->Y.ensure((size_t)n * b * sizeof(float));
+    h->G.ensure(kMaxB * kMaxB * sizeof(double));
+    h->H.ensure(kMaxB * kMaxB * sizeof(double));
+    h->Rinv.ensure(kMaxB * kMaxB * sizeof(double));
+    h->status.ensure(16);
+    h->rr.ensure(sizeof(RrOut));
+    h->tsave.ensure(kMaxB * sizeof(double));
+    ensure_apply_ws(h, bp);
+    float* Yc = h->X.as<float>();
+    float* Yn = h->Y.as<float>();
+    if (X0) CK(cudaMemcpyAsync(Yc, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
+    else launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, Yc, h->row0 * b);
+    auto grams = [&](const float* Y, const float* Yprev) {   // G, s (and H') summed over the ranks
+        gram(h, b, Y, Yprev, st, true);
+        sum(h->G.p, (size_t)b * b, ncclFloat64);
+        sum(h->s.p, (size_t)b, ncclFloat64);
+        if (Yprev) sum(h->H.p, (size_t)b * b, ncclFloat64);
+    };
+    grams(Yc, nullptr);
+    chol(h, b, st);
+    int hstat = 0;
+    peek_to_host(&hstat, h->status.p, sizeof(int), st);
+    if (hstat == 2) return fail(SBMDS_EBREAKDOWN, "Cholesky-QR of the initial block broke down");
+    smem_attr(k_rr, kRrSmem);
+    const double* Rinv = h->Rinv.as<double>();
+    if (!h->vg_ok) {   // v_g = D w_g (t_g = v_g^T Y1)
+        ensure_full_d(h, st);
+        h->vg.ensure((size_t)h->l * sizeof(double));
+        launch(k_symv_rows, dim3((unsigned)std::min<int64_t>(8 * (int64_t)h->num_sms, (h->l + 7) / 8)), dim3(256), 0,
+               st, h->l, (const float*)h->D, h->ldD, (const double*)h->w.as<double>(), h->vg.as<double>());
+        h->vg_ok = true;
+    }
+    int it = 1;
+    bool converged = false;
+    RrOut rr_host;
+    for (; it <= max_iters; ++it) {
+        const bool do_rr = (it % h->rr_period == 0) || it == max_iters;
+        // Y_{k+1} = B~ (Y_k R^-1): s = 1^T Y_k came with the Gram
+        spmm_csc(h, b, bp, Yc, st);                                     // Y1_g = S_g^T Y_k - w_g s^T
+        sum(h->Y1.p, (size_t)h->l * bp, ncclFloat32);
+        launch(k_vdot, dim3(1), dim3(256), 0, st, h->l, b, bp, (const double*)h->vg.as<double>(),
+               (const float*)h->Y1.as<float>(), h->tsave.as<double>());   // v_g^T Y1 (before the fold)
+        if (takes_sym(h, bp, true) || h->rank == 0) {
+            dstream(h, b, bp, st, Rinv);
+        } else {
+            CK(cudaMemsetAsync(h->Y2.p, 0, (size_t)h->l * bp * sizeof(float), st));
+        }
+        launch(k_vec_rinv, dim3(1), dim3(64), 0, st, b, (const double*)h->tsave.as<double>(), Rinv, h->t.as<double>());
+        if (h->comm) {
+            NK(nc->groupStart());
+            NK(nc->allReduce(h->Y2.p, h->Y2.p, (size_t)h->l * bp, ncclFloat32, ncclSum, comm, st));
+            NK(nc->allReduce(h->t.p, h->t.p, (size_t)b, ncclFloat64, ncclSum, comm, st));
+            NK(nc->groupEnd());
+        }
+        spmm_csr(h, b, bp, Yn, st);                                     // local rows of Y_{k+1}
+        grams(Yn, do_rr ? Yc : nullptr);
+        if (do_rr) {
+            launch(k_rr, dim3(1), dim3(256), (size_t)kRrSmem, st, b, m, tol, (const double*)h->H.as<double>(),
+                   (const double*)h->G.as<double>(), Rinv, h->rr.as<RrOut>());
+            int conv = 0;
+            CK(cudaMemcpyAsync(&conv, &h->rr.as<RrOut>()->converged, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (conv || it == max_iters) {
+                converged = conv != 0;
+                break;   // Ritz vectors Y_k (R_k^-1 U): Yc and Rinv stay valid
+            }
+        }
+        chol(h, b, st);
+        std::swap(Yc, Yn);
+    }
+    if (it > max_iters) it = max_iters;
+    CK(cudaMemcpyAsync(&rr_host, h->rr.p, sizeof(RrOut), cudaMemcpyDeviceToHost, st));
+    h->vsel.ensure(((size_t)b * m + 2 * m) * sizeof(double));
+    double* Msel_d = h->vsel.as<double>();
+    launch(k_select, dim3(1), dim3(256), 0, st, b, m, h->n_global, (const RrOut*)h->rr.as<RrOut>(), Rinv, Msel_d,
+           Msel_d + (size_t)b * m, Msel_d + (size_t)b * m + m);
+    std::vector<double> theta_out(m, 0.0);
+    CK(cudaMemcpyAsync(theta_out.data(), Msel_d + (size_t)b * m + m, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    const bool vdev = V && is_device_ptr(V), zdev = Z && is_device_ptr(Z);
+    const size_t vbytes = (size_t)n * m * sizeof(float);
+    float* Vd = vdev ? V : (h->vtmp.ensure(vbytes), h->vtmp.as<float>());
+    float* Zd = zdev ? Z : (Z ? (h->ztmp.ensure(vbytes), h->ztmp.as<float>()) : nullptr);
+    const double* theta = Msel_d + (size_t)b * m + m;
+    rotate(h, b, m, m, (const float*)Yc, (const double*)Msel_d, Vd, (const double*)(Msel_d + (size_t)b * m), false, st);
+    // the sign rule over all ranks' rows
+    h->apidx.ensure(kRedBlocks * kMaxB * sizeof(long long));
+    h->sign.ensure(kMaxB * sizeof(float));
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(h->apidx.p);
+    CK(cudaMemsetAsync(keys, 0, m * sizeof(unsigned long long), st));
+    launch(k_col_key, dim3((unsigned)std::min<int64_t>(4 * 148, (n * m + 255) / 256)), dim3(256), 0, st, n, m,
+           (const float*)Vd, h->row0, keys);
+    if (h->comm) NK(nc->allReduce(keys, keys, (size_t)m, ncclUint64, ncclMax, comm, st));
+    launch(k_key_sign, dim3(1), dim3(64), 0, st, n, m, (const float*)Vd, h->row0, (const unsigned long long*)keys,
+           h->sign.as<float>());
+    sum(h->sign.p, (size_t)m, ncclFloat32);
+    launch(k_finalize, dim3((unsigned)std::min<int64_t>(4 * 148, (n * m + 255) / 256)), dim3(256), 0, st, n, m,
+           (const float*)h->sign.as<float>(), theta, Vd, Zd);
+    gram(h, m, Vd, nullptr, st);
+    sum(h->G.p, (size_t)m * m, ncclFloat64);
+    std::vector<double> gv((size_t)m * m);
+    CK(cudaMemcpyAsync(gv.data(), h->G.p, gv.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (V && !vdev) CK(cudaMemcpyAsync(V, Vd, vbytes, cudaMemcpyDeviceToHost, st));
+    if (Z && !zdev) CK(cudaMemcpyAsync(Z, Zd, vbytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(e1, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    double orth = 0.0;
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) orth = std::max(orth, std::fabs(gv[i * m + j] - (i == j ? 1.0 : 0.0)));
+    int n_neg = 0;
+    for (int j = 0; j < m; ++j) {
+        eigvals[j] = theta_out[j];
+        if (theta_out[j] < 0.0) ++n_neg;
+    }
+    if (info) {
+        info->iters = it;
+        info->n_applies = it;
+        info->n_negative = n_neg;
+        info->converged = converged ? 1 : 0;
+        info->max_residual = rr_host.maxres;
+        info->orth_error = orth;
+        info->gpu_ms = ms;
+    }
+    if (tol > 0.0 && !converged)
+        return fail(SBMDS_ENOCONV, "no convergence in %d iterations (residual %g)", max_iters, rr_host.maxres);
+    return SBMDS_OK;
+}
+}  // namespace
+
 extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t max_iters, double tol, uint64_t seed,
                                    const float* X0, double* eigvals, float* V, float* Z, sbmds_info* info,
                                    void* cuda_stream) {
@@ -2873,7 +3028,24 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
 
     Nvtx nv_eigs("sbmds_eigs");
     if (!h) return fail(SBMDS_EINVAL, "NULL handle");
-    if (h->shard) return fail(SBMDS_EINVAL, "sbmds_eigs on a shard handle is not built (sharded apply only)");
+    if (h->shard) {
+        if (h->world > 1 && !h->comm)
+            return fail(SBMDS_EINVAL, "sbmds_eigs on a shard handle (world %d) needs an attached communicator", h->world);
+        if (h->solver == 1) return fail(SBMDS_EINVAL, "the block Lanczos solver is not sharded");
+        if (block < 1 || block > kMaxB || block >= h->n_global || m < 1 || m > block || max_iters < 1 || !eigvals)
+            return fail(SBMDS_EINVAL, "need 1 <= m <= block <= 64, block < n, max_iters >= 1, eigvals");
+        cudaStream_t sst = reinterpret_cast<cudaStream_t>(cuda_stream);
+        DevGuard gs(h->dev);
+        try {
+            ensure_dq(h, sst);
+            return eigs_shard(h, m, block, max_iters, tol, seed, X0, eigvals, V, Z, info, sst);
+        } catch (const CudaError& e) {
+            if (e.e == cudaErrorMemoryAllocation) return fail(SBMDS_ENOMEM, "device allocation failed (%s)", e.what);
+            return fail(SBMDS_ECUDA, "%s: %s%s", e.what, cudaGetErrorString(e.e), hang_note().c_str());
+        } catch (const NcclError& e) {
+            return fail(SBMDS_ECUDA, "%s: %s", e.what, nccl_api().errorString(e.r));
+        }
+    }
     if (block < 1 || block > kMaxB || block >= h->n) return fail(SBMDS_EINVAL, "need 1 <= block <= 64, block < n");
     if (m < 1 || m > block) return fail(SBMDS_EINVAL, "need 1 <= m <= block");
     if (max_iters < 1) return fail(SBMDS_EINVAL, "need max_iters >= 1");
@@ -2934,7 +3106,7 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
             } else
             CK(cudaMemcpyAsync(Yc, X0, (size_t)n * b * sizeof(float), cudaMemcpyDefault, st));
         } else {
-            launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, Yc);
+            launch(k_init_philox, dim3(4 * 148), dim3(256), 0, st, n, b, seed, Yc, (int64_t)0);
         }
         gram(h, b, Yc, nullptr, st, true);
         chol(h, b, st);

@@ -104,8 +104,6 @@ def test_nccl_world1_apply():
         h.attach_nccl(nccl_unique_id())
         Y = h.apply(torch.from_numpy(X).cuda()).cpu().numpy()
         assert h.stat("dstream_path") == 3
-        with pytest.raises(SbmdsError, match="EINVAL"):
-            h.eigs(3, 16)
     Ys, _ = staged_apply(p, 1, X)
     assert relerr(Y, oracle_apply(p, X)) <= TOL
     assert np.array_equal(Y, Ys)
@@ -119,6 +117,8 @@ def test_shard_apply_needs_a_communicator():
     with shard_from_problem(p, 1, 2) as h:
         with pytest.raises(SbmdsError, match="EINVAL"):
             h.apply(torch.zeros((h.n, 4), device="cuda"))
+        with pytest.raises(SbmdsError, match="EINVAL"):
+            h.eigs(3, 8)
 
 
 def _manual_shards(p, cuts, device="cuda"):
@@ -179,3 +179,31 @@ def test_uneven_partitions_and_host_inputs(cuts_frac, b, device):
     got = np.vstack([Y.cpu().numpy() for Y in Ys])
     assert paths == [3] * W
     assert relerr(got, oracle_apply(p, X)) <= TOL
+
+
+@pytest.mark.parametrize("cfg,nccl", [(1, False), (2, True), (2, False)])
+def test_sharded_eigensolver_world1(cfg, nccl):
+    """The sharded subspace iteration (local rows, allreduced Grams, the global sign rule) on a
+    world-1 shard -- with the NCCL communicator attached (every allreduce issued) or without --
+    against the oracle's eigenpairs; a warm start and the Philox start both."""
+    import torch
+    from paper_1705_10887_b200.sbmds import nccl_unique_id, shard_from_problem
+    p = configs.config(cfg)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    lam_o, V_o = (O.eigs_dense(S, p.D, p.m)[:2] if cfg == 1 else O.eigs_matfree(S, p.D, p.m)[:2])
+    with shard_from_problem(p, 0, 1) as h:
+        if nccl:
+            h.attach_nccl(nccl_unique_id())
+        lam, V, Z, info = h.eigs(p.m, p.block, max_iters=500, tol=1e-6)
+        X0 = torch.from_numpy(configs.x_block(p.n, p.block, seed=2)).cuda()
+        lam2, _, _, info2 = h.eigs(p.m, p.block, max_iters=500, tol=1e-6, X0=X0)
+    V = V.cpu().numpy().astype(np.float64)
+    Z = Z.cpu().numpy().astype(np.float64)
+    assert info["converged"] == 1 and info2["converged"] == 1
+    for l_ in (lam, lam2):
+        assert np.all(np.abs(l_ - lam_o) <= 1e-4 * np.abs(lam_o)), (l_, lam_o)
+    assert O.principal_angle(V, V_o) <= 1e-3
+    assert np.abs(V.T @ V - np.eye(p.m)).max() < 1e-5
+    for j in range(p.m):
+        assert V[np.argmax(np.abs(V[:, j])), j] > 0
+    assert np.allclose(Z, V * np.sqrt(np.maximum(lam, 0))[None, :], rtol=1e-5, atol=1e-7)
