@@ -154,3 +154,77 @@ def test_split_rows_balances_entries():
     from paper_1705_10887_b200._lib import lib
     assert lib().sbmds_shard_tiles(100, 5, 2, 2, None, 0) < 0        # rank outside the world
     assert lib().sbmds_shard_plan_selfcheck(100, 5, 51, 4, 1, 0, 0) < 0
+
+
+def _eigs_worker(rank, port, q):
+    """The sharded subspace iteration's reduction plan (sbmds.cu eigs_shard) in fp64 with gloo:
+    local rows of the iterate, s / Y1 / Y2 | t / G / H' summed over the ranks, t_g = (D w_g)^T Y1
+    R^-1 for the folded iterate X = Y R^-1, Cholesky and Rayleigh-Ritz identical on every rank."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2",
+                      LOCAL_RANK=str(rank))
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from gen import configs
+    from paper_1705_10887_b200.sbmds import split_rows
+    dist.init_process_group("gloo")
+    try:
+        p = configs.config(1)
+        n, l, b, m = p.n, p.l, p.block, p.m
+        r0, r1 = split_rows(p.row_ptr, 2)[rank]
+        rp = np.asarray(p.row_ptr)
+        Sg = np.zeros((r1 - r0, l))
+        for i in range(r0, r1):
+            for e in range(rp[i], rp[i + 1]):
+                Sg[i - r0, p.col_idx[e]] += np.float32(p.val[e])
+        D = p.D.astype(np.float64)
+        wg = Sg.sum(0) / n
+        vg = D @ wg
+
+        def ar(a):
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+            dist.all_reduce(t)
+            return t.numpy()
+
+        Y = np.random.default_rng(7).standard_normal((n, b))[r0:r1]    # the global start's rows
+        G = ar(Y.T @ Y)
+        s = ar(Y.sum(0))
+        for it in range(60):
+            R = np.linalg.cholesky(G).T                                   # G = R^T R
+            Ri = np.linalg.inv(R)
+            Y1 = ar(Sg.T @ Y - np.outer(wg, s))
+            Y2 = D @ (Y1 @ Ri)                                            # (each rank's tiles, summed)
+            t = ar((vg @ Y1) @ Ri)
+            Yn = -0.5 * (Sg @ Y2 - t[None, :])
+            G = ar(Yn.T @ Yn)
+            Hp = ar(Y.T @ Yn)
+            s = ar(Yn.sum(0))
+            Y = Yn
+            Yprev_Ri = Ri
+        H = Yprev_Ri.T @ Hp                                                # X^T B~ X with X = Y_k R^-1
+        theta = np.sort(np.linalg.eigvalsh(0.5 * (H + H.T)))[::-1][:m]
+        q.put((rank, theta))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_sharded_eigensolver_plan_world2():
+    sys.path.insert(0, ROOT)
+    from gen import configs
+    from oracle import sbmds_oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=_eigs_worker, args=(r, port, q)) for r in range(2)]
+    for p_ in ps:
+        p_.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p_ in ps:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    p = configs.config(1)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    lam_o = O.eigs_dense(S, p.D, p.m)[0]
+    assert np.array_equal(res[0], res[1])                                 # both ranks, the same problem
+    assert np.all(np.abs(res[0] - lam_o) <= 1e-8 * np.abs(lam_o)), (res[0], lam_o)
