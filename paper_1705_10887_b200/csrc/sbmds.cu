@@ -2918,10 +2918,12 @@ sbmds_status eigs_shard(sbmds_ctx* h, int m, int b, int max_iters, double tol, u
     for (; it <= max_iters; ++it) {
         const bool do_rr = (it % h->rr_period == 0) || it == max_iters;
         // Y_{k+1} = B~ (Y_k R^-1): s = 1^T Y_k came with the Gram
-        spmm_csc(h, b, bp, Yc, st);                                     // Y1_g = S_g^T Y_k - w_g s^T
+        profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, Yc, st); });   // Y1_g = S_g^T Y_k - w_g s^T
         sum(h->Y1.p, (size_t)h->l * bp, ncclFloat32);
-        launch(k_vdot, dim3(1), dim3(256), 0, st, h->l, b, bp, (const double*)h->vg.as<double>(),
-               (const float*)h->Y1.as<float>(), h->tsave.as<double>());   // v_g^T Y1 (before the fold)
+        profiled(h->prof, PK_SPLIT, st, [&] {
+            launch(k_vdot, dim3(1), dim3(256), 0, st, h->l, b, bp, (const double*)h->vg.as<double>(),
+                   (const float*)h->Y1.as<float>(), h->tsave.as<double>());   // v_g^T Y1 (before the fold)
+        });
         if (takes_sym(h, bp, true) || h->rank == 0) {
             dstream(h, b, bp, st, Rinv);
         } else {
@@ -2934,7 +2936,7 @@ sbmds_status eigs_shard(sbmds_ctx* h, int m, int b, int max_iters, double tol, u
             NK(nc->allReduce(h->t.p, h->t.p, (size_t)b, ncclFloat64, ncclSum, comm, st));
             NK(nc->groupEnd());
         }
-        spmm_csr(h, b, bp, Yn, st);                                     // local rows of Y_{k+1}
+        profiled(h->prof, PK_CSR, st, [&] { spmm_csr(h, b, bp, Yn, st); });   // local rows of Y_{k+1}
         grams(Yn, do_rr ? Yc : nullptr);
         if (do_rr) {
             launch(k_rr, dim3(1), dim3(256), (size_t)kRrSmem, st, b, m, tol, (const double*)h->H.as<double>(),
