@@ -533,15 +533,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                const float* __restrict__ rs1, const int32_t* __restrict__ ppos,
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
-               unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int stream_only,
+               unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int mode,
                double* __restrict__ Rinv_next, int* __restrict__ status, int defer_gram) {
     using C = Sp8Cfg<BP>;
-    // (diagnostics) trace[ev * 64 + i]: globaltimer of event ev for block i < 64 of CTA 0
+    // (diagnostics) trace[ev * 64 + i] (ev < 12; 2048 + (ev - 12) * 64 + i for ev 12..19):
+    // globaltimer of event ev for block i < 64 of CTA 0
 #define SP8_TR(ev, i)                                                                          \
     if (trace && blockIdx.x == 0 && (i) < 64) {                                                \
         unsigned long long t_;                                                                 \
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                 \
-        trace[(ev) * 64 + (i)] = t_;                                                           \
+        trace[((ev) < 12 ? (ev) * 64 : 2048 + ((ev) - 12) * 64) + (i)] = t_;                    \
     }
     constexpr int NB = C::NB;
     constexpr int NCB = BP / 8;
@@ -565,6 +566,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* yp_full = bars + 26;
     uint64_t* yp_empty = bars + 28;
     uint64_t* ey_full = bars + 38;      // [4] eyb[k % 4] written (lanes c < BP of the 4 epilogue warps)
+    uint64_t* ey_empty = bars + 6;      // [4] eyb[k % 4] read by the T drain (group B's 4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
     int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
     int* eyb = ey2 + BP;                                   // [4][4][BP] exponents of Y_B per block (ring) and warp
@@ -574,6 +576,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     const int64_t b0 = blockIdx.x * nblk / gridDim.x, b1 = (blockIdx.x + 1) * nblk / gridDim.x;
     const int nb = (int)(b1 - b0);
     const bool want_t = P1 != nullptr;
+    const bool stream_only = (mode & 1) != 0;    // (diagnostics) images streamed, no MMA
+    const unsigned poll_ns = (unsigned)mode >> 8;   // MMA warp: back-off between unready polls
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < 3; ++s) {
@@ -581,9 +585,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_init(&empty_img[s], 1);
         }
         for (int a = 0; a < C::NBN; ++a) {
-            mbar_init(&bn_full[a], 128);
+            mbar_init(&bn_full[a], 32);   // the producer warp's lanes
             mbar_init(&bn_empty[a], 1);
             mbar_init(&ey_full[a], 2 * BP);   // one warp per pair, 8 lanes per half
+            mbar_init(&ey_empty[a], 4);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&an_full[a], 1);
@@ -630,18 +635,6 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     };
     if (blockIdx.x < 256) tail_tr(768 + blockIdx.x);
     if (threadIdx.x < BP) ey2[threadIdx.x] = ey2in[threadIdx.x];
-    if (warp >= 2 && warp < 14) {   // c3 groups of every accumulator start at zero
-        const uint32_t lo = (uint32_t)(32 * (warp & 3)) << 16;
-        if (warp < 10) {
-            const uint32_t cb = (uint32_t)(8 * ((warp - 2) >> 2));
-            tmem_zero8(tbase + lo + C::ACCN + 3 * BP + cb);
-            tmem_zero8(tbase + lo + C::ACCN + C::ACCW + 3 * BP + cb);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) tmem_zero16(tbase + lo + C::ACCT + j * C::ACCW + 3 * BP);   // T[2][2]
-        }
-        tmem_wait_st_();
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -662,10 +655,42 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     for (int c = 0; c < NCB; ++c) csum[c] = 0.0;
 
     if (warp == 0) {
-        // ------------------------------------------------ producer
-        if (lane == 0) {
-            for (int i = 0; i < nb; ++i) {
-                const int64_t B = b0 + i;
+        // ------------------------------------------------ producer: B operand of N (all lanes: the
+        // dictionary's Y2 digit rows, cp.async, lane g owning entries g, g + 32, ...) and the image
+        // (lane 0, one bulk copy) of each block. B(i) needs N(i - NBN) done, image(i) T(i - 3):
+        // neither waits on the epilogue or the T drain, so staging never trails the pipeline.
+        int32_t s_d0 = m_doff[0], s_du = nb > 0 ? m_doff[1] - s_d0 : 0;
+        int32_t s_j[kSp8DK / 32];
+#pragma unroll
+        for (int u = 0; u < kSp8DK / 32; ++u) s_j[u] = (32 * u + lane < s_du) ? __ldg(dict + s_d0 + 32 * u + lane) : 0;
+        for (int i = 0; i < nb; ++i) {
+            const int64_t B = b0 + i;
+            const int32_t du = s_du;
+            int32_t j[kSp8DK / 32];
+#pragma unroll
+            for (int u = 0; u < kSp8DK / 32; ++u) j[u] = s_j[u];
+            if (i + 1 < nb) {   // the next block's dictionary rows of this lane
+                s_d0 = m_doff[i + 1];
+                s_du = m_doff[i + 2] - s_d0;
+#pragma unroll
+                for (int u = 0; u < kSp8DK / 32; ++u) s_j[u] = (32 * u + lane < s_du) ? __ldg(dict + s_d0 + 32 * u + lane) : 0;
+            }
+            if (!stream_only) {
+                const int sb = i % C::NBN;
+                mbar_wait(&bn_empty[sb], ((uint32_t)((i / C::NBN) & 1)) ^ 1u, 154 * 65536 + (i & 0xFFFF));
+                uint8_t* bn = base + C::OFF_BN + sb * C::BN;
+#pragma unroll
+                for (int u = 0; u < kSp8DK / 32; ++u) {
+                    const int g = 32 * u + lane;
+                    if (g < du) {
+#pragma unroll
+                        for (int pl = 0; pl < 3; ++pl) cp_async16(bn + sp8_boff<NB>(g, pl), Yd + (pl * l_rows + j[u]) * 16);
+                    }
+                }
+                cp_async_arrive_noinc(&bn_full[sb]);
+                if (lane == 0) SP8_TR(7, i);
+            }
+            if (lane == 0) {
                 const int s = i % 3;
                 const uint32_t ph = (uint32_t)((i / 3) & 1);
                 const uint32_t bytes = (uint32_t)(3 * kSp8RB * dpad_of(B));
@@ -675,6 +700,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 bulk_load(base + s * C::IMG, gimg + m_ioff[i], bytes, &full_img[s]);
                 SP8_TR(0, i);
             }
+            __syncwarp();
         }
     } else if (warp == 1 && stream_only) {
         // (diagnostics) consume the images without any MMA; the other roles idle
@@ -689,9 +715,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         // ------------------------------------------------ MMA issue: N(i), then T(i - 1)
         // d0 x [y0|y1|y2] -> groups 0-2, d1 x [y0|y1|y2] -> 1-3, d2 x [y0|y1] -> 2-3
         constexpr uint32_t id1n = idesc_i8_bmn(128, NB, 0), id2n = idesc_i8_bmn(128, NB, 0),
-                           id3n = idesc_i8_bmn(128, 2 * BP, 0);
+                           id3n = idesc_i8_bmn(128, 2 * BP, 0), id0n = idesc_i8_bmn(128, BP, 0);
         constexpr uint32_t id1t = idesc_i8_bmn(128, NB, 1), id2t = idesc_i8_bmn(128, NB, 1),
-                           id3t = idesc_i8_bmn(128, 2 * BP, 1);
+                           id3t = idesc_i8_bmn(128, 2 * BP, 1), id0t = idesc_i8_bmn(128, BP, 1);
         constexpr uint32_t KG = NB / 16 * 128;   // B: bytes per 8-row K group (the LBO)
         // Both products are issued as soon as their operands are ready (polled, non-blocking):
         // T(i) does not wait behind N(i + 1), so an image stage is released as early as possible.
@@ -717,8 +743,15 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue quadrant j's) per MMA
                     const uint32_t d = tbase + (uint32_t)(C::ACCT + (2 * a + (j >> 1)) * C::ACCW);
                     const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
-                    tc_mma_i8(d, umma_desc_none(sa + 512 * j, 128, 2048), bd, id1t, (j & 1) ? 1u : 0u);
-                    tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
+                    const uint64_t a0 = umma_desc_none(sa + 512 * j, 128, 2048);
+                    if (j & 1) {
+                        tc_mma_i8(d, a0, bd, id1t, 1u);
+                        tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
+                    } else {   // chain start: every group initialised by an MMA (no TMEM zeroing)
+                        tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 0u);
+                        tc_mma_i8(d, a0, bd, id0t, 0u);
+                        tc_mma_i8(d + BP, a0, umma_desc_none(sb + 4 * KG * j + 128, KG, 128), id3t, 1u);
+                    }
                     tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
                 }
                 tc_commit(&at_full[a]);
@@ -741,8 +774,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             if (elect_one()) {
                 for (int j = 0; j < dp / 32; ++j) {   // K = 32 dictionary entries per MMA
                     const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
-                    tc_mma_i8(d, umma_desc_none(sa + 4096 * j, 2048, 128), bd, id1n, j > 0 ? 1u : 0u);
-                    tc_mma_i8(d + BP, umma_desc_none(sa + plane + 4096 * j, 2048, 128), bd, id2n, 1u);
+                    const uint64_t a0 = umma_desc_none(sa + 4096 * j, 2048, 128);
+                    if (j > 0) {
+                        tc_mma_i8(d, a0, bd, id1n, 1u);
+                        tc_mma_i8(d + BP, umma_desc_none(sa + plane + 4096 * j, 2048, 128), bd, id2n, 1u);
+                    } else {   // chain start: d1 [y0|y1|y2] initialises groups 1-3, d0 y0 group 0,
+                               // then d0 [y1|y2] accumulates into groups 1-2 (no TMEM zeroing)
+                        tc_mma_i8(d + BP, umma_desc_none(sa + plane, 2048, 128), bd, id2n, 0u);
+                        tc_mma_i8(d, a0, bd, id0n, 0u);
+                        tc_mma_i8(d + BP, a0, umma_desc_none(sb + 128, KG, 128), id3n, 1u);
+                    }
                     tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 4096 * j, 2048, 128), bd, id3n, 1u);
                 }
                 tc_commit(&an_full[a]);
@@ -763,7 +804,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             } else if (nN < nb && __all_sync(0xffffffffu, ready_n(nN))) {
                 issue_n(nN++);
                 spin = 0;
-            } else if ((spin & 4095u) == 4095u) {   // watchdog, as mbar_wait
+            } else if (poll_ns) {
+                __nanosleep(poll_ns);
+            }
+            if ((spin & 4095u) == 4095u) {   // watchdog, as mbar_wait
                 uint64_t t;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
                 if (t - t_start > 4000000000ull)
@@ -793,6 +837,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < HC; ++c) sce[c] = pow2f2(16 - eS - ey2[cb + c]);
             const float rsm1 = r < rows ? __ldg(rs1 + B * kSp8RB + r) : 0.f;
+            if (r == 32 && hf == 0) SP8_TR(18, i);
             mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             if (r == 0 && hf == 0) SP8_TR(3, i);
@@ -804,11 +849,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 tmem_ld8_u(col + 2 * BP, g2);
                 tmem_ld8_u(col + 3 * BP, g3);
                 tmem_wait_ld();
-                tmem_zero8(col + 3 * BP);
-                tmem_wait_st_();
             }
             tc_fence_before();
             mbar_arrive(&an_empty[a]);
+            if (r == 0 && hf == 0) SP8_TR(11, i);
             // Y = -1/2 (S Y2 - 1 t^T) = -1/2 (S (Y2 - 1 t^T) + (S 1 - 1) t^T) for this row
             float y[HC];
             const bool live = r < rows;
@@ -838,7 +882,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 const int pr = q >> 1;
                 float* pm = reinterpret_cast<float*>(eyb + 4 * 2 * BP) + ((a * 2 + hf) * 4 + q) * HC;   // [2][2][4][HC]
                 if ((lane & 3) == 0) pm[cl] = m[0];
+                if (r == 32 && hf == 0) SP8_TR(19, i);
                 named_bar(1 + 2 * hf + pr, 64);
+                if (r == 0 && hf == 0) SP8_TR(12, i);
                 const float mp = fmaxf(m[0], pm[((q ^ 1) - q) * HC + cl]);
                 const int my_e = i8_scale_exp(mp);   // exponent of column cb + cl for the pair's 64 rows
                 int ey[HC];
@@ -846,6 +892,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 for (int c = 0; c < HC; ++c)   // lane holding column c: bits 4..2 = c's bits 2..0
                     ey[c] = __shfl_sync(0xffffffffu, my_e, ((c >> 2) & 1) << 4 | ((c >> 1) & 1) << 3 | (c & 1) << 2);
                 if ((q & 1) == 0 && (lane & 3) == 0) {   // published for group B's T drain of this block
+                    mbar_wait(&ey_empty[i & 3], ((uint32_t)((i >> 2) & 1)) ^ 1u, 157 * 65536 + (i & 0xFFFF));
+                    if (r == 0 && hf == 0) SP8_TR(13, i);
                     eyb[((i & 3) * 2 + pr) * BP + cb + cl] = my_e;
                     mbar_arrive(&ey_full[i & 3]);
                 }
@@ -855,6 +903,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 uint2 w0, w1, w2;
                 digit_rows8(y, ysc, w0, w1, w2);
                 mbar_wait(&bt_empty[a], pa ^ 1u, 151 * 65536 + (i & 0xFFFF));
+                if (r == 0 && hf == 0) SP8_TR(14, i);
                 uint8_t* bt = base + C::OFF_BT + a * C::BT;
                 *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 0) + cb) = w0;
                 *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 1) + cb) = w1;
@@ -869,7 +918,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 dst[0] = make_float4(y[0], y[1], y[2], y[3]);
                 dst[1] = make_float4(y[4], y[5], y[6], y[7]);
             }
+            if (r == 0 && hf == 0) SP8_TR(15, i);
             mbar_wait(&yr_empty[a], pa ^ 1u, 150 * 65536 + (i & 0xFFFF));
+            if (r == 0 && hf == 0) SP8_TR(16, i);
             {
                 float4* yr = reinterpret_cast<float4*>(reinterpret_cast<float*>(base + C::OFF_YR + a * C::YR) + r * BP + cb);
                 yr[0] = make_float4(y[0], y[1], y[2], y[3]);
@@ -878,18 +929,18 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_arrive(&yr_full[a]);
         }
     } else if (warp < 14) {
-        // ------------------------------------------------ group B (warps 10-13): B operand of N, T accumulator -> P1
+        // ------------------------------------------------ group B (warps 10-13): T accumulator -> P1
         const int gt = threadIdx.x - 320;   // 0..127 (T accumulator: TMEM lane = dictionary entry gt)
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-        // T accumulator of block i -> P1 partials, scaled by A's exponents of Y_B (ey ring of 4:
-        // A runs at most two blocks ahead of this group, so neither the ring slot nor the phase
-        // of ey_full can be reused before it is read); d0 / du / eS of that block are passed in
-        auto drain_t = [&](int i, int32_t d0, int32_t du, int eS) {
+        // T accumulator of block i -> P1 partials, scaled by A's exponents of Y_B (ey ring of 4,
+        // ey_full / ey_empty); the P1 slot of this thread, du and eS of that block are passed in
+        auto drain_t = [&](int i, int32_t pos, int32_t du, int eS) {
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
             mbar_wait(&ey_full[i & 3], (uint32_t)((i >> 2) & 1), 155 * 65536 + (i & 0xFFFF));
             mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
             tc_fence_after();
+            if (threadIdx.x == 320) SP8_TR(17, i);
             const int lrow = 32 * (warp & 3) + lane;   // the TMEM lane (dictionary entry) this thread drains
             float out[BP];
 #pragma unroll
@@ -906,57 +957,35 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                     tmem_ld8_u(tbase + lane_off + col + 3 * BP + c0, *reinterpret_cast<int(*)[8]>(&g3[c0]));
                 }
                 tmem_wait_ld();
-                tmem_zero16(tbase + lane_off + col + 3 * BP);
-                tmem_wait_st_();
                 const int* ey = eyb + ((i & 3) * 2 + j) * BP;
 #pragma unroll
                 for (int c = 0; c < BP; ++c) out[c] += acc4f(g0[c], g1[c], g2[c], g3[c], pow2f2(16 - eS - ey[c]));
             }
             tc_fence_before();
             mbar_arrive(&at_empty[a]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ey_empty[i & 3]);   // this warp has read eyb[i % 4]
             if (lrow < du) {
-                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)__ldg(ppos + d0 + lrow) * BP);
+                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)pos * BP);
 #pragma unroll
                 for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]);
             }
         };
-        // B_N of block k: thread g copies dictionary entry g's three 16-byte digit rows
-        // asynchronously; bn_full completes when every thread's copies have landed. The
-        // dictionary index of the next block is loaded one staging ahead.
-        int32_t s_d0 = m_doff[0], s_du = nb > 0 ? m_doff[1] - s_d0 : 0;
-        int64_t s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
-        auto stage = [&](int k) {
-            const int64_t B = b0 + k;
-            const int32_t d0 = s_d0, du = s_du;
-            const int64_t j = s_j;
-            if (k + 1 < nb) {   // prefetch the next block's dictionary row of this thread
-                s_d0 = m_doff[k + 1];
-                s_du = m_doff[k + 2] - s_d0;
-                s_j = (gt < s_du) ? __ldg(dict + s_d0 + gt) : 0;
-            }
-            const int sb = k % C::NBN;
-            mbar_wait(&bn_empty[sb], ((uint32_t)((k / C::NBN) & 1)) ^ 1u, 154 * 65536 + (k & 0xFFFF));
-            uint8_t* bn = base + C::OFF_BN + sb * C::BN;
-            if (gt < du) {
-#pragma unroll
-                for (int pl = 0; pl < 3; ++pl) cp_async16(bn + sp8_boff<NB>(gt, pl), Yd + (pl * l_rows + j) * 16);
-            }
-            cp_async_arrive_noinc(&bn_full[sb]);
-            if (gt == 0) SP8_TR(7, k);
-        };
-        if (nb > 0) stage(0);
-        if (nb > 1) stage(1);
-        int32_t p_d0 = m_doff[0], p_du = nb > 0 ? m_doff[1] - p_d0 : 0;
+        int32_t p_d0 = nb > 0 ? m_doff[0] : 0, p_du = nb > 0 ? m_doff[1] - p_d0 : 0;
         int p_eS = nb > 0 ? m_es[0] : 0;
+        const int lrow = 32 * (warp & 3) + lane;
+        int32_t p_pos = (nb > 0 && lrow < p_du) ? __ldg(ppos + p_d0 + lrow) : 0;
         for (int i = 0; i < nb; ++i) {
-            if (i + 2 < nb) stage(i + 2);
-            if (want_t) drain_t(i, p_d0, p_du, p_eS);
-            if (gt == 0) SP8_TR(6, i);
-            if (i + 1 < nb) {
+            const int32_t du = p_du, pos = p_pos;
+            const int eS = p_eS;
+            if (i + 1 < nb) {   // the next block's P1 slot of this thread, one block ahead
                 p_d0 = m_doff[i + 1];
                 p_du = m_doff[i + 2] - p_d0;
                 p_eS = m_es[i + 1];
+                p_pos = (lrow < p_du) ? __ldg(ppos + p_d0 + lrow) : 0;
             }
+            if (want_t) drain_t(i, pos, du, eS);
+            if (lane == 0 && warp == 10) SP8_TR(6, i);
         }
     } else {
         // ------------------------------------------------ group C (warps 14-15): the Grams on the FP64 tensor cores

@@ -503,6 +503,7 @@ struct sbmds_ctx {
     int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product,
                            // 2 = timeline of CTA 0, 4 = stream the images only, 8 = T product in the last iteration too,
                            // 16 = no H' (as between Rayleigh-Ritz steps)
+    int sp8_poll = 0;      // k_sp8_step: the MMA warp's back-off (ns) between unready polls
     int64_t s8_bytes = 0;
     // D_ll
     float* D = nullptr;
@@ -1511,7 +1512,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     launch_pdl(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
            (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2mm, ey2,
            h->s8yd.as<uint8_t>(), h->y16aux.as<unsigned int>() + 64);
-    if (h->sp8_dbg & 2) h->s8trace.ensure((12 * 64 + 1280) * sizeof(unsigned long long));
+    if (h->sp8_dbg & 2) h->s8trace.ensure((2048 + 8 * 64) * sizeof(unsigned long long));
     auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
     // non-Rayleigh-Ritz eigs steps whose next apply folds through k_blk_reduce_fold (sym8 D
     // stream) leave E2/E3 to that fold (off this kernel's tail)
@@ -1524,7 +1525,8 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            (const int32_t*)h->s8pos.as<int32_t>(), Y,
            want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
-           h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr, (h->sp8_dbg & 4) ? 1 : 0,
+           h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr,
+           ((h->sp8_dbg & 4) ? 1 : 0) | (h->sp8_poll << 8),
            with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>(), defer ? 1 : 0);
     h->gram_deferred = defer;
     h->gram_parts = grid;
@@ -3912,6 +3914,9 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "lanczos_blocks")) {
         if (value < 0 || value > 32) return fail(SBMDS_EINVAL, "lanczos_blocks in [0, 32] (0: 64 / block)");
         h->lz_blocks = (int)value;
+    } else if (!strcmp(key, "sp8_poll")) {
+        if (value < 0 || value > 100000) return fail(SBMDS_EINVAL, "sp8_poll must be in [0, 100000] ns");
+        h->sp8_poll = (int)value;
     } else if (!strcmp(key, "sp8_dbg")) {
         h->sp8_dbg = (int)value;
     } else if (!strcmp(key, "fuse")) {
@@ -3960,7 +3965,7 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_slots")) *value = h->sp8_state > 0 ? (int64_t)h->s8.total_u : -1;   // 128-row dictionary entries
     else if (!strncmp(key, "sp8_trace_", 10)) {   // (diagnostics, sp8_dbg & 2) event timestamps of CTA 0
         const int k = atoi(key + 10);
-        if (k < 0 || k >= 12 * 64 + 1280 || !h->s8trace.p) return fail(SBMDS_EINVAL, "no sp8 trace");
+        if (k < 0 || k >= 2048 + 8 * 64 || !h->s8trace.p) return fail(SBMDS_EINVAL, "no sp8 trace");
         unsigned long long v = 0;
         if (cudaMemcpy(&v, h->s8trace.as<unsigned long long>() + k, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess)
             return fail(SBMDS_ECUDA, "sp8 trace read");

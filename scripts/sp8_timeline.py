@@ -6,18 +6,20 @@ import torch
 from gen import configs
 from paper_1705_10887_b200 import from_problem
 EV = ["load_issued", "N_start", "T_start", "A_got_N", "A_digits", "C_gram", "B_T_drained", "B_staged",
-      "prod_empty_ok", "prod_yp_ok", "T_issued"]
+      "prod_empty_ok", "prod_yp_ok", "T_issued", "A_tmem", "A_pairbar", "A_eyempty", "A_btempty", "A_ystored",
+      "A_yrempty", "B_atfull", "A5_pre_N", "A5_prebar"]
 p = configs.config(4)
 with from_problem(p) as h:
     h.eigs(p.m, p.block, max_iters=4, tol=0.0)
-    h.set_option("sp8_dbg", 2)
+    h.set_option("sp8_dbg", int(sys.argv[1]) if len(sys.argv) > 1 else 10)
+    h.set_option("sp8_poll", int(sys.argv[2]) if len(sys.argv) > 2 else 0)
     h.eigs(p.m, p.block, max_iters=3, tol=0.0)
     torch.cuda.synchronize()
-    tr = [[h.stat(f"sp8_trace_{e * 64 + i}") for i in range(64)] for e in range(len(EV))]
+    tr = [[h.stat(f"sp8_trace_{(e * 64 if e < 12 else 2048 + (e - 12) * 64) + i}") for i in range(64)] for e in range(len(EV))]
     t0 = tr[0][0]
-    print("event  " + " ".join(f"{e[:9]:>9}" for e in EV))
+    print("event " + " ".join(f"{e[:8]:>8}" for e in EV))
     for i in range(48):
-        print(f"{i:3d}   " + " ".join(f"{(tr[e][i] - t0) / 1000:9.2f}" if tr[e][i] else "        -" for e in range(len(EV))))
+        print(f"{i:3d}   " + " ".join(f"{(tr[e][i] - t0) / 1000:8.2f}" if tr[e][i] else "       -" for e in range(len(EV))))
     starts = [h.stat(f"sp8_trace_{768 + c}") for c in range(148)]
     ends = [h.stat(f"sp8_trace_{1024 + c}") for c in range(148)]
     s0 = min(starts)
