@@ -306,9 +306,13 @@ __global__ void __launch_bounds__(256, 4) k_blk_reduce_fold(int64_t l, int64_t l
                 a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w;
             }
         }
-        for (; k < e0; ++k) {
-            const float4 t = __ldcs(base + (int64_t)k * (BP / 4));
-            a[0] += t.x; a[1] += t.y; a[2] += t.z; a[3] += t.w;
+        if (k < e0) {   // the remainder as one predicated batch (slot order kept)
+            float4 pv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) pv[u] = k + u < e0 ? __ldcs(base + (int64_t)(k + u) * (BP / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (k + u < e0) { a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w; }
         }
     };
     const bool deferred = fg.part != nullptr;
@@ -357,9 +361,14 @@ __global__ void __launch_bounds__(256, 4) k_blk_reduce_fold(int64_t l, int64_t l
                             a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w;
                         }
                     }
-                    for (; k < k1; ++k) {
-                        const float4 t = __ldcs(base + (int64_t)k * (BP / 4));
-                        a[0] += t.x; a[1] += t.y; a[2] += t.z; a[3] += t.w;
+                    if (k < k1) {   // the remainder as one predicated batch (slot order kept)
+                        float4 pv[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            pv[u] = k + u < k1 ? __ldcs(base + (int64_t)(k + u) * (BP / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (k + u < k1) { a[0] += pv[u].x; a[1] += pv[u].y; a[2] += pv[u].z; a[3] += pv[u].w; }
                     }
                 }
 #pragma unroll

@@ -411,12 +411,20 @@ __device__ __forceinline__ void dreduce16_body(int64_t l, int b, const int* __re
                     v[3] += (double)pv[u].w;
                 }
             }
-            for (; q < a1; ++q) {
-                const float4 pv = __ldcs(base + (int64_t)q * (128 * BP / 4));
-                v[0] += (double)pv.x;
-                v[1] += (double)pv.y;
-                v[2] += (double)pv.z;
-                v[3] += (double)pv.w;
+            if (q < a1) {   // the remainder as one predicated batch (all loads in flight; slot order kept)
+                float4 pv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    pv[u] = q + u < a1 ? __ldcs(base + (int64_t)(q + u) * (128 * BP / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (q + u < a1) {
+                        v[0] += (double)pv[u].x;
+                        v[1] += (double)pv[u].y;
+                        v[2] += (double)pv[u].z;
+                        v[3] += (double)pv[u].w;
+                    }
+                }
             }
         }
 #pragma unroll
@@ -514,14 +522,12 @@ struct Sp8Cfg {
     static constexpr int SMEM = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 16 + 1024;   // + alignment slack
     static constexpr int THREADS = 16 * 32;   // 4 warps per scheduler (<= 128 registers)
     static constexpr int NGW = 2;                        // Gram warps (group C)
-    // TMEM columns: N[2] (NB each), then T[2][4]: one T accumulator per 32-row K step, since
-    // each epilogue warp scales its own 32 rows of Y_B (no cross-warp reduction on the path)
-    // Accumulators have four 16-column groups (c0 = d0 y0, c1, c2, c3 = d1 y2 + d2 y1): N[2] and
-    // T[2][2] (double-buffered; one per 64-row K half, rows of an epilogue warp pair, which
-    // share their column scales).
+    // TMEM columns: accumulators with four 16-column groups (c0 = d0 y0, c1, c2, c3 = d1 y2 + d2 y1):
+    // N[2] and T[2] (double-buffered; one T accumulator per block, whose 128 rows share the
+    // column scales of Y_B's digits), 256 of 512 columns
     static constexpr int ACCW = 4 * BP;
     static constexpr int ACCN = 0, ACCT = 2 * ACCW;
-    static_assert(ACCT + 4 * ACCW <= 512, "tmem");
+    static_assert(ACCT + 2 * ACCW <= 512, "tmem");
     static_assert(BP == 16, "the tensor-core sparse step is built for b = 16");
 };
 
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* ey_empty = bars + 6;      // [4] eyb[k % 4] read by the T drain (group B's 4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
     int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
-    int* eyb = ey2 + BP;                                   // [4][4][BP] exponents of Y_B per block (ring) and warp
+    int* eyb = ey2 + BP;                                   // [4][BP] exponents of Y_B per block (ring)
 
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -587,7 +593,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         for (int a = 0; a < C::NBN; ++a) {
             mbar_init(&bn_full[a], 32);   // the producer warp's lanes
             mbar_init(&bn_empty[a], 1);
-            mbar_init(&ey_full[a], 2 * BP);   // one warp per pair, 8 lanes per half
+            mbar_init(&ey_full[a], BP);   // quadrant-0 warp of each half, 8 lanes
             mbar_init(&ey_empty[a], 4);
         }
         for (int a = 0; a < 2; ++a) {
@@ -741,10 +747,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             if (elect_one()) {
 #pragma unroll
                 for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue quadrant j's) per MMA
-                    const uint32_t d = tbase + (uint32_t)(C::ACCT + (2 * a + (j >> 1)) * C::ACCW);
+                    const uint32_t d = tbase + (uint32_t)(C::ACCT + a * C::ACCW);   // one accumulator per block
                     const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
                     const uint64_t a0 = umma_desc_none(sa + 512 * j, 128, 2048);
-                    if (j & 1) {
+                    if (j > 0) {
                         tc_mma_i8(d, a0, bd, id1t, 1u);
                         tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
                     } else {   // chain start: every group initialised by an MMA (no TMEM zeroing)
@@ -837,7 +843,6 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < HC; ++c) sce[c] = pow2f2(16 - eS - ey2[cb + c]);
             const float rsm1 = r < rows ? __ldg(rs1 + B * kSp8RB + r) : 0.f;
-            if (r == 32 && hf == 0) SP8_TR(18, i);
             mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             if (r == 0 && hf == 0) SP8_TR(3, i);
@@ -861,8 +866,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 y[c] = live ? fmaf(-0.5f, acc4f(g0[c], g1[c], g2[c], g3[c], sce[c]), rsm1 * mht[c]) : 0.f;
             if (want_t) {
                 // this warp's column maxima over its 32 rows (butterfly reduce-scatter: lane ends
-                // with column cl, then an all-gather of the exponents), the per-warp exponents ey
-                // (K step q of the T product has its own accumulator), the digits of Y_B
+                // with column cl, then an all-gather of the exponents), the block's exponents ey
+                // (the four quadrant warps of this column half share them: one T accumulator per
+                // block), the digits of Y_B
                 float m[HC];
 #pragma unroll
                 for (int c = 0; c < HC; ++c) m[c] = fabsf(y[c]);
@@ -878,23 +884,21 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 2));
                 m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 1));
                 const int cl = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                // the warp pair (quadrants 2p, 2p + 1) shares its column maxima: one K half
-                const int pr = q >> 1;
-                float* pm = reinterpret_cast<float*>(eyb + 4 * 2 * BP) + ((a * 2 + hf) * 4 + q) * HC;   // [2][2][4][HC]
-                if ((lane & 3) == 0) pm[cl] = m[0];
-                if (r == 32 && hf == 0) SP8_TR(19, i);
-                named_bar(1 + 2 * hf + pr, 64);
+                // the four quadrant warps of this half share their column maxima (the block's)
+                float* pm = reinterpret_cast<float*>(eyb + 4 * 2 * BP) + (a * 2 + hf) * 4 * HC;   // [2][2][4][HC]
+                if ((lane & 3) == 0) pm[q * HC + cl] = m[0];
+                named_bar(1 + hf, 128);
                 if (r == 0 && hf == 0) SP8_TR(12, i);
-                const float mp = fmaxf(m[0], pm[((q ^ 1) - q) * HC + cl]);
-                const int my_e = i8_scale_exp(mp);   // exponent of column cb + cl for the pair's 64 rows
+                const float mp = fmaxf(fmaxf(pm[cl], pm[HC + cl]), fmaxf(pm[2 * HC + cl], pm[3 * HC + cl]));
+                const int my_e = i8_scale_exp(mp);   // exponent of column cb + cl for the block's 128 rows
                 int ey[HC];
 #pragma unroll
                 for (int c = 0; c < HC; ++c)   // lane holding column c: bits 4..2 = c's bits 2..0
                     ey[c] = __shfl_sync(0xffffffffu, my_e, ((c >> 2) & 1) << 4 | ((c >> 1) & 1) << 3 | (c & 1) << 2);
-                if ((q & 1) == 0 && (lane & 3) == 0) {   // published for group B's T drain of this block
+                if (q == 0 && (lane & 3) == 0) {   // published for group B's T drain of this block
                     mbar_wait(&ey_empty[i & 3], ((uint32_t)((i >> 2) & 1)) ^ 1u, 157 * 65536 + (i & 0xFFFF));
                     if (r == 0 && hf == 0) SP8_TR(13, i);
-                    eyb[((i & 3) * 2 + pr) * BP + cb + cl] = my_e;
+                    eyb[(i & 3) * BP + cb + cl] = my_e;
                     mbar_arrive(&ey_full[i & 3]);
                 }
                 float ysc[HC];
@@ -910,6 +914,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 2) + cb) = w2;
                 fence_proxy_async();
                 mbar_arrive(&bt_full[a]);
+                if (r == 0 && hf == 1) SP8_TR(18, i);
+                if (r == 64 && hf == 1) SP8_TR(19, i);
                 if (r == 0 && hf == 0) SP8_TR(4, i);
             }
             // (after the digits, which gate the T product and the image's release)
@@ -943,12 +949,12 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             if (threadIdx.x == 320) SP8_TR(17, i);
             const int lrow = 32 * (warp & 3) + lane;   // the TMEM lane (dictionary entry) this thread drains
             float out[BP];
+            if (mode & 4) {   // (diagnostics: drain arithmetic skipped)
 #pragma unroll
-            for (int c = 0; c < BP; ++c) out[c] = 0.f;
-#pragma unroll 1
-            for (int j = 0; j < 2; ++j) {   // K half j = rows of epilogue quadrants 2j, 2j + 1 (their exponents)
+                for (int c = 0; c < BP; ++c) out[c] = 0.f;
+            } else {
                 int g0[BP], g1[BP], g2[BP], g3[BP];
-                const uint32_t col = (uint32_t)(C::ACCT + (2 * a + j) * C::ACCW);
+                const uint32_t col = (uint32_t)(C::ACCT + a * C::ACCW);
 #pragma unroll
                 for (int c0 = 0; c0 < BP; c0 += 8) {
                     tmem_ld8_u(tbase + lane_off + col + c0, *reinterpret_cast<int(*)[8]>(&g0[c0]));
@@ -957,9 +963,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                     tmem_ld8_u(tbase + lane_off + col + 3 * BP + c0, *reinterpret_cast<int(*)[8]>(&g3[c0]));
                 }
                 tmem_wait_ld();
-                const int* ey = eyb + ((i & 3) * 2 + j) * BP;
+                const int* ey = eyb + (i & 3) * BP;
 #pragma unroll
-                for (int c = 0; c < BP; ++c) out[c] += acc4f(g0[c], g1[c], g2[c], g3[c], pow2f2(16 - eS - ey[c]));
+                for (int c = 0; c < BP; ++c) out[c] = acc4f(g0[c], g1[c], g2[c], g3[c], pow2f2(16 - eS - ey[c]));
             }
             tc_fence_before();
             mbar_arrive(&at_empty[a]);
@@ -1023,10 +1029,12 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                         for (int c2 = 0; c2 < NCB; ++c2) dmma_8x8x4(ha[c * NCB + c2], xv[c], yv[c2]);
                 }
             };
+            if (!(mode & 2)) {   // (mode & 2: diagnostics, Gram skipped)
 #pragma unroll 2
-            for (int s4 = 0; s4 < 16; s4 += 2) {
-                step(s4, gacc, hacc);
-                step(s4 + 1, gacc1, hacc1);
+                for (int s4 = 0; s4 < 16; s4 += 2) {
+                    step(s4, gacc, hacc);
+                    step(s4 + 1, gacc1, hacc1);
+                }
             }
             mbar_arrive(&yr_empty[a]);
         };

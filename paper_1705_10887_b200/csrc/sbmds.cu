@@ -502,7 +502,7 @@ struct sbmds_ctx {
     DevBuf lzQ, lzW, lzC, lzT, lzGl, lzI, lzR;
     int sp8_dbg = 0;       // diagnostics (timing only, results invalid): 1 = skip the T product,
                            // 2 = timeline of CTA 0, 4 = stream the images only, 8 = T product in the last iteration too,
-                           // 16 = no H' (as between Rayleigh-Ritz steps)
+                           // 16 = no H' (as between Rayleigh-Ritz steps), 256 = no Gram, 512 = no T drain arithmetic
     int sp8_poll = 0;      // k_sp8_step: the MMA warp's back-off (ns) between unready polls
     int64_t s8_bytes = 0;
     // D_ll
@@ -1526,7 +1526,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
            h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr,
-           ((h->sp8_dbg & 4) ? 1 : 0) | (h->sp8_poll << 8),
+           ((h->sp8_dbg & 4) ? 1 : 0) | ((h->sp8_dbg >> 7) & 6) | (h->sp8_poll << 8),
            with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>(), defer ? 1 : 0);
     h->gram_deferred = defer;
     h->gram_parts = grid;

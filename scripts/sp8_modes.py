@@ -8,7 +8,7 @@ from paper_1705_10887_b200 import from_problem
 p = configs.config(int(sys.argv[1]) if len(sys.argv) > 1 else 4)
 with from_problem(p) as h:
     h.eigs(p.m, p.block, max_iters=5, tol=0.0)
-    for dbg in (0, 1, 4, 0):
+    for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else ['0', '1', '4', '0'])]:
         h.set_option("sp8_dbg", dbg)
         h.set_option("profile", (1 << 10) - 1); h.set_option("profile_reset", 1)
         try:
