@@ -17,7 +17,8 @@
 // Arithmetic (as k_dstream_sym8.cuh): S_B is scaled by 2^eS_B (per block) and stored as three
 // balanced signed digits per entry (3 planes, k_sp8_build, once per handle); the B operands are
 // digitised on the fly: Y2 with one scale 2^ey_c per column (from its column maxima), Y_B with
-// per-block column scales. kind::i8 products and int32 sums are exact; the three accumulator
+// one scale per column for the whole launch (from an a-priori bound on |Y|, so the epilogue
+// warps exchange nothing). kind::i8 products and int32 sums are exact; the three accumulator
 // column groups give c0 + c1/256 + c2/65536, undone in fp64 (error <= ~2^-23 of the scaled
 // maxima per product, the same bound as the D stream).
 //
@@ -25,8 +26,8 @@
 //   warp 0      producer: the block's image (one bulk copy, 384 d_pad bytes) into a 3-stage ring;
 //               at Rayleigh-Ritz steps also the block's rows of Y_prev (bulk copy)
 //   warp 1      MMA issue, order N(i), T(i-1)
-//   warps 2-5   epilogue: N accumulator -> Y rows (HBM once, smem for the Gram), the block's
-//               column maxima, Y_B digits (B operand of T); T accumulator -> P1 partials
+//   warps 2-5   epilogue: N accumulator -> Y rows (HBM once, smem for the Gram), Y_B digits
+//               (B operand of T); T accumulator -> P1 partials
 //   warps 6-9   B operand of N (Y2[dict_B] digits), then the FP64-tensor-core Gram of the
 //               previous block (G = Y^T Y, 1^T Y, and H' = Y_prev^T Y at RR steps)
 // Every sum has a fixed order: Y, P1 and the Grams are bitwise reproducible.
@@ -272,13 +273,30 @@ __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, cons
     }
 }
 
-// rs1[i] = (sum_j S_ij) - 1 (fp64 sum), the row-sum deviation the centred step adds back
+// rs1[i] = (sum_j S_ij) - 1 (fp64 sum), the row-sum deviation the centred step adds back;
+// norms[0] = max_i sum_j |S_ij|, norms[1] = max_i |rs1[i]| (bits of non-negative floats, zeroed
+// by the caller): the step kernel's a-priori bound on |Y| (static scales of Y_B's digits)
 __global__ void k_rowsum_m1(int64_t n, const int32_t* __restrict__ rp, const float* __restrict__ val,
-                            float* __restrict__ rs1) {
+                            float* __restrict__ rs1, unsigned int* __restrict__ norms) {
+    float ma = 0.f, mr = 0.f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double a = 0.0;
-        for (int32_t e = rp[i]; e < rp[i + 1]; ++e) a += (double)val[e];
+        double a = 0.0, aa = 0.0;
+        for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+            a += (double)val[e];
+            aa += fabs((double)val[e]);
+        }
         rs1[i] = (float)(a - 1.0);
+        ma = fmaxf(ma, __double2float_ru(aa));
+        mr = fmaxf(mr, fabsf(rs1[i]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+        mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(norms, __float_as_uint(ma));
+        atomicMax(norms + 1, __float_as_uint(mr));
     }
 }
 
@@ -536,7 +554,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     k_sp8_step(int64_t n, int64_t l_rows, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
                const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
                const uint8_t* __restrict__ Yd, const int* __restrict__ ey2in, const double* __restrict__ t,
-               const float* __restrict__ rs1, const int32_t* __restrict__ ppos,
+               const float* __restrict__ rs1, const float* __restrict__ norms, const int32_t* __restrict__ ppos,
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
                unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int mode,
@@ -571,11 +589,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* yr_empty = bars + 24;
     uint64_t* yp_full = bars + 26;
     uint64_t* yp_empty = bars + 28;
-    uint64_t* ey_full = bars + 38;      // [4] eyb[k % 4] written (lanes c < BP of the 4 epilogue warps)
-    uint64_t* ey_empty = bars + 6;      // [4] eyb[k % 4] read by the T drain (group B's 4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
     int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
-    int* eyb = ey2 + BP;                                   // [4][BP] exponents of Y_B per block (ring)
+    int* eyb = ey2 + BP;                                   // [BP] scale exponents of Y_B's columns (static bound)
 
     pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -593,8 +609,6 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         for (int a = 0; a < C::NBN; ++a) {
             mbar_init(&bn_full[a], 32);   // the producer warp's lanes
             mbar_init(&bn_empty[a], 1);
-            mbar_init(&ey_full[a], BP);   // quadrant-0 warp of each half, 8 lanes
-            mbar_init(&ey_empty[a], 4);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&an_full[a], 1);
@@ -640,7 +654,16 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         }
     };
     if (blockIdx.x < 256) tail_tr(768 + blockIdx.x);
-    if (threadIdx.x < BP) ey2[threadIdx.x] = ey2in[threadIdx.x];
+    if (threadIdx.x < BP) {
+        // Y_B's digits take one scale per column for the whole launch, from an a-priori bound:
+        // |Y_rc| <= 1/2 (sum_j |S_rj|) max_j |Y2 - 1 t^T|_jc + 1/2 |rs1_r| |t_c|, the digitised
+        // Y2 column being <= 2^(22 - ey2_c) (no per-block maxima, no exchange between the epilogue
+        // warps; the quantum is the column's, as the D stream's Y1 digits)
+        const int e2 = ey2in[threadIdx.x];
+        ey2[threadIdx.x] = e2;
+        const float bound = 0.5f * (norms[0] * pow2f(22 - e2) + norms[1] * fabsf((float)t[threadIdx.x]));
+        eyb[threadIdx.x] = i8_scale_exp(bound * 1.001f);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -833,6 +856,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         float mht[HC];   // -t / 2
 #pragma unroll
         for (int c = 0; c < HC; ++c) mht[c] = (float)(-0.5 * t[cb + c]);
+        float ysc[HC];
+#pragma unroll
+        for (int c = 0; c < HC; ++c) ysc[c] = pow2f(eyb[cb + c]);
         for (int i = 0; i < nb; ++i) {
             const int64_t B = b0 + i;
             const int a = i & 1;
@@ -865,45 +891,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             for (int c = 0; c < HC; ++c)
                 y[c] = live ? fmaf(-0.5f, acc4f(g0[c], g1[c], g2[c], g3[c], sce[c]), rsm1 * mht[c]) : 0.f;
             if (want_t) {
-                // this warp's column maxima over its 32 rows (butterfly reduce-scatter: lane ends
-                // with column cl, then an all-gather of the exponents), the block's exponents ey
-                // (the four quadrant warps of this column half share them: one T accumulator per
-                // block), the digits of Y_B
-                float m[HC];
-#pragma unroll
-                for (int c = 0; c < HC; ++c) m[c] = fabsf(y[c]);
-#pragma unroll
-                for (int h = HC / 2, o = 16; h >= 1; h >>= 1, o >>= 1) {
-                    const bool up = (lane & o) != 0;
-#pragma unroll
-                    for (int j = 0; j < h; ++j) {
-                        const float send = up ? m[j] : m[j + h], keep = up ? m[j + h] : m[j];
-                        m[j] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
-                    }
-                }
-                m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 2));
-                m[0] = fmaxf(m[0], __shfl_xor_sync(0xffffffffu, m[0], 1));
-                const int cl = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-                // the four quadrant warps of this half share their column maxima (the block's)
-                float* pm = reinterpret_cast<float*>(eyb + 4 * 2 * BP) + (a * 2 + hf) * 4 * HC;   // [2][2][4][HC]
-                if ((lane & 3) == 0) pm[q * HC + cl] = m[0];
-                named_bar(1 + hf, 128);
-                if (r == 0 && hf == 0) SP8_TR(12, i);
-                const float mp = fmaxf(fmaxf(pm[cl], pm[HC + cl]), fmaxf(pm[2 * HC + cl], pm[3 * HC + cl]));
-                const int my_e = i8_scale_exp(mp);   // exponent of column cb + cl for the block's 128 rows
-                int ey[HC];
-#pragma unroll
-                for (int c = 0; c < HC; ++c)   // lane holding column c: bits 4..2 = c's bits 2..0
-                    ey[c] = __shfl_sync(0xffffffffu, my_e, ((c >> 2) & 1) << 4 | ((c >> 1) & 1) << 3 | (c & 1) << 2);
-                if (q == 0 && (lane & 3) == 0) {   // published for group B's T drain of this block
-                    mbar_wait(&ey_empty[i & 3], ((uint32_t)((i >> 2) & 1)) ^ 1u, 157 * 65536 + (i & 0xFFFF));
-                    if (r == 0 && hf == 0) SP8_TR(13, i);
-                    eyb[(i & 3) * BP + cb + cl] = my_e;
-                    mbar_arrive(&ey_full[i & 3]);
-                }
-                float ysc[HC];
-#pragma unroll
-                for (int c = 0; c < HC; ++c) ysc[c] = pow2f(ey[c]);
+                // the digits of Y_B (B operand of T) on the launch's static column scales
                 uint2 w0, w1, w2;
                 digit_rows8(y, ysc, w0, w1, w2);
                 mbar_wait(&bt_empty[a], pa ^ 1u, 151 * 65536 + (i & 0xFFFF));
@@ -938,12 +926,11 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         // ------------------------------------------------ group B (warps 10-13): T accumulator -> P1
         const int gt = threadIdx.x - 320;   // 0..127 (T accumulator: TMEM lane = dictionary entry gt)
         const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-        // T accumulator of block i -> P1 partials, scaled by A's exponents of Y_B (ey ring of 4,
-        // ey_full / ey_empty); the P1 slot of this thread, du and eS of that block are passed in
+        // T accumulator of block i -> P1 partials, scaled by Y_B's column exponents; the P1 slot
+        // of this thread, du and eS of that block are passed in
         auto drain_t = [&](int i, int32_t pos, int32_t du, int eS) {
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
-            mbar_wait(&ey_full[i & 3], (uint32_t)((i >> 2) & 1), 155 * 65536 + (i & 0xFFFF));
             mbar_wait(&at_full[a], pa, 148 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             if (threadIdx.x == 320) SP8_TR(17, i);
@@ -963,14 +950,12 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                     tmem_ld8_u(tbase + lane_off + col + 3 * BP + c0, *reinterpret_cast<int(*)[8]>(&g3[c0]));
                 }
                 tmem_wait_ld();
-                const int* ey = eyb + (i & 3) * BP;
+                const int* ey = eyb;
 #pragma unroll
                 for (int c = 0; c < BP; ++c) out[c] = acc4f(g0[c], g1[c], g2[c], g3[c], pow2f2(16 - eS - ey[c]));
             }
             tc_fence_before();
             mbar_arrive(&at_empty[a]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ey_empty[i & 3]);   // this warp has read eyb[i % 4]
             if (lrow < du) {
                 float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)pos * BP);
 #pragma unroll

@@ -1522,7 +1522,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
            (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
            (const int*)ey2, (const double*)h->t.as<double>(), (const float*)h->s8rs1.as<float>(),
-           (const int32_t*)h->s8pos.as<int32_t>(), Y,
+           (const float*)h->s8rs1.as<float>() + h->n, (const int32_t*)h->s8pos.as<int32_t>(), Y,
            want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
            h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr,
@@ -1873,9 +1873,12 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     h->s8pos.ensure(std::max<int32_t>(1, o.total_u) * sizeof(int32_t));
     launch(k_inverse_perm, dim3(1024), dim3(256), 0, st, o.total_u, (const int32_t*)o.jlist.as<int32_t>(),
            h->s8pos.as<int32_t>());
-    h->s8rs1.ensure(h->n * sizeof(float));
+    // rs1[n], then the two norms of the step's a-priori bound on |Y| (k_rowsum_m1)
+    h->s8rs1.ensure((h->n + 2) * sizeof(float));
+    CK(cudaMemsetAsync(h->s8rs1.as<float>() + h->n, 0, 2 * sizeof(float), st));
     launch(k_rowsum_m1, dim3((unsigned)std::min<int64_t>(4 * 148, (h->n + 255) / 256)), dim3(256), 0, st, h->n,
-           (const int32_t*)h->rp.as<int32_t>(), (const float*)h->val.as<float>(), h->s8rs1.as<float>());
+           (const int32_t*)h->rp.as<int32_t>(), (const float*)h->val.as<float>(), h->s8rs1.as<float>(),
+           reinterpret_cast<unsigned int*>(h->s8rs1.as<float>() + h->n));
     h->s8_bytes = total;
     h->sp8_state = 1;
     return true;
