@@ -537,7 +537,10 @@ struct Sp8Cfg {
     static constexpr int OFF_BAR = OFF_YP + 2 * YR;
     static constexpr int MAXNB = 256;                    // blocks per CTA (per-CTA metadata table)
     static constexpr int OFF_META = OFF_BAR + 2048;      // int64 ioff[256], int32 doff[257], int32 eS[256]
-    static constexpr int SMEM = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 16 + 1024;   // + alignment slack
+    static constexpr int NRS = 8;                        // rs1 ring: a slot is rewritten 8 blocks later, after N(i + 4)
+    static constexpr int OFF_RS = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 12;   // (16-byte aligned)
+    static constexpr int SMEM = OFF_RS + NRS * kSp8RB * 4 + 1024;   // + alignment slack
+    static_assert(OFF_RS % 16 == 0, "rs ring alignment");
     static constexpr int THREADS = 16 * 32;   // 4 warps per scheduler (<= 128 registers)
     static constexpr int NGW = 2;                        // Gram warps (group C)
     // TMEM columns: accumulators with four 16-column groups (c0 = d0 y0, c1, c2, c3 = d1 y2 + d2 y1):
@@ -600,6 +603,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     const bool want_t = P1 != nullptr;
     const bool stream_only = (mode & 1) != 0;    // (diagnostics) images streamed, no MMA
     const unsigned poll_ns = (unsigned)mode >> 8;   // MMA warp: back-off between unready polls
+    const int pf_ahead = (mode >> 4) & 15;          // producer: L2 prefetch of the image pf_ahead blocks ahead (0: off)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < 3; ++s) {
@@ -716,6 +720,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                         for (int pl = 0; pl < 3; ++pl) cp_async16(bn + sp8_boff<NB>(g, pl), Yd + (pl * l_rows + j[u]) * 16);
                     }
                 }
+                // the block's row-sum deviations (512 B, one 16-byte chunk per lane; rs1 is padded to
+                // whole blocks) into their ring: the epilogue reads them from shared memory, with
+                // no global load between the N accumulator and the digits
+                cp_async16(base + C::OFF_RS + ((i % C::NRS) * kSp8RB + 4 * lane) * 4, rs1 + B * kSp8RB + 4 * lane);
                 cp_async_arrive_noinc(&bn_full[sb]);
                 if (lane == 0) SP8_TR(7, i);
             }
@@ -728,6 +736,11 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 mbar_arrive_expect_tx(&full_img[s], bytes);
                 bulk_load(base + s * C::IMG, gimg + m_ioff[i], bytes, &full_img[s]);
                 SP8_TR(0, i);
+                // the image pf_ahead blocks on: HBM -> L2 now, so that its load into a freed stage
+                // (three stages cover ~1.5 blocks of the ~2.2 us HBM latency) finds it in L2
+                if (pf_ahead && i + pf_ahead < nb)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gimg + m_ioff[i + pf_ahead]),
+                                 "r"((uint32_t)(3 * kSp8RB * dpad_of(B + pf_ahead))) : "memory");
             }
             __syncwarp();
         }
@@ -820,13 +833,19 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 if (!want_t) tc_commit(&empty_img[s]);
             }
             __syncwarp();
+            if (lane == 0) SP8_TR(9, i);
         };
         int nN = 0, nT = 0;
         const int nt_total = want_t ? nb : 0;
         uint64_t t_start;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        int seenN = 0;   // (diagnostics) N accumulators seen complete by this loop
         for (uint32_t spin = 0; nN < nb || nT < nt_total; ++spin) {
             // (warp-uniform: every lane tests the same barriers)
+            if (trace && seenN < nN && mbar_test(&an_full[seenN & 1], (uint32_t)((seenN >> 1) & 1))) {
+                if (lane == 0) SP8_TR(13, seenN);
+                ++seenN;
+            }
             if (nT < nN && nT < nt_total && __all_sync(0xffffffffu, ready_t(nT))) {
                 issue_t(nT++);
                 spin = 0;
@@ -859,6 +878,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         float ysc[HC];
 #pragma unroll
         for (int c = 0; c < HC; ++c) ysc[c] = pow2f(eyb[cb + c]);
+        const float* rs_ring = reinterpret_cast<const float*>(base + C::OFF_RS);
         for (int i = 0; i < nb; ++i) {
             const int64_t B = b0 + i;
             const int a = i & 1;
@@ -868,7 +888,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             float2 sce[HC];   // accumulator 2^(16 - eS - ey2_c) -> S Y2
 #pragma unroll
             for (int c = 0; c < HC; ++c) sce[c] = pow2f2(16 - eS - ey2[cb + c]);
-            const float rsm1 = r < rows ? __ldg(rs1 + B * kSp8RB + r) : 0.f;
+            if (r == 0 && hf == 0) SP8_TR(12, i);
             mbar_wait(&an_full[a], pa, 149 * 65536 + (i & 0xFFFF));
             tc_fence_after();
             if (r == 0 && hf == 0) SP8_TR(3, i);
@@ -881,6 +901,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 tmem_ld8_u(col + 3 * BP, g3);
                 tmem_wait_ld();
             }
+            // (staged by the producer with the B operand of N(i): visible once N(i) has completed)
+            const float rsm1 = rs_ring[(i % C::NRS) * kSp8RB + r];
             tc_fence_before();
             mbar_arrive(&an_empty[a]);
             if (r == 0 && hf == 0) SP8_TR(11, i);

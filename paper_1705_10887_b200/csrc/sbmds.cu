@@ -504,6 +504,7 @@ struct sbmds_ctx {
                            // 2 = timeline of CTA 0, 4 = stream the images only, 8 = T product in the last iteration too,
                            // 16 = no H' (as between Rayleigh-Ritz steps), 256 = no Gram, 512 = no T drain arithmetic
     int sp8_poll = 0;      // k_sp8_step: the MMA warp's back-off (ns) between unready polls
+    int sp8_pf = 0;        // k_sp8_step: L2 prefetch distance of the images, in blocks (0: off)
     int64_t s8_bytes = 0;
     // D_ll
     float* D = nullptr;
@@ -1522,11 +1523,11 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
            (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
            (const int*)ey2, (const double*)h->t.as<double>(), (const float*)h->s8rs1.as<float>(),
-           (const float*)h->s8rs1.as<float>() + h->n, (const int32_t*)h->s8pos.as<int32_t>(), Y,
+           (const float*)h->s8rs1.as<float>() + h->s8.nblk * kSp8RB, (const int32_t*)h->s8pos.as<int32_t>(), Y,
            want_p1 ? h->P1.as<float>() : nullptr,
            Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
            h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr,
-           ((h->sp8_dbg & 4) ? 1 : 0) | ((h->sp8_dbg >> 7) & 6) | (h->sp8_poll << 8),
+           ((h->sp8_dbg & 4) ? 1 : 0) | ((h->sp8_dbg >> 7) & 6) | ((h->sp8_pf & 15) << 4) | (h->sp8_poll << 8),
            with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>(), defer ? 1 : 0);
     h->gram_deferred = defer;
     h->gram_parts = grid;
@@ -1873,12 +1874,14 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     h->s8pos.ensure(std::max<int32_t>(1, o.total_u) * sizeof(int32_t));
     launch(k_inverse_perm, dim3(1024), dim3(256), 0, st, o.total_u, (const int32_t*)o.jlist.as<int32_t>(),
            h->s8pos.as<int32_t>());
-    // rs1[n], then the two norms of the step's a-priori bound on |Y| (k_rowsum_m1)
-    h->s8rs1.ensure((h->n + 2) * sizeof(float));
-    CK(cudaMemsetAsync(h->s8rs1.as<float>() + h->n, 0, 2 * sizeof(float), st));
+    // rs1 padded with zeros to whole 128-row blocks (the step stages 512 B per block), then the
+    // two norms of the step's a-priori bound on |Y| (k_rowsum_m1)
+    const int64_t rs_pad = o.nblk * kSp8RB;
+    h->s8rs1.ensure((rs_pad + 4) * sizeof(float));
+    CK(cudaMemsetAsync(h->s8rs1.as<float>() + h->n, 0, (rs_pad + 4 - h->n) * sizeof(float), st));
     launch(k_rowsum_m1, dim3((unsigned)std::min<int64_t>(4 * 148, (h->n + 255) / 256)), dim3(256), 0, st, h->n,
            (const int32_t*)h->rp.as<int32_t>(), (const float*)h->val.as<float>(), h->s8rs1.as<float>(),
-           reinterpret_cast<unsigned int*>(h->s8rs1.as<float>() + h->n));
+           reinterpret_cast<unsigned int*>(h->s8rs1.as<float>() + rs_pad));
     h->s8_bytes = total;
     h->sp8_state = 1;
     return true;
@@ -3920,6 +3923,9 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "sp8_poll")) {
         if (value < 0 || value > 100000) return fail(SBMDS_EINVAL, "sp8_poll must be in [0, 100000] ns");
         h->sp8_poll = (int)value;
+    } else if (!strcmp(key, "sp8_pf")) {
+        if (value < 0 || value > 15) return fail(SBMDS_EINVAL, "sp8_pf must be in [0, 15] blocks");
+        h->sp8_pf = (int)value;
     } else if (!strcmp(key, "sp8_dbg")) {
         h->sp8_dbg = (int)value;
     } else if (!strcmp(key, "fuse")) {

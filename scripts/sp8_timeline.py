@@ -6,7 +6,7 @@ import torch
 from gen import configs
 from paper_1705_10887_b200 import from_problem
 EV = ["load_issued", "N_start", "T_start", "A_got_N", "A_digits", "C_gram", "B_T_drained", "B_staged",
-      "prod_empty_ok", "prod_yp_ok", "T_issued", "A_tmem", "A_pairbar", "A_eyempty", "A_btempty", "A_ystored",
+      "prod_empty_ok", "N_issued", "T_issued", "A_tmem", "A_waitN", "N_done_seen", "A_btempty", "A_ystored",
       "A_yrempty", "B_atfull", "A8_btfull", "A6_btfull"]
 p = configs.config(4)
 with from_problem(p) as h:
