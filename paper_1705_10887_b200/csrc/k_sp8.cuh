@@ -527,7 +527,8 @@ struct Sp8Cfg {
     static constexpr int IMG = 3 * kSp8RB * kSp8DK;      // 48 KB: largest image
     static constexpr int NS = 3;                         // image stages
     static constexpr int BN = NB * kSp8DK;               // B of N: d_pad x NB (MN-major)
-    static constexpr int BT = NB * kSp8RB;               // B of T: 128 rows x NB (MN-major)
+    static constexpr int NBT = 64;                       // B of T: row width [y0 | y1 | y2 | ones chunk]
+    static constexpr int BT = NBT * kSp8RB;              // B of T: 128 rows x NBT (MN-major)
     static constexpr int YR = kSp8RB * BP * 4;           // fp32 rows of a block
     static constexpr int OFF_BN = NS * IMG;
     static constexpr int NBN = 4;                        // B_N ring (staged two blocks ahead)
@@ -535,24 +536,30 @@ struct Sp8Cfg {
     static constexpr int OFF_YR = OFF_BT + 2 * BT;
     static constexpr int OFF_YP = OFF_YR + 2 * YR;
     static constexpr int OFF_BAR = OFF_YP + 2 * YR;
-    static constexpr int MAXNB = 256;                    // blocks per CTA (per-CTA metadata table)
-    static constexpr int OFF_META = OFF_BAR + 2048;      // int64 ioff[256], int32 doff[257], int32 eS[256]
+    static constexpr int MAXNB = 192;                    // blocks per CTA (per-CTA metadata table)
+    static constexpr int OFF_META = OFF_BAR + 1024;      // int64 ioff[MAXNB], int32 doff[MAXNB + 1], int32 eS[MAXNB]
     static constexpr int NRS = 8;                        // rs1 ring: a slot is rewritten 8 blocks later, after N(i + 4)
     static constexpr int OFF_RS = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 12;   // (16-byte aligned)
     static constexpr int SMEM = OFF_RS + NRS * kSp8RB * 4 + 1024;   // + alignment slack
     static_assert(OFF_RS % 16 == 0, "rs ring alignment");
-    static constexpr int THREADS = 16 * 32;   // 4 warps per scheduler (<= 128 registers)
+    static_assert(SMEM + 1024 <= 227 * 1024, "dynamic + the kernel's 1 KB of static shared memory");
+    static constexpr int THREADS = 17 * 32;   // (<= 120 registers); warp 16 issues the T products
     static constexpr int NGW = 2;                        // Gram warps (group C)
     // TMEM columns: accumulators with four 16-column groups (c0 = d0 y0, c1, c2, c3 = d1 y2 + d2 y1):
     // N[2] and T[2] (double-buffered; one T accumulator per block, whose 128 rows share the
     // column scales of Y_B's digits), 256 of 512 columns
     static constexpr int ACCW = 4 * BP;
     static constexpr int ACCN = 0, ACCT = 2 * ACCW;
-    static_assert(ACCT + 2 * ACCW <= 512, "tmem");
+    static constexpr int ACCG = 4 * ACCW;                // int8 Gram accumulator (GRAM8): 3 BP columns
+    static_assert(ACCG + 3 * BP <= 512, "tmem");
     static_assert(BP == 16, "the tensor-core sparse step is built for b = 16");
 };
 
-template <int BP, bool WITH_H>
+// GRAM8 (steps whose Gram only feeds the next Cholesky-QR, never a Rayleigh-Ritz step): G and
+// 1^T Y are formed from Y_B's digits on the int8 tensor cores, Yd^T [Yd | 1] accumulated exactly
+// in one TMEM accumulator over the CTA's blocks (the digits' scales are per launch), instead of
+// the FP64 Gram of the fp32 rows: no Gram warps, no staging of Y for them.
+template <int BP, bool WITH_H, bool GRAM8>
 __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     k_sp8_step(int64_t n, int64_t l_rows, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
                const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
@@ -563,6 +570,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int mode,
                double* __restrict__ Rinv_next, int* __restrict__ status, int defer_gram) {
     using C = Sp8Cfg<BP>;
+    static_assert(!(GRAM8 && WITH_H), "the int8 Gram has no H'");
     // (diagnostics) trace[ev * 64 + i] (ev < 12; 2048 + (ev - 12) * 64 + i for ev 12..19):
     // globaltimer of event ev for block i < 64 of CTA 0
 #define SP8_TR(ev, i)                                                                          \
@@ -592,6 +600,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* yr_empty = bars + 24;
     uint64_t* yp_full = bars + 26;
     uint64_t* yp_empty = bars + 28;
+    uint64_t* gram_full = bars + 6;     // (GRAM8) the CTA's last Gram MMA has completed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
     int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
     int* eyb = ey2 + BP;                                   // [BP] scale exponents of Y_B's columns (static bound)
@@ -614,6 +623,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             mbar_init(&bn_full[a], 32);   // the producer warp's lanes
             mbar_init(&bn_empty[a], 1);
         }
+        mbar_init(gram_full, 1);
         for (int a = 0; a < 2; ++a) {
             mbar_init(&an_full[a], 1);
             mbar_init(&an_empty[a], 256);
@@ -637,6 +647,11 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             m_ioff[k] = __ldg(ioff + b0 + k);
             m_es[k] = __ldg(escale + b0 + k);
         }
+    }
+    if (threadIdx.x < 2 * kSp8RB) {   // the ones chunk of both B_T buffers' rows (byte 0 = 1): 1^T Yd for GRAM8
+        uint8_t* bt = base + C::OFF_BT + (threadIdx.x >> 7) * C::BT;
+        *reinterpret_cast<uint4*>(bt + sp8_boff<C::NBT>(threadIdx.x & 127, 3)) = make_uint4(1u, 0u, 0u, 0u);
+        fence_proxy_async();
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -753,115 +768,103 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             __syncwarp();
         }
     } else if (stream_only) {
-    } else if (warp == 1) {
-        // ------------------------------------------------ MMA issue: N(i), then T(i - 1)
+    } else if (warp == 1 || warp == 16) {
+        // ------------------------------------------------ MMA issue: warp 1 the N products, warp 16 the
+        // T products. Each waits (blocking mbarrier waits, woken by the hardware) for its own
+        // operands only, so T(i) never queues behind the issue of N(i + 1) and neither polls.
         // d0 x [y0|y1|y2] -> groups 0-2, d1 x [y0|y1|y2] -> 1-3, d2 x [y0|y1] -> 2-3
         constexpr uint32_t id1n = idesc_i8_bmn(128, NB, 0), id2n = idesc_i8_bmn(128, NB, 0),
                            id3n = idesc_i8_bmn(128, 2 * BP, 0), id0n = idesc_i8_bmn(128, BP, 0);
         constexpr uint32_t id1t = idesc_i8_bmn(128, NB, 1), id2t = idesc_i8_bmn(128, NB, 1),
                            id3t = idesc_i8_bmn(128, 2 * BP, 1), id0t = idesc_i8_bmn(128, BP, 1);
-        constexpr uint32_t KG = NB / 16 * 128;   // B: bytes per 8-row K group (the LBO)
-        // Both products are issued as soon as their operands are ready (polled, non-blocking):
-        // T(i) does not wait behind N(i + 1), so an image stage is released as early as possible.
-        auto ready_t = [&](int i) {
-            const uint32_t pa = (uint32_t)((i >> 1) & 1);
-            return mbar_test(&bt_full[i & 1], pa) && mbar_test(&at_empty[i & 1], pa ^ 1u);
-        };
-        auto ready_n = [&](int i) {
-            const uint32_t ph = (uint32_t)((i / 3) & 1), pa = (uint32_t)((i >> 1) & 1);
-            return mbar_test(&full_img[i % 3], ph) && mbar_test(&bn_full[i % C::NBN], (uint32_t)((i / C::NBN) & 1)) &&
-                   mbar_test(&an_empty[i & 1], pa ^ 1u);
-        };
-        auto issue_t = [&](int i) {
-            const int64_t B = b0 + i;
-            const int s = i % 3, a = i & 1;
-            const int dp = dpad_of(B);
-            tc_fence_after();
-            if (lane == 0) SP8_TR(2, i);
-            const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BT + a * C::BT);
-            const uint32_t plane = (uint32_t)(kSp8RB * dp);
-            if (elect_one()) {
+        constexpr uint32_t KG = NB / 16 * 128;        // B of N: bytes per 8-row K group (the LBO)
+        constexpr uint32_t KGT = C::NBT / 16 * 128;   // B of T
+        constexpr uint32_t idg = idesc_i8_bmn(128, NB, 1);   // Gram: A = B = Y_B's digit image (MN-major)
+        (void)poll_ns;
+        if (warp == 16) {
+            for (int i = 0; want_t && i < nb; ++i) {
+                const int64_t B = b0 + i;
+                const int s = i % 3, a = i & 1;
+                const uint32_t pa = (uint32_t)((i >> 1) & 1);
+                const int dp = dpad_of(B);
+                mbar_wait(&bt_full[a], pa, 145 * 65536 + (i & 0xFFFF));
+                mbar_wait(&at_empty[a], pa ^ 1u, 146 * 65536 + (i & 0xFFFF));
+                mbar_wait(&full_img[s], (uint32_t)((i / 3) & 1), 147 * 65536 + (i & 0xFFFF));   // (passed: N(i) is done)
+                tc_fence_after();
+                if (lane == 0) SP8_TR(2, i);
+                const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BT + a * C::BT);
+                const uint32_t plane = (uint32_t)(kSp8RB * dp);
+                if (elect_one()) {
 #pragma unroll
-                for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue quadrant j's) per MMA
-                    const uint32_t d = tbase + (uint32_t)(C::ACCT + a * C::ACCW);   // one accumulator per block
-                    const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
-                    const uint64_t a0 = umma_desc_none(sa + 512 * j, 128, 2048);
-                    if (j > 0) {
-                        tc_mma_i8(d, a0, bd, id1t, 1u);
-                        tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
-                    } else {   // chain start: every group initialised by an MMA (no TMEM zeroing)
-                        tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 0u);
-                        tc_mma_i8(d, a0, bd, id0t, 0u);
-                        tc_mma_i8(d + BP, a0, umma_desc_none(sb + 4 * KG * j + 128, KG, 128), id3t, 1u);
+                    for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows (epilogue quadrant j's) per MMA
+                        const uint32_t d = tbase + (uint32_t)(C::ACCT + a * C::ACCW);   // one accumulator per block
+                        const uint64_t bd = umma_desc_none(sb + 4 * KGT * j, KGT, 128);
+                        const uint64_t a0 = umma_desc_none(sa + 512 * j, 128, 2048);
+                        if (j > 0) {
+                            tc_mma_i8(d, a0, bd, id1t, 1u);
+                            tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 1u);
+                        } else {   // chain start: every group initialised by an MMA (no TMEM zeroing)
+                            tc_mma_i8(d + BP, umma_desc_none(sa + plane + 512 * j, 128, 2048), bd, id2t, 0u);
+                            tc_mma_i8(d, a0, bd, id0t, 0u);
+                            tc_mma_i8(d + BP, a0, umma_desc_none(sb + 4 * KGT * j + 128, KGT, 128), id3t, 1u);
+                        }
+                        tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
                     }
-                    tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
-                }
-                tc_commit(&at_full[a]);
-                tc_commit(&bt_empty[a]);
-                tc_commit(&empty_img[s]);
-            }
-            __syncwarp();
-            if (lane == 0) SP8_TR(10, i);
-        };
-        auto issue_n = [&](int i) {
-            const int64_t B = b0 + i;
-            const int s = i % 3, a = i & 1;
-            const int dp = dpad_of(B);
-            fence_proxy_async();   // B_N arrived by cp.async (generic proxy) -> visible to the MMA (async proxy)
-            tc_fence_after();
-            if (lane == 0) SP8_TR(1, i);
-            const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BN + (i % C::NBN) * C::BN);
-            const uint32_t d = tbase + (uint32_t)(C::ACCN + a * C::ACCW);
-            const uint32_t plane = (uint32_t)(kSp8RB * dp);
-            if (elect_one()) {
-                for (int j = 0; j < dp / 32; ++j) {   // K = 32 dictionary entries per MMA
-                    const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
-                    const uint64_t a0 = umma_desc_none(sa + 4096 * j, 2048, 128);
-                    if (j > 0) {
-                        tc_mma_i8(d, a0, bd, id1n, 1u);
-                        tc_mma_i8(d + BP, umma_desc_none(sa + plane + 4096 * j, 2048, 128), bd, id2n, 1u);
-                    } else {   // chain start: d1 [y0|y1|y2] initialises groups 1-3, d0 y0 group 0,
-                               // then d0 [y1|y2] accumulates into groups 1-2 (no TMEM zeroing)
-                        tc_mma_i8(d + BP, umma_desc_none(sa + plane, 2048, 128), bd, id2n, 0u);
-                        tc_mma_i8(d, a0, bd, id0n, 0u);
-                        tc_mma_i8(d + BP, a0, umma_desc_none(sb + 128, KG, 128), id3n, 1u);
+                    tc_commit(&at_full[a]);
+                    if constexpr (GRAM8) {
+                        // Yd^T [Yd | 1]: M = the image's 16-byte chunks as rows (digit planes 0-2, the
+                        // ones chunk: lanes 0-48 are used, the rest read the next K group), K = the
+                        // block's rows, N = 3 BP; one accumulator for the whole CTA (exact in int32:
+                        // <= 2^14 per product, <= 2^15 rows)
+#pragma unroll
+                        for (int j = 0; j < kSp8RB / 32; ++j) {
+                            const uint64_t gd = umma_desc_none(sb + 4 * KGT * j, KGT, 128);
+                            tc_mma_i8(tbase + (uint32_t)C::ACCG, gd, gd, idg, (i > 0 || j > 0) ? 1u : 0u);
+                        }
+                        if (i + 1 == nb) tc_commit(gram_full);
                     }
-                    tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 4096 * j, 2048, 128), bd, id3n, 1u);
+                    tc_commit(&bt_empty[a]);
+                    tc_commit(&empty_img[s]);
                 }
-                tc_commit(&an_full[a]);
-                tc_commit(&bn_empty[i % C::NBN]);
-                if (!want_t) tc_commit(&empty_img[s]);
+                __syncwarp();
+                if (lane == 0) SP8_TR(10, i);
             }
-            __syncwarp();
-            if (lane == 0) SP8_TR(9, i);
-        };
-        int nN = 0, nT = 0;
-        const int nt_total = want_t ? nb : 0;
-        uint64_t t_start;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-        int seenN = 0;   // (diagnostics) N accumulators seen complete by this loop
-        for (uint32_t spin = 0; nN < nb || nT < nt_total; ++spin) {
-            // (warp-uniform: every lane tests the same barriers)
-            if (trace && seenN < nN && mbar_test(&an_full[seenN & 1], (uint32_t)((seenN >> 1) & 1))) {
-                if (lane == 0) SP8_TR(13, seenN);
-                ++seenN;
+        } else {
+            for (int i = 0; i < nb; ++i) {
+                const int64_t B = b0 + i;
+                const int s = i % 3, a = i & 1;
+                const int dp = dpad_of(B);
+                mbar_wait(&full_img[s], (uint32_t)((i / 3) & 1), 142 * 65536 + (i & 0xFFFF));
+                mbar_wait(&bn_full[i % C::NBN], (uint32_t)((i / C::NBN) & 1), 143 * 65536 + (i & 0xFFFF));
+                mbar_wait(&an_empty[a], ((uint32_t)((i >> 1) & 1)) ^ 1u, 144 * 65536 + (i & 0xFFFF));
+                fence_proxy_async();   // B_N arrived by cp.async (generic proxy) -> visible to the MMA (async proxy)
+                tc_fence_after();
+                if (lane == 0) SP8_TR(1, i);
+                const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BN + (i % C::NBN) * C::BN);
+                const uint32_t d = tbase + (uint32_t)(C::ACCN + a * C::ACCW);
+                const uint32_t plane = (uint32_t)(kSp8RB * dp);
+                if (elect_one()) {
+                    for (int j = 0; j < dp / 32; ++j) {   // K = 32 dictionary entries per MMA
+                        const uint64_t bd = umma_desc_none(sb + 4 * KG * j, KG, 128);
+                        const uint64_t a0 = umma_desc_none(sa + 4096 * j, 2048, 128);
+                        if (j > 0) {
+                            tc_mma_i8(d, a0, bd, id1n, 1u);
+                            tc_mma_i8(d + BP, umma_desc_none(sa + plane + 4096 * j, 2048, 128), bd, id2n, 1u);
+                        } else {   // chain start: d1 [y0|y1|y2] initialises groups 1-3, d0 y0 group 0,
+                                   // then d0 [y1|y2] accumulates into groups 1-2 (no TMEM zeroing)
+                            tc_mma_i8(d + BP, umma_desc_none(sa + plane, 2048, 128), bd, id2n, 0u);
+                            tc_mma_i8(d, a0, bd, id0n, 0u);
+                            tc_mma_i8(d + BP, a0, umma_desc_none(sb + 128, KG, 128), id3n, 1u);
+                        }
+                        tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 4096 * j, 2048, 128), bd, id3n, 1u);
+                    }
+                    tc_commit(&an_full[a]);
+                    tc_commit(&bn_empty[i % C::NBN]);
+                    if (!want_t) tc_commit(&empty_img[s]);
+                }
+                __syncwarp();
+                if (lane == 0) SP8_TR(9, i);
             }
-            if (nT < nN && nT < nt_total && __all_sync(0xffffffffu, ready_t(nT))) {
-                issue_t(nT++);
-                spin = 0;
-            } else if (nN < nb && __all_sync(0xffffffffu, ready_n(nN))) {
-                issue_n(nN++);
-                spin = 0;
-            } else if (poll_ns) {
-                __nanosleep(poll_ns);
-            }
-            if ((spin & 4095u) == 4095u) {   // watchdog, as mbar_wait
-                uint64_t t;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                if (t - t_start > 4000000000ull)
-                    mbar_hang(nT < nN ? &bt_full[nT & 1] : &full_img[nN % 3], 0, 145 * 65536 + (nN & 0xFF) * 256 + (nT & 0xFF));
-            }
-            if (spin == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         }
     } else if (warp < 10) {
         // ------------------------------------------------ epilogue A (warps 2-9, TMEM lane = row): two
@@ -919,9 +922,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 mbar_wait(&bt_empty[a], pa ^ 1u, 151 * 65536 + (i & 0xFFFF));
                 if (r == 0 && hf == 0) SP8_TR(14, i);
                 uint8_t* bt = base + C::OFF_BT + a * C::BT;
-                *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 0) + cb) = w0;
-                *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 1) + cb) = w1;
-                *reinterpret_cast<uint2*>(bt + sp8_boff<NB>(r, 2) + cb) = w2;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<C::NBT>(r, 0) + cb) = w0;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<C::NBT>(r, 1) + cb) = w1;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<C::NBT>(r, 2) + cb) = w2;
                 fence_proxy_async();
                 mbar_arrive(&bt_full[a]);
                 if (r == 0 && hf == 1) SP8_TR(18, i);
@@ -935,14 +938,14 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 dst[1] = make_float4(y[4], y[5], y[6], y[7]);
             }
             if (r == 0 && hf == 0) SP8_TR(15, i);
-            mbar_wait(&yr_empty[a], pa ^ 1u, 150 * 65536 + (i & 0xFFFF));
-            if (r == 0 && hf == 0) SP8_TR(16, i);
-            {
+            if constexpr (!GRAM8) {   // the rows for the FP64 Gram warps
+                mbar_wait(&yr_empty[a], pa ^ 1u, 150 * 65536 + (i & 0xFFFF));
+                if (r == 0 && hf == 0) SP8_TR(16, i);
                 float4* yr = reinterpret_cast<float4*>(reinterpret_cast<float*>(base + C::OFF_YR + a * C::YR) + r * BP + cb);
                 yr[0] = make_float4(y[0], y[1], y[2], y[3]);
                 yr[1] = make_float4(y[4], y[5], y[6], y[7]);
+                mbar_arrive(&yr_full[a]);
             }
-            mbar_arrive(&yr_full[a]);
         }
     } else if (warp < 14) {
         // ------------------------------------------------ group B (warps 10-13): T accumulator -> P1
@@ -1000,6 +1003,35 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
             if (want_t) drain_t(i, pos, du, eS);
             if (lane == 0 && warp == 10) SP8_TR(6, i);
         }
+        if constexpr (GRAM8) {
+            // the CTA's Gram accumulator -> fp64 in shared memory (image stage 0: every MMA and load
+            // of the CTA has completed once gram_full has): TMEM lane 16 p + i, column 16 q + j holds
+            // sum_r d_p[r][i] d_q[r][j] (p <= 2), lane 48 the column sums of the digit planes
+            if ((warp == 12 || warp == 13) && nb > 0) {
+                mbar_wait(gram_full, 0u, 158 * 65536);
+                tc_fence_after();
+                const int L = 32 * (warp & 3) + lane;
+                int g[3 * BP];
+#pragma unroll
+                for (int c0 = 0; c0 < 3 * BP; c0 += 8)
+                    tmem_ld8_u(tbase + lane_off + (uint32_t)(C::ACCG + c0), *reinterpret_cast<int(*)[8]>(&g[c0]));
+                tmem_wait_ld();
+                tc_fence_before();
+                double* dbuf = reinterpret_cast<double*>(base);   // [3][BP][BP], then cs[BP]
+                if (L <= 3 * BP) {
+                    const int p = L / BP, ii = L % BP;
+                    const double place = p == 0 ? 65536.0 : (p == 1 ? 256.0 : 1.0);   // 2^(16 - 8 p); the sums row: 1
+#pragma unroll
+                    for (int j = 0; j < BP; ++j) {
+                        const double v = ((double)g[j] * 65536.0 + (double)g[BP + j] * 256.0 + (double)g[2 * BP + j]) * place;
+                        if (p < 3) dbuf[(p * BP + ii) * BP + j] = v;
+                        else if (ii == 0) dbuf[3 * BP * BP + j] = v;
+                    }
+                }
+            }
+        }
+    } else if constexpr (GRAM8) {
+        // (group C idles: the Gram runs on the int8 tensor cores)
     } else {
         // ------------------------------------------------ group C (warps 14-15): the Grams on the FP64 tensor cores
         const int gt = threadIdx.x - 448;   // 0..63: rows gt, gt + 64 of Y_prev this thread stages
@@ -1100,7 +1132,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         hacc[i][0] += hacc1[i][0];
         hacc[i][1] += hacc1[i][1];
     }
-    if (warp >= 14) {
+    if (!GRAM8 && (warp == 14 || warp == 15)) {
 #pragma unroll
         for (int c = 0; c < NCB; ++c) {
             double v = csum[c];
@@ -1123,15 +1155,28 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     __syncthreads();
     if (blockIdx.x < 256) tail_tr(1792 + blockIdx.x);
     double* pg = part + (int64_t)blockIdx.x * kGramPart;
-    for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
-        const int p = pq / BP, qq = pq % BP;
-        pg[pq] = red[0][p][qq] + red[1][p][qq];
+    if constexpr (GRAM8) {
+        // G_ij = 2^-(e_i + e_j) sum_p dbuf[p][i][j] (= sum_pq 2^(32 - 8p - 8q) c_pq[i][j]; the upper
+        // triangle, mirrored), 1^T Y_j = 2^-e_j cs[j]; a CTA without blocks contributes zeros
+        const double* dbuf = reinterpret_cast<const double*>(base);
+        for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
+            const int p = pq / BP, qq = pq % BP, i = p < qq ? p : qq, j = p < qq ? qq : p;
+            const double v = (dbuf[(0 * BP + i) * BP + j] + dbuf[(1 * BP + i) * BP + j]) + dbuf[(2 * BP + i) * BP + j];
+            pg[pq] = nb > 0 ? ldexp(v, -(eyb[i] + eyb[j])) : 0.0;
+        }
+        for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
+            pg[2 * kMaxB * kMaxB + qq] = nb > 0 ? ldexp(dbuf[3 * BP * BP + qq], -eyb[qq]) : 0.0;
+    } else {
+        for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
+            const int p = pq / BP, qq = pq % BP;
+            pg[pq] = red[0][p][qq] + red[1][p][qq];
+        }
+        for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
+            pg[2 * kMaxB * kMaxB + qq] = cred[0][qq] + cred[1][qq];
     }
-    for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
-        pg[2 * kMaxB * kMaxB + qq] = cred[0][qq] + cred[1][qq];
     if constexpr (WITH_H) {
         __syncthreads();
-        if (warp >= 14) {
+        if (warp == 14 || warp == 15) {
 #pragma unroll
             for (int c = 0; c < NCB; ++c)
 #pragma unroll

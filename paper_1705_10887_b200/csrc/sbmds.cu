@@ -505,6 +505,8 @@ struct sbmds_ctx {
                            // 16 = no H' (as between Rayleigh-Ritz steps), 256 = no Gram, 512 = no T drain arithmetic
     int sp8_poll = 0;      // k_sp8_step: the MMA warp's back-off (ns) between unready polls
     int sp8_pf = 0;        // k_sp8_step: L2 prefetch distance of the images, in blocks (0: off)
+    int sp8_gram8 = 1;     // k_sp8_step: int8-tensor-core Gram on steps that feed no Rayleigh-Ritz step
+    int64_t gram8_launches = 0;   // steps that took it (stat)
     int64_t s8_bytes = 0;
     // D_ll
     float* D = nullptr;
@@ -1483,7 +1485,9 @@ void colsum(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
 //   kApplySp8:     (with kApplyFused) the tensor-core sparse step k_sp8_step instead, and the
 //                  partials of kApplyY1Ready are its 128-row-block slots
 //   kApplyChol:    (with kApplySp8) the step's last CTA also factors G = R^T R into h->Rinv2
-constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8, kApplyChol = 16;
+//   kApplyGram8:   (with kApplySp8) G and 1^T Y from Y's 24-bit digits on the int8 tensor cores
+//                  (steps whose Gram feeds only the next Cholesky-QR, not a Rayleigh-Ritz step)
+constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8, kApplyChol = 16, kApplyGram8 = 32;
 
 bool ensure_sp8(sbmds_ctx* h, cudaStream_t st);
 
@@ -1491,10 +1495,14 @@ bool sp8_ok(sbmds_ctx* h, int b, cudaStream_t st) {
     return h->fuse == 3 && b == 16 && h->blocked && (h->use_blocked & 1) && ensure_sp8(h, st);
 }
 
-void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st, bool with_chol) {
+void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st, bool with_chol,
+                bool gram8) {
     using C = Sp8Cfg<16>;
-    smem_attr(k_sp8_step<16, false>, C::SMEM);
-    smem_attr(k_sp8_step<16, true>, C::SMEM);
+    smem_attr(k_sp8_step<16, false, false>, C::SMEM);
+    smem_attr(k_sp8_step<16, true, false>, C::SMEM);
+    smem_attr(k_sp8_step<16, false, true>, C::SMEM);
+    gram8 = gram8 && !Yprev && want_p1;   // (the int8 Gram reads the digits the T product stages)
+    if (gram8) ++h->gram8_launches;
     h->y16aux.ensure(352 * sizeof(unsigned int));
     unsigned int* y2mm = h->y16aux.as<unsigned int>() + 192;   // Y2 column max [0, 64) / min [64, 128) keys
     int* ey2 = reinterpret_cast<int*>(h->y16aux.as<unsigned int>() + 320);
@@ -1514,7 +1522,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2mm, ey2,
            h->s8yd.as<uint8_t>(), h->y16aux.as<unsigned int>() + 64);
     if (h->sp8_dbg & 2) h->s8trace.ensure((2048 + 8 * 64) * sizeof(unsigned long long));
-    auto kern = Yprev ? k_sp8_step<16, true> : k_sp8_step<16, false>;
+    auto kern = Yprev ? k_sp8_step<16, true, false> : (gram8 ? k_sp8_step<16, false, true> : k_sp8_step<16, false, false>);
     // non-Rayleigh-Ritz eigs steps whose next apply folds through k_blk_reduce_fold (sym8 D
     // stream) leave E2/E3 to that fold (off this kernel's tail)
     const bool defer = with_chol && !Yprev && grid >= 1 && uses_sym(h, 16) && h->dstream != 4 && !(h->sp8_dbg & 128);
@@ -1675,7 +1683,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     // A5: Y = -1/2 (S Y2 - 1 t^T)
     if ((flags & kApplyFused) && (flags & kApplySp8)) {
         profiled(h->prof, PK_CSR, st, [&] {
-            launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1) && !(h->sp8_dbg & 1), st, (flags & kApplyChol) != 0);
+            launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1) && !(h->sp8_dbg & 1), st, (flags & kApplyChol) != 0,
+                       (flags & kApplyGram8) != 0);
         });
     } else if (flags & kApplyFused) {
         const bool want_p1 = !(flags & kApplyNoP1);
@@ -3138,8 +3147,12 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         auto enqueue_iteration = [&](int itx, bool do_rr) {
             if (sp8) {
                 // A5 + Grams + the next apply's S^T Y_{k+1} partials on the int8 tensor cores (k_sp8.cuh)
+                // (a Rayleigh-Ritz step reads G_k (through R_k) and G_{k+1}: those two stay on the
+                // FP64 Gram of the fp32 rows; the others only orthonormalise the next iterate)
+                const bool rr_next = (tol > 0.0 && (itx + 1) % std::max(1, h->rr_period) == 0) || itx + 1 >= max_iters;
                 const int fl = kApplyFused | kApplySp8 | kApplyChol | (itx > 1 ? kApplyY1Ready : 0) |
-                               (itx == max_iters && !(h->sp8_dbg & 8) ? kApplyNoP1 : 0);
+                               (itx == max_iters && !(h->sp8_dbg & 8) ? kApplyNoP1 : 0) |
+                               (h->sp8_gram8 && ((!do_rr && !rr_next) || (h->sp8_dbg & 32)) ? kApplyGram8 : 0);   // (sp8_dbg & 32: diagnostics)
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl,
                              do_rr && !(h->sp8_dbg & 16) ? Yc : nullptr);
             } else if (fused) {
@@ -3923,6 +3936,8 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "sp8_poll")) {
         if (value < 0 || value > 100000) return fail(SBMDS_EINVAL, "sp8_poll must be in [0, 100000] ns");
         h->sp8_poll = (int)value;
+    } else if (!strcmp(key, "sp8_gram8")) {
+        h->sp8_gram8 = value != 0;
     } else if (!strcmp(key, "sp8_pf")) {
         if (value < 0 || value > 15) return fail(SBMDS_EINVAL, "sp8_pf must be in [0, 15] blocks");
         h->sp8_pf = (int)value;
@@ -3959,6 +3974,7 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     }
     else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a, -2 precision check
+    else if (!strcmp(key, "gram8_launches")) *value = h->gram8_launches;   // eigs steps with the int8 Gram
     else if (!strcmp(key, "sp8_range")) *value = h->sp8_range;          // its binade range (-1 not built)
     else if (!strcmp(key, "chol_retries")) *value = h->chol_retries;
     else if (!strcmp(key, "row_permuted")) *value = h->permuted ? 1 : 0;     // create kept a reordered S

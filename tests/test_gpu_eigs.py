@@ -360,3 +360,40 @@ def test_deferred_gram_and_fused_y2_digits():
     S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
     lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, p.m)
     check_against(lam, V, Z, lam_o, V_o, Z_o)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_int8_gram_steps(cfg):
+    """Eigs steps whose Gram only feeds the next Cholesky-QR take G = Y^T Y and 1^T Y from Y's
+    24-bit digits on the int8 tensor cores (k_sp8_step GRAM8; exact integer sums of the digitised
+    block); the step before a Rayleigh-Ritz step and that step keep the FP64 Gram of the fp32
+    rows. Both ways run the same iteration within the fixed point's rounding (the Gram only
+    chooses the basis of the next iterate), the int8 path is taken where expected, it is bitwise
+    deterministic, and the tolerance-mode solve converges to the oracle."""
+    p = configs.config(cfg)
+    it = 25 if cfg == 2 else 12
+    with handle(p) as h:
+        h.set_option("fuse", 3)
+        h.set_option("sp8_gram8", 0)
+        ref = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=3)
+        assert h.stat("sp8_state") == 1 and h.stat("gram8_launches") == 0
+        h.set_option("sp8_gram8", 1)
+        a = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=3)
+        # fixed-iteration solve: Rayleigh-Ritz at the end only; every step but the last two
+        assert h.stat("gram8_launches") == it - 2
+        rep = gpu_eigs(h, p.m, 16, max_iters=it, tol=0.0, seed=3)
+        n8 = h.stat("gram8_launches")
+        lam, V, Z, info = gpu_eigs(h, p.m, 16, max_iters=500, tol=1e-6, seed=5)
+        # tolerance mode, rr_period 5: steps 1-3 of every 5
+        assert h.stat("gram8_launches") - n8 == 3 * (info["iters"] // 5) + min(3, info["iters"] % 5)
+    (la, Va, _, ia), (lb, Vb, _, ib) = a, ref
+    assert np.allclose(la, lb, rtol=1e-5), (la, lb)
+    assert O.principal_angle(Va, Vb) <= 1e-3
+    assert ia["orth_error"] <= 1e-9, ia["orth_error"]
+    assert np.array_equal(la, rep[0]) and np.array_equal(Va, rep[1])
+    assert info["converged"] == 1
+    if cfg == 2:
+        S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+        lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, p.m)
+        check_against(lam, V, Z, lam_o, V_o, Z_o)
