@@ -521,7 +521,12 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 }
 
 // ------------------------------------------------------------------ the step kernel
-template <int BP>
+// GRAM8 (see k_sp8_step): no fp32 row buffers for the FP64 Gram warps. A fourth image stage then
+// fits (NS = 4 with a B_N ring of 2 and an rs1 ring of 4) and was measured: no gain (0.185 vs
+// 0.182 ms per launch at config 4) -- with the Gram off the epilogue's path the step is bound by
+// shared-memory bandwidth (~220 KB per block: the image written once by the bulk copy and read
+// once by each product's MMAs, ~75 B/clk per SM), not by the stages.
+template <int BP, bool GRAM8 = false>
 struct Sp8Cfg {
     static constexpr int NB = 3 * BP;                    // B rows [y0; y1; y2]
     static constexpr int IMG = 3 * kSp8RB * kSp8DK;      // 48 KB: largest image
@@ -531,17 +536,20 @@ struct Sp8Cfg {
     static constexpr int BT = NBT * kSp8RB;              // B of T: 128 rows x NBT (MN-major)
     static constexpr int YR = kSp8RB * BP * 4;           // fp32 rows of a block
     static constexpr int OFF_BN = NS * IMG;
-    static constexpr int NBN = 4;                        // B_N ring (staged two blocks ahead)
+    static constexpr int NBN = 4;                        // B_N ring (staged NBN blocks ahead)
     static constexpr int OFF_BT = OFF_BN + NBN * BN;
-    static constexpr int OFF_YR = OFF_BT + 2 * BT;
-    static constexpr int OFF_YP = OFF_YR + 2 * YR;
-    static constexpr int OFF_BAR = OFF_YP + 2 * YR;
+    static constexpr int OFF_YR = OFF_BT + 2 * BT;       // (GRAM8: no Y rows, no Y_prev rows)
+    static constexpr int OFF_YP = OFF_YR + (GRAM8 ? 0 : 2 * YR);
+    static constexpr int OFF_BAR = OFF_YP + (GRAM8 ? 0 : 2 * YR);
     static constexpr int MAXNB = 192;                    // blocks per CTA (per-CTA metadata table)
-    static constexpr int OFF_META = OFF_BAR + 1024;      // int64 ioff[MAXNB], int32 doff[MAXNB + 1], int32 eS[MAXNB]
-    static constexpr int NRS = 8;                        // rs1 ring: a slot is rewritten 8 blocks later, after N(i + 4)
+    static constexpr int OFF_META = OFF_BAR + 512;       // int64 ioff[MAXNB], int32 doff[MAXNB + 1], int32 eS[MAXNB]
+    // rs1 ring: slot i % NRS is rewritten when block i + NRS is staged, i.e. after N(i + NRS - NBN)
+    // has completed, which needs the epilogue's release of N(i + NRS - NBN - 2): NRS >= NBN + 2
+    static constexpr int NRS = 8;
     static constexpr int OFF_RS = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 12;   // (16-byte aligned)
-    static constexpr int SMEM = OFF_RS + NRS * kSp8RB * 4 + 1024;   // + alignment slack
+    static constexpr int SMEM = OFF_RS + NRS * kSp8RB * 4 + 128;   // + alignment slack (no swizzle: 128 B suffices)
     static_assert(OFF_RS % 16 == 0, "rs ring alignment");
+    static_assert(NRS >= NBN + 2, "rs ring depth");
     static_assert(SMEM + 1024 <= 227 * 1024, "dynamic + the kernel's 1 KB of static shared memory");
     static constexpr int THREADS = 17 * 32;   // (<= 120 registers); warp 16 issues the T products
     static constexpr int NGW = 2;                        // Gram warps (group C)
@@ -560,7 +568,7 @@ struct Sp8Cfg {
 // in one TMEM accumulator over the CTA's blocks (the digits' scales are per launch), instead of
 // the FP64 Gram of the fp32 rows: no Gram warps, no staging of Y for them.
 template <int BP, bool WITH_H, bool GRAM8>
-__global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
+__global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
     k_sp8_step(int64_t n, int64_t l_rows, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
                const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
                const uint8_t* __restrict__ Yd, const int* __restrict__ ey2in, const double* __restrict__ t,
@@ -569,7 +577,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
                unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int mode,
                double* __restrict__ Rinv_next, int* __restrict__ status, int defer_gram) {
-    using C = Sp8Cfg<BP>;
+    using C = Sp8Cfg<BP, GRAM8>;
     static_assert(!(GRAM8 && WITH_H), "the int8 Gram has no H'");
     // (diagnostics) trace[ev * 64 + i] (ev < 12; 2048 + (ev - 12) * 64 + i for ev 12..19):
     // globaltimer of event ev for block i < 64 of CTA 0
@@ -583,11 +591,11 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     constexpr int NCB = BP / 8;
     constexpr int NPG = NCB * (NCB + 1) / 2;
     constexpr int NPH = WITH_H ? NCB * NCB : 1;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
-    uint64_t* full_img = bars;          // [3]
-    uint64_t* empty_img = bars + 3;     // [3]
+    uint64_t* full_img = bars;          // [NS <= 4]
+    uint64_t* empty_img = bars + 4;     // [NS <= 4]
     uint64_t* bn_full = bars + 30;      // [4]
     uint64_t* bn_empty = bars + 34;     // [4]
     uint64_t* an_full = bars + 10;
@@ -600,7 +608,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     uint64_t* yr_empty = bars + 24;
     uint64_t* yp_full = bars + 26;
     uint64_t* yp_empty = bars + 28;
-    uint64_t* gram_full = bars + 6;     // (GRAM8) the CTA's last Gram MMA has completed
+    uint64_t* gram_full = bars + 8;     // (GRAM8) the CTA's last Gram MMA has completed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 42);
     int* ey2 = reinterpret_cast<int*>(bars + 44);          // [BP] scale exponents of Y2's columns
     int* eyb = ey2 + BP;                                   // [BP] scale exponents of Y_B's columns (static bound)
@@ -615,7 +623,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     const int pf_ahead = (mode >> 4) & 15;          // producer: L2 prefetch of the image pf_ahead blocks ahead (0: off)
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 3; ++s) {
+        for (int s = 0; s < C::NS; ++s) {
             mbar_init(&full_img[s], 1);
             mbar_init(&empty_img[s], 1);
         }
@@ -705,8 +713,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
     if (warp == 0) {
         // ------------------------------------------------ producer: B operand of N (all lanes: the
         // dictionary's Y2 digit rows, cp.async, lane g owning entries g, g + 32, ...) and the image
-        // (lane 0, one bulk copy) of each block. B(i) needs N(i - NBN) done, image(i) T(i - 3):
-        // neither waits on the epilogue or the T drain, so staging never trails the pipeline.
+        // (lane 0, one bulk copy, issued first) of each block. image(i) needs T(i - NS) done, B(i)
+        // N(i - NBN) done (with NBN = 2 that comes later, and B(i) has the image's flight time to land).
         int32_t s_d0 = m_doff[0], s_du = nb > 0 ? m_doff[1] - s_d0 : 0;
         int32_t s_j[kSp8DK / 32];
 #pragma unroll
@@ -723,6 +731,22 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
 #pragma unroll
                 for (int u = 0; u < kSp8DK / 32; ++u) s_j[u] = (32 * u + lane < s_du) ? __ldg(dict + s_d0 + 32 * u + lane) : 0;
             }
+            if (lane == 0) {
+                const int s = i % C::NS;
+                const uint32_t ph = (uint32_t)((i / C::NS) & 1);
+                const uint32_t bytes = (uint32_t)(3 * kSp8RB * dpad_of(B));
+                mbar_wait(&empty_img[s], ph ^ 1u, 141 * 65536 + (i & 0xFFFF));
+                SP8_TR(8, i);
+                mbar_arrive_expect_tx(&full_img[s], bytes);
+                bulk_load(base + s * C::IMG, gimg + m_ioff[i], bytes, &full_img[s]);
+                SP8_TR(0, i);
+                // the image pf_ahead blocks on: HBM -> L2 now, so that its load into a freed stage
+                // (three stages cover ~1.5 blocks of the ~2.2 us HBM latency) finds it in L2
+                if (pf_ahead && i + pf_ahead < nb)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gimg + m_ioff[i + pf_ahead]),
+                                 "r"((uint32_t)(3 * kSp8RB * dpad_of(B + pf_ahead))) : "memory");
+            }
+            __syncwarp();
             if (!stream_only) {
                 const int sb = i % C::NBN;
                 mbar_wait(&bn_empty[sb], ((uint32_t)((i / C::NBN) & 1)) ^ 1u, 154 * 65536 + (i & 0xFFFF));
@@ -742,29 +766,14 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
                 cp_async_arrive_noinc(&bn_full[sb]);
                 if (lane == 0) SP8_TR(7, i);
             }
-            if (lane == 0) {
-                const int s = i % 3;
-                const uint32_t ph = (uint32_t)((i / 3) & 1);
-                const uint32_t bytes = (uint32_t)(3 * kSp8RB * dpad_of(B));
-                mbar_wait(&empty_img[s], ph ^ 1u, 141 * 65536 + (i & 0xFFFF));
-                SP8_TR(8, i);
-                mbar_arrive_expect_tx(&full_img[s], bytes);
-                bulk_load(base + s * C::IMG, gimg + m_ioff[i], bytes, &full_img[s]);
-                SP8_TR(0, i);
-                // the image pf_ahead blocks on: HBM -> L2 now, so that its load into a freed stage
-                // (three stages cover ~1.5 blocks of the ~2.2 us HBM latency) finds it in L2
-                if (pf_ahead && i + pf_ahead < nb)
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gimg + m_ioff[i + pf_ahead]),
-                                 "r"((uint32_t)(3 * kSp8RB * dpad_of(B + pf_ahead))) : "memory");
-            }
             __syncwarp();
         }
     } else if (warp == 1 && stream_only) {
         // (diagnostics) consume the images without any MMA; the other roles idle
         for (int i = 0; i < nb; ++i) {
-            mbar_wait(&full_img[i % 3], (uint32_t)((i / 3) & 1), 156 * 65536 + (i & 0xFFFF));
+            mbar_wait(&full_img[i % C::NS], (uint32_t)((i / C::NS) & 1), 156 * 65536 + (i & 0xFFFF));
             if (lane == 0) SP8_TR(1, i);
-            if (elect_one()) mbar_arrive(&empty_img[i % 3]);
+            if (elect_one()) mbar_arrive(&empty_img[i % C::NS]);
             __syncwarp();
         }
     } else if (stream_only) {
@@ -784,12 +793,12 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         if (warp == 16) {
             for (int i = 0; want_t && i < nb; ++i) {
                 const int64_t B = b0 + i;
-                const int s = i % 3, a = i & 1;
+                const int s = i % C::NS, a = i & 1;
                 const uint32_t pa = (uint32_t)((i >> 1) & 1);
                 const int dp = dpad_of(B);
                 mbar_wait(&bt_full[a], pa, 145 * 65536 + (i & 0xFFFF));
                 mbar_wait(&at_empty[a], pa ^ 1u, 146 * 65536 + (i & 0xFFFF));
-                mbar_wait(&full_img[s], (uint32_t)((i / 3) & 1), 147 * 65536 + (i & 0xFFFF));   // (passed: N(i) is done)
+                mbar_wait(&full_img[s], (uint32_t)((i / C::NS) & 1), 147 * 65536 + (i & 0xFFFF));   // (passed: N(i) is done)
                 tc_fence_after();
                 if (lane == 0) SP8_TR(2, i);
                 const uint32_t sa = smem_u32(base + s * C::IMG), sb = smem_u32(base + C::OFF_BT + a * C::BT);
@@ -832,9 +841,9 @@ __global__ void __launch_bounds__(Sp8Cfg<BP>::THREADS, 1)
         } else {
             for (int i = 0; i < nb; ++i) {
                 const int64_t B = b0 + i;
-                const int s = i % 3, a = i & 1;
+                const int s = i % C::NS, a = i & 1;
                 const int dp = dpad_of(B);
-                mbar_wait(&full_img[s], (uint32_t)((i / 3) & 1), 142 * 65536 + (i & 0xFFFF));
+                mbar_wait(&full_img[s], (uint32_t)((i / C::NS) & 1), 142 * 65536 + (i & 0xFFFF));
                 mbar_wait(&bn_full[i % C::NBN], (uint32_t)((i / C::NBN) & 1), 143 * 65536 + (i & 0xFFFF));
                 mbar_wait(&an_empty[a], ((uint32_t)((i >> 1) & 1)) ^ 1u, 144 * 65536 + (i & 0xFFFF));
                 fence_proxy_async();   // B_N arrived by cp.async (generic proxy) -> visible to the MMA (async proxy)

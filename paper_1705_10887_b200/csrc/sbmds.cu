@@ -1500,7 +1500,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     using C = Sp8Cfg<16>;
     smem_attr(k_sp8_step<16, false, false>, C::SMEM);
     smem_attr(k_sp8_step<16, true, false>, C::SMEM);
-    smem_attr(k_sp8_step<16, false, true>, C::SMEM);
+    smem_attr(k_sp8_step<16, false, true>, Sp8Cfg<16, true>::SMEM);
     gram8 = gram8 && !Yprev && want_p1;   // (the int8 Gram reads the digits the T product stages)
     if (gram8) ++h->gram8_launches;
     h->y16aux.ensure(352 * sizeof(unsigned int));
@@ -1526,7 +1526,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     // non-Rayleigh-Ritz eigs steps whose next apply folds through k_blk_reduce_fold (sym8 D
     // stream) leave E2/E3 to that fold (off this kernel's tail)
     const bool defer = with_chol && !Yprev && grid >= 1 && uses_sym(h, 16) && h->dstream != 4 && !(h->sp8_dbg & 128);
-    launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
+    launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)(gram8 ? Sp8Cfg<16, true>::SMEM : C::SMEM), st, h->n, h->l, h->s8.nblk,
            (const int8_t*)h->s8img.as<int8_t>(),
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
            (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
