@@ -249,11 +249,18 @@ def run_ours(args, ws, rank, local):
     # (A5 + Grams + next A2), CUDA events around its launches during one more solve
     sparse = None
     if h.stat("sp8_state") == 1:
-        h.set_option("profile", 1 << 4)       # family "csr" = the sparse step (+ its Y2-digit pass)
+        # (events around every kernel family: with events only around this kernel its programmatic
+        # early start would count the previous kernel's tail; per-family times per iteration ride along)
+        h.set_option("profile", (1 << 10) - 1)
         h.set_option("profile_reset", 1)
+        n8 = h.stat("gram8_launches")
         step()
         torch.cuda.synchronize()
+        n8 = h.stat("gram8_launches") - n8
         sp_ns, sp_n = h.stat("csr_ns"), h.stat("csr_launches")
+        fams = {"landmark reduce + R^-1 fold + Y1 digits": "csc", "D stream": "dstream",
+                "D-partial reduce + t + Y2 digits": "dreduce", "sparse step": "csr", "Rayleigh-Ritz": "rr"}
+        fam_ms = {k: round(h.stat(f + "_ns") / 1e6 / iters, 5) for k, f in fams.items()}
         h.set_option("profile", 0)
         slots = h.stat("sp8_slots")
         # bytes the step must move per launch: the S images once, Y written once (n x b fp32), the
@@ -263,7 +270,9 @@ def run_ours(args, ws, rank, local):
         sp_s = sp_ns / max(sp_n, 1) / 1e9
         sparse = {"kernel": "k_sp8_step (tcgen05 kind::i8 on dense 128-row images of S)", "launches": int(sp_n),
                   "avg_launch_ms": sp_s * 1e3, "algorithmic_bytes_per_launch": int(sp_bytes),
-                  "achieved_gbs": sp_bytes / sp_s / 1e9, "frac_of_hbm_peak": sp_bytes / sp_s / 1e9 / hbm_peak}
+                  "achieved_gbs": sp_bytes / sp_s / 1e9, "frac_of_hbm_peak": sp_bytes / sp_s / 1e9 / hbm_peak,
+                  "int8_gram_launches": int(n8),
+                  "family_ms_per_iteration": fam_ms}
 
     # ---- end to end through the C ABI from pinned HOST buffers (create + eigs + D2H)
     e2e = None

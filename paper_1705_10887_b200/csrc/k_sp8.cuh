@@ -567,7 +567,10 @@ struct Sp8Cfg {
 // 1^T Y are formed from Y_B's digits on the int8 tensor cores, Yd^T [Yd | 1] accumulated exactly
 // in one TMEM accumulator over the CTA's blocks (the digits' scales are per launch), instead of
 // the FP64 Gram of the fp32 rows: no Gram warps, no staging of Y for them.
-template <int BP, bool WITH_H, bool GRAM8>
+// TONLY (the standalone apply's A2, S^T X): only the T products, on a block of rows given in
+// global memory (Yprev = X, n x BP fp32, staged by bulk copies into the fp32 row buffers) with
+// the column scales of `norms` (= the bits of max |X_c|, BP words): no N products, no Gram, no Y.
+template <int BP, bool WITH_H, bool GRAM8, bool TONLY = false>
 __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
     k_sp8_step(int64_t n, int64_t l_rows, int64_t nblk, const int8_t* __restrict__ gimg, const int64_t* __restrict__ ioff,
                const int32_t* __restrict__ doff, const int32_t* __restrict__ dict, const int* __restrict__ escale,
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                double* __restrict__ Rinv_next, int* __restrict__ status, int defer_gram) {
     using C = Sp8Cfg<BP, GRAM8>;
     static_assert(!(GRAM8 && WITH_H), "the int8 Gram has no H'");
+    static_assert(!TONLY || (!GRAM8 && !WITH_H), "TONLY uses the row buffers of the plain layout");
     // (diagnostics) trace[ev * 64 + i] (ev < 12; 2048 + (ev - 12) * 64 + i for ev 12..19):
     // globaltimer of event ev for block i < 64 of CTA 0
 #define SP8_TR(ev, i)                                                                          \
@@ -639,8 +643,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             mbar_init(&bt_empty[a], 1);
             mbar_init(&at_full[a], 1);
             mbar_init(&at_empty[a], 128);
-            mbar_init(&yr_full[a], 256);
-            mbar_init(&yr_empty[a], 32 * C::NGW);
+            mbar_init(&yr_full[a], TONLY ? 1 : 256);            // (TONLY: the producer's bulk copy of X_B)
+            mbar_init(&yr_empty[a], TONLY ? 256 : 32 * C::NGW);
             mbar_init(&yp_full[a], 32 * C::NGW);   // the Gram group's cp.async rows of Y_prev
         }
         fence_barrier_init();
@@ -686,10 +690,15 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
         // |Y_rc| <= 1/2 (sum_j |S_rj|) max_j |Y2 - 1 t^T|_jc + 1/2 |rs1_r| |t_c|, the digitised
         // Y2 column being <= 2^(22 - ey2_c) (no per-block maxima, no exchange between the epilogue
         // warps; the quantum is the column's, as the D stream's Y1 digits)
-        const int e2 = ey2in[threadIdx.x];
-        ey2[threadIdx.x] = e2;
-        const float bound = 0.5f * (norms[0] * pow2f(22 - e2) + norms[1] * fabsf((float)t[threadIdx.x]));
-        eyb[threadIdx.x] = i8_scale_exp(bound * 1.001f);
+        if constexpr (TONLY) {   // X's digits: one scale per column from max |X_c|
+            ey2[threadIdx.x] = 0;
+            eyb[threadIdx.x] = i8_scale_exp(__uint_as_float(reinterpret_cast<const unsigned int*>(norms)[threadIdx.x]));
+        } else {
+            const int e2 = ey2in[threadIdx.x];
+            ey2[threadIdx.x] = e2;
+            const float bound = 0.5f * (norms[0] * pow2f(22 - e2) + norms[1] * fabsf((float)t[threadIdx.x]));
+            eyb[threadIdx.x] = i8_scale_exp(bound * 1.001f);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -747,7 +756,15 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                                  "r"((uint32_t)(3 * kSp8RB * dpad_of(B + pf_ahead))) : "memory");
             }
             __syncwarp();
-            if (!stream_only) {
+            if constexpr (TONLY) {
+                if (lane == 0) {   // the block's rows of X (contiguous: rows x BP floats) into the row buffers
+                    const int a = i & 1;
+                    const uint32_t xb = (uint32_t)(rows_of(B) * BP * 4);
+                    mbar_wait(&yr_empty[a], ((uint32_t)((i >> 1) & 1)) ^ 1u, 159 * 65536 + (i & 0xFFFF));
+                    mbar_arrive_expect_tx(&yr_full[a], xb);
+                    bulk_load(base + C::OFF_YR + a * C::YR, Yprev + B * kSp8RB * BP, xb, &yr_full[a]);
+                }
+            } else if (!stream_only) {
                 const int sb = i % C::NBN;
                 mbar_wait(&bn_empty[sb], ((uint32_t)((i / C::NBN) & 1)) ^ 1u, 154 * 65536 + (i & 0xFFFF));
                 uint8_t* bn = base + C::OFF_BN + sb * C::BN;
@@ -839,7 +856,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                 if (lane == 0) SP8_TR(10, i);
             }
         } else {
-            for (int i = 0; i < nb; ++i) {
+            for (int i = 0; !TONLY && i < nb; ++i) {
                 const int64_t B = b0 + i;
                 const int s = i % C::NS, a = i & 1;
                 const int dp = dpad_of(B);
@@ -896,6 +913,27 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             const int a = i & 1;
             const uint32_t pa = (uint32_t)((i >> 1) & 1);
             const int rows = rows_of(B);
+            if constexpr (TONLY) {
+                // X_B's rows from shared memory -> digits -> B operand of T
+                mbar_wait(&yr_full[a], pa, 160 * 65536 + (i & 0xFFFF));
+                const float4* xr = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base + C::OFF_YR + a * C::YR) + r * BP + cb);
+                const float4 x0 = xr[0], x1 = xr[1];
+                mbar_arrive(&yr_empty[a]);
+                const bool livex = r < rows;   // (rows past the block's end hold stale bytes)
+                float xv[HC] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                for (int c = 0; c < HC; ++c) xv[c] = livex ? xv[c] : 0.f;
+                uint2 w0, w1, w2;
+                digit_rows8(xv, ysc, w0, w1, w2);
+                mbar_wait(&bt_empty[a], pa ^ 1u, 151 * 65536 + (i & 0xFFFF));
+                uint8_t* bt = base + C::OFF_BT + a * C::BT;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<C::NBT>(r, 0) + cb) = w0;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<C::NBT>(r, 1) + cb) = w1;
+                *reinterpret_cast<uint2*>(bt + sp8_boff<C::NBT>(r, 2) + cb) = w2;
+                fence_proxy_async();
+                mbar_arrive(&bt_full[a]);
+                continue;
+            }
             const int eS = m_es[i];
             float2 sce[HC];   // accumulator 2^(16 - eS - ey2_c) -> S Y2
 #pragma unroll
@@ -1016,7 +1054,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             // the CTA's Gram accumulator -> fp64 in shared memory (image stage 0: every MMA and load
             // of the CTA has completed once gram_full has): TMEM lane 16 p + i, column 16 q + j holds
             // sum_r d_p[r][i] d_q[r][j] (p <= 2), lane 48 the column sums of the digit planes
-            if ((warp == 12 || warp == 13) && nb > 0) {
+            if ((warp == 12 || warp == 13) && nb > 0 && want_t) {   // (no T products: no Gram, standalone A5)
                 mbar_wait(gram_full, 0u, 158 * 65536);
                 tc_fence_after();
                 const int L = 32 * (warp & 3) + lane;
@@ -1039,8 +1077,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                 }
             }
         }
-    } else if constexpr (GRAM8) {
-        // (group C idles: the Gram runs on the int8 tensor cores)
+    } else if constexpr (GRAM8 || TONLY) {
+        // (group C idles: the Gram runs on the int8 tensor cores, or there is none)
     } else {
         // ------------------------------------------------ group C (warps 14-15): the Grams on the FP64 tensor cores
         const int gt = threadIdx.x - 448;   // 0..63: rows gt, gt + 64 of Y_prev this thread stages
@@ -1164,17 +1202,19 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
     __syncthreads();
     if (blockIdx.x < 256) tail_tr(1792 + blockIdx.x);
     double* pg = part + (int64_t)blockIdx.x * kGramPart;
-    if constexpr (GRAM8) {
+    if constexpr (TONLY) {
+        (void)pg;   // no Gram
+    } else if constexpr (GRAM8) {
         // G_ij = 2^-(e_i + e_j) sum_p dbuf[p][i][j] (= sum_pq 2^(32 - 8p - 8q) c_pq[i][j]; the upper
         // triangle, mirrored), 1^T Y_j = 2^-e_j cs[j]; a CTA without blocks contributes zeros
         const double* dbuf = reinterpret_cast<const double*>(base);
         for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
             const int p = pq / BP, qq = pq % BP, i = p < qq ? p : qq, j = p < qq ? qq : p;
             const double v = (dbuf[(0 * BP + i) * BP + j] + dbuf[(1 * BP + i) * BP + j]) + dbuf[(2 * BP + i) * BP + j];
-            pg[pq] = nb > 0 ? ldexp(v, -(eyb[i] + eyb[j])) : 0.0;
+            pg[pq] = nb > 0 && want_t ? ldexp(v, -(eyb[i] + eyb[j])) : 0.0;
         }
         for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
-            pg[2 * kMaxB * kMaxB + qq] = nb > 0 ? ldexp(dbuf[3 * BP * BP + qq], -eyb[qq]) : 0.0;
+            pg[2 * kMaxB * kMaxB + qq] = nb > 0 && want_t ? ldexp(dbuf[3 * BP * BP + qq], -eyb[qq]) : 0.0;
     } else {
         for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
             const int p = pq / BP, qq = pq % BP;

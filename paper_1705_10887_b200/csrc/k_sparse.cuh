@@ -168,9 +168,16 @@ __global__ void __launch_bounds__(256) k_colsum(int64_t n, int b, const float* _
 // k_colsum for b % 4 == 0 and 16-byte aligned X: a thread owns a column quad (float4 loads)
 // and keeps eight rows in flight in four fixed-order partial sums (round 2: the scalar form ran
 // at ~2.3 TB/s on config 4's 115 MB block).
+// STAT: also the per-column max |x| (atomicMax on the float bits) and sum of squares (atomicAdd)
+// into stat[0, 64) / the 64 doubles after them (zeroed by the caller), for the check and the
+// scales of the standalone apply's tensor-core A2 (as k_ycheck's for Y1).
+template <bool STAT>
 __global__ void __launch_bounds__(256) k_colsum4(int64_t n, int b, const float* __restrict__ X, double* __restrict__ part,
-                                                 double* __restrict__ s, unsigned int* __restrict__ counter) {
+                                                 double* __restrict__ s, unsigned int* __restrict__ counter,
+                                                 unsigned int* __restrict__ stat) {
     __shared__ double red[256][4];
+    float mx[4] = {0.f, 0.f, 0.f, 0.f};
+    double sq[4] = {0.0, 0.0, 0.0, 0.0};
     const int nq = b / 4, rps = blockDim.x / nq;
     const int t = threadIdx.x, cq = t % nq, r0 = t / nq;
     const int64_t rows_per_blk = (n + gridDim.x - 1) / gridDim.x;
@@ -190,6 +197,18 @@ __global__ void __launch_bounds__(256) k_colsum4(int64_t n, int b, const float* 
                 a[u & 3][2] += (double)v[u].z;
                 a[u & 3][3] += (double)v[u].w;
             }
+            if constexpr (STAT) {
+                float q[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    mx[0] = fmaxf(mx[0], fabsf(v[u].x)); q[0] = fmaf(v[u].x, v[u].x, q[0]);
+                    mx[1] = fmaxf(mx[1], fabsf(v[u].y)); q[1] = fmaf(v[u].y, v[u].y, q[1]);
+                    mx[2] = fmaxf(mx[2], fabsf(v[u].z)); q[2] = fmaf(v[u].z, v[u].z, q[2]);
+                    mx[3] = fmaxf(mx[3], fabsf(v[u].w)); q[3] = fmaf(v[u].w, v[u].w, q[3]);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) sq[k] += (double)q[k];
+            }
         }
         for (; i < end; i += rps) {
             const float4 v = __ldcs(X4 + i * nq + cq);
@@ -197,6 +216,21 @@ __global__ void __launch_bounds__(256) k_colsum4(int64_t n, int b, const float* 
             a[0][1] += (double)v.y;
             a[0][2] += (double)v.z;
             a[0][3] += (double)v.w;
+            if constexpr (STAT) {
+                mx[0] = fmaxf(mx[0], fabsf(v.x)); sq[0] += (double)v.x * v.x;
+                mx[1] = fmaxf(mx[1], fabsf(v.y)); sq[1] += (double)v.y * v.y;
+                mx[2] = fmaxf(mx[2], fabsf(v.z)); sq[2] += (double)v.z * v.z;
+                mx[3] = fmaxf(mx[3], fabsf(v.w)); sq[3] += (double)v.w * v.w;
+            }
+        }
+    }
+    if constexpr (STAT) {
+        if (r0 < rps) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                atomicMax(stat + 4 * cq + k, __float_as_uint(mx[k]));
+                atomicAdd(reinterpret_cast<double*>(stat + 64) + 4 * cq + k, sq[k]);
+            }
         }
     }
 #pragma unroll

@@ -506,6 +506,8 @@ struct sbmds_ctx {
     int sp8_poll = 0;      // k_sp8_step: the MMA warp's back-off (ns) between unready polls
     int sp8_pf = 0;        // k_sp8_step: L2 prefetch distance of the images, in blocks (0: off)
     int sp8_gram8 = 1;     // k_sp8_step: int8-tensor-core Gram on steps that feed no Rayleigh-Ritz step
+    int sp8_apply = 1;     // standalone apply at b = 16: A5 through the tensor-core step's N products
+    int64_t sp8_apply_launches = 0, sp8_apply_t_launches = 0, x_fallbacks = 0;
     int64_t gram8_launches = 0;   // steps that took it (stat)
     int64_t s8_bytes = 0;
     // D_ll
@@ -550,6 +552,7 @@ struct sbmds_ctx {
     int dy_max_range = 3;
     bool y_fallback = false;
     int64_t y_fallbacks = 0;
+    DevBuf xstat;            // standalone apply: X's column max bits [0, 64) and sums of squares (64 doubles)
     DevBuf ychk;             // last eigs: Cholesky-QR factorisations that needed the shifted retry
     struct PairPlan {
         bool ok = false;
@@ -1469,11 +1472,61 @@ void ycheck(sbmds_ctx* h, int b, int bp, cudaStream_t st) {
 void colsum(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
     const unsigned grid = (unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256);
     if (b % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0)
-        launch(k_colsum4, dim3(grid), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(), h->s.as<double>(),
-               h->counters.as<unsigned int>() + CNT_COLSUM);
+        launch(k_colsum4<false>, dim3(grid), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(), h->s.as<double>(),
+               h->counters.as<unsigned int>() + CNT_COLSUM, (unsigned int*)nullptr);
     else
         launch(k_colsum, dim3(grid), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(), h->s.as<double>(),
                h->counters.as<unsigned int>() + CNT_COLSUM);
+}
+
+// A1 with the per-column max |x| and sum of squares of X (b = 16, X 16-byte aligned), then the
+// check of the standalone apply's tensor-core A2 (one small readback, as ycheck): X's 24-bit
+// digits take one scale per column, so a column whose max is > 2^dy_max_range times its rms (a
+// dominant row) keeps the fp32 CSC SpMM instead (stat x_fallbacks). Returns whether the
+// tensor-core path may be taken; h->xstat[0, 16) then holds the bits of max |X_c|.
+bool colsum_xcheck(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
+    h->xstat.ensure(64 * sizeof(unsigned int) + 64 * sizeof(double));
+    CK(cudaMemsetAsync(h->xstat.p, 0, h->xstat.bytes, st));
+    const unsigned grid = (unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256);
+    launch(k_colsum4<true>, dim3(grid), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(), h->s.as<double>(),
+           h->counters.as<unsigned int>() + CNT_COLSUM, h->xstat.as<unsigned int>());
+    unsigned char buf[64 * 4 + 64 * 8];
+    peek_to_host(buf, h->xstat.p, sizeof buf, st);
+    const unsigned int* mx = reinterpret_cast<const unsigned int*>(buf);
+    const double* ss = reinterpret_cast<const double*>(buf + 256);
+    const double lim = std::ldexp(1.0, h->dy_max_range);
+    for (int c = 0; c < b; ++c) {
+        float m;
+        memcpy(&m, &mx[c], 4);
+        const double rms = std::sqrt(ss[c] / (double)h->n);
+        if (!(m < 3.0e38f) || (m > 0.f && (double)m > lim * rms)) {
+            ++h->x_fallbacks;
+            return false;
+        }
+    }
+    return true;
+}
+
+// The standalone apply's A2 on the tensor cores: the T products of the sparse step on X's rows
+// (k_sp8_step TONLY), partials per 128-row block slot; k_blk_reduce then sums them per landmark.
+void launch_sp8_t(sbmds_ctx* h, const float* X, cudaStream_t st) {
+    using C = Sp8Cfg<16>;
+    auto kern = k_sp8_step<16, false, false, true>;
+    smem_attr(kern, C::SMEM);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->s8.nblk, h->num_sms));
+    h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
+    h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
+    h->s8yd.ensure((size_t)3 * h->l * 16);
+    h->y16aux.ensure(352 * sizeof(unsigned int));
+    launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
+               (const int8_t*)h->s8img.as<int8_t>(), (const int64_t*)h->s8ioff.as<int64_t>(),
+               (const int32_t*)h->s8.doff.as<int32_t>(), (const int32_t*)h->s8.dict.as<int32_t>(),
+               (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
+               (const int*)(h->y16aux.as<unsigned int>() + 320), (const double*)h->t.as<double>(),
+               (const float*)h->s8rs1.as<float>(), (const float*)h->xstat.as<float>(),
+               (const int32_t*)h->s8pos.as<int32_t>(), (float*)nullptr, h->P1.as<float>(), X, h->gpart.as<double>(),
+               h->G.as<double>(), h->H.as<double>(), h->s.as<double>(), h->counters.as<unsigned int>() + CNT_GRAM,
+               (unsigned long long*)nullptr, 0, (double*)nullptr, h->status.as<int>(), 1);
 }
 
 // The whole operator apply on device buffers (stream-ordered; the standalone apply on the int8
@@ -1495,14 +1548,20 @@ bool sp8_ok(sbmds_ctx* h, int b, cudaStream_t st) {
     return h->fuse == 3 && b == 16 && h->blocked && (h->use_blocked & 1) && ensure_sp8(h, st);
 }
 
+// no_gram: the standalone apply's A5 (N products only: no T partials, no Gram)
 void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st, bool with_chol,
-                bool gram8) {
+                bool gram8, bool no_gram = false) {
     using C = Sp8Cfg<16>;
     smem_attr(k_sp8_step<16, false, false>, C::SMEM);
     smem_attr(k_sp8_step<16, true, false>, C::SMEM);
     smem_attr(k_sp8_step<16, false, true>, Sp8Cfg<16, true>::SMEM);
     gram8 = gram8 && !Yprev && want_p1;   // (the int8 Gram reads the digits the T product stages)
     if (gram8) ++h->gram8_launches;
+    if (no_gram) {   // (the GRAM8 variant without T products forms nothing but Y)
+        gram8 = true;
+        want_p1 = false;
+        Yprev = nullptr;
+    }
     h->y16aux.ensure(352 * sizeof(unsigned int));
     unsigned int* y2mm = h->y16aux.as<unsigned int>() + 192;   // Y2 column max [0, 64) / min [64, 128) keys
     int* ey2 = reinterpret_cast<int*>(h->y16aux.as<unsigned int>() + 320);
@@ -1525,7 +1584,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     auto kern = Yprev ? k_sp8_step<16, true, false> : (gram8 ? k_sp8_step<16, false, true> : k_sp8_step<16, false, false>);
     // non-Rayleigh-Ritz eigs steps whose next apply folds through k_blk_reduce_fold (sym8 D
     // stream) leave E2/E3 to that fold (off this kernel's tail)
-    const bool defer = with_chol && !Yprev && grid >= 1 && uses_sym(h, 16) && h->dstream != 4 && !(h->sp8_dbg & 128);
+    const bool defer = no_gram || (with_chol && !Yprev && grid >= 1 && uses_sym(h, 16) && h->dstream != 4 && !(h->sp8_dbg & 128));
     launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)(gram8 ? Sp8Cfg<16, true>::SMEM : C::SMEM), st, h->n, h->l, h->s8.nblk,
            (const int8_t*)h->s8img.as<int8_t>(),
            (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
@@ -1537,7 +1596,7 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
            h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr,
            ((h->sp8_dbg & 4) ? 1 : 0) | ((h->sp8_dbg >> 7) & 6) | ((h->sp8_pf & 15) << 4) | (h->sp8_poll << 8),
            with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>(), defer ? 1 : 0);
-    h->gram_deferred = defer;
+    h->gram_deferred = defer && !no_gram;
     h->gram_parts = grid;
 }
 
@@ -1578,9 +1637,17 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
                   const double* Rinv = nullptr, int flags = 0, const float* Yprev = nullptr) {
     const int bp = next_pow2(b);
     ensure_apply_ws(h, bp);
-    // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
-    if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] { colsum(h, b, X, st); });
     const bool blk = blocked_ok(h, b, bp, X, Y);
+    // standalone apply at b = 16 with S local (k_sp8.cuh's images): A2 as the T products, A5 as the
+    // N products of the tensor-core sparse step
+    const bool sp8_a = flags == 0 && b == 16 && blk && h->sp8_apply && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                       sp8_ok(h, b, st);
+    bool sp8_a2 = false;
+    // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
+    if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] {
+        if (sp8_a && h->dy_max_range < 64) sp8_a2 = colsum_xcheck(h, b, X, st);
+        else colsum(h, b, X, st);
+    });
     // blocked mask: the option, or (auto, standalone apply) S^T X blocked and S Y2 plain for
     // b >= 32: measured on config 3 (b = 32) 0.63 ms vs 0.83 ms with the b = 16 default
     // (blocked S Y2, CSC S^T X), DESIGN.md §4
@@ -1645,6 +1712,14 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
                 default: go_r(k_blk_reduce<8>); break;
             }
         });
+    } else if (sp8_a2) {
+        profiled(h->prof, PK_CSC, st, [&] {
+            launch_sp8_t(h, X, st);
+            launch(k_blk_reduce<4>, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
+                   (const int32_t*)h->s8.jptr.as<int32_t>(), (const int32_t*)nullptr,   // landmark-major partials
+                   (const float*)h->P1.as<float>(), wvec(h), (const double*)h->s.as<double>(), h->Y1.as<float>());
+        });
+        ++h->sp8_apply_t_launches;
     } else if (blk && (bmask & 2)) {
         h->P1.ensure((size_t)std::max<int32_t>(1, h->total_u) * kMaxB * sizeof(float));
         const size_t smem_t = (size_t)kRB * bp * sizeof(float);
@@ -1675,7 +1750,9 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp, Rinv != nullptr))
         ycheck(h, b, bp, st);
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
-    h->y2d_want = (flags & kApplyFused) && (flags & kApplySp8) && b == 16 && !(h->sp8_dbg & 64);   // (sp8_dbg & 64: separate k_y2_digits, diagnostics)
+    // standalone apply at b = 16: A5 through the N products of the tensor-core sparse step
+    const bool sp8_a5 = sp8_a;
+    h->y2d_want = (((flags & kApplyFused) && (flags & kApplySp8)) || sp8_a5) && b == 16 && !(h->sp8_dbg & 64);   // (sp8_dbg & 64: separate k_y2_digits, diagnostics)
     h->y2d_ready = false;
     dstream(h, b, bp, st, Rinv);
     h->y2d_want = false;
@@ -1696,6 +1773,11 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
                 default: launch_fused<8>(h, b, Y, Yprev, want_p1, st); break;
             }
         });
+    } else if (sp8_a5) {
+        // standalone apply: the N products of the tensor-core sparse step (S_B as dense digit
+        // images, Y2 - 1 t^T as 24-bit digits; k_sp8.cuh) instead of the row-blocked fp32 SpMM
+        profiled(h->prof, PK_CSR, st, [&] { launch_sp8(h, b, Y, nullptr, false, st, false, false, true); });
+        ++h->sp8_apply_launches;
     } else if (blk && (bmask & 1)) {
         const size_t smem = (size_t)h->umax * bp * sizeof(float);
         auto go = [&](auto kern) {
@@ -1904,7 +1986,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
                       &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
-                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->Y1w, &h->Y2w, &h->tsave, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
+                      &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->xstat, &h->Y1w, &h->Y2w, &h->tsave, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
                       &h->s8plan[1].tiles, &h->s8plan[1].pbeg, &h->s8plan[1].sbase, &h->s8plan[1].xptr, &h->s8plan[1].xslot, &h->s8plan[1].smap,
                       &h->s8plan[2].tiles, &h->s8plan[2].pbeg, &h->s8plan[2].sbase, &h->s8plan[2].xptr, &h->s8plan[2].xslot, &h->s8plan[2].smap,
@@ -3936,6 +4018,8 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
     } else if (!strcmp(key, "sp8_poll")) {
         if (value < 0 || value > 100000) return fail(SBMDS_EINVAL, "sp8_poll must be in [0, 100000] ns");
         h->sp8_poll = (int)value;
+    } else if (!strcmp(key, "sp8_apply")) {
+        h->sp8_apply = value != 0;
     } else if (!strcmp(key, "sp8_gram8")) {
         h->sp8_gram8 = value != 0;
     } else if (!strcmp(key, "sp8_pf")) {
@@ -3974,6 +4058,9 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     }
     else if (!strcmp(key, "blocked_slots")) *value = h->total_u;
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a, -2 precision check
+    else if (!strcmp(key, "sp8_apply_launches")) *value = h->sp8_apply_launches;   // standalone applies whose A5 took it
+    else if (!strcmp(key, "sp8_apply_t_launches")) *value = h->sp8_apply_t_launches;   // ... whose A2 took it
+    else if (!strcmp(key, "x_fallbacks")) *value = h->x_fallbacks;   // ... whose X failed the column check
     else if (!strcmp(key, "gram8_launches")) *value = h->gram8_launches;   // eigs steps with the int8 Gram
     else if (!strcmp(key, "sp8_range")) *value = h->sp8_range;          // its binade range (-1 not built)
     else if (!strcmp(key, "chol_retries")) *value = h->chol_retries;
