@@ -393,6 +393,8 @@ def run_apply_mode(args, ws, rank, local, p):
     ds_ns, ds_n = h.stat("dstream_ns"), h.stat("dstream_launches")
     ds_path, ds_bytes = h.stat("dstream_path"), h.stat("dstream_bytes")
     h.set_option("profile", 0)
+    sp8_path = h.stat("sp8_apply_launches") > 0
+    sp8_t = h.stat("sp8_apply_t_launches") > 0
     ms_max = max_over_ranks(ms, ws, device="cuda")
     apply_s = ms / 1e3 / steps
     path_bytes = ds_bytes + 16 * p.nnz + 4 * (p.n + 1) + 4 * (p.l + 1) + 8 * p.n * b
@@ -407,8 +409,15 @@ def run_apply_mode(args, ws, rank, local, p):
                    "l2": "no flush: S, D and X, Y exceed the 126 MB L2 at configs 3-5"},
         "roofline": {"bound": "hbm", "achieved": path_bytes / apply_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                      "frac": path_bytes / apply_s / 1e9 / hbm_peak, "traffic": None,
-                     "kernel": "whole apply (" + DSTREAM_KERNELS.get(ds_path, str(ds_path)) + " + CSC/CSR SpMMs)",
-                     "algorithmic_bytes_per_launch": int(path_bytes)},
+                     "kernel": "whole apply (" + DSTREAM_KERNELS.get(ds_path, str(ds_path)) + " + " +
+                               ("k_sp8_step T-only / N-only on the digit images of S" if sp8_path else "CSC/CSR SpMMs") + ")",
+                     "algorithmic_bytes_per_launch": int(path_bytes),
+                     "bytes_basis": "D stream's bytes + S once through CSR and once through CSC (16 B per nonzero) + "
+                                    "pointers + X, Y; the tensor-core sparse path reads its images (sparse_image_bytes, "
+                                    "twice per apply) instead of CSR/CSC and is charged the same algorithmic bytes"},
+        "sparse_path": {"a5_on_tensor_cores": bool(sp8_path), "a2_on_tensor_cores": bool(sp8_t),
+                        "sparse_image_bytes": int(h.stat("sp8_bytes")) if sp8_path else 0,
+                        "x_fallbacks": int(h.stat("x_fallbacks"))},
         "dstream": {"kernel": DSTREAM_KERNELS.get(ds_path, str(ds_path)), "avg_launch_ms": ds_s * 1e3,
                     "bytes_per_launch": ds_bytes, "gbs": ds_bytes / ds_s / 1e9, "frac": ds_bytes / ds_s / 1e9 / hbm_peak},
         "apply_full_d_equivalent_gbs": algorithmic_bytes(p, b) / apply_s / 1e9,

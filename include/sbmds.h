@@ -20,7 +20,8 @@
  *     pointers on the device the call is asynchronous on `cuda_stream` (eigs reads a
  *     small convergence flag back every rr_period iterations; the first call of a handle
  *     reads D's precision check back once; a standalone apply on the int8 stream reads
- *     its Y1 column check back unless "dy_max_range" >= 64).
+ *     its Y1 column check back, and at b = 16 on the tensor-core sparse kernels X's column
+ *     check, unless "dy_max_range" >= 64).
  *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
  *   - Dense blocks (X, Y, V, Z) are row-major n x b fp32: the b values of vertex i
  *     are contiguous at offset i*b.
@@ -213,6 +214,18 @@ const char* sbmds_last_error(void);
  *                      (k_sp8.cuh: A5 + Grams + next A2 on the int8 tensor cores from dense
  *                      128-row digit images of S) where it applies -- b = 16 and every
  *                      128-row block touching <= 128 landmarks -- else as 1
+ *     "sp8_gram8"      (0/1, default 1) eigs on the tensor-core step: steps whose Gram only feeds
+ *                      the next Cholesky-QR (neither a Rayleigh-Ritz step nor the one before it)
+ *                      take G = Y^T Y and 1^T Y from Y's 24-bit digits on the int8 tensor cores
+ *                      (exact integer sums) instead of the FP64 Gram of the fp32 rows (stat
+ *                      "gram8_launches")
+ *     "sp8_apply"      (0/1, default 1) standalone sbmds_apply at b = 16 where the tensor-core
+ *                      step applies: A2 = S^T X as its T products (unless X fails the column
+ *                      check of "dy_max_range": stat "x_fallbacks") and A5 as its N products
+ *                      (stats "sp8_apply_t_launches", "sp8_apply_launches"); 0 keeps the fp32
+ *                      CSC / row-blocked CSR kernels
+ *     "sp8_pf"         (blocks, default 0) tensor-core step: L2 prefetch distance of the images
+ *                      (measured: no gain)
  *     "solver"         eigs: 0 (default) block subspace iteration; 1 restarted block Lanczos with
  *                      full reorthogonalisation (block <= 32, k
  *                      blocks of b per cycle with k b <= 64; max_iters counts block applies)
@@ -235,8 +248,10 @@ const char* sbmds_last_error(void);
                       max |D| (stat "dq_range"); otherwise the full D on 3xTF32 (stat "dq_state" -1)
      "dy_max_range"   (binades, default 3) standalone apply on the int8 stream: a Y1 column whose
                       max |y| exceeds 2^range times its rms sends that apply to the fp32-grade
-                      stream (stat "y_fallbacks"); the check reads 0.8 KB back (a stream sync),
-                      >= 64 turns it off (no host sync: the apply can then be graph-captured)
+                      stream (stat "y_fallbacks"); likewise a column of X for the tensor-core A2
+                      (stat "x_fallbacks": that apply's S^T X stays on the fp32 CSC kernel); each
+                      check reads 0.8 KB back (a stream sync), >= 64 turns both off (no host
+                      sync: the apply can then be graph-captured; A2 then stays on the CSC kernel)
      "sp8_max_range"  (binades, default 7) tensor-core sparse step: a 128-row block whose smallest
                       nonzero row maximum sits more than this many binades below the block's max
                       keeps the eigs step on the fp32 sparse kernels (stat "sp8_state" -2,

@@ -224,14 +224,25 @@ __global__ void __launch_bounds__(256) k_colsum4(int64_t n, int b, const float* 
             }
         }
     }
-    if constexpr (STAT) {
-        if (r0 < rps) {
+    if constexpr (STAT) {   // block-level first: one atomic pair per column per block
+        __shared__ float smx[256][4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                atomicMax(stat + 4 * cq + k, __float_as_uint(mx[k]));
-                atomicAdd(reinterpret_cast<double*>(stat + 64) + 4 * cq + k, sq[k]);
-            }
+        for (int k = 0; k < 4; ++k) {
+            smx[t][k] = (r0 < rps) ? mx[k] : 0.f;
+            red[t][k] = (r0 < rps) ? sq[k] : 0.0;
         }
+        __syncthreads();
+        if (t < b) {
+            float m = 0.f;
+            double v = 0.0;
+            for (int q = 0; q < rps; ++q) {
+                m = fmaxf(m, smx[q * nq + t / 4][t % 4]);
+                v += red[q * nq + t / 4][t % 4];
+            }
+            atomicMax(stat + t, __float_as_uint(m));
+            atomicAdd(reinterpret_cast<double*>(stat + 64) + t, v);
+        }
+        __syncthreads();
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) red[t][k] = (r0 < rps) ? (a[0][k] + a[1][k]) + (a[2][k] + a[3][k]) : 0.0;
