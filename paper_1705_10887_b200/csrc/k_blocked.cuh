@@ -26,17 +26,26 @@ namespace sbmds {
 constexpr int kRB = 256;   // rows per block (local row fits in 8 bits)
 
 // ------------------------------------------------------------------ create-time build
-__global__ void k_blk_offsets(int64_t n, int64_t nblk, int rb, const int32_t* __restrict__ rp, int32_t* __restrict__ off) {
+// Blocks are rb consecutive rows each, or (brow0 != NULL) the row ranges [brow0[B], brow0[B + 1])
+// with blkof[row] = B (the tensor-core sparse step splits a 128-row block whose dictionary
+// exceeds its image into shorter ones).
+__global__ void k_blk_offsets(int64_t n, int64_t nblk, int rb, const int32_t* __restrict__ rp, int32_t* __restrict__ off,
+                              const int32_t* __restrict__ brow0) {
     for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B <= nblk; B += (int64_t)gridDim.x * blockDim.x)
-        off[B] = rp[min(B * rb, n)];
+        off[B] = rp[brow0 ? (int64_t)brow0[B] : min(B * rb, n)];
+}
+
+__global__ void k_blk_fill_blkof(int64_t nblk, const int32_t* __restrict__ brow0, int32_t* __restrict__ blkof) {
+    for (int64_t B = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; B < nblk; B += (int64_t)gridDim.x * blockDim.x)
+        for (int32_t r = brow0[B]; r < brow0[B + 1]; ++r) blkof[r] = (int32_t)B;
 }
 
 // flag[p] = 1 where a new (block, column) pair starts in the block-segmented col sort.
 __global__ void k_blk_flags(int32_t nnz, int rb, const int32_t* __restrict__ scol, const int32_t* __restrict__ perm,
                             const int32_t* __restrict__ rowof, const int32_t* __restrict__ off,
-                            int32_t* __restrict__ flag) {
+                            int32_t* __restrict__ flag, const int32_t* __restrict__ blkof) {
     for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x) {
-        const int32_t B = rowof[perm[p]] / rb;
+        const int32_t B = blkof ? blkof[rowof[perm[p]]] : rowof[perm[p]] / rb;
         flag[p] = (p == off[B] || scol[p] != scol[p - 1]) ? 1 : 0;
     }
 }
@@ -64,11 +73,12 @@ __global__ void k_blk_scatter(int32_t nnz, int rb, const int32_t* __restrict__ s
                               const int32_t* __restrict__ flag, const int32_t* __restrict__ incl,
                               const int32_t* __restrict__ dict_off, int32_t* __restrict__ dict,
                               int32_t* __restrict__ lcp, uint16_t* __restrict__ lcol, uint8_t* __restrict__ lrow,
-                              float* __restrict__ lval) {
+                              float* __restrict__ lval, const int32_t* __restrict__ blkof,
+                              const int32_t* __restrict__ brow0) {
     for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x) {
         const int32_t e = perm[p];
         const int32_t row = rowof[e];
-        const int32_t B = row / rb;
+        const int32_t B = blkof ? blkof[row] : row / rb;
         const int32_t d = incl[p] - 1;
         if (flag[p]) {
             dict[d] = scol[p];
@@ -76,7 +86,7 @@ __global__ void k_blk_scatter(int32_t nnz, int rb, const int32_t* __restrict__ s
         }
         lcol[e] = (uint16_t)(d - dict_off[B]);
         if (lrow) {
-            lrow[p] = (uint8_t)(row - B * rb);
+            lrow[p] = (uint8_t)(row - (brow0 ? brow0[B] : B * rb));
             lval[p] = val[e];
         }
     }

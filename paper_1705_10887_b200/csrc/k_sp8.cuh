@@ -202,12 +202,12 @@ __global__ void __launch_bounds__(128) k_sp8_build(int64_t n, int64_t nblk, cons
                                                    const float* __restrict__ val, const uint16_t* __restrict__ lcol,
                                                    const int32_t* __restrict__ doff, const int64_t* __restrict__ ioff,
                                                    int8_t* __restrict__ img, int* __restrict__ escale,
-                                                   unsigned int* __restrict__ rrange) {
+                                                   unsigned int* __restrict__ rrange, const int32_t* __restrict__ brow0) {
     __shared__ float red[4], red2[4];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int64_t B = blockIdx.x; B < nblk; B += gridDim.x) {
-        const int64_t r0 = B * kSp8RB;
-        const int rows = (int)((n - r0) < kSp8RB ? (n - r0) : kSp8RB);
+        const int64_t r0 = brow0[B];   // the block's rows [brow0[B], brow0[B + 1]): <= 128
+        const int rows = (int)(brow0[B + 1] - r0);
         float m = 0.f, mn = INFINITY;   // block max |S|, smallest nonzero row max (this warp's rows)
         for (int r = wid; r < rows; r += 4) {
             const int32_t beg = rp[r0 + r], end = rp[r0 + r + 1];
@@ -342,10 +342,13 @@ __global__ void __launch_bounds__(256) k_colminmax(int64_t l, int bp, const floa
 // bits of the digits cover what survives the centring.
 // (max |Y2_c - t_c| = max(max_c - t_c, t_c - min_c) from the column max / min keys; block 0
 // records the exponents for the step kernel)
+// (pitch: floats per row of Y2; a 16-column half of a wider block passes Y2, t, y2mm, ey2_out
+// offset by its first column)
 template <int BP>
 __device__ __forceinline__ void y2_digits_body(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
                                                const unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
-                                               uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
+                                               uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next,
+                                               int pitch = BP) {
     static_assert(BP == 16, "b = 16");
     // zero_next: the Y1f column maxima the next iteration's k_blk_reduce_fold accumulates (this
     // iteration's k_y8_split has read them)
@@ -361,7 +364,7 @@ __device__ __forceinline__ void y2_digits_body(int64_t l, const float* __restric
     }
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < l; j += (int64_t)gridDim.x * blockDim.x) {
         float v[BP];
-        const float4* src = reinterpret_cast<const float4*>(Y2 + j * BP);
+        const float4* src = reinterpret_cast<const float4*>(Y2 + j * pitch);
 #pragma unroll
         for (int c4 = 0; c4 < BP / 4; ++c4) {
             const float4 x = src[c4];
@@ -381,10 +384,11 @@ __device__ __forceinline__ void y2_digits_body(int64_t l, const float* __restric
 template <int BP>
 __global__ void __launch_bounds__(256) k_y2_digits(int64_t l, const float* __restrict__ Y2, const double* __restrict__ t,
                                                    const unsigned int* __restrict__ y2mm, int* __restrict__ ey2_out,
-                                                   uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next) {
+                                                   uint8_t* __restrict__ Yd, unsigned int* __restrict__ zero_next,
+                                                   int pitch) {
     pdl_trigger();
     pdl_wait();
-    y2_digits_body<BP>(l, Y2, t, y2mm, ey2_out, Yd, zero_next);
+    y2_digits_body<BP>(l, Y2, t, y2mm, ey2_out, Yd, zero_next, pitch);
 }
 
 // k_dreduce_pair's reduction at b = 16 with 16-byte loads: a thread owns four columns of one
@@ -546,7 +550,8 @@ struct Sp8Cfg {
     // rs1 ring: slot i % NRS is rewritten when block i + NRS is staged, i.e. after N(i + NRS - NBN)
     // has completed, which needs the epilogue's release of N(i + NRS - NBN - 2): NRS >= NBN + 2
     static constexpr int NRS = 8;
-    static constexpr int OFF_RS = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 12;   // (16-byte aligned)
+    // int64 ioff[MAXNB], int32 doff[MAXNB + 1], int32 eS[MAXNB], int32 r0[MAXNB + 1] (+ 8: 16-byte aligned)
+    static constexpr int OFF_RS = OFF_META + 8 * MAXNB + 4 * (MAXNB + 1) + 4 * MAXNB + 4 * (MAXNB + 1) + 8;
     static constexpr int SMEM = OFF_RS + NRS * kSp8RB * 4 + 128;   // + alignment slack (no swizzle: 128 B suffices)
     static_assert(OFF_RS % 16 == 0, "rs ring alignment");
     static_assert(NRS >= NBN + 2, "rs ring depth");
@@ -579,7 +584,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                float* __restrict__ Y, float* __restrict__ P1, const float* __restrict__ Yprev,
                double* __restrict__ part, double* __restrict__ G, double* __restrict__ H, double* __restrict__ cs,
                unsigned int* __restrict__ counter, unsigned long long* __restrict__ trace, int mode,
-               double* __restrict__ Rinv_next, int* __restrict__ status, int defer_gram) {
+               double* __restrict__ Rinv_next, int* __restrict__ status, int defer_gram, int ypitch, int p1pitch,
+               const int32_t* __restrict__ brow0) {
     using C = Sp8Cfg<BP, GRAM8>;
     static_assert(!(GRAM8 && WITH_H), "the int8 Gram has no H'");
     static_assert(!TONLY || (!GRAM8 && !WITH_H), "TONLY uses the row buffers of the plain layout");
@@ -624,6 +630,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
     const bool want_t = P1 != nullptr;
     const bool stream_only = (mode & 1) != 0;    // (diagnostics) images streamed, no MMA
     const unsigned poll_ns = (unsigned)mode >> 8;   // MMA warp: back-off between unready polls
+    const bool no_gram = (mode & 8) != 0;           // (GRAM8) a 16-column half of a wider block: no Gram here
     const int pf_ahead = (mode >> 4) & 15;          // producer: L2 prefetch of the image pf_ahead blocks ahead (0: off)
 
     if (threadIdx.x == 0) {
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             mbar_init(&bt_empty[a], 1);
             mbar_init(&at_full[a], 1);
             mbar_init(&at_empty[a], 128);
-            mbar_init(&yr_full[a], TONLY ? 1 : 256);            // (TONLY: the producer's bulk copy of X_B)
+            mbar_init(&yr_full[a], TONLY ? (ypitch == BP ? 1 : 32) : 256);   // (TONLY: the producer's copy of X_B)
             mbar_init(&yr_empty[a], TONLY ? 256 : 32 * C::NGW);
             mbar_init(&yp_full[a], 32 * C::NGW);   // the Gram group's cp.async rows of Y_prev
         }
@@ -653,8 +660,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
     int64_t* m_ioff = reinterpret_cast<int64_t*>(base + C::OFF_META);
     int32_t* m_doff = reinterpret_cast<int32_t*>(m_ioff + C::MAXNB);
     int32_t* m_es = m_doff + C::MAXNB + 1;
+    int32_t* m_r0 = m_es + C::MAXNB;   // first row of each block (blocks are <= 128 consecutive rows)
     for (int k = threadIdx.x; k <= nb; k += blockDim.x) {
         m_doff[k] = __ldg(doff + b0 + k);
+        m_r0[k] = __ldg(brow0 + b0 + k);
         if (k < nb) {
             m_ioff[k] = __ldg(ioff + b0 + k);
             m_es[k] = __ldg(escale + b0 + k);
@@ -704,10 +713,8 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
     __syncthreads();
     tc_fence_after();
     auto dpad_of = [&](int64_t B) { return sp8_dpad(m_doff[B - b0 + 1] - m_doff[B - b0]); };
-    auto rows_of = [&](int64_t B) {
-        const int64_t r0 = B * kSp8RB;
-        return (int)((n - r0) < kSp8RB ? (n - r0) : kSp8RB);
-    };
+    auto rows_of = [&](int64_t B) { return (int)(m_r0[B - b0 + 1] - m_r0[B - b0]); };
+    auto row0_of = [&](int64_t B) { return (int64_t)m_r0[B - b0]; };
 
     // Gram accumulators live in warps 10-11 (per-warp DMMA fragments, as k_fused.cuh)
     // two interleaved accumulator sets (even / odd 4-row steps) halve the DMMA dependency chains
@@ -757,12 +764,24 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             }
             __syncwarp();
             if constexpr (TONLY) {
-                if (lane == 0) {   // the block's rows of X (contiguous: rows x BP floats) into the row buffers
-                    const int a = i & 1;
-                    const uint32_t xb = (uint32_t)(rows_of(B) * BP * 4);
-                    mbar_wait(&yr_empty[a], ((uint32_t)((i >> 1) & 1)) ^ 1u, 159 * 65536 + (i & 0xFFFF));
-                    mbar_arrive_expect_tx(&yr_full[a], xb);
-                    bulk_load(base + C::OFF_YR + a * C::YR, Yprev + B * kSp8RB * BP, xb, &yr_full[a]);
+                // the block's rows of X into the row buffers: one bulk copy where they are contiguous
+                // (ypitch == BP), else 16-byte cp.async chunks (a 16-column half of a wider block)
+                const int a = i & 1;
+                const int xrows = rows_of(B);
+                mbar_wait(&yr_empty[a], ((uint32_t)((i >> 1) & 1)) ^ 1u, 159 * 65536 + (i & 0xFFFF));
+                if (ypitch == BP) {
+                    if (lane == 0) {
+                        const uint32_t xb = (uint32_t)(xrows * BP * 4);
+                        mbar_arrive_expect_tx(&yr_full[a], xb);
+                        bulk_load(base + C::OFF_YR + a * C::YR, Yprev + row0_of(B) * BP, xb, &yr_full[a]);
+                    }
+                } else {
+                    for (int q = lane; q < xrows * (BP / 4); q += 32) {
+                        const int rr = q / (BP / 4), ch = q % (BP / 4);
+                        cp_async16(base + C::OFF_YR + a * C::YR + (rr * BP + 4 * ch) * 4,
+                                   Yprev + (row0_of(B) + rr) * (int64_t)ypitch + 4 * ch);
+                    }
+                    cp_async_arrive_noinc(&yr_full[a]);
                 }
             } else if (!stream_only) {
                 const int sb = i % C::NBN;
@@ -779,7 +798,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                 // the block's row-sum deviations (512 B, one 16-byte chunk per lane; rs1 is padded to
                 // whole blocks) into their ring: the epilogue reads them from shared memory, with
                 // no global load between the N accumulator and the digits
-                cp_async16(base + C::OFF_RS + ((i % C::NRS) * kSp8RB + 4 * lane) * 4, rs1 + B * kSp8RB + 4 * lane);
+                cp_async16(base + C::OFF_RS + ((i % C::NRS) * kSp8RB + 4 * lane) * 4, rs1 + row0_of(B) + 4 * lane);
                 cp_async_arrive_noinc(&bn_full[sb]);
                 if (lane == 0) SP8_TR(7, i);
             }
@@ -837,7 +856,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                         tc_mma_i8(d + 2 * BP, umma_desc_none(sa + 2 * plane + 512 * j, 128, 2048), bd, id3t, 1u);
                     }
                     tc_commit(&at_full[a]);
-                    if constexpr (GRAM8) {
+                    if (GRAM8 && !no_gram) {
                         // Yd^T [Yd | 1]: M = the image's 16-byte chunks as rows (digit planes 0-2, the
                         // ones chunk: lanes 0-48 are used, the rest read the next K group), K = the
                         // block's rows, N = 3 BP; one accumulator for the whole CTA (exact in int32:
@@ -980,7 +999,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             }
             // (after the digits, which gate the T product and the image's release)
             if (live) {
-                float4* dst = reinterpret_cast<float4*>(Y + (B * kSp8RB + r) * BP + cb);
+                float4* dst = reinterpret_cast<float4*>(Y + (row0_of(B) + r) * (int64_t)ypitch + cb);
                 dst[0] = make_float4(y[0], y[1], y[2], y[3]);
                 dst[1] = make_float4(y[4], y[5], y[6], y[7]);
             }
@@ -1029,7 +1048,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             tc_fence_before();
             mbar_arrive(&at_empty[a]);
             if (lrow < du) {
-                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)pos * BP);
+                float4* dst = reinterpret_cast<float4*>(P1 + (int64_t)pos * p1pitch);
 #pragma unroll
                 for (int c = 0; c < BP; c += 4) dst[c / 4] = make_float4(out[c], out[c + 1], out[c + 2], out[c + 3]);
             }
@@ -1054,7 +1073,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
             // the CTA's Gram accumulator -> fp64 in shared memory (image stage 0: every MMA and load
             // of the CTA has completed once gram_full has): TMEM lane 16 p + i, column 16 q + j holds
             // sum_r d_p[r][i] d_q[r][j] (p <= 2), lane 48 the column sums of the digit planes
-            if ((warp == 12 || warp == 13) && nb > 0 && want_t) {   // (no T products: no Gram, standalone A5)
+            if ((warp == 12 || warp == 13) && nb > 0 && want_t && !no_gram) {   // (no T products: no Gram, standalone A5)
                 mbar_wait(gram_full, 0u, 158 * 65536);
                 tc_fence_after();
                 const int L = 32 * (warp & 3) + lane;
@@ -1134,7 +1153,7 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
                 for (int h = 0; h < 2; ++h) {
                     const int rr = gt + 64 * h;
                     if (rr < rows) {
-                        const uint8_t* src = reinterpret_cast<const uint8_t*>(Yprev + (B * kSp8RB + rr) * BP);
+                        const uint8_t* src = reinterpret_cast<const uint8_t*>(Yprev + (row0_of(B) + rr) * BP);
 #pragma unroll
                         for (int u = 0; u < BP / 4; ++u) cp_async16(yp + rr * BP * 4 + 16 * u, src + 16 * u);
                     }
@@ -1211,10 +1230,10 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
         for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
             const int p = pq / BP, qq = pq % BP, i = p < qq ? p : qq, j = p < qq ? qq : p;
             const double v = (dbuf[(0 * BP + i) * BP + j] + dbuf[(1 * BP + i) * BP + j]) + dbuf[(2 * BP + i) * BP + j];
-            pg[pq] = nb > 0 && want_t ? ldexp(v, -(eyb[i] + eyb[j])) : 0.0;
+            pg[pq] = nb > 0 && want_t && !no_gram ? ldexp(v, -(eyb[i] + eyb[j])) : 0.0;
         }
         for (int qq = threadIdx.x; qq < BP; qq += blockDim.x)
-            pg[2 * kMaxB * kMaxB + qq] = nb > 0 && want_t ? ldexp(dbuf[3 * BP * BP + qq], -eyb[qq]) : 0.0;
+            pg[2 * kMaxB * kMaxB + qq] = nb > 0 && want_t && !no_gram ? ldexp(dbuf[3 * BP * BP + qq], -eyb[qq]) : 0.0;
     } else {
         for (int pq = threadIdx.x; pq < BP * BP; pq += blockDim.x) {
             const int p = pq / BP, qq = pq % BP;

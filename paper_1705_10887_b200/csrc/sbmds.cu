@@ -359,12 +359,13 @@ struct DevBuf {
 // columns (CSR order), optional block-local CSC, and landmark -> dictionary-slot lists.
 struct BlkIdx {
     DevBuf doff{true}, dict{true}, lcol{true}, lcp{true}, lrow{true}, lval{true}, jptr{true}, jlist{true};
+    DevBuf brow0{true};   // (tensor-core step) first row of each block, nblk + 1 entries: blocks are <= rb rows
     int rb = 0;
     int64_t nblk = 0;
     int32_t total_u = 0;
     uint32_t umax = 0;
     void reset() {
-        for (DevBuf* b : {&doff, &dict, &lcol, &lcp, &lrow, &lval, &jptr, &jlist}) b->release();
+        for (DevBuf* b : {&doff, &dict, &lcol, &lcp, &lrow, &lval, &jptr, &jlist, &brow0}) b->release();
         rb = 0;
         nblk = 0;
         total_u = 0;
@@ -508,6 +509,7 @@ struct sbmds_ctx {
     int sp8_gram8 = 1;     // k_sp8_step: int8-tensor-core Gram on steps that feed no Rayleigh-Ritz step
     int sp8_apply = 1;     // standalone apply at b = 16: A5 through the tensor-core step's N products
     int64_t sp8_apply_launches = 0, sp8_apply_t_launches = 0, x_fallbacks = 0;
+    int64_t sp8_splits = 0;   // 128-row blocks halved because their dictionary exceeded one image
     int64_t gram8_launches = 0;   // steps that took it (stat)
     int64_t s8_bytes = 0;
     // D_ll
@@ -1509,7 +1511,7 @@ bool colsum_xcheck(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
 
 // The standalone apply's A2 on the tensor cores: the T products of the sparse step on X's rows
 // (k_sp8_step TONLY), partials per 128-row block slot; k_blk_reduce then sums them per landmark.
-void launch_sp8_t(sbmds_ctx* h, const float* X, cudaStream_t st) {
+void launch_sp8_t(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
     using C = Sp8Cfg<16>;
     auto kern = k_sp8_step<16, false, false, true>;
     smem_attr(kern, C::SMEM);
@@ -1518,15 +1520,17 @@ void launch_sp8_t(sbmds_ctx* h, const float* X, cudaStream_t st) {
     h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
     h->s8yd.ensure((size_t)3 * h->l * 16);
     h->y16aux.ensure(352 * sizeof(unsigned int));
-    launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
-               (const int8_t*)h->s8img.as<int8_t>(), (const int64_t*)h->s8ioff.as<int64_t>(),
-               (const int32_t*)h->s8.doff.as<int32_t>(), (const int32_t*)h->s8.dict.as<int32_t>(),
-               (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
-               (const int*)(h->y16aux.as<unsigned int>() + 320), (const double*)h->t.as<double>(),
-               (const float*)h->s8rs1.as<float>(), (const float*)h->xstat.as<float>(),
-               (const int32_t*)h->s8pos.as<int32_t>(), (float*)nullptr, h->P1.as<float>(), X, h->gpart.as<double>(),
-               h->G.as<double>(), h->H.as<double>(), h->s.as<double>(), h->counters.as<unsigned int>() + CNT_GRAM,
-               (unsigned long long*)nullptr, 0, (double*)nullptr, h->status.as<int>(), 1);
+    for (int c0 = 0; c0 < b; c0 += 16)   // (b = 32: one pass per 16-column half of X)
+        launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, st, h->n, h->l, h->s8.nblk,
+                   (const int8_t*)h->s8img.as<int8_t>(), (const int64_t*)h->s8ioff.as<int64_t>(),
+                   (const int32_t*)h->s8.doff.as<int32_t>(), (const int32_t*)h->s8.dict.as<int32_t>(),
+                   (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
+                   (const int*)(h->y16aux.as<unsigned int>() + 320), (const double*)h->t.as<double>(),
+                   (const float*)h->s8rs1.as<float>(), (const float*)h->xstat.as<float>() + c0,
+                   (const int32_t*)h->s8pos.as<int32_t>(), (float*)nullptr, h->P1.as<float>() + c0, X + c0,
+                   h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
+                   h->counters.as<unsigned int>() + CNT_GRAM, (unsigned long long*)nullptr, 0, (double*)nullptr,
+                   h->status.as<int>(), 1, b, b, (const int32_t*)h->s8.brow0.as<int32_t>());
 }
 
 // The whole operator apply on device buffers (stream-ordered; the standalone apply on the int8
@@ -1543,23 +1547,33 @@ void launch_sp8_t(sbmds_ctx* h, const float* X, cudaStream_t st) {
 constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8, kApplyChol = 16, kApplyGram8 = 32;
 
 bool ensure_sp8(sbmds_ctx* h, cudaStream_t st);
+// index of the two norms behind the padded row-sum deviations in h->s8rs1
+int64_t sp8_rs_pad(const sbmds_ctx* h) { return ((h->n + 3) & ~(int64_t)3) + kSp8RB; }
 
 bool sp8_ok(sbmds_ctx* h, int b, cudaStream_t st) {
     return h->fuse == 3 && b == 16 && h->blocked && (h->use_blocked & 1) && ensure_sp8(h, st);
 }
 
-// no_gram: the standalone apply's A5 (N products only: no T partials, no Gram)
+// no_gram: the standalone apply's A5 (N products only: no T partials, no Gram).
+// b = 32: two passes over the images, one per 16-column half of the block (the kernel's widths
+// are 16: a 32-wide step would need TMEM and shared memory it does not have); the halves share
+// nothing but the images, so no Gram is formed here (the caller runs the Gram kernel on Y).
 void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1, cudaStream_t st, bool with_chol,
                 bool gram8, bool no_gram = false) {
     using C = Sp8Cfg<16>;
     smem_attr(k_sp8_step<16, false, false>, C::SMEM);
     smem_attr(k_sp8_step<16, true, false>, C::SMEM);
     smem_attr(k_sp8_step<16, false, true>, Sp8Cfg<16, true>::SMEM);
-    gram8 = gram8 && !Yprev && want_p1;   // (the int8 Gram reads the digits the T product stages)
+    const int nh = b / 16;   // 16-column halves
+    gram8 = gram8 && !Yprev && want_p1 && nh == 1;   // (the int8 Gram reads the digits the T product stages)
     if (gram8) ++h->gram8_launches;
     if (no_gram) {   // (the GRAM8 variant without T products forms nothing but Y)
         gram8 = true;
         want_p1 = false;
+        Yprev = nullptr;
+    }
+    if (nh == 2) {   // (no Gram in the kernel: GRAM8 layout, mode bit 8)
+        gram8 = true;
         Yprev = nullptr;
     }
     h->y16aux.ensure(352 * sizeof(unsigned int));
@@ -1568,35 +1582,43 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     if (h->last_dpath != 3 && h->last_dpath != 4) {   // the full-D reductions do not form the keys
         CK(cudaMemsetAsync(y2mm, 0, 64 * sizeof(unsigned int), st));
         CK(cudaMemsetAsync(y2mm + 64, 0xFF, 64 * sizeof(unsigned int), st));
-        launch(k_colminmax, dim3((unsigned)std::min<int64_t>(2 * 148, (h->l + 15) / 16)), dim3(256), 0, st, h->l, 16,
+        launch(k_colminmax, dim3((unsigned)std::min<int64_t>(2 * 148, (h->l + 15) / 16)), dim3(256), 0, st, h->l, b,
                (const float*)h->Y2.as<float>(), y2mm);
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->s8.nblk, h->num_sms));
     h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
     h->P1.ensure((size_t)std::max<int32_t>(std::max(1, h->s8.total_u), h->total_u) * kMaxB * sizeof(float));
-    // Y2's digit planes (one pass over l x 16), then the step
-    h->s8yd.ensure((size_t)3 * h->l * 16);
-    if (!h->y2d_ready)
-    launch_pdl(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
-           (const float*)h->Y2.as<float>(), (const double*)h->t.as<double>(), (const unsigned int*)y2mm, ey2,
-           h->s8yd.as<uint8_t>(), h->y16aux.as<unsigned int>() + 64);
+    // Y2's digit planes (one pass over l x 16 per half), then the step
+    h->s8yd.ensure((size_t)3 * h->l * 16 * nh);
     if (h->sp8_dbg & 2) h->s8trace.ensure((2048 + 8 * 64) * sizeof(unsigned long long));
     auto kern = Yprev ? k_sp8_step<16, true, false> : (gram8 ? k_sp8_step<16, false, true> : k_sp8_step<16, false, false>);
     // non-Rayleigh-Ritz eigs steps whose next apply folds through k_blk_reduce_fold (sym8 D
     // stream) leave E2/E3 to that fold (off this kernel's tail)
-    const bool defer = no_gram || (with_chol && !Yprev && grid >= 1 && uses_sym(h, 16) && h->dstream != 4 && !(h->sp8_dbg & 128));
-    launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)(gram8 ? Sp8Cfg<16, true>::SMEM : C::SMEM), st, h->n, h->l, h->s8.nblk,
-           (const int8_t*)h->s8img.as<int8_t>(),
-           (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
-           (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)h->s8yd.as<uint8_t>(),
-           (const int*)ey2, (const double*)h->t.as<double>(), (const float*)h->s8rs1.as<float>(),
-           (const float*)h->s8rs1.as<float>() + h->s8.nblk * kSp8RB, (const int32_t*)h->s8pos.as<int32_t>(), Y,
-           want_p1 ? h->P1.as<float>() : nullptr,
-           Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
-           h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr,
-           ((h->sp8_dbg & 4) ? 1 : 0) | ((h->sp8_dbg >> 7) & 6) | ((h->sp8_pf & 15) << 4) | (h->sp8_poll << 8),
-           with_chol ? h->Rinv2.as<double>() : nullptr, h->status.as<int>(), defer ? 1 : 0);
-    h->gram_deferred = defer && !no_gram;
+    const bool defer = no_gram || nh == 2 ||
+                       (with_chol && !Yprev && grid >= 1 && uses_sym(h, 16) && h->dstream != 4 && !(h->sp8_dbg & 128));
+    for (int hf = 0; hf < nh; ++hf) {
+        const int c0 = 16 * hf;
+        uint8_t* yd = h->s8yd.as<uint8_t>() + (size_t)hf * 3 * h->l * 16;
+        if (!h->y2d_ready)
+            launch_pdl(k_y2_digits<16>, dim3((unsigned)std::min<int64_t>(4 * 148, (h->l + 255) / 256)), dim3(256), 0, st, h->l,
+                       (const float*)h->Y2.as<float>() + c0, (const double*)h->t.as<double>() + c0,
+                       (const unsigned int*)y2mm + c0, ey2 + c0, yd,
+                       hf == 0 ? h->y16aux.as<unsigned int>() + 64 : (unsigned int*)nullptr, b);
+        launch_pdl(kern, dim3(grid), dim3(C::THREADS), (size_t)(gram8 ? Sp8Cfg<16, true>::SMEM : C::SMEM), st, h->n, h->l,
+               h->s8.nblk, (const int8_t*)h->s8img.as<int8_t>(),
+               (const int64_t*)h->s8ioff.as<int64_t>(), (const int32_t*)h->s8.doff.as<int32_t>(),
+               (const int32_t*)h->s8.dict.as<int32_t>(), (const int*)h->s8esc.as<int>(), (const uint8_t*)yd,
+               (const int*)ey2 + c0, (const double*)h->t.as<double>() + c0, (const float*)h->s8rs1.as<float>(),
+               (const float*)h->s8rs1.as<float>() + sp8_rs_pad(h), (const int32_t*)h->s8pos.as<int32_t>(), Y + c0,
+               want_p1 ? h->P1.as<float>() + c0 : nullptr,
+               Yprev, h->gpart.as<double>(), h->G.as<double>(), h->H.as<double>(), h->s.as<double>(),
+               h->counters.as<unsigned int>() + CNT_GRAM, (h->sp8_dbg & 2) ? h->s8trace.as<unsigned long long>() : nullptr,
+               ((h->sp8_dbg & 4) ? 1 : 0) | ((h->sp8_dbg >> 7) & 6) | (nh == 2 ? 8 : 0) | ((h->sp8_pf & 15) << 4) |
+                   (h->sp8_poll << 8),
+               with_chol && nh == 1 ? h->Rinv2.as<double>() : nullptr, h->status.as<int>(), defer ? 1 : 0, b, b,
+               (const int32_t*)h->s8.brow0.as<int32_t>());
+    }
+    h->gram_deferred = defer && !no_gram && nh == 1;
     h->gram_parts = grid;
 }
 
@@ -1640,8 +1662,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     const bool blk = blocked_ok(h, b, bp, X, Y);
     // standalone apply at b = 16 with S local (k_sp8.cuh's images): A2 as the T products, A5 as the
     // N products of the tensor-core sparse step
-    const bool sp8_a = flags == 0 && b == 16 && blk && h->sp8_apply && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
-                       sp8_ok(h, b, st);
+    const bool sp8_a = flags == 0 && (b == 16 || b == 32) && blk && h->sp8_apply &&
+                       (reinterpret_cast<uintptr_t>(X) & 15) == 0 && sp8_ok(h, 16, st);
     bool sp8_a2 = false;
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
     if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] {
@@ -1714,10 +1736,14 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         });
     } else if (sp8_a2) {
         profiled(h->prof, PK_CSC, st, [&] {
-            launch_sp8_t(h, X, st);
-            launch(k_blk_reduce<4>, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
-                   (const int32_t*)h->s8.jptr.as<int32_t>(), (const int32_t*)nullptr,   // landmark-major partials
-                   (const float*)h->P1.as<float>(), wvec(h), (const double*)h->s.as<double>(), h->Y1.as<float>());
+            launch_sp8_t(h, b, X, st);
+            auto go_r = [&](auto kern) {
+                launch(kern, dim3((unsigned)((h->l + 7) / 8)), dim3(256), 0, st, h->l, b, bp,
+                       (const int32_t*)h->s8.jptr.as<int32_t>(), (const int32_t*)nullptr,   // landmark-major partials
+                       (const float*)h->P1.as<float>(), wvec(h), (const double*)h->s.as<double>(), h->Y1.as<float>());
+            };
+            if (b == 16) go_r(k_blk_reduce<4>);
+            else go_r(k_blk_reduce<8>);
         });
         ++h->sp8_apply_t_launches;
     } else if (blk && (bmask & 2)) {
@@ -1803,10 +1829,12 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
 // Row-blocked S (k_blocked.cuh): segmented stable sort of each rb-row block's entries by
 // column, unique -> per-block dictionary, 16-bit local columns (CSR order), optionally the
 // block-local CSC (sorted order), and for each landmark its dictionary slots in block order.
-void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, BlkIdx& o, cudaStream_t st) {
+// (brow0 / blkof / nblk_var: blocks of <= rb rows with explicit row ranges instead of rb rows each)
+void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, BlkIdx& o, cudaStream_t st,
+                     const int32_t* brow0 = nullptr, const int32_t* blkof = nullptr, int64_t nblk_var = 0) {
     const int64_t n = h->n, l = h->l, nnz = h->nnz;
     o.rb = rb;
-    o.nblk = (n + rb - 1) / rb;
+    o.nblk = brow0 ? nblk_var : (n + rb - 1) / rb;
     const int64_t nb = o.nblk;
     // temporaries from the stream-ordered pool (every use completes before the stream syncs below)
     DevBuf off{true}, scol{true}, iota_perm{true}, flag{true}, incl{true}, tmp{true}, keys2{true};
@@ -1818,7 +1846,7 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
     int32_t* iota = iota_perm.as<int32_t>();
     int32_t* perm = iota + nnz;
     launch(k_blk_offsets, dim3((unsigned)std::min<int64_t>(1024, (nb + 256) / 256)), dim3(256), 0, st, n, nb, rb,
-           (const int32_t*)h->rp.as<int32_t>(), off.as<int32_t>());
+           (const int32_t*)h->rp.as<int32_t>(), off.as<int32_t>(), brow0);
     launch(k_iota, dim3(1024), dim3(256), 0, st, (int32_t)nnz, iota);
     size_t tb = 0;
     CK(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, h->col.as<int32_t>(), scol.as<int32_t>(), iota, perm,
@@ -1828,7 +1856,7 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
                                                  (int)nnz, (int)nb, off.as<int32_t>(), off.as<int32_t>() + 1, st));
     g_launches.fetch_add(1);
     launch(k_blk_flags, dim3(1024), dim3(256), 0, st, (int32_t)nnz, rb, (const int32_t*)scol.as<int32_t>(),
-           (const int32_t*)perm, rowof, (const int32_t*)off.as<int32_t>(), flag.as<int32_t>());
+           (const int32_t*)perm, rowof, (const int32_t*)off.as<int32_t>(), flag.as<int32_t>(), blkof);
     tb = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tb, flag.as<int32_t>(), incl.as<int32_t>(), (int)nnz, st));
     DevBuf tmp2{true};
@@ -1855,7 +1883,7 @@ void build_blk_index(sbmds_ctx* h, const int32_t* rowof, int rb, bool want_csc, 
            (const int32_t*)perm, rowof, (const float*)h->val.as<float>(), (const int32_t*)flag.as<int32_t>(),
            (const int32_t*)incl.as<int32_t>(), (const int32_t*)o.doff.as<int32_t>(), o.dict.as<int32_t>(),
            want_csc ? o.lcp.as<int32_t>() : nullptr, o.lcol.as<uint16_t>(), want_csc ? o.lrow.as<uint8_t>() : nullptr,
-           want_csc ? o.lval.as<float>() : nullptr);
+           want_csc ? o.lval.as<float>() : nullptr, blkof, brow0);
     const int32_t nnz32 = (int32_t)nnz;
     if (want_csc)
         CK(cudaMemcpyAsync(o.lcp.as<int32_t>() + total_u, &nnz32, sizeof(int32_t), cudaMemcpyHostToDevice, st));
@@ -1921,10 +1949,56 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
            bad.as<int>());
     BlkIdx& o = h->s8;
     build_blk_index(h, rowof.as<int32_t>(), kSp8RB, false, o, st);
+    // block row ranges: 128 rows each; a block whose dictionary exceeds one image (an ordering
+    // jump inside it: a Morton-numbered mesh has a few) is halved, at multiples of 4 rows, until
+    // its pieces fit (the image keeps 128 row slots, the unused ones zero)
+    std::vector<int32_t> r0((size_t)o.nblk + 1);
+    for (int64_t B = 0; B <= o.nblk; ++B) r0[B] = (int32_t)std::min<int64_t>(B * kSp8RB, h->n);
+    h->sp8_splits = 0;
+    for (int round = 0; o.umax > (uint32_t)kSp8DK && round < 6; ++round) {
+        if ((double)o.umax > 4.0 * kSp8DK && round == 0) break;   // (not local at all: random structure)
+        std::vector<int32_t> doff((size_t)o.nblk + 1);
+        CK(cudaMemcpyAsync(doff.data(), o.doff.p, doff.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<int32_t> nr;
+        nr.reserve(r0.size() + 64);
+        bool stuck = false;
+        for (int64_t B = 0; B < o.nblk; ++B) {
+            nr.push_back(r0[B]);
+            const int32_t rows = r0[B + 1] - r0[B];
+            if (doff[B + 1] - doff[B] > kSp8DK) {
+                if (rows < 8) { stuck = true; break; }
+                nr.push_back(r0[B] + ((rows / 2 + 3) & ~3));
+                ++h->sp8_splits;
+            }
+        }
+        nr.push_back((int32_t)h->n);
+        if (stuck || nr.size() > (size_t)2 * ((h->n + kSp8RB - 1) / kSp8RB) + 2) break;   // (would double the images)
+        r0.swap(nr);
+        const int64_t nb2 = (int64_t)r0.size() - 1;
+        o.reset();
+        o.brow0.ensure(r0.size() * sizeof(int32_t));
+        CK(cudaMemcpyAsync(o.brow0.p, r0.data(), r0.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        DevBuf blkof{true};
+        blkof.ensure(h->n * sizeof(int32_t));
+        launch(k_blk_fill_blkof, dim3((unsigned)std::min<int64_t>(1024, (nb2 + 255) / 256)), dim3(256), 0, st, nb2,
+               (const int32_t*)o.brow0.as<int32_t>(), blkof.as<int32_t>());
+        DevBuf keep{true};
+        keep.swap(o.brow0);   // (build_blk_index leaves brow0 alone, reset() above must not free it mid-build)
+        build_blk_index(h, rowof.as<int32_t>(), kSp8RB, false, o, st, (const int32_t*)keep.as<int32_t>(),
+                        (const int32_t*)blkof.as<int32_t>(), nb2);
+        o.brow0.swap(keep);
+        CK(cudaStreamSynchronize(st));   // (r0 / the pool temporaries of this round)
+    }
     if (o.umax > (uint32_t)kSp8DK ||   // a block touches more landmarks than one image holds, or
         (o.nblk + h->num_sms - 1) / h->num_sms > Sp8Cfg<16>::MAXNB) {   // a CTA's metadata table overflows
         o.reset();
         return false;
+    }
+    if (!o.brow0.p) {   // the plain ranges
+        o.brow0.ensure(r0.size() * sizeof(int32_t));
+        CK(cudaMemcpyAsync(o.brow0.p, r0.data(), r0.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
     }
     h->s8ioff.ensure((o.nblk + 1) * sizeof(int64_t));
     DevBuf sizes{true}, tmp{true};
@@ -1947,7 +2021,8 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     launch(k_sp8_build, dim3((unsigned)std::min<int64_t>(o.nblk, 32 * (int64_t)h->num_sms)), dim3(128), 0, st, h->n,
            o.nblk, (const int32_t*)h->rp.as<int32_t>(), (const float*)h->val.as<float>(),
            (const uint16_t*)o.lcol.as<uint16_t>(), (const int32_t*)o.doff.as<int32_t>(),
-           (const int64_t*)h->s8ioff.as<int64_t>(), h->s8img.as<int8_t>(), h->s8esc.as<int>(), bad.as<unsigned int>());
+           (const int64_t*)h->s8ioff.as<int64_t>(), h->s8img.as<int8_t>(), h->s8esc.as<int>(), bad.as<unsigned int>(),
+           (const int32_t*)o.brow0.as<int32_t>());
     unsigned int rrange = 0;
     peek_to_host(&rrange, bad.p, sizeof rrange, st);
     h->sp8_range = (int)rrange;
@@ -1965,9 +2040,9 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     h->s8pos.ensure(std::max<int32_t>(1, o.total_u) * sizeof(int32_t));
     launch(k_inverse_perm, dim3(1024), dim3(256), 0, st, o.total_u, (const int32_t*)o.jlist.as<int32_t>(),
            h->s8pos.as<int32_t>());
-    // rs1 padded with zeros to whole 128-row blocks (the step stages 512 B per block), then the
+    // rs1 padded with 128 zeros (the step stages 512 B from each block's first row), then the
     // two norms of the step's a-priori bound on |Y| (k_rowsum_m1)
-    const int64_t rs_pad = o.nblk * kSp8RB;
+    const int64_t rs_pad = sp8_rs_pad(h);
     h->s8rs1.ensure((rs_pad + 4) * sizeof(float));
     CK(cudaMemsetAsync(h->s8rs1.as<float>() + h->n, 0, (rs_pad + 4 - h->n) * sizeof(float), st));
     launch(k_rowsum_m1, dim3((unsigned)std::min<int64_t>(4 * 148, (h->n + 255) / 256)), dim3(256), 0, st, h->n,
@@ -1984,7 +2059,7 @@ void for_each_buf(sbmds_ctx* h, F&& f) {
                       &h->bdoff, &h->bdict, &h->blcp, &h->blcol, &h->blrow, &h->blval, &h->bjptr, &h->bjlist,
                       &h->P1, &h->Y1, &h->Y2, &h->P, &h->colpart, &h->s, &h->t, &h->tpart, &h->counters, &h->X, &h->Y,
                       &h->gpart, &h->G, &h->H, &h->Rinv, &h->Rinv2, &h->status, &h->rr, &h->vtmp, &h->ztmp, &h->sign,
-                      &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
+                      &h->s8.doff, &h->s8.dict, &h->s8.lcol, &h->s8.jptr, &h->s8.jlist, &h->s8.brow0, &h->s8img, &h->s8ioff, &h->s8esc, &h->s8yd, &h->s8rs1, &h->s8pos,
                       &h->lzQ, &h->lzW, &h->lzC, &h->lzT, &h->lzGl, &h->lzI, &h->lzR,
                       &h->apval, &h->apidx, &h->xhost, &h->yhost, &h->vsel, &h->Y1T, &h->w0, &h->rawR, &h->Dt, &h->pdbg, &h->Y16T, &h->Y1f, &h->y16aux, &h->Dt8, &h->Y8T, &h->dqhist, &h->ychk, &h->xstat, &h->Y1w, &h->Y2w, &h->tsave, &h->vg, &h->perm, &h->xperm, &h->yperm, &h->foldscr, &h->s8trace,
                       &h->s8plan[0].tiles, &h->s8plan[0].pbeg, &h->s8plan[0].sbase, &h->s8plan[0].xptr, &h->s8plan[0].xslot, &h->s8plan[0].smap,
@@ -4060,6 +4135,8 @@ extern "C" sbmds_status sbmds_get_stat(sbmds_t h, const char* key, int64_t* valu
     else if (!strcmp(key, "sp8_state")) *value = h->sp8_state;          // tensor-core sparse step: 1 built, -1 n/a, -2 precision check
     else if (!strcmp(key, "sp8_apply_launches")) *value = h->sp8_apply_launches;   // standalone applies whose A5 took it
     else if (!strcmp(key, "sp8_apply_t_launches")) *value = h->sp8_apply_t_launches;   // ... whose A2 took it
+    else if (!strcmp(key, "sp8_splits")) *value = h->sp8_splits;   // 128-row blocks halved to fit their images
+    else if (!strcmp(key, "sp8_blocks")) *value = h->s8.nblk;
     else if (!strcmp(key, "x_fallbacks")) *value = h->x_fallbacks;   // ... whose X failed the column check
     else if (!strcmp(key, "gram8_launches")) *value = h->gram8_launches;   // eigs steps with the int8 Gram
     else if (!strcmp(key, "sp8_range")) *value = h->sp8_range;          // its binade range (-1 not built)

@@ -489,3 +489,57 @@ def test_apply_on_tensor_core_sparse_kernels(kind):
     assert relerr(Y32, ref) <= TOL
     assert relerr(Y, Y32) <= 5e-6
     assert np.array_equal(Y, Y_again)
+
+
+def test_apply_b32_on_tensor_core_sparse_kernels():
+    """b = 32 (config 3's width) on the tensor-core sparse kernels: two passes over the images,
+    one per 16-column half of X (strided rows, cp.async staging) and of Y2 / Y."""
+    p = configs.config(2)
+    X = configs.x_block(p.n, 32, seed=13)
+    ref = oracle_apply(p, X)
+    with make_handle(p) as h:
+        n0, t0 = h.stat("sp8_apply_launches"), h.stat("sp8_apply_t_launches")
+        Y = run_apply(h, X)
+        assert h.stat("sp8_apply_launches") == n0 + 1 and h.stat("sp8_apply_t_launches") == t0 + 1
+        Y_again = run_apply(h, X)
+        h.set_option("sp8_apply", 0)
+        Y32 = run_apply(h, X)
+    assert relerr(Y, ref) <= TOL, relerr(Y, ref)
+    assert relerr(Y32, ref) <= TOL
+    assert relerr(Y, Y32) <= 5e-6
+    assert np.array_equal(Y, Y_again)
+
+
+def test_tensor_core_sparse_kernels_split_blocks():
+    """A 128-row block whose rows sit in two distant regions of the mesh touches more landmarks
+    than one 128-column image holds (a Morton-numbered mesh has such blocks at the curve's
+    jumps): the build halves it (stat sp8_splits) instead of giving up the tensor-core kernels.
+    Config 2 with seven 16-row ranges of block 0 swapped with rows far across the mesh: apply (b = 16, 32) and the eigs step
+    against the oracle."""
+    p0 = configs.config(2)
+    n = p0.n
+    perm = np.arange(n)
+    for q in range(7):   # block 0 then holds 16 rows of each of eight regions: 163 distinct landmarks
+        a, b_ = 16 * (q + 1), 12_000 * (q + 1) + 16 * (q + 1)
+        perm[a:a + 16], perm[b_:b_ + 16] = np.arange(b_, b_ + 16), np.arange(a, a + 16)
+    lens = np.diff(p0.row_ptr)[perm]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    row_ptr[1:] = np.cumsum(lens)
+    idx = np.concatenate([np.arange(p0.row_ptr[r], p0.row_ptr[r + 1]) for r in perm])
+    p = configs.Problem("cfg2_swapped", n, p0.l, row_ptr, p0.col_idx[idx], p0.val[idx], p0.D)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    with make_handle(p) as h:
+        for b in (16, 32):
+            X = configs.x_block(p.n, b, seed=b)
+            n0 = h.stat("sp8_apply_launches")
+            Y = run_apply(h, X)
+            assert h.stat("sp8_state") == 1 and h.stat("sp8_splits") >= 1 and h.stat("sp8_apply_launches") == n0 + 1
+            assert h.stat("sp8_blocks") > (n + 127) // 128
+            assert relerr(Y, O.apply(S, p.D, X.astype(np.float64))) <= TOL
+        torch = _torch()
+        lam, V, Z, info = h.eigs(3, 16, max_iters=500, tol=1e-6)
+        torch.cuda.synchronize()
+        assert info["converged"] == 1 and h.stat("gram8_launches") > 0
+    lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, 3)
+    assert np.all(np.abs(np.asarray(lam) - lam_o) <= 1e-4 * np.abs(lam_o))
+    assert O.principal_angle(V.cpu().numpy().astype(np.float64), V_o) <= 1e-3
