@@ -1544,9 +1544,13 @@ void launch_sp8_t(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
 //   kApplyChol:    (with kApplySp8) the step's last CTA also factors G = R^T R into h->Rinv2
 //   kApplyGram8:   (with kApplySp8) G and 1^T Y from Y's 24-bit digits on the int8 tensor cores
 //                  (steps whose Gram feeds only the next Cholesky-QR, not a Rayleigh-Ritz step)
-constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8, kApplyChol = 16, kApplyGram8 = 32;
+//   kApplySp8Halves: (with kApplySp8, b = 32) the step as two 16-column passes over the images, then the
+//                  Gram kernel on Y (the halves share no Gram)
+constexpr int kApplyY1Ready = 1, kApplyFused = 2, kApplyNoP1 = 4, kApplySp8 = 8, kApplyChol = 16, kApplyGram8 = 32,
+              kApplySp8Halves = 64;
 
 bool ensure_sp8(sbmds_ctx* h, cudaStream_t st);
+void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, bool want_s);
 // index of the two norms behind the padded row-sum deviations in h->s8rs1
 int64_t sp8_rs_pad(const sbmds_ctx* h) { return ((h->n + 3) & ~(int64_t)3) + kSp8RB; }
 
@@ -1789,6 +1793,8 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
             launch_sp8(h, b, Y, Yprev, !(flags & kApplyNoP1) && !(h->sp8_dbg & 1), st, (flags & kApplyChol) != 0,
                        (flags & kApplyGram8) != 0);
         });
+        // G = Y^T Y, s = 1^T Y (and H' = Yprev^T Y) of the two halves together
+        if (flags & kApplySp8Halves) gram(h, b, Y, Yprev, st, true);
     } else if (flags & kApplyFused) {
         const bool want_p1 = !(flags & kApplyNoP1);
         profiled(h->prof, PK_CSR, st, [&] {
@@ -3299,6 +3305,9 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         bool converged = false;
         const bool fused = fused_ok(h, b) && blocked_ok(h, b, b, Yc, Yn);
         const bool sp8 = fused && sp8_ok(h, b, st);   // tensor-core sparse step (fuse = 3)
+        // b = 32 (config 3): the same kernel as two 16-column passes per step, Gram and Cholesky
+        // by their own kernels
+        const bool sp8h = !sp8 && fused && b == 32 && h->fuse == 3 && h->sp8_apply && sp8_ok(h, 16, st);
         // one iteration's device work: Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1} (s = 1^T Y_k came from
         // the last Gram), the Grams, and at Rayleigh-Ritz steps the Jacobi solve (no host syncs)
         auto enqueue_iteration = [&](int itx, bool do_rr) {
@@ -3312,6 +3321,10 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                                (h->sp8_gram8 && ((!do_rr && !rr_next) || (h->sp8_dbg & 32)) ? kApplyGram8 : 0);   // (sp8_dbg & 32: diagnostics)
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl,
                              do_rr && !(h->sp8_dbg & 16) ? Yc : nullptr);
+            } else if (sp8h) {
+                const int fl = kApplyFused | kApplySp8 | kApplySp8Halves | (itx > 1 ? kApplyY1Ready : 0) |
+                               (itx == max_iters ? kApplyNoP1 : 0);
+                apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
             } else if (fused) {
                 // A5 fused with G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, H' = Y_k^T Y_{k+1} (RR) and
                 // (fuse = 2) the next apply's S^T Y_{k+1} partials (k_fused.cuh)

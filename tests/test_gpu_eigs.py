@@ -397,3 +397,25 @@ def test_int8_gram_steps(cfg):
         S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
         lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, p.m)
         check_against(lam, V, Z, lam_o, V_o, Z_o)
+
+
+@pytest.mark.gpu
+def test_eigs_b32_two_half_passes():
+    """block = 32 where S is local: the tensor-core sparse step runs as two 16-column passes over
+    the images per iteration (Gram and Cholesky by their own kernels). Same iteration as the fp32
+    fused kernels (sp8_apply = 0 keeps them), bitwise deterministic, converges to the oracle."""
+    p = configs.config(2)
+    with handle(p) as h:
+        h.set_option("sp8_apply", 0)
+        ref = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)
+        h.set_option("sp8_apply", 1)
+        a = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)
+        assert h.stat("sp8_state") == 1
+        rep = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)
+        lam, V, Z, info = gpu_eigs(h, 3, 32, max_iters=500, tol=1e-6, seed=5)
+    assert np.allclose(a[0], ref[0], rtol=1e-5), (a[0], ref[0])
+    assert np.array_equal(a[0], rep[0]) and np.array_equal(a[1], rep[1])
+    assert info["converged"] == 1
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, 3)
+    check_against(lam, V, Z, lam_o, V_o, Z_o)
