@@ -251,6 +251,29 @@ __device__ __forceinline__ double ordered_sum(const double* __restrict__ p, int 
     return acc;
 }
 
+// ordered_sum for the four entries tid, tid + 256, tid + 512, tid + 768 (< nent) of a 256-thread
+// last block at once: the loads of all four of a batch are in flight together (a b = 32 Gram's
+// last block otherwise serialises ~80 L2 round trips per thread). Each entry is added in index
+// order (absent entries and the batch tail add exact zeros), so the sums equal ordered_sum's.
+template <int U = 8>
+__device__ __forceinline__ void ordered_sum_x4(const double* __restrict__ p, int tid, int nent, int count,
+                                               int64_t stride, double (&acc)[4]) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[e] = 0.0;
+    for (int q = 0; q < count; q += U) {
+        double v[4][U];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                v[e][u] = (tid + 256 * e < nent && q + u < count) ? p[(int64_t)(q + u) * stride + tid + 256 * e] : 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[e] += v[e][u];
+    }
+}
+
 // Block-wide fixed-order column sums for a last block: out[c] = sum over q < count of
 // p[q * stride + c], 1 <= ncols <= 256. Thread (c, k), k < 256 / ncols, sums chunk k of the q
 // range in order, then thread c adds the chunk results in order: a fixed order, so the result

@@ -263,9 +263,18 @@ __global__ void __launch_bounds__(256) k_gram_tc(int64_t n, int b, const float* 
     if (last_block_done(counter)) {
         if (cs)
             for (int q = threadIdx.x; q < b; q += 256) cs[q] = ordered_sum(part + 2 * kMaxB * kMaxB + q, gridDim.x, kGramPart);
-        for (int pq = threadIdx.x; pq < b * b; pq += 256) {
-            G[pq] = ordered_sum(part + pq, gridDim.x, kGramPart);
-            if constexpr (WITH_H) H[pq] = ordered_sum(part + kMaxB * kMaxB + pq, gridDim.x, kGramPart);
+        {   // this thread's entries tid + 256 e (b <= 32: at most 4), their partial loads batched together
+            double o[4];
+            ordered_sum_x4(part, (int)threadIdx.x, b * b, gridDim.x, kGramPart, o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((int)threadIdx.x + 256 * e < b * b) G[threadIdx.x + 256 * e] = o[e];
+            if constexpr (WITH_H) {
+                ordered_sum_x4(part + kMaxB * kMaxB, (int)threadIdx.x, b * b, gridDim.x, kGramPart, o);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if ((int)threadIdx.x + 256 * e < b * b) H[threadIdx.x + 256 * e] = o[e];
+            }
         }
         if (threadIdx.x == 0) *counter = 0;
     }
