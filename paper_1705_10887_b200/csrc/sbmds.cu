@@ -1448,25 +1448,36 @@ void ensure_apply_ws(sbmds_ctx* h, int bp) {
 // product, so a column whose max sits far above its rms (an X with a dominant row) keeps its
 // bulk with few bits. Measured: max/rms = 17 gave 2.5e-5 relative error on the apply (bar 1e-5);
 // Gaussian blocks sit at ~4. Above 2^dy_max_range this apply uses the fp32-grade stream.
-void ycheck(sbmds_ctx* h, int b, int bp, cudaStream_t st) {
-    h->ychk.ensure(64 * sizeof(unsigned int) + 64 * sizeof(double));
-    CK(cudaMemsetAsync(h->ychk.p, 0, h->ychk.bytes, st));
-    launch(k_ycheck, dim3((unsigned)std::min<int64_t>(2 * (int64_t)h->num_sms, (h->l * bp + 255) / 256)), dim3(256), 0,
-           st, h->l, b, bp, (const float*)h->Y1.as<float>(), h->ychk.as<unsigned int>());
-    unsigned char buf[64 * 4 + 64 * 8];
-    peek_to_host(buf, h->ychk.p, sizeof buf, st);
-    const unsigned int* mx = reinterpret_cast<const unsigned int*>(buf);
-    const double* ss = reinterpret_cast<const double*>(buf + 256);
+// x_ok (optional): the standalone apply's X statistics (h->xstat, formed by colsum_xstat before
+// its tensor-core A2) ride in the same readback; *x_ok = false when a column of X fails the same
+// bound (dominant row). want_y = false reads only them.
+void ycheck(sbmds_ctx* h, int b, int bp, cudaStream_t st, bool want_y = true, bool* x_ok = nullptr) {
+    constexpr size_t kStat = 64 * sizeof(unsigned int) + 64 * sizeof(double);
+    h->ychk.ensure(2 * kStat);   // [0, kStat): Y1's statistics; [kStat, 2 kStat): a copy of X's
+    unsigned char buf[2 * kStat];
+    if (want_y) {
+        CK(cudaMemsetAsync(h->ychk.p, 0, kStat, st));
+        launch(k_ycheck, dim3((unsigned)std::min<int64_t>(2 * (int64_t)h->num_sms, (h->l * bp + 255) / 256)), dim3(256), 0,
+               st, h->l, b, bp, (const float*)h->Y1.as<float>(), h->ychk.as<unsigned int>());
+    }
+    if (x_ok) CK(cudaMemcpyAsync(h->ychk.as<unsigned char>() + kStat, h->xstat.p, kStat, cudaMemcpyDeviceToDevice, st));
+    peek_to_host(buf, h->ychk.p, x_ok ? 2 * kStat : kStat, st);
     const double lim = std::ldexp(1.0, h->dy_max_range);
-    for (int c = 0; c < b; ++c) {
-        float m;
-        memcpy(&m, &mx[c], 4);
-        const double rms = std::sqrt(ss[c] / (double)h->l);
-        if (m > 0.f && (double)m > lim * rms) {
-            h->y_fallback = true;
-            ++h->y_fallbacks;
-            return;
+    auto bad = [&](const unsigned char* q, double count) {
+        const unsigned int* mx = reinterpret_cast<const unsigned int*>(q);
+        const double* ss = reinterpret_cast<const double*>(q + 256);
+        for (int c = 0; c < b; ++c) {
+            float m;
+            memcpy(&m, &mx[c], 4);
+            const double rms = std::sqrt(ss[c] / count);
+            if (!(m < 3.0e38f) || (m > 0.f && (double)m > lim * rms)) return true;
         }
+        return false;
+    };
+    if (x_ok) *x_ok = !bad(buf + kStat, (double)h->n);
+    if (want_y && bad(buf, (double)h->l)) {
+        h->y_fallback = true;
+        ++h->y_fallbacks;
     }
 }
 
@@ -1481,32 +1492,17 @@ void colsum(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
                h->counters.as<unsigned int>() + CNT_COLSUM);
 }
 
-// A1 with the per-column max |x| and sum of squares of X (b = 16, X 16-byte aligned), then the
-// check of the standalone apply's tensor-core A2 (one small readback, as ycheck): X's 24-bit
-// digits take one scale per column, so a column whose max is > 2^dy_max_range times its rms (a
-// dominant row) keeps the fp32 CSC SpMM instead (stat x_fallbacks). Returns whether the
-// tensor-core path may be taken; h->xstat[0, 16) then holds the bits of max |X_c|.
-bool colsum_xcheck(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
+// A1 with the per-column max |x| and sum of squares of X (b = 16 / 32, X 16-byte aligned) into
+// h->xstat: the scales of the standalone apply's tensor-core A2 (X's 24-bit digits take one scale
+// per column) and its check, read back together with Y1's after A2 (ycheck): a column whose max
+// is > 2^dy_max_range times its rms (a dominant row) redoes A2 on the fp32 CSC SpMM (stat
+// x_fallbacks).
+void colsum_xstat(sbmds_ctx* h, int b, const float* X, cudaStream_t st) {
     h->xstat.ensure(64 * sizeof(unsigned int) + 64 * sizeof(double));
     CK(cudaMemsetAsync(h->xstat.p, 0, h->xstat.bytes, st));
     const unsigned grid = (unsigned)std::min<int64_t>(4 * kRedBlocks, (h->n + 255) / 256);
     launch(k_colsum4<true>, dim3(grid), dim3(256), 0, st, h->n, b, X, h->colpart.as<double>(), h->s.as<double>(),
            h->counters.as<unsigned int>() + CNT_COLSUM, h->xstat.as<unsigned int>());
-    unsigned char buf[64 * 4 + 64 * 8];
-    peek_to_host(buf, h->xstat.p, sizeof buf, st);
-    const unsigned int* mx = reinterpret_cast<const unsigned int*>(buf);
-    const double* ss = reinterpret_cast<const double*>(buf + 256);
-    const double lim = std::ldexp(1.0, h->dy_max_range);
-    for (int c = 0; c < b; ++c) {
-        float m;
-        memcpy(&m, &mx[c], 4);
-        const double rms = std::sqrt(ss[c] / (double)h->n);
-        if (!(m < 3.0e38f) || (m > 0.f && (double)m > lim * rms)) {
-            ++h->x_fallbacks;
-            return false;
-        }
-    }
-    return true;
 }
 
 // The standalone apply's A2 on the tensor cores: the T products of the sparse step on X's rows
@@ -1671,8 +1667,12 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     bool sp8_a2 = false;
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
     if (!s_ready) profiled(h->prof, PK_COLSUM, st, [&] {
-        if (sp8_a && h->dy_max_range < 64) sp8_a2 = colsum_xcheck(h, b, X, st);
-        else colsum(h, b, X, st);
+        if (sp8_a && h->dy_max_range < 64) {
+            colsum_xstat(h, b, X, st);
+            sp8_a2 = true;   // (optimistic: X's check is read with Y1's, after A2)
+        } else {
+            colsum(h, b, X, st);
+        }
     });
     // blocked mask: the option, or (auto, standalone apply) S^T X blocked and S Y2 plain for
     // b >= 32: measured on config 3 (b = 32) 0.63 ms vs 0.83 ms with the b = 16 default
@@ -1777,8 +1777,22 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
     }
     // standalone apply on the int8 stream (auto): check Y1's columns first (one small readback)
-    if (flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 && takes_sym(h, bp, Rinv != nullptr))
-        ycheck(h, b, bp, st);
+    const bool want_y = flags == 0 && (!Rinv || h->raw_now) && h->dstream == 0 && h->dy_max_range < 64 &&
+                        takes_sym(h, bp, Rinv != nullptr);
+    if (want_y || sp8_a2) {
+        bool x_ok = true;
+        ycheck(h, b, bp, st, want_y, sp8_a2 ? &x_ok : nullptr);   // one readback for both
+        if (!x_ok) {   // a dominant row in X: A2 again on the fp32 CSC kernel, and Y1's check on that Y1
+            ++h->x_fallbacks;
+            --h->sp8_apply_t_launches;
+            if (h->y_fallback) {
+                h->y_fallback = false;
+                --h->y_fallbacks;
+            }
+            profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, X, st); });
+            if (want_y) ycheck(h, b, bp, st);
+        }
+    }
     // A3, A4: Y2 = D Y1, t = w^T Y2   (eigs: Y1 <- Y1 R^-1 first, the R^-1 fold)
     // standalone apply at b = 16: A5 through the N products of the tensor-core sparse step
     const bool sp8_a5 = sp8_a;

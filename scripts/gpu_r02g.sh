@@ -1,16 +1,7 @@
-# Round 2 measurement: full GPU suite, the default bench line, per-config lines (configs 3, 4
-# apply, config 5 sweep), the round-2 additions' times.
+# one readback for the X and Y1 checks: apply tests, apply lines at configs 3 and 4
 export SBMDS_GEN_CACHE=/root/.cache/sbmds_gen
-mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
-(time timeout 2400 python -m pytest tests/ -q -m gpu) > gpurun_out/r02g_tests.log 2>&1; tail -5 gpurun_out/r02g_tests.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench_r02g.json 2> gpurun_out/bench_r02g.err; echo bench rc=$?
-cat gpurun_out/bench_r02g.json | head -c 600; echo
-timeout 600 python bench.py --mode apply --config 4 --no-cpu-baseline > gpurun_out/bench_r02g_apply4.json 2>&1; echo rc=$?
-timeout 900 python bench.py --config 3 --iters 50 --no-e2e --no-cpu-baseline > gpurun_out/bench_r02g_cfg3.json 2>&1; echo rc=$?
-timeout 600 python bench.py --mode apply --config 3 --b 32 --no-cpu-baseline > gpurun_out/bench_r02g_apply3.json 2>&1; echo rc=$?
-for k in 8 16 64; do for b in 1 4 16 64; do
-  timeout 600 python bench.py --mode apply --config 5 --k5 $k --b $b > gpurun_out/bench_r02g_cfg5_k${k}_b${b}.json 2>&1; echo cfg5 k=$k b=$b rc=$?
-done; done
-timeout 900 python scripts/time_next.py > gpurun_out/r02g_next.json 2>&1; echo next rc=$?
+mkdir -p gpurun_out/r02g2
+O=gpurun_out/r02g2
+(timeout 1500 python -m pytest tests/test_gpu_apply.py tests/test_gpu_precision.py tests/test_gpu_shard.py -q -m gpu -x) > $O/tests.log 2>&1; tail -5 $O/tests.log
+for i in 1 2; do timeout 600 python bench.py --mode apply --config 3 --b 32 --no-cpu-baseline > $O/apply3_$i.json 2> $O/apply3.err; echo rc=$?; head -c 330 $O/apply3_$i.json | tail -c 120; echo; done
+timeout 600 python bench.py --mode apply --config 4 --no-cpu-baseline > $O/apply4.json 2> $O/apply4.err; echo rc=$?; head -c 330 $O/apply4.json | tail -c 120; echo
