@@ -284,6 +284,11 @@ int64_t sbmds_launch_count(void);
    returns the number of violated invariants (0 = consistent; < 0 = bad arguments). Used by the
    CPU tests; see k_dstream_sym8.cuh / k_dstream_pair.cuh and DESIGN.md §4. */
 int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous);
+/* The same for blocks of SR x SC tiles (k_dstream_sym8 walks SR = 9, SC = 1 at b = 16: a column
+   accumulator becomes a partial once per SR tiles, so tall one-tile-wide blocks write the fewest
+   partials) and for the tile range of `rank` in `world` (sharded apply). */
+int64_t sbmds_plan_selfcheck_rect(int64_t l, int32_t SR, int32_t SC, int32_t gN, int32_t max_ctas, int32_t contiguous,
+                                  int32_t rank, int32_t world);
 
 /*
  * Sharded apply. The matvec of PAPER.md:221-222 splits by rows of P (= S)

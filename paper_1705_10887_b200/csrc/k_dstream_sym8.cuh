@@ -50,11 +50,18 @@ struct Sym8Cfg {
     static constexpr int NB = 3 * BP;                      // B rows [y0; y1; y2]
     static constexpr int N3 = BP < 16 ? 16 : BP;           // N of the d2 product (>= 16 for M = 128)
     static constexpr int ACCW = BP < 16 ? 32 : 3 * BP;     // TMEM columns per accumulator: c0 | c1 | c2
-    static constexpr int S = (256 / ACCW) > 16 ? 16 : (256 / ACCW);   // accumulators per role
-    static constexpr int T0 = S * ACCW;                     // first column of the T accumulators
-    // a row accumulator spans at most GN blocks (GN * S <= 256 tiles = 32,768 k): the int32 sums
+    // Blocks of SR x SC tiles: SR row ("N") accumulators and SC column ("T") accumulators in the 512
+    // TMEM columns. A T accumulator becomes a partial at every block change (1 / SR partials per
+    // tile), an N accumulator after GN blocks of its block row, so the blocks are as tall as TMEM
+    // allows and one tile wide: 9 x 1 at b = 16 writes 0.115 partials per tile where 5 x 5 wrote 0.204
+    // (132 -> 74 MB per launch at config 4).
+    static constexpr int NACC = 512 / ACCW > 17 ? 17 : 512 / ACCW;
+    static constexpr int SC = 1;
+    static constexpr int SR = NACC - SC;
+    static constexpr int T0 = SR * ACCW;                    // first column of the T accumulators
+    // a row accumulator spans at most GN blocks (GN * SC <= 256 tiles = 32,768 k): the int32 sums
     // of up to 3 digit products (|.| <= 16,129) stay below 2^31
-    static constexpr int GN = 256 / S;
+    static constexpr int GN = 256 / SC;
     static constexpr int PLANE = TT * 128;                  // 16 KB: 128 rows x 128 int8
     static constexpr int A_BYTES = 3 * PLANE;               // 48 KB packed tile
     static constexpr int BOX_B = NB * 128;                  // 128 k of [y0; y1; y2]
@@ -63,7 +70,7 @@ struct Sym8Cfg {
     static constexpr int THREADS = 6 * 32;
     static constexpr int SMEM = NS * STAGE + 1024 + 1024;
     static_assert(STAGE % 1024 == 0 && BOX_B % 1024 == 0, "stage alignment");
-    static_assert(S >= 1 && 2 * S * ACCW <= 512, "tmem");
+    static_assert(SR >= 1 && SR <= 16 && (SR + SC) * ACCW <= 512, "tmem");
 };
 
 struct Sym8Event {
@@ -112,16 +119,16 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
                    const int* __restrict__ sbase, const int* __restrict__ smap, int NT, float* __restrict__ P,
                    int dbg_mode) {
     using C = Sym8Cfg<BP>;
-    constexpr int S = C::S;
+    constexpr int SR = C::SR, SC = C::SC;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + C::NS * C::STAGE);
     uint64_t* empty = full + C::NS;
     uint64_t* ev_full = empty + C::NS;        // [2] accumulators final + event written
     uint64_t* ev_empty = ev_full + 2;         // [2] event consumed
-    uint64_t* emptyN = ev_empty + 2;          // [S] N accumulator drained
-    uint64_t* emptyT = emptyN + S;            // [S] T accumulator drained
-    Sym8Event* evq = reinterpret_cast<Sym8Event*>(emptyT + S);   // [2]
+    uint64_t* emptyN = ev_empty + 2;          // [SR] N accumulator drained
+    uint64_t* emptyT = emptyN + SR;           // [SC] T accumulator drained
+    Sym8Event* evq = reinterpret_cast<Sym8Event*>(emptyT + SC + ((SR + SC) & 1));   // [2] (16-byte aligned)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(evq + 2);
 
     pdl_trigger();
@@ -137,10 +144,8 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
             mbar_init(&ev_full[s], 2);   // tcgen05.commit + the MMA warp's event arrive
             mbar_init(&ev_empty[s], 128);
         }
-        for (int a = 0; a < S; ++a) {
-            mbar_init(&emptyN[a], 128);
-            mbar_init(&emptyT[a], 128);
-        }
+        for (int a = 0; a < SR; ++a) mbar_init(&emptyN[a], 128);
+        for (int a = 0; a < SC; ++a) mbar_init(&emptyT[a], 128);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -191,18 +196,18 @@ __global__ void __launch_bounds__(Sym8Cfg<BP>::THREADS, 1)
         for (int64_t t = t0; t < t1; ++t) {
             int I, J;
             tile_of(t, I, J);
-            const int bi = I / S, bj = J / S;
+            const int bi = I / SR, bj = J / SC;
             // segment ends: T (column accumulators) at every block change, N (row accumulators)
             // when the block row or the group of GN block columns changes
             bool end_seg = (t + 1 == t1), end_n = end_seg;
             if (!end_seg) {
                 int I2, J2;
                 tile_of(t + 1, I2, J2);
-                end_seg = (I2 / S != bi) || (J2 / S != bj);
-                end_n = (I2 / S != bi) || ((J2 / S) / C::GN != bj / C::GN);
+                end_seg = (I2 / SR != bi) || (J2 / SC != bj);
+                end_n = (I2 / SR != bi) || ((J2 / SC) / C::GN != bj / C::GN);
             }
             const bool diag = (I == J);
-            const int aN = I - bi * S, aT = J - bj * S;
+            const int aN = I - bi * SR, aT = J - bj * SC;
             const uint32_t bN = 1u << aN, bT = 1u << aT;
             const bool firstN = !(maskN & bN), firstT = !diag && !(maskT & bT);
             // an accumulator's first tile in a segment waits until its previous segment's drain

@@ -744,7 +744,7 @@ void run_dstream_tc(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) {
 // contiguous: physical slot = rank of (X, logical slot), so each row tile's partials are
 // contiguous for k_dreduce_pair; the kernel maps logical -> physical through pl.smap.
 struct PlanHost {
-    int S = 0, NT = 0, P = 0;
+    int S = 0, SC = 0, NT = 0, P = 0;   // blocks of S x SC tiles
     int64_t T = 0;
     std::vector<uint32_t> tiles;
     std::vector<int64_t> pbeg;
@@ -753,18 +753,20 @@ struct PlanHost {
 
 // The upper tiles in walk order (blocks of S x S tiles, block rows, row-major inside a block);
 // a shard (rank of world) keeps the contiguous range [T r / W, T (r + 1) / W).
-PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous, int rank = 0, int world = 1) {
+// (SC = 0: square blocks of S x S tiles; else S rows x SC columns, the int8 stream's 9 x 1)
+PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous, int rank = 0, int world = 1, int SC = 0) {
     PlanHost ph;
+    if (SC <= 0) SC = S;
     const int NT = (int)((l + 127) / 128);
     if (NT > 65535) throw std::runtime_error("l too large for the symmetric-half stream");
-    const int NBk = (NT + S - 1) / S;
+    const int NBr = (NT + S - 1) / S, NBc = (NT + SC - 1) / SC;
     auto& tiles = ph.tiles;
     tiles.reserve((size_t)NT * (NT + 1) / 2);
-    for (int bi = 0; bi < NBk; ++bi)
-        for (int bj = bi; bj < NBk; ++bj)
+    for (int bi = 0; bi < NBr; ++bi)
+        for (int bj = (bi * S) / SC; bj < NBc; ++bj)   // block columns that reach the diagonal or lie right of it
             for (int r = 0; r < S; ++r)
-                for (int c = 0; c < S; ++c) {
-                    const int I = bi * S + r, J = bj * S + c;
+                for (int c = 0; c < SC; ++c) {
+                    const int I = bi * S + r, J = bj * SC + c;
                     if (I < NT && J < NT && J >= I) tiles.push_back(((uint32_t)I << 16) | (uint32_t)J);
                 }
     if (world > 1) {
@@ -787,20 +789,20 @@ PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous, int
             uint32_t mask = 0;
             int cbi = -1, cbj = -1, ckey = -1;
             auto emit = [&]() {
-                for (int a = 0; a < S; ++a)
-                    if (mask & (1u << a)) slot_x.push_back(role ? cbj * S + a : cbi * S + a);
+                for (int a = 0; a < (role ? SC : S); ++a)
+                    if (mask & (1u << a)) slot_x.push_back(role ? cbj * SC + a : cbi * S + a);
                 mask = 0;
             };
             for (int64_t t = pbeg[p]; t < pbeg[p + 1]; ++t) {
                 const int I = (int)(tiles[t] >> 16), J = (int)(tiles[t] & 0xFFFFu);
-                const int bi = I / S, bj = J / S;
+                const int bi = I / S, bj = J / SC;
                 const int key = role ? bj : bj / gN;
                 if ((bi != cbi || key != ckey) && mask) emit();
                 cbi = bi;
                 cbj = bj;
                 ckey = key;
                 if (role == 1 && I == J) continue;
-                mask |= 1u << (role ? J - bj * S : I - bi * S);
+                mask |= 1u << (role ? J - bj * SC : I - bi * S);
             }
             emit();
         }
@@ -821,6 +823,7 @@ PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous, int
         for (int pq = 0; pq < nslots; ++pq) xslot[pq] = pq;
     }
     ph.S = S;
+    ph.SC = SC;
     ph.NT = NT;
     ph.P = P;
     ph.T = T;
@@ -828,8 +831,8 @@ PlanHost plan_host(int64_t l, int max_pairs, int S, int gN, bool contiguous, int
 }
 
 void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S, int gN = 1, bool contiguous = false,
-                     const PlanHost* pre = nullptr) {
-    const PlanHost ph = pre ? *pre : plan_host(h->l, max_pairs, S, gN, contiguous, h->rank, h->world);
+                     const PlanHost* pre = nullptr, int SC = 0) {
+    const PlanHost ph = pre ? *pre : plan_host(h->l, max_pairs, S, gN, contiguous, h->rank, h->world, SC);
     const int nslots = (int)ph.slot_x.size();
     if (contiguous) {
         pl.smap.ensure(ph.smap.size() * sizeof(int));
@@ -862,12 +865,15 @@ void build_pair_plan(sbmds_ctx* h, sbmds_ctx::PairPlan& pl, int max_pairs, int S
 // every (tile, T), I < J, in exactly one slot of row tile J; slot -> row tile as recorded; the
 // reduction lists (or the contiguous slot map) consistent.
 namespace {
-int64_t plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous, int rank, int world) {
-    if (l < 1 || S < 1 || S > 16 || gN < 1 || max_ctas < 1 || world < 1 || rank < 0 || rank >= world) return -1;
+int64_t plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous, int rank, int world,
+                       int32_t SC = 0) {
+    if (l < 1 || S < 1 || S > 16 || SC < 0 || SC > 16 || gN < 1 || max_ctas < 1 || world < 1 || rank < 0 || rank >= world)
+        return -1;
+    if (SC == 0) SC = S;
     int64_t err = 0;
     PlanHost ph;
     try {
-        ph = plan_host(l, max_ctas, S, gN, contiguous != 0, rank, world);
+        ph = plan_host(l, max_ctas, S, gN, contiguous != 0, rank, world, SC);
     } catch (...) {
         return -2;
     }
@@ -887,13 +893,13 @@ int64_t plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32
     std::vector<int> used_n(T, 0), used_t(T, 0);
     std::vector<int> slot_seen(nslots, 0);
     for (int p = 0; p < ph.P; ++p) {
-        std::vector<std::vector<int64_t>> accN(S), accT(S);
+        std::vector<std::vector<int64_t>> accN(S), accT(SC);
         uint32_t maskN = 0, maskT = 0;
         int slotN = ph.sbase[2 * p], slotT = ph.sbase[2 * p + 1];
         auto flush = [&](uint32_t mask, std::vector<std::vector<int64_t>>& acc, int& slot, int role, int bi, int bj) {
-            for (int a = 0; a < S; ++a) {
+            for (int a = 0; a < (role ? SC : S); ++a) {
                 if (!(mask & (1u << a))) continue;
-                const int X = role ? bj * S + a : bi * S + a;
+                const int X = role ? bj * SC + a : bi * S + a;
                 if (slot < 0 || slot >= nslots || ph.slot_x[slot] != X) ++err;
                 if (slot >= 0 && slot < nslots) ++slot_seen[slot];
                 for (const int64_t t : acc[a]) {
@@ -907,14 +913,14 @@ int64_t plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32
         };
         for (int64_t t = ph.pbeg[p]; t < ph.pbeg[p + 1]; ++t) {
             const int I = (int)(ph.tiles[t] >> 16), J = (int)(ph.tiles[t] & 0xFFFFu);
-            const int bi = I / S, bj = J / S;
+            const int bi = I / S, bj = J / SC;
             bool end_seg = (t + 1 == ph.pbeg[p + 1]), end_n = end_seg;
             if (!end_seg) {
                 const int I2 = (int)(ph.tiles[t + 1] >> 16), J2 = (int)(ph.tiles[t + 1] & 0xFFFFu);
-                end_seg = (I2 / S != bi) || (J2 / S != bj);
-                end_n = (I2 / S != bi) || ((J2 / S) / gN != bj / gN);
+                end_seg = (I2 / S != bi) || (J2 / SC != bj);
+                end_n = (I2 / S != bi) || ((J2 / SC) / gN != bj / gN);
             }
-            const int aN = I - bi * S, aT = J - bj * S;
+            const int aN = I - bi * S, aT = J - bj * SC;
             accN[aN].push_back(t);
             maskN |= 1u << aN;
             if (I != J) {
@@ -961,6 +967,12 @@ int64_t plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32
 
 extern "C" int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous) {
     return plan_selfcheck(l, S, gN, max_ctas, contiguous, 0, 1);
+}
+
+extern "C" int64_t sbmds_plan_selfcheck_rect(int64_t l, int32_t SR, int32_t SC, int32_t gN, int32_t max_ctas,
+                                             int32_t contiguous, int32_t rank, int32_t world) {
+    if (SC < 1) return -1;
+    return plan_selfcheck(l, SR, gN, max_ctas, contiguous, rank, world, SC);
 }
 
 extern "C" int64_t sbmds_shard_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas, int32_t contiguous,
@@ -1097,7 +1109,7 @@ void run_dstream_sym8(sbmds_ctx* h, int b, cudaStream_t st, const double* Rinv) 
         fprintf(stderr, "[sbmds_dstream]  %8.2f ms  %s\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
     };
-    if (!pl.ok) { build_pair_plan(h, pl, h->num_sms, C::S, C::GN, true); dphase("pair plan"); }   // one CTA per SM, both roles
+    if (!pl.ok) { build_pair_plan(h, pl, h->num_sms, C::SR, C::GN, true, nullptr, C::SC); dphase("pair plan"); }   // one CTA per SM, both roles
     h->y16aux.ensure(352 * sizeof(unsigned int));   // + [192, 320): Y2 column max / min keys, [320, 336) exponents
     unsigned int* aux = h->y16aux.as<unsigned int>();
     unsigned int* dmax8 = aux + 2;
@@ -2475,7 +2487,7 @@ sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, in
         // the int8 D stream's schedule (host work) while D is still crossing the link
         PlanHost ph16;
         const bool pre_plan = h->dmax8_ok && !h->s8plan[1].ok;
-        if (pre_plan) ph16 = plan_host(l, h->num_sms, Sym8Cfg<16>::S, Sym8Cfg<16>::GN, true, h->rank, h->world);
+        if (pre_plan) ph16 = plan_host(l, h->num_sms, Sym8Cfg<16>::SR, Sym8Cfg<16>::GN, true, h->rank, h->world, Sym8Cfg<16>::SC);
         // ---- D_ll: borrow (device, l % 4 == 0), copy a device D into a 16-byte-pitched buffer, or
         // join the host upload started above
         if (!d_dev) {
@@ -2527,7 +2539,7 @@ sbmds_status create_impl(int64_t n, int64_t n_global, int64_t row0, int rank, in
             // D-stream launch waits for it
             using C8 = Sym8Cfg<16>;
             auto& pl = h->s8plan[1];
-            build_pair_plan(h, pl, h->num_sms, C8::S, C8::GN, true, &ph16);
+            build_pair_plan(h, pl, h->num_sms, C8::SR, C8::GN, true, &ph16, C8::SC);
             h->Dt8.ensure((size_t)((int64_t)pl.NT * (pl.NT + 1) / 2) * C8::A_BYTES);
             unsigned int* aux = h->y16aux.as<unsigned int>();
             CK(cudaStreamCreateWithFlags(&h->pack_st, cudaStreamNonBlocking));
