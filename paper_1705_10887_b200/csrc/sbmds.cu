@@ -1563,6 +1563,10 @@ void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, 
 int64_t sp8_rs_pad(const sbmds_ctx* h) { return ((h->n + 3) & ~(int64_t)3) + kSp8RB; }
 
 bool sp8_ok(sbmds_ctx* h, int b, cudaStream_t st) {
+    if (h->sp8_state == 0) {   // (the build reads sizes back: never inside a stream capture)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    }
     return h->fuse == 3 && b == 16 && h->blocked && (h->use_blocked & 1) && ensure_sp8(h, st);
 }
 

@@ -543,3 +543,28 @@ def test_tensor_core_sparse_kernels_split_blocks():
     lam_o, V_o, Z_o, _ = O.eigs_matfree(S, p.D, 3)
     assert np.all(np.abs(np.asarray(lam) - lam_o) <= 1e-4 * np.abs(lam_o))
     assert O.principal_angle(V.cpu().numpy().astype(np.float64), V_o) <= 1e-3
+
+
+def test_apply_graph_capture_without_checks():
+    """With dy_max_range >= 64 the standalone apply reads nothing back (include/sbmds.h): after a
+    warm-up call it can be captured into a CUDA graph and replayed -- A2 then stays on the CSC
+    kernel, A5 on the tensor-core N products -- with the eager call's result bit for bit."""
+    torch = _torch()
+    p = configs.config(2)
+    X = torch.from_numpy(configs.x_block(p.n, 16, seed=4)).cuda()
+    Y = torch.empty_like(X)
+    Yg = torch.empty_like(X)
+    with make_handle(p) as h:
+        h.set_option("dy_max_range", 64)
+        h.apply(X, out=Y)
+        torch.cuda.synchronize()
+        n5 = h.stat("sp8_apply_launches")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            h.apply(X, out=Yg)
+        Yg.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert h.stat("sp8_apply_launches") == n5 + 1 and h.stat("sp8_apply_t_launches") == 0
+    assert torch.equal(Y, Yg)
+    assert relerr(Y.cpu().numpy(), oracle_apply(p, X.cpu().numpy())) <= TOL
