@@ -148,6 +148,10 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void gtc_cp16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+
 template <int NCB, bool WITH_H>
 __global__ void __launch_bounds__(256) k_gram_tc(int64_t n, int b, const float* __restrict__ Y,
                                                  const float* __restrict__ X, double* __restrict__ part,
@@ -172,19 +176,8 @@ __global__ void __launch_bounds__(256) k_gram_tc(int64_t n, int b, const float* 
     const int64_t rows_per_warp = ((n + nw - 1) / nw + 15) & ~int64_t(15);
     const int64_t beg = wid * rows_per_warp, end = min(n, beg + rows_per_warp);
     constexpr int U = 4;   // 4-row groups whose loads are issued together (memory-level parallelism)
-    for (int64_t r0 = beg; r0 < end; r0 += 4 * U) {
-        float yf[U][NCB], xf[U][NCB];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t r = r0 + 4 * u + kr;
-            const bool ok = r < end;
-#pragma unroll
-            for (int c = 0; c < NCB; ++c) {
-                const int col = 8 * c + cc;
-                yf[u][c] = (ok && col < b) ? __ldg(Y + r * b + col) : 0.f;
-                if constexpr (WITH_H) xf[u][c] = (ok && col < b) ? __ldg(X + r * b + col) : 0.f;
-            }
-        }
+    // one 16-row chunk of fragments: y / x values of 4-row group u for this lane
+    auto consume = [&](const float (&yf)[U][NCB], const float (&xf)[U][NCB]) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             double y[NCB], x[NCB];
@@ -206,6 +199,69 @@ __global__ void __launch_bounds__(256) k_gram_tc(int64_t n, int b, const float* 
                     for (int c2 = 0; c2 < NCB; ++c2) dmma_8x8x4(h[c * NCB + c2], x[c], y[c2]);
             }
         }
+    };
+    const bool vec = (b % 4 == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0) &&
+                     (!WITH_H || (reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    if (vec) {
+        // Rows staged through shared memory: a warp copies its next 16 rows (16 b floats, contiguous in
+        // Y) with 16-byte cp.async while it works on the current ones (two stages; row pitch b + 8
+        // floats: the fragment reads of a 4-row group then hit 32 distinct banks), instead of 4-byte
+        // gathers in the fragment layout (0.9 TB/s at b = 32).
+        const int pitch = b + 8, cpr = b / 4;   // floats per staged row, 16-byte chunks per row
+        float* stg = reinterpret_cast<float*>(gtc_smem) + (size_t)warp * (WITH_H ? 4 : 2) * 16 * pitch;
+        auto stage = [&](int64_t r0, int sidx) {
+            const int nrow = (int)min((int64_t)16, end - r0);
+            for (int q = lane; q < nrow * cpr; q += 32) {
+                const int rr = q / cpr, ch = q % cpr;
+                gtc_cp16(stg + (sidx * 16 + rr) * pitch + 4 * ch, Y + (r0 + rr) * b + 4 * ch);
+                if constexpr (WITH_H) gtc_cp16(stg + ((2 + sidx) * 16 + rr) * pitch + 4 * ch, X + (r0 + rr) * b + 4 * ch);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (beg < end) stage(beg, 0);
+        int sidx = 0;
+        for (int64_t r0 = beg; r0 < end; r0 += 16, sidx ^= 1) {
+            if (r0 + 16 < end) {
+                stage(r0 + 16, sidx ^ 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncwarp();
+            float yf[U][NCB], xf[U][NCB];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool ok = r0 + 4 * u + kr < end;
+#pragma unroll
+                for (int c = 0; c < NCB; ++c) {
+                    const int col = 8 * c + cc;
+                    const int o = (sidx * 16 + 4 * u + kr) * pitch + col;
+                    yf[u][c] = (ok && col < b) ? stg[o] : 0.f;
+                    if constexpr (WITH_H) xf[u][c] = (ok && col < b) ? stg[o + 2 * 16 * pitch] : 0.f;
+                    else xf[u][c] = 0.f;
+                }
+            }
+            consume(yf, xf);
+            __syncwarp();   // every lane has read stage sidx before it is refilled two chunks on
+        }
+        __syncthreads();   // the staging area is reused for the fragment reduction below
+    } else {
+    for (int64_t r0 = beg; r0 < end; r0 += 4 * U) {
+        float yf[U][NCB], xf[U][NCB];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = r0 + 4 * u + kr;
+            const bool ok = r < end;
+#pragma unroll
+            for (int c = 0; c < NCB; ++c) {
+                const int col = 8 * c + cc;
+                yf[u][c] = (ok && col < b) ? __ldg(Y + r * b + col) : 0.f;
+                if constexpr (WITH_H) xf[u][c] = (ok && col < b) ? __ldg(X + r * b + col) : 0.f;
+                else xf[u][c] = 0.f;
+            }
+        }
+        consume(yf, xf);
+    }
     }
     // column sums: lanes with the same cc hold the same columns
 #pragma unroll
@@ -280,8 +336,14 @@ __global__ void __launch_bounds__(256) k_gram_tc(int64_t n, int b, const float* 
     }
 }
 
+// the per-warp fragment reduction, or the row staging (8 warps x 2 stages x 16 rows x (8 NCB + 8) floats,
+// twice with H), whichever is larger
 template <int NCB>
-constexpr size_t gram_tc_smem() { return (size_t)8 * (NCB * 8) * (NCB * 8 + 1 + 1) * sizeof(double); }
+constexpr size_t gram_tc_smem(bool with_h = true) {
+    const size_t red = (size_t)8 * (NCB * 8) * (NCB * 8 + 1 + 1) * sizeof(double);
+    const size_t stg = (size_t)8 * (with_h ? 4 : 2) * 16 * (NCB * 8 + 8) * sizeof(float);
+    return red > stg ? red : stg;
+}
 
 // dynamic smem: max(2 tiles of TR x b4, 2*groups*b4^2 + groups*b4) doubles
 inline size_t gram_smem_bytes(int b) {

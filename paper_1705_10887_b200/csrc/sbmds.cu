@@ -2848,6 +2848,8 @@ void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, 
     unsigned int* cnt = h->counters.as<unsigned int>() + CNT_GRAM;
     smem_attr(k_gram_tc<4, true>, (int)gram_tc_smem<4>());
     smem_attr(k_gram_tc<4, false>, (int)gram_tc_smem<4>());
+    smem_attr(k_gram_tc<2, true>, (int)gram_tc_smem<2>());   // (48 KB of row staging + the kernel's static 1 KB)
+    smem_attr(k_gram_tc<2, false>, (int)gram_tc_smem<2>());
     const size_t smem_tc = b <= 8 ? gram_tc_smem<1>() : (b <= 16 ? gram_tc_smem<2>() : gram_tc_smem<4>());
     auto tc = [&](auto kern) {
         launch(kern, dim3(kRedBlocks), dim3(256), smem_tc, st, h->n, b, Y, X, P, Gd, Hd, cs, cnt);
