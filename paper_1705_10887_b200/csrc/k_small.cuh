@@ -868,17 +868,37 @@ __device__ __forceinline__ void philox4x32_10(uint32_t ctr[4], uint32_t k0, uint
     }
 }
 
-// (e0: the counter of the first element -- a shard's rows continue the global sequence)
+// Element ge of the global n x b block is output (ge & 3) of the Philox call with counter ge >> 2:
+// the four 32-bit words of a call give two Box-Muller pairs (r cos, r sin), in fp32 (the initial
+// block only has to be generic). A thread forms one call's four normals and stores those inside
+// [e0, e0 + total) (e0: the global index of X's first element -- a shard's rows continue the
+// global sequence, so the sharded and the unsharded solve start from the same block).
 __global__ void k_init_philox(int64_t n, int b, uint64_t seed, float* __restrict__ X, int64_t e0) {
     const int64_t total = n * b;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t ge = e0 + e;
-        uint32_t ctr[4] = {(uint32_t)ge, (uint32_t)(ge >> 32), 0x5eed5eedu, 0u};
+    const int64_t q0 = e0 >> 2, q1 = (e0 + total + 3) >> 2;
+    const bool vec = (e0 & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+    for (int64_t q = q0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < q1; q += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t ctr[4] = {(uint32_t)q, (uint32_t)(q >> 32), 0x5eed5eedu, 0u};
         philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
-        const double u1 = ((double)ctr[0] + 1.0) * (1.0 / 4294967296.0);  // (0, 1]
-        const double u2 = (double)ctr[1] * (1.0 / 4294967296.0);
-        X[e] = (float)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+        float z[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float u1 = (float)((ctr[2 * h] >> 8) + 1u) * (1.0f / 16777216.0f);   // (0, 1], exact
+            const float u2 = (float)(ctr[2 * h + 1] >> 8) * (1.0f / 16777216.0f);        // [0, 1)
+            const float r = sqrtf(-2.0f * logf(u1));
+            float sn, cs;
+            sincospif(2.0f * u2, &sn, &cs);
+            z[2 * h] = r * cs;
+            z[2 * h + 1] = r * sn;
+        }
+        const int64_t e = 4 * q - e0;   // local index of z[0]
+        if (vec && e + 3 < total) {
+            *reinterpret_cast<float4*>(X + e) = make_float4(z[0], z[1], z[2], z[3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (e + i >= 0 && e + i < total) X[e + i] = z[i];
+        }
     }
 }
 
