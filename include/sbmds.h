@@ -212,8 +212,10 @@ const char* sbmds_last_error(void);
  *     "fuse"           eigs: 0 separate kernels, 1 A5 fused with the Gram, 2 also the next
  *                      apply's S^T partials, 3 (default) the tensor-core sparse step
  *                      (k_sp8.cuh: A5 + Grams + next A2 on the int8 tensor cores from dense
- *                      128-row digit images of S) where it applies -- b = 16 and every
- *                      128-row block touching <= 128 landmarks -- else as 1
+ *                      digit images of blocks of <= 128 consecutive rows of S) where it applies
+ *                      -- b = 16, or b = 32 as two 16-column passes, and every block touching
+ *                      <= 128 landmarks after the build has halved the blocks that do not (stat
+ *                      "sp8_splits") -- else as 1
  *     "sp8_gram8"      (0/1, default 1) eigs on the tensor-core step: steps whose Gram only feeds
  *                      the next Cholesky-QR (neither a Rayleigh-Ritz step nor the one before it)
  *                      take G = Y^T Y and 1^T Y from Y's 24-bit digits on the int8 tensor cores

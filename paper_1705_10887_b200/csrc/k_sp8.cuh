@@ -1,12 +1,14 @@
-// The eigensolver's sparse step on the int8 tensor cores ("tensor-core sparse
-// step"): A5 of this apply, the Gram step, and A2 of the next apply, per 128-row block of S.
+// The sparse products on the int8 tensor cores ("tensor-core sparse step"): inside
+// sbmds_eigs A5 of this apply, the Gram step and A2 of the next apply in one kernel per block of
+// S; in the standalone sbmds_apply A2 and A5 as two passes of the same kernel.
 //
 // Inside sbmds_eigs the block Y = B~X formed by A5 (Y = -1/2 (S Y2 - 1 t^T)
 // "left-multiplying by P", PAPER.md:113 the -1/2) is consumed by the Gram step and by the next
 // apply's A2 (S^T Y, "right-multiplying by P^T"), both linear in Y's rows. S is
-// local: the 128 consecutive vertices of a block touch d_B <= 128 landmarks
-// (config 4: 115 on average), so the block's slice S_B (128 x d_B) is stored as a DENSE image
-// and both products become tensor-core GEMMs with no gathers at all:
+// local: a block of <= 128 consecutive vertices (row range brow0[B] ..
+// brow0[B + 1]; 128 rows unless the build split it) touches d_B <= 128 landmarks (config 4: 115
+// on average), so the block's slice S_B (128 x d_B) is stored as a DENSE image and both
+// products become tensor-core GEMMs with no gathers at all:
 //   N:  Y_B   = S_B   Y2[dict_B]    (M = 128 rows,  K = d_pad, N = 3 b)   A K-major
 //   T:  P1_B  = S_B^T Y_B           (M = 128 dict,  K = 128 rows, N = 3 b) A MN-major
 // One shared-memory image serves both: with the no-swizzle core-matrix layout (core = 8 rows x
@@ -18,19 +20,23 @@
 // balanced signed digits per entry (3 planes, k_sp8_build, once per handle); the B operands are
 // digitised on the fly: Y2 with one scale 2^ey_c per column (from its column maxima), Y_B with
 // one scale per column for the whole launch (from an a-priori bound on |Y|, so the epilogue
-// warps exchange nothing). kind::i8 products and int32 sums are exact; the three accumulator
-// column groups give c0 + c1/256 + c2/65536, undone in fp64 (error <= ~2^-23 of the scaled
-// maxima per product, the same bound as the D stream).
+// warps exchange nothing). kind::i8 products and int32 sums are exact; the accumulator's four
+// column groups give c0 + c1/256 + (c2 + c3/256)/65536, undone in fp32 (error <= ~2^-23 of the
+// scaled maxima per product, the same bound as the D stream).
 //
-// Per block (persistent CTAs, contiguous block ranges):
-//   warp 0      producer: the block's image (one bulk copy, 384 d_pad bytes) into a 3-stage ring;
-//               at Rayleigh-Ritz steps also the block's rows of Y_prev (bulk copy)
-//   warp 1      MMA issue, order N(i), T(i-1)
-//   warps 2-5   epilogue: N accumulator -> Y rows (HBM once, smem for the Gram), Y_B digits
-//               (B operand of T); T accumulator -> P1 partials
-//   warps 6-9   B operand of N (Y2[dict_B] digits), then the FP64-tensor-core Gram of the
-//               previous block (G = Y^T Y, 1^T Y, and H' = Y_prev^T Y at RR steps)
-// Every sum has a fixed order: Y, P1 and the Grams are bitwise reproducible.
+// Roles (persistent CTAs of 17 warps, contiguous block ranges):
+//   warp 0       producer: the block's image (one bulk copy, 384 d_pad bytes) into a 3-stage ring,
+//                the B operand of N (16-byte rows of Y2's digit planes, cp.async) and the block's
+//                row-sum deviations; TONLY: the block's rows of X instead
+//   warp 1       issues the N products (and owns the TMEM allocation); warp 16 the T products
+//                (and, GRAM8, the Gram MMAs Yd^T [Yd | 1] into one accumulator per CTA)
+//   warps 2-9    epilogue A: N accumulator -> Y rows (HBM), Y_B digits -> B operand of T
+//                (+ fp32 rows for the FP64 Gram warps in the variants that use them)
+//   warps 10-13  group B: T accumulator -> P1 partials; at the end (GRAM8) the Gram accumulator
+//   warps 14-15  group C: G = Y^T Y, 1^T Y and (Rayleigh-Ritz steps) H' = Y_prev^T Y on the FP64
+//                tensor cores; idle in the GRAM8 / TONLY variants
+// Every sum has a fixed order (or is an exact integer sum): Y, P1 and the Grams are bitwise
+// reproducible.
 #pragma once
 #include "common.cuh"
 #include "k_dstream_sym8.cuh"
