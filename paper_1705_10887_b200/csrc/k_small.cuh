@@ -316,7 +316,8 @@ __global__ void __launch_bounds__(256) k_gram_tc(int64_t n, int b, const float* 
             pg[kMaxB * kMaxB + pq] = a;
         }
     }
-    if (last_block_done(counter)) {
+    // (counter == NULL: the caller sums the partials with k_gram_sum)
+    if (counter && last_block_done(counter)) {
         if (cs)
             for (int q = threadIdx.x; q < b; q += 256) cs[q] = ordered_sum(part + 2 * kMaxB * kMaxB + q, gridDim.x, kGramPart);
         {   // this thread's entries tid + 256 e (b <= 32: at most 4), their partial loads batched together
@@ -343,6 +344,30 @@ constexpr size_t gram_tc_smem(bool with_h = true) {
     const size_t red = (size_t)8 * (NCB * 8) * (NCB * 8 + 1 + 1) * sizeof(double);
     const size_t stg = (size_t)8 * (with_h ? 4 : 2) * 16 * (NCB * 8 + 8) * sizeof(float);
     return red > stg ? red : stg;
+}
+
+// The block partials of a Gram kernel summed by several blocks instead of the kernel's last block
+// (b = 32: 1056 entries over ~300 partials were ~35 us of a 90 us launch in one block): four
+// consecutive lanes per entry, each summing a quarter of the partials in order, the first adding
+// the four in quarter order -- a fixed order, bitwise reproducible. Entries: G (b x b), H (with_h)
+// and the column sums (cs != NULL), at their offsets in a partial.
+__global__ void __launch_bounds__(256) k_gram_sum(int b, int nparts, const double* __restrict__ part,
+                                                  double* __restrict__ G, double* __restrict__ H,
+                                                  double* __restrict__ cs) {
+    const int nG = b * b, nH = H ? b * b : 0, nC = cs ? b : 0;
+    const int task = blockIdx.x * blockDim.x + threadIdx.x, e = task >> 2, qt = task & 3;
+    const int per = (nparts + 3) / 4, q0 = min(nparts, qt * per), q1 = min(nparts, q0 + per);
+    const bool live = e < nG + nH + nC;
+    int off = 0;
+    double* dst = nullptr;
+    if (e < nG) { off = e; dst = G + e; }
+    else if (e < nG + nH) { off = kMaxB * kMaxB + (e - nG); dst = H + (e - nG); }
+    else if (live) { off = 2 * kMaxB * kMaxB + (e - nG - nH); dst = cs + (e - nG - nH); }
+    double v = 0.0;
+    if (live) v = ordered_sum<16>(part + (int64_t)q0 * kGramPart + off, q1 - q0, kGramPart);
+    const double v1 = __shfl_down_sync(0xffffffffu, v, 1), v2 = __shfl_down_sync(0xffffffffu, v, 2),
+                 v3 = __shfl_down_sync(0xffffffffu, v, 3);
+    if (live && qt == 0) *dst = ((v + v1) + v2) + v3;
 }
 
 // dynamic smem: max(2 tiles of TR x b4, 2*groups*b4^2 + groups*b4) doubles

@@ -1290,4 +1290,182 @@ __global__ void __launch_bounds__(Sp8Cfg<BP, GRAM8>::THREADS, 1)
     }
 }
 
+// ------------------------------------------------------------------ the int8 Gram at width 32
+// G = Y^T Y and 1^T Y of an n x 32 block from Y's 24-bit digits (reading R18: eigs steps at
+// block = 32 that feed no Rayleigh-Ritz step; the two 16-column passes of the sparse step share no
+// Gram). Per 128-row block: the rows (16 KB, contiguous) by cp.async into one of two buffers;
+// thread (row r, half h) digitises its 16 columns on the same per-column scales as the sparse
+// step's Y_B digits into image h (rows of [y0 | y1 | y2 | ones chunk], the B_T layout); one
+// elected thread issues Yd_a^T [Yd_a | 1], Yd_a^T [Yd_b | 1], Yd_b^T [Yd_b | 1] (4 K steps each)
+// into three TMEM accumulators that live for the CTA's whole block list (exact int32 sums:
+// <= 2^14 per product, <= 2^17 rows per CTA). Two image sets: block k + 1 is digitised while
+// block k's MMAs run; two CTAs per SM hide the rest. At the end accumulator lane 16 p + i,
+// column 16 q + j = sum_r d_p[r][i] d_q[r][j] is combined in fp64 into the CTA's partial, and
+// the last CTA sums the partials in CTA order (fixed order: bitwise reproducible).
+struct Gram8Cfg {
+    static constexpr int ROWS = kSp8RB * 32 * 4;          // 16 KB: a block's fp32 rows
+    static constexpr int IMG = 64 * kSp8RB;               // 8 KB: one half's digit image
+    static constexpr int OFF_IMG = 2 * ROWS;              // [set][half]
+    static constexpr int OFF_BAR = OFF_IMG + 4 * IMG;
+    static constexpr int SMEM = OFF_BAR + 64 + 128;
+    static constexpr int THREADS = 256;
+    static constexpr int TCOLS = 256;                     // 3 accumulators of 48 columns
+};
+
+__global__ void __launch_bounds__(Gram8Cfg::THREADS, 2)
+    k_gram8_32(int64_t n, const float* __restrict__ Y, const int* __restrict__ ey2in, const double* __restrict__ t,
+               const float* __restrict__ norms, double* __restrict__ part, double* __restrict__ G,
+               double* __restrict__ cs, unsigned int* __restrict__ counter) {
+    using C = Gram8Cfg;
+    constexpr int BW = 32, NB = 48;
+    extern __shared__ __align__(128) uint8_t g8_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g8_raw) + 127) & ~uintptr_t(127));
+    uint64_t* mma_done = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 2);
+    __shared__ int ecol[BW];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t nblk = (n + kSp8RB - 1) / kSp8RB;
+    if (tid == 0) {
+        mbar_init(&mma_done[0], 1);
+        mbar_init(&mma_done[1], 1);
+        fence_barrier_init();
+    }
+    if (tid < BW) {   // the sparse step's scales of Y's digits (k_sp8_step, same bound)
+        const float bound = 0.5f * (norms[0] * pow2f(22 - ey2in[tid]) + norms[1] * fabsf((float)t[tid]));
+        ecol[tid] = i8_scale_exp(bound * 1.001f);
+    }
+    // the ones chunk of all four images' rows (byte 0 = 1)
+    for (int q = tid; q < 4 * kSp8RB; q += C::THREADS)
+        *reinterpret_cast<uint4*>(base + C::OFF_IMG + (q >> 7) * C::IMG + sp8_boff<64>(q & 127, 3)) = make_uint4(1u, 0u, 0u, 0u);
+    fence_proxy_async();
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(C::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+    const int r = tid & 127, hf = tid >> 7;
+    float sc[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) sc[c] = pow2f(ecol[16 * hf + c]);
+    auto stage = [&](int64_t B, int bufi) {   // rows of block B -> buffer bufi (16-byte chunks, 4 per thread)
+        const int64_t r0 = B * kSp8RB;
+        const int nrow = (int)min((int64_t)kSp8RB, n - r0);
+        for (int q = tid; q < nrow * (BW / 4); q += C::THREADS)
+            cp_async16(base + bufi * C::ROWS + q * 16, Y + r0 * BW + q * 4);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    constexpr uint32_t KGT = 64 / 16 * 128;
+    constexpr uint32_t idg = idesc_i8_bmn(128, NB, 1);
+    int k = 0;
+    if ((int64_t)blockIdx.x < nblk) stage(blockIdx.x, 0);
+    for (int64_t B = blockIdx.x; B < nblk; B += gridDim.x, ++k) {
+        const int bufi = k & 1, set = k & 1;
+        if (B + gridDim.x < nblk) {
+            stage(B + gridDim.x, bufi ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();   // block B's rows have landed (every thread's copies)
+        if (k >= 2) mbar_wait(&mma_done[set], (uint32_t)(((k - 2) >> 1) & 1), 161 * 65536 + (k & 0xFFFF));
+        {
+            const bool live = B * kSp8RB + r < n;
+            const float4* src = reinterpret_cast<const float4*>(base + bufi * C::ROWS + (r * BW + 16 * hf) * 4);
+            float v[16];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+                const float4 x = live ? src[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[4 * c4] = x.x; v[4 * c4 + 1] = x.y; v[4 * c4 + 2] = x.z; v[4 * c4 + 3] = x.w;
+            }
+            uint4 w0, w1, w2;
+            digit_rows16(v, sc, w0, w1, w2);
+            uint8_t* img = base + C::OFF_IMG + (2 * set + hf) * C::IMG;
+            *reinterpret_cast<uint4*>(img + sp8_boff<64>(r, 0)) = w0;
+            *reinterpret_cast<uint4*>(img + sp8_boff<64>(r, 1)) = w1;
+            *reinterpret_cast<uint4*>(img + sp8_boff<64>(r, 2)) = w2;
+        }
+        fence_proxy_async();
+        __syncthreads();   // both images complete; the row buffer may be refilled
+        if (warp == 0) {
+            tc_fence_after();
+            const uint32_t ia = smem_u32(base + C::OFF_IMG + (2 * set) * C::IMG), ib = ia + C::IMG;
+            if (elect_one()) {
+#pragma unroll
+                for (int j = 0; j < kSp8RB / 32; ++j) {   // K = 32 rows per MMA
+                    const uint64_t da = umma_desc_none(ia + 4 * KGT * j, KGT, 128), db = umma_desc_none(ib + 4 * KGT * j, KGT, 128);
+                    const uint32_t acc = (k > 0 || j > 0) ? 1u : 0u;
+                    tc_mma_i8(tbase, da, da, idg, acc);            // Yd_a^T [Yd_a | 1]
+                    tc_mma_i8(tbase + NB, da, db, idg, acc);       // Yd_a^T Yd_b (lane 48: 1^T Yd_b)
+                    tc_mma_i8(tbase + 2 * NB, db, db, idg, acc);   // Yd_b^T [Yd_b | 1]
+                }
+                tc_commit(&mma_done[set]);
+            }
+            __syncwarp();
+        }
+    }
+    // every MMA of this CTA has completed: the last commit of each set
+    for (int set = 0; set < 2; ++set) {
+        const int uses = (k + 1 - set) / 2;   // blocks k' < k with k' & 1 == set
+        if (uses > 0) mbar_wait(&mma_done[set], (uint32_t)((uses - 1) & 1), 162 * 65536 + set);
+    }
+    tc_fence_after();
+    // accumulators -> fp64: dbuf[a][p][i][j] (a = aa, ab, bb; p < 3), sums[a][j] from lane 48
+    double* dbuf = reinterpret_cast<double*>(base);   // 3 * 3 * 16 * 16 + 3 * 16 doubles = 18.8 KB (the row buffers)
+    if (warp < 2 && k > 0) {
+        const int L = 32 * warp + lane;
+        const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            int g[NB];
+#pragma unroll
+            for (int c0 = 0; c0 < NB; c0 += 8) tmem_ld8_u(tbase + lane_off + (uint32_t)(a * NB + c0), *reinterpret_cast<int(*)[8]>(&g[c0]));
+            tmem_wait_ld();
+            if (L <= 48) {
+                const int p = L / 16, ii = L % 16;
+                const double place = p == 0 ? 65536.0 : (p == 1 ? 256.0 : 1.0);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const double v = ((double)g[j] * 65536.0 + (double)g[16 + j] * 256.0 + (double)g[32 + j]) * place;
+                    if (p < 3) dbuf[((a * 3 + p) * 16 + ii) * 16 + j] = v;
+                    else if (ii == 0) dbuf[3 * 3 * 256 + a * 16 + j] = v;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(C::TCOLS));
+    }
+    // the CTA's partial: G (32 x 32, row-major at pitch 32), then the column sums
+    double* pg = part + (int64_t)blockIdx.x * kGramPart;
+    for (int pq = tid; pq < BW * BW; pq += C::THREADS) {
+        const int p_ = pq / BW, q_ = pq % BW, i = p_ < q_ ? p_ : q_, j = p_ < q_ ? q_ : p_;   // i <= j
+        const int a = (i < 16 ? 0 : 2) + ((i < 16 && j >= 16) ? 1 : 0), ii = i & 15, jj = j & 15;
+        double v = 0.0;
+        if (k > 0) {
+            v = (dbuf[((a * 3 + 0) * 16 + ii) * 16 + jj] + dbuf[((a * 3 + 1) * 16 + ii) * 16 + jj]) +
+                dbuf[((a * 3 + 2) * 16 + ii) * 16 + jj];
+            v = ldexp(v, -(ecol[i] + ecol[j]));
+        }
+        pg[pq] = v;
+    }
+    for (int q = tid; q < BW; q += C::THREADS)
+        pg[2 * kMaxB * kMaxB + q] = k > 0 ? ldexp(dbuf[3 * 3 * 256 + (q < 16 ? 0 : 2) * 16 + (q & 15)], -ecol[q]) : 0.0;
+    if (counter && last_block_done(counter)) {   // (counter == NULL: k_gram_sum follows)
+        if (cs)
+            for (int q = tid; q < BW; q += C::THREADS) cs[q] = ordered_sum(part + 2 * kMaxB * kMaxB + q, gridDim.x, kGramPart);
+        double o[4];
+        ordered_sum_x4(part, tid, BW * BW, gridDim.x, kGramPart, o);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) G[tid + 256 * e] = o[e];
+        if (tid == 0) *counter = 0;
+    }
+}
+
 }  // namespace sbmds

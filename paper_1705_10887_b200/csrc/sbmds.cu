@@ -1638,6 +1638,24 @@ void launch_sp8(sbmds_ctx* h, int b, float* Y, const float* Yprev, bool want_p1,
     h->gram_parts = grid;
 }
 
+// G = Y^T Y and s = 1^T Y of an n x 32 block from Y's digits on the int8 tensor cores (k_gram8_32;
+// the scales are the sparse step's: its ey2 exponents, t and norms of this apply)
+void gram8_32(sbmds_ctx* h, const float* Y, cudaStream_t st) {
+    smem_attr(k_gram8_32, Gram8Cfg::SMEM);
+    const int64_t nblk = (h->n + kSp8RB - 1) / kSp8RB;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nblk, 2 * (int64_t)h->num_sms));
+    h->gpart.ensure((size_t)std::max(grid, kRedBlocks) * kGramPart * sizeof(double));
+    profiled(h->prof, PK_GRAM, st, [&] {
+        launch(k_gram8_32, dim3(grid), dim3(Gram8Cfg::THREADS), (size_t)Gram8Cfg::SMEM, st, h->n, Y,
+               (const int*)(h->y16aux.as<unsigned int>() + 320), (const double*)h->t.as<double>(),
+               (const float*)h->s8rs1.as<float>() + sp8_rs_pad(h), h->gpart.as<double>(), h->G.as<double>(),
+               h->s.as<double>(), (unsigned int*)nullptr);
+        launch(k_gram_sum, dim3((unsigned)((4 * (32 * 32 + 32) + 255) / 256)), dim3(256), 0, st, 32, grid,
+               (const double*)h->gpart.as<double>(), h->G.as<double>(), (double*)nullptr, h->s.as<double>());
+    });
+    ++h->gram8_launches;
+}
+
 bool fused_ok(const sbmds_ctx* h, int b) {
     return h->fuse && h->blocked && (h->use_blocked & 1) && (b == 4 || b == 8 || b == 16 || b == 32) &&
            (size_t)h->umax * b * sizeof(float) <= kBlkSmem;
@@ -1824,7 +1842,10 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
                        (flags & kApplyGram8) != 0);
         });
         // G = Y^T Y, s = 1^T Y (and H' = Yprev^T Y) of the two halves together
-        if (flags & kApplySp8Halves) gram(h, b, Y, Yprev, st, true);
+        if (flags & kApplySp8Halves) {
+            if ((flags & kApplyGram8) && !Yprev) gram8_32(h, Y, st);   // (reading R18: no Rayleigh-Ritz step reads it)
+            else gram(h, b, Y, Yprev, st, true);
+        }
     } else if (flags & kApplyFused) {
         const bool want_p1 = !(flags & kApplyNoP1);
         profiled(h->prof, PK_CSR, st, [&] {
@@ -2845,7 +2866,9 @@ void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, 
     double* Hd = h->H.as<double>();
     double* Gd = h->G.as<double>();
     double* P = h->gpart.as<double>();
-    unsigned int* cnt = h->counters.as<unsigned int>() + CNT_GRAM;
+    // b > 16: the block partials are summed by k_gram_sum (several blocks) instead of the last block
+    const bool two_level = h->gram_tc && b > 16 && b <= 32;
+    unsigned int* cnt = two_level ? nullptr : h->counters.as<unsigned int>() + CNT_GRAM;
     smem_attr(k_gram_tc<4, true>, (int)gram_tc_smem<4>());
     smem_attr(k_gram_tc<4, false>, (int)gram_tc_smem<4>());
     smem_attr(k_gram_tc<2, true>, (int)gram_tc_smem<2>());   // (48 KB of row staging + the kernel's static 1 KB)
@@ -2865,6 +2888,11 @@ void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, 
                 if (ncb == 1) tc(k_gram_tc<1, false>);
                 else if (ncb == 2) tc(k_gram_tc<2, false>);
                 else tc(k_gram_tc<4, false>);
+            }
+            if (two_level) {
+                const int ent = b * b * (X ? 2 : 1) + (cs ? b : 0);
+                launch(k_gram_sum, dim3((unsigned)((4 * ent + 255) / 256)), dim3(256), 0, st, b, kRedBlocks, (const double*)P,
+                       Gd, X ? Hd : (double*)nullptr, cs);
             }
         } else if (X) {
             launch(k_gram<true>, dim3(kRedBlocks), dim3(256), smem, st, h->n, b, Y, X, P, Gd, Hd, cs, cnt);
@@ -3354,8 +3382,10 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl,
                              do_rr && !(h->sp8_dbg & 16) ? Yc : nullptr);
             } else if (sp8h) {
+                const bool rr_next = (tol > 0.0 && (itx + 1) % std::max(1, h->rr_period) == 0) || itx + 1 >= max_iters;
                 const int fl = kApplyFused | kApplySp8 | kApplySp8Halves | (itx > 1 ? kApplyY1Ready : 0) |
-                               (itx == max_iters ? kApplyNoP1 : 0);
+                               (itx == max_iters ? kApplyNoP1 : 0) |
+                               (h->sp8_gram8 && !do_rr && !rr_next ? kApplyGram8 : 0);
                 apply_device(h, b, Yc, Yn, st, true, h->Rinv.as<double>(), fl, do_rr ? Yc : nullptr);
             } else if (fused) {
                 // A5 fused with G = Y_{k+1}^T Y_{k+1}, s = 1^T Y_{k+1}, H' = Y_k^T Y_{k+1} (RR) and

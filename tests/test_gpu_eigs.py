@@ -402,15 +402,23 @@ def test_int8_gram_steps(cfg):
 @pytest.mark.gpu
 def test_eigs_b32_two_half_passes():
     """block = 32 where S is local: the tensor-core sparse step runs as two 16-column passes over
-    the images per iteration (Gram and Cholesky by their own kernels). Same iteration as the fp32
+    the images per iteration (Gram -- on the int8 tensor cores from Y's digits on steps that feed no
+    Rayleigh-Ritz step -- and Cholesky by their own kernels). Same iteration as the fp32
     fused kernels (sp8_apply = 0 keeps them), bitwise deterministic, converges to the oracle."""
     p = configs.config(2)
     with handle(p) as h:
         h.set_option("sp8_apply", 0)
         ref = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)
         h.set_option("sp8_apply", 1)
+        h.set_option("sp8_gram8", 0)
+        a64 = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)   # FP64 Gram kernel on every step
+        assert h.stat("sp8_state") == 1 and h.stat("gram8_launches") == 0
+        h.set_option("sp8_gram8", 1)
         a = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)
-        assert h.stat("sp8_state") == 1
+        # the int8 Gram of the 32-wide block (k_gram8_32) on every step but the last two
+        assert h.stat("gram8_launches") == 10
+        assert np.allclose(a[0], a64[0], rtol=1e-6), (a[0], a64[0])
+        assert O.principal_angle(a[1], a64[1]) <= 1e-4
         rep = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)
         lam, V, Z, info = gpu_eigs(h, 3, 32, max_iters=500, tol=1e-6, seed=5)
     assert np.allclose(a[0], ref[0], rtol=1e-5), (a[0], ref[0])
