@@ -568,3 +568,23 @@ def test_apply_graph_capture_without_checks():
         assert h.stat("sp8_apply_launches") == n5 + 1 and h.stat("sp8_apply_t_launches") == 0
     assert torch.equal(Y, Yg)
     assert relerr(Y.cpu().numpy(), oracle_apply(p, X.cpu().numpy())) <= TOL
+
+
+@pytest.mark.parametrize("n_rows", [99_991, 1_030, 1_001])
+def test_tensor_core_sparse_kernels_ragged_n(n_rows):
+    """n not a multiple of 128 (nor of 4): the last block of the tensor-core sparse kernels is a
+    few rows (23 at n = 99,991, 6 at n = 1,030, 105 at n = 1,001 -- an odd count; the library needs
+    n >= l = 1,000); apply at b = 16 and 32 on that path against the oracle."""
+    p0 = configs.config(2)
+    nnz = int(p0.row_ptr[n_rows])
+    p = configs.Problem("cfg2_head", n_rows, p0.l, p0.row_ptr[:n_rows + 1].copy(), p0.col_idx[:nnz].copy(),
+                        p0.val[:nnz].copy(), p0.D)
+    S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
+    with make_handle(p) as h:
+        for b in (16, 32):
+            X = configs.x_block(p.n, b, seed=b + 3)
+            n0 = h.stat("sp8_apply_launches")
+            Y = run_apply(h, X)
+            ref = O.apply(S, p.D, X.astype(np.float64))
+            assert relerr(Y, ref) <= TOL, (n_rows, b, relerr(Y, ref))
+            assert h.stat("sp8_apply_launches") == n0 + 1 and h.stat("sp8_state") == 1
