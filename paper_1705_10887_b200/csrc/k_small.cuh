@@ -779,7 +779,9 @@ __global__ void __launch_bounds__(256) k_rr(int b, int m, double tol, const doub
 // cs_part (optional): also produce s = 1^T out (fp64: warp sums -> per-warp smem rows ->
 // block partial -> last block, fixed order) = A1 of the next apply, so the eigs loop never
 // re-reads X for its column sums.
-template <int BT>
+// (CW: output columns formed together; 4 for the final V = Y (R^-1 U) with m <= 4 columns, where
+// 16 predicated accumulators per row made the kernel instruction-bound)
+template <int BT, int CW = 16>
 __global__ void __launch_bounds__(256) k_rotate(int64_t n, int b, int mo, int ldm, const float* __restrict__ in,
                                                 const double* __restrict__ M, float* __restrict__ out,
                                                 const double* __restrict__ addc, double* __restrict__ cs_part,
@@ -810,23 +812,23 @@ __global__ void __launch_bounds__(256) k_rotate(int64_t n, int b, int mo, int ld
 #pragma unroll
             for (int p = 0; p < BT; ++p) y[p] = (act && p < b) ? __ldg(row + p) : 0.f;
         }
-        for (int c0 = 0; c0 < mo; c0 += 16) {
-            double acc[16];
+        for (int c0 = 0; c0 < mo; c0 += CW) {
+            double acc[CW];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) acc[c] = (c0 + c < mo) ? As[c0 + c] : 0.0;
+            for (int c = 0; c < CW; ++c) acc[c] = (c0 + c < mo) ? As[c0 + c] : 0.0;
 #pragma unroll
             for (int p = 0; p < BT; ++p) {
                 if (p < b) {
                     const double yp = (double)y[p];
                     const double* mr = Ms + p * mo + c0;
 #pragma unroll
-                    for (int c = 0; c < 16; ++c)
+                    for (int c = 0; c < CW; ++c)
                         if (c0 + c < mo) acc[c] = fma(yp, mr[c], acc[c]);
                 }
             }
             float* orow = out + i * mo + c0;
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
+            for (int c = 0; c < CW; ++c) {
                 float v = 0.f;
                 if (c0 + c < mo) {
                     v = (float)acc[c];

@@ -2914,8 +2914,8 @@ void rotate(sbmds_ctx* h, int b, int mo, int ldm, const float* in, const double*
     profiled(h->prof, PK_ROTATE, st, [&] {
         if (b <= 4) go(k_rotate<4>);
         else if (b <= 8) go(k_rotate<8>);
-        else if (b <= 16) go(k_rotate<16>);
-        else if (b <= 32) go(k_rotate<32>);
+        else if (b <= 16) { if (mo <= 4) go(k_rotate<16, 4>); else go(k_rotate<16>); }
+        else if (b <= 32) { if (mo <= 4) go(k_rotate<32, 4>); else go(k_rotate<32>); }
         else go(k_rotate<64>);
     });
 }
