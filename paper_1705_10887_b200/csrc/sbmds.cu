@@ -2878,7 +2878,7 @@ void gram(sbmds_ctx* h, int b, const float* Y, const float* X, cudaStream_t st, 
         launch(kern, dim3(kRedBlocks), dim3(256), smem_tc, st, h->n, b, Y, X, P, Gd, Hd, cs, cnt);
     };
     profiled(h->prof, PK_GRAM, st, [&] {
-        if (h->gram_tc && b <= 32) {   // FP64 tensor cores (DMMA m8n8k4)
+        if (h->gram_tc && b <= 32 && b > 4) {   // FP64 tensor cores (DMMA m8n8k4); b <= 4 (the orthogonality check of V): k_gram
             const int ncb = (b + 7) / 8;
             if (X) {
                 if (ncb == 1) tc(k_gram_tc<1, true>);
