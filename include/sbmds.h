@@ -292,6 +292,16 @@ int64_t sbmds_plan_selfcheck(int64_t l, int32_t S, int32_t gN, int32_t max_ctas,
 int64_t sbmds_plan_selfcheck_rect(int64_t l, int32_t SR, int32_t SC, int32_t gN, int32_t max_ctas, int32_t contiguous,
                                   int32_t rank, int32_t world);
 
+/* Host logic of the tensor-core sparse kernels' blocks (no GPU; used by the CPU tests; DESIGN.md §4
+   "Blocks as row ranges"): one round of splitting. Block B is the row range [r0[B], r0[B + 1]) of S
+   (the operator is local, so consecutive vertices share landmarks) and touches
+   dsize[B] distinct landmarks; a block over `limit` (128 in the library: one image holds 128
+   landmark columns) is halved at a multiple of 4 rows from its start. r0_out receives the new
+   boundaries (at most `capacity` entries); returns the new block count, -1 when a block over the
+   limit has fewer than 8 rows, -2 for bad arguments or too small a capacity. */
+int64_t sbmds_sparse_split_rows(int64_t n, int64_t nblk, const int32_t* r0, const int32_t* dsize, int32_t limit,
+                             int32_t* r0_out, int64_t capacity);
+
 /*
  * Sharded apply. The matvec of PAPER.md:221-222 splits by rows of P (= S)
  * and by tiles of W (= D_ll): rank g of `world` holds rows [row0, row0 + n_local) of S and

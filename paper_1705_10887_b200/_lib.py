@@ -20,7 +20,7 @@ STATUS_NAMES = {0: "SBMDS_OK", 1: "SBMDS_EINVAL", 2: "SBMDS_ENOMEM", 3: "SBMDS_E
 # Every symbol include/sbmds.h declares (checked by tests/test_abi.py on CPU).
 EXPORTS = ("sbmds_create", "sbmds_apply", "sbmds_eigs", "sbmds_destroy", "sbmds_last_error",
            "sbmds_set_option", "sbmds_get_stat", "sbmds_launch_count", "sbmds_abi_version",
-           "sbmds_plan_selfcheck", "sbmds_plan_selfcheck_rect", "sbmds_create_shard", "sbmds_shard_stage", "sbmds_shard_exchange_bytes",
+           "sbmds_plan_selfcheck", "sbmds_plan_selfcheck_rect", "sbmds_sparse_split_rows", "sbmds_create_shard", "sbmds_shard_stage", "sbmds_shard_exchange_bytes",
            "sbmds_shard_attach_nccl", "sbmds_nccl_unique_id", "sbmds_shard_plan_selfcheck", "sbmds_shard_tiles", "sbmds_bmds", "sbmds_sbha_p", "sbmds_sbha_build")
 NCCL_UNIQUE_ID_BYTES = 128
 
@@ -78,6 +78,8 @@ def lib() -> ctypes.CDLL:
             L.sbmds_plan_selfcheck.restype = i64
             L.sbmds_plan_selfcheck_rect.argtypes = [i64, i32, i32, i32, i32, i32, i32, i32]
             L.sbmds_plan_selfcheck_rect.restype = i64
+            L.sbmds_sparse_split_rows.argtypes = [i64, i64, p, p, i32, p, i64]
+            L.sbmds_sparse_split_rows.restype = i64
             L.sbmds_create_shard.argtypes = [i64, i64, i64, i64, i64, p, p, p, p, i32, i32, u32, p,
                                              ctypes.POINTER(p)]
             L.sbmds_create_shard.restype = ctypes.c_int

@@ -1993,6 +1993,30 @@ void build_blocked(sbmds_ctx* h, const int32_t* rowof, cudaStream_t st) {
 // Tensor-core sparse step (k_sp8.cuh): 128-row blocks whose dictionaries all fit 128 entries,
 // S_B stored once as a dense three-plane digit image. Built at the first eigs that can use it
 // (the row index of every entry is re-expanded from the row pointers).
+// One round of the tensor-core sparse kernels' block splitting: every block [r0[B], r0[B + 1]) whose
+// dictionary (doff[B + 1] - doff[B] landmarks) exceeds `limit` is halved at a multiple of 4 rows
+// from its start (the step stages 16-byte groups of per-row data from a block's first row). Returns
+// the number of blocks halved, or -1 when such a block has fewer than 8 rows (it cannot be halved
+// into pieces of >= 4 rows); out = the new boundaries.
+int64_t sp8_split_rows(int64_t n, const std::vector<int32_t>& r0, const std::vector<int32_t>& doff, int limit,
+                       std::vector<int32_t>& out) {
+    const int64_t nblk = (int64_t)r0.size() - 1;
+    out.clear();
+    out.reserve(r0.size() + 64);
+    int64_t nsplit = 0;
+    for (int64_t B = 0; B < nblk; ++B) {
+        out.push_back(r0[B]);
+        const int32_t rows = r0[B + 1] - r0[B];
+        if (doff[B + 1] - doff[B] > limit) {
+            if (rows < 8) return -1;
+            out.push_back(r0[B] + ((rows / 2 + 3) & ~3));
+            ++nsplit;
+        }
+    }
+    out.push_back((int32_t)n);
+    return nsplit;
+}
+
 bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
     if (h->sp8_state != 0) return h->sp8_state > 0;
     h->sp8_state = -1;
@@ -2018,19 +2042,9 @@ bool ensure_sp8(sbmds_ctx* h, cudaStream_t st) {
         CK(cudaMemcpyAsync(doff.data(), o.doff.p, doff.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         std::vector<int32_t> nr;
-        nr.reserve(r0.size() + 64);
-        bool stuck = false;
-        for (int64_t B = 0; B < o.nblk; ++B) {
-            nr.push_back(r0[B]);
-            const int32_t rows = r0[B + 1] - r0[B];
-            if (doff[B + 1] - doff[B] > kSp8DK) {
-                if (rows < 8) { stuck = true; break; }
-                nr.push_back(r0[B] + ((rows / 2 + 3) & ~3));
-                ++h->sp8_splits;
-            }
-        }
-        nr.push_back((int32_t)h->n);
-        if (stuck || nr.size() > (size_t)2 * ((h->n + kSp8RB - 1) / kSp8RB) + 2) break;   // (would double the images)
+        const int64_t ns = sp8_split_rows(h->n, r0, doff, kSp8DK, nr);
+        if (ns < 0 || nr.size() > (size_t)2 * ((h->n + kSp8RB - 1) / kSp8RB) + 2) break;   // (stuck, or would double the images)
+        h->sp8_splits += ns;
         r0.swap(nr);
         const int64_t nb2 = (int64_t)r0.size() - 1;
         o.reset();
@@ -2160,6 +2174,21 @@ void destroy_ctx(sbmds_ctx* h) {
 }
 
 }  // namespace
+
+// One round of the block splitting of the tensor-core sparse kernels on the host (no GPU; CPU tests):
+// r0[nblk + 1] block boundaries, dsize[nblk] dictionary sizes, limit = 128 in the library. Writes
+// the new boundaries to r0_out (capacity entries) and returns their count - 1 = the new block
+// count, or -1 (a block over the limit has fewer than 8 rows) / -2 (bad arguments, capacity).
+extern "C" int64_t sbmds_sparse_split_rows(int64_t n, int64_t nblk, const int32_t* r0, const int32_t* dsize, int32_t limit,
+                                        int32_t* r0_out, int64_t capacity) {
+    if (n < 1 || nblk < 1 || !r0 || !dsize || limit < 1 || !r0_out) return -2;
+    std::vector<int32_t> rv(r0, r0 + nblk + 1), doff((size_t)nblk + 1, 0), out;
+    for (int64_t B = 0; B < nblk; ++B) doff[B + 1] = doff[B] + dsize[B];
+    if (sp8_split_rows(n, rv, doff, limit, out) < 0) return -1;
+    if ((int64_t)out.size() > capacity) return -2;
+    std::copy(out.begin(), out.end(), r0_out);
+    return (int64_t)out.size() - 1;
+}
 
 // ============================================================================ create
 namespace {

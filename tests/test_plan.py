@@ -54,3 +54,32 @@ def test_plan_selfcheck_rect_rejects_bad_arguments():
     assert lib().sbmds_plan_selfcheck_rect(100, 9, 0, 1, 1, 1, 0, 1) < 0
     assert lib().sbmds_plan_selfcheck_rect(100, 17, 1, 1, 1, 1, 0, 1) < 0
     assert lib().sbmds_plan_selfcheck_rect(100, 9, 1, 1, 1, 1, 2, 2) < 0
+
+
+def _split(n, r0, dsize, limit=128):
+    import numpy as np
+    r0 = np.ascontiguousarray(r0, dtype=np.int32)
+    ds = np.ascontiguousarray(dsize, dtype=np.int32)
+    out = np.zeros(2 * len(r0) + 2, dtype=np.int32)
+    nb = lib().sbmds_sparse_split_rows(n, len(ds), r0.ctypes.data, ds.ctypes.data, limit, out.ctypes.data, len(out))
+    return nb, out[:nb + 1] if nb > 0 else None
+
+
+def test_sp8_split_rows_rule():
+    """The block-splitting rule of the tensor-core sparse kernels (host part of ensure_sp8): only
+    blocks over the limit are halved, at a multiple of 4 rows from their start; the boundaries stay
+    a partition of [0, n); a block over the limit with fewer than 8 rows cannot be split."""
+    import numpy as np
+    n = 128 * 5 + 37
+    r0 = np.minimum(np.arange(7) * 128, n)           # 6 blocks, the last of 37 rows
+    nb, out = _split(n, r0, [100, 129, 128, 300, 20, 200])
+    assert nb == 9
+    assert list(out) == [0, 128, 192, 256, 384, 448, 512, 640, 660, n]
+    assert all(int(b) % 4 == 0 for b in out[:-1]) and out[0] == 0 and out[-1] == n and np.all(np.diff(out) > 0)
+    nb2, out2 = _split(n, out, [100, 60, 70, 128, 160, 150, 20, 110, 100])   # second round: two pieces still over
+    assert nb2 == 11 and list(out2[4:9]) == [384, 416, 448, 480, 512]
+    assert _split(8, [0, 8], [129])[0] == 2 and list(_split(8, [0, 8], [129])[1]) == [0, 4, 8]
+    assert _split(7, [0, 7], [129])[0] == -1          # fewer than 8 rows over the limit
+    assert _split(6, [0, 4, 6], [10, 500])[0] == -1
+    assert _split(640, np.arange(6) * 128, [128] * 5)[0] == 5   # nothing over the limit: unchanged count
+    assert lib().sbmds_sparse_split_rows(0, 1, None, None, 128, None, 0) == -2
