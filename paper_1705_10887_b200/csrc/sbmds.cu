@@ -508,6 +508,8 @@ struct sbmds_ctx {
     int sp8_pf = 0;        // k_sp8_step: L2 prefetch distance of the images, in blocks (0: off)
     int sp8_gram8 = 1;     // k_sp8_step: int8-tensor-core Gram on steps that feed no Rayleigh-Ritz step
     int sp8_apply = 1;     // standalone apply at b = 16: A5 through the tensor-core step's N products
+    int64_t sp8_min_rows = 16 * 128 * 148;   // ... and eigs at b = 32: only from this many rows on (the kernels' fixed
+                                             // costs lose to the fp32 SpMMs on small problems: config 2 0.125 vs 0.087 ms at b = 32)
     int64_t sp8_apply_launches = 0, sp8_apply_t_launches = 0, x_fallbacks = 0;
     int64_t sp8_splits = 0;   // 128-row blocks halved because their dictionary exceeded one image
     int64_t gram8_launches = 0;   // steps that took it (stat)
@@ -1696,7 +1698,7 @@ void apply_device(sbmds_ctx* h, int b, const float* X, float* Y, cudaStream_t st
     const bool blk = blocked_ok(h, b, bp, X, Y);
     // standalone apply at b = 16 with S local (k_sp8.cuh's images): A2 as the T products, A5 as the
     // N products of the tensor-core sparse step
-    const bool sp8_a = flags == 0 && (b == 16 || b == 32) && blk && h->sp8_apply &&
+    const bool sp8_a = flags == 0 && (b == 16 || b == 32) && blk && h->sp8_apply && h->n >= h->sp8_min_rows &&
                        (reinterpret_cast<uintptr_t>(X) & 15) == 0 && sp8_ok(h, 16, st);
     bool sp8_a2 = false;
     // A1: s = 1^T X (inside eigs it was produced by the previous rotate)
@@ -3396,7 +3398,8 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         const bool sp8 = fused && sp8_ok(h, b, st);   // tensor-core sparse step (fuse = 3)
         // b = 32 (config 3): the same kernel as two 16-column passes per step, Gram and Cholesky
         // by their own kernels
-        const bool sp8h = !sp8 && fused && b == 32 && h->fuse == 3 && h->sp8_apply && sp8_ok(h, 16, st);
+        const bool sp8h = !sp8 && fused && b == 32 && h->fuse == 3 && h->sp8_apply && h->n >= h->sp8_min_rows &&
+                          sp8_ok(h, 16, st);
         // one iteration's device work: Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1} (s = 1^T Y_k came from
         // the last Gram), the Grams, and at Rayleigh-Ritz steps the Jacobi solve (no host syncs)
         auto enqueue_iteration = [&](int itx, bool do_rr) {
@@ -4199,6 +4202,9 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         h->sp8_poll = (int)value;
     } else if (!strcmp(key, "sp8_apply")) {
         h->sp8_apply = value != 0;
+    } else if (!strcmp(key, "sp8_min_rows")) {
+        if (value < 0) return fail(SBMDS_EINVAL, "sp8_min_rows must be >= 0");
+        h->sp8_min_rows = value;
     } else if (!strcmp(key, "sp8_gram8")) {
         h->sp8_gram8 = value != 0;
     } else if (!strcmp(key, "sp8_pf")) {

@@ -471,6 +471,7 @@ def test_apply_on_tensor_core_sparse_kernels(kind):
         X[777] *= 1.0e4
     S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
     with make_handle(p) as h:
+        h.set_option("sp8_min_rows", 0)   # (config 2 is below the default size threshold of these kernels)
         if kind == "uncentred":
             h.set_option("center", 0)
             ref = O.apply_raw(S, p.D, X.astype(np.float64))
@@ -498,6 +499,7 @@ def test_apply_b32_on_tensor_core_sparse_kernels():
     X = configs.x_block(p.n, 32, seed=13)
     ref = oracle_apply(p, X)
     with make_handle(p) as h:
+        h.set_option("sp8_min_rows", 0)   # (config 2 is below the default size threshold of these kernels)
         n0, t0 = h.stat("sp8_apply_launches"), h.stat("sp8_apply_t_launches")
         Y = run_apply(h, X)
         assert h.stat("sp8_apply_launches") == n0 + 1 and h.stat("sp8_apply_t_launches") == t0 + 1
@@ -529,6 +531,7 @@ def test_tensor_core_sparse_kernels_split_blocks():
     p = configs.Problem("cfg2_swapped", n, p0.l, row_ptr, p0.col_idx[idx], p0.val[idx], p0.D)
     S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
     with make_handle(p) as h:
+        h.set_option("sp8_min_rows", 0)   # (config 2 is below the default size threshold of these kernels)
         for b in (16, 32):
             X = configs.x_block(p.n, b, seed=b)
             n0 = h.stat("sp8_apply_launches")
@@ -555,6 +558,7 @@ def test_apply_graph_capture_without_checks():
     Y = torch.empty_like(X)
     Yg = torch.empty_like(X)
     with make_handle(p) as h:
+        h.set_option("sp8_min_rows", 0)   # (config 2 is below the default size threshold of these kernels)
         h.set_option("dy_max_range", 64)
         h.apply(X, out=Y)
         torch.cuda.synchronize()
@@ -581,6 +585,7 @@ def test_tensor_core_sparse_kernels_ragged_n(n_rows):
                         p0.val[:nnz].copy(), p0.D)
     S = O.csr(p.n, p.l, p.row_ptr, p.col_idx, p.val32())
     with make_handle(p) as h:
+        h.set_option("sp8_min_rows", 0)   # (config 2 is below the default size threshold of these kernels)
         for b in (16, 32):
             X = configs.x_block(p.n, b, seed=b + 3)
             n0 = h.stat("sp8_apply_launches")

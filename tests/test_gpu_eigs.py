@@ -407,6 +407,7 @@ def test_eigs_b32_two_half_passes():
     fused kernels (sp8_apply = 0 keeps them), bitwise deterministic, converges to the oracle."""
     p = configs.config(2)
     with handle(p) as h:
+        h.set_option("sp8_min_rows", 0)   # (config 2 is below the default size threshold of these kernels)
         h.set_option("sp8_apply", 0)
         ref = gpu_eigs(h, 8, 32, max_iters=12, tol=0.0, seed=2)
         h.set_option("sp8_apply", 1)
