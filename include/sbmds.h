@@ -226,11 +226,11 @@ const char* sbmds_last_error(void);
  *                      check of "dy_max_range": stat "x_fallbacks") and A5 as its N products
  *                      (stats "sp8_apply_t_launches", "sp8_apply_launches"); 0 keeps the fp32
  *                      CSC / row-blocked CSR kernels
- *     "sp8_min_rows"   (default 303,104 = 16 blocks of 128 rows per SM) the standalone apply and the
- *                      b = 32 eigs step take the tensor-core sparse kernels only from this many
- *                      rows on: their fixed costs per launch lose to the fp32 SpMMs on small
- *                      problems (config 2, n = 100,000: 0.125 vs 0.087 ms per apply at b = 32);
- *                      0 = always where they apply
+ *     "sp8_min_rows"   (default 303,104 = 16 blocks of 128 rows per SM) the standalone apply takes
+ *                      the tensor-core sparse kernels only from this many rows on: their fixed
+ *                      costs per launch lose to the fp32 SpMMs on small problems (config 2,
+ *                      n = 100,000: 0.125 vs 0.087 ms per apply at b = 32); 0 = always where they
+ *                      apply (sbmds_eigs takes them at any size: there they replace several kernels)
  *     "sp8_pf"         (blocks, default 0) tensor-core step: L2 prefetch distance of the images
  *                      (measured: no gain)
  *     "solver"         eigs: 0 (default) block subspace iteration; 1 restarted block Lanczos with

@@ -508,8 +508,8 @@ struct sbmds_ctx {
     int sp8_pf = 0;        // k_sp8_step: L2 prefetch distance of the images, in blocks (0: off)
     int sp8_gram8 = 1;     // k_sp8_step: int8-tensor-core Gram on steps that feed no Rayleigh-Ritz step
     int sp8_apply = 1;     // standalone apply at b = 16: A5 through the tensor-core step's N products
-    int64_t sp8_min_rows = 16 * 128 * 148;   // ... and eigs at b = 32: only from this many rows on (the kernels' fixed
-                                             // costs lose to the fp32 SpMMs on small problems: config 2 0.125 vs 0.087 ms at b = 32)
+    int64_t sp8_min_rows = 16 * 128 * 148;   // ... only from this many rows on (the kernels' fixed costs lose to the fp32
+                                             // SpMMs on small problems: config 2 0.125 vs 0.087 ms per apply at b = 32)
     int64_t sp8_apply_launches = 0, sp8_apply_t_launches = 0, x_fallbacks = 0;
     int64_t sp8_splits = 0;   // 128-row blocks halved because their dictionary exceeded one image
     int64_t gram8_launches = 0;   // steps that took it (stat)
@@ -3398,8 +3398,8 @@ extern "C" sbmds_status sbmds_eigs(sbmds_t h, int32_t m, int32_t block, int32_t 
         const bool sp8 = fused && sp8_ok(h, b, st);   // tensor-core sparse step (fuse = 3)
         // b = 32 (config 3): the same kernel as two 16-column passes per step, Gram and Cholesky
         // by their own kernels
-        const bool sp8h = !sp8 && fused && b == 32 && h->fuse == 3 && h->sp8_apply && h->n >= h->sp8_min_rows &&
-                          sp8_ok(h, 16, st);
+        const bool sp8h = !sp8 && fused && b == 32 && h->fuse == 3 && h->sp8_apply && sp8_ok(h, 16, st);   // (also on small
+        // problems, unlike the standalone apply: config 2 at b = 32 7.5 vs 10.5 ms per 50 iterations on the fp32 fused kernels)
         // one iteration's device work: Y_{k+1} = B~ X_k = (B~ Y_k) R_k^{-1} (s = 1^T Y_k came from
         // the last Gram), the Grams, and at Rayleigh-Ritz steps the Jacobi solve (no host syncs)
         auto enqueue_iteration = [&](int itx, bool do_rr) {
