@@ -1484,7 +1484,9 @@ void ycheck(sbmds_ctx* h, int b, int bp, cudaStream_t st, bool want_y = true, bo
             float m;
             memcpy(&m, &mx[c], 4);
             const double rms = std::sqrt(ss[c] / count);
-            if (!(m < 3.0e38f) || (m > 0.f && (double)m > lim * rms)) return true;
+            // (a NaN / Inf anywhere in the column shows in its sum of squares: the fp32-grade kernels
+            // propagate it, the fixed point would turn it into garbage digits)
+            if (!(m < 3.0e38f) || !std::isfinite(rms) || (m > 0.f && (double)m > lim * rms)) return true;
         }
         return false;
     };

@@ -232,3 +232,23 @@ def test_no_convergence_status_fills_outputs():
     Z = Z.cpu().numpy().astype(np.float64)
     assert np.all(np.isfinite(lam)) and np.abs(V.T @ V - np.eye(p.m)).max() < 1e-5
     assert np.allclose(Z, V * np.sqrt(np.maximum(lam, 0))[None, :], rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.gpu
+def test_nan_in_x_propagates_through_the_standalone_apply():
+    """A NaN in X must come out as NaN (as the fp32 kernels give), not as garbage digits of the
+    fixed-point paths: the column check sees it in the sum of squares and keeps the fp32-grade
+    kernels (stats x_fallbacks / y_fallbacks)."""
+    import torch
+    from gen import configs
+    from paper_1705_10887_b200 import from_problem
+    p = configs.config(2)
+    X = configs.x_block(p.n, 16, seed=2)
+    X[4321, 5] = np.nan
+    with from_problem(p) as h:
+        h.set_option("sp8_min_rows", 0)
+        f0 = h.stat("x_fallbacks")
+        Y = h.apply(torch.from_numpy(X).cuda()).cpu().numpy()
+        assert h.stat("x_fallbacks") == f0 + 1
+    assert np.isnan(Y[:, 5]).all()          # B~ is dense in effect: every row of that column
+    assert np.isfinite(Y[:, [0, 1, 15]]).all()
