@@ -372,29 +372,72 @@ __global__ void __launch_bounds__(256) k_spmm_csc_gen(
 }
 
 // ------------------------------------------------------------------ A5: Y = -1/2 (S Y2 - 1 t^T)
-// CSR SpMM: LPR lanes per row (float4 gathers of the L2-resident Y2 rows), G rows per warp.
-template <int LPR>
+// CSR SpMM: LPR lanes per row (float4 gathers of the L1/L2-resident Y2 rows), G rows per warp.
+// The G rows of a warp are consecutive, so their (column, value) pairs are contiguous: each lane
+// loads one pair per chunk of LPR (four chunks in flight), and the group broadcasts them in entry
+// order with shuffles. One lane per pair instead of every lane of a group re-reading its row's
+// pair cuts the L1 wavefronts per step from ~16 (4 + 4 for the strided column and value words,
+// 8 for the gathered rows) to ~10; the sums keep the entry order (beg, beg + 1, ...), so results
+// are bitwise those of the plain loop. The trip count is warp-uniform (full-warp shuffles).
+// SHF = false: the plain loop (every lane of a group reads its row's pairs itself; measured faster for
+// wide rows, LPR >= 8, where a warp holds few rows and the pair loads are few lines anyway).
+template <int LPR, bool SHF>
 __global__ void __launch_bounds__(256) k_spmm_csr_vec4(
     int64_t n, int b, int bp, const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
     const float* __restrict__ val, const float* __restrict__ Y2, const double* __restrict__ t,
     float* __restrict__ Y) {
     constexpr int G = 32 / LPR;
+    constexpr int U = 4;   // chunks of LPR entries loaded ahead
     const int lane = threadIdx.x & 31;
     const int g = lane / LPR, q = lane % LPR;
     const int64_t i = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * G + g;
-    if (i >= n) return;
-    const int32_t beg = rp[i], end = rp[i + 1];
+    const bool live = i < n;
+    const int32_t beg = live ? rp[i] : 0, end = live ? rp[i + 1] : 0;
+    const int len = end - beg;
+    const float4* __restrict__ Y24 = reinterpret_cast<const float4*>(Y2);
+    const int nv = bp / 4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (!SHF) {
 #pragma unroll 4
-    for (int32_t e = beg; e < end; ++e) {
-        const int32_t c = __ldg(col + e);
-        const float v = __ldg(val + e);
-        const float4 y = __ldg(reinterpret_cast<const float4*>(Y2 + (int64_t)c * bp) + q);
-        acc.x = fmaf(v, y.x, acc.x);
-        acc.y = fmaf(v, y.y, acc.y);
-        acc.z = fmaf(v, y.z, acc.z);
-        acc.w = fmaf(v, y.w, acc.w);
+        for (int32_t e = beg; e < end; ++e) {
+            const int32_t c = __ldg(col + e);
+            const float v = __ldg(val + e);
+            const float4 y = __ldg(Y24 + (int64_t)c * nv + q);
+            acc.x = fmaf(v, y.x, acc.x);
+            acc.y = fmaf(v, y.y, acc.y);
+            acc.z = fmaf(v, y.z, acc.z);
+            acc.w = fmaf(v, y.w, acc.w);
+        }
     }
+    const int maxlen = SHF ? (int)__reduce_max_sync(0xffffffffu, (unsigned)len) : 0;
+    for (int c0 = 0; c0 < maxlen; c0 += U * LPR) {
+        int lc[U];
+        float lv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t e = beg + c0 + u * LPR + q;
+            const bool ok = e < end;
+            lc[u] = ok ? __ldg(col + e) : 0;
+            lv[u] = ok ? __ldg(val + e) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (c0 + u * LPR >= maxlen) break;   // (warp-uniform)
+#pragma unroll
+            for (int tq = 0; tq < LPR; ++tq) {
+                const int c = __shfl_sync(0xffffffffu, lc[u], tq, LPR);
+                const float v = __shfl_sync(0xffffffffu, lv[u], tq, LPR);
+                if (c0 + u * LPR + tq < len) {
+                    const float4 y = __ldg(Y24 + (int64_t)c * nv + q);
+                    acc.x = fmaf(v, y.x, acc.x);
+                    acc.y = fmaf(v, y.y, acc.y);
+                    acc.z = fmaf(v, y.z, acc.z);
+                    acc.w = fmaf(v, y.w, acc.w);
+                }
+            }
+        }
+    }
+    if (!live) return;
     const int c0 = 4 * q;
     float4 out;
     out.x = (float)(-0.5 * ((double)acc.x - t[c0 + 0]));

@@ -486,6 +486,7 @@ struct sbmds_ctx {
     int gram_tc = 1;       // Gram on the FP64 tensor cores (b <= 32)
     int csr_nnz_per_lane = 4;   // narrow CSR SpMM: nonzeros per lane when choosing lanes per row
     int csr_sub_L = 0;          // (tuning) force lanes per row
+    int csr_shfl = -1;          // (tuning) k_spmm_csr_vec4's shuffled pair loads: -1 auto, 0 off, 1 on
     int fuse = 3;          // eigs: 1 = A5 fused with the Gram, 2 = also the next A2's S^T partials (k_fused.cuh),
                            // 3 = the tensor-core sparse step where it applies (k_sp8.cuh), else 1
     // tensor-core sparse step (k_sp8.cuh): 128-row blocks, dense three-plane digit images of S_B
@@ -1428,12 +1429,18 @@ void spmm_csr(sbmds_ctx* h, int b, int bp, float* Y, cudaStream_t st) {
         std::apply([&](auto... a) { launch(kern, dim3(grid), dim3(256), 0, st, a...); }, args);
     };
     if (vec) {
+        // pairs loaded once per group and broadcast by shuffles (option csr_shfl: -1 auto, 0, 1). Auto:
+        // b <= 16, or rows long enough to fill a group's four chunks (>= 4 * lanes per row entries on
+        // average): measured on the config-5 sweep (scripts/csr_shfl_sweep.py) 1.1-1.7x faster there,
+        // 1.1-1.5x slower for short rows at b >= 32 (most of a chunk's shuffles are padding).
+        const double avg = (double)h->nnz / (double)std::max<int64_t>(1, h->n);
+        const bool shf = h->csr_shfl < 0 ? (lpr <= 4 || avg >= 4.0 * lpr) : h->csr_shfl != 0;
         switch (b / 4) {
-            case 1: go(k_spmm_csr_vec4<1>); break;
-            case 2: go(k_spmm_csr_vec4<2>); break;
-            case 4: go(k_spmm_csr_vec4<4>); break;
-            case 8: go(k_spmm_csr_vec4<8>); break;
-            default: go(k_spmm_csr_vec4<16>); break;
+            case 1: shf ? go(k_spmm_csr_vec4<1, true>) : go(k_spmm_csr_vec4<1, false>); break;
+            case 2: shf ? go(k_spmm_csr_vec4<2, true>) : go(k_spmm_csr_vec4<2, false>); break;
+            case 4: shf ? go(k_spmm_csr_vec4<4, true>) : go(k_spmm_csr_vec4<4, false>); break;
+            case 8: shf ? go(k_spmm_csr_vec4<8, true>) : go(k_spmm_csr_vec4<8, false>); break;
+            default: shf ? go(k_spmm_csr_vec4<16, true>) : go(k_spmm_csr_vec4<16, false>); break;
         }
     } else {
         switch (bp) {
@@ -4155,6 +4162,9 @@ extern "C" sbmds_status sbmds_set_option(sbmds_t h, const char* key, int64_t val
         if (value < 0 || value > 3) return fail(SBMDS_EINVAL, "blocked is a bit mask in [0, 3]");
         h->use_blocked = (int)value;
         h->blocked_auto = false;
+    } else if (!strcmp(key, "csr_shfl")) {
+        if (value < -1 || value > 1) return fail(SBMDS_EINVAL, "csr_shfl in {-1 auto, 0, 1}");
+        h->csr_shfl = (int)value;
     } else if (!strcmp(key, "gram_tc")) {
         h->gram_tc = value ? 1 : 0;
     } else if (!strcmp(key, "order_columns")) {
