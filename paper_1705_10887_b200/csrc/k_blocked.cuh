@@ -118,6 +118,7 @@ __device__ __forceinline__ float4 blk_row_sum(int32_t beg, int32_t end, int maxl
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
+            if (c0 + u * LPR >= maxlen) break;   // (warp-uniform) the rest of the chunk is padding in every row
 #pragma unroll
             for (int tq = 0; tq < LPR; ++tq) {
                 const int c = __shfl_sync(0xffffffffu, lc[u], tq, LPR);

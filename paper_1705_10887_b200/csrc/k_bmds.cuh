@@ -363,16 +363,32 @@ __global__ void __launch_bounds__(256) k_symv_rows(int64_t l, const float* __res
     }
 }
 
+// t = v^T Y1 (b values, fp64). Block B takes the contiguous row range B of gridDim.x and writes
+// its partial to part[B][64]; k_vdot_sum adds the partials in block order (fixed order, bitwise
+// reproducible for a given grid). A single CTA over all l rows took 3 ms at l = 50,000 (12,500
+// dependent fp64 FMAs per thread): two thirds of a sharded eigs iteration.
+constexpr int kVdotBlocks = 128;
 __global__ void __launch_bounds__(256) k_vdot(int64_t l, int b, int bp, const double* __restrict__ v,
-                                              const float* __restrict__ Y1, double* __restrict__ t) {
-    __shared__ double part[256];
+                                              const float* __restrict__ Y1, double* __restrict__ part) {
+    __shared__ double red[256];
     const int c = threadIdx.x % 64, r0 = threadIdx.x / 64;
+    const int64_t per = (l + gridDim.x - 1) / gridDim.x;
+    const int64_t beg = blockIdx.x * per, end = min(l, beg + per);
     double acc = 0.0;
     if (c < b)
-        for (int64_t i = r0; i < l; i += 4) acc = fma(v[i], (double)Y1[i * bp + c], acc);
-    part[threadIdx.x] = acc;
+        for (int64_t i = beg + r0; i < end; i += 4) acc = fma(v[i], (double)Y1[i * bp + c], acc);
+    red[threadIdx.x] = acc;
     __syncthreads();
-    if (threadIdx.x < b) t[threadIdx.x] = part[c] + part[64 + c] + part[128 + c] + part[192 + c];
+    if (threadIdx.x < 64)
+        part[blockIdx.x * 64 + threadIdx.x] = (red[c] + red[64 + c]) + (red[128 + c] + red[192 + c]);
+}
+
+__global__ void __launch_bounds__(64) k_vdot_sum(int nblocks, int b, const double* __restrict__ part,
+                                                 double* __restrict__ t) {
+    if ((int)threadIdx.x >= b) return;
+    double acc = 0.0;
+    for (int B = 0; B < nblocks; ++B) acc += part[B * 64 + threadIdx.x];
+    t[threadIdx.x] = acc;
 }
 
 }  // namespace sbmds

@@ -575,7 +575,7 @@ struct sbmds_ctx {
     int last_dpath = 0;          // D-stream path of the last apply: 1 ffma, 2 tcgen05, 3 tcgen05 symmetric half
     int64_t last_dbytes = 0;     // its bytes per launch (bench roofline)
     // apply workspace
-    DevBuf Y1, Y2, P, colpart, s, t, tpart, counters;
+    DevBuf Y1, Y2, P, colpart, s, t, tpart, counters, vdpart;
     int64_t y1_rows = 0;
     // eigs workspace
     DevBuf X, Y, gpart, G, H, Rinv, Rinv2, status, rr, vtmp, ztmp, sign, apval, apidx, xhost, yhost, vsel;
@@ -2755,6 +2755,14 @@ extern "C" sbmds_status sbmds_apply(sbmds_t h, int32_t b, const float* X, float*
 // not tiled by rank: rank 0 streams all of D and the other ranks contribute zero partials.
 namespace {
 
+// out = v_g^T Y1 (b values): block partials + a fixed-order sum
+void vdot(sbmds_ctx* h, int b, int bp, double* out, cudaStream_t st) {
+    h->vdpart.ensure((size_t)kVdotBlocks * 64 * sizeof(double));
+    launch(k_vdot, dim3(kVdotBlocks), dim3(256), 0, st, h->l, b, bp, (const double*)h->vg.as<double>(),
+           (const float*)h->Y1.as<float>(), h->vdpart.as<double>());
+    launch(k_vdot_sum, dim3(1), dim3(64), 0, st, kVdotBlocks, b, (const double*)h->vdpart.as<double>(), out);
+}
+
 int64_t exch_t_offset(int64_t l, int b) { return ((int64_t)4 * l * b + 7) / 8 * 8; }
 
 // One stage on device buffers; the compact exchange layouts are those of sbmds_shard_stage.
@@ -2795,8 +2803,7 @@ void shard_stage_dev(sbmds_ctx* h, int stage, int b, const float* X, const void*
                    st, l, (const float*)h->D, h->ldD, (const double*)h->w.as<double>(), h->vg.as<double>());
             h->vg_ok = true;
         }
-        launch(k_vdot, dim3(1), dim3(256), 0, st, l, b, bp, (const double*)h->vg.as<double>(),
-               (const float*)h->Y1.as<float>(), h->t.as<double>());
+        vdot(h, b, bp, h->t.as<double>(), st);
         if (exch_out) {
             CK(cudaMemcpy2DAsync(exch_out, (size_t)b * 4, h->Y2.p, (size_t)bp * 4, (size_t)b * 4, l,
                                  cudaMemcpyDeviceToDevice, st));
@@ -3201,8 +3208,7 @@ sbmds_status eigs_shard(sbmds_ctx* h, int m, int b, int max_iters, double tol, u
         profiled(h->prof, PK_CSC, st, [&] { spmm_csc(h, b, bp, Yc, st); });   // Y1_g = S_g^T Y_k - w_g s^T
         sum(h->Y1.p, (size_t)h->l * bp, ncclFloat32);
         profiled(h->prof, PK_SPLIT, st, [&] {
-            launch(k_vdot, dim3(1), dim3(256), 0, st, h->l, b, bp, (const double*)h->vg.as<double>(),
-                   (const float*)h->Y1.as<float>(), h->tsave.as<double>());   // v_g^T Y1 (before the fold)
+            vdot(h, b, bp, h->tsave.as<double>(), st);   // v_g^T Y1 (before the fold)
         });
         if (takes_sym(h, bp, true) || h->rank == 0) {
             dstream(h, b, bp, st, Rinv);
