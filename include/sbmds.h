@@ -231,6 +231,9 @@ const char* sbmds_last_error(void);
  *                      costs per launch lose to the fp32 SpMMs on small problems (config 2,
  *                      n = 100,000: 0.125 vs 0.087 ms per apply at b = 32); 0 = always where they
  *                      apply (sbmds_eigs takes them at any size: there they replace several kernels)
+ *     "csr_shfl"       (-1 auto / 0 / 1) fp32 CSR SpMM at b in {4, 8, 16, 32, 64}: a group's (column,
+ *                      value) pairs loaded once and broadcast by shuffles (same sums bit for bit);
+ *                      auto: b <= 16 or a mean row of >= b entries (measured on config 5)
  *     "sp8_pf"         (blocks, default 0) tensor-core step: L2 prefetch distance of the images
  *                      (measured: no gain)
  *     "solver"         eigs: 0 (default) block subspace iteration; 1 restarted block Lanczos with
