@@ -593,3 +593,24 @@ def test_tensor_core_sparse_kernels_ragged_n(n_rows):
             ref = O.apply(S, p.D, X.astype(np.float64))
             assert relerr(Y, ref) <= TOL, (n_rows, b, relerr(Y, ref))
             assert h.stat("sp8_apply_launches") == n0 + 1 and h.stat("sp8_state") == 1
+
+
+@pytest.mark.parametrize("b", [8, 16, 32, 64])
+def test_csr_spmm_shuffled_pairs_bitwise(b):
+    """k_spmm_csr_vec4 with a group's (column, value) pairs loaded once and broadcast by shuffles
+    (option csr_shfl = 1) sums in the same entry order as the plain loop (0): Y is bit-equal, and
+    equals the oracle's to the tolerance. Rows of 1..70 entries: shorter than one chunk, longer
+    than the four chunks in flight at every width; n is not a multiple of the rows per warp."""
+    torch = _torch()
+    p = synth_problem(n=4099, l=301, k=70, seed=11, negative=True, rowsum_one=False)
+    X = configs.x_block(p.n, b, seed=5)
+    Yo = oracle_apply(p, X)
+    with make_handle(p) as h:
+        h.set_option("blocked", 0)
+        h.set_option("sp8_apply", 0)
+        ys = []
+        for shf in (0, 1):
+            h.set_option("csr_shfl", shf)
+            ys.append(run_apply(h, X))
+    assert np.array_equal(ys[0], ys[1])
+    assert relerr(ys[1], Yo) <= TOL
